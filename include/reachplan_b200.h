@@ -1,0 +1,339 @@
+/*
+ * reachplan-b200 C ABI: the drop-in boundary for the gMS reach / path hot path.
+ *
+ * The reference (`reachplan`, /root/reference/proj) exposes this path as plain
+ * C++20 free functions in namespace reachplan with value semantics and
+ * exceptions. This header replaces them with opaque device-resident handles,
+ * plain-old-data parameter structs, caller-owned output buffers and an int
+ * status code. Each entry point cites the reference declaration it replaces.
+ *
+ * Conventions
+ *   - Every function returns rp_status: 0 = OK, k+1 = reference Errc ordinal k
+ *     (inc/reachplan/types.hpp:34-46), RP_E_CUDA / RP_E_INTERNAL otherwise.
+ *     Nothing throws across the ABI. rp_last_error() gives the message,
+ *     prefixed with the reference's errc_name (types.hpp:48-63).
+ *   - Angles are radians, lengths metres, all arithmetic fp64.
+ *   - A context owns one CUDA device + stream; it is not thread-safe, distinct
+ *     contexts are. All device work is on the context stream.
+ *   - There is no CPU fallback: without a CUDA device every compute entry
+ *     point fails with RP_E_CUDA.
+ */
+#ifndef REACHPLAN_B200_H
+#define REACHPLAN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RP_ABI_VERSION 1
+#define RP_MAX_SEGMENTS 4
+#define RP_MAX_RELAX 8
+
+typedef int32_t rp_status;
+enum {
+  RP_OK = 0,
+  RP_E_INVALID_PARAMETER = 1, /* Errc::invalid_parameter */
+  RP_E_CAPACITY_EXCEEDED = 2,
+  RP_E_DEGENERATE_INPUT = 3,
+  RP_E_UNREACHABLE_TARGET = 4,
+  RP_E_EMPTY_CONE = 5,
+  RP_E_NO_SOLUTION = 6,
+  RP_E_NO_PATH = 7,
+  RP_E_INFEASIBLE_TIMING = 8,
+  RP_E_EXECUTION_COLLISION = 9,
+  RP_E_TIMEOUT = 10,
+  RP_E_PARSE_ERROR = 11,
+  RP_E_CUDA = 100,
+  RP_E_INTERNAL = 101
+};
+
+/* ---- plain parameter structs (reference types in brackets) ---------------- */
+
+/* [JointLimit, inc/reachplan/arm_model.hpp:14-21] */
+typedef struct rp_joint_limit {
+  double elev_min, elev_max, azim_min, azim_max;
+} rp_joint_limit;
+
+/* [ArmSpec, inc/reachplan/arm_model.hpp:23-42]; rp_arm_init fills the defaults */
+typedef struct rp_arm {
+  int32_t n_segments; /* 3 (6DOF) or 4 (8DOF) */
+  int32_t n_limits;   /* 0 = unrestricted */
+  int32_t n_offsets;  /* 0 = coaxial */
+  int32_t _pad;
+  double lengths[RP_MAX_SEGMENTS];
+  double root[3];
+  double arm_radius;
+  rp_joint_limit limits[RP_MAX_SEGMENTS];
+  double offsets[RP_MAX_SEGMENTS];
+  double fold_plane_normal[3];
+  double fold_flex;
+  double base_axis[3];
+  double base_ref[3];
+} rp_arm;
+
+enum { RP_MODE_6DOF = 0, RP_MODE_8DOF = 1 };
+
+/* [ReachParams, inc/reachplan/reach_solver.hpp:15-35] negative = derived */
+typedef struct rp_reach_params {
+  double epsilon_gap;
+  double approach_axis[3];
+  double approach_half_angle;
+  double near_target_radius;
+  int32_t n_samples;
+  int32_t mode;
+  int32_t cone_precheck;
+  int32_t disable_geom_pruning;
+  int32_t refine_triangle_8dof;
+  int32_t workers; /* accepted for API parity; the device decides parallelism */
+} rp_reach_params;
+
+/* [PathParams, inc/reachplan/path_planner.hpp:11-22] negative = derived */
+typedef struct rp_path_params {
+  double epsilon_waypoint, d_w, slack, joint1_max_move, joint2_max_move;
+  double relax_schedule[RP_MAX_RELAX];
+  int32_t n_relax;
+  int32_t unfold_steps;
+} rp_path_params;
+
+enum { RP_SHAPE_BOX = 0, RP_SHAPE_CLOUD = 1 };
+
+/* [SceneObstacle, inc/reachplan/voxgrid.hpp:15-23] */
+typedef struct rp_obstacle {
+  int32_t shape;
+  int32_t dynamic;
+  double box_min[3], box_max[3];
+  const double* points; /* cloud: xyz triples, host memory */
+  int64_t n_points;
+  const char* id; /* optional label, used in replan provenance notes */
+} rp_obstacle;
+
+/* [SolveStats, inc/reachplan/reach_solver.hpp:76-93] */
+typedef struct rp_solve_stats {
+  int64_t seg1_candidates, seg1_limit_pass, seg1_reach_pass, seg1_survivors;
+  int64_t pair_candidates, seg2_limit_pass, seg2_clear_pass;
+  int64_t gap_tested, gap_pass, joint_pass, v3_clear_pass;
+  int64_t solutions, shortcuts_found;
+  double wall_ms; /* informational */
+} rp_solve_stats;
+
+/* [PoseChain, inc/reachplan/arm_model.hpp:58-72] waypoints travel separately */
+typedef struct rp_pose {
+  int32_t n_segments;
+  int32_t has_elbows;
+  int32_t quiver_indices[RP_MAX_SEGMENTS]; /* -1 = free / refined */
+  int32_t n_waypoints;
+  int32_t _pad;
+  double s4_length_dev;
+  double segments[RP_MAX_SEGMENTS][3];
+  double joints[RP_MAX_SEGMENTS + 1][3];
+  double elbows[RP_MAX_SEGMENTS][3];
+} rp_pose;
+
+/* [ShortcutPath, inc/reachplan/reach_solver.hpp:60-74] */
+typedef struct rp_shortcut {
+  int32_t segment_index; /* 1 or 2 */
+  int32_t hit_sample_index;
+  int32_t seg1_index, seg2_index;
+  int32_t has_bridge;
+  int32_t via_origin_direct;
+  int32_t n_prefix, n_sublength; /* sample counts of the tip path pieces */
+  double bridge[3];
+  double path_length;
+} rp_shortcut;
+
+enum { RP_CHOSEN_REACH_POSE = 0, RP_CHOSEN_SHORTCUT = 1 };
+
+/* [ChosenPath, inc/reachplan/reach_solver.hpp:155-161] by index into a set */
+typedef struct rp_chosen {
+  int32_t kind;
+  int32_t _pad;
+  int64_t index; /* solution or shortcut index in canonical order */
+  double path_length;
+} rp_chosen;
+
+/* [PathPlan, inc/reachplan/path_planner.hpp:27-41] sizes + provenance scalars */
+typedef struct rp_plan_info {
+  int32_t n_waypoints;
+  int32_t n_poses;
+  int32_t n_unfold;
+  int32_t n_notes;
+  int32_t replan_switch_index;
+  int32_t _pad;
+  char kind[32]; /* reach-pose | shortcut | virtual-arm | out-and-back | replan */
+} rp_plan_info;
+
+/* ---- opaque handles ---------------------------------------------------------- */
+typedef struct rp_ctx rp_ctx;
+typedef struct rp_quiver rp_quiver;
+typedef struct rp_grid rp_grid;
+typedef struct rp_solution_set rp_solution_set;
+typedef struct rp_plan rp_plan;
+
+/* ---- context --------------------------------------------------------------- */
+int32_t rp_abi_version(void);
+const char* rp_last_error(void); /* thread-local message of the last failure */
+rp_status rp_ctx_create(int32_t device, rp_ctx** out);
+rp_status rp_ctx_destroy(rp_ctx* ctx);
+/* Run on a caller stream (cudaStream_t as void*); NULL restores the own stream. */
+rp_status rp_ctx_set_stream(rp_ctx* ctx, void* stream);
+void* rp_ctx_stream(rp_ctx* ctx);
+rp_status rp_ctx_synchronize(rp_ctx* ctx);
+/* Per-kernel device timing (CUDA events on the ctx stream): enable, reset,
+ * then read totals for a kernel family name ("dilate", "seg2", ...). */
+rp_status rp_ctx_enable_timing(rp_ctx* ctx, int32_t enable);
+rp_status rp_ctx_kernel_time(rp_ctx* ctx, const char* name, double* total_ms, int64_t* launches);
+rp_status rp_ctx_reset_timing(rp_ctx* ctx);
+/* Number of this library's kernels launched on ctx since creation. */
+int64_t rp_ctx_launch_count(rp_ctx* ctx);
+
+/* ---- defaults (mirror the reference's member initialisers) ----------------- */
+void rp_arm_init(rp_arm* arm, int32_t n_segments, const double* lengths);
+void rp_reach_params_init(rp_reach_params* rp);
+void rp_path_params_init(rp_path_params* pp);
+/* [ReachParams::nominal_spacing / resolved_epsilon / resolved_near_radius,
+ *  src/reach_solver.cpp:28-43] */
+double rp_nominal_spacing(const rp_arm* arm, const rp_reach_params* rp);
+double rp_resolved_epsilon(const rp_arm* arm, const rp_reach_params* rp);
+double rp_resolved_near_radius(const rp_arm* arm, const rp_reach_params* rp);
+/* [effective_dilation, src/pipeline.cpp:8-15]; configured < 0 = derive */
+double rp_effective_dilation(const rp_arm* arm, const rp_reach_params* rp, double configured);
+
+/* ---- quiver [inc/reachplan/quiver.hpp:38-49] ---------------------------------- */
+/* [generate_quiver, src/quiver.cpp:16-51] */
+rp_status rp_quiver_generate(rp_ctx* ctx, double elev_step, double equator_azim_step,
+                             int32_t min_per_ring, rp_quiver** out);
+/* Upload an existing reference Quiver's vectors (xyz triples). */
+rp_status rp_quiver_upload(rp_ctx* ctx, const double* xyz, int32_t n, rp_quiver** out);
+int32_t rp_quiver_size(const rp_quiver* q);
+rp_status rp_quiver_download(const rp_quiver* q, double* xyz, int32_t cap);
+/* [cone_subset, src/quiver.cpp:53-63] indices ascending; *n_out = count */
+rp_status rp_cone_subset(rp_ctx* ctx, const rp_quiver* q, const double axis[3],
+                         double half_angle, int32_t* idx, int32_t cap, int32_t* n_out);
+rp_status rp_quiver_destroy(rp_quiver* q);
+
+/* ---- voxel grid [inc/reachplan/voxgrid.hpp:60-84] ----------------------------- */
+/* [build_grid, src/voxgrid.cpp:12-33] cell_budget 0 = 2^27 (voxgrid.hpp:57) */
+rp_status rp_grid_build(rp_ctx* ctx, const double bounds_min[3], const double bounds_max[3],
+                        double voxel_size, uint64_t cell_budget, rp_grid** out);
+/* [mark_obstacles, src/voxgrid.cpp:35-62] */
+rp_status rp_grid_mark(rp_grid* g, const rp_obstacle* obs, int32_t n);
+/* [dilate, src/voxgrid.cpp:64-92] */
+rp_status rp_grid_dilate(rp_grid* g, double radius);
+/* Fused mark + dilate of boxes onto an empty or existing grid: exactly
+ * mark_obstacles(boxes) then dilate(radius) when the grid holds no other
+ * occupancy; see DESIGN.md. */
+rp_status rp_grid_mark_dilate_boxes(rp_grid* g, const rp_obstacle* obs, int32_t n, double radius);
+/* [build_scene_grid, src/pipeline.cpp:17-34] dilation < 0 = effective_dilation */
+rp_status rp_build_scene_grid(rp_ctx* ctx, const double bounds_min[3], const double bounds_max[3],
+                              double voxel_size, double dilation, const rp_obstacle* obs,
+                              int32_t n_obs, const rp_arm* arm, const rp_reach_params* rp,
+                              rp_grid** out);
+/* Dynamic-obstacle overlay [src/path_planner.cpp:1011-1021]: aug = base OR
+ * dilate(mark(new_obstacle), base.dilation_radius). aug may be a fresh handle
+ * (*aug == NULL) or an existing same-shape grid that is overwritten. */
+rp_status rp_grid_overlay(const rp_grid* base, const rp_obstacle* obs, rp_grid** aug);
+rp_status rp_grid_info(const rp_grid* g, int32_t dims[3], double origin[3], double* voxel_size,
+                       double* dilation_radius);
+/* Reference layout bytes (x fastest, 1 = obstacle). cap in bytes. */
+rp_status rp_grid_download_u8(rp_grid* g, uint8_t* dst, uint64_t cap);
+/* Device bit words: row-padded, word = (iz*ny + iy)*ceil(nx/64) + ix/64. */
+rp_status rp_grid_download_bits(rp_grid* g, uint64_t* dst, uint64_t cap_words);
+rp_status rp_grid_upload_u8(rp_ctx* ctx, const double origin[3], double voxel_size,
+                            const int32_t dims[3], const uint8_t* occ, double dilation_radius,
+                            rp_grid** out);
+rp_status rp_grid_occupied_count(rp_grid* g, uint64_t* count);
+/* [point_clear, src/voxgrid.cpp:94-98] batched: out[k] = 1 if clear */
+rp_status rp_grid_point_clear(rp_grid* g, const double* xyz, int64_t n, uint8_t* out);
+/* [segment_clear, src/voxgrid.cpp:100-112] batched segments (from,to pairs) */
+rp_status rp_grid_segment_clear(rp_grid* g, const double* from_xyz, const double* to_xyz,
+                                int64_t n, int32_t n_samples, uint8_t* out);
+rp_status rp_grid_copy(const rp_grid* src, rp_grid** out);
+rp_status rp_grid_destroy(rp_grid* g);
+
+/* ---- reach solver [inc/reachplan/reach_solver.hpp] ---------------------------- */
+/* [prune_segment1, src/reach_solver.cpp:224-300] survivors' quiver indices */
+rp_status rp_prune_segment1(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q, const rp_grid* g,
+                            const double* target_points, int32_t n_targets,
+                            const rp_reach_params* rp, int32_t* survivors, int32_t cap,
+                            int32_t* n_out, rp_solve_stats* stats);
+/* [solve_reach, src/reach_solver.cpp:480-546]; the set stays on the device */
+rp_status rp_solve_reach(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q, const rp_grid* g,
+                         const double target[3], const rp_reach_params* rp,
+                         rp_solution_set** out);
+rp_status rp_solution_set_stats(const rp_solution_set* s, rp_solve_stats* stats);
+rp_status rp_solution_set_sizes(const rp_solution_set* s, int64_t* n_solutions,
+                                int64_t* n_shortcuts);
+/* keys[3k..3k+2] = (seg1 index, seg2 index, backward index) canonical order */
+rp_status rp_solution_set_keys(const rp_solution_set* s, int32_t* keys, int64_t cap_solutions);
+/* Materialise solution k (PoseChain incl. waypoints, reach_solver.cpp:434-449). */
+rp_status rp_solution_set_pose(const rp_solution_set* s, int64_t k, rp_pose* pose,
+                               double* waypoints, int32_t cap_waypoints);
+/* Shortcut k; tip waypoints (root excluded) into wps (ShortcutPath::tip_waypoints). */
+rp_status rp_solution_set_shortcut(const rp_solution_set* s, int64_t k, rp_shortcut* sc,
+                                   double* tip_wps, int32_t cap_wps, int32_t* n_wps);
+rp_status rp_solution_set_destroy(rp_solution_set* s);
+/* [select_solution, src/reach_solver.cpp:548-577] */
+rp_status rp_select_solution(const rp_solution_set* s, rp_chosen* out);
+/* [exact_refine_8dof / _6dof / _8dof_triangle, src/arm_model.cpp:258-324] */
+rp_status rp_exact_refine(rp_ctx* ctx, const rp_arm* arm, const rp_pose* approx,
+                          const double target[3], int32_t variant /*0 auto,1 triangle*/,
+                          rp_pose* out);
+
+/* ---- path planner [inc/reachplan/path_planner.hpp] ---------------------------- */
+/* [plan_reach_then_path, src/path_planner.cpp:824-829] */
+rp_status rp_plan_reach_then_path(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q,
+                                  const rp_grid* g, const double target[3],
+                                  const rp_reach_params* rp, const rp_path_params* pp,
+                                  rp_plan** out);
+/* [plan_from_reach, src/path_planner.cpp:729-738] */
+rp_status rp_plan_from_reach(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q, const rp_grid* g,
+                             const rp_solution_set* set, const rp_chosen* chosen,
+                             const double target[3], const rp_reach_params* rp,
+                             const rp_path_params* pp, rp_plan** out);
+/* [plan_arbitrary, src/path_planner.cpp:906-998]; start pose joints/segments */
+rp_status rp_plan_arbitrary(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q, const rp_grid* g,
+                            const rp_pose* start_pose, const double target[3],
+                            const rp_reach_params* rp, const rp_path_params* pp, rp_plan** out);
+/* [replan_dynamic, src/path_planner.cpp:1000-1102] */
+rp_status rp_replan_dynamic(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q,
+                            const rp_grid* grid_static, const rp_plan* active,
+                            int32_t current_index, const rp_obstacle* new_obstacle,
+                            double waypoint_period, double replan_per_waypoint,
+                            const rp_reach_params* rp, const rp_path_params* pp, rp_plan** out);
+/* [waypoint_ik, src/path_planner.cpp:167-291]; trail dirs optional (NULL),
+ * bias optional. *found = 0 when no pose qualifies (std::nullopt). */
+rp_status rp_waypoint_ik(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q, const rp_grid* g,
+                         const double waypoint[3], const rp_pose* prev, const rp_reach_params* rp,
+                         const rp_path_params* pp, double relax, const double* trail_back,
+                         const double* trail_fwd, const rp_pose* junction_bias, int32_t* found,
+                         rp_pose* out, double* waypoints, int32_t cap_waypoints);
+/* [smoothness_ok, src/path_planner.cpp:114-120] with resolved path params */
+rp_status rp_smoothness_ok(const rp_arm* arm, const rp_reach_params* rp, const rp_path_params* pp,
+                           const rp_pose* prev, const rp_pose* cand, double relax, int32_t* ok);
+/* [mean_polyline_deviation, src/path_planner.cpp:76-87] on the device */
+rp_status rp_mean_polyline_deviation(rp_ctx* ctx, const double* pts, int32_t n_pts,
+                                     const double* poly, int32_t n_poly, double* out);
+/* [folded_pose, src/path_planner.cpp:711-727] */
+rp_status rp_folded_pose(rp_ctx* ctx, const rp_arm* arm, rp_pose* out);
+
+rp_status rp_plan_get_info(const rp_plan* p, rp_plan_info* info);
+rp_status rp_plan_waypoints(const rp_plan* p, double* xyz, int32_t cap);
+rp_status rp_plan_relax(const rp_plan* p, double* relax, int32_t cap);
+/* which: 0 = poses (one per waypoint), 1 = unfold prefix */
+rp_status rp_plan_pose(const rp_plan* p, int32_t which, int32_t k, rp_pose* pose,
+                       double* waypoints, int32_t cap_waypoints);
+rp_status rp_plan_note(const rp_plan* p, int32_t k, char* buf, int32_t cap);
+/* Build a plan handle from host data (e.g. a plan file) for rp_replan_dynamic. */
+rp_status rp_plan_create(const char* kind, const double* waypoints, const rp_pose* poses,
+                         const double* relax, int32_t n, const rp_pose* unfold, int32_t n_unfold,
+                         rp_plan** out);
+rp_status rp_plan_destroy(rp_plan* p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* REACHPLAN_B200_H */

@@ -1,0 +1,434 @@
+// Context, errors, parameters, quiver and pose conversions of libreachplan_b200.
+#include "rp_internal.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+namespace rp {
+
+namespace {
+thread_local std::string g_last_error;
+constexpr double kPi = 3.14159265358979323846;
+}  // namespace
+
+const char* errc_name(rp_status code) {
+  static const char* names[] = {"invalid-parameter", "capacity-exceeded", "degenerate-input",
+                                "unreachable-target", "empty-cone", "no-solution", "no-path",
+                                "infeasible-timing", "execution-collision", "timeout",
+                                "parse-error"};
+  if (code >= 1 && code <= 11) return names[code - 1];
+  if (code == RP_E_CUDA) return "cuda-error";
+  return "internal";
+}
+
+void fail(rp_status code, const std::string& msg) {
+  throw Fail{code, std::string(errc_name(code)) + ": " + msg};
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(RP_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void set_last_error(const std::string& s) { g_last_error = s; }
+
+void launch_begin(rp_ctx* ctx, const char* name, cudaEvent_t* ev) {
+  ++ctx->launches;
+  if (!ctx->timing) return;
+  cudaEvent_t e;
+  if (!ctx->event_pool.empty()) {
+    e = ctx->event_pool.back();
+    ctx->event_pool.pop_back();
+  } else {
+    RP_CUDA(cudaEventCreate(&e));
+  }
+  RP_CUDA(cudaEventRecord(e, ctx->stream));
+  *ev = e;
+  (void)name;
+}
+
+void launch_end(rp_ctx* ctx, const char* name, cudaEvent_t ev) {
+  RP_CUDA(cudaGetLastError());
+  if (!ctx->timing || !ev) return;
+  cudaEvent_t e;
+  if (!ctx->event_pool.empty()) {
+    e = ctx->event_pool.back();
+    ctx->event_pool.pop_back();
+  } else {
+    RP_CUDA(cudaEventCreate(&e));
+  }
+  RP_CUDA(cudaEventRecord(e, ctx->stream));
+  ctx->pending.push_back({name, ev, e});
+}
+
+static void drain_timing(rp_ctx* ctx) {
+  if (ctx->pending.empty()) return;
+  RP_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (auto& t : ctx->pending) {
+    float ms = 0.f;
+    RP_CUDA(cudaEventElapsedTime(&ms, t.start, t.stop));
+    auto& acc = ctx->kernel_ms[t.name];
+    acc.first += ms;
+    acc.second += 1;
+    ctx->event_pool.push_back(t.start);
+    ctx->event_pool.push_back(t.stop);
+  }
+  ctx->pending.clear();
+}
+
+void copy_to_host(rp_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  RP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  RP_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void copy_to_device(rp_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  RP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  // The source may be a temporary host buffer: make the copy complete.
+  RP_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+double nominal_spacing(const rp_arm& a, const rp_reach_params& r) {
+  const int segs = (r.mode == RP_MODE_6DOF) ? 3 : a.n_segments;
+  double sum = 0.0;
+  for (int j = 0; j < std::min(segs, 3); ++j) sum += a.lengths[j];
+  return sum / (3.0 * r.n_samples);
+}
+
+double resolved_epsilon(const rp_arm& a, const rp_reach_params& r) {
+  if (r.epsilon_gap >= 0.0) return r.epsilon_gap;
+  return 0.5 * a.lengths[2] / r.n_samples;
+}
+
+double resolved_near_radius(const rp_arm& a, const rp_reach_params& r) {
+  if (r.near_target_radius >= 0.0) return r.near_target_radius;
+  return 0.5 * nominal_spacing(a, r);
+}
+
+static double n3(const double* v) {
+  const double xy = v[0] * v[0] + v[1] * v[1];
+  return std::sqrt(xy + v[2] * v[2]);
+}
+
+void validate_arm(const rp_arm& a) {
+  require(a.n_segments == 3 || a.n_segments == 4, RP_E_INVALID_PARAMETER,
+          "arm must have 3 or 4 segments");
+  for (int k = 0; k < a.n_segments; ++k)
+    require(a.lengths[k] > 0.0, RP_E_INVALID_PARAMETER, "segment lengths must be > 0");
+  require(a.arm_radius >= 0.0, RP_E_INVALID_PARAMETER, "arm_radius must be >= 0");
+  require(a.n_limits >= 0 && a.n_limits <= 4 && a.n_offsets >= 0 && a.n_offsets <= 4,
+          RP_E_INVALID_PARAMETER, "at most 4 joint limits / offsets");
+  for (int k = 0; k < a.n_limits; ++k) {
+    const auto& l = a.limits[k];
+    require(l.elev_min >= -1e-12 && l.elev_max <= kPi + 1e-12 && l.elev_min <= l.elev_max,
+            RP_E_INVALID_PARAMETER, "elevation limits must satisfy 0 <= min <= max <= pi");
+    require(l.azim_min <= l.azim_max, RP_E_INVALID_PARAMETER,
+            "azimuth limits must satisfy min <= max");
+  }
+  for (int k = 0; k < a.n_offsets; ++k)
+    require(a.offsets[k] >= 0.0, RP_E_INVALID_PARAMETER, "joint offsets must be >= 0");
+  require(std::abs(n3(a.base_axis) - 1.0) <= 1e-9, RP_E_INVALID_PARAMETER,
+          "base_axis must be unit");
+  require(std::abs(n3(a.fold_plane_normal) - 1.0) <= 1e-9, RP_E_INVALID_PARAMETER,
+          "fold_plane_normal must be unit");
+  const double d = (a.base_axis[0] * a.base_ref[0] + a.base_axis[1] * a.base_ref[1]) +
+                   a.base_axis[2] * a.base_ref[2];
+  require(std::abs(d) <= 1e-9 && std::abs(n3(a.base_ref) - 1.0) <= 1e-9, RP_E_INVALID_PARAMETER,
+          "base_ref must be unit and orthogonal to base_axis");
+}
+
+void validate_reach(const rp_reach_params& r) {
+  require(r.n_samples >= 1, RP_E_INVALID_PARAMETER, "n_samples must be >= 1");
+  require(r.approach_half_angle >= 0.0 && r.approach_half_angle <= kPi, RP_E_INVALID_PARAMETER,
+          "approach_half_angle must be in [0, pi]");
+  require(std::abs(n3(r.approach_axis) - 1.0) <= 1e-9, RP_E_INVALID_PARAMETER,
+          "approach_axis must be unit");
+  require(r.workers >= 1, RP_E_INVALID_PARAMETER, "workers must be >= 1");
+}
+
+ArmDev make_arm_dev(const rp_arm& a) {
+  ArmDev d{};
+  d.nseg = a.n_segments;
+  for (int k = 0; k < 4; ++k) {
+    d.L[k] = k < a.n_segments ? a.lengths[k] : 0.0;
+    d.off[k] = k < a.n_offsets ? a.offsets[k] : 0.0;
+    if (d.off[k] != 0.0) d.has_offsets = 1;
+    if (k < a.n_limits) {
+      d.lim[k] = {a.limits[k].elev_min, a.limits[k].elev_max, a.limits[k].azim_min,
+                  a.limits[k].azim_max};
+    } else {
+      d.lim[k] = {0.0, kPi, -kPi, kPi};
+    }
+    d.lim_active[k] = rpd::limit_active(d.lim[k]) ? 1 : 0;
+    if (d.lim_active[k]) d.any_limit = 1;
+  }
+  d.root = V3{a.root[0], a.root[1], a.root[2]};
+  d.arm_radius = a.arm_radius;
+  // base_frame (src/arm_model.cpp:94-100): columns ref, axis x ref, axis.
+  const V3 axis{a.base_axis[0], a.base_axis[1], a.base_axis[2]};
+  const V3 ref{a.base_ref[0], a.base_ref[1], a.base_ref[2]};
+  const V3 c1 = rpd::cross(axis, ref);
+  const V3 cols[3] = {ref, c1, axis};
+  for (int c = 0; c < 3; ++c) {
+    d.base.a[0][c] = cols[c].x;
+    d.base.a[1][c] = cols[c].y;
+    d.base.a[2][c] = cols[c].z;
+  }
+  return d;
+}
+
+void to_abi(const HostPose& p, rp_pose* out, double* wps, int cap) {
+  std::memset(out, 0, sizeof(*out));
+  out->n_segments = p.nseg;
+  out->has_elbows = p.has_elbows ? 1 : 0;
+  for (int k = 0; k < 4; ++k) out->quiver_indices[k] = k < p.nseg ? p.qidx[k] : -1;
+  out->s4_length_dev = p.s4dev;
+  for (int k = 0; k < p.nseg; ++k) {
+    out->segments[k][0] = p.seg[k].x;
+    out->segments[k][1] = p.seg[k].y;
+    out->segments[k][2] = p.seg[k].z;
+    if (p.has_elbows) {
+      out->elbows[k][0] = p.elbows[k].x;
+      out->elbows[k][1] = p.elbows[k].y;
+      out->elbows[k][2] = p.elbows[k].z;
+    }
+  }
+  for (int k = 0; k <= p.nseg; ++k) {
+    out->joints[k][0] = p.joints[k].x;
+    out->joints[k][1] = p.joints[k].y;
+    out->joints[k][2] = p.joints[k].z;
+  }
+  out->n_waypoints = static_cast<int>(p.waypoints.size());
+  if (wps)
+    for (int k = 0; k < out->n_waypoints && k < cap; ++k) {
+      wps[3 * k] = p.waypoints[k].x;
+      wps[3 * k + 1] = p.waypoints[k].y;
+      wps[3 * k + 2] = p.waypoints[k].z;
+    }
+}
+
+HostPose from_abi(const rp_pose& p, const double* wps) {
+  HostPose h;
+  h.nseg = p.n_segments;
+  h.has_elbows = p.has_elbows != 0;
+  for (int k = 0; k < p.n_segments; ++k) {
+    h.seg[k] = V3{p.segments[k][0], p.segments[k][1], p.segments[k][2]};
+    h.elbows[k] = V3{p.elbows[k][0], p.elbows[k][1], p.elbows[k][2]};
+    h.qidx[k] = p.quiver_indices[k];
+  }
+  for (int k = 0; k <= p.n_segments; ++k)
+    h.joints[k] = V3{p.joints[k][0], p.joints[k][1], p.joints[k][2]};
+  h.s4dev = p.s4_length_dev;
+  if (wps)
+    for (int k = 0; k < p.n_waypoints; ++k)
+      h.waypoints.push_back(V3{wps[3 * k], wps[3 * k + 1], wps[3 * k + 2]});
+  return h;
+}
+
+}  // namespace rp
+
+using namespace rp;
+
+extern "C" {
+
+int32_t rp_abi_version(void) { return RP_ABI_VERSION; }
+const char* rp_last_error(void) { return g_last_error.c_str(); }
+
+rp_status rp_ctx_create(int32_t device, rp_ctx** out) {
+  return guarded([&] {
+    require(out != nullptr, RP_E_INVALID_PARAMETER, "null output");
+    int count = 0;
+    RP_CUDA(cudaGetDeviceCount(&count));
+    require(count > 0, RP_E_CUDA, "no CUDA device (the library has no CPU fallback)");
+    require(device >= 0 && device < count, RP_E_INVALID_PARAMETER, "device index out of range");
+    RP_CUDA(cudaSetDevice(device));
+    auto* c = new rp_ctx();
+    c->device = device;
+    RP_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+    c->stream = c->own;
+    cudaDeviceProp prop;
+    RP_CUDA(cudaGetDeviceProperties(&prop, device));
+    c->sm_count = prop.multiProcessorCount;
+    *out = c;
+  });
+}
+
+rp_status rp_ctx_destroy(rp_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& t : ctx->pending) {
+      cudaEventDestroy(t.start);
+      cudaEventDestroy(t.stop);
+    }
+    for (auto e : ctx->event_pool) cudaEventDestroy(e);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->own) cudaStreamDestroy(ctx->own);
+    delete ctx;
+  });
+}
+
+rp_status rp_ctx_set_stream(rp_ctx* ctx, void* stream) {
+  return guarded([&] {
+    require(ctx != nullptr, RP_E_INVALID_PARAMETER, "null ctx");
+    drain_timing(ctx);
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+  });
+}
+
+void* rp_ctx_stream(rp_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+
+rp_status rp_ctx_synchronize(rp_ctx* ctx) {
+  return guarded([&] { RP_CUDA(cudaStreamSynchronize(ctx->stream)); });
+}
+
+rp_status rp_ctx_enable_timing(rp_ctx* ctx, int32_t enable) {
+  return guarded([&] {
+    drain_timing(ctx);
+    ctx->timing = enable != 0;
+  });
+}
+
+rp_status rp_ctx_kernel_time(rp_ctx* ctx, const char* name, double* total_ms, int64_t* launches) {
+  return guarded([&] {
+    drain_timing(ctx);
+    auto it = ctx->kernel_ms.find(name);
+    *total_ms = it == ctx->kernel_ms.end() ? 0.0 : it->second.first;
+    *launches = it == ctx->kernel_ms.end() ? 0 : it->second.second;
+  });
+}
+
+rp_status rp_ctx_reset_timing(rp_ctx* ctx) {
+  return guarded([&] {
+    drain_timing(ctx);
+    ctx->kernel_ms.clear();
+  });
+}
+
+int64_t rp_ctx_launch_count(rp_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+void rp_arm_init(rp_arm* a, int32_t n_segments, const double* lengths) {
+  std::memset(a, 0, sizeof(*a));
+  a->n_segments = n_segments;
+  for (int k = 0; k < n_segments && k < 4; ++k) a->lengths[k] = lengths ? lengths[k] : 0.0;
+  a->fold_plane_normal[1] = 1.0;
+  a->fold_flex = 170.0 * (kPi / 180.0);
+  a->base_axis[2] = 1.0;
+  a->base_ref[0] = 1.0;
+}
+
+void rp_reach_params_init(rp_reach_params* r) {
+  std::memset(r, 0, sizeof(*r));
+  r->epsilon_gap = -1.0;
+  r->n_samples = 8;
+  r->approach_axis[0] = 1.0;
+  r->near_target_radius = -1.0;
+  r->mode = RP_MODE_8DOF;
+  r->workers = 1;
+}
+
+void rp_path_params_init(rp_path_params* p) {
+  std::memset(p, 0, sizeof(*p));
+  p->epsilon_waypoint = p->d_w = p->slack = p->joint1_max_move = p->joint2_max_move = -1.0;
+  p->n_relax = 3;
+  p->relax_schedule[0] = 1.5;
+  p->relax_schedule[1] = 2.0;
+  p->relax_schedule[2] = 3.0;
+  p->unfold_steps = 16;
+}
+
+double rp_nominal_spacing(const rp_arm* a, const rp_reach_params* r) {
+  return nominal_spacing(*a, *r);
+}
+double rp_resolved_epsilon(const rp_arm* a, const rp_reach_params* r) {
+  return resolved_epsilon(*a, *r);
+}
+double rp_resolved_near_radius(const rp_arm* a, const rp_reach_params* r) {
+  return resolved_near_radius(*a, *r);
+}
+double rp_effective_dilation(const rp_arm* a, const rp_reach_params* r, double configured) {
+  if (configured >= 0.0) return configured;
+  double m = 0.0;
+  for (int j = 0; j < a->n_segments; ++j) m = std::max(m, a->lengths[j] / r->n_samples);
+  return a->arm_radius + 1.25 * m;
+}
+
+// ---- quiver (src/quiver.cpp:16-51): generated with the reference formula on
+// the host (glibc cos/sin, so the vectors are bit-identical), then uploaded
+// once as structure-of-arrays for coalesced device reads.
+static rp_quiver* upload_quiver(rp_ctx* ctx, const std::vector<double>& xyz) {
+  auto* q = new rp_quiver();
+  q->ctx = ctx;
+  q->n = static_cast<int>(xyz.size() / 3);
+  q->host_xyz = xyz;
+  std::vector<double> soa(3 * static_cast<size_t>(q->n));
+  for (int k = 0; k < q->n; ++k) {
+    soa[k] = xyz[3 * k];
+    soa[q->n + k] = xyz[3 * k + 1];
+    soa[2 * q->n + k] = xyz[3 * k + 2];
+  }
+  RP_CUDA(cudaMalloc(&q->d_soa, soa.size() * sizeof(double) + 8));
+  copy_to_device(ctx, q->d_soa, soa.data(), soa.size() * sizeof(double));
+  return q;
+}
+
+rp_status rp_quiver_generate(rp_ctx* ctx, double elev_step, double azim_step,
+                             int32_t min_per_ring, rp_quiver** out) {
+  return guarded([&] {
+    require(elev_step > 0.0 && elev_step <= kPi / 2.0, RP_E_INVALID_PARAMETER,
+            "elev_step must be in (0, pi/2]");
+    require(azim_step > 0.0 && azim_step <= kPi / 2.0, RP_E_INVALID_PARAMETER,
+            "equator_azim_step must be in (0, pi/2]");
+    require(min_per_ring >= 1, RP_E_INVALID_PARAMETER, "min_per_ring must be >= 1");
+    std::vector<double> rings;
+    for (int k = 0;; ++k) {
+      const double phi = -kPi / 2.0 + k * elev_step;
+      if (phi >= kPi / 2.0 - 1e-12) {
+        rings.push_back(kPi / 2.0);
+        break;
+      }
+      rings.push_back(phi);
+    }
+    const long n_eq = std::llround(2.0 * kPi / azim_step);
+    std::vector<double> xyz;
+    for (double phi : rings) {
+      const long by_circ = std::llround(static_cast<double>(n_eq) * std::cos(phi));
+      const int count = static_cast<int>(std::max<long>(min_per_ring, by_circ));
+      const double cp = std::cos(phi), sp = std::sin(phi);
+      for (int m = 0; m < count; ++m) {
+        const double theta = 2.0 * kPi * m / count;
+        xyz.push_back(cp * std::cos(theta));
+        xyz.push_back(cp * std::sin(theta));
+        xyz.push_back(sp);
+      }
+    }
+    *out = upload_quiver(ctx, xyz);
+  });
+}
+
+rp_status rp_quiver_upload(rp_ctx* ctx, const double* xyz, int32_t n, rp_quiver** out) {
+  return guarded([&] {
+    require(n > 0 && xyz != nullptr, RP_E_INVALID_PARAMETER, "empty quiver");
+    *out = upload_quiver(ctx, std::vector<double>(xyz, xyz + 3 * static_cast<size_t>(n)));
+  });
+}
+
+int32_t rp_quiver_size(const rp_quiver* q) { return q ? q->n : 0; }
+
+rp_status rp_quiver_download(const rp_quiver* q, double* xyz, int32_t cap) {
+  return guarded([&] {
+    require(cap >= q->n, RP_E_INVALID_PARAMETER, "buffer too small");
+    std::memcpy(xyz, q->host_xyz.data(), q->host_xyz.size() * sizeof(double));
+  });
+}
+
+rp_status rp_quiver_destroy(rp_quiver* q) {
+  return guarded([&] {
+    if (!q) return;
+    if (q->d_soa) cudaFree(q->d_soa);
+    delete q;
+  });
+}
+
+}  // extern "C"

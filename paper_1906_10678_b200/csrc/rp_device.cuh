@@ -1,0 +1,281 @@
+// Device geometry for the gMS hot path (sm_100a).
+//
+// Every decision the reference takes is a threshold on an fp64 expression, so
+// these helpers reproduce the reference's IEEE operation sequence exactly:
+// the library is compiled with -fmad=false (no FMA contraction, like x86-64
+// g++ without -march), double '/' and sqrt are IEEE round-to-nearest, and
+// vector reductions follow Eigen's fixed-size-3 order (x*x' + y*y') + z*z'.
+// Transcendentals (atan2/hypot/sin/cos) only appear with joint limits,
+// offsets or in the unfold interpolation; those results are tolerance-class
+// (CUDA libm vs glibc may differ in the last ulp), see DESIGN.md.
+#pragma once
+
+#include <cstdint>
+
+namespace rpd {
+
+struct V3 {
+  double x, y, z;
+};
+
+__host__ __device__ __forceinline__ V3 mk(double x, double y, double z) { return V3{x, y, z}; }
+__host__ __device__ __forceinline__ V3 operator+(V3 a, V3 b) { return V3{a.x + b.x, a.y + b.y, a.z + b.z}; }
+__host__ __device__ __forceinline__ V3 operator-(V3 a, V3 b) { return V3{a.x - b.x, a.y - b.y, a.z - b.z}; }
+__host__ __device__ __forceinline__ V3 operator-(V3 a) { return V3{-a.x, -a.y, -a.z}; }
+/// scalar * vector (Eigen: s * v)
+__host__ __device__ __forceinline__ V3 operator*(double s, V3 v) { return V3{s * v.x, s * v.y, s * v.z}; }
+/// vector * scalar (Eigen: v * s); IEEE multiply commutes, kept for readability
+__host__ __device__ __forceinline__ V3 operator*(V3 v, double s) { return V3{v.x * s, v.y * s, v.z * s}; }
+__host__ __device__ __forceinline__ V3 operator/(V3 v, double s) { return V3{v.x / s, v.y / s, v.z / s}; }
+
+/// Eigen fixed-size-3 dot: one 2-wide packet then the tail.
+__host__ __device__ __forceinline__ double dot(V3 a, V3 b) {
+  const double xy = a.x * b.x + a.y * b.y;
+  return xy + a.z * b.z;
+}
+__host__ __device__ __forceinline__ double sqnorm(V3 a) { return dot(a, a); }
+__host__ __device__ __forceinline__ double norm(V3 a) { return sqrt(sqnorm(a)); }
+__host__ __device__ __forceinline__ V3 normalized(V3 a) {
+  const double n2 = sqnorm(a);
+  if (n2 > 0.0) {
+    const double n = sqrt(n2);
+    return V3{a.x / n, a.y / n, a.z / n};
+  }
+  return a;
+}
+__host__ __device__ __forceinline__ V3 cross(V3 a, V3 b) {
+  return V3{a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+/// std::clamp(v, lo, hi)
+__host__ __device__ __forceinline__ double clampd(double v, double lo, double hi) {
+  return (v < lo) ? lo : (hi < v) ? hi : v;
+}
+
+// ---------------------------------------------------------------------------
+// Bit-packed occupancy grid. Rows of x are padded to whole 64-bit words:
+// word(ix, iy, iz) = (iz*ny + iy)*wx + ix/64, bit ix%64. 1 = obstacle.
+struct GridView {
+  const uint64_t* bits;
+  int nx, ny, nz, wx;
+  double ox, oy, oz;
+  double vs;   // voxel_size
+  double rvs;  // fl(1/voxel_size), for the exact-floor fast path
+};
+
+/// floor(a / vs) exactly as the reference (inc/voxgrid.hpp:46-50): the
+/// correctly rounded quotient is bracketed by a*fl(1/vs) +- 4u|q|; if no
+/// integer lies in the bracket the floor is decided without dividing,
+/// otherwise the IEEE division is done. Bit-exact by construction.
+__device__ __forceinline__ int vox_floor(double a, double vs, double rvs) {
+  const double q = a * rvs;
+  const double d = fabs(q) * 8.9e-16 + 1e-300;
+  const double lo = floor(q - d);
+  const double hi = floor(q + d);
+  if (lo == hi) return static_cast<int>(lo);
+  return static_cast<int>(floor(a / vs));
+}
+
+/// point_clear (src/voxgrid.cpp:94-98): outside the grid = free.
+__device__ __forceinline__ bool point_clear(const GridView& g, V3 p) {
+  const int ix = vox_floor(p.x - g.ox, g.vs, g.rvs);
+  const int iy = vox_floor(p.y - g.oy, g.vs, g.rvs);
+  const int iz = vox_floor(p.z - g.oz, g.vs, g.rvs);
+  if (ix < 0 || iy < 0 || iz < 0 || ix >= g.nx || iy >= g.ny || iz >= g.nz) return true;
+  const uint64_t w =
+      __ldg(g.bits + ((static_cast<size_t>(iz) * g.ny + iy) * g.wx + (ix >> 6)));
+  return ((w >> (ix & 63)) & 1ull) == 0ull;
+}
+
+/// Sample k of a segment walk: from + (double(k)/n) * (to - from)
+/// (src/voxgrid.cpp:105-107, src/reach_solver.cpp:114-116).
+__host__ __device__ __forceinline__ V3 walk_sample(V3 from, V3 diff, int k, int n) {
+  const double t = static_cast<double>(k) / static_cast<double>(n);
+  return from + t * diff;
+}
+
+/// All n samples clear (segment_clear verdict; walk_points).
+__device__ __forceinline__ bool walk_clear(const GridView& g, V3 from, V3 to, int n) {
+  const V3 diff = to - from;
+  for (int k = 1; k <= n; ++k)
+    if (!point_clear(g, walk_sample(from, diff, k, n))) return false;
+  return true;
+}
+
+/// walk_segment_into with early exit (src/reach_solver.cpp:109-126):
+/// returns the 1-based first blocked sample, 0 when fully clear.
+__device__ __forceinline__ int walk_first_blocked(const GridView& g, V3 from, V3 to, int n) {
+  const V3 diff = to - from;
+  for (int k = 1; k <= n; ++k)
+    if (!point_clear(g, walk_sample(from, diff, k, n))) return k;
+  return 0;
+}
+
+/// scaled_sample_count (src/reach_solver.cpp:143-145)
+__host__ __device__ __forceinline__ int scaled_sample_count(double len, double spacing) {
+  const double s = spacing > 1e-12 ? spacing : 1e-12;
+  const int c = static_cast<int>(ceil(len / s));
+  return c > 1 ? c : 1;
+}
+
+/// point_to_segment (src/reach_solver.cpp:135-141; path_planner.cpp:12-18)
+__host__ __device__ __forceinline__ double point_to_segment(V3 p, V3 a, V3 b) {
+  const V3 ab = b - a;
+  const double len2 = sqnorm(ab);
+  if (len2 <= 1e-30) return norm(p - a);
+  const double t = clampd(dot(p - a, ab) / len2, 0.0, 1.0);
+  return norm(p - (a + t * ab));
+}
+
+/// segment_segment_distance (src/arm_model.cpp:326-361)
+__host__ __device__ __forceinline__ double seg_seg_distance(V3 a0, V3 a1, V3 b0, V3 b1) {
+  const V3 d1 = a1 - a0;
+  const V3 d2 = b1 - b0;
+  const V3 r = a0 - b0;
+  const double a = sqnorm(d1);
+  const double e = sqnorm(d2);
+  const double f = dot(d2, r);
+  double s = 0.0, t = 0.0;
+  if (a <= 1e-30 && e <= 1e-30) return norm(r);
+  if (a <= 1e-30) {
+    t = clampd(f / e, 0.0, 1.0);
+  } else {
+    const double c = dot(d1, r);
+    if (e <= 1e-30) {
+      s = clampd(-c / a, 0.0, 1.0);
+    } else {
+      const double b = dot(d1, d2);
+      const double denom = a * e - b * b;
+      if (denom > 1e-30) s = clampd((b * f - c * e) / denom, 0.0, 1.0);
+      t = (b * s + f) / e;
+      if (t < 0.0) {
+        t = 0.0;
+        s = clampd(-c / a, 0.0, 1.0);
+      } else if (t > 1.0) {
+        t = 1.0;
+        s = clampd((b - c) / a, 0.0, 1.0);
+      }
+    }
+  }
+  return norm((a0 + s * d1) - (b0 + t * d2));
+}
+
+/// self_collision_free over a coaxial chain (src/arm_model.cpp:376-388):
+/// links k = [joints[k], joints[k+1]], non-adjacent pairs >= 2*radius.
+__host__ __device__ __forceinline__ bool self_collision_free(const V3* joints, int n_links,
+                                                             double min_sep) {
+  for (int i = 0; i + 2 < n_links; ++i)
+    for (int j = i + 2; j < n_links; ++j)
+      if (seg_seg_distance(joints[i], joints[i + 1], joints[j], joints[j + 1]) < min_sep)
+        return false;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// Frames and joint limits (src/arm_model.cpp:12-70, 195-200). Only used when
+// limits or offsets are active.
+struct M3 {
+  double a[3][3];
+};
+
+__host__ __device__ __forceinline__ M3 m_identity() {
+  M3 m{};
+  m.a[0][0] = m.a[1][1] = m.a[2][2] = 1.0;
+  return m;
+}
+__host__ __device__ __forceinline__ M3 m_mul(const M3& A, const M3& B) {
+  M3 m;
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      double s = A.a[r][0] * B.a[0][c];
+      s = s + A.a[r][1] * B.a[1][c];
+      s = s + A.a[r][2] * B.a[2][c];
+      m.a[r][c] = s;
+    }
+  return m;
+}
+__host__ __device__ __forceinline__ V3 m_tmul(const M3& A, V3 v) {  // A^T v
+  const double in[3] = {v.x, v.y, v.z};
+  double out[3];
+  for (int r = 0; r < 3; ++r) {
+    double s = A.a[0][r] * in[0];
+    s = s + A.a[1][r] * in[1];
+    s = s + A.a[2][r] * in[2];
+    out[r] = s;
+  }
+  return V3{out[0], out[1], out[2]};
+}
+__host__ __device__ __forceinline__ V3 m_col(const M3& A, int c) {
+  return V3{A.a[0][c], A.a[1][c], A.a[2][c]};
+}
+__host__ __device__ __forceinline__ M3 rot_z(double t) {
+  const double c = cos(t), s = sin(t);
+  M3 m{};
+  m.a[0][0] = c; m.a[0][1] = -s; m.a[0][2] = 0;
+  m.a[1][0] = s; m.a[1][1] = c;  m.a[1][2] = 0;
+  m.a[2][0] = 0; m.a[2][1] = 0;  m.a[2][2] = 1;
+  return m;
+}
+__host__ __device__ __forceinline__ M3 rot_y(double t) {
+  const double c = cos(t), s = sin(t);
+  M3 m{};
+  m.a[0][0] = c;  m.a[0][1] = 0; m.a[0][2] = s;
+  m.a[1][0] = 0;  m.a[1][1] = 1; m.a[1][2] = 0;
+  m.a[2][0] = -s; m.a[2][1] = 0; m.a[2][2] = c;
+  return m;
+}
+
+struct FrameStep {
+  double theta, phi;
+  bool degenerate;
+  M3 after_azimuth, frame;
+};
+
+/// advance_frame (src/arm_model.cpp:34-59)
+__host__ __device__ __forceinline__ FrameStep advance_frame(const M3& parent, V3 dir) {
+  const V3 local = m_tmul(parent, dir);
+  FrameStep st;
+  const double planar = hypot(local.x, local.y);
+  st.phi = atan2(planar, local.z);
+  if (planar < 1e-12) {
+    st.degenerate = true;
+    st.theta = 0.0;
+  } else {
+    st.degenerate = false;
+    st.theta = atan2(local.y, local.x);
+  }
+  st.after_azimuth = m_mul(parent, rot_z(st.theta));
+  st.frame = m_mul(st.after_azimuth, rot_y(st.phi));
+  return st;
+}
+
+struct Limit {
+  double elev_min, elev_max, azim_min, azim_max;
+};
+
+__host__ __device__ __forceinline__ bool full_azimuth(const Limit& l) {
+  return l.azim_min <= -3.14159265358979323846 && l.azim_max >= 3.14159265358979323846;
+}
+__host__ __device__ __forceinline__ bool limit_active(const Limit& l) {
+  return l.elev_min > 1e-12 || l.elev_max < 3.14159265358979323846 - 1e-12 || !full_azimuth(l);
+}
+__host__ __device__ __forceinline__ double wrap_angle(double a) {
+  const double kPi = 3.14159265358979323846;
+  a = fmod(a, 2.0 * kPi);
+  if (a <= -kPi) a += 2.0 * kPi;
+  if (a > kPi) a -= 2.0 * kPi;
+  return a;
+}
+/// joint_angle_within (src/arm_model.cpp:63-70, 195-200)
+__host__ __device__ __forceinline__ bool joint_angle_within(double theta, double phi, bool degenerate,
+                                                            const Limit& l) {
+  const double kPi = 3.14159265358979323846;
+  if (phi < l.elev_min - 1e-12 || phi > l.elev_max + 1e-12) return false;
+  if (degenerate || full_azimuth(l)) return true;
+  const double w = wrap_angle(theta);
+  const double c[3] = {w, w - 2.0 * kPi, w + 2.0 * kPi};
+  for (int k = 0; k < 3; ++k)
+    if (c[k] >= l.azim_min - 1e-12 && c[k] <= l.azim_max + 1e-12) return true;
+  return false;
+}
+
+}  // namespace rpd

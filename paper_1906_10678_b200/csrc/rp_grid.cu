@@ -1,0 +1,674 @@
+// Bit-packed voxel grid on the device: voxelizer, obstacle dilation, overlay,
+// point / segment clearance queries.
+//
+// Layout: one bit per cell, rows of x padded to whole 64-bit words,
+// word(ix,iy,iz) = (iz*ny + iy)*wx + ix/64. 512^3 is 16 MiB instead of the
+// reference's 128 MiB of bytes (inc/reachplan/voxgrid.hpp:32), so every grid
+// the configurations use stays L2-resident during the search kernels.
+//
+// Dilation semantics (src/voxgrid.cpp:64-92): r_c = radius/vs,
+// reach = floor(r_c + 1e-9), ball = {d in Z^3 : |d_i| <= reach,
+// dx^2+dy^2+dz^2 <= r_c^2 + 1e-9}, applied from the pre-dilation snapshot.
+// For a row offset (dy, dz) the admissible x half-width is the table
+// wtab[dy^2+dz^2] = max{dx <= reach : dx^2 + s <= r2} (-1 if none), built on
+// the host with the reference's own double comparison (all terms are exact
+// integers), so every kernel below decides membership identically.
+#include "rp_internal.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+namespace rp {
+namespace {
+
+using rpd::GridView;
+using rpd::V3;
+
+/// Integer index box of one marked primitive (inclusive), empty if a > b.
+struct Prim {
+  int a[3], b[3];
+};
+
+struct DilTable {
+  int reach = 0;
+  std::vector<int> w;  // indexed by dy^2 + dz^2
+};
+
+DilTable make_table(double radius, double vs) {
+  DilTable t;
+  const double r_cells = radius / vs;
+  t.reach = static_cast<int>(std::floor(r_cells + 1e-9));
+  const double r2 = r_cells * r_cells + 1e-9;
+  const int smax = 2 * t.reach * t.reach;
+  t.w.assign(smax + 1, -1);
+  for (int s = 0; s <= smax; ++s)
+    for (int dx = 0; dx <= t.reach; ++dx)
+      if (double(dx) * dx + double(s) <= r2) t.w[s] = dx;
+  return t;
+}
+
+/// Box -> clipped index ranges, exactly the loop bounds and the cell-centre
+/// test of mark_obstacles (src/voxgrid.cpp:41-52). Thread per (box, axis).
+__global__ void k_box_ranges(const double* __restrict__ boxes, int n, GridView g,
+                             Prim* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 3 * n) return;
+  const int k = t / 3, ax = t % 3;
+  const double mn = boxes[6 * k + ax], mx = boxes[6 * k + 3 + ax];
+  const double o = ax == 0 ? g.ox : (ax == 1 ? g.oy : g.oz);
+  const int nd = ax == 0 ? g.nx : (ax == 1 ? g.ny : g.nz);
+  const int lo = rpd::vox_floor(mn - o, g.vs, g.rvs);
+  const int hi = rpd::vox_floor(mx - o, g.vs, g.rvs);
+  int a = lo > 0 ? lo : 0;
+  int b = hi < nd - 1 ? hi : nd - 1;
+  // cell_center(i)_ax = origin_ax + vs * (i + 0.5); monotone in i, so the
+  // cells whose centre is inside [mn, mx] form one contiguous run.
+  while (a <= b && !(o + g.vs * (a + 0.5) >= mn && o + g.vs * (a + 0.5) <= mx)) ++a;
+  while (b >= a && !(o + g.vs * (b + 0.5) >= mn && o + g.vs * (b + 0.5) <= mx)) --b;
+  out[k].a[ax] = a;
+  out[k].b[ax] = b;
+}
+
+/// Cloud point -> its floor-index cell if inside the grid (voxgrid.cpp:54-59).
+__global__ void k_cloud_cells(const double* __restrict__ pts, int64_t n, GridView g,
+                              Prim* __restrict__ out) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int ix = rpd::vox_floor(pts[3 * k] - g.ox, g.vs, g.rvs);
+  const int iy = rpd::vox_floor(pts[3 * k + 1] - g.oy, g.vs, g.rvs);
+  const int iz = rpd::vox_floor(pts[3 * k + 2] - g.oz, g.vs, g.rvs);
+  Prim p;
+  const bool in = ix >= 0 && iy >= 0 && iz >= 0 && ix < g.nx && iy < g.ny && iz < g.nz;
+  p.a[0] = ix; p.a[1] = iy; p.a[2] = iz;
+  p.b[0] = in ? ix : ix - 1; p.b[1] = iy; p.b[2] = iz;
+  out[k] = p;
+}
+
+__device__ __forceinline__ uint64_t range_mask(int lo, int hi, int base) {
+  // bits [lo, hi] of the word whose first cell is `base`
+  const int l = lo - base, h = hi - base;
+  if (h < 0 || l > 63) return 0ull;
+  const int l2 = l < 0 ? 0 : l, h2 = h > 63 ? 63 : h;
+  const uint64_t upto = (h2 == 63) ? ~0ull : ((1ull << (h2 + 1)) - 1ull);
+  return upto & ~((1ull << l2) - 1ull);
+}
+
+/// Fused rasterise + dilate of index boxes, one thread per output word, rows
+/// restricted to [y0,y1] x [z0,z1]. For a row at distance (dy, dz) from a
+/// box the dilated box covers x in [a_x - w, b_x + w], w = wtab[dy^2+dz^2]:
+/// the union over boxes of these intervals is exactly dilate(mark(boxes)).
+/// Write-only on HBM (N^3/8 bytes) unless accumulating into existing bits.
+__global__ void __launch_bounds__(256) k_mark_dilate_rows(uint64_t* __restrict__ bits, GridView g,
+                                                          const Prim* __restrict__ prims, int np,
+                                                          const int* __restrict__ wtab, int reach,
+                                                          int y0, int ny_rows, int z0,
+                                                          int accumulate) {
+  extern __shared__ Prim sp[];
+  for (int k = threadIdx.x; k < np; k += blockDim.x) sp[k] = prims[k];
+  __syncthreads();
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t per_plane = static_cast<int64_t>(ny_rows) * g.wx;
+  const int z = z0 + static_cast<int>(t / per_plane);
+  const int rem = static_cast<int>(t % per_plane);
+  const int y = y0 + rem / g.wx;
+  const int ww = rem % g.wx;
+  if (z >= g.nz || y >= g.ny || z < 0 || y < 0) return;
+  const int base = ww * 64;
+  uint64_t m = 0;
+  for (int k = 0; k < np; ++k) {
+    const Prim p = sp[k];
+    if (p.a[0] > p.b[0] || p.a[1] > p.b[1] || p.a[2] > p.b[2]) continue;
+    const int dy = y < p.a[1] ? p.a[1] - y : (y > p.b[1] ? y - p.b[1] : 0);
+    const int dz = z < p.a[2] ? p.a[2] - z : (z > p.b[2] ? z - p.b[2] : 0);
+    if (dy > reach || dz > reach) continue;
+    const int w = __ldg(wtab + dy * dy + dz * dz);
+    if (w < 0) continue;
+    int lo = p.a[0] - w, hi = p.b[0] + w;
+    lo = lo < 0 ? 0 : lo;
+    hi = hi > g.nx - 1 ? g.nx - 1 : hi;
+    m |= range_mask(lo, hi, base);
+  }
+  const size_t idx = (static_cast<size_t>(z) * g.ny + y) * g.wx + ww;
+  bits[idx] = accumulate ? (bits[idx] | m) : m;
+}
+
+/// Scatter-mark single cells (cloud points) with atomicOr.
+__global__ void k_mark_cells(uint64_t* bits, GridView g, const Prim* __restrict__ prims,
+                             int64_t n) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const Prim p = prims[k];
+  if (p.a[0] > p.b[0]) return;
+  const size_t idx = (static_cast<size_t>(p.a[2]) * g.ny + p.a[1]) * g.wx + (p.a[0] >> 6);
+  atomicOr(reinterpret_cast<unsigned long long*>(bits + idx), 1ull << (p.a[0] & 63));
+}
+
+/// x-dilation of the word `ww` of a row by half-width w (< 64): OR over
+/// d in [-w, w] of the row shifted by d, neighbours supplying the carries.
+__device__ __forceinline__ uint64_t xdilate_small(uint64_t prev, uint64_t cur, uint64_t next, int w) {
+  if (w == 0) return cur;
+  // left smear over the 128-bit (cur:prev): bit x set if any of x-w..x set
+  uint64_t hi = cur, lo = prev;
+  int p = 1;
+  while (2 * p <= w + 1) {
+    hi |= (hi << p) | (lo >> (64 - p));
+    lo |= lo << p;
+    p *= 2;
+  }
+  if (p < w + 1) {
+    const int s = w + 1 - p;
+    hi |= (hi << s) | (lo >> (64 - s));
+  }
+  const uint64_t left = hi;
+  // right smear over the 128-bit (next:cur)
+  uint64_t h2 = next, l2 = cur;
+  p = 1;
+  while (2 * p <= w + 1) {
+    l2 |= (l2 >> p) | (h2 << (64 - p));
+    h2 |= h2 >> p;
+    p *= 2;
+  }
+  if (p < w + 1) {
+    const int s = w + 1 - p;
+    l2 |= (l2 >> s) | (h2 << (64 - s));
+  }
+  return left | l2;
+}
+
+/// Generic x-dilation for any half-width: interval OR from each set bit of
+/// the words that can reach word ww (rare: dilation above 63 voxels).
+__device__ uint64_t xdilate_any(const uint64_t* __restrict__ row, int wx, int nx, int ww, int w) {
+  const int span = (w + 63) / 64;
+  const int base = ww * 64;
+  uint64_t m = 0;
+  for (int v = ww - span; v <= ww + span; ++v) {
+    if (v < 0 || v >= wx) continue;
+    uint64_t bitsv = __ldg(row + v);
+    while (bitsv) {
+      const int b = __ffsll(static_cast<long long>(bitsv)) - 1;
+      bitsv &= bitsv - 1;
+      const int x = v * 64 + b;
+      int lo = x - w, hi = x + w;
+      lo = lo < 0 ? 0 : lo;
+      hi = hi > nx - 1 ? nx - 1 : hi;
+      m |= range_mask(lo, hi, base);
+    }
+  }
+  return m;
+}
+
+/// General dilation of arbitrary occupancy, one thread per output word:
+/// OR over row offsets (dy, dz) of the source row x-dilated by wtab.
+__global__ void __launch_bounds__(256) k_dilate_general(const uint64_t* __restrict__ in,
+                                                        uint64_t* __restrict__ out, GridView g,
+                                                        const int* __restrict__ wtab, int reach) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t total = static_cast<int64_t>(g.nz) * g.ny * g.wx;
+  if (t >= total) return;
+  const int ww = static_cast<int>(t % g.wx);
+  const int64_t row = t / g.wx;
+  const int y = static_cast<int>(row % g.ny);
+  const int z = static_cast<int>(row / g.ny);
+  uint64_t m = 0;
+  for (int dz = -reach; dz <= reach; ++dz) {
+    const int zz = z + dz;
+    if (zz < 0 || zz >= g.nz) continue;
+    for (int dy = -reach; dy <= reach; ++dy) {
+      const int yy = y + dy;
+      if (yy < 0 || yy >= g.ny) continue;
+      const int w = __ldg(wtab + dy * dy + dz * dz);
+      if (w < 0) continue;
+      const uint64_t* r = in + (static_cast<size_t>(zz) * g.ny + yy) * g.wx;
+      if (w < 64) {
+        const uint64_t cur = __ldg(r + ww);
+        const uint64_t prev = ww > 0 ? __ldg(r + ww - 1) : 0ull;
+        const uint64_t next = ww + 1 < g.wx ? __ldg(r + ww + 1) : 0ull;
+        m |= xdilate_small(prev, cur, next, w);
+      } else {
+        m |= xdilate_any(r, g.wx, g.nx, ww, w);
+      }
+    }
+  }
+  // padding bits past nx stay clear
+  const int base = ww * 64;
+  if (base + 64 > g.nx) m &= range_mask(0, g.nx - 1, base);
+  out[t] = m;
+}
+
+__global__ void k_or_into(uint64_t* __restrict__ dst, const uint64_t* __restrict__ src, size_t n) {
+  const size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < n) dst[k] |= src[k];
+}
+
+/// bits -> reference bytes (x fastest), 8 cells per thread.
+__global__ void k_bits_to_u8(const uint64_t* __restrict__ bits, GridView g, uint8_t* __restrict__ out) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t cells = static_cast<int64_t>(g.nx) * g.ny * g.nz;
+  const int64_t c0 = t * 8;
+  if (c0 >= cells) return;
+  for (int k = 0; k < 8 && c0 + k < cells; ++k) {
+    const int64_t c = c0 + k;
+    const int ix = static_cast<int>(c % g.nx);
+    const int64_t r = c / g.nx;
+    const uint64_t w = bits[r * g.wx + (ix >> 6)];
+    out[c] = static_cast<uint8_t>((w >> (ix & 63)) & 1ull);
+  }
+}
+
+/// reference bytes -> bits, one thread per word.
+__global__ void k_u8_to_bits(const uint8_t* __restrict__ occ, GridView g, uint64_t* __restrict__ bits) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t total = static_cast<int64_t>(g.nz) * g.ny * g.wx;
+  if (t >= total) return;
+  const int ww = static_cast<int>(t % g.wx);
+  const int64_t row = t / g.wx;
+  uint64_t m = 0;
+  for (int b = 0; b < 64; ++b) {
+    const int ix = ww * 64 + b;
+    if (ix >= g.nx) break;
+    if (occ[row * g.nx + ix]) m |= 1ull << b;
+  }
+  bits[t] = m;
+}
+
+__global__ void k_popcount(const uint64_t* __restrict__ bits, size_t n, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+       k += static_cast<size_t>(gridDim.x) * blockDim.x)
+    c += __popcll(bits[k]);
+  c = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(c));
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, c);
+}
+
+__global__ void k_point_clear(GridView g, const double* __restrict__ xyz, int64_t n,
+                              uint8_t* __restrict__ out) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  out[k] = rpd::point_clear(g, V3{xyz[3 * k], xyz[3 * k + 1], xyz[3 * k + 2]}) ? 1 : 0;
+}
+
+__global__ void k_segment_clear(GridView g, const double* __restrict__ a, const double* __restrict__ b,
+                                int64_t n, int ns, uint8_t* __restrict__ out) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const V3 f{a[3 * k], a[3 * k + 1], a[3 * k + 2]};
+  const V3 t{b[3 * k], b[3 * k + 1], b[3 * k + 2]};
+  out[k] = rpd::walk_clear(g, f, t, ns) ? 1 : 0;
+}
+
+inline unsigned blocks_for(int64_t n, int threads) {
+  return static_cast<unsigned>((n + threads - 1) / threads);
+}
+
+constexpr int kFusedPrimLimit = 512;
+
+/// Build the index-box list of the obstacles on the device.
+DevBuf<Prim> obstacles_to_prims(rp_grid* g, const rp_obstacle* obs, int n, int64_t* n_out,
+                                bool* only_boxes) {
+  rp_ctx* ctx = g->ctx;
+  std::vector<double> boxes;
+  std::vector<double> cloud;
+  for (int k = 0; k < n; ++k) {
+    if (obs[k].shape == RP_SHAPE_BOX) {
+      require(obs[k].box_min[0] <= obs[k].box_max[0] && obs[k].box_min[1] <= obs[k].box_max[1] &&
+                  obs[k].box_min[2] <= obs[k].box_max[2],
+              RP_E_INVALID_PARAMETER, "obstacle box min must be <= max: ");
+      for (int a = 0; a < 3; ++a) boxes.push_back(obs[k].box_min[a]);
+      for (int a = 0; a < 3; ++a) boxes.push_back(obs[k].box_max[a]);
+    } else {
+      for (int64_t p = 0; p < obs[k].n_points; ++p)
+        for (int a = 0; a < 3; ++a) cloud.push_back(obs[k].points[3 * p + a]);
+    }
+  }
+  const int nb = static_cast<int>(boxes.size() / 6);
+  const int64_t nc = static_cast<int64_t>(cloud.size() / 3);
+  *only_boxes = nc == 0;
+  DevBuf<Prim> prims(nb + nc, ctx->stream);
+  const GridView v = g->view();
+  if (nb) {
+    DevBuf<double> dbox(boxes.size(), ctx->stream);
+    copy_to_device(ctx, dbox.p, boxes.data(), boxes.size() * sizeof(double));
+    launch(ctx, "voxelize", k_box_ranges, dim3(blocks_for(3 * nb, 128)), dim3(128), 0, dbox.p, nb,
+           v, prims.p);
+  }
+  if (nc) {
+    DevBuf<double> dpts(cloud.size(), ctx->stream);
+    copy_to_device(ctx, dpts.p, cloud.data(), cloud.size() * sizeof(double));
+    launch(ctx, "voxelize", k_cloud_cells, dim3(blocks_for(nc, 256)), dim3(256), 0, dpts.p, nc, v,
+           prims.p + nb);
+  }
+  *n_out = nb + nc;
+  return prims;
+}
+
+void run_rows(rp_grid* g, const Prim* prims, int np, const DilTable& t, int y0, int y1, int z0,
+              int z1, bool accumulate, const char* name) {
+  rp_ctx* ctx = g->ctx;
+  y0 = std::max(0, y0);
+  z0 = std::max(0, z0);
+  y1 = std::min(g->dims[1] - 1, y1);
+  z1 = std::min(g->dims[2] - 1, z1);
+  if (y0 > y1 || z0 > z1) return;
+  DevBuf<int> wtab(t.w.size(), ctx->stream);
+  copy_to_device(ctx, wtab.p, t.w.data(), t.w.size() * sizeof(int));
+  const int ny_rows = y1 - y0 + 1;
+  const int64_t words = static_cast<int64_t>(z1 - z0 + 1) * ny_rows * g->wx;
+  launch(ctx, name, k_mark_dilate_rows, dim3(blocks_for(words, 256)), dim3(256),
+         static_cast<size_t>(np) * sizeof(Prim), g->bits, g->view(), prims, np, wtab.p, t.reach,
+         y0, ny_rows, z0, accumulate ? 1 : 0);
+}
+
+void dilate_general(rp_grid* g, double radius) {
+  rp_ctx* ctx = g->ctx;
+  const DilTable t = make_table(radius, g->voxel_size);
+  DevBuf<int> wtab(t.w.size(), ctx->stream);
+  copy_to_device(ctx, wtab.p, t.w.data(), t.w.size() * sizeof(int));
+  uint64_t* out = nullptr;
+  RP_CUDA(cudaMalloc(&out, g->n_words * sizeof(uint64_t) + 8));
+  launch(ctx, "dilate", k_dilate_general, dim3(blocks_for(static_cast<int64_t>(g->n_words), 256)),
+         dim3(256), 0, static_cast<const uint64_t*>(g->bits), out, g->view(),
+         static_cast<const int*>(wtab.p), t.reach);
+  RP_CUDA(cudaStreamSynchronize(ctx->stream));
+  RP_CUDA(cudaFree(g->bits));
+  g->bits = out;
+}
+
+rp_grid* new_grid(rp_ctx* ctx, const double* origin, double vs, const int* dims) {
+  auto* g = new rp_grid();
+  g->ctx = ctx;
+  for (int a = 0; a < 3; ++a) {
+    g->dims[a] = dims[a];
+    g->origin[a] = origin[a];
+  }
+  g->voxel_size = vs;
+  g->wx = (dims[0] + 63) / 64;
+  g->n_words = static_cast<size_t>(g->wx) * dims[1] * dims[2];
+  RP_CUDA(cudaMalloc(&g->bits, g->n_words * sizeof(uint64_t) + 8));
+  RP_CUDA(cudaMemsetAsync(g->bits, 0, g->n_words * sizeof(uint64_t), ctx->stream));
+  return g;
+}
+
+}  // namespace
+
+rp_grid* grid_alloc_like(const rp_grid* src) {
+  rp_grid* g = new_grid(src->ctx, src->origin, src->voxel_size, src->dims);
+  g->dilation_radius = src->dilation_radius;
+  return g;
+}
+
+/// mark_obstacles + dilate(radius) for box / cloud obstacles (see file head).
+void grid_mark_dilate_boxes(rp_grid* g, const rp_obstacle* obs, int n, double radius,
+                            bool or_into_existing) {
+  require(radius >= 0.0, RP_E_INVALID_PARAMETER, "dilation radius must be >= 0");
+  int64_t np = 0;
+  bool only_boxes = true;
+  DevBuf<Prim> prims = obstacles_to_prims(g, obs, n, &np, &only_boxes);
+  const bool fused_ok = (!or_into_existing || g->empty) && np <= kFusedPrimLimit;
+  if (np > 0 && fused_ok) {
+    const DilTable t = make_table(radius, g->voxel_size);
+    run_rows(g, prims.p, static_cast<int>(np), t, 0, g->dims[1] - 1, 0, g->dims[2] - 1,
+             or_into_existing && !g->empty, "mark_dilate");
+  } else if (np > 0) {
+    // many primitives or pre-existing occupancy: mark, then general dilation
+    DilTable t0;
+    t0.reach = 0;
+    t0.w = {0};
+    if (only_boxes || np <= kFusedPrimLimit) {
+      run_rows(g, prims.p, static_cast<int>(np), t0, 0, g->dims[1] - 1, 0, g->dims[2] - 1, true,
+               "voxelize");
+    } else {
+      launch(g->ctx, "voxelize", k_mark_cells, dim3(blocks_for(np, 256)), dim3(256), 0, g->bits,
+             g->view(), static_cast<const Prim*>(prims.p), np);
+    }
+    g->empty = false;
+    if (radius != 0.0) dilate_general(g, radius);
+  }
+  if (np > 0) g->empty = false;
+  if (radius != 0.0) g->dilation_radius += radius;
+}
+
+}  // namespace rp
+
+using namespace rp;
+
+extern "C" {
+
+rp_status rp_grid_build(rp_ctx* ctx, const double bmin[3], const double bmax[3], double vs,
+                        uint64_t budget, rp_grid** out) {
+  return guarded([&] {
+    require(vs > 0.0, RP_E_INVALID_PARAMETER, "voxel_size must be > 0");
+    for (int a = 0; a < 3; ++a)
+      require(bmin[a] < bmax[a], RP_E_INVALID_PARAMETER,
+              "bounds_min must be < bounds_max componentwise");
+    if (budget == 0) budget = uint64_t(1) << 27;
+    int dims[3];
+    for (int a = 0; a < 3; ++a) {
+      const double extent = bmax[a] - bmin[a];
+      dims[a] = std::max(1, static_cast<int>(std::ceil(extent / vs - 1e-9)));
+    }
+    const uint64_t cells = static_cast<uint64_t>(dims[0]) * dims[1] * dims[2];
+    require(cells <= budget, RP_E_CAPACITY_EXCEEDED, "grid would exceed the configured cell budget");
+    *out = new_grid(ctx, bmin, vs, dims);
+  });
+}
+
+rp_status rp_grid_mark(rp_grid* g, const rp_obstacle* obs, int32_t n) {
+  return guarded([&] {
+    if (n <= 0) return;
+    int64_t np = 0;
+    bool only_boxes = true;
+    DevBuf<Prim> prims = obstacles_to_prims(g, obs, n, &np, &only_boxes);
+    if (np == 0) return;
+    if (np <= kFusedPrimLimit) {
+      DilTable t0;
+      t0.reach = 0;
+      t0.w = {0};
+      run_rows(g, prims.p, static_cast<int>(np), t0, 0, g->dims[1] - 1, 0, g->dims[2] - 1,
+               !g->empty, "voxelize");
+    } else {
+      launch(g->ctx, "voxelize", k_mark_cells, dim3(blocks_for(np, 256)), dim3(256), 0, g->bits,
+             g->view(), static_cast<const Prim*>(prims.p), np);
+    }
+    g->empty = false;
+  });
+}
+
+rp_status rp_grid_dilate(rp_grid* g, double radius) {
+  return guarded([&] {
+    require(radius >= 0.0, RP_E_INVALID_PARAMETER, "dilation radius must be >= 0");
+    if (radius == 0.0) return;
+    if (!g->empty) dilate_general(g, radius);
+    g->dilation_radius += radius;
+  });
+}
+
+rp_status rp_grid_mark_dilate_boxes(rp_grid* g, const rp_obstacle* obs, int32_t n, double radius) {
+  return guarded([&] { grid_mark_dilate_boxes(g, obs, n, radius, true); });
+}
+
+rp_status rp_build_scene_grid(rp_ctx* ctx, const double bmin[3], const double bmax[3], double vs,
+                              double dilation, const rp_obstacle* obs, int32_t n_obs,
+                              const rp_arm* arm, const rp_reach_params* rp, rp_grid** out) {
+  return guarded([&] {
+    rp_grid* g = nullptr;
+    rp_status s = rp_grid_build(ctx, bmin, bmax, vs, 0, &g);
+    if (s != RP_OK) throw Fail{s, rp_last_error()};
+    try {
+      const double r = rp_effective_dilation(arm, rp, dilation);
+      grid_mark_dilate_boxes(g, obs, n_obs, r, false);
+    } catch (...) {
+      rp_grid_destroy(g);
+      throw;
+    }
+    *out = g;
+  });
+}
+
+rp_status rp_grid_overlay(const rp_grid* base, const rp_obstacle* obs, rp_grid** aug) {
+  return guarded([&] {
+    rp_ctx* ctx = base->ctx;
+    // The reference rebuilds the overlay from origin + dims*vs
+    // (path_planner.cpp:1013-1016); it must land on the same shape.
+    for (int a = 0; a < 3; ++a) {
+      const double extent =
+          (base->origin[a] + base->dims[a] * base->voxel_size) - base->origin[a];
+      const int d = std::max(1, static_cast<int>(std::ceil(extent / base->voxel_size - 1e-9)));
+      require(d == base->dims[a], RP_E_INTERNAL, "overlay grid shape differs from the base grid");
+    }
+    rp_grid* g = *aug;
+    if (!g) {
+      g = grid_alloc_like(base);
+    } else {
+      require(g->dims[0] == base->dims[0] && g->dims[1] == base->dims[1] &&
+                  g->dims[2] == base->dims[2],
+              RP_E_INVALID_PARAMETER, "overlay target grid has a different shape");
+    }
+    RP_CUDA(cudaMemcpyAsync(g->bits, base->bits, base->n_words * sizeof(uint64_t),
+                            cudaMemcpyDeviceToDevice, ctx->stream));
+    g->dilation_radius = base->dilation_radius;
+    g->empty = base->empty;
+    int64_t np = 0;
+    bool only_boxes = true;
+    DevBuf<Prim> prims = obstacles_to_prims(g, obs, 1, &np, &only_boxes);
+    if (np > 0) {
+      const DilTable t = make_table(base->dilation_radius, base->voxel_size);
+      if (np <= kFusedPrimLimit) {
+        // bbox-limited: only rows within reach of the obstacle are touched
+        std::vector<Prim> hp(np);
+        copy_to_host(ctx, hp.data(), prims.p, np * sizeof(Prim));
+        int y0 = 1 << 30, y1 = -1, z0 = 1 << 30, z1 = -1;
+        for (const Prim& p : hp) {
+          if (p.a[0] > p.b[0] || p.a[1] > p.b[1] || p.a[2] > p.b[2]) continue;
+          y0 = std::min(y0, p.a[1]);
+          y1 = std::max(y1, p.b[1]);
+          z0 = std::min(z0, p.a[2]);
+          z1 = std::max(z1, p.b[2]);
+        }
+        if (y1 >= 0)
+          run_rows(g, prims.p, static_cast<int>(np), t, y0 - t.reach, y1 + t.reach, z0 - t.reach,
+                   z1 + t.reach, true, "overlay");
+      } else {
+        rp_grid* ov = grid_alloc_like(base);
+        ov->dilation_radius = 0.0;
+        launch(ctx, "voxelize", k_mark_cells, dim3(blocks_for(np, 256)), dim3(256), 0, ov->bits,
+               ov->view(), static_cast<const Prim*>(prims.p), np);
+        ov->empty = false;
+        if (base->dilation_radius != 0.0) dilate_general(ov, base->dilation_radius);
+        launch(ctx, "overlay", k_or_into, dim3(blocks_for(static_cast<int64_t>(g->n_words), 256)),
+               dim3(256), 0, g->bits, static_cast<const uint64_t*>(ov->bits), g->n_words);
+        rp_grid_destroy(ov);
+      }
+      g->empty = false;
+    }
+    *aug = g;
+  });
+}
+
+rp_status rp_grid_info(const rp_grid* g, int32_t dims[3], double origin[3], double* vs,
+                       double* dil) {
+  return guarded([&] {
+    for (int a = 0; a < 3; ++a) {
+      if (dims) dims[a] = g->dims[a];
+      if (origin) origin[a] = g->origin[a];
+    }
+    if (vs) *vs = g->voxel_size;
+    if (dil) *dil = g->dilation_radius;
+  });
+}
+
+rp_status rp_grid_download_u8(rp_grid* g, uint8_t* dst, uint64_t cap) {
+  return guarded([&] {
+    const int64_t cells = static_cast<int64_t>(g->dims[0]) * g->dims[1] * g->dims[2];
+    require(cap >= static_cast<uint64_t>(cells), RP_E_INVALID_PARAMETER, "buffer too small");
+    DevBuf<uint8_t> d(cells, g->ctx->stream);
+    launch(g->ctx, "download", k_bits_to_u8, dim3(blocks_for((cells + 7) / 8, 256)), dim3(256), 0,
+           static_cast<const uint64_t*>(g->bits), g->view(), d.p);
+    copy_to_host(g->ctx, dst, d.p, cells);
+  });
+}
+
+rp_status rp_grid_download_bits(rp_grid* g, uint64_t* dst, uint64_t cap_words) {
+  return guarded([&] {
+    require(cap_words >= g->n_words, RP_E_INVALID_PARAMETER, "buffer too small");
+    copy_to_host(g->ctx, dst, g->bits, g->n_words * sizeof(uint64_t));
+  });
+}
+
+rp_status rp_grid_upload_u8(rp_ctx* ctx, const double origin[3], double vs, const int32_t dims[3],
+                            const uint8_t* occ, double dil, rp_grid** out) {
+  return guarded([&] {
+    require(vs > 0.0 && dims[0] > 0 && dims[1] > 0 && dims[2] > 0, RP_E_INVALID_PARAMETER,
+            "bad grid shape");
+    rp_grid* g = new_grid(ctx, origin, vs, dims);
+    g->dilation_radius = dil;
+    const int64_t cells = static_cast<int64_t>(dims[0]) * dims[1] * dims[2];
+    DevBuf<uint8_t> d(cells, ctx->stream);
+    copy_to_device(ctx, d.p, occ, cells);
+    launch(ctx, "upload", k_u8_to_bits, dim3(blocks_for(static_cast<int64_t>(g->n_words), 256)),
+           dim3(256), 0, static_cast<const uint8_t*>(d.p), g->view(), g->bits);
+    g->empty = false;
+    *out = g;
+  });
+}
+
+rp_status rp_grid_occupied_count(rp_grid* g, uint64_t* count) {
+  return guarded([&] {
+    DevBuf<unsigned long long> c(1, g->ctx->stream);
+    c.zero();
+    launch(g->ctx, "popcount", k_popcount, dim3(g->ctx->sm_count * 4), dim3(256), 0,
+           static_cast<const uint64_t*>(g->bits), g->n_words, c.p);
+    unsigned long long h = 0;
+    copy_to_host(g->ctx, &h, c.p, sizeof(h));
+    *count = h;
+  });
+}
+
+rp_status rp_grid_point_clear(rp_grid* g, const double* xyz, int64_t n, uint8_t* out) {
+  return guarded([&] {
+    if (n <= 0) return;
+    DevBuf<double> d(3 * n, g->ctx->stream);
+    DevBuf<uint8_t> o(n, g->ctx->stream);
+    copy_to_device(g->ctx, d.p, xyz, 3 * n * sizeof(double));
+    launch(g->ctx, "point_clear", k_point_clear, dim3(blocks_for(n, 256)), dim3(256), 0, g->view(),
+           static_cast<const double*>(d.p), n, o.p);
+    copy_to_host(g->ctx, out, o.p, n);
+  });
+}
+
+rp_status rp_grid_segment_clear(rp_grid* g, const double* a, const double* b, int64_t n,
+                                int32_t ns, uint8_t* out) {
+  return guarded([&] {
+    require(ns >= 1, RP_E_INVALID_PARAMETER, "n_samples must be >= 1");
+    if (n <= 0) return;
+    DevBuf<double> da(3 * n, g->ctx->stream), db(3 * n, g->ctx->stream);
+    DevBuf<uint8_t> o(n, g->ctx->stream);
+    copy_to_device(g->ctx, da.p, a, 3 * n * sizeof(double));
+    copy_to_device(g->ctx, db.p, b, 3 * n * sizeof(double));
+    launch(g->ctx, "segment_clear", k_segment_clear, dim3(blocks_for(n, 256)), dim3(256), 0,
+           g->view(), static_cast<const double*>(da.p), static_cast<const double*>(db.p), n, ns,
+           o.p);
+    copy_to_host(g->ctx, out, o.p, n);
+  });
+}
+
+rp_status rp_grid_copy(const rp_grid* src, rp_grid** out) {
+  return guarded([&] {
+    rp_grid* g = grid_alloc_like(src);
+    RP_CUDA(cudaMemcpyAsync(g->bits, src->bits, src->n_words * sizeof(uint64_t),
+                            cudaMemcpyDeviceToDevice, src->ctx->stream));
+    g->empty = src->empty;
+    *out = g;
+  });
+}
+
+rp_status rp_grid_destroy(rp_grid* g) {
+  return guarded([&] {
+    if (!g) return;
+    cudaStreamSynchronize(g->ctx->stream);
+    if (g->bits) cudaFree(g->bits);
+    delete g;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,226 @@
+// Internal host-side structures of libreachplan_b200 (not part of the ABI).
+#pragma once
+
+#include "reachplan_b200.h"
+#include "rp_device.cuh"
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <exception>
+#include <map>
+#include <new>
+#include <string>
+#include <vector>
+
+namespace rp {
+
+using rpd::V3;
+
+/// Thrown inside the library, converted to rp_status at the ABI.
+struct Fail {
+  rp_status code;
+  std::string msg;
+};
+
+const char* errc_name(rp_status code);
+[[noreturn]] void fail(rp_status code, const std::string& msg);
+inline void require(bool ok, rp_status code, const std::string& msg) {
+  if (!ok) fail(code, msg);
+}
+void cuda_check(cudaError_t e, const char* what);
+void set_last_error(const std::string& s);
+
+/// Every ABI entry point runs its body through this guard: nothing throws
+/// across the C boundary.
+template <typename F>
+inline rp_status guarded(F&& f) {
+  try {
+    f();
+    return RP_OK;
+  } catch (const Fail& e) {
+    set_last_error(e.msg);
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("internal: host allocation failed");
+    return RP_E_INTERNAL;
+  } catch (const std::exception& e) {
+    set_last_error(std::string("internal: ") + e.what());
+    return RP_E_INTERNAL;
+  }
+}
+#define RP_CUDA(x) ::rp::cuda_check((x), #x)
+
+struct TimedLaunch {
+  std::string name;
+  cudaEvent_t start, stop;
+};
+
+}  // namespace rp
+
+struct rp_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  bool timing = false;
+  int64_t launches = 0;
+  std::vector<rp::TimedLaunch> pending;
+  std::vector<cudaEvent_t> event_pool;
+  std::map<std::string, std::pair<double, int64_t>> kernel_ms;
+  int sm_count = 148;
+  // Small pinned staging buffer for scalar read-backs.
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+};
+
+struct rp_quiver {
+  rp_ctx* ctx = nullptr;
+  int n = 0;
+  std::vector<double> host_xyz;  // AoS, reference order
+  double* d_soa = nullptr;       // x[n], y[n], z[n]
+};
+
+struct rp_grid {
+  rp_ctx* ctx = nullptr;
+  int dims[3] = {0, 0, 0};
+  int wx = 0;  // 64-bit words per x row
+  double origin[3] = {0, 0, 0};
+  double voxel_size = 0.0;
+  double dilation_radius = 0.0;
+  uint64_t* bits = nullptr;
+  size_t n_words = 0;
+  bool empty = true;  // no occupancy since build: fused mark+dilate is exact
+
+  rpd::GridView view() const {
+    rpd::GridView v;
+    v.bits = bits;
+    v.nx = dims[0];
+    v.ny = dims[1];
+    v.nz = dims[2];
+    v.wx = wx;
+    v.ox = origin[0];
+    v.oy = origin[1];
+    v.oz = origin[2];
+    v.vs = voxel_size;
+    v.rvs = 1.0 / voxel_size;
+    return v;
+  }
+};
+
+namespace rp {
+
+/// Device arm description used by every search kernel.
+struct ArmDev {
+  int nseg;
+  int has_offsets;
+  int any_limit;
+  int lim_active[4];
+  double L[4];
+  double off[4];
+  rpd::Limit lim[4];
+  V3 root;
+  double arm_radius;
+  rpd::M3 base;
+};
+
+ArmDev make_arm_dev(const rp_arm& a);
+void validate_arm(const rp_arm& a);            // ArmSpec::validate (src/arm_model.cpp:102-122)
+void validate_reach(const rp_reach_params& r);  // ReachParams::validate (src/reach_solver.cpp:45-52)
+
+/// Materialised pose on the host: PoseChain equivalent.
+struct HostPose {
+  int nseg = 0;
+  bool has_elbows = false;
+  V3 seg[4];
+  V3 joints[5];
+  V3 elbows[4];
+  int qidx[4] = {-1, -1, -1, -1};
+  double s4dev = 0.0;
+  std::vector<V3> waypoints;
+};
+
+void to_abi(const HostPose& p, rp_pose* out, double* wps, int cap);
+HostPose from_abi(const rp_pose& p, const double* wps);
+
+/// Shortcut record (ShortcutPath, inc/reachplan/reach_solver.hpp:60-74).
+struct HostShortcut {
+  int segment_index = 1;
+  int hit = 0;
+  int seg1 = -1, seg2 = -1;
+  bool has_bridge = false;
+  bool via_direct = false;
+  V3 bridge{0, 0, 0};
+  double path_length = 0.0;
+  std::vector<V3> prefix;     // segment-1 samples (segment-2 hits)
+  std::vector<V3> sublength;  // hit samples, or the direct origin->target samples
+  HostPose basis;
+
+  std::vector<V3> tip_waypoints(V3 target) const {
+    std::vector<V3> w = prefix;
+    w.insert(w.end(), sublength.begin(), sublength.end());
+    if (has_bridge) w.push_back(target);
+    return w;
+  }
+};
+
+// Launch accounting: every kernel of the library goes through this.
+void launch_begin(rp_ctx* ctx, const char* name, cudaEvent_t* ev);
+void launch_end(rp_ctx* ctx, const char* name, cudaEvent_t ev);
+
+template <typename K, typename... Args>
+inline void launch(rp_ctx* ctx, const char* name, K kernel, dim3 grid, dim3 block, size_t smem,
+                   Args... args) {
+  cudaEvent_t ev = nullptr;
+  launch_begin(ctx, name, &ev);
+  kernel<<<grid, block, smem, ctx->stream>>>(args...);
+  launch_end(ctx, name, ev);
+}
+
+/// Stream-ordered device buffer.
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(size_t count, cudaStream_t stream) { alloc(count, stream); }
+  void alloc(size_t count, cudaStream_t stream) {
+    release();
+    s = stream;
+    n = count;
+    if (count) RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), stream));
+  }
+  void zero() {
+    if (n) RP_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { release(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    release();
+    p = o.p; n = o.n; s = o.s;
+    o.p = nullptr; o.n = 0;
+    return *this;
+  }
+};
+
+void copy_to_host(rp_ctx* ctx, void* dst, const void* src, size_t bytes);  // syncs
+void copy_to_device(rp_ctx* ctx, void* dst, const void* src, size_t bytes);
+
+// Derived reach parameters (src/reach_solver.cpp:28-43).
+double nominal_spacing(const rp_arm& a, const rp_reach_params& r);
+double resolved_epsilon(const rp_arm& a, const rp_reach_params& r);
+double resolved_near_radius(const rp_arm& a, const rp_reach_params& r);
+
+// Grid entry points used across translation units.
+rp_grid* grid_alloc_like(const rp_grid* g);
+void grid_mark_dilate_boxes(rp_grid* g, const rp_obstacle* obs, int n, double radius,
+                            bool or_into_existing);
+
+}  // namespace rp

@@ -1,0 +1,1015 @@
+// Path-planner device kernels (src/path_planner.cpp, src/arm_model.cpp):
+// waypoint IK search, pose validity batches, unfold interpolation,
+// refinement, polyline-deviation scoring.
+#include "rp_path.cuh"
+#include "rp_planner.hpp"
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+
+namespace rp {
+
+using rpd::V3;
+
+namespace {
+constexpr unsigned FULL = 0xffffffffu;
+constexpr double kPi = 3.14159265358979323846;
+
+inline unsigned nblk(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Pose helpers (host + device so materialisation replays the same arithmetic).
+
+/// link_clear_scaled (src/path_planner.cpp:41-46)
+__device__ inline bool link_clear_scaled(const rpd::GridView& g, V3 from, V3 to, double spacing) {
+  const double len = rpd::norm(to - from);
+  if (len == 0.0) return true;
+  return rpd::walk_clear(g, from, to, rpd::scaled_sample_count(len, spacing));
+}
+
+/// pose_clear (src/path_planner.cpp:50-61)
+__device__ inline bool pose_clear(const rpd::GridView& g, const DevPose& p, int n, double spacing) {
+  for (int j = 0; j < p.nseg; ++j) {
+    V3 from = p.joints[j];
+    if (p.has_elbows) {
+      if (!link_clear_scaled(g, p.joints[j], p.elbows[j], spacing)) return false;
+      from = p.elbows[j];
+    }
+    if (!rpd::walk_clear(g, from, p.joints[j + 1], n)) return false;
+  }
+  return true;
+}
+
+/// pose_valid (src/path_planner.cpp:63-67)
+__device__ inline bool pose_valid(const rpd::GridView& g, const ArmDev& arm, const DevPose& p, int n,
+                                  double spacing) {
+  return pose_clear(g, p, n, spacing) && pose_limits_ok(arm, p) &&
+         pose_self_free(p, 2.0 * arm.arm_radius);
+}
+
+__host__ __device__ inline rpd::M3 angle_axis(double angle, V3 axis) {
+  // Eigen AngleAxis::toRotationMatrix
+  rpd::M3 r;
+  const V3 sa = sin(angle) * axis;
+  const double c = cos(angle);
+  const V3 c1 = (1.0 - c) * axis;
+  double tmp = c1.x * axis.y;
+  r.a[0][1] = tmp - sa.z;
+  r.a[1][0] = tmp + sa.z;
+  tmp = c1.x * axis.z;
+  r.a[0][2] = tmp + sa.y;
+  r.a[2][0] = tmp - sa.y;
+  tmp = c1.y * axis.z;
+  r.a[1][2] = tmp - sa.x;
+  r.a[2][1] = tmp + sa.x;
+  r.a[0][0] = c1.x * axis.x + c;
+  r.a[1][1] = c1.y * axis.y + c;
+  r.a[2][2] = c1.z * axis.z + c;
+  return r;
+}
+
+__host__ __device__ inline V3 m_vec(const rpd::M3& m, V3 v) {
+  const double in[3] = {v.x, v.y, v.z};
+  double out[3];
+  for (int r = 0; r < 3; ++r) {
+    double s = m.a[r][0] * in[0];
+    s = s + m.a[r][1] * in[1];
+    s = s + m.a[r][2] * in[2];
+    out[r] = s;
+  }
+  return V3{out[0], out[1], out[2]};
+}
+
+__host__ __device__ inline rpd::M3 m_transpose(const rpd::M3& m) {
+  rpd::M3 t;
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) t.a[r][c] = m.a[c][r];
+  return t;
+}
+
+/// folded_pose (src/path_planner.cpp:711-727)
+__host__ __device__ inline DevPose folded_pose(const ArmDev& arm, V3 n, double flex) {
+  V3 seed{1, 0, 0};
+  if (fabs(rpd::dot(n, seed)) > fabs(rpd::dot(n, V3{0, 0, 1}))) seed = V3{0, 0, 1};
+  if (fabs(rpd::dot(n, seed)) > fabs(rpd::dot(n, V3{0, 1, 0}))) seed = V3{0, 1, 0};
+  V3 dir = rpd::normalized(seed - rpd::dot(seed, n) * n);
+  DevPose p{};
+  p.nseg = arm.nseg;
+  double sign = 1.0;
+  for (int j = 0; j < arm.nseg; ++j) {
+    p.seg[j] = arm.L[j] * dir;
+    p.qidx[j] = -1;
+    dir = m_vec(angle_axis(sign * flex, n), dir);
+    sign = -sign;
+  }
+  build_chain(arm, p);
+  return p;
+}
+
+__host__ __device__ inline V3 perpendicular_of(V3 dir) {
+  const V3 seed = fabs(dir.z) < 0.9 ? V3{0, 0, 1} : V3{1, 0, 0};
+  return rpd::normalized(rpd::cross(dir, seed));
+}
+
+/// pose_plane_normal (src/path_planner.cpp:450-454)
+__host__ __device__ inline V3 pose_plane_normal(const DevPose& p) {
+  const V3 n = rpd::cross(p.seg[0], p.seg[1]);
+  if (rpd::norm(n) <= 1e-12) return perpendicular_of(rpd::normalized(p.seg[0]));
+  return rpd::normalized(n);
+}
+
+/// vectors_to_joint_angles (src/arm_model.cpp:163-176)
+__host__ __device__ inline bool to_angles(const ArmDev& arm, const DevPose& p, double* az, double* el) {
+  rpd::M3 frame = arm.base;
+  for (int k = 0; k < p.nseg; ++k) {
+    const double len = rpd::norm(p.seg[k]);
+    if (!(len > 0.0)) return false;
+    const rpd::FrameStep st = rpd::advance_frame(frame, p.seg[k] / len);
+    az[k] = st.theta;
+    el[k] = st.phi;
+    frame = rpd::m_mul(rpd::m_mul(frame, rpd::rot_z(st.theta)), rpd::rot_y(st.phi));
+  }
+  return true;
+}
+
+/// joint_angles_to_vectors (src/arm_model.cpp:178-193)
+__host__ __device__ inline DevPose from_angles(const ArmDev& arm, const double* az, const double* el) {
+  DevPose p{};
+  p.nseg = arm.nseg;
+  rpd::M3 frame = arm.base;
+  for (int j = 0; j < arm.nseg; ++j) {
+    frame = rpd::m_mul(rpd::m_mul(frame, rpd::rot_z(az[j])), rpd::rot_y(el[j]));
+    p.seg[j] = arm.L[j] * rpd::m_col(frame, 2);
+    p.qidx[j] = -1;
+  }
+  build_chain(arm, p);
+  return p;
+}
+
+// ---------------------------------------------------------------------------
+// waypoint_ik (src/path_planner.cpp:167-291)
+
+__device__ inline V3 wq(const WikDev& w, int i) { return V3{w.qx[i], w.qy[i], w.qz[i]}; }
+
+/// One (i, j) candidate through every test of waypoint_ik, in order.
+__device__ bool wik_eval(const WikDev& w, const CiData& c, int j, DevPose* out, double* metric_out,
+                         int* opt_out) {
+  const ArmDev& arm = w.arm;
+  const V3 qj = wq(w, j);
+  rpd::FrameStep st2{};
+  bool have_st2 = false;
+  if (w.cond2) {
+    st2 = rpd::advance_frame(c.frame1, qj);
+    have_st2 = true;
+    if (!rpd::joint_angle_within(st2.theta, st2.phi, st2.degenerate, arm.lim[1])) return false;
+  }
+  V3 link2 = c.p1, elbow2{0, 0, 0};
+  const bool e2 = arm.off[1] > 0.0;
+  if (e2) {
+    elbow2 = c.p1 + arm.off[1] * rpd::m_col(st2.after_azimuth, 0);
+    link2 = elbow2;
+  }
+  const V3 p2 = link2 + arm.L[1] * qj;
+  const double move2 = rpd::norm(p2 - w.prev_j2);
+  if (move2 > w.j2max) return false;
+  const V3 v3 = w.wp - p2;
+  const double v3_len = rpd::norm(v3);
+  if (fabs(v3_len - arm.L[2]) > w.eps || v3_len < 1e-12) return false;
+  const V3 v3_hat = v3 / v3_len;
+  if (w.cond3) {
+    if (!have_st2) st2 = rpd::advance_frame(c.frame1, qj);
+    const rpd::FrameStep st3 = rpd::advance_frame(st2.frame, v3_hat);
+    if (!rpd::joint_angle_within(st3.theta, st3.phi, st3.degenerate, arm.lim[2])) return false;
+  }
+  double metric = c.move1 + move2;
+  if (w.has_bias) metric += rpd::norm(c.p1 - w.bias_j1) + rpd::norm(p2 - w.bias_j2);
+  if (!c.ok) return false;  // segment 1 blocked for every j (lazy walk1 + break)
+  if (e2 && !link_clear_scaled(w.g, c.p1, elbow2, w.spacing)) return false;
+  if (!rpd::walk_clear(w.g, link2, p2, w.n)) return false;
+  const V3 s3 = v3_hat * arm.L[2];
+  const V3 p3 = p2 + s3;
+  if (!rpd::walk_clear(w.g, p2, p3, w.n)) return false;
+  DevPose ch{};
+  ch.nseg = 3;
+  ch.seg[0] = arm.L[0] * wq(w, c.i);
+  ch.seg[1] = arm.L[1] * qj;
+  ch.seg[2] = s3;
+  ch.qidx[0] = c.i;
+  ch.qidx[1] = j;
+  ch.qidx[2] = -1;
+  ch.qidx[3] = -1;
+  build_chain(arm, ch);
+  ch.n_wp_links = 3;
+  ch.wp_from[0] = c.link1; ch.wp_to[0] = c.p1;
+  ch.wp_from[1] = link2;   ch.wp_to[1] = p2;
+  ch.wp_from[2] = p2;      ch.wp_to[2] = p3;
+  ch.n_wp[0] = ch.n_wp[1] = ch.n_wp[2] = w.n;
+  int opt = -1;
+  const double min_sep = 2.0 * arm.arm_radius;
+  if (w.four) {
+    // append_trail (src/path_planner.cpp:127-150)
+    bool done = false;
+    for (int o = 0; o <= w.n_opts && !done; ++o) {
+      const V3 dir = o < w.n_opts ? w.opt_dir[o] : rpd::normalized(ch.seg[2]);
+      DevPose cand = ch;
+      cand.nseg = 4;
+      cand.seg[3] = w.L4 * dir;
+      cand.qidx[3] = -1;
+      build_chain(arm, cand);
+      if (!pose_limits_ok(arm, cand)) continue;
+      if (!rpd::walk_clear(w.g, cand.joints[3], cand.joints[4], w.n)) continue;
+      if (!pose_self_free(cand, min_sep)) continue;
+      cand.n_wp_links = 4;
+      cand.wp_from[3] = cand.joints[3];
+      cand.wp_to[3] = cand.joints[4];
+      cand.n_wp[3] = w.n;
+      ch = cand;
+      opt = o;
+      done = true;
+    }
+    if (!done) return false;
+  } else if (!pose_self_free(ch, min_sep)) {
+    return false;
+  }
+  if (!pose_limits_ok(arm, ch)) return false;
+  if (!(rpd::norm(ch.joints[1] - w.prev_j1) <= w.sm1 &&
+        rpd::norm(ch.joints[2] - w.prev_j2) <= w.sm2))
+    return false;
+  *metric_out = metric;
+  *opt_out = opt;
+  if (out) *out = ch;
+  return true;
+}
+
+/// Candidate filters over the quiver: segment-1 directions inside the
+/// reference's cone that pass the joint-1 limit and the move1 bound, and
+/// segment-2 directions inside its cone (all directions for offset arms).
+__global__ void k_wik_filter(WikDev w, double cone1, double cone2, V3 u1, V3 u2,
+                             uint32_t* ibits, uint32_t* jbits) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  bool pi = false, pj = false;
+  if (i < w.Q) {
+    const V3 q = wq(w, i);
+    const ArmDev& arm = w.arm;
+    bool in1 = true;
+    if (w.filter_j) in1 = atan2(rpd::norm(rpd::cross(q, u1)), rpd::dot(q, u1)) <= cone1;
+    if (in1) {
+      rpd::FrameStep st{};
+      if (arm.lim_active[0] || arm.off[0] > 0.0) st = rpd::advance_frame(arm.base, q);
+      bool ok = !arm.lim_active[0] || rpd::joint_angle_within(st.theta, st.phi, st.degenerate, arm.lim[0]);
+      if (ok) {
+        V3 link = arm.root;
+        if (arm.off[0] > 0.0) link = arm.root + arm.off[0] * rpd::m_col(st.after_azimuth, 0);
+        const V3 p1 = link + arm.L[0] * q;
+        pi = !(rpd::norm(p1 - w.prev_j1) > w.j1max);
+      }
+    }
+    pj = !w.filter_j || atan2(rpd::norm(rpd::cross(q, u2)), rpd::dot(q, u2)) <= cone2;
+  }
+  const unsigned mi = __ballot_sync(FULL, pi), mj = __ballot_sync(FULL, pj);
+  if ((threadIdx.x & 31) == 0 && (i >> 5) < (w.Q + 31) / 32) {
+    ibits[i >> 5] = mi;
+    jbits[i >> 5] = mj;
+  }
+}
+
+/// Ordered compaction of both candidate lists + segment-1 data (one block).
+__global__ void __launch_bounds__(1024) k_wik_compact(WikDev w, WikScratch s) {
+  typedef cub::BlockScan<int, 1024> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int carry;
+  const int nwords = (w.Q + 31) / 32;
+  for (int which = 0; which < 2; ++which) {
+    const uint32_t* bits = which == 0 ? s.ibits : s.jbits;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int w0 = 0; w0 < nwords; w0 += 1024) {
+      const int wd = w0 + threadIdx.x;
+      const uint32_t word = wd < nwords ? bits[wd] : 0u;
+      int off = 0, total = 0;
+      Scan(tmp).ExclusiveSum(__popc(word), off, total);
+      off += carry;
+      uint32_t x = word;
+      while (x) {
+        const int b = __ffs(x) - 1;
+        x &= x - 1;
+        const int idx = wd * 32 + b;
+        if (which == 0) {
+          CiData c{};
+          c.i = idx;
+          const ArmDev& arm = w.arm;
+          const V3 q = wq(w, idx);
+          rpd::FrameStep st{};
+          if (arm.any_limit || arm.has_offsets) st = rpd::advance_frame(arm.base, q);
+          c.frame1 = st.frame;
+          V3 link = arm.root;
+          bool elb = arm.off[0] > 0.0;
+          if (elb) link = arm.root + arm.off[0] * rpd::m_col(st.after_azimuth, 0);
+          c.link1 = link;
+          c.p1 = link + arm.L[0] * q;
+          c.move1 = rpd::norm(c.p1 - w.prev_j1);
+          c.ok = (!elb || link_clear_scaled(w.g, arm.root, link, w.spacing)) &&
+                 rpd::walk_clear(w.g, link, c.p1, w.n);
+          s.ci[off] = c;
+        } else {
+          s.cj[off] = idx;
+        }
+        ++off;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) carry += total;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) s.counts[which] = carry;
+    __syncthreads();
+  }
+}
+
+__device__ inline bool wik_better(double m, long long o, double bm, long long bo) {
+  return m < bm || (m == bm && o < bo);
+}
+
+/// All (i, j) candidates; argmin of (metric, canonical order) = the first
+/// strict minimum of the reference's sequential scan. The last block to
+/// finish reduces the per-block winners and materialises the pose.
+__global__ void __launch_bounds__(256) k_wik_pairs(WikDev w, WikScratch s) {
+  const int nci = s.counts[0], ncj = s.counts[1];
+  const long long total = static_cast<long long>(nci) * ncj;
+  double bm = 1e308;
+  long long bo = LLONG_MAX;
+  int bopt = -1;
+  for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int a = static_cast<int>(t / ncj);
+    const CiData& c = s.ci[a];
+    if (!c.ok) continue;
+    double m;
+    int opt;
+    if (wik_eval(w, c, s.cj[t - static_cast<long long>(a) * ncj], nullptr, &m, &opt) &&
+        wik_better(m, t, bm, bo)) {
+      bm = m;
+      bo = t;
+      bopt = opt;
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    const double om = __shfl_down_sync(FULL, bm, off);
+    const long long oo = __shfl_down_sync(FULL, bo, off);
+    const int op = __shfl_down_sync(FULL, bopt, off);
+    if (wik_better(om, oo, bm, bo)) {
+      bm = om;
+      bo = oo;
+      bopt = op;
+    }
+  }
+  __shared__ WikBest wb[8];
+  __shared__ bool last;
+  if ((threadIdx.x & 31) == 0) wb[threadIdx.x >> 5] = WikBest{bm, bo, bopt};
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    WikBest b = wb[0];
+    for (int k = 1; k < static_cast<int>(blockDim.x >> 5); ++k)
+      if (wik_better(wb[k].metric, wb[k].ord, b.metric, b.ord)) b = wb[k];
+    s.block_best[blockIdx.x] = b;
+    __threadfence();
+    const unsigned ticket = atomicAdd(s.done, 1u);
+    last = ticket == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  WikBest b{1e308, LLONG_MAX, -1};
+  for (int k = 0; k < static_cast<int>(gridDim.x); ++k) {
+    WikBest r;
+    r.metric = __ldcg(&s.block_best[k].metric);
+    r.ord = __ldcg(&s.block_best[k].ord);
+    r.opt = __ldcg(&s.block_best[k].opt);
+    if (wik_better(r.metric, r.ord, b.metric, b.ord)) b = r;
+  }
+  WikResult res{};
+  res.found = 0;
+  if (b.ord != LLONG_MAX) {
+    const int a = static_cast<int>(b.ord / ncj);
+    const int j = s.cj[b.ord - static_cast<long long>(a) * ncj];
+    double m;
+    int opt;
+    if (wik_eval(w, s.ci[a], j, &res.pose, &m, &opt)) {
+      res.found = 1;
+      res.i = s.ci[a].i;
+      res.j = j;
+      res.opt = opt;
+      res.metric = m;
+    }
+  }
+  *s.result = res;
+  *s.done = 0;
+}
+
+// ---------------------------------------------------------------------------
+// Single-pose operations (one thread): refinement and trail folding.
+
+__device__ inline int triangle_vertex(V3 a, V3 b, double la, double lb, V3 n, V3 hint, V3* out,
+                                      int* msg) {
+  const V3 ab = b - a;
+  const double c = rpd::norm(ab);
+  if (!(c <= (la + lb) * (1.0 + 1e-12))) { *msg = 1; return RP_E_UNREACHABLE_TARGET; }
+  if (!(c >= fabs(la - lb) * (1.0 - 1e-12) - 1e-15)) { *msg = 2; return RP_E_UNREACHABLE_TARGET; }
+  const V3 c_hat = ab / c;
+  V3 m_hat = rpd::cross(n, c_hat);
+  const double m_norm = rpd::norm(m_hat);
+  if (!(m_norm > 1e-12)) { *msg = 3; return RP_E_DEGENERATE_INPUT; }
+  m_hat = m_hat / m_norm;
+  const double along = (c * c + la * la - lb * lb) / (2.0 * c);
+  const double h2 = la * la - along * along;
+  const double h = sqrt(h2 > 0.0 ? h2 : 0.0);
+  const V3 base = a + along * c_hat;
+  const V3 pp = base + h * m_hat;
+  const V3 pm = base - h * m_hat;
+  *out = rpd::sqnorm(pp - hint) <= rpd::sqnorm(pm - hint) ? pp : pm;
+  return 0;
+}
+
+__device__ inline V3 plane_normal_for_refine(const DevPose& p, V3 anchor, V3 target, int sa, int sb) {
+  V3 n = rpd::cross(p.seg[sa], p.seg[sb]);
+  if (rpd::norm(n) > 1e-12 * rpd::norm(p.seg[sa]) * rpd::norm(p.seg[sb])) return rpd::normalized(n);
+  n = rpd::cross(target - anchor, p.joints[sa + 1] - anchor);
+  if (rpd::norm(n) > 1e-12) return rpd::normalized(n);
+  const V3 chord = rpd::normalized(target - anchor);
+  const V3 seed = fabs(chord.z) < 0.9 ? V3{0, 0, 1} : V3{1, 0, 0};
+  return rpd::normalized(rpd::cross(chord, seed));
+}
+
+/// mode 0: exact_refine_8dof, 1: _8dof_triangle, 2: exact_refine_6dof
+/// (src/arm_model.cpp:258-324).
+__global__ void k_refine(ArmDev arm, DevPose ap, V3 target, int mode, PoseOpOut* out) {
+  PoseOpOut r{};
+  r.pose = ap;
+  if (mode == 2) {
+    if (ap.nseg < 3) { r.status = RP_E_INVALID_PARAMETER; r.msg = 4; *out = r; return; }
+    if (arm.off[1] != 0.0 || arm.off[2] != 0.0) { r.status = RP_E_INVALID_PARAMETER; r.msg = 5; *out = r; return; }
+    const V3 p1 = ap.joints[1];
+    const V3 n = plane_normal_for_refine(ap, p1, target, 1, 2);
+    V3 p2;
+    r.status = triangle_vertex(p1, target, arm.L[1], arm.L[2], n, ap.joints[2], &p2, &r.msg);
+    if (!r.status) {
+      r.pose.seg[1] = p2 - p1;
+      r.pose.seg[2] = target - p2;
+      r.pose.joints[2] = p2;
+      r.pose.joints[3] = target;
+      r.pose.qidx[1] = -1;
+      r.pose.qidx[2] = -1;
+    }
+  } else {
+    if (ap.nseg != 4) { r.status = RP_E_INVALID_PARAMETER; r.msg = 6; *out = r; return; }
+    if (arm.off[2] != 0.0 || arm.off[3] != 0.0) { r.status = RP_E_INVALID_PARAMETER; r.msg = 7; *out = r; return; }
+    if (mode == 0) {
+      const V3 v3 = ap.seg[2];
+      const double v3_len = rpd::norm(v3);
+      if (!(v3_len >= 1e-9)) { r.status = RP_E_DEGENERATE_INPUT; r.msg = 8; *out = r; return; }
+      const V3 p2 = ap.joints[2];
+      const V3 d3 = target - p2;
+      const V3 s3 = v3 * (arm.L[2] / v3_len);
+      const V3 s4 = d3 - s3;
+      r.pose.seg[2] = s3;
+      r.pose.seg[3] = s4;
+      r.pose.joints[3] = p2 + s3;
+      r.pose.joints[4] = r.pose.joints[3] + s4;
+      r.pose.s4dev = fabs(rpd::norm(s4) - arm.L[3]);
+    } else {
+      const V3 p2 = ap.joints[2];
+      const V3 n = plane_normal_for_refine(ap, p2, target, 2, 3);
+      V3 p3;
+      r.status = triangle_vertex(p2, target, arm.L[2], arm.L[3], n, ap.joints[3], &p3, &r.msg);
+      if (!r.status) {
+        r.pose.seg[2] = p3 - p2;
+        r.pose.seg[3] = target - p3;
+        r.pose.joints[3] = p3;
+        r.pose.joints[4] = target;
+        r.pose.s4dev = fabs(rpd::norm(r.pose.seg[3]) - arm.L[3]);
+      }
+    }
+    r.pose.qidx[2] = -1;
+    r.pose.qidx[3] = -1;
+  }
+  *out = r;
+}
+
+/// append_trail on a 3-segment chain (src/path_planner.cpp:127-150).
+__global__ void k_append_trail(rpd::GridView g, ArmDev arm, DevPose ch, int n_opts, V3 o0, V3 o1,
+                               int n, PoseOpOut* out) {
+  PoseOpOut r{};
+  r.status = RP_E_NO_PATH;
+  const V3 opts[2] = {o0, o1};
+  for (int o = 0; o <= n_opts; ++o) {
+    const V3 dir = o < n_opts ? opts[o] : rpd::normalized(ch.seg[2]);
+    DevPose cand = ch;
+    cand.nseg = 4;
+    cand.seg[3] = arm.L[3] * dir;
+    cand.qidx[3] = -1;
+    build_chain(arm, cand);
+    if (!pose_limits_ok(arm, cand)) continue;
+    if (!rpd::walk_clear(g, cand.joints[3], cand.joints[4], n)) continue;
+    if (!pose_self_free(cand, 2.0 * arm.arm_radius)) continue;
+    r.status = 0;
+    r.pose = cand;
+    break;
+  }
+  *out = r;
+}
+
+// ---------------------------------------------------------------------------
+// Unfold (src/path_planner.cpp:405-484)
+
+/// smoothness_ok over consecutive poses of the sequence, relax 1.
+__global__ void k_seq_smooth(const DevPose* __restrict__ seq, int count, double sm1, double sm2,
+                             int* __restrict__ rough) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s + 1 >= count) return;
+  const DevPose& a = seq[s];
+  const DevPose& b = seq[s + 1];
+  if (!(rpd::norm(b.joints[1] - a.joints[1]) <= sm1 && rpd::norm(b.joints[2] - a.joints[2]) <= sm2))
+    atomicExch(rough, 1);
+}
+
+/// pose_clear / pose_valid for a batch (replan collide scan).
+__global__ void k_pose_check(rpd::GridView g, ArmDev arm, const DevPose* __restrict__ poses, int count,
+                             int n, double spacing, int full, int* __restrict__ first_bad) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  const bool ok = full ? pose_valid(g, arm, poses[k], n, spacing)
+                       : pose_clear(g, poses[k], n, spacing);
+  if (!ok) atomicMin(first_bad, k);
+}
+
+// ---------------------------------------------------------------------------
+// mean_polyline_deviation (src/path_planner.cpp:76-87) over solution tip paths.
+
+__device__ inline double polyline_dist(V3 p, const V3* poly, int np) {
+  double best = rpd::norm(p - poly[0]);
+  for (int i = 0; i + 1 < np; ++i) {
+    const double d = rpd::point_to_segment(p, poly[i], poly[i + 1]);
+    best = d < best ? d : best;  // std::min(best, d)
+  }
+  return best;
+}
+
+/// Scores every solution of a set: tip path = [lead?] + the first 3 sample
+/// blocks of the pose (candidate_tip_path / the replan tip list).
+__global__ void k_score_solutions(SolveDev a, const SurvDev* __restrict__ sv,
+                                  const long long* __restrict__ keys, int64_t count,
+                                  const V3* __restrict__ poly, int npoly, int has_lead, V3 lead,
+                                  unsigned long long* __restrict__ dev_bits,
+                                  long long* __restrict__ ordinal, long long ord_base) {
+  extern __shared__ V3 spoly[];
+  for (int k = threadIdx.x; k < npoly; k += blockDim.x) spoly[k] = poly[k];
+  __syncthreads();
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  const long long key = keys[t];
+  const long long p = key / a.B;
+  const int bi = static_cast<int>(key - p * a.B);
+  const int s = static_cast<int>(p / a.Q);
+  const int j = static_cast<int>(p - static_cast<long long>(s) * a.Q);
+  const SurvDev h = sv[s];
+  const ArmDev& arm = a.arm;
+  const V3 dir2 = qvec(a, j);
+  V3 link2 = h.p1;
+  if (arm.off[1] > 0.0) {
+    const rpd::FrameStep st2 = rpd::advance_frame(h.frame, dir2);
+    link2 = h.p1 + arm.off[1] * rpd::m_col(st2.after_azimuth, 0);
+  }
+  const V3 p2 = link2 + arm.L[1] * dir2;
+  const V3 from[3] = {h.link_start, link2, p2};
+  const V3 to[3] = {h.p1, p2, a.bpts[bi]};
+  double acc = 0.0;
+  int cnt = 0;
+  if (has_lead) {
+    acc += polyline_dist(lead, spoly, npoly);
+    ++cnt;
+  }
+  for (int l = 0; l < 3; ++l) {
+    const V3 diff = to[l] - from[l];
+    for (int k = 1; k <= a.n; ++k) {
+      acc += polyline_dist(rpd::walk_sample(from[l], diff, k, a.n), spoly, npoly);
+      ++cnt;
+    }
+  }
+  const double dev = acc / static_cast<double>(cnt);
+  dev_bits[t] = __double_as_longlong(dev);
+  ordinal[t] = ord_base + t;
+}
+
+/// Scores explicit point lists (shortcut tip paths).
+__global__ void k_score_lists(const V3* __restrict__ pts, const int* __restrict__ offs, int count,
+                              const V3* __restrict__ poly, int npoly,
+                              unsigned long long* __restrict__ dev_bits, long long* __restrict__ ordinal) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  double acc = 0.0;
+  const int b = offs[t], e = offs[t + 1];
+  for (int k = b; k < e; ++k) acc += polyline_dist(pts[k], poly, npoly);
+  dev_bits[t] = __double_as_longlong(acc / static_cast<double>(e - b));
+  ordinal[t] = t;
+}
+
+/// mean_polyline_deviation of one point list: block-parallel over points,
+/// summed in the reference's sequential order by thread 0.
+__global__ void k_mean_dev(const V3* __restrict__ pts, int npts, const V3* __restrict__ poly,
+                           int npoly, double* __restrict__ scratch, double* out) {
+  for (int k = threadIdx.x; k < npts; k += blockDim.x) scratch[k] = polyline_dist(pts[k], poly, npoly);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int k = 0; k < npts; ++k) acc += scratch[k];
+    *out = acc / static_cast<double>(npts);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host wrappers
+
+/// folded_pose with glibc sin/cos (bit-identical to the reference's).
+HostPose folded_pose_host(rp_ctx* ctx, const rp_arm& arm) {
+  (void)ctx;
+  const DevPose h = folded_pose(
+      make_arm_dev(arm),
+      V3{arm.fold_plane_normal[0], arm.fold_plane_normal[1], arm.fold_plane_normal[2]},
+      arm.fold_flex);
+  return host_pose_from_dev(h);
+}
+
+double mean_polyline_deviation(rp_ctx* ctx, const std::vector<V3>& pts, const std::vector<V3>& poly) {
+  require(!pts.empty() && !poly.empty(), RP_E_INVALID_PARAMETER, "empty polyline");
+  DevBuf<V3> dp(pts.size(), ctx->stream), dq(poly.size(), ctx->stream);
+  DevBuf<double> sc(pts.size(), ctx->stream), o(1, ctx->stream);
+  copy_to_device(ctx, dp.p, pts.data(), pts.size() * sizeof(V3));
+  copy_to_device(ctx, dq.p, poly.data(), poly.size() * sizeof(V3));
+  launch(ctx, "score", k_mean_dev, dim3(1), dim3(256), 0, static_cast<const V3*>(dp.p),
+         static_cast<int>(pts.size()), static_cast<const V3*>(dq.p), static_cast<int>(poly.size()),
+         sc.p, o.p);
+  double h = 0.0;
+  copy_to_host(ctx, &h, o.p, sizeof(h));
+  return h;
+}
+
+static const char* refine_msg(int m) {
+  switch (m) {
+    case 1: return "target beyond combined segment lengths";
+    case 2: return "target inside the unreachable inner sphere";
+    case 3: return "solution plane normal parallel to chord";
+    case 4: return "need a 3-segment pose";
+    case 5: return "triangle refinement requires coaxial joints 2 and 3";
+    case 6: return "need a 4-segment pose";
+    case 7: return "8DOF refinement requires coaxial joints 3 and 4";
+    case 8: return "gap vector is numerically zero";
+  }
+  return "refinement failed";
+}
+
+DevPose to_dev(const HostPose& h) {
+  DevPose d{};
+  d.nseg = h.nseg;
+  d.has_elbows = h.has_elbows ? 1 : 0;
+  for (int k = 0; k < 4; ++k) d.qidx[k] = k < h.nseg ? h.qidx[k] : -1;
+  for (int k = 0; k < h.nseg; ++k) {
+    d.seg[k] = h.seg[k];
+    d.elbows[k] = h.elbows[k];
+  }
+  for (int k = 0; k <= h.nseg; ++k) d.joints[k] = h.joints[k];
+  d.s4dev = h.s4dev;
+  d.n_wp_links = 0;
+  return d;
+}
+
+Planner::Planner(rp_ctx* c, const rp_arm& a, const rp_quiver* qv, const rp_grid* gr,
+                 const rp_reach_params& r, const rp_path_params& p)
+    : ctx(c), arm(a), q(qv), g(gr), rp(r) {
+  ad = make_arm_dev(a);
+  pp = resolve_path_params(p, a, r);
+  n = r.n_samples;
+  spacing = nominal_spacing(a, r);
+  cudaStream_t st = ctx->stream;
+  const int qw = (q->n + 31) / 32 + 1;
+  ibits.alloc(qw, st);
+  jbits.alloc(qw, st);
+  cj.alloc(q->n + 1, st);
+  ci.alloc(q->n + 1, st);
+  counts.alloc(2, st);
+  wik_blocks = ctx->sm_count * 2;
+  block_best.alloc(wik_blocks, st);
+  done.alloc(1, st);
+  done.zero();
+  result.alloc(1, st);
+  opout.alloc(1, st);
+  RP_CUDA(cudaMallocHost(&h_result, sizeof(WikResult)));
+}
+
+Planner::~Planner() {
+  if (h_result) cudaFreeHost(h_result);
+}
+
+bool Planner::waypoint_ik(V3 wp, const HostPose& prev, double relax, const Trail& tr,
+                          const HostPose* bias, HostPose* out) {
+  WikDev w{};
+  w.g = g->view();
+  w.arm = ad;
+  w.n = n;
+  w.Q = q->n;
+  w.qx = q->d_soa;
+  w.qy = q->d_soa + q->n;
+  w.qz = q->d_soa + 2 * static_cast<size_t>(q->n);
+  w.spacing = spacing;
+  w.wp = wp;
+  w.prev_j1 = prev.joints[1];
+  w.prev_j2 = prev.joints[2];
+  w.eps = pp.eps_wp * relax + 1e-12;
+  w.j1max = pp.j1 * relax + 1e-12;
+  w.j2max = pp.j2 * relax + 1e-12;
+  w.sm1 = pp.j1 * relax + 1e-12;
+  w.sm2 = pp.j2 * relax + 1e-12;
+  w.has_bias = bias ? 1 : 0;
+  if (bias) {
+    w.bias_j1 = bias->joints[1];
+    w.bias_j2 = bias->joints[2];
+  }
+  w.four = arm.n_segments == 4;
+  w.n_opts = 0;
+  if (tr.has_back) w.opt_dir[w.n_opts++] = tr.back;
+  if (tr.has_fwd) w.opt_dir[w.n_opts++] = tr.fwd;
+  w.L4 = arm.n_segments == 4 ? arm.lengths[3] : 0.0;
+  const rpd::Limit& l2 = ad.lim[1];
+  const rpd::Limit& l3 = ad.lim[2];
+  w.cond2 = (ad.off[1] > 0.0 || !rpd::full_azimuth(l2) || l2.elev_min > 0.0 || l2.elev_max < kPi);
+  w.cond3 = (!rpd::full_azimuth(l3) || l3.elev_min > 0.0 || l3.elev_max < kPi);
+  // candidate cones (src/path_planner.cpp:184-194); none for offset arms
+  w.filter_j = ad.has_offsets ? 0 : 1;
+  double cone1 = 0, cone2 = 0;
+  V3 u1{0, 0, 1}, u2{0, 0, 1};
+  if (w.filter_j) {
+    auto chord_to_angle = [](double chord) {
+      return 2.0 * std::asin(std::clamp(chord / 2.0, 0.0, 1.0));
+    };
+    const double ang1 = chord_to_angle(w.j1max / arm.lengths[0]) + 1e-9;
+    const double ang2 = chord_to_angle((w.j1max + w.j2max) / arm.lengths[1]) + 1e-9;
+    u1 = rpd::normalized(prev.seg[0]);
+    u2 = rpd::normalized(prev.seg[1]);
+    require(std::abs(rpd::norm(u1) - 1.0) <= 1e-9 && std::abs(rpd::norm(u2) - 1.0) <= 1e-9,
+            RP_E_INVALID_PARAMETER, "cone axis must be unit");
+    cone1 = std::min(kPi, ang1) + 1e-12;
+    cone2 = std::min(kPi, ang2) + 1e-12;
+  }
+  WikScratch s{ibits.p, jbits.p, cj.p, ci.p, counts.p, block_best.p, done.p, result.p, wik_blocks};
+  launch(ctx, "wik_filter", k_wik_filter, dim3(nblk(q->n, 256)), dim3(256), 0, w, cone1, cone2, u1,
+         u2, ibits.p, jbits.p);
+  launch(ctx, "wik_compact", k_wik_compact, dim3(1), dim3(1024), 0, w, s);
+  launch(ctx, "wik_pairs", k_wik_pairs, dim3(wik_blocks), dim3(256), 0, w, s);
+  RP_CUDA(cudaMemcpyAsync(h_result, result.p, sizeof(WikResult), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  RP_CUDA(cudaStreamSynchronize(ctx->stream));
+  ++wik_calls;
+  if (!h_result->found) return false;
+  *out = host_pose_from_dev(h_result->pose);
+  return true;
+}
+
+PoseOpOut run_pose_op(Planner& P) {
+  PoseOpOut h;
+  copy_to_host(P.ctx, &h, P.opout.p, sizeof(PoseOpOut));
+  return h;
+}
+
+HostPose Planner::refine(const HostPose& approx, V3 target, int mode) {
+  launch(ctx, "refine", k_refine, dim3(1), dim3(1), 0, ad, to_dev(approx), target, mode,
+         opout.p);
+  PoseOpOut r = run_pose_op(*this);
+  if (r.status) fail(r.status, refine_msg(r.msg));
+  HostPose h = host_pose_from_dev(r.pose);
+  h.waypoints = approx.waypoints;  // PoseChain out = approx
+  return h;
+}
+
+bool Planner::append_trail(const HostPose& chain3, const Trail& tr, HostPose* out) {
+  V3 o[2] = {V3{0, 0, 0}, V3{0, 0, 0}};
+  int no = 0;
+  if (tr.has_back) o[no++] = tr.back;
+  if (tr.has_fwd) o[no++] = tr.fwd;
+  launch(ctx, "trail", k_append_trail, dim3(1), dim3(1), 0, g->view(), ad, to_dev(chain3), no, o[0],
+         o[1], n, opout.p);
+  PoseOpOut r = run_pose_op(*this);
+  if (r.status) return false;
+  HostPose h = host_pose_from_dev(r.pose);
+  h.waypoints = chain3.waypoints;
+  const V3 diff = h.joints[4] - h.joints[3];
+  for (int k = 1; k <= n; ++k) h.waypoints.push_back(rpd::walk_sample(h.joints[3], diff, k, n));
+  *out = h;
+  return true;
+}
+
+std::optional<std::vector<HostPose>> Planner::interpolate(const HostPose* from_or_null,
+                                                          const HostPose& to, int base_steps,
+                                                          bool* rotated_valid) {
+  // The joint-space interpolation is evaluated with the host's glibc
+  // transcendentals, exactly as the reference does: the folded zig-zag puts
+  // azimuths at +-pi, so the direction of wrap_angle(qb - qa) -- and with it
+  // every interpolated pose -- is decided by the sign of last-ulp noise in
+  // sin/atan2 (CUDA's libm differs in the last ulp). The device does the
+  // bulk of the work: collision / limit / self-collision validity of every
+  // pose and the smoothness of every consecutive pair.
+  cudaStream_t st = ctx->stream;
+  HostPose from;
+  DevPose dfrom;
+  if (from_or_null) {
+    from = *from_or_null;
+    dfrom = to_dev(from);
+  } else {
+    // build_unfold (src/path_planner.cpp:458-484): rotate the folded pose so
+    // its first segment and fold plane co-align with the triangle pose.
+    const V3 fn{arm.fold_plane_normal[0], arm.fold_plane_normal[1], arm.fold_plane_normal[2]};
+    const DevPose fold = folded_pose(ad, fn, arm.fold_flex);
+    const DevPose tri = to_dev(to);
+    const V3 u1f = rpd::normalized(fold.seg[0]);
+    const V3 u1t = rpd::normalized(tri.seg[0]);
+    const V3 nf = pose_plane_normal(fold);
+    const V3 nt = pose_plane_normal(tri);
+    rpd::M3 a, b;
+    const V3 ca[3] = {u1f, rpd::cross(nf, u1f), nf};
+    const V3 cb[3] = {u1t, rpd::cross(nt, u1t), nt};
+    for (int c = 0; c < 3; ++c) {
+      a.a[0][c] = ca[c].x; a.a[1][c] = ca[c].y; a.a[2][c] = ca[c].z;
+      b.a[0][c] = cb[c].x; b.a[1][c] = cb[c].y; b.a[2][c] = cb[c].z;
+    }
+    const rpd::M3 rot = rpd::m_mul(b, m_transpose(a));
+    dfrom = DevPose{};
+    dfrom.nseg = fold.nseg;
+    for (int k = 0; k < fold.nseg; ++k) {
+      dfrom.seg[k] = m_vec(rot, fold.seg[k]);
+      dfrom.qidx[k] = -1;
+    }
+    build_chain(ad, dfrom);
+    from = host_pose_from_dev(dfrom);
+    from.waypoints.clear();
+    const bool ok = valid_poses(&dfrom, 1) < 0;
+    if (rotated_valid) *rotated_valid = ok;
+    if (!ok) return std::nullopt;
+  }
+  double qa_az[4], qa_el[4], qb_az[4], qb_el[4];
+  if (!to_angles(ad, dfrom, qa_az, qa_el) || !to_angles(ad, to_dev(to), qb_az, qb_el))
+    fail(RP_E_DEGENERATE_INPUT, "zero-length segment");
+  for (int steps = std::max(1, base_steps); steps <= 4096; steps *= 2) {
+    std::vector<DevPose> seq(steps + 1);
+    seq[0] = dfrom;
+    seq[steps] = to_dev(to);
+    for (int s = 1; s < steps; ++s) {
+      const double t = static_cast<double>(s) / steps;
+      double az[4], el[4];
+      for (int j = 0; j < ad.nseg; ++j) {
+        az[j] = qa_az[j] + t * rpd::wrap_angle(qb_az[j] - qa_az[j]);
+        el[j] = qa_el[j] + t * (qb_el[j] - qa_el[j]);
+      }
+      seq[s] = from_angles(ad, az, el);
+    }
+    DevBuf<DevPose> dseq(steps + 1, st);
+    DevBuf<int> flags(2, st);
+    flags.zero();
+    const int init = INT_MAX;
+    copy_to_device(ctx, flags.p, &init, sizeof(int));
+    copy_to_device(ctx, dseq.p, seq.data(), (steps + 1) * sizeof(DevPose));
+    if (steps > 1)
+      launch(ctx, "unfold", k_pose_check, dim3(nblk(steps - 1, 64)), dim3(64), 0, g->view(), ad,
+             static_cast<const DevPose*>(dseq.p + 1), steps - 1, n, spacing, 1, flags.p);
+    launch(ctx, "unfold", k_seq_smooth, dim3(nblk(steps, 128)), dim3(128), 0,
+           static_cast<const DevPose*>(dseq.p), steps + 1, pp.j1 * 1.0 + 1e-12,
+           pp.j2 * 1.0 + 1e-12, flags.p + 1);
+    int hf[2];
+    copy_to_host(ctx, hf, flags.p, sizeof(hf));
+    if (hf[0] != INT_MAX) return std::nullopt;
+    if (!hf[1]) {
+      std::vector<HostPose> out;
+      out.push_back(from);
+      for (int s = 1; s < steps; ++s) {
+        HostPose h = host_pose_from_dev(seq[s]);
+        h.waypoints.clear();
+        out.push_back(h);
+      }
+      out.push_back(to);
+      return out;
+    }
+  }
+  return std::nullopt;
+}
+
+int Planner::first_colliding(const std::vector<HostPose>& poses, const rp_grid* grid) {
+  if (poses.empty()) return -1;
+  cudaStream_t st = ctx->stream;
+  std::vector<DevPose> d(poses.size());
+  for (size_t k = 0; k < poses.size(); ++k) d[k] = to_dev(poses[k]);
+  DevBuf<DevPose> dp(d.size(), st);
+  copy_to_device(ctx, dp.p, d.data(), d.size() * sizeof(DevPose));
+  DevBuf<int> first(1, st);
+  const int init = INT_MAX;
+  copy_to_device(ctx, first.p, &init, sizeof(int));
+  launch(ctx, "pose_check", k_pose_check, dim3(nblk(static_cast<int64_t>(d.size()), 64)), dim3(64),
+         0, grid->view(), ad, static_cast<const DevPose*>(dp.p), static_cast<int>(d.size()), n,
+         spacing, 0, first.p);
+  int h = INT_MAX;
+  copy_to_host(ctx, &h, first.p, sizeof(int));
+  return h == INT_MAX ? -1 : h;
+}
+
+int Planner::valid_poses(const DevPose* poses, int count) {
+  cudaStream_t st = ctx->stream;
+  DevBuf<DevPose> dp(count, st);
+  copy_to_device(ctx, dp.p, poses, count * sizeof(DevPose));
+  DevBuf<int> first(1, st);
+  const int init = INT_MAX;
+  copy_to_device(ctx, first.p, &init, sizeof(int));
+  launch(ctx, "pose_check", k_pose_check, dim3(nblk(count, 64)), dim3(64), 0, g->view(), ad,
+         static_cast<const DevPose*>(dp.p), count, n, spacing, 1, first.p);
+  int h = INT_MAX;
+  copy_to_host(ctx, &h, first.p, sizeof(int));
+  return h == INT_MAX ? -1 : h;
+}
+
+/// Scores of (shortcut tip lists, solutions) against a polyline, sorted by
+/// (deviation, ordinal); returns the ordinals in sorted order.
+std::vector<long long> Planner::rank_by_deviation(rp_solution_set* set,
+                                                  const std::vector<std::vector<V3>>& lists,
+                                                  const std::vector<V3>& poly, bool lead,
+                                                  V3 lead_pt, int64_t* total_out,
+                                                  std::vector<long long>* tail, int head_n,
+                                                  int tail_n) {
+  cudaStream_t st = ctx->stream;
+  const int64_t ns = static_cast<int64_t>(lists.size());
+  const int64_t nsol = set ? set->n_solutions : 0;
+  const int64_t total = ns + nsol;
+  *total_out = total;
+  std::vector<long long> head;
+  if (total == 0) return head;
+  DevBuf<unsigned long long> dev(total, st), dev_sorted(total, st);
+  DevBuf<long long> ord(total, st), ord_sorted(total, st);
+  DevBuf<V3> dpoly(poly.size(), st);
+  copy_to_device(ctx, dpoly.p, poly.data(), poly.size() * sizeof(V3));
+  if (ns > 0) {
+    std::vector<V3> pts;
+    std::vector<int> offs{0};
+    for (const auto& l : lists) {
+      pts.insert(pts.end(), l.begin(), l.end());
+      offs.push_back(static_cast<int>(pts.size()));
+    }
+    DevBuf<V3> dpts(pts.size() + 1, st);
+    DevBuf<int> doffs(offs.size(), st);
+    copy_to_device(ctx, dpts.p, pts.data(), pts.size() * sizeof(V3));
+    copy_to_device(ctx, doffs.p, offs.data(), offs.size() * sizeof(int));
+    launch(ctx, "score", k_score_lists, dim3(nblk(ns, 128)), dim3(128), 0,
+           static_cast<const V3*>(dpts.p), static_cast<const int*>(doffs.p), static_cast<int>(ns),
+           static_cast<const V3*>(dpoly.p), static_cast<int>(poly.size()), dev.p, ord.p);
+  }
+  if (nsol > 0) {
+    ensure_keys(set);
+    launch(ctx, "score", k_score_solutions, dim3(nblk(nsol, 256)), dim3(256),
+           poly.size() * sizeof(V3), set->sd, static_cast<const SurvDev*>(set->surv.p),
+           static_cast<const long long*>(set->keys.p), nsol, static_cast<const V3*>(dpoly.p),
+           static_cast<int>(poly.size()), lead ? 1 : 0, lead_pt, dev.p + ns, ord.p + ns,
+           static_cast<long long>(ns));
+  }
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, dev.p, dev_sorted.p, ord.p, ord_sorted.p,
+                                  static_cast<int>(total), 0, 64, st);
+  DevBuf<unsigned char> tmp(tb, st);
+  RP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, dev.p, dev_sorted.p, ord.p, ord_sorted.p,
+                                          static_cast<int>(total), 0, 64, st));
+  const int64_t nh = std::min<int64_t>(head_n, total);
+  head.resize(nh);
+  copy_to_host(ctx, head.data(), ord_sorted.p, nh * sizeof(long long));
+  if (tail) {
+    const int64_t nt = std::min<int64_t>(tail_n, total);
+    tail->resize(nt);
+    copy_to_host(ctx, tail->data(), ord_sorted.p + (total - nt), nt * sizeof(long long));
+  }
+  return head;
+}
+
+}  // namespace rp
+
+using namespace rp;
+
+extern "C" rp_status rp_exact_refine(rp_ctx* ctx, const rp_arm* arm, const rp_pose* approx,
+                                     const double target[3], int32_t variant, rp_pose* out) {
+  return guarded([&] {
+    HostPose a = from_abi(*approx, nullptr);
+    const ArmDev ad = make_arm_dev(*arm);
+    const int mode = a.nseg == 4 ? (variant == 1 ? 1 : 0) : 2;
+    DevBuf<PoseOpOut> o(1, ctx->stream);
+    launch(ctx, "refine", k_refine, dim3(1), dim3(1), 0, ad, to_dev(a),
+           V3{target[0], target[1], target[2]}, mode, o.p);
+    PoseOpOut r;
+    copy_to_host(ctx, &r, o.p, sizeof(r));
+    if (r.status) fail(r.status, refine_msg(r.msg));
+    to_abi(host_pose_from_dev(r.pose), out, nullptr, 0);
+  });
+}

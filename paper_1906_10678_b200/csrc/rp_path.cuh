@@ -1,0 +1,103 @@
+// Path-planner device structures (src/path_planner.cpp).
+#pragma once
+
+#include "rp_reach.cuh"
+
+namespace rp {
+
+/// Resolved PathParams (src/path_planner.cpp:89-102).
+struct PP {
+  double eps_wp, d_w, slack, j1, j2;
+  std::vector<double> relax;
+  int unfold_steps;
+};
+PP resolve_path_params(const rp_path_params& pp, const rp_arm& arm, const rp_reach_params& rp);
+
+/// One waypoint_ik call (src/path_planner.cpp:167-291), passed by value.
+struct WikDev {
+  rpd::GridView g;
+  ArmDev arm;
+  int n, Q;
+  const double* qx;
+  const double* qy;
+  const double* qz;
+  double spacing;
+  V3 wp;
+  V3 prev_j1, prev_j2, prev_s2dir;
+  double prev_s2len;
+  double eps, j1max, j2max;  // relaxed, + 1e-12 as the reference
+  double sm1, sm2;           // smoothness bounds (same values)
+  int has_bias;
+  V3 bias_j1, bias_j2;
+  int four;
+  int n_opts;
+  V3 opt_dir[2];
+  double L4;
+  int filter_j;  // conservative cone filter for segment 2 (coaxial arms)
+  int cond2, cond3;
+  double jbound;
+};
+
+struct CiData {
+  int i;
+  int ok;  // walk1 (and offset link) clear
+  double move1;
+  V3 p1, link1;
+  rpd::M3 frame1;
+};
+
+struct WikBest {
+  double metric;
+  long long ord;
+  int opt;
+};
+
+struct WikResult {
+  int found;
+  int i, j, opt;
+  double metric;
+  DevPose pose;
+};
+
+/// Result of a single-pose device operation (refinement, trail folding).
+struct PoseOpOut {
+  int status;  // 0 ok, else rp_status
+  int msg;
+  DevPose pose;
+};
+
+/// Device scratch reused by every waypoint_ik call of a planner.
+struct WikScratch {
+  uint32_t* ibits;
+  uint32_t* jbits;
+  int* cj;
+  CiData* ci;
+  int* counts;  // [n_ci, n_cj]
+  WikBest* block_best;
+  unsigned* done;
+  WikResult* result;
+  int max_blocks;
+};
+
+}  // namespace rp
+
+struct rp_plan {
+  std::string kind;
+  std::vector<rp::V3> waypoints;
+  std::vector<rp::HostPose> poses;
+  std::vector<rp::HostPose> unfold;
+  std::vector<double> relax;
+  std::vector<std::string> notes;
+  int switch_index = -1;
+
+  /// PathPlan::full_sequence (src/path_planner.cpp:104-112)
+  std::vector<const rp::HostPose*> full_sequence() const {
+    std::vector<const rp::HostPose*> s;
+    for (const auto& p : unfold) s.push_back(&p);
+    for (size_t k = 0; k < poses.size(); ++k) {
+      if (k == 0 && !unfold.empty()) continue;
+      s.push_back(&poses[k]);
+    }
+    return s;
+  }
+};

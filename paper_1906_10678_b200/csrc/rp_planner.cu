@@ -1,0 +1,914 @@
+// Path planner control flow (src/path_planner.cpp) on top of the device
+// searches: the sequential backward pass, candidate builds, the fallback
+// cascade, arbitrary-pose planning and the dynamic re-plan. Every geometric
+// search (waypoint IK, solve_reach, unfold validity, deviation scoring,
+// collide scans) runs on the GPU; the host only sequences them.
+#include "rp_planner.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+
+namespace rp {
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;
+
+V3 tracked_point(const HostPose& p) { return p.joints[std::min(3, p.nseg)]; }
+
+double total_length(const rp_arm& a) {
+  double t = 0.0;
+  for (int k = 0; k < a.n_segments; ++k) t += a.lengths[k];
+  return t;
+}
+
+bool smoothness_ok(const HostPose& prev, const HostPose& cand, const PP& pp, double relax) {
+  const double d1 = rpd::norm(cand.joints[1] - prev.joints[1]);
+  const double d2 = rpd::norm(cand.joints[2] - prev.joints[2]);
+  return d1 <= pp.j1 * relax + 1e-12 && d2 <= pp.j2 * relax + 1e-12;
+}
+
+V3 perpendicular_of(V3 dir) {
+  const V3 seed = std::abs(dir.z) < 0.9 ? V3{0, 0, 1} : V3{1, 0, 0};
+  return rpd::normalized(rpd::cross(dir, seed));
+}
+
+Trail trail_context(const std::vector<V3>& wps, size_t k) {
+  Trail t;
+  if (k > 0) {
+    const V3 d = wps[k - 1] - wps[k];
+    if (rpd::norm(d) > 1e-12) {
+      t.has_back = true;
+      t.back = rpd::normalized(d);
+    }
+  }
+  if (k + 1 < wps.size()) {
+    const V3 d = wps[k + 1] - wps[k];
+    if (rpd::norm(d) > 1e-12) {
+      t.has_fwd = true;
+      t.fwd = rpd::normalized(d);
+    }
+  }
+  return t;
+}
+
+std::vector<double> with_unit_first(const std::vector<double>& s) {
+  std::vector<double> f{1.0};
+  f.insert(f.end(), s.begin(), s.end());
+  return f;
+}
+
+/// A reach candidate (ChosenPath) carried through the planner.
+struct Cand {
+  int kind = RP_CHOSEN_REACH_POSE;
+  int64_t ordinal = -1;  // in its solution set (reach) or shortcut list
+  HostPose pose;         // unrefined solution pose with its 4n waypoints
+  HostShortcut sc;
+};
+
+struct PassOptions {
+  std::vector<double> factors{1.0};
+  bool cloud = false;
+  double cloud_radius = 0.0;
+  const HostPose* fixed_first = nullptr;
+  const HostPose* junction_bias = nullptr;
+};
+
+struct PassResult {
+  bool ok = false;
+  int failed_index = -1;
+  std::vector<HostPose> poses;
+  std::vector<double> relax;
+  std::vector<V3> waypoints;
+  std::vector<std::string> notes;
+};
+
+struct Failure {
+  Cand candidate;
+  std::vector<V3> waypoints;
+  int blocked_index = -1;
+  std::string reason;
+};
+
+/// backward_pass (src/path_planner.cpp:322-400)
+PassResult backward_pass(Planner& P, const std::vector<V3>& waypoints, const HostPose& anchor,
+                         const PassOptions& opt) {
+  PassResult res;
+  const size_t m = waypoints.size();
+  res.poses.assign(m, HostPose{});
+  res.relax.assign(m, 1.0);
+  res.waypoints = waypoints;
+  res.poses[m - 1] = anchor;
+  for (size_t k = m - 1; k-- > 0;) {
+    const HostPose prev = res.poses[k + 1];
+    bool found = false;
+    if (k == 0 && opt.fixed_first) {
+      for (double f : opt.factors) {
+        if (smoothness_ok(prev, *opt.fixed_first, P.pp, f)) {
+          res.poses[0] = *opt.fixed_first;
+          res.relax[0] = f;
+          if (f > 1.0) res.notes.push_back("relaxed junction at waypoint 0");
+          found = true;
+          break;
+        }
+      }
+      if (!found) {
+        res.failed_index = 0;
+        return res;
+      }
+      continue;
+    }
+    const Trail trail = trail_context(res.waypoints, k);
+    const HostPose* bias = (opt.fixed_first && k == 1) ? opt.fixed_first : opt.junction_bias;
+    HostPose pose;
+    for (double f : opt.factors) {
+      if (P.waypoint_ik(res.waypoints[k], prev, f, trail, bias, &pose)) {
+        res.poses[k] = pose;
+        res.relax[k] = f;
+        if (f > 1.0)
+          res.notes.push_back("relaxed x" + std::to_string(f) + " at waypoint " + std::to_string(k));
+        found = true;
+        break;
+      }
+    }
+    if (!found && opt.cloud) {
+      V3 dir = res.waypoints[k + 1] - res.waypoints[k];
+      if (rpd::norm(dir) < 1e-12 && k > 0) dir = res.waypoints[k] - res.waypoints[k - 1];
+      if (rpd::norm(dir) < 1e-12) dir = V3{0, 0, 1};
+      dir = rpd::normalized(dir);
+      const V3 u = perpendicular_of(dir);
+      const V3 v = rpd::cross(dir, u);
+      for (int t = 0; t < 8 && !found; ++t) {
+        const double a = 2.0 * kPi * t / 8.0;
+        const V3 cp = res.waypoints[k] + opt.cloud_radius * (std::cos(a) * u + std::sin(a) * v);
+        for (double f : opt.factors) {
+          if (P.waypoint_ik(cp, prev, f, trail, bias, &pose)) {
+            res.poses[k] = pose;
+            res.relax[k] = f;
+            res.waypoints[k] = cp;
+            res.notes.push_back("cloud target at waypoint " + std::to_string(k));
+            found = true;
+            break;
+          }
+        }
+      }
+    }
+    if (!found) {
+      res.failed_index = static_cast<int>(k);
+      return res;
+    }
+  }
+  res.ok = true;
+  return res;
+}
+
+struct Build {
+  std::string kind;
+  std::vector<V3> waypoints;
+  HostPose anchor;
+  std::string fail_reason;
+  bool ok = false;
+};
+
+std::vector<HostPose> solution_poses(rp_solution_set* s, const std::vector<long long>& ordinals);
+
+/// make_candidate_build (src/path_planner.cpp:497-560)
+Build make_candidate_build(Planner& P, const Cand& cand, V3 target) {
+  Build out;
+  const int n = P.n;
+  try {
+    if (cand.kind == RP_CHOSEN_REACH_POSE) {
+      out.kind = "reach-pose";
+      const int traversal = std::min(3, cand.pose.nseg);
+      out.waypoints.push_back(P.ad.root);
+      out.waypoints.insert(out.waypoints.end(), cand.pose.waypoints.begin(),
+                           cand.pose.waypoints.begin() + traversal * n);
+      if (cand.pose.nseg == 4) {
+        out.anchor = P.refine(cand.pose, target, P.rp.refine_triangle_8dof ? 1 : 0);
+      } else {
+        HostPose refined = P.refine(cand.pose, target, 2);
+        if (P.arm.n_segments == 4) {
+          HostPose trailed;
+          if (!P.append_trail(refined, trail_context(out.waypoints, out.waypoints.size() - 1),
+                              &trailed)) {
+            out.fail_reason = "no valid fourth-segment fold at the final pose";
+            return out;
+          }
+          refined = trailed;
+        }
+        out.anchor = refined;
+      }
+    } else {
+      out.kind = "shortcut";
+      out.waypoints.push_back(P.ad.root);
+      const auto tips = cand.sc.tip_waypoints(target);
+      out.waypoints.insert(out.waypoints.end(), tips.begin(), tips.end());
+      rp_reach_params rp6 = P.rp;
+      rp6.mode = RP_MODE_6DOF;
+      rp6.near_target_radius = 0.0;
+      const V3 final_wp = out.waypoints.back();
+      std::unique_ptr<rp_solution_set> aset(solve_reach(P.ctx, P.arm, P.q, P.g, final_wp, rp6));
+      if (aset->n_solutions == 0) {
+        out.fail_reason = "no full pose at the shortcut endpoint";
+        return out;
+      }
+      const rp_chosen ch = select(aset.get());
+      if (ch.kind != RP_CHOSEN_REACH_POSE)
+        fail(RP_E_INVALID_PARAMETER, "need a 3-segment pose");  // refine of an empty pose
+      HostPose refined = P.refine(solution_poses(aset.get(), {ch.index})[0], final_wp, 2);
+      if (P.arm.n_segments == 4) {
+        HostPose trailed;
+        if (!P.append_trail(refined, trail_context(out.waypoints, out.waypoints.size() - 1),
+                            &trailed)) {
+          out.fail_reason = "no valid fourth-segment fold at the shortcut pose";
+          return out;
+        }
+        refined = trailed;
+      }
+      out.anchor = refined;
+    }
+  } catch (const Fail& e) {
+    if (e.code == RP_E_CUDA || e.code == RP_E_INTERNAL) throw;
+    out.fail_reason = e.msg;
+    return out;
+  }
+  out.ok = true;
+  return out;
+}
+
+rp_plan* assemble(PassResult&& pass, std::vector<HostPose>&& unfold, const std::string& kind) {
+  auto* p = new rp_plan();
+  p->waypoints = std::move(pass.waypoints);
+  p->poses = std::move(pass.poses);
+  p->unfold = std::move(unfold);
+  p->kind = kind;
+  p->relax = std::move(pass.relax);
+  p->notes = std::move(pass.notes);
+  return p;
+}
+
+struct Attempt {
+  rp_plan* plan = nullptr;
+  Failure failure;
+};
+
+/// attempt_candidate (src/path_planner.cpp:580-602)
+Attempt attempt_candidate(Planner& P, const Cand& cand, V3 target, const PassOptions& opt) {
+  Attempt r;
+  Build b = make_candidate_build(P, cand, target);
+  if (!b.ok) {
+    r.failure = {cand, b.waypoints, -1, b.fail_reason};
+    return r;
+  }
+  PassResult pass = backward_pass(P, b.waypoints, b.anchor, opt);
+  if (!pass.ok) {
+    r.failure = {cand, b.waypoints, pass.failed_index, "no pose at waypoint"};
+    return r;
+  }
+  auto unfold = P.interpolate(nullptr, pass.poses[0], P.pp.unfold_steps);
+  if (!unfold) {
+    r.failure = {cand, b.waypoints, 0, "unfold blocked"};
+    return r;
+  }
+  r.plan = assemble(std::move(pass), std::move(*unfold), b.kind);
+  return r;
+}
+
+std::vector<V3> candidate_tip_path(const Cand& c, int n, V3 target) {
+  if (c.kind == RP_CHOSEN_SHORTCUT) return c.sc.tip_waypoints(target);
+  const int traversal = std::min(3, c.pose.nseg);
+  return {c.pose.waypoints.begin(), c.pose.waypoints.begin() + traversal * n};
+}
+
+/// alternate_candidates (src/path_planner.cpp:612-663): the 3 nearest and
+/// then up to 13 farthest by (mean polyline deviation, ordinal), scored and
+/// sorted on the device.
+std::vector<Cand> alternate_candidates(Planner& P, rp_solution_set* set, const Cand& failed,
+                                       V3 target) {
+  const std::vector<V3> failed_path = candidate_tip_path(failed, P.n, target);
+  const int64_t S = static_cast<int64_t>(set->shortcuts.size());
+  std::vector<std::vector<V3>> lists;
+  for (const auto& sc : set->shortcuts) lists.push_back(sc.tip_waypoints(target));
+  int64_t skip = -1;
+  if (failed.kind == RP_CHOSEN_SHORTCUT) {
+    for (int64_t k = 0; k < S; ++k) {
+      const auto& sc = set->shortcuts[k];
+      if (sc.seg1 == failed.sc.seg1 && sc.seg2 == failed.sc.seg2 &&
+          sc.segment_index == failed.sc.segment_index) {
+        skip = k;
+        break;
+      }
+    }
+  } else {
+    skip = S + failed.ordinal;
+  }
+  int64_t total = 0;
+  std::vector<long long> tail;
+  const int want = 64;
+  std::vector<long long> head =
+      P.rank_by_deviation(set, lists, failed_path, false, V3{0, 0, 0}, &total, &tail, want, want);
+  // Filtered sorted order F (skip removed), then near 3 + far <= 13.
+  std::vector<long long> F_head, F_tail;
+  for (long long o : head)
+    if (o != skip) F_head.push_back(o);
+  for (long long o : tail)
+    if (o != skip) F_tail.push_back(o);
+  const int64_t F = total - ((skip >= 0 && skip < total) ? 1 : 0);
+  std::vector<long long> ordered;
+  for (int64_t k = 0; k < F && k < 3; ++k) ordered.push_back(F_head[k]);
+  for (int64_t k = F; k-- > 3 && ordered.size() < 16;) {
+    // index k of F from the end of F_tail
+    const int64_t from_end = F - 1 - k;
+    ordered.push_back(F_tail[F_tail.size() - 1 - from_end]);
+  }
+  std::vector<Cand> out;
+  std::vector<long long> sol_ords;
+  for (long long o : ordered)
+    if (o >= S) sol_ords.push_back(o - S);
+  std::vector<HostPose> poses = solution_poses(set, sol_ords);
+  size_t next = 0;
+  for (long long o : ordered) {
+    Cand c;
+    if (o < S) {
+      c.kind = RP_CHOSEN_SHORTCUT;
+      c.ordinal = o;
+      c.sc = set->shortcuts[o];
+    } else {
+      c.kind = RP_CHOSEN_REACH_POSE;
+      c.ordinal = o - S;
+      c.pose = poses[next++];
+    }
+    out.push_back(c);
+  }
+  return out;
+}
+
+rp_arm virtual_arm(V3 root, double reach, double clamp_total) {
+  rp_arm v;
+  const double lv = std::max(1e-6, std::min(reach, clamp_total) / 3.0);
+  const double L[3] = {lv, lv, lv};
+  rp_arm_init(&v, 3, L);
+  v.root[0] = root.x;
+  v.root[1] = root.y;
+  v.root[2] = root.z;
+  v.arm_radius = 0.0;
+  return v;
+}
+
+rp_reach_params virtual_params(const rp_reach_params& rp) {
+  rp_reach_params v = rp;
+  v.mode = RP_MODE_6DOF;
+  v.epsilon_gap = -1.0;
+  v.near_target_radius = 0.0;
+  v.approach_half_angle = 0.0;
+  return v;
+}
+
+/// solve_reach that maps solver errors to an empty set (the reference's
+/// try / catch around the virtual-arm solves).
+std::unique_ptr<rp_solution_set> try_solve(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
+                                           const rp_grid* g, V3 target, const rp_reach_params& rp) {
+  try {
+    return std::unique_ptr<rp_solution_set>(solve_reach(ctx, arm, q, g, target, rp));
+  } catch (const Fail& e) {
+    if (e.code == RP_E_CUDA || e.code == RP_E_INTERNAL) throw;
+    return nullptr;
+  }
+}
+
+/// fallback_cascade (src/path_planner.cpp:740-822)
+rp_plan* fallback_cascade(Planner& P, const Failure& failure, rp_solution_set* set, V3 target) {
+  PassOptions esc;
+  esc.factors = with_unit_first(P.pp.relax);
+  if (!P.pp.relax.empty()) {
+    const double last = P.pp.relax.back();
+    for (double s : P.pp.relax) esc.factors.push_back(last * s);
+  }
+  {
+    Attempt r = attempt_candidate(P, failure.candidate, target, esc);
+    if (r.plan) {
+      r.plan->notes.push_back("fallback: relaxation escalation");
+      return r.plan;
+    }
+  }
+  PassOptions cloud = esc;
+  cloud.cloud = true;
+  cloud.cloud_radius = 2.0 * P.pp.eps_wp;
+  {
+    Attempt r = attempt_candidate(P, failure.candidate, target, cloud);
+    if (r.plan) {
+      r.plan->notes.push_back("fallback: target cloud");
+      return r.plan;
+    }
+  }
+  for (const Cand& c : alternate_candidates(P, set, failure.candidate, target)) {
+    Attempt r = attempt_candidate(P, c, target, cloud);
+    if (r.plan) {
+      r.plan->notes.push_back("fallback: alternate solution");
+      return r.plan;
+    }
+  }
+  Build b = make_candidate_build(P, failure.candidate, target);
+  if (b.ok && failure.blocked_index > 0 && !failure.waypoints.empty()) {
+    const V3 path_target = tracked_point(b.anchor);
+    std::vector<V3> work(failure.waypoints.begin(),
+                         failure.waypoints.begin() + failure.blocked_index + 1);
+    for (int depth = 0; depth < 3; ++depth) {
+      const V3 from = work.back();
+      const rp_arm vspec = virtual_arm(from, rpd::norm(path_target - from), total_length(P.arm));
+      auto vset = try_solve(P.ctx, vspec, P.q, P.g, path_target, virtual_params(P.rp));
+      if (!vset || vset->n_solutions == 0) break;
+      bool advanced = false;
+      std::vector<long long> first;
+      for (long long k = 0; k < std::min<int64_t>(8, vset->n_solutions); ++k) first.push_back(k);
+      const std::vector<HostPose> vs = solution_poses(vset.get(), first);
+      for (const HostPose& v : vs) {
+        std::vector<V3> stitched = work;
+        stitched.insert(stitched.end(), v.waypoints.begin(), v.waypoints.end());
+        PassResult pass = backward_pass(P, stitched, b.anchor, cloud);
+        if (pass.ok) {
+          auto unfold = P.interpolate(nullptr, pass.poses[0], P.pp.unfold_steps);
+          if (!unfold) continue;
+          rp_plan* plan = assemble(std::move(pass), std::move(*unfold), b.kind);
+          plan->notes.push_back("fallback: virtual-arm detour");
+          return plan;
+        }
+        if (pass.failed_index > static_cast<int>(work.size())) {
+          work.assign(stitched.begin(), stitched.begin() + pass.failed_index + 1);
+          advanced = true;
+          break;
+        }
+      }
+      if (!advanced) break;
+    }
+  }
+  fail(RP_E_NO_PATH, "no motion plan after relaxation, alternate solutions and detours");
+}
+
+Cand chosen_cand(rp_solution_set* set, const rp_chosen& ch) {
+  Cand c;
+  c.kind = ch.kind;
+  c.ordinal = ch.index;
+  if (ch.kind == RP_CHOSEN_SHORTCUT) {
+    c.sc = set->shortcuts[ch.index];
+  } else {
+    c.pose = solution_poses(set, {ch.index})[0];
+  }
+  return c;
+}
+
+/// plan_from_reach (src/path_planner.cpp:729-738)
+rp_plan* plan_from_reach(Planner& P, rp_solution_set* set, const rp_chosen& ch, V3 target) {
+  PassOptions opt;
+  opt.factors = with_unit_first(P.pp.relax);
+  const Cand c = chosen_cand(set, ch);
+  Attempt r = attempt_candidate(P, c, target, opt);
+  if (r.plan) return r.plan;
+  return fallback_cascade(P, r.failure, set, target);
+}
+
+/// build_target_anchor (src/path_planner.cpp:872-902)
+bool build_target_anchor(Planner& P, V3 target, const rp_reach_params& rp, V3 hint, HostPose* out) {
+  rp_reach_params rpa = rp;
+  rpa.near_target_radius = 0.0;
+  auto set = try_solve(P.ctx, P.arm, P.q, P.g, target, rpa);
+  if (!set || set->n_solutions == 0) return false;
+  const rp_chosen ch = select(set.get());
+  if (ch.kind != RP_CHOSEN_REACH_POSE) return false;  // refine of an empty pose throws
+  try {
+    const HostPose pose = solution_poses(set.get(), {ch.index})[0];
+    if (pose.nseg == 4) {
+      *out = P.refine(pose, target, 0);
+      return true;
+    }
+    HostPose refined = P.refine(pose, target, 2);
+    if (P.arm.n_segments == 4) {
+      Trail trail;
+      if (rpd::norm(hint) > 1e-12) {
+        trail.has_back = true;
+        trail.back = -rpd::normalized(hint);
+      }
+      HostPose trailed;
+      if (!P.append_trail(refined, trail, &trailed)) return false;
+      refined = trailed;
+    }
+    *out = refined;
+    return true;
+  } catch (const Fail& e) {
+    if (e.code == RP_E_CUDA || e.code == RP_E_INTERNAL) throw;
+    return false;
+  }
+}
+
+/// screen_real_reach (src/path_planner.cpp:692-707)
+bool screen_real_reach(const rp_arm& a, const std::vector<V3>& wps, int n, double eps) {
+  const double L0 = a.lengths[0], L1 = a.lengths[1], L2 = a.lengths[2];
+  const double r_max = L0 + L1 + L2 + eps;
+  const double lmax = std::max({L0, L1, L2});
+  const double r_min = std::max(0.0, 2.0 * lmax - (L0 + L1 + L2)) - eps;
+  const V3 root{a.root[0], a.root[1], a.root[2]};
+  const size_t segs = wps.size() / static_cast<size_t>(n);
+  for (size_t s = 0; s < segs; ++s) {
+    for (size_t k : {s * n + n / 2, s * n + n - 1}) {
+      const double d = rpd::norm(wps[k] - root);
+      if (d > r_max || d < std::max(0.0, r_min)) return false;
+    }
+  }
+  return true;
+}
+
+/// plan_virtual_path (src/path_planner.cpp:840-868); candidates come lazily
+/// in batches from `next_batch` (empty = exhausted).
+template <typename NextBatch>
+rp_plan* plan_virtual_path(Planner& P, const HostPose& start, NextBatch next_batch,
+                           const HostPose& anchor, V3 path_target) {
+  const V3 e0 = tracked_point(start);
+  PassOptions opt;
+  opt.factors = with_unit_first(P.pp.relax);
+  opt.fixed_first = &start;
+  for (;;) {
+    const std::vector<HostPose> batch = next_batch();
+    if (batch.empty()) return nullptr;
+    for (const HostPose& v : batch) {
+      if (!screen_real_reach(P.arm, v.waypoints, P.n, P.pp.eps_wp)) continue;
+      std::vector<V3> wps{e0};
+      wps.insert(wps.end(), v.waypoints.begin(), v.waypoints.end());
+      wps.back() = path_target;
+      PassResult pass = backward_pass(P, wps, anchor, opt);
+      if (!pass.ok) continue;
+      auto* plan = new rp_plan();
+      plan->waypoints = std::move(pass.waypoints);
+      plan->poses = std::move(pass.poses);
+      plan->kind = "virtual-arm";
+      plan->relax = std::move(pass.relax);
+      plan->notes = std::move(pass.notes);
+      return plan;
+    }
+  }
+}
+
+}  // namespace
+
+PP resolve_path_params(const rp_path_params& p, const rp_arm& arm, const rp_reach_params& rp) {
+  PP r;
+  r.d_w = p.d_w < 0.0 ? nominal_spacing(arm, rp) : p.d_w;
+  r.slack = p.slack < 0.0 ? 0.5 * r.d_w : p.slack;
+  r.j1 = p.joint1_max_move < 0.0 ? 0.5 * r.d_w + r.slack : p.joint1_max_move;
+  r.j2 = p.joint2_max_move < 0.0 ? 1.0 * r.d_w + r.slack : p.joint2_max_move;
+  r.eps_wp = p.epsilon_waypoint < 0.0 ? r.d_w : p.epsilon_waypoint;
+  r.unfold_steps = p.unfold_steps;
+  require(r.eps_wp > 0 && r.d_w > 0 && r.slack >= 0 && r.j1 > 0 && r.j2 > 0 && r.unfold_steps >= 1,
+          RP_E_INVALID_PARAMETER, "path parameters must be positive");
+  require(p.n_relax >= 0 && p.n_relax <= RP_MAX_RELAX, RP_E_INVALID_PARAMETER,
+          "at most 8 relaxation factors");
+  for (int k = 0; k < p.n_relax; ++k) {
+    require(p.relax_schedule[k] >= 1.0, RP_E_INVALID_PARAMETER,
+            "relaxation factors must be >= 1");
+    r.relax.push_back(p.relax_schedule[k]);
+  }
+  return r;
+}
+
+namespace {
+
+__global__ void k_gather_keys(const long long* __restrict__ keys, const long long* __restrict__ ords,
+                              int64_t n, long long* __restrict__ out) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < n) out[t] = keys[ords[t]];
+}
+
+std::vector<HostPose> solution_poses(rp_solution_set* s, const std::vector<long long>& ordinals) {
+  std::vector<HostPose> out;
+  if (ordinals.empty()) return out;
+  ensure_keys(s);
+  rp_ctx* ctx = s->ctx;
+  const int64_t n = static_cast<int64_t>(ordinals.size());
+  DevBuf<long long> ords(n, ctx->stream), keys(n, ctx->stream);
+  copy_to_device(ctx, ords.p, ordinals.data(), n * sizeof(long long));
+  launch(ctx, "materialize", k_gather_keys, dim3(static_cast<unsigned>((n + 127) / 128)),
+         dim3(128), 0, static_cast<const long long*>(s->keys.p),
+         static_cast<const long long*>(ords.p), n, keys.p);
+  DevBuf<DevPose> d(n, ctx->stream);
+  materialize_solutions(s, keys.p, nullptr, n, d.p);
+  std::vector<DevPose> h(n);
+  copy_to_host(ctx, h.data(), d.p, n * sizeof(DevPose));
+  for (const auto& p : h) out.push_back(host_pose_from_dev(p));
+  return out;
+}
+
+}  // namespace
+
+rp_plan* plan_reach_then_path(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q, const rp_grid* g,
+                              V3 target, const rp_reach_params& rp, const rp_path_params& pp) {
+  std::unique_ptr<rp_solution_set> set(solve_reach(ctx, arm, q, g, target, rp));
+  const rp_chosen ch = select(set.get());
+  Planner P(ctx, arm, q, g, rp, pp);
+  return plan_from_reach(P, set.get(), ch, target);
+}
+
+/// plan_arbitrary (src/path_planner.cpp:906-998)
+rp_plan* plan_arbitrary(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q, const rp_grid* g,
+                        const HostPose& start, V3 target, const rp_reach_params& rp,
+                        const rp_path_params& pp) {
+  Planner P(ctx, arm, q, g, rp, pp);
+  const V3 e0 = tracked_point(start);
+  if (rpd::norm(e0 - target) <= P.pp.eps_wp && arm.n_segments == start.nseg) {
+    auto* plan = new rp_plan();
+    plan->waypoints = {e0};
+    plan->poses = {start};
+    plan->kind = "virtual-arm";
+    plan->relax = {1.0};
+    return plan;
+  }
+  HostPose anchor;
+  if (build_target_anchor(P, target, rp, target - e0, &anchor)) {
+    const V3 path_target = tracked_point(anchor);
+    const rp_arm vspec = virtual_arm(e0, rpd::norm(path_target - e0), total_length(arm));
+    auto vset = try_solve(ctx, vspec, q, g, path_target, virtual_params(rp));
+    bool served = false;
+    auto batch = [&]() -> std::vector<HostPose> {
+      if (served || !vset || vset->n_solutions == 0) return {};
+      served = true;
+      std::vector<long long> ords;
+      for (long long k = 0; k < std::min<int64_t>(24, vset->n_solutions); ++k) ords.push_back(k);
+      return solution_poses(vset.get(), ords);
+    };
+    if (rp_plan* plan = plan_virtual_path(P, start, batch, anchor, path_target)) return plan;
+  }
+  rp_reach_params rp_back = rp;
+  rp_back.mode = RP_MODE_6DOF;
+  rp_back.approach_half_angle = 0.0;
+  std::unique_ptr<rp_plan> back(plan_reach_then_path(ctx, arm, q, g, e0, rp_back, pp));
+  std::unique_ptr<rp_plan> out(plan_reach_then_path(ctx, arm, q, g, target, rp, pp));
+  double junction = 0.0;
+  for (double f : with_unit_first(P.pp.relax)) {
+    if (smoothness_ok(start, back->poses.back(), P.pp, f)) {
+      junction = f;
+      break;
+    }
+  }
+  require(junction > 0.0, RP_E_NO_PATH, "start pose does not join the retraction path smoothly");
+  const auto back_seq = back->full_sequence();
+  const auto out_seq = out->full_sequence();
+  auto bridge = P.interpolate(back_seq.front(), *out_seq.front(), P.pp.unfold_steps);
+  require(bridge.has_value(), RP_E_NO_PATH, "folded poses of the two legs cannot be joined");
+  auto* plan = new rp_plan();
+  plan->kind = "out-and-back";
+  auto push = [&](const HostPose& p, double relax) {
+    plan->poses.push_back(p);
+    plan->waypoints.push_back(tracked_point(p));
+    plan->relax.push_back(relax);
+  };
+  push(start, junction);
+  for (size_t k = back_seq.size(); k-- > 0;) {
+    const size_t wp_count = back->poses.size();
+    double relax = 1.0;
+    if (k >= back_seq.size() - wp_count) relax = back->relax[k - (back_seq.size() - wp_count)];
+    push(*back_seq[k], relax);
+  }
+  for (size_t k = 1; k + 1 < bridge->size(); ++k) push((*bridge)[k], 1.0);
+  for (size_t k = 0; k < out_seq.size(); ++k) {
+    const size_t wp_count = out->poses.size();
+    double relax = 1.0;
+    if (k >= out_seq.size() - wp_count) relax = out->relax[k - (out_seq.size() - wp_count)];
+    push(*out_seq[k], relax);
+  }
+  plan->notes.push_back("out-and-back via the folded pose");
+  return plan;
+}
+
+/// replan_dynamic (src/path_planner.cpp:1000-1102)
+rp_plan* replan_dynamic(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q, const rp_grid* gs,
+                        const rp_plan& active, int current, const rp_obstacle& obs, double period,
+                        double cost, const rp_reach_params& rp, const rp_path_params& pp) {
+  const PP ppr = resolve_path_params(pp, arm, rp);
+  const int m = static_cast<int>(active.poses.size());
+  require(current >= 0 && current < m, RP_E_INVALID_PARAMETER, "current waypoint index out of range");
+  require(period > 0.0 && cost >= 0.0, RP_E_INVALID_PARAMETER, "replan timing must be positive");
+  rp_grid* aug_raw = nullptr;
+  rp_status st = rp_grid_overlay(gs, &obs, &aug_raw);
+  if (st != RP_OK) throw Fail{st, rp_last_error()};
+  struct GridDel {
+    void operator()(rp_grid* g) const { rp_grid_destroy(g); }
+  };
+  std::unique_ptr<rp_grid, GridDel> aug(aug_raw);
+  Planner P(ctx, arm, q, aug.get(), rp, pp);
+  const int collide_at = P.first_colliding(active.poses, aug.get());
+  if (collide_at < 0) return new rp_plan(active);
+  require(collide_at - current >= 3, RP_E_INFEASIBLE_TIMING,
+          "collision fewer than three waypoints ahead of the arm");
+  const double est = cost * (m - current);
+  const int switch_index =
+      current + std::max(1, static_cast<int>(std::ceil(est / period))) + 1;
+  require(switch_index <= collide_at - 1, RP_E_INFEASIBLE_TIMING,
+          "no time to switch paths before the collision point");
+  const HostPose switch_pose = active.poses[switch_index];
+  const V3 from = tracked_point(switch_pose);
+  const V3 target = active.waypoints.back();
+  HostPose anchor;
+  require(build_target_anchor(P, target, rp, target - from, &anchor), RP_E_NO_PATH,
+          "target unreachable while the dynamic obstacle is in the way");
+  const V3 path_target = tracked_point(anchor);
+  const rp_arm vspec = virtual_arm(from, rpd::norm(path_target - from), total_length(arm));
+  auto vset = try_solve(ctx, vspec, q, aug.get(), path_target, virtual_params(rp));
+  require(vset && vset->n_solutions > 0, RP_E_NO_PATH, "no avoidance path around the dynamic obstacle");
+  // order = all candidates by (mean deviation of [from] + tip, ordinal)
+  int64_t total = 0;
+  const int64_t nsol = vset->n_solutions;
+  std::vector<long long> order = P.rank_by_deviation(vset.get(), {}, active.waypoints, true, from,
+                                                     &total, nullptr, static_cast<int>(nsol), 0);
+  size_t pos = 0;
+  auto batch = [&]() -> std::vector<HostPose> {
+    if (pos >= order.size()) return {};
+    const size_t e = std::min(order.size(), pos + 256);
+    std::vector<long long> ords(order.begin() + pos, order.begin() + e);
+    pos = e;
+    return solution_poses(vset.get(), ords);
+  };
+  std::unique_ptr<rp_plan> att(plan_virtual_path(P, switch_pose, batch, anchor, path_target));
+  require(att != nullptr, RP_E_NO_PATH, "no valid pose sequence along any avoidance path");
+  auto* plan = new rp_plan();
+  plan->kind = "replan";
+  plan->switch_index = switch_index;
+  plan->unfold = active.unfold;
+  plan->waypoints.assign(active.waypoints.begin(), active.waypoints.begin() + switch_index + 1);
+  plan->poses.assign(active.poses.begin(), active.poses.begin() + switch_index + 1);
+  plan->relax.assign(active.relax.begin(), active.relax.begin() + switch_index + 1);
+  for (size_t k = 1; k < att->poses.size(); ++k) {
+    plan->poses.push_back(att->poses[k]);
+    plan->waypoints.push_back(att->waypoints[k]);
+    plan->relax.push_back(att->relax[k]);
+  }
+  plan->notes = att->notes;
+  plan->notes.push_back(std::string("replanned around dynamic obstacle ") +
+                        (obs.id ? obs.id : ""));
+  (void)ppr;
+  return plan;
+}
+
+}  // namespace rp
+
+using namespace rp;
+
+extern "C" {
+
+rp_status rp_plan_reach_then_path(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q,
+                                  const rp_grid* g, const double target[3],
+                                  const rp_reach_params* rp, const rp_path_params* pp,
+                                  rp_plan** out) {
+  return guarded([&] {
+    *out = plan_reach_then_path(ctx, *arm, q, g, V3{target[0], target[1], target[2]}, *rp, *pp);
+  });
+}
+
+rp_status rp_plan_from_reach(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q, const rp_grid* g,
+                             const rp_solution_set* set, const rp_chosen* chosen,
+                             const double target[3], const rp_reach_params* rp,
+                             const rp_path_params* pp, rp_plan** out) {
+  return guarded([&] {
+    Planner P(ctx, *arm, q, g, *rp, *pp);
+    *out = plan_from_reach(P, const_cast<rp_solution_set*>(set), *chosen,
+                           V3{target[0], target[1], target[2]});
+  });
+}
+
+rp_status rp_plan_arbitrary(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q, const rp_grid* g,
+                            const rp_pose* start, const double target[3], const rp_reach_params* rp,
+                            const rp_path_params* pp, rp_plan** out) {
+  return guarded([&] {
+    *out = plan_arbitrary(ctx, *arm, q, g, from_abi(*start, nullptr),
+                          V3{target[0], target[1], target[2]}, *rp, *pp);
+  });
+}
+
+rp_status rp_replan_dynamic(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q,
+                            const rp_grid* grid_static, const rp_plan* active, int32_t current,
+                            const rp_obstacle* obs, double period, double cost,
+                            const rp_reach_params* rp, const rp_path_params* pp, rp_plan** out) {
+  return guarded([&] {
+    *out = replan_dynamic(ctx, *arm, q, grid_static, *active, current, *obs, period, cost, *rp, *pp);
+  });
+}
+
+rp_status rp_waypoint_ik(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q, const rp_grid* g,
+                         const double waypoint[3], const rp_pose* prev, const rp_reach_params* rp,
+                         const rp_path_params* pp, double relax, const double* back,
+                         const double* fwd, const rp_pose* bias, int32_t* found, rp_pose* out,
+                         double* wps, int32_t cap) {
+  return guarded([&] {
+    Planner P(ctx, *arm, q, g, *rp, *pp);
+    Trail t;
+    if (back) {
+      t.has_back = true;
+      t.back = V3{back[0], back[1], back[2]};
+    }
+    if (fwd) {
+      t.has_fwd = true;
+      t.fwd = V3{fwd[0], fwd[1], fwd[2]};
+    }
+    const HostPose hp = from_abi(*prev, nullptr);
+    HostPose hb;
+    if (bias) hb = from_abi(*bias, nullptr);
+    HostPose res;
+    const bool ok = P.waypoint_ik(V3{waypoint[0], waypoint[1], waypoint[2]}, hp, relax, t,
+                                  bias ? &hb : nullptr, &res);
+    *found = ok ? 1 : 0;
+    if (ok) to_abi(res, out, wps, cap);
+  });
+}
+
+rp_status rp_smoothness_ok(const rp_arm* arm, const rp_reach_params* rp, const rp_path_params* pp,
+                           const rp_pose* prev, const rp_pose* cand, double relax, int32_t* ok) {
+  return guarded([&] {
+    const PP r = resolve_path_params(*pp, *arm, *rp);
+    *ok = smoothness_ok(from_abi(*prev, nullptr), from_abi(*cand, nullptr), r, relax) ? 1 : 0;
+  });
+}
+
+rp_status rp_mean_polyline_deviation(rp_ctx* ctx, const double* pts, int32_t n, const double* poly,
+                                     int32_t np, double* out) {
+  return guarded([&] {
+    std::vector<V3> a(n), b(np);
+    std::memcpy(a.data(), pts, n * sizeof(V3));
+    std::memcpy(b.data(), poly, np * sizeof(V3));
+    *out = mean_polyline_deviation(ctx, a, b);
+  });
+}
+
+rp_status rp_folded_pose(rp_ctx* ctx, const rp_arm* arm, rp_pose* out) {
+  return guarded([&] {
+    validate_arm(*arm);
+    to_abi(folded_pose_host(ctx, *arm), out, nullptr, 0);
+  });
+}
+
+rp_status rp_plan_get_info(const rp_plan* p, rp_plan_info* info) {
+  return guarded([&] {
+    std::memset(info, 0, sizeof(*info));
+    info->n_waypoints = static_cast<int>(p->waypoints.size());
+    info->n_poses = static_cast<int>(p->poses.size());
+    info->n_unfold = static_cast<int>(p->unfold.size());
+    info->n_notes = static_cast<int>(p->notes.size());
+    info->replan_switch_index = p->switch_index;
+    std::strncpy(info->kind, p->kind.c_str(), sizeof(info->kind) - 1);
+  });
+}
+
+rp_status rp_plan_waypoints(const rp_plan* p, double* xyz, int32_t cap) {
+  return guarded([&] {
+    for (size_t k = 0; k < p->waypoints.size() && static_cast<int>(k) < cap; ++k) {
+      xyz[3 * k] = p->waypoints[k].x;
+      xyz[3 * k + 1] = p->waypoints[k].y;
+      xyz[3 * k + 2] = p->waypoints[k].z;
+    }
+  });
+}
+
+rp_status rp_plan_relax(const rp_plan* p, double* relax, int32_t cap) {
+  return guarded([&] {
+    for (size_t k = 0; k < p->relax.size() && static_cast<int>(k) < cap; ++k) relax[k] = p->relax[k];
+  });
+}
+
+rp_status rp_plan_pose(const rp_plan* p, int32_t which, int32_t k, rp_pose* pose, double* wps,
+                       int32_t cap) {
+  return guarded([&] {
+    const auto& v = which == 0 ? p->poses : p->unfold;
+    require(k >= 0 && k < static_cast<int>(v.size()), RP_E_INVALID_PARAMETER, "pose index out of range");
+    to_abi(v[k], pose, wps, cap);
+  });
+}
+
+rp_status rp_plan_note(const rp_plan* p, int32_t k, char* buf, int32_t cap) {
+  return guarded([&] {
+    require(k >= 0 && k < static_cast<int>(p->notes.size()) && cap > 0, RP_E_INVALID_PARAMETER,
+            "note index out of range");
+    std::strncpy(buf, p->notes[k].c_str(), cap - 1);
+    buf[cap - 1] = 0;
+  });
+}
+
+rp_status rp_plan_create(const char* kind, const double* waypoints, const rp_pose* poses,
+                         const double* relax, int32_t n, const rp_pose* unfold, int32_t n_unfold,
+                         rp_plan** out) {
+  return guarded([&] {
+    auto* p = new rp_plan();
+    p->kind = kind ? kind : "";
+    for (int k = 0; k < n; ++k) {
+      p->waypoints.push_back(V3{waypoints[3 * k], waypoints[3 * k + 1], waypoints[3 * k + 2]});
+      p->poses.push_back(from_abi(poses[k], nullptr));
+      p->relax.push_back(relax ? relax[k] : 1.0);
+    }
+    for (int k = 0; k < n_unfold; ++k) p->unfold.push_back(from_abi(unfold[k], nullptr));
+    *out = p;
+  });
+}
+
+rp_status rp_plan_destroy(rp_plan* p) {
+  return guarded([&] { delete p; });
+}
+
+}  // extern "C"

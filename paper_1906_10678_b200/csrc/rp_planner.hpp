@@ -1,0 +1,70 @@
+// Host orchestration of the path planner over the device kernels.
+#pragma once
+
+#include "rp_path.cuh"
+
+#include <optional>
+#include <string>
+#include <vector>
+
+namespace rp {
+
+/// TrailContext (inc/reachplan/path_planner.hpp:51-54)
+struct Trail {
+  bool has_back = false, has_fwd = false;
+  V3 back{0, 0, 0}, fwd{0, 0, 0};
+};
+
+/// Planner state for one (arm, quiver, grid, params) tuple: owns the
+/// device scratch reused by every waypoint_ik call.
+struct Planner {
+  rp_ctx* ctx;
+  rp_arm arm;
+  const rp_quiver* q;
+  const rp_grid* g;
+  rp_reach_params rp;
+  ArmDev ad;
+  PP pp;
+  int n;
+  double spacing;
+  int wik_blocks = 0;
+  int64_t wik_calls = 0;
+  DevBuf<uint32_t> ibits, jbits;
+  DevBuf<int> cj, counts;
+  DevBuf<CiData> ci;
+  DevBuf<WikBest> block_best;
+  DevBuf<unsigned> done;
+  DevBuf<WikResult> result;
+  DevBuf<PoseOpOut> opout;
+  WikResult* h_result = nullptr;
+
+  Planner(rp_ctx* c, const rp_arm& a, const rp_quiver* qv, const rp_grid* gr,
+          const rp_reach_params& r, const rp_path_params& p);
+  ~Planner();
+  Planner(const Planner&) = delete;
+  Planner& operator=(const Planner&) = delete;
+
+  bool waypoint_ik(V3 wp, const HostPose& prev, double relax, const Trail& tr,
+                   const HostPose* bias, HostPose* out);
+  HostPose refine(const HostPose& approx, V3 target, int mode);
+  bool append_trail(const HostPose& chain3, const Trail& tr, HostPose* out);
+  /// from == nullptr: build_unfold (rotated folded pose); else interpolate_poses.
+  std::optional<std::vector<HostPose>> interpolate(const HostPose* from, const HostPose& to,
+                                                   int base_steps, bool* rotated_valid = nullptr);
+  int first_colliding(const std::vector<HostPose>& poses, const rp_grid* grid);
+  /// pose_valid over a batch on the device: first invalid index or -1.
+  int valid_poses(const DevPose* poses, int count);
+  std::vector<long long> rank_by_deviation(rp_solution_set* set,
+                                           const std::vector<std::vector<V3>>& lists,
+                                           const std::vector<V3>& poly, bool lead, V3 lead_pt,
+                                           int64_t* total, std::vector<long long>* tail,
+                                           int head_n, int tail_n);
+};
+
+HostPose folded_pose_host(rp_ctx* ctx, const rp_arm& arm);
+double mean_polyline_deviation(rp_ctx* ctx, const std::vector<V3>& pts, const std::vector<V3>& poly);
+
+rp_plan* plan_reach_then_path(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q, const rp_grid* g,
+                              V3 target, const rp_reach_params& rp, const rp_path_params& pp);
+
+}  // namespace rp

@@ -1,0 +1,1084 @@
+// gMS reach-pose search on the device (src/reach_solver.cpp:224-577).
+//
+//   k_seg1     prune_segment1 (:224-300): one thread per quiver direction.
+//   k_seg2     seg2_worker (:316-456) = the per-segment reachability expansion
+//              (p2 = p1 + L2 q_j, swept-segment clearance) fused with the
+//              forward/backward intersection (gap band |b - p2| ~ L3, v3 / s4
+//              clearance, self-collision). One thread per (survivor, j) pair,
+//              grid-stride over warps; solutions are written as a bit set in
+//              canonical (i, j, l) order by warp ballot, counters are reduced
+//              per thread and flushed with one atomic per warp, the
+//              select_solution argmin (:548-577) is reduced per block.
+//   k_shortcuts short_reach_scan (:176-222) on the rare near-encounter pairs.
+//
+// All decisions use rp_device.cuh's reference-order fp64 arithmetic, so the
+// solution set, the shortcut set and all 13 SolveStats counters are
+// bit-identical to the reference.
+#include "rp_reach.cuh"
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+
+namespace rp {
+
+using rpd::V3;
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr unsigned kShortcutCap = 1u << 20;
+
+__device__ __forceinline__ bool offset_link_clear(const rpd::GridView& g, V3 from, V3 to,
+                                                  double spacing) {
+  const double len = rpd::norm(to - from);
+  if (len == 0.0) return true;
+  return rpd::walk_first_blocked(g, from, to, rpd::scaled_sample_count(len, spacing)) == 0;
+}
+
+__device__ __forceinline__ void warp_flush(unsigned long long* ctr, int idx, unsigned v) {
+  v = __reduce_add_sync(FULL, v);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(ctr + idx, static_cast<unsigned long long>(v));
+}
+
+// ---------------------------------------------------------------------------
+__global__ void k_walk4(SolveDev a, uint8_t* out) {
+  const int bi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (bi >= a.B) return;
+  out[bi] = rpd::walk_first_blocked(a.g, a.bpts[bi], a.target, a.n) == 0 ? 1 : 0;
+}
+
+/// cone_subset membership (src/quiver.cpp:53-63) with an ambiguity flag for
+/// angles within 1e-9 rad of the limit (re-decided on the host with glibc).
+__global__ void k_cone(const double* qx, const double* qy, const double* qz, int Q, V3 axis,
+                       double limit, uint8_t* inside, uint8_t* ambiguous) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= Q) return;
+  const V3 v{qx[i], qy[i], qz[i]};
+  const double ang = atan2(rpd::norm(rpd::cross(v, axis)), rpd::dot(v, axis));
+  inside[i] = ang <= limit ? 1 : 0;
+  ambiguous[i] = fabs(ang - limit) < 1e-9 ? 1 : 0;
+}
+
+/// prune_segment1 for every quiver direction.
+__global__ void __launch_bounds__(256) k_seg1(SolveDev a, uint32_t* __restrict__ surv_bits,
+                                              unsigned long long* ctr, long long* sc_list,
+                                              unsigned* sc_count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  bool lim_pass = false, reach = false, surv = false;
+  if (i < a.Q) {
+    const ArmDev& arm = a.arm;
+    const V3 dir = qvec(a, i);
+    rpd::FrameStep st{};
+    const bool has_elbow = arm.off[0] > 0.0;
+    if (arm.lim_active[0] || has_elbow) st = rpd::advance_frame(arm.base, dir);
+    lim_pass = !arm.lim_active[0] || rpd::joint_angle_within(st.theta, st.phi, st.degenerate, arm.lim[0]);
+    if (lim_pass) {
+      V3 link = arm.root, elbow{0, 0, 0};
+      if (has_elbow) {
+        elbow = arm.root + arm.off[0] * rpd::m_col(st.after_azimuth, 0);
+        link = elbow;
+      }
+      const V3 p1 = link + arm.L[0] * dir;
+      reach = a.disable_prune != 0;
+      for (int t = 0; !reach && t < a.n_targets; ++t)
+        if (rpd::sqnorm(p1 - a.targets[t]) <= a.budget2) reach = true;
+      if (reach || a.scanning) {
+        if (!has_elbow || offset_link_clear(a.g, arm.root, elbow, a.spacing)) {
+          const int fb = rpd::walk_first_blocked(a.g, link, p1, a.n);
+          if (a.scanning && rpd::point_to_segment(a.target, link, p1) <= a.near_r + 1e-9) {
+            const unsigned pos = atomicAdd(sc_count, 1u);
+            if (pos < kShortcutCap) sc_list[pos] = i;
+          }
+          surv = reach && fb == 0;
+        }
+      }
+    }
+  }
+  const unsigned m = __ballot_sync(FULL, surv);
+  if ((threadIdx.x & 31) == 0 && (i >> 5) < (a.Q + 31) / 32) surv_bits[i >> 5] = m;
+  warp_flush(ctr, C_SEG1_LIMIT, lim_pass ? 1u : 0u);
+  warp_flush(ctr, C_SEG1_REACH, (lim_pass && reach) ? 1u : 0u);
+  warp_flush(ctr, C_SEG1_SURV, surv ? 1u : 0u);
+}
+
+/// Ordered compaction of a small bit set in one block (bit k -> out[rank]).
+__global__ void k_compact_small(const uint32_t* __restrict__ bits, int nbits, int* __restrict__ out,
+                                int* __restrict__ count) {
+  typedef cub::BlockScan<int, 1024> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int nwords = (nbits + 31) / 32;
+  for (int w0 = 0; w0 < nwords; w0 += 1024) {
+    const int w = w0 + threadIdx.x;
+    const uint32_t word = w < nwords ? bits[w] : 0u;
+    const int c = __popc(word);
+    int off = 0, total = 0;
+    Scan(tmp).ExclusiveSum(c, off, total);
+    off += carry;
+    uint32_t x = word;
+    while (x) {
+      const int b = __ffs(x) - 1;
+      x &= x - 1;
+      out[off++] = w * 32 + b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *count = carry;
+}
+
+__global__ void k_surv_data(SolveDev a, const int* __restrict__ idx, int S1, SurvDev* __restrict__ out) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S1) return;
+  const ArmDev& arm = a.arm;
+  SurvDev h{};
+  h.i = idx[s];
+  const V3 dir = qvec(a, h.i);
+  V3 link = arm.root;
+  if (arm.any_limit || arm.has_offsets) {
+    const rpd::FrameStep st = rpd::advance_frame(arm.base, dir);
+    h.frame = st.frame;
+    if (arm.off[0] > 0.0) {
+      link = arm.root + arm.off[0] * rpd::m_col(st.after_azimuth, 0);
+      h.has_elbow = 1;
+    }
+  }
+  h.link_start = link;
+  h.p1 = link + arm.L[0] * dir;
+  out[s] = h;
+}
+
+/// seg2_worker over all (survivor, j) pairs; see the file head.
+template <bool EIGHT, bool GENERAL, bool B1>
+__global__ void __launch_bounds__(256) k_seg2(SolveDev a, const SurvDev* __restrict__ sv,
+                                              int64_t npairs, uint32_t* __restrict__ sol_bits,
+                                              unsigned long long* ctr, long long* sc_list,
+                                              unsigned* sc_count, BestRec* __restrict__ block_best) {
+  unsigned c_lim = 0, c_clear = 0, c_gt = 0, c_gp = 0, c_jp = 0, c_v3 = 0, c_sol = 0;
+  double best_len = 1e308;
+  long long best_key = LLONG_MAX;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp_id = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const ArmDev& arm = a.arm;
+  const double L1 = arm.L[0], L2 = arm.L[1], L3 = arm.L[2];
+  const double min_sep = 2.0 * arm.arm_radius;
+
+  for (int64_t base = warp_id * 32; base < npairs; base += nwarps * 32) {
+    const int64_t p = base + lane;
+    bool solbit = false;
+    if (p < npairs) {
+      const int s = static_cast<int>(p / a.Q);
+      const int j = static_cast<int>(p - static_cast<int64_t>(s) * a.Q);
+      const V3 dir2 = qvec(a, j);
+      const SurvDev& h = sv[s];
+      rpd::FrameStep st2{};
+      bool have_st2 = false;
+      bool ok = true;
+      if (GENERAL && (arm.lim_active[1] || arm.off[1] > 0.0)) {
+        st2 = rpd::advance_frame(h.frame, dir2);
+        have_st2 = true;
+        ok = rpd::joint_angle_within(st2.theta, st2.phi, st2.degenerate, arm.lim[1]);
+      }
+      if (ok) {
+        ++c_lim;
+        V3 link = h.p1, e2{0, 0, 0};
+        const bool has_e2 = GENERAL && arm.off[1] > 0.0;
+        if (has_e2) {
+          e2 = h.p1 + arm.off[1] * rpd::m_col(st2.after_azimuth, 0);
+          link = e2;
+        }
+        const V3 p2 = link + L2 * dir2;
+        if (GENERAL && EIGHT && a.cone_precheck && !a.disable_prune) {
+          const double dist_t = rpd::norm(a.target - p2);
+          if (dist_t - a.L4 > L3 + a.eps + 1e-9 || dist_t + a.L4 < L3 - a.eps - 1e-9) ok = false;
+        }
+        if (ok && has_e2 && !offset_link_clear(a.g, h.p1, e2, a.spacing)) ok = false;
+        if (ok) {
+          const int fb = rpd::walk_first_blocked(a.g, link, p2, a.n);
+          if (rpd::point_to_segment(a.target, link, p2) <= a.near_r + 1e-9) {
+            const unsigned pos = atomicAdd(sc_count, 1u);
+            if (pos < kShortcutCap) sc_list[pos] = (1ll << 62) | p;
+          }
+          if (fb == 0) {
+            ++c_clear;
+            for (int bi = 0; bi < a.B; ++bi) {
+              ++c_gt;
+              const V3 b = a.bpts[bi];
+              const V3 v3 = b - p2;
+              if (rpd::sqnorm(v3) > a.coarse2) continue;
+              const double v3_len = rpd::norm(v3);
+              if (fabs(v3_len - L3) > a.eps) continue;
+              ++c_gp;
+              if (v3_len < 1e-12) continue;
+              if (GENERAL) {
+                const bool l3 = arm.lim_active[2] != 0;
+                const bool l4 = EIGHT && arm.lim_active[3] != 0;
+                if (l3 || l4) {
+                  const V3 v3_hat = v3 / v3_len;
+                  if (!have_st2) {
+                    st2 = rpd::advance_frame(h.frame, dir2);
+                    have_st2 = true;
+                  }
+                  const rpd::FrameStep st3 = rpd::advance_frame(st2.frame, v3_hat);
+                  if (l3 && !rpd::joint_angle_within(st3.theta, st3.phi, st3.degenerate, arm.lim[2]))
+                    continue;
+                  if (l4) {
+                    const rpd::FrameStep st4 = rpd::advance_frame(st3.frame, a.bdirs[bi]);
+                    if (!rpd::joint_angle_within(st4.theta, st4.phi, st4.degenerate, arm.lim[3]))
+                      continue;
+                  }
+                }
+              }
+              ++c_jp;
+              if (rpd::walk_first_blocked(a.g, p2, b, a.n) != 0) continue;
+              ++c_v3;
+              if (EIGHT && !a.walk4_ok[bi]) continue;
+              const V3 qi = qvec(a, h.i);
+              const V3 s1 = L1 * qi;
+              const V3 s2 = L2 * dir2;
+              bool free_ok;
+              if (!GENERAL || !arm.has_offsets) {
+                V3 J[5];
+                J[0] = arm.root;
+                J[1] = J[0] + s1;
+                J[2] = J[1] + s2;
+                J[3] = J[2] + v3;
+                if (EIGHT) J[4] = J[3] + a.L4 * a.bdirs[bi];
+                free_ok = rpd::self_collision_free(J, EIGHT ? 4 : 3, min_sep);
+              } else {
+                DevPose dp;
+                dp.nseg = EIGHT ? 4 : 3;
+                dp.seg[0] = s1;
+                dp.seg[1] = s2;
+                dp.seg[2] = v3;
+                if (EIGHT) dp.seg[3] = a.L4 * a.bdirs[bi];
+                build_chain(arm, dp);
+                free_ok = pose_self_free(dp, min_sep);
+              }
+              if (!free_ok) continue;
+              ++c_sol;
+              const long long key = p * a.B + bi;
+              if (B1) {
+                solbit = true;
+              } else {
+                atomicOr(sol_bits + (key >> 5), 1u << (key & 31));
+              }
+              const double len = (rpd::norm(s1) + rpd::norm(s2)) + rpd::norm(v3);
+              if (len < best_len || (len == best_len && key < best_key)) {
+                best_len = len;
+                best_key = key;
+              }
+            }
+          }
+        }
+      }
+    }
+    if (B1) {
+      const unsigned m = __ballot_sync(FULL, solbit);
+      if (lane == 0) sol_bits[base >> 5] = m;
+    }
+  }
+  warp_flush(ctr, C_SEG2_LIMIT, c_lim);
+  warp_flush(ctr, C_SEG2_CLEAR, c_clear);
+  warp_flush(ctr, C_GAP_TESTED, c_gt);
+  warp_flush(ctr, C_GAP_PASS, c_gp);
+  warp_flush(ctr, C_JOINT_PASS, c_jp);
+  warp_flush(ctr, C_V3_CLEAR, c_v3);
+  warp_flush(ctr, C_SOLUTIONS, c_sol);
+  // block argmin of (length, canonical key)
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ol = __shfl_down_sync(FULL, best_len, off);
+    const long long ok = __shfl_down_sync(FULL, best_key, off);
+    if (ol < best_len || (ol == best_len && ok < best_key)) {
+      best_len = ol;
+      best_key = ok;
+    }
+  }
+  __shared__ BestRec wb[8];
+  if (lane == 0) wb[threadIdx.x >> 5] = BestRec{best_len, best_key};
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    BestRec b = wb[0];
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+      if (wb[w].len < b.len || (wb[w].len == b.len && wb[w].key < b.key)) b = wb[w];
+    block_best[blockIdx.x] = b;
+  }
+}
+
+__global__ void k_best_final(const BestRec* __restrict__ in, int n, BestRec* out) {
+  __shared__ BestRec sh[256];
+  BestRec b{1e308, LLONG_MAX};
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const BestRec r = in[k];
+    if (r.len < b.len || (r.len == b.len && r.key < b.key)) b = r;
+  }
+  sh[threadIdx.x] = b;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const BestRec r = sh[threadIdx.x + s];
+      if (r.len < sh[threadIdx.x].len ||
+          (r.len == sh[threadIdx.x].len && r.key < sh[threadIdx.x].key))
+        sh[threadIdx.x] = r;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
+/// short_reach_scan for one candidate: hypothesis samples along
+/// [link, end] (walk truncated at the first blocked sample), origin for the
+/// direct completion, prefix length for polyline_length.
+__device__ void scan_one(const SolveDev& a, V3 link, V3 end, V3 origin, int fb, ShortcutRec& r,
+                         bool has_prefix, V3 prefix_from, V3 prefix_to) {
+  const int len = fb ? fb : a.n;
+  const V3 diff = end - link;
+  int hit = 0;
+  for (int k = 0; k < len; ++k) {
+    const V3 sk = rpd::walk_sample(link, diff, k + 1, a.n);
+    if (rpd::norm(sk - a.target) <= a.near_r + 1e-12) {
+      hit = k + 1;
+      break;
+    }
+    const bool clear = !(fb && k + 1 == fb);
+    if (!clear) break;
+  }
+  r.valid = 0;
+  if (hit == 0) return;
+  r.hit = hit;
+  r.n_sub = hit;
+  r.origin = origin;
+  const V3 hp = rpd::walk_sample(link, diff, hit, a.n);
+  const double dist = rpd::norm(hp - a.target);
+  r.has_bridge = 0;
+  r.via_direct = 0;
+  r.n_direct = 0;
+  if (dist > 1e-9) {
+    const bool bridge_ok =
+        rpd::walk_first_blocked(a.g, hp, a.target, rpd::scaled_sample_count(dist, a.spacing)) == 0;
+    if (bridge_ok) {
+      r.has_bridge = 1;
+      r.bridge = a.target - hp;
+    } else {
+      const double dl = rpd::norm(a.target - origin);
+      const int nd = rpd::scaled_sample_count(dl, a.spacing);
+      if (rpd::walk_first_blocked(a.g, origin, a.target, nd) != 0) return;
+      r.via_direct = 1;
+      r.n_direct = nd;
+    }
+  }
+  // polyline_length(root, tip_waypoints) (reach_solver.cpp:157-165, 169-174)
+  double acc = 0.0;
+  V3 prev = a.arm.root;
+  if (has_prefix) {
+    const V3 pd = prefix_to - prefix_from;
+    for (int k = 1; k <= a.n; ++k) {
+      const V3 q = rpd::walk_sample(prefix_from, pd, k, a.n);
+      acc += rpd::norm(q - prev);
+      prev = q;
+    }
+  }
+  if (r.via_direct) {
+    const V3 dd = a.target - origin;
+    for (int k = 1; k <= r.n_direct; ++k) {
+      const V3 q = rpd::walk_sample(origin, dd, k, r.n_direct);
+      acc += rpd::norm(q - prev);
+      prev = q;
+    }
+  } else {
+    for (int k = 1; k <= hit; ++k) {
+      const V3 q = rpd::walk_sample(link, diff, k, a.n);
+      acc += rpd::norm(q - prev);
+      prev = q;
+    }
+  }
+  if (r.has_bridge) acc += rpd::norm(a.target - prev);
+  r.path_length = acc;
+  r.valid = 1;
+}
+
+__global__ void k_shortcuts(SolveDev a, const SurvDev* __restrict__ sv, const long long* keys,
+                            int n, ShortcutRec* out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const long long key = keys[t];
+  ShortcutRec r{};
+  r.key = key;
+  const ArmDev& arm = a.arm;
+  if (!(key >> 62)) {
+    const int i = static_cast<int>(key);
+    const V3 dir = qvec(a, i);
+    V3 link = arm.root;
+    if (arm.off[0] > 0.0) {
+      const rpd::FrameStep st = rpd::advance_frame(arm.base, dir);
+      link = arm.root + arm.off[0] * rpd::m_col(st.after_azimuth, 0);
+    }
+    const V3 p1 = link + arm.L[0] * dir;
+    const int fb = rpd::walk_first_blocked(a.g, link, p1, a.n);
+    r.segment_index = 1;
+    r.seg1 = i;
+    r.seg2 = -1;
+    scan_one(a, link, p1, arm.root, fb, r, false, link, link);
+  } else {
+    const long long p = key & ((1ll << 62) - 1);
+    const int s = static_cast<int>(p / a.Q);
+    const int j = static_cast<int>(p - static_cast<long long>(s) * a.Q);
+    const SurvDev h = sv[s];
+    const V3 dir2 = qvec(a, j);
+    V3 link = h.p1;
+    if (arm.off[1] > 0.0) {
+      const rpd::FrameStep st2 = rpd::advance_frame(h.frame, dir2);
+      link = h.p1 + arm.off[1] * rpd::m_col(st2.after_azimuth, 0);
+    }
+    const V3 p2 = link + arm.L[1] * dir2;
+    const int fb = rpd::walk_first_blocked(a.g, link, p2, a.n);
+    r.segment_index = 2;
+    r.seg1 = h.i;
+    r.seg2 = j;
+    scan_one(a, link, p2, h.p1, fb, r, true, h.link_start, h.p1);
+  }
+  out[t] = r;
+}
+
+__global__ void k_word_popc(const uint32_t* __restrict__ w, int64_t nw, unsigned long long* __restrict__ c) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < nw) c[k] = __popc(w[k]);
+}
+
+__global__ void k_scatter_bits(const uint32_t* __restrict__ w, int64_t nw,
+                               const unsigned long long* __restrict__ off, long long* __restrict__ keys) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= nw) return;
+  uint32_t x = w[k];
+  unsigned long long o = off[k];
+  while (x) {
+    const int b = __ffs(x) - 1;
+    x &= x - 1;
+    keys[o++] = k * 32 + b;
+  }
+}
+
+__global__ void k_rank(const uint32_t* __restrict__ w, long long key, unsigned long long* out) {
+  unsigned long long c = 0;
+  const long long nw = key >> 5;
+  for (long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; k < nw;
+       k += static_cast<long long>(gridDim.x) * blockDim.x)
+    c += __popc(w[k]);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (key & 31))
+    c += __popc(w[nw] & ((1u << (key & 31)) - 1u));
+  c = __reduce_add_sync(FULL, static_cast<unsigned>(c));
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, c);
+}
+
+}  // namespace
+
+/// Materialise solution poses from canonical keys (reach_solver.cpp:434-449).
+__global__ void k_materialize(SolveDev a, const SurvDev* __restrict__ sv,
+                              const long long* __restrict__ keys, int64_t n, DevPose* __restrict__ out) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const long long key = keys[t];
+  const long long p = key / a.B;
+  const int bi = static_cast<int>(key - p * a.B);
+  const int s = static_cast<int>(p / a.Q);
+  const int j = static_cast<int>(p - static_cast<long long>(s) * a.Q);
+  const SurvDev h = sv[s];
+  const ArmDev& arm = a.arm;
+  const V3 dir2 = qvec(a, j);
+  V3 link2 = h.p1;
+  if (arm.off[1] > 0.0) {
+    const rpd::FrameStep st2 = rpd::advance_frame(h.frame, dir2);
+    link2 = h.p1 + arm.off[1] * rpd::m_col(st2.after_azimuth, 0);
+  }
+  const V3 p2 = link2 + arm.L[1] * dir2;
+  const V3 b = a.bpts[bi];
+  DevPose d{};
+  d.nseg = a.eight ? 4 : 3;
+  d.seg[0] = arm.L[0] * qvec(a, h.i);
+  d.seg[1] = arm.L[1] * dir2;
+  d.seg[2] = b - p2;
+  d.qidx[0] = h.i;
+  d.qidx[1] = j;
+  d.qidx[2] = -1;
+  d.qidx[3] = -1;
+  if (a.eight) {
+    d.seg[3] = a.L4 * a.bdirs[bi];
+    d.qidx[3] = a.bcone[bi];
+  }
+  build_chain(arm, d);
+  d.n_wp_links = a.eight ? 4 : 3;
+  d.wp_from[0] = h.link_start; d.wp_to[0] = h.p1;
+  d.wp_from[1] = link2;        d.wp_to[1] = p2;
+  d.wp_from[2] = p2;           d.wp_to[2] = b;
+  d.wp_from[3] = b;            d.wp_to[3] = a.target;
+  for (int k = 0; k < 4; ++k) d.n_wp[k] = a.n;
+  out[t] = d;
+}
+
+HostPose host_pose_from_dev(const DevPose& d) {
+  HostPose h;
+  h.nseg = d.nseg;
+  h.has_elbows = d.has_elbows != 0;
+  for (int k = 0; k < d.nseg; ++k) {
+    h.seg[k] = d.seg[k];
+    h.elbows[k] = d.elbows[k];
+    h.qidx[k] = d.qidx[k];
+  }
+  for (int k = 0; k <= d.nseg; ++k) h.joints[k] = d.joints[k];
+  h.s4dev = d.s4dev;
+  h.waypoints = dev_pose_waypoints(d);
+  return h;
+}
+
+std::vector<V3> dev_pose_waypoints(const DevPose& d) {
+  std::vector<V3> w;
+  for (int l = 0; l < d.n_wp_links; ++l) {
+    const V3 diff = d.wp_to[l] - d.wp_from[l];
+    for (int k = 1; k <= d.n_wp[l]; ++k) w.push_back(rpd::walk_sample(d.wp_from[l], diff, k, d.n_wp[l]));
+  }
+  return w;
+}
+
+static unsigned nblk(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
+
+/// backward_endpoints (src/reach_solver.cpp:54-83).
+static void backward_endpoints(rp_ctx* ctx, const rp_quiver* q, V3 target, double L4,
+                               const rp_reach_params& rp, std::vector<V3>& pts,
+                               std::vector<V3>& dirs, std::vector<int>& cone) {
+  const V3 axis{rp.approach_axis[0], rp.approach_axis[1], rp.approach_axis[2]};
+  if (rp.mode == RP_MODE_6DOF) {
+    pts.push_back(target);
+    dirs.push_back(V3{0, 0, 0});
+    cone.push_back(-1);
+    return;
+  }
+  if (rp.approach_half_angle == 0.0) {
+    require(std::abs(rpd::norm(axis) - 1.0) <= 1e-9, RP_E_INVALID_PARAMETER,
+            "approach_axis must be unit");
+    pts.push_back(target - L4 * axis);
+    dirs.push_back(axis);
+    cone.push_back(-1);
+    return;
+  }
+  int32_t cnt = 0;
+  std::vector<int32_t> idx(q->n);
+  rp_status st = rp_cone_subset(ctx, q, rp.approach_axis, rp.approach_half_angle, idx.data(),
+                                q->n, &cnt);
+  if (st != RP_OK) throw Fail{st, rp_last_error()};
+  require(cnt > 0, RP_E_EMPTY_CONE,
+          "no quiver vector inside the approach cone; widen the cone or refine the quiver");
+  for (int k = 0; k < cnt; ++k) {
+    const int i = idx[k];
+    const V3 d{q->host_xyz[3 * i], q->host_xyz[3 * i + 1], q->host_xyz[3 * i + 2]};
+    pts.push_back(target - L4 * d);
+    dirs.push_back(d);
+    cone.push_back(i);
+  }
+}
+
+static HostShortcut host_shortcut(const rp_solution_set* s, const ShortcutRec& r) {
+  const SolveDev& a = s->sd;
+  const ArmDev& arm = a.arm;
+  const std::vector<double>& qx = s->quiver->host_xyz;
+  auto q = [&](int i) { return V3{qx[3 * i], qx[3 * i + 1], qx[3 * i + 2]}; };
+  HostShortcut h;
+  h.segment_index = r.segment_index;
+  h.seg1 = r.seg1;
+  h.seg2 = r.seg2;
+  h.hit = r.hit;
+  h.has_bridge = r.has_bridge != 0;
+  h.via_direct = r.via_direct != 0;
+  h.bridge = r.bridge;
+  h.path_length = r.path_length;
+  const V3 d1 = q(r.seg1);
+  V3 link1 = arm.root;
+  rpd::FrameStep st{};
+  if (arm.any_limit || arm.has_offsets) st = rpd::advance_frame(arm.base, d1);
+  if (arm.off[0] > 0.0) link1 = arm.root + arm.off[0] * rpd::m_col(st.after_azimuth, 0);
+  const V3 p1 = link1 + arm.L[0] * d1;
+  V3 link = link1, end = p1;
+  DevPose basis{};
+  basis.seg[0] = arm.L[0] * d1;
+  basis.qidx[0] = r.seg1;
+  basis.nseg = 1;
+  if (r.segment_index == 2) {
+    const V3 d2 = q(r.seg2);
+    link = p1;
+    if (arm.off[1] > 0.0) {
+      const rpd::FrameStep st2 = rpd::advance_frame(st.frame, d2);
+      link = p1 + arm.off[1] * rpd::m_col(st2.after_azimuth, 0);
+    }
+    end = link + arm.L[1] * d2;
+    const V3 pd = p1 - link1;
+    for (int k = 1; k <= a.n; ++k) h.prefix.push_back(rpd::walk_sample(link1, pd, k, a.n));
+    basis.seg[1] = arm.L[1] * d2;
+    basis.qidx[1] = r.seg2;
+    basis.nseg = 2;
+  }
+  if (h.via_direct) {
+    const V3 dd = a.target - r.origin;
+    for (int k = 1; k <= r.n_direct; ++k)
+      h.sublength.push_back(rpd::walk_sample(r.origin, dd, k, r.n_direct));
+  } else {
+    const V3 diff = end - link;
+    for (int k = 1; k <= r.hit; ++k) h.sublength.push_back(rpd::walk_sample(link, diff, k, a.n));
+  }
+  build_chain(arm, basis);
+  basis.n_wp_links = 0;
+  h.basis = host_pose_from_dev(basis);
+  return h;
+}
+
+rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q, const rp_grid* g,
+                             V3 target, const rp_reach_params& rp) {
+  validate_arm(arm);
+  validate_reach(rp);
+  if (rp.mode == RP_MODE_8DOF) {
+    require(arm.n_segments == 4, RP_E_INVALID_PARAMETER, "8DOF solve needs 4 segments");
+  } else {
+    require(arm.n_segments >= 3, RP_E_INVALID_PARAMETER, "6DOF solve needs 3 segments");
+  }
+  const double off2 = arm.n_offsets > 2 ? arm.offsets[2] : 0.0;
+  const double off3 = arm.n_offsets > 3 ? arm.offsets[3] : 0.0;
+  require(off2 == 0.0 && off3 == 0.0, RP_E_INVALID_PARAMETER,
+          "reach solving supports joint offsets at joints 1 and 2 only");
+  require(q && g && q->ctx == ctx && g->ctx == ctx, RP_E_INVALID_PARAMETER,
+          "quiver / grid belong to another context");
+
+  auto* s = new rp_solution_set();
+  try {
+    s->ctx = ctx;
+    s->quiver = q;
+    s->arm = arm;
+    s->rp = rp;
+    s->target[0] = target.x;
+    s->target[1] = target.y;
+    s->target[2] = target.z;
+    cudaStream_t st = ctx->stream;
+    const bool eight = rp.mode == RP_MODE_8DOF;
+    const double L4 = eight ? arm.lengths[3] : 0.0;
+    backward_endpoints(ctx, q, target, L4, rp, s->h_bpts, s->h_bdirs, s->h_bcone);
+    s->B = static_cast<int>(s->h_bpts.size());
+
+    SolveDev& a = s->sd;
+    a.g = g->view();
+    a.arm = make_arm_dev(arm);
+    a.n = rp.n_samples;
+    a.eight = eight ? 1 : 0;
+    a.Q = q->n;
+    a.B = s->B;
+    a.scanning = 1;
+    a.cone_precheck = rp.cone_precheck;
+    a.disable_prune = rp.disable_geom_pruning;
+    const double eps = resolved_epsilon(arm, rp);
+    const double L3 = arm.lengths[2];
+    a.eps = eps;
+    a.coarse2 = (L3 + eps) * (L3 + eps) * (1.0 + 1e-12);
+    double budget = arm.lengths[1] + arm.lengths[2] + eps;
+    if (eight) budget += arm.lengths[3];
+    budget += 1e-9;
+    a.budget2 = budget * budget;
+    a.near_r = resolved_near_radius(arm, rp);
+    a.spacing = nominal_spacing(arm, rp);
+    a.L4 = L4;
+    a.target = target;
+    a.qx = q->d_soa;
+    a.qy = q->d_soa + q->n;
+    a.qz = q->d_soa + 2 * static_cast<size_t>(q->n);
+    s->bpts.alloc(s->B + 1, st);
+    s->bdirs.alloc(s->B + 1, st);
+    s->bcone.alloc(s->B + 1, st);
+    s->walk4.alloc(s->B + 1, st);
+    copy_to_device(ctx, s->bpts.p, s->h_bpts.data(), s->B * sizeof(V3));
+    copy_to_device(ctx, s->bdirs.p, s->h_bdirs.data(), s->B * sizeof(V3));
+    copy_to_device(ctx, s->bcone.p, s->h_bcone.data(), s->B * sizeof(int));
+    a.bpts = s->bpts.p;
+    a.bdirs = s->bdirs.p;
+    a.bcone = s->bcone.p;
+    a.walk4_ok = s->walk4.p;
+    DevBuf<V3> tg(1, st);
+    copy_to_device(ctx, tg.p, &target, sizeof(V3));
+    a.targets = tg.p;
+    a.n_targets = 1;
+    if (eight) launch(ctx, "walk4", k_walk4, dim3(nblk(s->B, 128)), dim3(128), 0, a, s->walk4.p);
+
+    DevBuf<unsigned long long> ctr(C_COUNT, st);
+    ctr.zero();
+    DevBuf<unsigned> sc_count(1, st);
+    sc_count.zero();
+    DevBuf<long long> sc_list(kShortcutCap, st);
+    const int qwords = (q->n + 31) / 32;
+    DevBuf<uint32_t> surv_bits(qwords, st);
+    launch(ctx, "seg1", k_seg1, dim3(nblk(q->n, 256)), dim3(256), 0, a, surv_bits.p, ctr.p,
+           sc_list.p, sc_count.p);
+    DevBuf<int> surv_idx(q->n + 1, st), surv_cnt(1, st);
+    launch(ctx, "compact", k_compact_small, dim3(1), dim3(1024), 0,
+           static_cast<const uint32_t*>(surv_bits.p), q->n, surv_idx.p, surv_cnt.p);
+    int S1 = 0;
+    copy_to_host(ctx, &S1, surv_cnt.p, sizeof(int));
+    s->S1 = S1;
+    s->surv.alloc(S1 + 1, st);
+    if (S1 > 0)
+      launch(ctx, "seg1", k_surv_data, dim3(nblk(S1, 128)), dim3(128), 0, a,
+             static_cast<const int*>(surv_idx.p), S1, s->surv.p);
+    s->surv_i.resize(S1);
+    copy_to_host(ctx, s->surv_i.data(), surv_idx.p, S1 * sizeof(int));
+
+    s->n_pairs = static_cast<int64_t>(S1) * q->n;
+    const int64_t nbits = s->n_pairs * s->B;
+    const int64_t nwords = (nbits + 31) / 32 + 1;
+    s->sol_bits.alloc(nwords, st);
+    const bool B1 = s->B == 1;
+    if (!B1) s->sol_bits.zero();
+    const bool general = a.arm.any_limit || a.arm.has_offsets || (rp.cone_precheck && eight);
+    const int threads = 256;
+    int blocks = ctx->sm_count * 8;
+    const int64_t need = (s->n_pairs + threads - 1) / threads;
+    if (need < blocks) blocks = static_cast<int>(std::max<int64_t>(1, need));
+    DevBuf<BestRec> bb(blocks, st), best(1, st);
+    if (s->n_pairs > 0) {
+      auto run = [&](auto kern) {
+        launch(ctx, "seg2", kern, dim3(blocks), dim3(threads), 0, a,
+               static_cast<const SurvDev*>(s->surv.p), s->n_pairs, s->sol_bits.p, ctr.p,
+               sc_list.p, sc_count.p, bb.p);
+      };
+      if (eight) {
+        if (general) B1 ? run(k_seg2<true, true, true>) : run(k_seg2<true, true, false>);
+        else B1 ? run(k_seg2<true, false, true>) : run(k_seg2<true, false, false>);
+      } else {
+        if (general) B1 ? run(k_seg2<false, true, true>) : run(k_seg2<false, true, false>);
+        else B1 ? run(k_seg2<false, false, true>) : run(k_seg2<false, false, false>);
+      }
+      launch(ctx, "select", k_best_final, dim3(1), dim3(256), 0,
+             static_cast<const BestRec*>(bb.p), blocks, best.p);
+    }
+    unsigned long long hc[C_COUNT];
+    copy_to_host(ctx, hc, ctr.p, sizeof(hc));
+    unsigned nsc = 0;
+    copy_to_host(ctx, &nsc, sc_count.p, sizeof(unsigned));
+    require(nsc <= kShortcutCap, RP_E_CAPACITY_EXCEEDED, "too many near-encounter hypotheses");
+    BestRec hb{0.0, -1};
+    if (s->n_pairs > 0) copy_to_host(ctx, &hb, best.p, sizeof(BestRec));
+
+    rp_solve_stats& S = s->stats;
+    std::memset(&S, 0, sizeof(S));
+    S.seg1_candidates = q->n;
+    S.seg1_limit_pass = hc[C_SEG1_LIMIT];
+    S.seg1_reach_pass = hc[C_SEG1_REACH];
+    S.seg1_survivors = hc[C_SEG1_SURV];
+    S.pair_candidates = s->n_pairs;
+    S.seg2_limit_pass = hc[C_SEG2_LIMIT];
+    S.seg2_clear_pass = hc[C_SEG2_CLEAR];
+    S.gap_tested = hc[C_GAP_TESTED];
+    S.gap_pass = hc[C_GAP_PASS];
+    S.joint_pass = hc[C_JOINT_PASS];
+    S.v3_clear_pass = hc[C_V3_CLEAR];
+    S.solutions = hc[C_SOLUTIONS];
+    s->n_solutions = S.solutions;
+    s->best_key = S.solutions > 0 ? hb.key : -1;
+    s->best_len = hb.len;
+
+    if (nsc > 0) {
+      DevBuf<long long> sorted(nsc, st);
+      size_t tmp_bytes = 0;
+      cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, sc_list.p, sorted.p, static_cast<int>(nsc),
+                                     0, 64, st);
+      DevBuf<unsigned char> tmp(tmp_bytes, st);
+      RP_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, sc_list.p, sorted.p,
+                                             static_cast<int>(nsc), 0, 64, st));
+      DevBuf<ShortcutRec> recs(nsc, st);
+      launch(ctx, "shortcuts", k_shortcuts, dim3(nblk(nsc, 128)), dim3(128), 0, a,
+             static_cast<const SurvDev*>(s->surv.p), static_cast<const long long*>(sorted.p),
+             static_cast<int>(nsc), recs.p);
+      std::vector<ShortcutRec> h(nsc);
+      copy_to_host(ctx, h.data(), recs.p, nsc * sizeof(ShortcutRec));
+      for (const auto& r : h)
+        if (r.valid) s->shortcuts.push_back(host_shortcut(s, r));
+    }
+    S.shortcuts_found = static_cast<int64_t>(s->shortcuts.size());
+  } catch (...) {
+    delete s;
+    throw;
+  }
+  return s;
+}
+
+void ensure_keys(rp_solution_set* s) {
+  if (s->keys_ready) return;
+  rp_ctx* ctx = s->ctx;
+  cudaStream_t st = ctx->stream;
+  s->keys.alloc(s->n_solutions + 1, st);
+  if (s->n_solutions > 0) {
+    const int64_t nw = (s->n_pairs * s->B + 31) / 32;
+    DevBuf<unsigned long long> cnt(nw, st), off(nw, st);
+    launch(ctx, "compact", k_word_popc, dim3(nblk(nw, 256)), dim3(256), 0,
+           static_cast<const uint32_t*>(s->sol_bits.p), nw, cnt.p);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.p, off.p, nw, st);
+    DevBuf<unsigned char> tmp(tb, st);
+    RP_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.p, off.p, nw, st));
+    launch(ctx, "compact", k_scatter_bits, dim3(nblk(nw, 256)), dim3(256), 0,
+           static_cast<const uint32_t*>(s->sol_bits.p), nw,
+           static_cast<const unsigned long long*>(off.p), s->keys.p);
+  }
+  s->keys_ready = true;
+}
+
+void materialize_solutions(rp_solution_set* s, const long long* d_keys, const long long* h_keys,
+                           int64_t n, DevPose* d_out) {
+  if (n <= 0) return;
+  DevBuf<long long> tmp;
+  const long long* keys = d_keys;
+  if (!keys) {
+    tmp.alloc(n, s->ctx->stream);
+    copy_to_device(s->ctx, tmp.p, h_keys, n * sizeof(long long));
+    keys = tmp.p;
+  }
+  launch(s->ctx, "materialize", k_materialize, dim3(nblk(n, 128)), dim3(128), 0, s->sd,
+         static_cast<const SurvDev*>(s->surv.p), keys, n, d_out);
+}
+
+static long long key_of_ordinal(rp_solution_set* s, int64_t ordinal) {
+  ensure_keys(s);
+  long long key = 0;
+  copy_to_host(s->ctx, &key, s->keys.p + ordinal, sizeof(long long));
+  return key;
+}
+
+DevPose solution_dev_pose_by_key(rp_solution_set* s, long long key) {
+  DevBuf<DevPose> d(1, s->ctx->stream);
+  materialize_solutions(s, nullptr, &key, 1, d.p);
+  DevPose h;
+  copy_to_host(s->ctx, &h, d.p, sizeof(DevPose));
+  return h;
+}
+
+DevPose solution_dev_pose(rp_solution_set* s, int64_t ordinal) {
+  return solution_dev_pose_by_key(s, key_of_ordinal(s, ordinal));
+}
+
+HostPose solution_pose(rp_solution_set* s, int64_t ordinal) {
+  return host_pose_from_dev(solution_dev_pose(s, ordinal));
+}
+
+static int64_t rank_of_key(const rp_solution_set* s, long long key) {
+  DevBuf<unsigned long long> c(1, s->ctx->stream);
+  c.zero();
+  launch(s->ctx, "select", k_rank, dim3(s->ctx->sm_count), dim3(256), 0,
+         static_cast<const uint32_t*>(s->sol_bits.p), key, c.p);
+  unsigned long long h = 0;
+  copy_to_host(s->ctx, &h, c.p, sizeof(h));
+  return static_cast<int64_t>(h);
+}
+
+rp_chosen select(const rp_solution_set* s) {
+  require(s->n_solutions > 0 || !s->shortcuts.empty(), RP_E_NO_SOLUTION,
+          "no reach solution under the given constraints");
+  rp_chosen c{};
+  if (!s->shortcuts.empty()) {
+    size_t best = 0;
+    for (size_t k = 1; k < s->shortcuts.size(); ++k)
+      if (s->shortcuts[k].path_length < s->shortcuts[best].path_length) best = k;
+    c.kind = RP_CHOSEN_SHORTCUT;
+    c.index = static_cast<int64_t>(best);
+    c.path_length = s->shortcuts[best].path_length;
+    return c;
+  }
+  c.kind = RP_CHOSEN_REACH_POSE;
+  c.index = rank_of_key(s, s->best_key);
+  c.path_length = s->best_len;
+  return c;
+}
+
+}  // namespace rp
+
+using namespace rp;
+
+extern "C" {
+
+rp_status rp_cone_subset(rp_ctx* ctx, const rp_quiver* q, const double axis[3], double half,
+                         int32_t* idx, int32_t cap, int32_t* n_out) {
+  return guarded([&] {
+    const V3 ax{axis[0], axis[1], axis[2]};
+    require(std::abs(rpd::norm(ax) - 1.0) <= 1e-9, RP_E_INVALID_PARAMETER,
+            "cone axis must be unit");
+    require(half >= 0.0 && half <= 3.14159265358979323846, RP_E_INVALID_PARAMETER,
+            "half_angle must be in [0, pi]");
+    const double limit = half + 1e-12;
+    DevBuf<uint8_t> in(q->n, ctx->stream), amb(q->n, ctx->stream);
+    launch(ctx, "cone", k_cone, dim3(nblk(q->n, 256)), dim3(256), 0,
+           static_cast<const double*>(q->d_soa), static_cast<const double*>(q->d_soa + q->n),
+           static_cast<const double*>(q->d_soa + 2 * static_cast<size_t>(q->n)), q->n, ax, limit,
+           in.p, amb.p);
+    std::vector<uint8_t> hin(q->n), hamb(q->n);
+    copy_to_host(ctx, hin.data(), in.p, q->n);
+    copy_to_host(ctx, hamb.data(), amb.p, q->n);
+    int32_t cnt = 0;
+    for (int i = 0; i < q->n; ++i) {
+      bool inside = hin[i] != 0;
+      if (hamb[i]) {  // within 1e-9 rad of the boundary: decide with glibc atan2
+        const V3 v{q->host_xyz[3 * i], q->host_xyz[3 * i + 1], q->host_xyz[3 * i + 2]};
+        inside = std::atan2(rpd::norm(rpd::cross(v, ax)), rpd::dot(v, ax)) <= limit;
+      }
+      if (inside) {
+        if (cnt < cap) idx[cnt] = i;
+        ++cnt;
+      }
+    }
+    *n_out = cnt;
+  });
+}
+
+rp_status rp_prune_segment1(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q, const rp_grid* g,
+                            const double* targets, int32_t n_targets, const rp_reach_params* rp,
+                            int32_t* survivors, int32_t cap, int32_t* n_out,
+                            rp_solve_stats* stats) {
+  return guarded([&] {
+    cudaStream_t st = ctx->stream;
+    SolveDev a{};
+    a.g = g->view();
+    a.arm = make_arm_dev(*arm);
+    a.n = rp->n_samples;
+    a.eight = rp->mode == RP_MODE_8DOF;
+    a.Q = q->n;
+    a.disable_prune = rp->disable_geom_pruning;
+    const double eps = resolved_epsilon(*arm, *rp);
+    double budget = arm->lengths[1] + arm->lengths[2] + eps;
+    if (a.eight) budget += arm->lengths[3];
+    budget += 1e-9;
+    a.budget2 = budget * budget;
+    a.spacing = nominal_spacing(*arm, *rp);
+    a.near_r = resolved_near_radius(*arm, *rp);
+    a.qx = q->d_soa;
+    a.qy = q->d_soa + q->n;
+    a.qz = q->d_soa + 2 * static_cast<size_t>(q->n);
+    DevBuf<V3> tg(std::max(1, n_targets), st);
+    copy_to_device(ctx, tg.p, targets, n_targets * sizeof(V3));
+    a.targets = tg.p;
+    a.n_targets = n_targets;
+    a.scanning = 0;
+    DevBuf<unsigned long long> ctr(C_COUNT, st);
+    ctr.zero();
+    DevBuf<unsigned> scc(1, st);
+    scc.zero();
+    DevBuf<long long> scl(1, st);
+    DevBuf<uint32_t> bits((q->n + 31) / 32, st);
+    launch(ctx, "seg1", k_seg1, dim3(nblk(q->n, 256)), dim3(256), 0, a, bits.p, ctr.p, scl.p,
+           scc.p);
+    DevBuf<int> idx(q->n + 1, st), cnt(1, st);
+    launch(ctx, "compact", k_compact_small, dim3(1), dim3(1024), 0,
+           static_cast<const uint32_t*>(bits.p), q->n, idx.p, cnt.p);
+    int S1 = 0;
+    copy_to_host(ctx, &S1, cnt.p, sizeof(int));
+    std::vector<int> h(S1);
+    copy_to_host(ctx, h.data(), idx.p, S1 * sizeof(int));
+    for (int k = 0; k < S1 && k < cap; ++k) survivors[k] = h[k];
+    *n_out = S1;
+    if (stats) {
+      unsigned long long hc[C_COUNT];
+      copy_to_host(ctx, hc, ctr.p, sizeof(hc));
+      std::memset(stats, 0, sizeof(*stats));
+      stats->seg1_candidates = q->n;
+      stats->seg1_limit_pass = hc[C_SEG1_LIMIT];
+      stats->seg1_reach_pass = hc[C_SEG1_REACH];
+      stats->seg1_survivors = hc[C_SEG1_SURV];
+    }
+  });
+}
+
+rp_status rp_solve_reach(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q, const rp_grid* g,
+                         const double target[3], const rp_reach_params* rp, rp_solution_set** out) {
+  return guarded([&] {
+    *out = solve_reach(ctx, *arm, q, g, V3{target[0], target[1], target[2]}, *rp);
+  });
+}
+
+rp_status rp_solution_set_stats(const rp_solution_set* s, rp_solve_stats* stats) {
+  return guarded([&] { *stats = s->stats; });
+}
+
+rp_status rp_solution_set_sizes(const rp_solution_set* s, int64_t* ns, int64_t* nc) {
+  return guarded([&] {
+    if (ns) *ns = s->n_solutions;
+    if (nc) *nc = static_cast<int64_t>(s->shortcuts.size());
+  });
+}
+
+rp_status rp_solution_set_keys(const rp_solution_set* cs, int32_t* keys, int64_t cap) {
+  return guarded([&] {
+    auto* s = const_cast<rp_solution_set*>(cs);
+    ensure_keys(s);
+    const int64_t n = std::min<int64_t>(cap, s->n_solutions);
+    std::vector<long long> k(n);
+    copy_to_host(s->ctx, k.data(), s->keys.p, n * sizeof(long long));
+    for (int64_t t = 0; t < n; ++t) {
+      const long long p = k[t] / s->B;
+      const int bi = static_cast<int>(k[t] - p * s->B);
+      const int sidx = static_cast<int>(p / s->sd.Q);
+      keys[3 * t] = s->surv_i[sidx];
+      keys[3 * t + 1] = static_cast<int>(p - static_cast<long long>(sidx) * s->sd.Q);
+      keys[3 * t + 2] = s->sd.eight ? s->h_bcone[bi] : -1;
+    }
+  });
+}
+
+rp_status rp_solution_set_pose(const rp_solution_set* cs, int64_t k, rp_pose* pose, double* wps,
+                               int32_t cap) {
+  return guarded([&] {
+    auto* s = const_cast<rp_solution_set*>(cs);
+    require(k >= 0 && k < s->n_solutions, RP_E_INVALID_PARAMETER, "solution index out of range");
+    to_abi(solution_pose(s, k), pose, wps, cap);
+  });
+}
+
+rp_status rp_solution_set_shortcut(const rp_solution_set* s, int64_t k, rp_shortcut* sc,
+                                   double* tip, int32_t cap, int32_t* n_tip) {
+  return guarded([&] {
+    require(k >= 0 && k < static_cast<int64_t>(s->shortcuts.size()), RP_E_INVALID_PARAMETER,
+            "shortcut index out of range");
+    const HostShortcut& h = s->shortcuts[k];
+    std::memset(sc, 0, sizeof(*sc));
+    sc->segment_index = h.segment_index;
+    sc->hit_sample_index = h.hit;
+    sc->seg1_index = h.seg1;
+    sc->seg2_index = h.seg2;
+    sc->has_bridge = h.has_bridge;
+    sc->via_origin_direct = h.via_direct;
+    sc->n_prefix = static_cast<int>(h.prefix.size());
+    sc->n_sublength = static_cast<int>(h.sublength.size());
+    sc->bridge[0] = h.bridge.x;
+    sc->bridge[1] = h.bridge.y;
+    sc->bridge[2] = h.bridge.z;
+    sc->path_length = h.path_length;
+    const auto w = h.tip_waypoints(V3{s->target[0], s->target[1], s->target[2]});
+    if (n_tip) *n_tip = static_cast<int>(w.size());
+    if (tip)
+      for (int q = 0; q < static_cast<int>(w.size()) && q < cap; ++q) {
+        tip[3 * q] = w[q].x;
+        tip[3 * q + 1] = w[q].y;
+        tip[3 * q + 2] = w[q].z;
+      }
+  });
+}
+
+rp_status rp_solution_set_destroy(rp_solution_set* s) {
+  return guarded([&] {
+    if (!s) return;
+    cudaStreamSynchronize(s->ctx->stream);
+    delete s;
+  });
+}
+
+rp_status rp_select_solution(const rp_solution_set* s, rp_chosen* out) {
+  return guarded([&] { *out = select(s); });
+}
+
+}  // extern "C"
