@@ -226,6 +226,10 @@ rp_status rp_grid_dilate(rp_grid* g, double radius);
  * mark_obstacles(boxes) then dilate(radius) when the grid holds no other
  * occupancy; see DESIGN.md. */
 rp_status rp_grid_mark_dilate_boxes(rp_grid* g, const rp_obstacle* obs, int32_t n, double radius);
+/* Benchmark helper: the fused mark + dilate of `obs` onto g (overwriting it)
+ * `reps` times back to back on the ctx stream; *ms = device time per pass. */
+rp_status rp_grid_mark_dilate_repeat(rp_grid* g, const rp_obstacle* obs, int32_t n, double radius,
+                                     int32_t reps, double* ms);
 /* [build_scene_grid, src/pipeline.cpp:17-34] dilation < 0 = effective_dilation */
 rp_status rp_build_scene_grid(rp_ctx* ctx, const double bounds_min[3], const double bounds_max[3],
                               double voxel_size, double dilation, const rp_obstacle* obs,

@@ -66,7 +66,9 @@ def lib():
         "rp_grid_mark": ([vp, P(abi.Obstacle), C.c_int32], C.c_int32),
         "rp_grid_dilate": ([vp, C.c_double], C.c_int32),
         "rp_grid_mark_dilate_boxes": ([vp, P(abi.Obstacle), C.c_int32, C.c_double], C.c_int32),
-        "rp_build_scene_grid": ([vp, d3, d3, C.c_double, C.c_double, P(abi.Obstacle), C.c_int32,
+        "rp_grid_mark_dilate_repeat": ([vp, P(abi.Obstacle), C.c_int32, C.c_double, C.c_int32,
+                                        P(C.c_double)], C.c_int32),
+        "rp_build_scene_grid":([vp, d3, d3, C.c_double, C.c_double, P(abi.Obstacle), C.c_int32,
                                  P(abi.Arm), P(abi.ReachParams), P(vp)], C.c_int32),
         "rp_grid_overlay": ([vp, P(abi.Obstacle), P(vp)], C.c_int32),
         "rp_grid_info": ([vp, P(C.c_int32), d3, P(C.c_double), P(C.c_double)], C.c_int32),
@@ -253,6 +255,12 @@ class Grid:
     def mark_dilate(self, obstacles, radius):
         _check(lib().rp_grid_mark_dilate_boxes(self.h, abi.obstacle_array(obstacles),
                                                len(obstacles), radius))
+
+    def mark_dilate_repeat(self, obstacles, radius, reps) -> float:
+        ms = C.c_double()
+        _check(lib().rp_grid_mark_dilate_repeat(self.h, abi.obstacle_array(obstacles),
+                                                len(obstacles), radius, reps, C.byref(ms)))
+        return ms.value
 
     def overlay(self, obstacle, into: "Grid | None" = None) -> "Grid":
         h = C.c_void_p(into.h.value if into is not None else 0)

@@ -250,6 +250,12 @@ rp_status rp_ctx_create(int32_t device, rp_ctx** out) {
     cudaDeviceProp prop;
     RP_CUDA(cudaGetDeviceProperties(&prop, device));
     c->sm_count = prop.multiProcessorCount;
+    // Keep freed stream-ordered allocations cached in the pool: solves and
+    // plans allocate their scratch per call.
+    cudaMemPool_t pool;
+    RP_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;
+    RP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     *out = c;
   });
 }

@@ -102,35 +102,166 @@ __device__ __forceinline__ uint64_t range_mask(int lo, int hi, int base) {
 __global__ void __launch_bounds__(256) k_mark_dilate_rows(uint64_t* __restrict__ bits, GridView g,
                                                           const Prim* __restrict__ prims, int np,
                                                           const int* __restrict__ wtab, int reach,
-                                                          int y0, int ny_rows, int z0,
-                                                          int accumulate) {
-  extern __shared__ Prim sp[];
-  for (int k = threadIdx.x; k < np; k += blockDim.x) sp[k] = prims[k];
+                                                          int y0, int y1, int z0, int z1, int tw,
+                                                          int ty, int tz, int accumulate) {
+  // Tile: planes [zt, zt+tz), rows [yt, yt+ty), words [wt, wt+tw);
+  // tw*ty == blockDim; each thread writes tz words of one (y, word) column.
+  // dynamic smem: [all prims][culled prims][width table]
+  extern __shared__ Prim sp_all[];
+  Prim* sp = sp_all + np;
+  int* swt = reinterpret_cast<int*>(sp_all + 2 * np);
+  __shared__ int ns;
+  const int zt = z0 + static_cast<int>(blockIdx.z) * tz;
+  const int yt = y0 + static_cast<int>(blockIdx.y) * ty;
+  const int wt = static_cast<int>(blockIdx.x) * tw;
+  if (threadIdx.x == 0) ns = 0;
+  // coalesced staging of the primitive list and the width table
+  {
+    const int* src = reinterpret_cast<const int*>(prims);
+    int* dst = reinterpret_cast<int*>(sp_all);
+    for (int k = threadIdx.x; k < 6 * np; k += blockDim.x) dst[k] = __ldg(src + k);
+    const int nw = 2 * reach * reach + 1;
+    for (int k = threadIdx.x; k < nw; k += blockDim.x) swt[k] = __ldg(wtab + k);
+  }
   __syncthreads();
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t per_plane = static_cast<int64_t>(ny_rows) * g.wx;
-  const int z = z0 + static_cast<int>(t / per_plane);
-  const int rem = static_cast<int>(t % per_plane);
-  const int y = y0 + rem / g.wx;
-  const int ww = rem % g.wx;
-  if (z >= g.nz || y >= g.ny || z < 0 || y < 0) return;
-  const int base = ww * 64;
-  uint64_t m = 0;
-  for (int k = 0; k < np; ++k) {
-    const Prim p = sp[k];
+  // cull the primitives that can reach this tile (distance <= reach on
+  // every axis); most tiles see one or two boxes instead of all of them
+  const int xlo_t = wt * 64, xhi_t = (wt + tw) * 64 - 1;
+  const int yhi_t = yt + ty - 1, zhi_t = zt + tz - 1;
+  for (int k = threadIdx.x; k < np; k += blockDim.x) {
+    const Prim p = sp_all[k];
     if (p.a[0] > p.b[0] || p.a[1] > p.b[1] || p.a[2] > p.b[2]) continue;
+    if (p.a[2] - reach > zhi_t || p.b[2] + reach < zt) continue;
+    if (p.a[1] - reach > yhi_t || p.b[1] + reach < yt) continue;
+    if (p.a[0] - reach > xhi_t || p.b[0] + reach < xlo_t) continue;
+    sp[atomicAdd(&ns, 1)] = p;
+  }
+  __syncthreads();
+  const int y = yt + static_cast<int>(threadIdx.x) / tw;
+  const int ww = wt + static_cast<int>(threadIdx.x) % tw;
+  if (y > y1 || y >= g.ny || ww >= g.wx) return;
+  const int base = ww * 64;
+  const int n_here = ns;
+  for (int z = zt; z < zt + tz && z <= z1 && z < g.nz; ++z) {
+    uint64_t m = 0;
+    for (int k = 0; k < n_here; ++k) {
+      const Prim p = sp[k];
+      const int dy = y < p.a[1] ? p.a[1] - y : (y > p.b[1] ? y - p.b[1] : 0);
+      const int dz = z < p.a[2] ? p.a[2] - z : (z > p.b[2] ? z - p.b[2] : 0);
+      if (dy > reach || dz > reach) continue;
+      const int w = swt[dy * dy + dz * dz];
+      if (w < 0) continue;
+      int lo = p.a[0] - w, hi = p.b[0] + w;
+      lo = lo < 0 ? 0 : lo;
+      hi = hi > g.nx - 1 ? g.nx - 1 : hi;
+      m |= range_mask(lo, hi, base);
+    }
+    const size_t idx = (static_cast<size_t>(z) * g.ny + y) * g.wx + ww;
+    bits[idx] = accumulate ? (bits[idx] | m) : m;
+  }
+}
+
+constexpr int kRowsTz = 4;  // z-planes per block of k_mark_dilate_rows
+
+/// Row-per-thread variant for rows of WX words (WX in {1,2,4,8}): each
+/// thread computes every primitive's x-interval for its row once, builds the
+/// WX words in registers and writes them with 16-byte stores. Block tile =
+/// 32 rows (y) x 8 planes (z); primitives culled to the tile in smem.
+template <int WX>
+__global__ void __launch_bounds__(256) k_mark_dilate_rowwise(uint64_t* __restrict__ bits, GridView g,
+                                                             const Prim* __restrict__ prims, int np,
+                                                             const int* __restrict__ wtab, int reach,
+                                                             int y0, int y1, int z0, int z1,
+                                                             int accumulate) {
+  extern __shared__ Prim sp_all[];
+  Prim* sp = sp_all + np;
+  int* swt = reinterpret_cast<int*>(sp_all + 2 * np);
+  __shared__ int ns;
+  const int yt = y0 + static_cast<int>(blockIdx.x) * 32;
+  const int zt = z0 + static_cast<int>(blockIdx.y) * 8;
+  if (threadIdx.x == 0) ns = 0;
+  {
+    const int* src = reinterpret_cast<const int*>(prims);
+    int* dst = reinterpret_cast<int*>(sp_all);
+    for (int k = threadIdx.x; k < 6 * np; k += blockDim.x) dst[k] = __ldg(src + k);
+    const int nw = 2 * reach * reach + 1;
+    for (int k = threadIdx.x; k < nw; k += blockDim.x) swt[k] = __ldg(wtab + k);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < np; k += blockDim.x) {
+    const Prim p = sp_all[k];
+    if (p.a[0] > p.b[0] || p.a[1] > p.b[1] || p.a[2] > p.b[2]) continue;
+    if (p.a[2] - reach > zt + 7 || p.b[2] + reach < zt) continue;
+    if (p.a[1] - reach > yt + 31 || p.b[1] + reach < yt) continue;
+    sp[atomicAdd(&ns, 1)] = p;
+  }
+  __syncthreads();
+  const int y = yt + (threadIdx.x & 31);
+  const int z = zt + (threadIdx.x >> 5);
+  if (y > y1 || y >= g.ny || z > z1 || z >= g.nz) return;
+  uint64_t m[WX];
+#pragma unroll
+  for (int w = 0; w < WX; ++w) m[w] = 0;
+  const int n_here = ns;
+  for (int k = 0; k < n_here; ++k) {
+    const Prim p = sp[k];
     const int dy = y < p.a[1] ? p.a[1] - y : (y > p.b[1] ? y - p.b[1] : 0);
     const int dz = z < p.a[2] ? p.a[2] - z : (z > p.b[2] ? z - p.b[2] : 0);
     if (dy > reach || dz > reach) continue;
-    const int w = __ldg(wtab + dy * dy + dz * dz);
-    if (w < 0) continue;
-    int lo = p.a[0] - w, hi = p.b[0] + w;
+    const int wd = swt[dy * dy + dz * dz];
+    if (wd < 0) continue;
+    int lo = p.a[0] - wd, hi = p.b[0] + wd;
     lo = lo < 0 ? 0 : lo;
     hi = hi > g.nx - 1 ? g.nx - 1 : hi;
-    m |= range_mask(lo, hi, base);
+#pragma unroll
+    for (int w = 0; w < WX; ++w) m[w] |= range_mask(lo, hi, 64 * w);
   }
-  const size_t idx = (static_cast<size_t>(z) * g.ny + y) * g.wx + ww;
-  bits[idx] = accumulate ? (bits[idx] | m) : m;
+  uint64_t* row = bits + (static_cast<size_t>(z) * g.ny + y) * WX;
+  if (accumulate) {
+#pragma unroll
+    for (int w = 0; w < WX; ++w) m[w] |= row[w];
+  }
+  if (WX == 1) {
+    row[0] = m[0];
+  } else {
+#pragma unroll
+    for (int w = 0; w < WX; w += 2)
+      reinterpret_cast<ulonglong2*>(row)[w / 2] = make_ulonglong2(m[w], m[w + 1]);
+  }
+}
+
+/// dynamic shared memory of k_mark_dilate_rows: prims, culled prims, widths
+inline size_t rows_smem(int np, int reach) {
+  return 2 * static_cast<size_t>(np) * sizeof(Prim) +
+         static_cast<size_t>(2 * reach * reach + 1) * sizeof(int);
+}
+
+/// Launch the fused rasterise(+dilate) over rows [y0,y1] x [z0,z1].
+void launch_rows(rp_ctx* ctx, const char* name, rp_grid* g, const Prim* prims, int np,
+                 const int* wtab, int reach, int y0, int y1, int z0, int z1, bool accumulate) {
+  const size_t smem = rows_smem(np, reach);
+  const int acc = accumulate ? 1 : 0;
+  auto rowwise = [&](auto kern) {
+    const dim3 grid(static_cast<unsigned>((y1 - y0 + 32) / 32),
+                    static_cast<unsigned>((z1 - z0 + 8) / 8));
+    launch(ctx, name, kern, grid, dim3(256), smem, g->bits, g->view(), prims, np, wtab, reach, y0,
+           y1, z0, z1, acc);
+  };
+  switch (g->wx) {
+    case 1: rowwise(k_mark_dilate_rowwise<1>); return;
+    case 2: rowwise(k_mark_dilate_rowwise<2>); return;
+    case 4: rowwise(k_mark_dilate_rowwise<4>); return;
+    case 8: rowwise(k_mark_dilate_rowwise<8>); return;
+    default: break;
+  }
+  const int tw = std::min(g->wx, 256);
+  const int ty = 256 / tw;
+  const int tz = std::min(kRowsTz, z1 - z0 + 1);
+  const dim3 grid(static_cast<unsigned>((g->wx + tw - 1) / tw),
+                  static_cast<unsigned>((y1 - y0 + ty) / ty),
+                  static_cast<unsigned>((z1 - z0 + tz) / tz));
+  launch(ctx, name, k_mark_dilate_rows, grid, dim3(tw * ty), smem, g->bits, g->view(), prims, np,
+         wtab, reach, y0, y1, z0, z1, tw, ty, tz, acc);
 }
 
 /// Scatter-mark single cells (cloud points) with atomicOr.
@@ -352,11 +483,7 @@ void run_rows(rp_grid* g, const Prim* prims, int np, const DilTable& t, int y0, 
   if (y0 > y1 || z0 > z1) return;
   DevBuf<int> wtab(t.w.size(), ctx->stream);
   copy_to_device(ctx, wtab.p, t.w.data(), t.w.size() * sizeof(int));
-  const int ny_rows = y1 - y0 + 1;
-  const int64_t words = static_cast<int64_t>(z1 - z0 + 1) * ny_rows * g->wx;
-  launch(ctx, name, k_mark_dilate_rows, dim3(blocks_for(words, 256)), dim3(256),
-         static_cast<size_t>(np) * sizeof(Prim), g->bits, g->view(), prims, np, wtab.p, t.reach,
-         y0, ny_rows, z0, accumulate ? 1 : 0);
+  launch_rows(ctx, name, g, prims, np, wtab.p, t.reach, y0, y1, z0, z1, accumulate);
 }
 
 void dilate_general(rp_grid* g, double radius) {
@@ -365,12 +492,12 @@ void dilate_general(rp_grid* g, double radius) {
   DevBuf<int> wtab(t.w.size(), ctx->stream);
   copy_to_device(ctx, wtab.p, t.w.data(), t.w.size() * sizeof(int));
   uint64_t* out = nullptr;
-  RP_CUDA(cudaMalloc(&out, g->n_words * sizeof(uint64_t) + 8));
+  RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&out), g->n_words * sizeof(uint64_t) + 8,
+                          ctx->stream));
   launch(ctx, "dilate", k_dilate_general, dim3(blocks_for(static_cast<int64_t>(g->n_words), 256)),
          dim3(256), 0, static_cast<const uint64_t*>(g->bits), out, g->view(),
          static_cast<const int*>(wtab.p), t.reach);
-  RP_CUDA(cudaStreamSynchronize(ctx->stream));
-  RP_CUDA(cudaFree(g->bits));
+  RP_CUDA(cudaFreeAsync(g->bits, ctx->stream));
   g->bits = out;
 }
 
@@ -384,7 +511,8 @@ rp_grid* new_grid(rp_ctx* ctx, const double* origin, double vs, const int* dims)
   g->voxel_size = vs;
   g->wx = (dims[0] + 63) / 64;
   g->n_words = static_cast<size_t>(g->wx) * dims[1] * dims[2];
-  RP_CUDA(cudaMalloc(&g->bits, g->n_words * sizeof(uint64_t) + 8));
+  RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&g->bits), g->n_words * sizeof(uint64_t) + 8,
+                          ctx->stream));
   RP_CUDA(cudaMemsetAsync(g->bits, 0, g->n_words * sizeof(uint64_t), ctx->stream));
   return g;
 }
@@ -485,6 +613,50 @@ rp_status rp_grid_dilate(rp_grid* g, double radius) {
 
 rp_status rp_grid_mark_dilate_boxes(rp_grid* g, const rp_obstacle* obs, int32_t n, double radius) {
   return guarded([&] { grid_mark_dilate_boxes(g, obs, n, radius, true); });
+}
+
+rp_status rp_grid_mark_dilate_repeat(rp_grid* g, const rp_obstacle* obs, int32_t n, double radius,
+                                     int32_t reps, double* ms) {
+  return guarded([&] {
+    rp_ctx* ctx = g->ctx;
+    int64_t np = 0;
+    bool only_boxes = true;
+    DevBuf<Prim> prims = obstacles_to_prims(g, obs, n, &np, &only_boxes);
+    require(np > 0 && np <= kFusedPrimLimit, RP_E_INVALID_PARAMETER,
+            "repeat benchmark needs 1..512 primitives");
+    const DilTable t = make_table(radius, g->voxel_size);
+    DevBuf<int> wtab(t.w.size(), ctx->stream);
+    copy_to_device(ctx, wtab.p, t.w.data(), t.w.size() * sizeof(int));
+    // Capture the passes in a CUDA graph so the device runs them back to
+    // back: the events then bracket kernel time, not host launch rate.
+    const bool timing = ctx->timing;
+    ctx->timing = false;
+    cudaGraph_t graph;
+    cudaGraphExec_t exec;
+    RP_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    for (int r = 0; r < reps; ++r)
+      launch_rows(ctx, "mark_dilate", g, prims.p, static_cast<int>(np), wtab.p, t.reach, 0,
+                  g->dims[1] - 1, 0, g->dims[2] - 1, false);
+    RP_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
+    ctx->timing = timing;
+    RP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    RP_CUDA(cudaGraphLaunch(exec, ctx->stream));  // warm
+    cudaEvent_t e0, e1;
+    RP_CUDA(cudaEventCreate(&e0));
+    RP_CUDA(cudaEventCreate(&e1));
+    RP_CUDA(cudaEventRecord(e0, ctx->stream));
+    RP_CUDA(cudaGraphLaunch(exec, ctx->stream));
+    RP_CUDA(cudaEventRecord(e1, ctx->stream));
+    RP_CUDA(cudaEventSynchronize(e1));
+    float total = 0.f;
+    RP_CUDA(cudaEventElapsedTime(&total, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    *ms = total / std::max(1, reps);
+    g->empty = false;
+  });
 }
 
 rp_status rp_build_scene_grid(rp_ctx* ctx, const double bmin[3], const double bmax[3], double vs,
@@ -665,8 +837,7 @@ rp_status rp_grid_copy(const rp_grid* src, rp_grid** out) {
 rp_status rp_grid_destroy(rp_grid* g) {
   return guarded([&] {
     if (!g) return;
-    cudaStreamSynchronize(g->ctx->stream);
-    if (g->bits) cudaFree(g->bits);
+    if (g->bits) RP_CUDA(cudaFreeAsync(g->bits, g->ctx->stream));
     delete g;
   });
 }

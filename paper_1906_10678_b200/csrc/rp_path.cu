@@ -250,7 +250,7 @@ __device__ bool wik_eval(const WikDev& w, const CiData& c, int j, DevPose* out, 
 /// reference's cone that pass the joint-1 limit and the move1 bound, and
 /// segment-2 directions inside its cone (all directions for offset arms).
 __global__ void k_wik_filter(WikDev w, double cone1, double cone2, V3 u1, V3 u2,
-                             uint32_t* ibits, uint32_t* jbits) {
+                             uint32_t* ibits, uint32_t* jbits, CiData* ci_by_index) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   bool pi = false, pj = false;
   if (i < w.Q) {
@@ -260,13 +260,27 @@ __global__ void k_wik_filter(WikDev w, double cone1, double cone2, V3 u1, V3 u2,
     if (w.filter_j) in1 = atan2(rpd::norm(rpd::cross(q, u1)), rpd::dot(q, u1)) <= cone1;
     if (in1) {
       rpd::FrameStep st{};
-      if (arm.lim_active[0] || arm.off[0] > 0.0) st = rpd::advance_frame(arm.base, q);
+      if (arm.any_limit || arm.has_offsets) st = rpd::advance_frame(arm.base, q);
       bool ok = !arm.lim_active[0] || rpd::joint_angle_within(st.theta, st.phi, st.degenerate, arm.lim[0]);
       if (ok) {
         V3 link = arm.root;
-        if (arm.off[0] > 0.0) link = arm.root + arm.off[0] * rpd::m_col(st.after_azimuth, 0);
+        const bool elb = arm.off[0] > 0.0;
+        if (elb) link = arm.root + arm.off[0] * rpd::m_col(st.after_azimuth, 0);
         const V3 p1 = link + arm.L[0] * q;
-        pi = !(rpd::norm(p1 - w.prev_j1) > w.j1max);
+        const double move1 = rpd::norm(p1 - w.prev_j1);
+        pi = !(move1 > w.j1max);
+        if (pi) {
+          // segment-1 data and its (lazy in the reference) walk, once per i
+          CiData c;
+          c.i = i;
+          c.frame1 = st.frame;
+          c.link1 = link;
+          c.p1 = p1;
+          c.move1 = move1;
+          c.ok = (!elb || link_clear_scaled(w.g, arm.root, link, w.spacing)) &&
+                 rpd::walk_clear(w.g, link, p1, w.n);
+          ci_by_index[i] = c;
+        }
       }
     }
     pj = !w.filter_j || atan2(rpd::norm(rpd::cross(q, u2)), rpd::dot(q, u2)) <= cone2;
@@ -300,22 +314,7 @@ __global__ void __launch_bounds__(1024) k_wik_compact(WikDev w, WikScratch s) {
         x &= x - 1;
         const int idx = wd * 32 + b;
         if (which == 0) {
-          CiData c{};
-          c.i = idx;
-          const ArmDev& arm = w.arm;
-          const V3 q = wq(w, idx);
-          rpd::FrameStep st{};
-          if (arm.any_limit || arm.has_offsets) st = rpd::advance_frame(arm.base, q);
-          c.frame1 = st.frame;
-          V3 link = arm.root;
-          bool elb = arm.off[0] > 0.0;
-          if (elb) link = arm.root + arm.off[0] * rpd::m_col(st.after_azimuth, 0);
-          c.link1 = link;
-          c.p1 = link + arm.L[0] * q;
-          c.move1 = rpd::norm(c.p1 - w.prev_j1);
-          c.ok = (!elb || link_clear_scaled(w.g, arm.root, link, w.spacing)) &&
-                 rpd::walk_clear(w.g, link, c.p1, w.n);
-          s.ci[off] = c;
+          s.ci[off] = s.ci_by_index[idx];
         } else {
           s.cj[off] = idx;
         }
@@ -381,16 +380,30 @@ __global__ void __launch_bounds__(256) k_wik_pairs(WikDev w, WikScratch s) {
     last = ticket == gridDim.x - 1;
   }
   __syncthreads();
-  if (!last || threadIdx.x != 0) return;
+  if (!last) return;
   __threadfence();
+  // last block: reduce the per-block winners with the whole block
   WikBest b{1e308, LLONG_MAX, -1};
-  for (int k = 0; k < static_cast<int>(gridDim.x); ++k) {
+  for (int k = threadIdx.x; k < static_cast<int>(gridDim.x); k += blockDim.x) {
     WikBest r;
     r.metric = __ldcg(&s.block_best[k].metric);
     r.ord = __ldcg(&s.block_best[k].ord);
     r.opt = __ldcg(&s.block_best[k].opt);
     if (wik_better(r.metric, r.ord, b.metric, b.ord)) b = r;
   }
+  for (int off = 16; off > 0; off >>= 1) {
+    const double om = __shfl_down_sync(FULL, b.metric, off);
+    const long long oo = __shfl_down_sync(FULL, b.ord, off);
+    const int op = __shfl_down_sync(FULL, b.opt, off);
+    if (wik_better(om, oo, b.metric, b.ord)) b = WikBest{om, oo, op};
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) wb[threadIdx.x >> 5] = b;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  b = wb[0];
+  for (int k = 1; k < static_cast<int>(blockDim.x >> 5); ++k)
+    if (wik_better(wb[k].metric, wb[k].ord, b.metric, b.ord)) b = wb[k];
   WikResult res{};
   res.found = 0;
   if (b.ord != LLONG_MAX) {
@@ -699,8 +712,9 @@ Planner::Planner(rp_ctx* c, const rp_arm& a, const rp_quiver* qv, const rp_grid*
   jbits.alloc(qw, st);
   cj.alloc(q->n + 1, st);
   ci.alloc(q->n + 1, st);
+  ci_by_index.alloc(q->n + 1, st);
   counts.alloc(2, st);
-  wik_blocks = ctx->sm_count * 2;
+  wik_blocks = ctx->sm_count;
   block_best.alloc(wik_blocks, st);
   done.alloc(1, st);
   done.zero();
@@ -763,9 +777,10 @@ bool Planner::waypoint_ik(V3 wp, const HostPose& prev, double relax, const Trail
     cone1 = std::min(kPi, ang1) + 1e-12;
     cone2 = std::min(kPi, ang2) + 1e-12;
   }
-  WikScratch s{ibits.p, jbits.p, cj.p, ci.p, counts.p, block_best.p, done.p, result.p, wik_blocks};
+  WikScratch s{ibits.p, jbits.p, cj.p, ci.p, ci_by_index.p, counts.p, block_best.p, done.p,
+               result.p, wik_blocks};
   launch(ctx, "wik_filter", k_wik_filter, dim3(nblk(q->n, 256)), dim3(256), 0, w, cone1, cone2, u1,
-         u2, ibits.p, jbits.p);
+         u2, ibits.p, jbits.p, ci_by_index.p);
   launch(ctx, "wik_compact", k_wik_compact, dim3(1), dim3(1024), 0, w, s);
   launch(ctx, "wik_pairs", k_wik_pairs, dim3(wik_blocks), dim3(256), 0, w, s);
   RP_CUDA(cudaMemcpyAsync(h_result, result.p, sizeof(WikResult), cudaMemcpyDeviceToHost,

@@ -72,6 +72,7 @@ struct WikScratch {
   uint32_t* jbits;
   int* cj;
   CiData* ci;
+  CiData* ci_by_index;
   int* counts;  // [n_ci, n_cj]
   WikBest* block_best;
   unsigned* done;

@@ -31,7 +31,7 @@ struct Planner {
   int64_t wik_calls = 0;
   DevBuf<uint32_t> ibits, jbits;
   DevBuf<int> cj, counts;
-  DevBuf<CiData> ci;
+  DevBuf<CiData> ci, ci_by_index;
   DevBuf<WikBest> block_best;
   DevBuf<unsigned> done;
   DevBuf<WikResult> result;
