@@ -198,11 +198,11 @@ __global__ void __launch_bounds__(256) k_mark_dilate_rowwise(uint64_t* __restric
   __syncthreads();
   const int y = yt + (threadIdx.x & 31);
   const int z = zt + (threadIdx.x >> 5);
-  if (y > y1 || y >= g.ny || z > z1 || z >= g.nz) return;
+  const bool valid = !(y > y1 || y >= g.ny || z > z1 || z >= g.nz);
   uint64_t m[WX];
 #pragma unroll
   for (int w = 0; w < WX; ++w) m[w] = 0;
-  const int n_here = ns;
+  const int n_here = valid ? ns : 0;
   for (int k = 0; k < n_here; ++k) {
     const Prim p = sp[k];
     const int dy = y < p.a[1] ? p.a[1] - y : (y > p.b[1] ? y - p.b[1] : 0);
@@ -217,16 +217,39 @@ __global__ void __launch_bounds__(256) k_mark_dilate_rowwise(uint64_t* __restric
     for (int w = 0; w < WX; ++w) m[w] |= range_mask(lo, hi, 64 * w);
   }
   uint64_t* row = bits + (static_cast<size_t>(z) * g.ny + y) * WX;
-  if (accumulate) {
+  const int rows = min(32, min(y1, g.ny - 1) - yt + 1);
+  const bool bulk = !accumulate && WX >= 2 && (g.ny * WX) % 2 == 0 && rows > 0;
+  if (!bulk) {
+    if (!valid) return;
+    if (accumulate) {
 #pragma unroll
-    for (int w = 0; w < WX; ++w) m[w] |= row[w];
+      for (int w = 0; w < WX; ++w) m[w] |= row[w];
+    }
+#pragma unroll
+    for (int w = 0; w < WX; ++w) row[w] = m[w];
+    return;
   }
-  if (WX == 1) {
-    row[0] = m[0];
-  } else {
+  // Stage the tile (8 planes x 32 rows) in shared memory, then one thread
+  // per plane streams its contiguous rows*WX*8-byte run out with a TMA bulk
+  // store (cp.async.bulk): full-line writes instead of 32 strided stores.
+  __shared__ __align__(128) uint64_t tile[256 * WX];
 #pragma unroll
-    for (int w = 0; w < WX; w += 2)
-      reinterpret_cast<ulonglong2*>(row)[w / 2] = make_ulonglong2(m[w], m[w + 1]);
+  for (int w = 0; w < WX; ++w) tile[threadIdx.x * WX + w] = m[w];
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x < 8) {
+    const int zz = zt + static_cast<int>(threadIdx.x);
+    if (zz <= z1 && zz < g.nz) {
+      uint64_t* gdst = bits + (static_cast<size_t>(zz) * g.ny + yt) * WX;
+      const uint32_t sa =
+          static_cast<uint32_t>(__cvta_generic_to_shared(&tile[threadIdx.x * 32 * WX]));
+      const uint32_t nbytes = static_cast<uint32_t>(rows * WX * 8);
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+                   "r"(sa), "r"(nbytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
   }
 }
 
@@ -234,6 +257,77 @@ __global__ void __launch_bounds__(256) k_mark_dilate_rowwise(uint64_t* __restric
 inline size_t rows_smem(int np, int reach) {
   return 2 * static_cast<size_t>(np) * sizeof(Prim) +
          static_cast<size_t>(2 * reach * reach + 1) * sizeof(int);
+}
+
+/// Box / cloud -> index boxes on the host with the reference's arithmetic
+/// (world_to_index floor of the IEEE quotient, cell-centre test); returns
+/// false when there are more primitives than the parameter block holds.
+constexpr size_t kHostPrimLimit = 512;
+bool host_prims(const rp_grid* g, const rp_obstacle* obs, int n, std::vector<Prim>* out) {
+  out->clear();
+  for (int k = 0; k < n; ++k) {
+    if (obs[k].shape == RP_SHAPE_BOX) {
+      Prim p;
+      for (int ax = 0; ax < 3; ++ax) {
+        const double mn = obs[k].box_min[ax], mx = obs[k].box_max[ax];
+        const double o = g->origin[ax];
+        const int nd = g->dims[ax];
+        const int lo = static_cast<int>(std::floor((mn - o) / g->voxel_size));
+        const int hi = static_cast<int>(std::floor((mx - o) / g->voxel_size));
+        int a = std::max(0, lo), b = std::min(nd - 1, hi);
+        auto inside = [&](int i) {
+          const double c = o + g->voxel_size * (i + 0.5);
+          return c >= mn && c <= mx;
+        };
+        while (a <= b && !inside(a)) ++a;
+        while (b >= a && !inside(b)) --b;
+        p.a[ax] = a;
+        p.b[ax] = b;
+      }
+      out->push_back(p);
+    } else {
+      for (int64_t q = 0; q < obs[k].n_points; ++q) {
+        Prim p;
+        bool in = true;
+        for (int ax = 0; ax < 3; ++ax) {
+          const int i = static_cast<int>(
+              std::floor((obs[k].points[3 * q + ax] - g->origin[ax]) / g->voxel_size));
+          p.a[ax] = p.b[ax] = i;
+          in = in && i >= 0 && i < g->dims[ax];
+        }
+        if (!in) p.b[0] = p.a[0] - 1;
+        out->push_back(p);
+        if (out->size() > kHostPrimLimit) return false;
+      }
+    }
+    if (out->size() > kHostPrimLimit) return false;
+  }
+  return true;
+}
+
+void check_boxes(const rp_obstacle* obs, int n) {
+  for (int k = 0; k < n; ++k)
+    if (obs[k].shape == RP_SHAPE_BOX)
+      require(obs[k].box_min[0] <= obs[k].box_max[0] && obs[k].box_min[1] <= obs[k].box_max[1] &&
+                  obs[k].box_min[2] <= obs[k].box_max[2],
+              RP_E_INVALID_PARAMETER,
+              std::string("obstacle box min must be <= max: ") + (obs[k].id ? obs[k].id : ""));
+}
+
+void launch_rows(rp_ctx* ctx, const char* name, rp_grid* g, const Prim* prims, int np,
+                 const int* wtab, int reach, int y0, int y1, int z0, int z1, bool accumulate);
+
+/// Rasterise host-computed index boxes (one async upload, no box kernel).
+bool launch_rows_param(rp_ctx* ctx, const char* name, rp_grid* g, const std::vector<Prim>& prims,
+                       const DilTable& t, int y0, int y1, int z0, int z1, bool accumulate) {
+  if (prims.empty() || prims.size() > kHostPrimLimit) return false;
+  DevBuf<Prim> dp(prims.size(), ctx->stream);
+  copy_to_device(ctx, dp.p, prims.data(), prims.size() * sizeof(Prim));
+  DevBuf<int> wtab(t.w.size(), ctx->stream);
+  copy_to_device(ctx, wtab.p, t.w.data(), t.w.size() * sizeof(int));
+  launch_rows(ctx, name, g, dp.p, static_cast<int>(prims.size()), wtab.p, t.reach, y0, y1, z0, z1,
+              accumulate);
+  return true;
 }
 
 /// Launch the fused rasterise(+dilate) over rows [y0,y1] x [z0,z1].
@@ -529,6 +623,18 @@ rp_grid* grid_alloc_like(const rp_grid* src) {
 void grid_mark_dilate_boxes(rp_grid* g, const rp_obstacle* obs, int n, double radius,
                             bool or_into_existing) {
   require(radius >= 0.0, RP_E_INVALID_PARAMETER, "dilation radius must be >= 0");
+  check_boxes(obs, n);
+  if (!or_into_existing || g->empty) {
+    std::vector<Prim> hp;
+    const DilTable t = make_table(radius, g->voxel_size);
+    if (host_prims(g, obs, n, &hp) &&
+        launch_rows_param(g->ctx, "mark_dilate", g, hp, t, 0, g->dims[1] - 1, 0, g->dims[2] - 1,
+                          false)) {
+      if (!hp.empty()) g->empty = false;
+      if (radius != 0.0) g->dilation_radius += radius;
+      return;
+    }
+  }
   int64_t np = 0;
   bool only_boxes = true;
   DevBuf<Prim> prims = obstacles_to_prims(g, obs, n, &np, &only_boxes);
@@ -584,6 +690,21 @@ rp_status rp_grid_build(rp_ctx* ctx, const double bmin[3], const double bmax[3],
 rp_status rp_grid_mark(rp_grid* g, const rp_obstacle* obs, int32_t n) {
   return guarded([&] {
     if (n <= 0) return;
+    check_boxes(obs, n);
+    {
+      std::vector<Prim> hp;
+      DilTable t0;
+      t0.reach = 0;
+      t0.w = {0};
+      if (host_prims(g, obs, n, &hp)) {
+        if (hp.empty()) return;
+        if (launch_rows_param(g->ctx, "voxelize", g, hp, t0, 0, g->dims[1] - 1, 0,
+                              g->dims[2] - 1, !g->empty)) {
+          g->empty = false;
+          return;
+        }
+      }
+    }
     int64_t np = 0;
     bool only_boxes = true;
     DevBuf<Prim> prims = obstacles_to_prims(g, obs, n, &np, &only_boxes);
@@ -700,6 +821,32 @@ rp_status rp_grid_overlay(const rp_grid* base, const rp_obstacle* obs, rp_grid**
                             cudaMemcpyDeviceToDevice, ctx->stream));
     g->dilation_radius = base->dilation_radius;
     g->empty = base->empty;
+    *aug = g;
+    check_boxes(obs, 1);
+    {
+      // bbox-limited overlay: only rows within reach of the obstacle change
+      std::vector<Prim> hp;
+      const DilTable t = make_table(base->dilation_radius, base->voxel_size);
+      if (host_prims(g, obs, 1, &hp)) {
+        int y0 = 1 << 30, y1 = -1, z0 = 1 << 30, z1 = -1;
+        for (const Prim& p : hp) {
+          if (p.a[0] > p.b[0] || p.a[1] > p.b[1] || p.a[2] > p.b[2]) continue;
+          y0 = std::min(y0, p.a[1]);
+          y1 = std::max(y1, p.b[1]);
+          z0 = std::min(z0, p.a[2]);
+          z1 = std::max(z1, p.b[2]);
+        }
+        if (y1 < 0) return;
+        y0 = std::max(0, y0 - t.reach);
+        z0 = std::max(0, z0 - t.reach);
+        y1 = std::min(g->dims[1] - 1, y1 + t.reach);
+        z1 = std::min(g->dims[2] - 1, z1 + t.reach);
+        if (launch_rows_param(ctx, "overlay", g, hp, t, y0, y1, z0, z1, true)) {
+          g->empty = false;
+          return;
+        }
+      }
+    }
     int64_t np = 0;
     bool only_boxes = true;
     DevBuf<Prim> prims = obstacles_to_prims(g, obs, 1, &np, &only_boxes);
