@@ -2,7 +2,10 @@
 #include "rp_internal.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 namespace rp {
@@ -74,6 +77,29 @@ static void drain_timing(rp_ctx* ctx) {
     ctx->event_pool.push_back(t.stop);
   }
   ctx->pending.clear();
+}
+
+static double trace_threshold_ms() {
+  static const double t = [] {
+    const char* e = std::getenv("RP_TRACE_HOST");
+    return e ? std::atof(e) : -1.0;
+  }();
+  return t;
+}
+
+static double now_ms() {
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+HostSpan::HostSpan(const char* n) : name(n), t0(trace_threshold_ms() >= 0 ? now_ms() : 0.0) {}
+
+HostSpan::~HostSpan() {
+  const double th = trace_threshold_ms();
+  if (th < 0) return;
+  const double dt = now_ms() - t0;
+  if (dt >= th) std::fprintf(stderr, "[span] %-24s %9.3f ms\n", name, dt);
 }
 
 void copy_to_host(rp_ctx* ctx, void* dst, const void* src, size_t bytes) {

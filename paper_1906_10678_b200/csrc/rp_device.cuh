@@ -93,21 +93,65 @@ __host__ __device__ __forceinline__ V3 walk_sample(V3 from, V3 diff, int k, int 
   return from + t * diff;
 }
 
-/// All n samples clear (segment_clear verdict; walk_points).
-__device__ __forceinline__ bool walk_clear(const GridView& g, V3 from, V3 to, int n) {
-  const V3 diff = to - from;
-  for (int k = 1; k <= n; ++k)
-    if (!point_clear(g, walk_sample(from, diff, k, n))) return false;
-  return true;
+/// Word index and bit of the cell holding p, or -1 outside the grid (free).
+__device__ __forceinline__ long long cell_word(const GridView& g, V3 p, int* bit) {
+  const int ix = vox_floor(p.x - g.ox, g.vs, g.rvs);
+  const int iy = vox_floor(p.y - g.oy, g.vs, g.rvs);
+  const int iz = vox_floor(p.z - g.oz, g.vs, g.rvs);
+  if (ix < 0 || iy < 0 || iz < 0 || ix >= g.nx || iy >= g.ny || iz >= g.nz) return -1;
+  *bit = ix & 63;
+  return (static_cast<long long>(iz) * g.ny + iy) * g.wx + (ix >> 6);
 }
 
-/// walk_segment_into with early exit (src/reach_solver.cpp:109-126):
-/// returns the 1-based first blocked sample, 0 when fully clear.
+/// walk_segment_into / segment_clear (src/reach_solver.cpp:109-126,
+/// src/voxgrid.cpp:100-112): the 1-based first blocked sample, 0 when fully
+/// clear (sequential with early exit: the search kernels are fp64-bound and
+/// most rejected walks stop at their first samples).
 __device__ __forceinline__ int walk_first_blocked(const GridView& g, V3 from, V3 to, int n) {
   const V3 diff = to - from;
-  for (int k = 1; k <= n; ++k)
-    if (!point_clear(g, walk_sample(from, diff, k, n))) return k;
+  for (int k = 1; k <= n; ++k) {
+    int bit = 0;
+    const long long idx = cell_word(g, walk_sample(from, diff, k, n), &bit);
+    if (idx >= 0 && ((__ldg(g.bits + idx) >> bit) & 1ull)) return k;
+  }
   return 0;
+}
+
+/// Verdicts of two walks of n samples with all 2n grid gathers in flight
+/// together (n <= 8; otherwise sequential). For latency-bound callers (a
+/// handful of candidates per thread) this replaces 2n dependent loads by
+/// one round trip; verdicts are identical to walk_first_blocked()==0.
+__device__ __forceinline__ void walks_clear2(const GridView& g, V3 a0, V3 b0, V3 a1, V3 b1, int n,
+                                             bool* c0, bool* c1) {
+  if (n > 8) {
+    *c0 = walk_first_blocked(g, a0, b0, n) == 0;
+    *c1 = walk_first_blocked(g, a1, b1, n) == 0;
+    return;
+  }
+  const V3 d0 = b0 - a0, d1 = b1 - a1;
+  long long idx[16];
+  int bit[16];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    bit[k] = bit[8 + k] = 0;
+    idx[k] = k < n ? cell_word(g, walk_sample(a0, d0, k + 1, n), &bit[k]) : -1;
+    idx[8 + k] = k < n ? cell_word(g, walk_sample(a1, d1, k + 1, n), &bit[8 + k]) : -1;
+  }
+  uint64_t hit0 = 0, hit1 = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint64_t w0 = idx[k] >= 0 ? __ldg(g.bits + idx[k]) : 0ull;
+    const uint64_t w1 = idx[8 + k] >= 0 ? __ldg(g.bits + idx[8 + k]) : 0ull;
+    hit0 |= (w0 >> bit[k]) & 1ull;
+    hit1 |= (w1 >> bit[8 + k]) & 1ull;
+  }
+  *c0 = hit0 == 0;
+  *c1 = hit1 == 0;
+}
+
+/// All n samples clear (segment_clear verdict; walk_points).
+__device__ __forceinline__ bool walk_clear(const GridView& g, V3 from, V3 to, int n) {
+  return walk_first_blocked(g, from, to, n) == 0;
 }
 
 /// scaled_sample_count (src/reach_solver.cpp:143-145)

@@ -210,6 +210,15 @@ struct DevBuf {
   }
 };
 
+/// Host span tracing (RP_TRACE_HOST=<ms>): prints spans longer than the
+/// threshold to stderr. Zero cost when the variable is unset.
+struct HostSpan {
+  const char* name;
+  double t0;
+  explicit HostSpan(const char* n);
+  ~HostSpan();
+};
+
 void copy_to_host(rp_ctx* ctx, void* dst, const void* src, size_t bytes);  // syncs
 void copy_to_device(rp_ctx* ctx, void* dst, const void* src, size_t bytes);
 

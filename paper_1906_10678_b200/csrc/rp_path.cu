@@ -9,6 +9,8 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 namespace rp {
@@ -246,18 +248,116 @@ __device__ bool wik_eval(const WikDev& w, const CiData& c, int j, DevPose* out, 
   return true;
 }
 
+/// wik_eval's verdict for a coaxial arm without joint limits, on joint
+/// arrays only (no DevPose construction or copies): the same tests in the
+/// same order with the same arithmetic (chain joints are the cumulative sums
+/// chain_from_segments forms, src/arm_model.cpp:141-143).
+__device__ bool wik_eval_fast(const WikDev& w, const CiData& c, int j, double* metric_out,
+                              int* opt_out) {
+  const ArmDev& arm = w.arm;
+  const V3 qj = wq(w, j);
+  const V3 p2 = c.p1 + arm.L[1] * qj;
+  const double move2 = rpd::norm(p2 - w.prev_j2);
+  if (move2 > w.j2max) return false;
+  const V3 v3 = w.wp - p2;
+  const double v3_len = rpd::norm(v3);
+  if (fabs(v3_len - arm.L[2]) > w.eps || v3_len < 1e-12) return false;
+  const V3 v3_hat = v3 / v3_len;
+  double metric = c.move1 + move2;
+  if (w.has_bias) metric += rpd::norm(c.p1 - w.bias_j1) + rpd::norm(p2 - w.bias_j2);
+  if (!c.ok) return false;
+  if (!rpd::walk_clear(w.g, c.p1, p2, w.n)) return false;  // link2 = p1 (coaxial)
+  const V3 s3 = v3_hat * arm.L[2];
+  const V3 p3 = p2 + s3;
+  if (!rpd::walk_clear(w.g, p2, p3, w.n)) return false;
+  V3 J[5];
+  J[0] = arm.root;
+  J[1] = J[0] + arm.L[0] * wq(w, c.i);
+  J[2] = J[1] + arm.L[1] * qj;
+  J[3] = J[2] + s3;
+  const double min_sep = 2.0 * arm.arm_radius;
+  int opt = -1;
+  if (w.four) {
+    bool done = false;
+    for (int o = 0; o <= w.n_opts && !done; ++o) {
+      const V3 dir = o < w.n_opts ? w.opt_dir[o] : rpd::normalized(s3);
+      J[4] = J[3] + w.L4 * dir;
+      if (!rpd::walk_clear(w.g, J[3], J[4], w.n)) continue;
+      if (!rpd::self_collision_free(J, 4, min_sep)) continue;
+      opt = o;
+      done = true;
+    }
+    if (!done) return false;
+  } else if (!rpd::self_collision_free(J, 3, min_sep)) {
+    return false;
+  }
+  if (!(rpd::norm(J[1] - w.prev_j1) <= w.sm1 && rpd::norm(J[2] - w.prev_j2) <= w.sm2)) return false;
+  *metric_out = metric;
+  *opt_out = opt;
+  return true;
+}
+
+__device__ __forceinline__ bool wik_test(const WikDev& w, const CiData& c, int j, double* m,
+                                         int* opt) {
+  if (!w.arm.any_limit && !w.arm.has_offsets) return wik_eval_fast(w, c, j, m, opt);
+  return wik_eval(w, c, j, nullptr, m, opt);
+}
+
+/// The pose wik_eval accepted for (i, j, trail option): the same arithmetic,
+/// without re-running its tests.
+__device__ DevPose wik_pose(const WikDev& w, const CiData& c, int j, int opt) {
+  const ArmDev& arm = w.arm;
+  const V3 qj = wq(w, j);
+  V3 link2 = c.p1;
+  if (arm.off[1] > 0.0) {
+    const rpd::FrameStep st2 = rpd::advance_frame(c.frame1, qj);
+    link2 = c.p1 + arm.off[1] * rpd::m_col(st2.after_azimuth, 0);
+  }
+  const V3 p2 = link2 + arm.L[1] * qj;
+  const V3 v3 = w.wp - p2;
+  const double v3_len = rpd::norm(v3);
+  const V3 v3_hat = v3 / v3_len;
+  const V3 s3 = v3_hat * arm.L[2];
+  const V3 p3 = p2 + s3;
+  DevPose ch{};
+  ch.nseg = 3;
+  ch.seg[0] = arm.L[0] * wq(w, c.i);
+  ch.seg[1] = arm.L[1] * qj;
+  ch.seg[2] = s3;
+  ch.qidx[0] = c.i;
+  ch.qidx[1] = j;
+  ch.qidx[2] = -1;
+  ch.qidx[3] = -1;
+  build_chain(arm, ch);
+  ch.n_wp_links = 3;
+  ch.wp_from[0] = c.link1; ch.wp_to[0] = c.p1;
+  ch.wp_from[1] = link2;   ch.wp_to[1] = p2;
+  ch.wp_from[2] = p2;      ch.wp_to[2] = p3;
+  ch.n_wp[0] = ch.n_wp[1] = ch.n_wp[2] = w.n;
+  if (w.four && opt >= 0) {
+    const V3 dir = opt < w.n_opts ? w.opt_dir[opt] : rpd::normalized(ch.seg[2]);
+    ch.nseg = 4;
+    ch.seg[3] = w.L4 * dir;
+    build_chain(arm, ch);
+    ch.n_wp_links = 4;
+    ch.wp_from[3] = ch.joints[3];
+    ch.wp_to[3] = ch.joints[4];
+    ch.n_wp[3] = w.n;
+  }
+  return ch;
+}
+
 /// Candidate filters over the quiver: segment-1 directions inside the
 /// reference's cone that pass the joint-1 limit and the move1 bound, and
 /// segment-2 directions inside its cone (all directions for offset arms).
-__global__ void k_wik_filter(WikDev w, double cone1, double cone2, V3 u1, V3 u2,
-                             uint32_t* ibits, uint32_t* jbits, CiData* ci_by_index) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+__device__ void wik_filter_one(const WikDev& w, double cone1, double cone2, V3 u1, V3 u2, int i,
+                               CiData* ci_by_index, bool* pi_out, bool* pj_out) {
   bool pi = false, pj = false;
-  if (i < w.Q) {
+  {
     const V3 q = wq(w, i);
     const ArmDev& arm = w.arm;
     bool in1 = true;
-    if (w.filter_j) in1 = atan2(rpd::norm(rpd::cross(q, u1)), rpd::dot(q, u1)) <= cone1;
+    if (w.filter_j) in1 = rpd::dot(q, u1) >= cone1;
     if (in1) {
       rpd::FrameStep st{};
       if (arm.any_limit || arm.has_offsets) st = rpd::advance_frame(arm.base, q);
@@ -283,8 +383,17 @@ __global__ void k_wik_filter(WikDev w, double cone1, double cone2, V3 u1, V3 u2,
         }
       }
     }
-    pj = !w.filter_j || atan2(rpd::norm(rpd::cross(q, u2)), rpd::dot(q, u2)) <= cone2;
+    pj = !w.filter_j || rpd::dot(q, u2) >= cone2;
   }
+  *pi_out = pi;
+  *pj_out = pj;
+}
+
+__global__ void k_wik_filter(WikDev w, double cone1, double cone2, V3 u1, V3 u2,
+                             uint32_t* ibits, uint32_t* jbits, CiData* ci_by_index) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  bool pi = false, pj = false;
+  if (i < w.Q) wik_filter_one(w, cone1, cone2, u1, u2, i, ci_by_index, &pi, &pj);
   const unsigned mi = __ballot_sync(FULL, pi), mj = __ballot_sync(FULL, pj);
   if ((threadIdx.x & 31) == 0 && (i >> 5) < (w.Q + 31) / 32) {
     ibits[i >> 5] = mi;
@@ -349,7 +458,7 @@ __global__ void __launch_bounds__(256) k_wik_pairs(WikDev w, WikScratch s) {
     if (!c.ok) continue;
     double m;
     int opt;
-    if (wik_eval(w, c, s.cj[t - static_cast<long long>(a) * ncj], nullptr, &m, &opt) &&
+    if (wik_test(w, c, s.cj[t - static_cast<long long>(a) * ncj], &m, &opt) &&
         wik_better(m, t, bm, bo)) {
       bm = m;
       bo = t;
@@ -421,6 +530,308 @@ __global__ void __launch_bounds__(256) k_wik_pairs(WikDev w, WikScratch s) {
   }
   *s.result = res;
   *s.done = 0;
+}
+
+// ---------------------------------------------------------------------------
+// Persistent backward pass: one cooperative launch runs the whole sequential
+// pass (src/path_planner.cpp:322-400). Per (waypoint, target, factor)
+// attempt: filter over the quiver (all blocks) | barrier | every block
+// compacts the candidate lists into its shared memory and evaluates its share
+// of the (i, j) pairs | barrier | block 0 reduces, materialises the pose and
+// publishes the decision | barrier. Blocks are co-resident (cooperative
+// launch), so the barrier is a plain global-memory one; its gpu-scope fence
+// also invalidates L1, so data written by other SMs is read fresh.
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    const unsigned g0 = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nblocks - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g0) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ bool pose_smooth(const DevPose& prev, const DevPose& c, double b1,
+                                            double b2) {
+  return rpd::norm(c.joints[1] - prev.joints[1]) <= b1 && rpd::norm(c.joints[2] - prev.joints[2]) <= b2;
+}
+
+/// Block-local ordered compaction of a quiver bit set into shared memory.
+template <int NT>
+__device__ int block_compact(const uint32_t* __restrict__ bits, int Q, int* out) {
+  typedef cub::BlockScan<int, NT> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int nwords = (Q + 31) / 32;
+  for (int w0 = 0; w0 < nwords; w0 += NT) {
+    const int wd = w0 + threadIdx.x;
+    const uint32_t word = wd < nwords ? __ldcg(bits + wd) : 0u;
+    int off = 0, total = 0;
+    Scan(tmp).ExclusiveSum(__popc(word), off, total);
+    off += carry;
+    uint32_t x = word;
+    while (x) {
+      const int b = __ffs(x) - 1;
+      x &= x - 1;
+      out[off++] = wd * 32 + b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += total;
+    __syncthreads();
+  }
+  const int result = carry;
+  __syncthreads();  // every thread has read carry before a next call resets it
+  return result;
+}
+
+/// Coherent (L2) read of a struct written by another block in this launch.
+template <typename T>
+__device__ __forceinline__ T ldcg_struct(const T* p) {
+  static_assert(sizeof(T) % 8 == 0, "8-byte granular");
+  T v;
+  const long long* s = reinterpret_cast<const long long*>(p);
+  long long* d = reinterpret_cast<long long*>(&v);
+#pragma unroll 4
+  for (int i = 0; i < static_cast<int>(sizeof(T) / 8); ++i) d[i] = __ldcg(s + i);
+  return v;
+}
+
+constexpr int kBpThreads = 512;
+
+__global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_constant__ BpArgs A) {
+  extern __shared__ int sh_lists[];
+  int* li = sh_lists;
+  int* lj = sh_lists + A.Q;
+  __shared__ WikBest wb[kBpThreads / 32];
+  const unsigned nb = gridDim.x;
+  const int lane = threadIdx.x & 31;
+  // per-attempt search descriptor, built once per block in shared memory
+  // (a per-thread copy would be ~700 B of local memory per thread)
+  __shared__ WikDev sw;
+  __shared__ V3 s_u1, s_u2, s_cu, s_cv, s_wk;
+  for (int k = A.m - 2; k >= 0; --k) {
+    if (k == 0 && A.has_fixed) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const DevPose prev = ldcg_struct(A.poses + 1);
+        int found = 0;
+        for (int fi = 0; fi < A.nf && !found; ++fi) {
+          const double f = A.factors[fi];
+          if (pose_smooth(prev, A.fixed_first, A.pj1 * f + 1e-12, A.pj2 * f + 1e-12)) {
+            A.poses[0] = A.fixed_first;
+            A.relax[0] = f;
+            A.kind[0] = 2;
+            found = 1;
+          }
+        }
+        A.state[0] = found;
+        A.state[1] = found ? -1 : 0;
+        A.state[2] = found;
+      }
+      return;  // k == 0 is the last waypoint either way
+    }
+    if (threadIdx.x == 0) {
+      // trail context from the (possibly cloud-substituted) waypoint list
+      const DevPose prev = ldcg_struct(A.poses + k + 1);
+      const V3 wk = ldcg_struct(A.wps + k);
+      const V3 wprev = k > 0 ? ldcg_struct(A.wps + k - 1) : wk;
+      const V3 wnext = ldcg_struct(A.wps + k + 1);
+      WikDev& w = sw;
+      w = WikDev{};
+      w.g = A.g;
+      w.arm = A.arm;
+      w.n = A.n;
+      w.Q = A.Q;
+      w.qx = A.qx;
+      w.qy = A.qy;
+      w.qz = A.qz;
+      w.spacing = A.spacing;
+      w.prev_j1 = prev.joints[1];
+      w.prev_j2 = prev.joints[2];
+      w.four = A.four;
+      w.L4 = A.L4;
+      w.cond2 = A.cond2;
+      w.cond3 = A.cond3;
+      w.filter_j = A.filter_j;
+      w.n_opts = 0;
+      if (k > 0) {
+        const V3 d = wprev - wk;
+        if (rpd::norm(d) > 1e-12) w.opt_dir[w.n_opts++] = rpd::normalized(d);
+      }
+      if (k + 1 < A.m) {
+        const V3 d = wnext - wk;
+        if (rpd::norm(d) > 1e-12) w.opt_dir[w.n_opts++] = rpd::normalized(d);
+      }
+      const bool fixed_bias = A.has_fixed && k == 1;
+      w.has_bias = (fixed_bias || A.has_bias) ? 1 : 0;
+      if (w.has_bias) {
+        const DevPose& b = fixed_bias ? A.fixed_first : A.bias;
+        w.bias_j1 = b.joints[1];
+        w.bias_j2 = b.joints[2];
+      }
+      s_u1 = rpd::normalized(prev.seg[0]);
+      s_u2 = rpd::normalized(prev.seg[1]);
+      s_wk = wk;
+      // cloud ring frame (src/path_planner.cpp:368-377)
+      s_cu = V3{0, 0, 0};
+      s_cv = V3{0, 0, 0};
+      if (A.cloud) {
+        V3 dir = wnext - wk;
+        if (rpd::norm(dir) < 1e-12 && k > 0) dir = wk - wprev;
+        if (rpd::norm(dir) < 1e-12) dir = V3{0, 0, 1};
+        dir = rpd::normalized(dir);
+        s_cu = perpendicular_of(dir);
+        s_cv = rpd::cross(dir, s_cu);
+      }
+    }
+    __syncthreads();
+    const WikDev& w = sw;
+    const V3 u1 = s_u1, u2 = s_u2;
+    bool found = false;
+    const int n_targets = A.cloud ? 9 : 1;
+    for (int t = 0; t < n_targets && !found; ++t) {
+      for (int fi = 0; fi < A.nf && !found; ++fi) {
+        const double f = A.factors[fi];
+        if (threadIdx.x == 0) {
+          sw.wp = t == 0 ? s_wk
+                         : s_wk + A.cloud_radius * (A.ring_c[t - 1] * s_cu + A.ring_s[t - 1] * s_cv);
+          // waypoint_ik's relaxed bounds (src/path_planner.cpp:172-174)
+          sw.eps = A.eps_wp * f + 1e-12;
+          sw.j1max = A.pj1 * f + 1e-12;
+          sw.j2max = A.pj2 * f + 1e-12;
+          sw.sm1 = sw.j1max;
+          sw.sm2 = sw.j2max;
+        }
+        __syncthreads();
+        const bool prof = A.prof && blockIdx.x == 0 && threadIdx.x == 0;
+        long long c0 = prof ? clock64() : 0;
+        // phase A: candidate filters
+        for (int i0 = blockIdx.x * blockDim.x; i0 < A.Q; i0 += nb * blockDim.x) {
+          const int i = i0 + threadIdx.x;
+          bool pi = false, pj = false;
+          if (i < A.Q) wik_filter_one(w, A.cone1[fi], A.cone2[fi], u1, u2, i, A.ci_by_index, &pi, &pj);
+          const unsigned mi = __ballot_sync(FULL, pi), mj = __ballot_sync(FULL, pj);
+          if (lane == 0 && (i >> 5) < (A.Q + 31) / 32) {
+            A.ibits[i >> 5] = mi;
+            A.jbits[i >> 5] = mj;
+          }
+        }
+        grid_barrier(A.bar, nb);
+        long long c1 = prof ? clock64() : 0;
+        // phase B: block-local compaction + this block's share of the pairs
+        const int nci = block_compact<kBpThreads>(A.ibits, A.Q, li);
+        const int ncj = block_compact<kBpThreads>(A.jbits, A.Q, lj);
+        long long c2 = prof ? clock64() : 0;
+        double bm = 1e308;
+        long long bo = LLONG_MAX;
+        int bopt = -1;
+        const long long total = static_cast<long long>(nci) * ncj;
+        for (long long tt = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+             tt < total; tt += static_cast<long long>(nb) * blockDim.x) {
+          const int a = static_cast<int>(tt / ncj);
+          if (!__ldcg(&A.ci_by_index[li[a]].ok)) continue;
+          const CiData c = ldcg_struct(A.ci_by_index + li[a]);
+          double mm;
+          int opt;
+          if (wik_test(w, c, lj[tt - static_cast<long long>(a) * ncj], &mm, &opt) &&
+              wik_better(mm, tt, bm, bo)) {
+            bm = mm;
+            bo = tt;
+            bopt = opt;
+          }
+        }
+        for (int off = 16; off > 0; off >>= 1) {
+          const double om = __shfl_down_sync(FULL, bm, off);
+          const long long oo = __shfl_down_sync(FULL, bo, off);
+          const int op = __shfl_down_sync(FULL, bopt, off);
+          if (wik_better(om, oo, bm, bo)) {
+            bm = om;
+            bo = oo;
+            bopt = op;
+          }
+        }
+        if (lane == 0) wb[threadIdx.x >> 5] = WikBest{bm, bo, bopt};
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          WikBest b = wb[0];
+          for (int q = 1; q < kBpThreads / 32; ++q)
+            if (wik_better(wb[q].metric, wb[q].ord, b.metric, b.ord)) b = wb[q];
+          A.block_best[blockIdx.x] = b;
+        }
+        long long c3 = prof ? clock64() : 0;
+        grid_barrier(A.bar, nb);
+        long long c4 = prof ? clock64() : 0;
+        // phase C: block 0 picks the first strict minimum and publishes it
+        if (blockIdx.x == 0) {
+          WikBest b{1e308, LLONG_MAX, -1};
+          for (unsigned q = threadIdx.x; q < nb; q += blockDim.x) {
+            const WikBest r = ldcg_struct(A.block_best + q);
+            if (wik_better(r.metric, r.ord, b.metric, b.ord)) b = r;
+          }
+          for (int off = 16; off > 0; off >>= 1) {
+            const double om = __shfl_down_sync(FULL, b.metric, off);
+            const long long oo = __shfl_down_sync(FULL, b.ord, off);
+            const int op = __shfl_down_sync(FULL, b.opt, off);
+            if (wik_better(om, oo, b.metric, b.ord)) b = WikBest{om, oo, op};
+          }
+          __syncthreads();
+          if (lane == 0) wb[threadIdx.x >> 5] = b;
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            b = wb[0];
+            for (int q = 1; q < kBpThreads / 32; ++q)
+              if (wik_better(wb[q].metric, wb[q].ord, b.metric, b.ord)) b = wb[q];
+            int ok = 0;
+            if (b.ord != LLONG_MAX) {
+              const int a = static_cast<int>(b.ord / ncj);
+              A.poses[k] = wik_pose(w, ldcg_struct(A.ci_by_index + li[a]),
+                                    lj[b.ord - static_cast<long long>(a) * ncj], b.opt);
+              A.relax[k] = f;
+              A.kind[k] = t > 0 ? 1 : 0;
+              if (t > 0) A.wps[k] = w.wp;
+              ok = 1;
+            }
+            A.state[0] = ok;
+          }
+        }
+        long long c5 = prof ? clock64() : 0;
+        grid_barrier(A.bar, nb);
+        if (prof) {
+          const long long c6 = clock64();
+          A.prof[0] += c1 - c0;  // filter + barrier
+          A.prof[1] += c2 - c1;  // compaction
+          A.prof[2] += c3 - c2;  // pairs (block 0's share)
+          A.prof[3] += c4 - c3;  // barrier wait (slowest block)
+          A.prof[4] += c5 - c4;  // publish
+          A.prof[5] += c6 - c5;  // barrier
+          A.prof[6] += 1;
+          A.prof[7] += static_cast<long long>(nci) * ncj;
+        }
+        found = __ldcg(A.state) != 0;
+      }
+    }
+    if (!found) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        A.state[1] = k;
+        A.state[2] = 0;
+      }
+      return;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    A.state[1] = -1;
+    A.state[2] = 1;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -646,6 +1057,15 @@ __global__ void k_mean_dev(const V3* __restrict__ pts, int npts, const V3* __res
 // ---------------------------------------------------------------------------
 // Host wrappers
 
+/// waypoint_ik's candidate cones (src/path_planner.cpp:190-193) as a
+/// conservative dot-product bound: cos of the half angle widened by 1e-9 rad
+/// (and 1e-12 on the cosine). Every candidate that passes the move tests is
+/// at least 1e-9 rad inside the reference's cone, so the filter only drops
+/// directions the reference's own tests would reject.
+static double cone_cos(double half_angle) {
+  return std::cos(std::min(half_angle + 1e-9, kPi)) - 1e-12;
+}
+
 /// folded_pose with glibc sin/cos (bit-identical to the reference's).
 HostPose folded_pose_host(rp_ctx* ctx, const rp_arm& arm) {
   (void)ctx;
@@ -702,6 +1122,7 @@ DevPose to_dev(const HostPose& h) {
 Planner::Planner(rp_ctx* c, const rp_arm& a, const rp_quiver* qv, const rp_grid* gr,
                  const rp_reach_params& r, const rp_path_params& p)
     : ctx(c), arm(a), q(qv), g(gr), rp(r) {
+  HostSpan span_("Planner::Planner");
   ad = make_arm_dev(a);
   pp = resolve_path_params(p, a, r);
   n = r.n_samples;
@@ -720,12 +1141,16 @@ Planner::Planner(rp_ctx* c, const rp_arm& a, const rp_quiver* qv, const rp_grid*
   done.zero();
   result.alloc(1, st);
   opout.alloc(1, st);
-  RP_CUDA(cudaMallocHost(&h_result, sizeof(WikResult)));
+  // pinned read-back slot: one per context, reused by every planner
+  if (!ctx->pinned || ctx->pinned_bytes < sizeof(WikResult)) {
+    if (ctx->pinned) RP_CUDA(cudaFreeHost(ctx->pinned));
+    ctx->pinned_bytes = std::max<size_t>(sizeof(WikResult), 4096);
+    RP_CUDA(cudaMallocHost(&ctx->pinned, ctx->pinned_bytes));
+  }
+  h_result = static_cast<WikResult*>(ctx->pinned);
 }
 
-Planner::~Planner() {
-  if (h_result) cudaFreeHost(h_result);
-}
+Planner::~Planner() {}
 
 bool Planner::waypoint_ik(V3 wp, const HostPose& prev, double relax, const Trail& tr,
                           const HostPose* bias, HostPose* out) {
@@ -774,8 +1199,8 @@ bool Planner::waypoint_ik(V3 wp, const HostPose& prev, double relax, const Trail
     u2 = rpd::normalized(prev.seg[1]);
     require(std::abs(rpd::norm(u1) - 1.0) <= 1e-9 && std::abs(rpd::norm(u2) - 1.0) <= 1e-9,
             RP_E_INVALID_PARAMETER, "cone axis must be unit");
-    cone1 = std::min(kPi, ang1) + 1e-12;
-    cone2 = std::min(kPi, ang2) + 1e-12;
+    cone1 = cone_cos(std::min(kPi, ang1) + 1e-12);
+    cone2 = cone_cos(std::min(kPi, ang2) + 1e-12);
   }
   WikScratch s{ibits.p, jbits.p, cj.p, ci.p, ci_by_index.p, counts.p, block_best.p, done.p,
                result.p, wik_blocks};
@@ -792,6 +1217,142 @@ bool Planner::waypoint_ik(V3 wp, const HostPose& prev, double relax, const Trail
   return true;
 }
 
+bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& anchor,
+                                   const std::vector<double>& factors, bool cloud,
+                                   double cloud_radius, const HostPose* fixed_first,
+                                   const HostPose* bias, BpOut* out) {
+  HostSpan span_("Planner::backward_pass_device");
+  if (!use_device_pass || factors.size() > static_cast<size_t>(kBpMaxFactors) || q->n > 16384 ||
+      wps.size() < 2)
+    return false;
+  cudaStream_t st = ctx->stream;
+  const size_t smem = 2 * static_cast<size_t>(q->n) * sizeof(int);
+  if (bp_blocks == 0) {
+    // kernel attribute + occupancy: once per process and shared-memory size
+    static size_t configured_smem = 0;
+    static int per_sm = 0;
+    if (configured_smem < smem) {
+      RP_CUDA(cudaFuncSetAttribute(k_backward_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+      RP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_backward_pass, kBpThreads,
+                                                            smem));
+      configured_smem = smem;
+    }
+    if (per_sm < 1) {
+      use_device_pass = false;
+      return false;
+    }
+    // The pass is latency-bound (a short serial chain per attempt): a few
+    // dozen resident blocks keep every phase parallel while making the grid
+    // barriers cheaper and the grid's L1 reuse higher.
+    const char* env = std::getenv("RP_BP_BLOCKS");
+    bp_blocks = std::min(ctx->sm_count * per_sm, env ? std::max(1, std::atoi(env)) : 32);
+    bp_bar.alloc(2, st);
+    bp_state.alloc(4, st);
+    bp_best.alloc(bp_blocks, st);
+  }
+  const int m = static_cast<int>(wps.size());
+  BpArgs A{};
+  A.g = g->view();
+  A.arm = ad;
+  A.n = n;
+  A.Q = q->n;
+  A.four = arm.n_segments == 4;
+  const rpd::Limit& l2 = ad.lim[1];
+  const rpd::Limit& l3 = ad.lim[2];
+  A.cond2 = (ad.off[1] > 0.0 || !rpd::full_azimuth(l2) || l2.elev_min > 0.0 || l2.elev_max < kPi);
+  A.cond3 = (!rpd::full_azimuth(l3) || l3.elev_min > 0.0 || l3.elev_max < kPi);
+  A.filter_j = ad.has_offsets ? 0 : 1;
+  A.qx = q->d_soa;
+  A.qy = q->d_soa + q->n;
+  A.qz = q->d_soa + 2 * static_cast<size_t>(q->n);
+  A.spacing = spacing;
+  A.L4 = arm.n_segments == 4 ? arm.lengths[3] : 0.0;
+  A.pj1 = pp.j1;
+  A.pj2 = pp.j2;
+  A.eps_wp = pp.eps_wp;
+  A.m = m;
+  A.nf = static_cast<int>(factors.size());
+  auto chord_to_angle = [](double chord) {
+    return 2.0 * std::asin(std::clamp(chord / 2.0, 0.0, 1.0));
+  };
+  for (int fi = 0; fi < A.nf; ++fi) {
+    const double f = factors[fi];
+    A.factors[fi] = f;
+    const double j1max = pp.j1 * f + 1e-12, j2max = pp.j2 * f + 1e-12;
+    A.cone1[fi] = cone_cos(std::min(kPi, chord_to_angle(j1max / arm.lengths[0]) + 1e-9) + 1e-12);
+    A.cone2[fi] =
+        cone_cos(std::min(kPi, chord_to_angle((j1max + j2max) / arm.lengths[1]) + 1e-9) + 1e-12);
+  }
+  A.cloud = cloud ? 1 : 0;
+  A.cloud_radius = cloud_radius;
+  for (int t = 0; t < 8; ++t) {
+    const double a = 2.0 * kPi * t / 8.0;
+    A.ring_c[t] = std::cos(a);
+    A.ring_s[t] = std::sin(a);
+  }
+  A.has_fixed = fixed_first ? 1 : 0;
+  if (fixed_first) A.fixed_first = to_dev(*fixed_first);
+  A.has_bias = bias ? 1 : 0;
+  if (bias) A.bias = to_dev(*bias);
+  DevBuf<V3> dw(m, st);
+  DevBuf<DevPose> dp(m, st);
+  DevBuf<double> dr(m, st);
+  DevBuf<int> dk(m, st);
+  copy_to_device(ctx, dw.p, wps.data(), m * sizeof(V3));
+  const DevPose da = to_dev(anchor);
+  copy_to_device(ctx, dp.p + (m - 1), &da, sizeof(DevPose));
+  std::vector<double> ones(m, 1.0);
+  copy_to_device(ctx, dr.p, ones.data(), m * sizeof(double));
+  dk.zero();
+  bp_bar.zero();
+  bp_state.zero();
+  A.wps = dw.p;
+  A.poses = dp.p;
+  A.relax = dr.p;
+  A.kind = dk.p;
+  A.ibits = ibits.p;
+  A.jbits = jbits.p;
+  A.ci_by_index = ci_by_index.p;
+  A.block_best = bp_best.p;
+  A.bar = bp_bar.p;
+  A.state = bp_state.p;
+  static const bool profile = std::getenv("RP_PROFILE_PASS") != nullptr;
+  DevBuf<long long> prof;
+  if (profile) {
+    prof.alloc(8, st);
+    prof.zero();
+    A.prof = prof.p;
+  }
+  void* args[] = {&A};
+  cudaEvent_t ev = nullptr;
+  launch_begin(ctx, "backward_pass", &ev);
+  RP_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_backward_pass), dim3(bp_blocks),
+                                      dim3(kBpThreads), args, smem, st));
+  launch_end(ctx, "backward_pass", ev);
+  int hs[4];
+  copy_to_host(ctx, hs, bp_state.p, sizeof(hs));
+  if (profile) {
+    long long hp[8];
+    copy_to_host(ctx, hp, prof.p, sizeof(hp));
+    std::fprintf(stderr,
+                 "[pass] m=%d attempts=%lld pairs=%lld cyc: filter %lld compact %lld pairs %lld "
+                 "wait %lld publish %lld barrier %lld\n",
+                 m, hp[6], hp[7], hp[0], hp[1], hp[2], hp[3], hp[4], hp[5]);
+  }
+  out->ok = hs[2] != 0;
+  out->failed_index = hs[1];
+  out->poses.resize(m);
+  out->relax.resize(m);
+  out->kind.resize(m);
+  out->wps.resize(m);
+  copy_to_host(ctx, out->poses.data(), dp.p, m * sizeof(DevPose));
+  copy_to_host(ctx, out->relax.data(), dr.p, m * sizeof(double));
+  copy_to_host(ctx, out->kind.data(), dk.p, m * sizeof(int));
+  copy_to_host(ctx, out->wps.data(), dw.p, m * sizeof(V3));
+  return true;
+}
+
 PoseOpOut run_pose_op(Planner& P) {
   PoseOpOut h;
   copy_to_host(P.ctx, &h, P.opout.p, sizeof(PoseOpOut));
@@ -799,6 +1360,7 @@ PoseOpOut run_pose_op(Planner& P) {
 }
 
 HostPose Planner::refine(const HostPose& approx, V3 target, int mode) {
+  HostSpan span_("Planner::refine");
   launch(ctx, "refine", k_refine, dim3(1), dim3(1), 0, ad, to_dev(approx), target, mode,
          opout.p);
   PoseOpOut r = run_pose_op(*this);
@@ -828,6 +1390,7 @@ bool Planner::append_trail(const HostPose& chain3, const Trail& tr, HostPose* ou
 std::optional<std::vector<HostPose>> Planner::interpolate(const HostPose* from_or_null,
                                                           const HostPose& to, int base_steps,
                                                           bool* rotated_valid) {
+  HostSpan span_("Planner::interpolate");
   // The joint-space interpolation is evaluated with the host's glibc
   // transcendentals, exactly as the reference does: the folded zig-zag puts
   // azimuths at +-pi, so the direction of wrap_angle(qb - qa) -- and with it
@@ -958,6 +1521,7 @@ std::vector<long long> Planner::rank_by_deviation(rp_solution_set* set,
                                                   V3 lead_pt, int64_t* total_out,
                                                   std::vector<long long>* tail, int head_n,
                                                   int tail_n) {
+  HostSpan span_("Planner::rank_by_deviation");
   cudaStream_t st = ctx->stream;
   const int64_t ns = static_cast<int64_t>(lists.size());
   const int64_t nsol = set ? set->n_solutions : 0;

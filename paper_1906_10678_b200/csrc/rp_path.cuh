@@ -66,6 +66,42 @@ struct PoseOpOut {
   DevPose pose;
 };
 
+/// Persistent backward pass (src/path_planner.cpp:322-400) in one
+/// cooperative launch: everything the host loop decides is decided on the
+/// device between grid barriers.
+constexpr int kBpMaxFactors = 16;
+struct BpArgs {
+  rpd::GridView g;
+  ArmDev arm;
+  int n, Q, four, cond2, cond3, filter_j;
+  const double* qx;
+  const double* qy;
+  const double* qz;
+  double spacing, L4, pj1, pj2;  // resolved joint1/joint2_max_move
+  double eps_wp;                 // resolved epsilon_waypoint
+  int m;
+  V3* wps;         // [m], cloud substitution writes back
+  DevPose* poses;  // [m], poses[m-1] = anchor on entry
+  double* relax;   // [m]
+  int* kind;       // [m] 0 plain, 1 cloud, 2 fixed junction
+  int nf;
+  double factors[kBpMaxFactors];
+  double cone1[kBpMaxFactors], cone2[kBpMaxFactors];  // host glibc asin, like waypoint_ik
+  int cloud;
+  double cloud_radius;
+  double ring_c[8], ring_s[8];  // cos/sin(2*pi*t/8), host glibc
+  int has_fixed, has_bias;
+  DevPose fixed_first, bias;
+  // scratch
+  uint32_t* ibits;
+  uint32_t* jbits;
+  CiData* ci_by_index;
+  WikBest* block_best;
+  unsigned* bar;  // [2] barrier count + generation
+  int* state;     // [4] found, failed_index, ok
+  long long* prof;  // optional [8] phase cycle counters (RP_PROFILE_PASS)
+};
+
 /// Device scratch reused by every waypoint_ik call of a planner.
 struct WikScratch {
   uint32_t* ibits;

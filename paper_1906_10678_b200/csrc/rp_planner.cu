@@ -96,12 +96,39 @@ struct Failure {
 /// backward_pass (src/path_planner.cpp:322-400)
 PassResult backward_pass(Planner& P, const std::vector<V3>& waypoints, const HostPose& anchor,
                          const PassOptions& opt) {
+  HostSpan span_("backward_pass");
   PassResult res;
   const size_t m = waypoints.size();
   res.poses.assign(m, HostPose{});
   res.relax.assign(m, 1.0);
   res.waypoints = waypoints;
   res.poses[m - 1] = anchor;
+  Planner::BpOut bo;
+  if (P.backward_pass_device(waypoints, anchor, opt.factors, opt.cloud, opt.cloud_radius,
+                             opt.fixed_first, opt.junction_bias, &bo)) {
+    res.waypoints = bo.wps;
+    res.relax = bo.relax;
+    if (!bo.ok) {
+      res.failed_index = bo.failed_index;
+      return res;
+    }
+    for (size_t k = m - 1; k-- > 0;) {
+      if (bo.kind[k] == 2) {
+        res.poses[k] = *opt.fixed_first;
+        if (bo.relax[k] > 1.0) res.notes.push_back("relaxed junction at waypoint 0");
+        continue;
+      }
+      res.poses[k] = host_pose_from_dev(bo.poses[k]);
+      if (bo.kind[k] == 1) {
+        res.notes.push_back("cloud target at waypoint " + std::to_string(k));
+      } else if (bo.relax[k] > 1.0) {
+        res.notes.push_back("relaxed x" + std::to_string(bo.relax[k]) + " at waypoint " +
+                            std::to_string(k));
+      }
+    }
+    res.ok = true;
+    return res;
+  }
   for (size_t k = m - 1; k-- > 0;) {
     const HostPose prev = res.poses[k + 1];
     bool found = false;
@@ -177,6 +204,7 @@ std::vector<HostPose> solution_poses(rp_solution_set* s, const std::vector<long 
 
 /// make_candidate_build (src/path_planner.cpp:497-560)
 Build make_candidate_build(Planner& P, const Cand& cand, V3 target) {
+  HostSpan span_("make_candidate_build");
   Build out;
   const int n = P.n;
   try {
@@ -257,6 +285,7 @@ struct Attempt {
 
 /// attempt_candidate (src/path_planner.cpp:580-602)
 Attempt attempt_candidate(Planner& P, const Cand& cand, V3 target, const PassOptions& opt) {
+  HostSpan span_("attempt_candidate");
   Attempt r;
   Build b = make_candidate_build(P, cand, target);
   if (!b.ok) {
@@ -288,6 +317,7 @@ std::vector<V3> candidate_tip_path(const Cand& c, int n, V3 target) {
 /// sorted on the device.
 std::vector<Cand> alternate_candidates(Planner& P, rp_solution_set* set, const Cand& failed,
                                        V3 target) {
+  HostSpan span_("alternate_candidates");
   const std::vector<V3> failed_path = candidate_tip_path(failed, P.n, target);
   const int64_t S = static_cast<int64_t>(set->shortcuts.size());
   std::vector<std::vector<V3>> lists;
@@ -581,6 +611,7 @@ __global__ void k_gather_keys(const long long* __restrict__ keys, const long lon
 }
 
 std::vector<HostPose> solution_poses(rp_solution_set* s, const std::vector<long long>& ordinals) {
+  HostSpan span_("solution_poses");
   std::vector<HostPose> out;
   if (ordinals.empty()) return out;
   ensure_keys(s);

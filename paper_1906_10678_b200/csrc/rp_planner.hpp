@@ -54,6 +54,26 @@ struct Planner {
   int first_colliding(const std::vector<HostPose>& poses, const rp_grid* grid);
   /// pose_valid over a batch on the device: first invalid index or -1.
   int valid_poses(const DevPose* poses, int count);
+
+  /// Whole backward pass in one persistent cooperative kernel. Returns
+  /// false (nothing done) when the configuration exceeds its limits; then
+  /// the caller runs the host-sequenced pass.
+  struct BpOut {
+    bool ok = false;
+    int failed_index = -1;
+    std::vector<DevPose> poses;
+    std::vector<double> relax;
+    std::vector<int> kind;
+    std::vector<V3> wps;
+  };
+  bool backward_pass_device(const std::vector<V3>& wps, const HostPose& anchor,
+                            const std::vector<double>& factors, bool cloud, double cloud_radius,
+                            const HostPose* fixed_first, const HostPose* bias, BpOut* out);
+  DevBuf<unsigned> bp_bar;
+  DevBuf<int> bp_state;
+  DevBuf<WikBest> bp_best;
+  int bp_blocks = 0;
+  bool use_device_pass = true;
   std::vector<long long> rank_by_deviation(rp_solution_set* set,
                                            const std::vector<std::vector<V3>>& lists,
                                            const std::vector<V3>& poly, bool lead, V3 lead_pt,

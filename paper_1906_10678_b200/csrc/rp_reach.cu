@@ -639,6 +639,7 @@ static HostShortcut host_shortcut(const rp_solution_set* s, const ShortcutRec& r
 
 rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q, const rp_grid* g,
                              V3 target, const rp_reach_params& rp) {
+  HostSpan span_("solve_reach");
   validate_arm(arm);
   validate_reach(rp);
   if (rp.mode == RP_MODE_8DOF) {
@@ -812,6 +813,7 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
 }
 
 void ensure_keys(rp_solution_set* s) {
+  HostSpan span_("ensure_keys");
   if (s->keys_ready) return;
   rp_ctx* ctx = s->ctx;
   cudaStream_t st = ctx->stream;

@@ -196,6 +196,24 @@ def test_oracle_equivalence(ctx, name):
     assert np.array_equal(S.keys(), R.keys(rns))
 
 
+def test_plan_deterministic(ctx):
+    """SPEC acceptance 9 analogue: identical inputs -> identical plans, run
+    after run (the device backward pass is a multi-block cooperative kernel)."""
+    api = _api()
+    sc = scenes.config("C2", quiver_deg=2.0)
+    arm, rp, q, g = gpu_problem(ctx, sc)
+    first = None
+    for _ in range(4):
+        rc, plan = api.plan_reach_then_path(ctx, arm, q, g, sc.target, rp)
+        assert rc == 0
+        s = plan.summary()
+        key = (s["kind"], tuple(s["notes"]), np.asarray(s["waypoints"]).tobytes(),
+               tuple(bytes(p) for p, _ in s["poses"]))
+        if first is None:
+            first = key
+        assert key == first
+
+
 @pytest.mark.parametrize("name,deg", [("C1", 5.0), ("C2", 5.0)])
 def test_plan_reach_then_path(ctx, name, deg):
     api = _api()
