@@ -261,8 +261,8 @@ def run_ours(args, sc):
     ctx.reset_timing()
     step(False)
     names = ["voxelize", "mark_dilate", "seg1", "compact", "seg2", "select", "shortcuts", "walk4",
-             "wik_filter", "wik_compact", "wik_pairs", "score", "materialize", "unfold",
-             "pose_check", "refine", "trail"]
+             "backward_pass", "wik_filter", "wik_compact", "wik_pairs", "score", "materialize",
+             "unfold", "pose_check", "refine", "trail"]
     kt = {n: ctx.kernel_time(n) for n in names}
     ctx.enable_timing(False)
     kernel_ms = {n: round(v[0], 4) for n, v in kt.items() if v[1]}

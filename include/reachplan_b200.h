@@ -297,10 +297,12 @@ rp_status rp_plan_from_reach(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q,
                              const rp_solution_set* set, const rp_chosen* chosen,
                              const double target[3], const rp_reach_params* rp,
                              const rp_path_params* pp, rp_plan** out);
-/* [plan_arbitrary, src/path_planner.cpp:906-998]; start pose joints/segments */
+/* [plan_arbitrary, src/path_planner.cpp:906-998]; start_waypoints (nullable)
+ * carries start_pose->n_waypoints xyz samples (PoseChain::waypoints) */
 rp_status rp_plan_arbitrary(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q, const rp_grid* g,
-                            const rp_pose* start_pose, const double target[3],
-                            const rp_reach_params* rp, const rp_path_params* pp, rp_plan** out);
+                            const rp_pose* start_pose, const double* start_waypoints,
+                            const double target[3], const rp_reach_params* rp,
+                            const rp_path_params* pp, rp_plan** out);
 /* [replan_dynamic, src/path_planner.cpp:1000-1102] */
 rp_status rp_replan_dynamic(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q,
                             const rp_grid* grid_static, const rp_plan* active,

@@ -96,7 +96,7 @@ def lib():
                                      P(abi.PathParams), P(vp)], C.c_int32),
         "rp_plan_from_reach": ([vp, P(abi.Arm), vp, vp, vp, P(abi.Chosen), d3, P(abi.ReachParams),
                                 P(abi.PathParams), P(vp)], C.c_int32),
-        "rp_plan_arbitrary": ([vp, P(abi.Arm), vp, vp, P(abi.Pose), d3, P(abi.ReachParams),
+        "rp_plan_arbitrary": ([vp, P(abi.Arm), vp, vp, P(abi.Pose), vp, d3, P(abi.ReachParams),
                                P(abi.PathParams), P(vp)], C.c_int32),
         "rp_replan_dynamic": ([vp, P(abi.Arm), vp, vp, vp, C.c_int32, P(abi.Obstacle), C.c_double,
                                C.c_double, P(abi.ReachParams), P(abi.PathParams), P(vp)], C.c_int32),
@@ -446,11 +446,16 @@ def plan_from_reach(ctx, arm, quiver, grid, sset, chosen, target, rp, pp=None):
                       n_samples=rp.n_samples)
 
 
-def plan_arbitrary(ctx, arm, quiver, grid, start_pose, target, rp, pp=None):
+def plan_arbitrary(ctx, arm, quiver, grid, start_pose, target, rp, pp=None, start_waypoints=None):
+    """plan_arbitrary; start_waypoints = the start PoseChain's waypoint samples."""
     pp = pp or abi.make_path_params()
+    w = None
+    if start_waypoints is not None and len(start_waypoints):
+        w = np.ascontiguousarray(start_waypoints, np.float64)
+        assert len(w) == start_pose.n_waypoints
     return _plan_call(lib().rp_plan_arbitrary, ctx.h, C.byref(arm), quiver.h, grid.h,
-                      C.byref(start_pose), d3(target), C.byref(rp), C.byref(pp),
-                      n_samples=rp.n_samples)
+                      C.byref(start_pose), w.ctypes.data if w is not None else None, d3(target),
+                      C.byref(rp), C.byref(pp), n_samples=rp.n_samples)
 
 
 def replan_dynamic(ctx, arm, quiver, grid_static, active: Plan, index, obstacle, rp, pp=None,

@@ -807,10 +807,10 @@ rp_status rp_plan_from_reach(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q,
 }
 
 rp_status rp_plan_arbitrary(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q, const rp_grid* g,
-                            const rp_pose* start, const double target[3], const rp_reach_params* rp,
-                            const rp_path_params* pp, rp_plan** out) {
+                            const rp_pose* start, const double* start_wps, const double target[3],
+                            const rp_reach_params* rp, const rp_path_params* pp, rp_plan** out) {
   return guarded([&] {
-    *out = plan_arbitrary(ctx, *arm, q, g, from_abi(*start, nullptr),
+    *out = plan_arbitrary(ctx, *arm, q, g, from_abi(*start, start_wps),
                           V3{target[0], target[1], target[2]}, *rp, *pp);
   });
 }
