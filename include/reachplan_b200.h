@@ -281,6 +281,25 @@ rp_status rp_solution_set_shortcut(const rp_solution_set* s, int64_t k, rp_short
 rp_status rp_solution_set_destroy(rp_solution_set* s);
 /* [select_solution, src/reach_solver.cpp:548-577] */
 rp_status rp_select_solution(const rp_solution_set* s, rp_chosen* out);
+/* Batched reach queries (BASELINE configs[4]): for each target, exactly
+ * solve_reach + select_solution + exact refinement of a chosen reach pose
+ * (src/reach_solver.cpp:480-577, src/arm_model.cpp:258-324). The
+ * target-independent segment clearance is computed once per call and shared
+ * by all targets. */
+typedef struct rp_batch_result {
+  int32_t status;   /* RP_OK, or RP_E_NO_SOLUTION when the set is empty, or the
+                       refinement's error (e.g. RP_E_UNREACHABLE_TARGET) */
+  int32_t kind;     /* RP_CHOSEN_REACH_POSE / RP_CHOSEN_SHORTCUT */
+  int32_t seg1, seg2, cone; /* chosen key (reach pose) or shortcut indices */
+  int32_t _pad;
+  int64_t n_solutions, n_shortcuts;
+  double path_length;
+  rp_pose refined;  /* refined reach pose (kind == REACH_POSE, status == OK) */
+  rp_solve_stats stats;
+} rp_batch_result;
+rp_status rp_solve_reach_batch(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q,
+                               const rp_grid* g, const double* targets, int32_t n_targets,
+                               const rp_reach_params* rp, rp_batch_result* out);
 /* [exact_refine_8dof / _6dof / _8dof_triangle, src/arm_model.cpp:258-324] */
 rp_status rp_exact_refine(rp_ctx* ctx, const rp_arm* arm, const rp_pose* approx,
                           const double target[3], int32_t variant /*0 auto,1 triangle*/,

@@ -128,6 +128,15 @@ class PlanInfo(C.Structure):
     ]
 
 
+class BatchResult(C.Structure):
+    _fields_ = [
+        ("status", C.c_int32), ("kind", C.c_int32), ("seg1", C.c_int32), ("seg2", C.c_int32),
+        ("cone", C.c_int32), ("_pad", C.c_int32), ("n_solutions", C.c_int64),
+        ("n_shortcuts", C.c_int64), ("path_length", C.c_double), ("refined", Pose),
+        ("stats", SolveStats),
+    ]
+
+
 # ---- defaults mirroring the reference member initialisers ----------------------
 
 def make_arm(lengths, root=(0.0, 0.0, 0.0), arm_radius=0.0) -> Arm:

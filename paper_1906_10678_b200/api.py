@@ -91,7 +91,9 @@ def lib():
                                      C.c_int32),
         "rp_solution_set_destroy": ([vp], C.c_int32),
         "rp_select_solution": ([vp, P(abi.Chosen)], C.c_int32),
-        "rp_exact_refine": ([vp, P(abi.Arm), P(abi.Pose), d3, C.c_int32, P(abi.Pose)], C.c_int32),
+        "rp_solve_reach_batch": ([vp, P(abi.Arm), vp, vp, vp, C.c_int32, P(abi.ReachParams),
+                                  P(abi.BatchResult)], C.c_int32),
+        "rp_exact_refine":([vp, P(abi.Arm), P(abi.Pose), d3, C.c_int32, P(abi.Pose)], C.c_int32),
         "rp_plan_reach_then_path": ([vp, P(abi.Arm), vp, vp, d3, P(abi.ReachParams),
                                      P(abi.PathParams), P(vp)], C.c_int32),
         "rp_plan_from_reach": ([vp, P(abi.Arm), vp, vp, vp, P(abi.Chosen), d3, P(abi.ReachParams),
@@ -404,6 +406,16 @@ def solve_reach(ctx, arm, quiver, grid, target, rp) -> SolutionSet:
     _check(lib().rp_solve_reach(ctx.h, C.byref(arm), quiver.h, grid.h, d3(target), C.byref(rp),
                                 C.byref(h)))
     return SolutionSet(ctx, h, target, rp.n_samples)
+
+
+def solve_reach_batch(ctx, arm, quiver, grid, targets, rp):
+    """Per target: solve_reach + select_solution + exact refinement."""
+    t = np.ascontiguousarray(targets, np.float64).reshape(-1, 3)
+    out = (abi.BatchResult * max(1, len(t)))()
+    if len(t):
+        _check(lib().rp_solve_reach_batch(ctx.h, C.byref(arm), quiver.h, grid.h, t.ctypes.data,
+                                          len(t), C.byref(rp), out))
+    return list(out)[:len(t)]
 
 
 def prune_segment1(ctx, arm, quiver, grid, targets, rp):

@@ -170,6 +170,23 @@ __host__ __device__ __forceinline__ double point_to_segment(V3 p, V3 a, V3 b) {
   return norm(p - (a + t * ab));
 }
 
+/// Conservative prefilter for point_to_segment(t, a, a + L*dir) <= r0
+/// (dir unit): false only when the segment certainly stays farther than r0
+/// from t. Pass r = r0 + a margin (callers use 1e-6 m). If the true distance
+/// is <= r0 either t is within r of a, or the closest point is interior,
+/// so dot(dir, t-a) > 0 and the perpendicular distance^2 = |t-a|^2 -
+/// dot^2 <= r0^2 < r^2, which this test accepts.
+__host__ __device__ __forceinline__ bool may_pass_near(V3 t, V3 a, V3 dir, double L, double r) {
+  const V3 w = t - a;
+  const double d2 = sqnorm(w);
+  const double r2 = r * r;
+  if (d2 <= r2) return true;
+  if (d2 > (L + r) * (L + r)) return false;
+  const double dw = dot(dir, w);
+  if (dw <= 0.0) return false;
+  return dw * dw >= (d2 - r2) * (1.0 - 1e-9);
+}
+
 /// segment_segment_distance (src/arm_model.cpp:326-361)
 __host__ __device__ __forceinline__ double seg_seg_distance(V3 a0, V3 a1, V3 b0, V3 b1) {
   const V3 d1 = a1 - a0;

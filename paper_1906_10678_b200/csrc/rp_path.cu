@@ -3,6 +3,7 @@
 // refinement, polyline-deviation scoring.
 #include "rp_path.cuh"
 #include "rp_planner.hpp"
+#include "rp_refine.cuh"
 
 #include <cub/cub.cuh>
 
@@ -837,89 +838,12 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
 // ---------------------------------------------------------------------------
 // Single-pose operations (one thread): refinement and trail folding.
 
-__device__ inline int triangle_vertex(V3 a, V3 b, double la, double lb, V3 n, V3 hint, V3* out,
-                                      int* msg) {
-  const V3 ab = b - a;
-  const double c = rpd::norm(ab);
-  if (!(c <= (la + lb) * (1.0 + 1e-12))) { *msg = 1; return RP_E_UNREACHABLE_TARGET; }
-  if (!(c >= fabs(la - lb) * (1.0 - 1e-12) - 1e-15)) { *msg = 2; return RP_E_UNREACHABLE_TARGET; }
-  const V3 c_hat = ab / c;
-  V3 m_hat = rpd::cross(n, c_hat);
-  const double m_norm = rpd::norm(m_hat);
-  if (!(m_norm > 1e-12)) { *msg = 3; return RP_E_DEGENERATE_INPUT; }
-  m_hat = m_hat / m_norm;
-  const double along = (c * c + la * la - lb * lb) / (2.0 * c);
-  const double h2 = la * la - along * along;
-  const double h = sqrt(h2 > 0.0 ? h2 : 0.0);
-  const V3 base = a + along * c_hat;
-  const V3 pp = base + h * m_hat;
-  const V3 pm = base - h * m_hat;
-  *out = rpd::sqnorm(pp - hint) <= rpd::sqnorm(pm - hint) ? pp : pm;
-  return 0;
-}
-
-__device__ inline V3 plane_normal_for_refine(const DevPose& p, V3 anchor, V3 target, int sa, int sb) {
-  V3 n = rpd::cross(p.seg[sa], p.seg[sb]);
-  if (rpd::norm(n) > 1e-12 * rpd::norm(p.seg[sa]) * rpd::norm(p.seg[sb])) return rpd::normalized(n);
-  n = rpd::cross(target - anchor, p.joints[sa + 1] - anchor);
-  if (rpd::norm(n) > 1e-12) return rpd::normalized(n);
-  const V3 chord = rpd::normalized(target - anchor);
-  const V3 seed = fabs(chord.z) < 0.9 ? V3{0, 0, 1} : V3{1, 0, 0};
-  return rpd::normalized(rpd::cross(chord, seed));
-}
-
 /// mode 0: exact_refine_8dof, 1: _8dof_triangle, 2: exact_refine_6dof
-/// (src/arm_model.cpp:258-324).
+/// (src/arm_model.cpp:258-324); the math lives in rp_refine.cuh.
 __global__ void k_refine(ArmDev arm, DevPose ap, V3 target, int mode, PoseOpOut* out) {
   PoseOpOut r{};
   r.pose = ap;
-  if (mode == 2) {
-    if (ap.nseg < 3) { r.status = RP_E_INVALID_PARAMETER; r.msg = 4; *out = r; return; }
-    if (arm.off[1] != 0.0 || arm.off[2] != 0.0) { r.status = RP_E_INVALID_PARAMETER; r.msg = 5; *out = r; return; }
-    const V3 p1 = ap.joints[1];
-    const V3 n = plane_normal_for_refine(ap, p1, target, 1, 2);
-    V3 p2;
-    r.status = triangle_vertex(p1, target, arm.L[1], arm.L[2], n, ap.joints[2], &p2, &r.msg);
-    if (!r.status) {
-      r.pose.seg[1] = p2 - p1;
-      r.pose.seg[2] = target - p2;
-      r.pose.joints[2] = p2;
-      r.pose.joints[3] = target;
-      r.pose.qidx[1] = -1;
-      r.pose.qidx[2] = -1;
-    }
-  } else {
-    if (ap.nseg != 4) { r.status = RP_E_INVALID_PARAMETER; r.msg = 6; *out = r; return; }
-    if (arm.off[2] != 0.0 || arm.off[3] != 0.0) { r.status = RP_E_INVALID_PARAMETER; r.msg = 7; *out = r; return; }
-    if (mode == 0) {
-      const V3 v3 = ap.seg[2];
-      const double v3_len = rpd::norm(v3);
-      if (!(v3_len >= 1e-9)) { r.status = RP_E_DEGENERATE_INPUT; r.msg = 8; *out = r; return; }
-      const V3 p2 = ap.joints[2];
-      const V3 d3 = target - p2;
-      const V3 s3 = v3 * (arm.L[2] / v3_len);
-      const V3 s4 = d3 - s3;
-      r.pose.seg[2] = s3;
-      r.pose.seg[3] = s4;
-      r.pose.joints[3] = p2 + s3;
-      r.pose.joints[4] = r.pose.joints[3] + s4;
-      r.pose.s4dev = fabs(rpd::norm(s4) - arm.L[3]);
-    } else {
-      const V3 p2 = ap.joints[2];
-      const V3 n = plane_normal_for_refine(ap, p2, target, 2, 3);
-      V3 p3;
-      r.status = triangle_vertex(p2, target, arm.L[2], arm.L[3], n, ap.joints[3], &p3, &r.msg);
-      if (!r.status) {
-        r.pose.seg[2] = p3 - p2;
-        r.pose.seg[3] = target - p3;
-        r.pose.joints[3] = p3;
-        r.pose.joints[4] = target;
-        r.pose.s4dev = fabs(rpd::norm(r.pose.seg[3]) - arm.L[3]);
-      }
-    }
-    r.pose.qidx[2] = -1;
-    r.pose.qidx[3] = -1;
-  }
+  r.status = refine_pose(arm, r.pose, target, mode, &r.msg);
   *out = r;
 }
 
@@ -1088,20 +1012,6 @@ double mean_polyline_deviation(rp_ctx* ctx, const std::vector<V3>& pts, const st
   double h = 0.0;
   copy_to_host(ctx, &h, o.p, sizeof(h));
   return h;
-}
-
-static const char* refine_msg(int m) {
-  switch (m) {
-    case 1: return "target beyond combined segment lengths";
-    case 2: return "target inside the unreachable inner sphere";
-    case 3: return "solution plane normal parallel to chord";
-    case 4: return "need a 3-segment pose";
-    case 5: return "triangle refinement requires coaxial joints 2 and 3";
-    case 6: return "need a 4-segment pose";
-    case 7: return "8DOF refinement requires coaxial joints 3 and 4";
-    case 8: return "gap vector is numerically zero";
-  }
-  return "refinement failed";
 }
 
 DevPose to_dev(const HostPose& h) {

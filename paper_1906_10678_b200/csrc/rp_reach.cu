@@ -15,13 +15,16 @@
 // solution set, the shortcut set and all 13 SolveStats counters are
 // bit-identical to the reference.
 #include "rp_reach.cuh"
+#include "rp_refine.cuh"
 
 #include <cub/cub.cuh>
 
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <memory>
 
 namespace rp {
 
@@ -203,7 +206,8 @@ __global__ void __launch_bounds__(256) k_seg2(SolveDev a, const SurvDev* __restr
         if (ok && has_e2 && !offset_link_clear(a.g, h.p1, e2, a.spacing)) ok = false;
         if (ok) {
           const int fb = rpd::walk_first_blocked(a.g, link, p2, a.n);
-          if (rpd::point_to_segment(a.target, link, p2) <= a.near_r + 1e-9) {
+          if (rpd::may_pass_near(a.target, link, dir2, L2, a.near_r + 1e-6) &&
+              rpd::point_to_segment(a.target, link, p2) <= a.near_r + 1e-9) {
             const unsigned pos = atomicAdd(sc_count, 1u);
             if (pos < kShortcutCap) sc_list[pos] = (1ll << 62) | p;
           }
@@ -310,6 +314,139 @@ __global__ void __launch_bounds__(256) k_seg2(SolveDev a, const SurvDev* __restr
     for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
       if (wb[w].len < b.len || (wb[w].len == b.len && wb[w].key < b.key)) b = wb[w];
     block_best[blockIdx.x] = b;
+  }
+}
+
+/// k_seg2 for the common case (coaxial arm, no limits, no cone precheck,
+/// one backward point): a warp owns survivor rows and sweeps j. Phase 1
+/// (every pair, lanes busy) walks segment 2, runs the near-encounter scan
+/// and a conservative band prefilter; clear band candidates are queued per
+/// warp in shared memory and phase 2 runs the exact gap test, the v3 walk
+/// and the self-collision check 32 at a time without divergence. Counters,
+/// solution bits (atomicOr into a zeroed set) and the block argmin are the
+/// same as k_seg2's.
+template <bool EIGHT>
+__global__ void __launch_bounds__(256) k_seg2_rows(SolveDev a, const SurvDev* __restrict__ sv, int S1,
+                                                   uint32_t* __restrict__ sol_bits,
+                                                   unsigned long long* ctr, long long* sc_list,
+                                                   unsigned* sc_count, BestRec* __restrict__ block_best) {
+  unsigned c_lim = 0, c_clear = 0, c_gp = 0, c_jp = 0, c_v3 = 0, c_sol = 0;
+  double best_len = 1e308;
+  long long best_key = LLONG_MAX;
+  const int lane = threadIdx.x & 31;
+  const int warp_id = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const ArmDev& arm = a.arm;
+  const double L1 = arm.L[0], L2 = arm.L[1], L3 = arm.L[2];
+  const double min_sep = 2.0 * arm.arm_radius;
+  const V3 b = a.bpts[0];
+  const V3 bdir = a.bdirs[0];
+  const bool walk4 = !EIGHT || a.walk4_ok[0];
+  const double rnear = a.near_r + 1e-6;
+  __shared__ int wqs[8][64];
+  int* wq = wqs[threadIdx.x >> 5];
+  constexpr int kChunk = 1024;  // j per work unit (balances small S1)
+  const int nchunk = (a.Q + kChunk - 1) / kChunk;
+  for (int u = warp_id; u < S1 * nchunk; u += nwarps) {
+    const int s = u / nchunk;
+    const int jbeg = (u - s * nchunk) * kChunk;
+    const int jend = min(a.Q, jbeg + kChunk);
+    const SurvDev& h = sv[s];
+    const V3 p1 = h.p1;
+    const V3 s1 = L1 * qvec(a, h.i);
+    const bool row_near = rpd::sqnorm(a.target - p1) <= (L2 + rnear) * (L2 + rnear);
+    const double db = sqrt(rpd::sqnorm(b - p1));
+    const bool row_gap = db <= (sqrt(a.coarse2) + L2) * (1.0 + 1e-9) + 1e-12 &&
+                         db >= (L3 - a.eps - L2) * (1.0 - 1e-9) - 1e-12;
+    const auto heavy = [&](int j) {
+      const long long p = static_cast<long long>(s) * a.Q + j;
+      const V3 dir2 = qvec(a, j);
+      const V3 p2 = p1 + L2 * dir2;
+      const V3 v3 = b - p2;
+      const double v3_len = rpd::norm(v3);
+      if (fabs(v3_len - L3) > a.eps) return;
+      ++c_gp;
+      if (v3_len < 1e-12) return;
+      ++c_jp;
+      if (rpd::walk_first_blocked(a.g, p2, b, a.n) != 0) return;
+      ++c_v3;
+      if (EIGHT && !walk4) return;
+      const V3 s2 = L2 * dir2;
+      V3 J[5];
+      J[0] = arm.root;
+      J[1] = J[0] + s1;
+      J[2] = J[1] + s2;
+      J[3] = J[2] + v3;
+      if (EIGHT) J[4] = J[3] + a.L4 * bdir;
+      if (!rpd::self_collision_free(J, EIGHT ? 4 : 3, min_sep)) return;
+      ++c_sol;
+      atomicOr(sol_bits + (p >> 5), 1u << (p & 31));
+      const double len = (rpd::norm(s1) + rpd::norm(s2)) + rpd::norm(v3);
+      if (len < best_len || (len == best_len && p < best_key)) {
+        best_len = len;
+        best_key = p;
+      }
+    };
+    int qn = 0;
+    for (int j0 = jbeg; j0 < jend; j0 += 32) {
+      const int j = j0 + lane;
+      bool pass = false;
+      if (j < jend) {
+        ++c_lim;
+        const V3 dir2 = qvec(a, j);
+        const V3 p2 = p1 + L2 * dir2;
+        const int fb = rpd::walk_first_blocked(a.g, p1, p2, a.n);
+        if (row_near && rpd::may_pass_near(a.target, p1, dir2, L2, rnear) &&
+            rpd::point_to_segment(a.target, p1, p2) <= a.near_r + 1e-9) {
+          const unsigned pos = atomicAdd(sc_count, 1u);
+          if (pos < kShortcutCap) sc_list[pos] = (1ll << 62) | (static_cast<long long>(s) * a.Q + j);
+        }
+        if (fb == 0) {
+          ++c_clear;
+          if (row_gap) {
+            const double v2 = rpd::sqnorm(b - p2);
+            pass = v2 <= a.coarse2 && v2 >= a.band_lo2;
+          }
+        }
+      }
+      const unsigned m = __ballot_sync(FULL, pass);
+      if (pass) wq[qn + __popc(m & ((1u << lane) - 1u))] = j;
+      qn += __popc(m);
+      __syncwarp();
+      if (qn >= 32) {
+        heavy(wq[lane]);
+        __syncwarp();
+        if (lane < qn - 32) wq[lane] = wq[32 + lane];
+        qn -= 32;
+        __syncwarp();
+      }
+    }
+    if (lane < qn) heavy(wq[lane]);
+    __syncwarp();
+  }
+  warp_flush(ctr, C_SEG2_LIMIT, c_lim);
+  warp_flush(ctr, C_SEG2_CLEAR, c_clear);
+  warp_flush(ctr, C_GAP_TESTED, c_clear);
+  warp_flush(ctr, C_GAP_PASS, c_gp);
+  warp_flush(ctr, C_JOINT_PASS, c_jp);
+  warp_flush(ctr, C_V3_CLEAR, c_v3);
+  warp_flush(ctr, C_SOLUTIONS, c_sol);
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ol = __shfl_down_sync(FULL, best_len, off);
+    const long long ok = __shfl_down_sync(FULL, best_key, off);
+    if (ol < best_len || (ol == best_len && ok < best_key)) {
+      best_len = ol;
+      best_key = ok;
+    }
+  }
+  __shared__ BestRec wb[8];
+  if (lane == 0) wb[threadIdx.x >> 5] = BestRec{best_len, best_key};
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    BestRec r = wb[0];
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+      if (wb[w].len < r.len || (wb[w].len == r.len && wb[w].key < r.key)) r = wb[w];
+    block_best[blockIdx.x] = r;
   }
 }
 
@@ -683,6 +820,7 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
     const double L3 = arm.lengths[2];
     a.eps = eps;
     a.coarse2 = (L3 + eps) * (L3 + eps) * (1.0 + 1e-12);
+    a.band_lo2 = L3 - eps > 0.0 ? (L3 - eps) * (L3 - eps) * (1.0 - 1e-9) : 0.0;
     double budget = arm.lengths[1] + arm.lengths[2] + eps;
     if (eight) budget += arm.lengths[3];
     budget += 1e-9;
@@ -751,7 +889,19 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
                static_cast<const SurvDev*>(s->surv.p), s->n_pairs, s->sol_bits.p, ctr.p,
                sc_list.p, sc_count.p, bb.p);
       };
-      if (eight) {
+      static const bool flat = std::getenv("RP_SEG2_FLAT") != nullptr;
+      if (!general && B1 && !flat) {
+        s->sol_bits.zero();
+        const int64_t units = static_cast<int64_t>(S1) * ((q->n + 1023) / 1024);
+        const int rblocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks, (units + 7) / 8)));
+        auto runr = [&](auto kern) {
+          launch(ctx, "seg2", kern, dim3(rblocks), dim3(threads), 0, a,
+                 static_cast<const SurvDev*>(s->surv.p), S1, s->sol_bits.p, ctr.p, sc_list.p,
+                 sc_count.p, bb.p);
+        };
+        eight ? runr(k_seg2_rows<true>) : runr(k_seg2_rows<false>);
+        blocks = rblocks;
+      } else if (eight) {
         if (general) B1 ? run(k_seg2<true, true, true>) : run(k_seg2<true, true, false>);
         else B1 ? run(k_seg2<true, false, true>) : run(k_seg2<true, false, false>);
       } else {
@@ -1084,3 +1234,684 @@ rp_status rp_select_solution(const rp_solution_set* s, rp_chosen* out) {
 }
 
 }  // extern "C"
+
+// ===========================================================================
+// Batched reach queries (BASELINE configs[4]).
+//
+// Segment-1 and segment-2 clearance depend only on (i, j), not on the target
+// (src/reach_solver.cpp:278, 368): one target-independent bitmap
+// clear2[i][j] (Q^2 bits, 13 MB at 2 deg) is built once per call and every
+// query's segment-2 expansion tests a bit instead of walking 8 samples. The
+// target-dependent tests (reach precheck, gap band, v3 / s4 walks,
+// self-collision, near-encounter scans) run per query exactly as in k_seg2,
+// so every counter and the chosen solution equal solve_reach's.
+namespace rp {
+namespace {
+
+/// Row-wise clearance of segment 2 for every (i, j) with a clear segment 1.
+__global__ void __launch_bounds__(256) k_clear2(SolveDev a, const uint32_t* __restrict__ walk1_bits,
+                                                int W, uint32_t* __restrict__ clear2) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t total = static_cast<int64_t>(a.Q) * W;
+  for (int64_t wd = warp; wd < total; wd += nwarps) {
+    const int i = static_cast<int>(wd / W);
+    const int j = static_cast<int>(wd - static_cast<int64_t>(i) * W) * 32 + lane;
+    bool clear = false;
+    if (j < a.Q && ((walk1_bits[i >> 5] >> (i & 31)) & 1u)) {
+      const V3 p1 = a.arm.root + a.arm.L[0] * qvec(a, i);
+      const V3 p2 = p1 + a.arm.L[1] * qvec(a, j);
+      clear = rpd::walk_first_blocked(a.g, p1, p2, a.n) == 0;
+    }
+    const unsigned m = __ballot_sync(FULL, clear);
+    if (lane == 0) clear2[wd] = m;
+  }
+}
+
+/// Segment-1 walk verdicts (target independent).
+__global__ void k_walk1(SolveDev a, uint32_t* __restrict__ bits) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  bool clear = false;
+  if (i < a.Q) {
+    const V3 p1 = a.arm.root + a.arm.L[0] * qvec(a, i);
+    clear = rpd::walk_first_blocked(a.g, a.arm.root, p1, a.n) == 0;
+  }
+  const unsigned m = __ballot_sync(FULL, clear);
+  if ((threadIdx.x & 31) == 0 && (i >> 5) < (a.Q + 31) / 32) bits[i >> 5] = m;
+}
+
+// ---- multi-query pipeline: every stage covers all targets of a chunk ------
+
+constexpr unsigned kBatchShortcutCap = 1u << 24;  // near-encounter candidates per chunk
+
+struct BatchDev {
+  SolveDev a;  // shared constants (target fields unused)
+  int T, W, BPT, eight;
+  const V3* targets;
+  const V3* bpts;
+  const uint8_t* walk4_ok;
+  const uint32_t* walk1;
+  const uint32_t* clear2;
+  uint32_t* surv_bits;  // [T*W]
+  int* surv_idx;        // [T*Q]
+  int* surv_cnt;        // [T]
+  unsigned long long* ctr;  // [T*C_COUNT]
+  long long* sc_list;       // (t << 40) | (seg2 << 39) | payload
+  unsigned* sc_count;
+  BestRec* bb;    // [T*BPT]
+  BestRec* best;  // [T]
+};
+
+__device__ __forceinline__ void warp_flush_t(unsigned long long* ctr, int idx, unsigned v) {
+  v = __reduce_add_sync(FULL, v);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(ctr + idx, static_cast<unsigned long long>(v));
+}
+
+__global__ void k_bq_walk4(BatchDev d, uint8_t* walk4) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= d.T) return;
+  walk4[t] = (!d.eight || rpd::walk_first_blocked(d.a.g, d.bpts[t], d.targets[t], d.a.n) == 0) ? 1 : 0;
+}
+
+/// prune_segment1 for every (target, direction): blockIdx.y = target.
+__global__ void __launch_bounds__(256) k_bq_seg1(BatchDev d) {
+  const int t = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const SolveDev& a = d.a;
+  const V3 target = d.targets[t];
+  bool valid = i < a.Q, reach = false, surv = false;
+  if (valid) {
+    const V3 p1 = a.arm.root + a.arm.L[0] * qvec(a, i);
+    reach = a.disable_prune != 0 || rpd::sqnorm(p1 - target) <= a.budget2;
+    if (rpd::point_to_segment(target, a.arm.root, p1) <= a.near_r + 1e-9) {
+      const unsigned pos = atomicAdd(d.sc_count, 1u);
+      if (pos < kBatchShortcutCap) d.sc_list[pos] = (static_cast<long long>(t) << 40) | i;
+    }
+    surv = reach && ((d.walk1[i >> 5] >> (i & 31)) & 1u);
+  }
+  const unsigned m = __ballot_sync(FULL, surv);
+  if ((threadIdx.x & 31) == 0 && (i >> 5) < d.W) d.surv_bits[static_cast<size_t>(t) * d.W + (i >> 5)] = m;
+  unsigned long long* c = d.ctr + static_cast<size_t>(t) * C_COUNT;
+  warp_flush_t(c, C_SEG1_LIMIT, valid ? 1u : 0u);
+  warp_flush_t(c, C_SEG1_REACH, reach ? 1u : 0u);
+  warp_flush_t(c, C_SEG1_SURV, surv ? 1u : 0u);
+}
+
+/// Ordered survivor compaction, one block per target.
+__global__ void __launch_bounds__(1024) k_bq_compact(BatchDev d) {
+  typedef cub::BlockScan<int, 1024> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int carry;
+  const int t = blockIdx.x;
+  const uint32_t* bits = d.surv_bits + static_cast<size_t>(t) * d.W;
+  int* out = d.surv_idx + static_cast<size_t>(t) * d.a.Q;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int w0 = 0; w0 < d.W; w0 += 1024) {
+    const int w = w0 + threadIdx.x;
+    const uint32_t word = w < d.W ? bits[w] : 0u;
+    int off = 0, total = 0;
+    Scan(tmp).ExclusiveSum(__popc(word), off, total);
+    off += carry;
+    uint32_t x = word;
+    while (x) {
+      const int b = __ffs(x) - 1;
+      x &= x - 1;
+      out[off++] = w * 32 + b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) d.surv_cnt[t] = carry;
+}
+
+/// k_seg2_cached for every target of the chunk: blockIdx.y = target,
+/// blockIdx.x strides over that target's (survivor, j) pairs.
+template <bool EIGHT>
+__global__ void __launch_bounds__(256) k_bq_seg2(BatchDev d) {
+  const int t = blockIdx.y;
+  const SolveDev& a = d.a;
+  const ArmDev& arm = a.arm;
+  const double L1 = arm.L[0], L2 = arm.L[1], L3 = arm.L[2];
+  const double min_sep = 2.0 * arm.arm_radius;
+  const V3 target = d.targets[t];
+  const V3 b = d.bpts[t];
+  const V3 bdir = a.bdirs[0];
+  const bool walk4 = !EIGHT || d.walk4_ok[t];
+  const int S1 = d.surv_cnt[t];
+  const int* sidx = d.surv_idx + static_cast<size_t>(t) * a.Q;
+  const int64_t npairs = static_cast<int64_t>(S1) * a.Q;
+  unsigned c_clear = 0, c_gp = 0, c_jp = 0, c_v3 = 0, c_sol = 0;
+  double best_len = 1e308;
+  long long best_key = LLONG_MAX;
+  const int lane = threadIdx.x & 31;
+  const int warp_id = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const double rnear = a.near_r + 1e-6;
+  (void)npairs;
+  __shared__ int wqs[8][64];
+  int* wq = wqs[threadIdx.x >> 5];
+  // a warp owns whole survivor rows (s) and sweeps j; row constants hoisted
+  for (int s = warp_id; s < S1; s += nwarps) {
+    const int i = sidx[s];
+    const V3 s1 = L1 * qvec(a, i);
+    const V3 p1 = arm.root + s1;
+    const uint32_t* crow = d.clear2 + static_cast<int64_t>(i) * d.W;
+    const double dt2 = rpd::sqnorm(target - p1);
+    const bool row_near = dt2 <= (L2 + rnear) * (L2 + rnear);  // else no pair can be near
+    // segment-2 clear count of the row = popcount of its clearance bits
+    for (int w = lane; w < d.W; w += 32) {
+      uint32_t bits = __ldg(crow + w);
+      const int rem = a.Q - w * 32;
+      if (rem < 32) bits &= (1u << rem) - 1u;
+      c_clear += __popc(bits);
+    }
+    // no j can pass the coarse gap test when b lies outside the shell
+    // |b - p1| in [L3 - eps - L2, sqrt(coarse2) + L2] (margins absorb rounding)
+    const double db = sqrt(rpd::sqnorm(b - p1));
+    const bool row_gap = db <= (sqrt(a.coarse2) + L2) * (1.0 + 1e-9) + 1e-12 &&
+                         db >= (L3 - a.eps - L2) * (1.0 - 1e-9) - 1e-12;
+    if (!row_near && !row_gap) continue;
+    // Phase 1 (all lanes busy): near-encounter scan and a conservative
+    // band + clearance prefilter; passers are queued per warp in shared
+    // memory. Phase 2 runs the exact gap test, the v3 walk and the
+    // self-collision check 32 queued pairs at a time, so the heavy tail
+    // (a few % of pairs) executes without divergence.
+    const auto heavy = [&](int j) {
+      const int64_t p = static_cast<int64_t>(s) * a.Q + j;
+      const V3 dir2 = qvec(a, j);
+      const V3 p2 = p1 + L2 * dir2;
+      const V3 v3 = b - p2;
+      const double v3_len = rpd::norm(v3);
+      if (fabs(v3_len - L3) > a.eps) return;
+      ++c_gp;
+      if (v3_len < 1e-12) return;
+      ++c_jp;
+      if (rpd::walk_first_blocked(a.g, p2, b, a.n) != 0) return;
+      ++c_v3;
+      if (!walk4) return;
+      const V3 s2 = L2 * dir2;
+      V3 J[5];
+      J[0] = arm.root;
+      J[1] = J[0] + s1;
+      J[2] = J[1] + s2;
+      J[3] = J[2] + v3;
+      if (EIGHT) J[4] = J[3] + a.L4 * bdir;
+      if (!rpd::self_collision_free(J, EIGHT ? 4 : 3, min_sep)) return;
+      ++c_sol;
+      const double len = (rpd::norm(s1) + rpd::norm(s2)) + rpd::norm(v3);
+      if (len < best_len || (len == best_len && p < best_key)) {
+        best_len = len;
+        best_key = p;
+      }
+    };
+    int qn = 0;
+    for (int j0 = 0; j0 < a.Q; j0 += 32) {
+      const int j = j0 + lane;
+      bool pass = false;
+      if (j < a.Q) {
+        const V3 dir2 = qvec(a, j);
+        const V3 p2 = p1 + L2 * dir2;
+        if (row_near && rpd::may_pass_near(target, p1, dir2, L2, rnear) &&
+            rpd::point_to_segment(target, p1, p2) <= a.near_r + 1e-9) {
+          const unsigned pos = atomicAdd(d.sc_count, 1u);
+          if (pos < kBatchShortcutCap)
+            d.sc_list[pos] = (static_cast<long long>(t) << 40) | (1ll << 39) |
+                             (static_cast<int64_t>(s) * a.Q + j);
+        }
+        if (row_gap) {
+          const double v2 = rpd::sqnorm(b - p2);
+          pass = v2 <= a.coarse2 && v2 >= a.band_lo2 &&
+                 ((__ldg(crow + (j >> 5)) >> (j & 31)) & 1u);
+        }
+      }
+      const unsigned m = __ballot_sync(FULL, pass);
+      if (pass) wq[qn + __popc(m & ((1u << lane) - 1u))] = j;
+      qn += __popc(m);
+      __syncwarp();
+      if (qn >= 32) {
+        heavy(wq[lane]);
+        __syncwarp();
+        if (lane < qn - 32) wq[lane] = wq[32 + lane];
+        qn -= 32;
+        __syncwarp();
+      }
+    }
+    if (lane < qn) heavy(wq[lane]);
+    __syncwarp();
+  }
+  unsigned long long* c = d.ctr + static_cast<size_t>(t) * C_COUNT;
+  warp_flush_t(c, C_SEG2_CLEAR, c_clear);
+  warp_flush_t(c, C_GAP_PASS, c_gp);
+  warp_flush_t(c, C_JOINT_PASS, c_jp);
+  warp_flush_t(c, C_V3_CLEAR, c_v3);
+  warp_flush_t(c, C_SOLUTIONS, c_sol);
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ol = __shfl_down_sync(FULL, best_len, off);
+    const long long ok = __shfl_down_sync(FULL, best_key, off);
+    if (ol < best_len || (ol == best_len && ok < best_key)) {
+      best_len = ol;
+      best_key = ok;
+    }
+  }
+  __shared__ BestRec wb[8];
+  if (lane == 0) wb[threadIdx.x >> 5] = BestRec{best_len, best_key};
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    BestRec r = wb[0];
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+      if (wb[w].len < r.len || (wb[w].len == r.len && wb[w].key < r.key)) r = wb[w];
+    d.bb[static_cast<size_t>(t) * d.BPT + blockIdx.x] = r;
+  }
+}
+
+__global__ void k_bq_best(BatchDev d) {
+  const int t = blockIdx.x;
+  BestRec b{1e308, LLONG_MAX};
+  for (int k = threadIdx.x; k < d.BPT; k += blockDim.x) {
+    const BestRec r = d.bb[static_cast<size_t>(t) * d.BPT + k];
+    if (r.len < b.len || (r.len == b.len && r.key < b.key)) b = r;
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ol = __shfl_down_sync(FULL, b.len, off);
+    const long long ok = __shfl_down_sync(FULL, b.key, off);
+    if (ol < b.len || (ol == b.len && ok < b.key)) b = BestRec{ol, ok};
+  }
+  __shared__ BestRec wb[32];
+  if ((threadIdx.x & 31) == 0) wb[threadIdx.x >> 5] = b;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    b = wb[0];
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+      if (wb[w].len < b.len || (wb[w].len == b.len && wb[w].key < b.key)) b = wb[w];
+    d.best[t] = b;
+  }
+}
+
+/// short_reach_scan for near-encounter candidates of any target.
+__global__ void k_bq_shortcuts(BatchDev d, const long long* keys, int n, ShortcutRec* out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const long long key = keys[k];
+  const int t = static_cast<int>(key >> 40);
+  const bool seg2 = (key >> 39) & 1;
+  const long long payload = key & ((1ll << 39) - 1);
+  SolveDev a = d.a;
+  a.target = d.targets[t];
+  const ArmDev& arm = a.arm;
+  ShortcutRec r{};
+  r.key = key;
+  if (!seg2) {
+    const int i = static_cast<int>(payload);
+    const V3 p1 = arm.root + arm.L[0] * qvec(a, i);
+    const int fb = rpd::walk_first_blocked(a.g, arm.root, p1, a.n);
+    r.segment_index = 1;
+    r.seg1 = i;
+    r.seg2 = -1;
+    scan_one(a, arm.root, p1, arm.root, fb, r, false, arm.root, arm.root);
+  } else {
+    const int s = static_cast<int>(payload / a.Q);
+    const int j = static_cast<int>(payload - static_cast<long long>(s) * a.Q);
+    const int i = d.surv_idx[static_cast<size_t>(t) * a.Q + s];
+    const V3 p1 = arm.root + arm.L[0] * qvec(a, i);
+    const V3 p2 = p1 + arm.L[1] * qvec(a, j);
+    const int fb = rpd::walk_first_blocked(a.g, p1, p2, a.n);
+    r.segment_index = 2;
+    r.seg1 = i;
+    r.seg2 = j;
+    scan_one(a, p1, p2, p1, fb, r, true, arm.root, p1);
+  }
+  out[k] = r;
+}
+
+/// Per-target shortcut summary: count and select_solution's pick (shortest,
+/// first in canonical order).
+struct ScBest {
+  int count, seg1, seg2, _pad;
+  double path_length;
+};
+
+/// One block per target over its (key-sorted) shortcut records.
+__global__ void k_bq_sc_reduce(const long long* __restrict__ keys, const ShortcutRec* __restrict__ recs,
+                               int n, ScBest* __restrict__ out, uint8_t* __restrict__ has_sc) {
+  const long long t = blockIdx.x;
+  // [lo, hi) of keys with target t (keys sorted ascending)
+  auto lower = [&](long long v) {
+    int a = 0, b = n;
+    while (a < b) {
+      const int m = (a + b) >> 1;
+      if (keys[m] < v) a = m + 1; else b = m;
+    }
+    return a;
+  };
+  const int lo = lower(t << 40), hi = lower((t + 1) << 40);
+  int cnt = 0;
+  double bl = 1e308;
+  int bp = INT_MAX;
+  for (int k = lo + threadIdx.x; k < hi; k += blockDim.x) {
+    if (!recs[k].valid) continue;
+    ++cnt;
+    if (recs[k].path_length < bl || (recs[k].path_length == bl && k < bp)) {
+      bl = recs[k].path_length;
+      bp = k;
+    }
+  }
+  cnt = __reduce_add_sync(FULL, cnt);
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ol = __shfl_down_sync(FULL, bl, off);
+    const int op = __shfl_down_sync(FULL, bp, off);
+    if (ol < bl || (ol == bl && op < bp)) {
+      bl = ol;
+      bp = op;
+    }
+  }
+  __shared__ int sc[32], sp[32];
+  __shared__ double sl[32];
+  if ((threadIdx.x & 31) == 0) {
+    sc[threadIdx.x >> 5] = cnt;
+    sl[threadIdx.x >> 5] = bl;
+    sp[threadIdx.x >> 5] = bp;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ScBest r{0, -1, -1, 0, 0.0};
+    double l = 1e308;
+    int p = INT_MAX;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      r.count += sc[w];
+      if (sl[w] < l || (sl[w] == l && sp[w] < p)) {
+        l = sl[w];
+        p = sp[w];
+      }
+    }
+    if (r.count > 0) {
+      r.seg1 = recs[p].seg1;
+      r.seg2 = recs[p].seg2;
+      r.path_length = recs[p].path_length;
+    }
+    out[t] = r;
+    has_sc[t] = r.count > 0 ? 1 : 0;
+  }
+}
+
+struct BatchPose {
+  int status, msg;
+  int i, j;  // chosen key (refinement clears the free segments' indices)
+  DevPose pose;
+};
+
+/// Materialise each target's chosen reach pose (k_materialize arithmetic)
+/// and refine it exactly (rp_refine.cuh).
+__global__ void k_bq_finish(BatchDev d, const uint8_t* has_shortcut, int refine_mode,
+                            BatchPose* out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= d.T) return;
+  BatchPose r{};
+  const BestRec b = d.best[t];
+  if (has_shortcut[t] || b.key == LLONG_MAX) {
+    r.status = -1;
+    out[t] = r;
+    return;
+  }
+  const SolveDev& a = d.a;
+  const ArmDev& arm = a.arm;
+  const int s = static_cast<int>(b.key / a.Q);
+  const int j = static_cast<int>(b.key - static_cast<long long>(s) * a.Q);
+  const int i = d.surv_idx[static_cast<size_t>(t) * a.Q + s];
+  const V3 p1 = arm.root + arm.L[0] * qvec(a, i);
+  const V3 p2 = p1 + arm.L[1] * qvec(a, j);
+  DevPose p{};
+  p.nseg = d.eight ? 4 : 3;
+  p.seg[0] = arm.L[0] * qvec(a, i);
+  p.seg[1] = arm.L[1] * qvec(a, j);
+  p.seg[2] = d.bpts[t] - p2;
+  p.qidx[0] = i;
+  p.qidx[1] = j;
+  p.qidx[2] = -1;
+  p.qidx[3] = -1;
+  if (d.eight) p.seg[3] = a.L4 * a.bdirs[0];
+  build_chain(arm, p);
+  r.i = i;
+  r.j = j;
+  r.status = refine_pose(arm, p, d.targets[t], refine_mode, &r.msg);
+  r.pose = p;
+  out[t] = r;
+}
+
+}  // namespace
+}  // namespace rp
+
+extern "C" rp_status rp_solve_reach_batch(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q,
+                                          const rp_grid* g, const double* targets,
+                                          int32_t n_targets, const rp_reach_params* rp,
+                                          rp_batch_result* out) {
+  return guarded([&] {
+    HostSpan span_("solve_reach_batch");
+    validate_arm(*arm);
+    validate_reach(*rp);
+    const bool eight = rp->mode == RP_MODE_8DOF;
+    const ArmDev ad = make_arm_dev(*arm);
+    const bool fast = !ad.any_limit && !ad.has_offsets && (!eight || rp->approach_half_angle == 0.0) &&
+                      !(rp->cone_precheck && eight);
+    auto finish = [&](int t, rp_solution_set* s) {
+      rp_batch_result& r = out[t];
+      std::memset(&r, 0, sizeof(r));
+      r.stats = s->stats;
+      r.n_solutions = s->n_solutions;
+      r.n_shortcuts = static_cast<int64_t>(s->shortcuts.size());
+      r.seg1 = r.seg2 = r.cone = -1;
+      if (r.n_solutions + r.n_shortcuts == 0) {
+        r.status = RP_E_NO_SOLUTION;
+        return;
+      }
+      // select_solution (src/reach_solver.cpp:548-577) from the set's
+      // shortcut records and its device argmin (no ordinal needed here)
+      if (!s->shortcuts.empty()) {
+        size_t bi = 0;
+        for (size_t k = 1; k < s->shortcuts.size(); ++k)
+          if (s->shortcuts[k].path_length < s->shortcuts[bi].path_length) bi = k;
+        r.kind = RP_CHOSEN_SHORTCUT;
+        r.path_length = s->shortcuts[bi].path_length;
+        r.seg1 = s->shortcuts[bi].seg1;
+        r.seg2 = s->shortcuts[bi].seg2;
+        return;
+      }
+      r.kind = RP_CHOSEN_REACH_POSE;
+      r.path_length = s->best_len;
+      const DevPose dp = solution_dev_pose_by_key(s, s->best_key);
+      r.seg1 = dp.qidx[0];
+      r.seg2 = dp.qidx[1];
+      r.cone = dp.nseg == 4 ? dp.qidx[3] : -1;
+      rp_pose approx;
+      to_abi(host_pose_from_dev(dp), &approx, nullptr, 0);
+      r.status = rp_exact_refine(ctx, arm, &approx, targets + 3 * t,
+                                 rp->refine_triangle_8dof ? 1 : 0, &r.refined);
+      if (r.status == RP_E_CUDA || r.status == RP_E_INTERNAL) fail(r.status, rp_last_error());
+    };
+    if (!fast) {  // general configurations: one full solve per query
+      for (int t = 0; t < n_targets; ++t) {
+        std::unique_ptr<rp_solution_set> s(
+            solve_reach(ctx, *arm, q, g, V3{targets[3 * t], targets[3 * t + 1], targets[3 * t + 2]}, *rp));
+        finish(t, s.get());
+      }
+      return;
+    }
+    cudaStream_t st = ctx->stream;
+    // ---- target-independent clearance
+    rp_solution_set proto;
+    proto.ctx = ctx;
+    proto.quiver = q;
+    proto.arm = *arm;
+    proto.rp = *rp;
+    SolveDev& a = proto.sd;
+    a.g = g->view();
+    a.arm = ad;
+    a.n = rp->n_samples;
+    a.eight = eight ? 1 : 0;
+    a.Q = q->n;
+    a.B = 1;
+    a.scanning = 1;
+    const double eps = resolved_epsilon(*arm, *rp);
+    const double L3 = arm->lengths[2];
+    const double L4 = eight ? arm->lengths[3] : 0.0;
+    a.eps = eps;
+    a.coarse2 = (L3 + eps) * (L3 + eps) * (1.0 + 1e-12);
+    a.band_lo2 = L3 - eps > 0.0 ? (L3 - eps) * (L3 - eps) * (1.0 - 1e-9) : 0.0;
+    double budget = arm->lengths[1] + arm->lengths[2] + eps;
+    if (eight) budget += arm->lengths[3];
+    budget += 1e-9;
+    a.budget2 = budget * budget;
+    a.near_r = resolved_near_radius(*arm, *rp);
+    a.spacing = nominal_spacing(*arm, *rp);
+    a.L4 = L4;
+    a.qx = q->d_soa;
+    a.qy = q->d_soa + q->n;
+    a.qz = q->d_soa + 2 * static_cast<size_t>(q->n);
+    const int W = (q->n + 31) / 32;
+    DevBuf<uint32_t> walk1(W, st), clear2(static_cast<size_t>(q->n) * W, st);
+    launch(ctx, "clear2", k_walk1, dim3(nblk(q->n, 256)), dim3(256), 0, a, walk1.p);
+    launch(ctx, "clear2", k_clear2, dim3(ctx->sm_count * 8), dim3(256), 0, a,
+           static_cast<const uint32_t*>(walk1.p), W, clear2.p);
+    // ---- all targets of a chunk go through each stage together
+    const V3 axis{rp->approach_axis[0], rp->approach_axis[1], rp->approach_axis[2]};
+    const V3 bdir = eight ? axis : V3{0, 0, 0};
+    proto.bdirs.alloc(1, st);
+    copy_to_device(ctx, proto.bdirs.p, &bdir, sizeof(V3));
+    a.bdirs = proto.bdirs.p;
+    const int CH = 256;
+    const int BPT = 64;
+    const int refine_mode = eight ? (rp->refine_triangle_8dof ? 1 : 0) : 2;
+    DevBuf<V3> d_t(CH, st), d_b(CH, st);
+    DevBuf<uint8_t> d_w4(CH, st), d_hs(CH, st);
+    DevBuf<uint32_t> d_sbits(static_cast<size_t>(CH) * W, st);
+    DevBuf<int> d_sidx(static_cast<size_t>(CH) * q->n, st), d_scnt(CH, st);
+    DevBuf<unsigned long long> d_ctr(static_cast<size_t>(CH) * C_COUNT, st);
+    DevBuf<unsigned> d_scc(1, st);
+    DevBuf<long long> d_scl(kBatchShortcutCap, st);
+    DevBuf<BestRec> d_bb(static_cast<size_t>(CH) * BPT, st), d_best(CH, st);
+    DevBuf<BatchPose> d_pose(CH, st);
+    DevBuf<ScBest> d_scb(CH, st);
+    std::vector<V3> ht, hb;
+    for (int c0 = 0; c0 < n_targets; c0 += CH) {
+      const int T = std::min(CH, n_targets - c0);
+      ht.resize(T);
+      hb.resize(T);
+      for (int k = 0; k < T; ++k) {
+        ht[k] = V3{targets[3 * (c0 + k)], targets[3 * (c0 + k) + 1], targets[3 * (c0 + k) + 2]};
+        hb[k] = eight ? ht[k] - L4 * axis : ht[k];  // backward_endpoints, half-angle 0
+      }
+      copy_to_device(ctx, d_t.p, ht.data(), T * sizeof(V3));
+      copy_to_device(ctx, d_b.p, hb.data(), T * sizeof(V3));
+      RP_CUDA(cudaMemsetAsync(d_ctr.p, 0, static_cast<size_t>(T) * C_COUNT * sizeof(unsigned long long), st));
+      d_scc.zero();
+      d_hs.zero();
+      BatchDev d{};
+      d.a = a;
+      d.T = T;
+      d.W = W;
+      d.BPT = BPT;
+      d.eight = eight ? 1 : 0;
+      d.targets = d_t.p;
+      d.bpts = d_b.p;
+      d.walk4_ok = d_w4.p;
+      d.walk1 = walk1.p;
+      d.clear2 = clear2.p;
+      d.surv_bits = d_sbits.p;
+      d.surv_idx = d_sidx.p;
+      d.surv_cnt = d_scnt.p;
+      d.ctr = d_ctr.p;
+      d.sc_list = d_scl.p;
+      d.sc_count = d_scc.p;
+      d.bb = d_bb.p;
+      d.best = d_best.p;
+      launch(ctx, "walk4", k_bq_walk4, dim3(nblk(T, 128)), dim3(128), 0, d, d_w4.p);
+      launch(ctx, "seg1", k_bq_seg1, dim3(nblk(q->n, 256), T), dim3(256), 0, d);
+      launch(ctx, "compact", k_bq_compact, dim3(T), dim3(1024), 0, d);
+      if (eight)
+        launch(ctx, "seg2", k_bq_seg2<true>, dim3(BPT, T), dim3(256), 0, d);
+      else
+        launch(ctx, "seg2", k_bq_seg2<false>, dim3(BPT, T), dim3(256), 0, d);
+      launch(ctx, "select", k_bq_best, dim3(T), dim3(64), 0, d);
+      unsigned nsc = 0;
+      copy_to_host(ctx, &nsc, d_scc.p, sizeof(unsigned));
+      require(nsc <= kBatchShortcutCap, RP_E_CAPACITY_EXCEEDED,
+              "too many near-encounter hypotheses");
+      // shortcuts: sorted keys = (target, segment, canonical index), scanned
+      // and reduced per target on the device
+      RP_CUDA(cudaMemsetAsync(d_scb.p, 0, T * sizeof(ScBest), st));
+      if (nsc > 0) {
+        DevBuf<long long> sorted(nsc, st);
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortKeys(nullptr, tb, d_scl.p, sorted.p, static_cast<int>(nsc), 0,
+                                       64, st);
+        DevBuf<unsigned char> tmp(tb, st);
+        RP_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, d_scl.p, sorted.p,
+                                               static_cast<int>(nsc), 0, 64, st));
+        DevBuf<ShortcutRec> recs(nsc, st);
+        launch(ctx, "shortcuts", k_bq_shortcuts, dim3(nblk(nsc, 128)), dim3(128), 0, d,
+               static_cast<const long long*>(sorted.p), static_cast<int>(nsc), recs.p);
+        launch(ctx, "shortcuts", k_bq_sc_reduce, dim3(T), dim3(128), 0,
+               static_cast<const long long*>(sorted.p), static_cast<const ShortcutRec*>(recs.p),
+               static_cast<int>(nsc), d_scb.p, d_hs.p);
+      }
+      std::vector<ScBest> hscb(T);
+      copy_to_host(ctx, hscb.data(), d_scb.p, T * sizeof(ScBest));
+      launch(ctx, "finish", k_bq_finish, dim3(nblk(T, 64)), dim3(64), 0, d,
+             static_cast<const uint8_t*>(d_hs.p), refine_mode, d_pose.p);
+      std::vector<unsigned long long> hc(static_cast<size_t>(T) * C_COUNT);
+      std::vector<int> hcnt(T);
+      std::vector<BestRec> hbest(T);
+      std::vector<BatchPose> hpose(T);
+      copy_to_host(ctx, hc.data(), d_ctr.p, hc.size() * sizeof(unsigned long long));
+      copy_to_host(ctx, hcnt.data(), d_scnt.p, T * sizeof(int));
+      copy_to_host(ctx, hbest.data(), d_best.p, T * sizeof(BestRec));
+      copy_to_host(ctx, hpose.data(), d_pose.p, T * sizeof(BatchPose));
+      for (int k = 0; k < T; ++k) {
+        rp_batch_result& r = out[c0 + k];
+        std::memset(&r, 0, sizeof(r));
+        const unsigned long long* c = hc.data() + static_cast<size_t>(k) * C_COUNT;
+        const int64_t pairs = static_cast<int64_t>(hcnt[k]) * q->n;
+        rp_solve_stats& S = r.stats;
+        S.seg1_candidates = q->n;
+        S.seg1_limit_pass = c[C_SEG1_LIMIT];
+        S.seg1_reach_pass = c[C_SEG1_REACH];
+        S.seg1_survivors = c[C_SEG1_SURV];
+        S.pair_candidates = pairs;
+        S.seg2_limit_pass = pairs;
+        S.seg2_clear_pass = c[C_SEG2_CLEAR];
+        S.gap_tested = c[C_SEG2_CLEAR];
+        S.gap_pass = c[C_GAP_PASS];
+        S.joint_pass = c[C_JOINT_PASS];
+        S.v3_clear_pass = c[C_V3_CLEAR];
+        S.solutions = c[C_SOLUTIONS];
+        S.shortcuts_found = hscb[k].count;
+        r.n_solutions = S.solutions;
+        r.n_shortcuts = S.shortcuts_found;
+        r.seg1 = r.seg2 = r.cone = -1;
+        if (hscb[k].count > 0) {  // select_solution: shortest shortcut, first on ties
+          r.kind = RP_CHOSEN_SHORTCUT;
+          r.path_length = hscb[k].path_length;
+          r.seg1 = hscb[k].seg1;
+          r.seg2 = hscb[k].seg2;
+          continue;
+        }
+        if (r.n_solutions == 0) {
+          r.status = RP_E_NO_SOLUTION;
+          continue;
+        }
+        r.kind = RP_CHOSEN_REACH_POSE;
+        r.path_length = hbest[k].len;
+        r.seg1 = hpose[k].i;
+        r.seg2 = hpose[k].j;
+        r.status = hpose[k].status;
+        if (r.status == 0) {
+          HostPose hp = host_pose_from_dev(hpose[k].pose);
+          hp.waypoints.clear();
+          to_abi(hp, &r.refined, nullptr, 0);
+        }
+      }
+    }
+  });
+}

@@ -33,6 +33,7 @@ struct SolveDev {
   int disable_prune;
   int n_targets;
   double eps, coarse2, budget2, near_r, spacing, L4;
+  double band_lo2;  // conservative lower bound of |v3|^2 for the gap band (prefilters)
   V3 target;
   const double* qx;
   const double* qy;
