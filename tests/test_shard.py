@@ -1,0 +1,91 @@
+"""Host logic of the multi-GPU batched-query sharding:
+contiguous blocks, record packing and the rank-order gather, run with two
+gloo ranks on CPU (world_size 2)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_1906_10678_b200 import abi, shard
+
+
+@pytest.mark.parametrize("n", [0, 1, 7, 64, 4096, 4099])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_shard_range_partitions(n, world):
+    prev = 0
+    sizes = []
+    for r in range(world):
+        lo, hi = shard.shard_range(n, r, world)
+        assert lo == prev and hi >= lo
+        sizes.append(hi - lo)
+        prev = hi
+    assert prev == n
+    assert max(sizes) - min(sizes) <= 1
+    assert sizes[0] == max(sizes)  # gather pads to rank 0's block
+
+
+def test_shard_range_rejects_bad_rank():
+    with pytest.raises(ValueError):
+        shard.shard_range(10, 2, 2)
+
+
+def _record(k: int) -> abi.BatchResult:
+    r = abi.BatchResult()
+    r.status = k % 3
+    r.kind = 1 + k % 2
+    r.seg1, r.seg2, r.cone = k, 10 * k + 1, -1
+    r.n_solutions = 1_000_003 * k
+    r.n_shortcuts = k // 5
+    r.path_length = 1.0 / (k + 3)
+    r.refined.n_segments = 4
+    r.refined.segments[1][2] = k * 0.125
+    r.stats.seg2_clear_pass = 7 * k
+    return r
+
+
+def test_pack_unpack_roundtrip():
+    recs = [_record(k) for k in range(5)]
+    raw = shard.pack(recs)
+    assert raw.shape == (5, shard.RECORD_BYTES)
+    back = shard.unpack(raw)
+    for a, b in zip(recs, back):
+        assert bytes(a) == bytes(b)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, n, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lo, hi = shard.shard_range(n, rank, world)
+        local = shard.pack([_record(k) for k in range(lo, hi)])
+        full = shard.gather_records(local, n, rank, world)
+        q.put((rank, full.tobytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [0, 5, 33])
+def test_gather_two_gloo_ranks(n):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = shard.pack([_record(k) for k in range(n)]).tobytes()
+    for r in range(world):
+        assert got[r] == want, f"rank {r} gathered a different record list"
