@@ -160,7 +160,7 @@ __host__ __device__ inline DevPose from_angles(const ArmDev& arm, const double* 
 __device__ inline V3 wq(const WikDev& w, int i) { return V3{w.qx[i], w.qy[i], w.qz[i]}; }
 
 /// One (i, j) candidate through every test of waypoint_ik, in order.
-__device__ bool wik_eval(const WikDev& w, const CiData& c, int j, DevPose* out, double* metric_out,
+__device__ __noinline__ bool wik_eval(const WikDev& w, const CiData& c, int j, DevPose* out, double* metric_out,
                          int* opt_out) {
   const ArmDev& arm = w.arm;
   const V3 qj = wq(w, j);
@@ -256,6 +256,14 @@ __device__ bool wik_eval(const WikDev& w, const CiData& c, int j, DevPose* out, 
 __device__ bool wik_eval_fast(const WikDev& w, const CiData& c, int j, double* metric_out,
                               int* opt_out) {
   const ArmDev& arm = w.arm;
+  long long tp = w.prof ? clock64() : 0;
+  const auto mark = [&](int slot) {
+    if (w.prof) {
+      const long long t = clock64();
+      atomicMax(reinterpret_cast<unsigned long long*>(w.prof + slot), t - tp);
+      tp = t;
+    }
+  };
   const V3 qj = wq(w, j);
   const V3 p2 = c.p1 + arm.L[1] * qj;
   const double move2 = rpd::norm(p2 - w.prev_j2);
@@ -267,10 +275,13 @@ __device__ bool wik_eval_fast(const WikDev& w, const CiData& c, int j, double* m
   double metric = c.move1 + move2;
   if (w.has_bias) metric += rpd::norm(c.p1 - w.bias_j1) + rpd::norm(p2 - w.bias_j2);
   if (!c.ok) return false;
+  mark(10);
   if (!rpd::walk_clear(w.g, c.p1, p2, w.n)) return false;  // link2 = p1 (coaxial)
+  mark(11);
   const V3 s3 = v3_hat * arm.L[2];
   const V3 p3 = p2 + s3;
   if (!rpd::walk_clear(w.g, p2, p3, w.n)) return false;
+  mark(12);
   V3 J[5];
   J[0] = arm.root;
   J[1] = J[0] + arm.L[0] * wq(w, c.i);
@@ -288,6 +299,7 @@ __device__ bool wik_eval_fast(const WikDev& w, const CiData& c, int j, double* m
       opt = o;
       done = true;
     }
+    mark(13);
     if (!done) return false;
   } else if (!rpd::self_collision_free(J, 3, min_sep)) {
     return false;
@@ -306,7 +318,7 @@ __device__ __forceinline__ bool wik_test(const WikDev& w, const CiData& c, int j
 
 /// The pose wik_eval accepted for (i, j, trail option): the same arithmetic,
 /// without re-running its tests.
-__device__ DevPose wik_pose(const WikDev& w, const CiData& c, int j, int opt) {
+__device__ __noinline__ DevPose wik_pose(const WikDev& w, const CiData& c, int j, int opt) {
   const ArmDev& arm = w.arm;
   const V3 qj = wq(w, j);
   V3 link2 = c.p1;
@@ -664,6 +676,7 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
       w.cond2 = A.cond2;
       w.cond3 = A.cond3;
       w.filter_j = A.filter_j;
+      w.prof = blockIdx.x == 0 ? A.prof : nullptr;
       w.n_opts = 0;
       if (k > 0) {
         const V3 d = wprev - wk;
@@ -737,15 +750,24 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
         long long bo = LLONG_MAX;
         int bopt = -1;
         const long long total = static_cast<long long>(nci) * ncj;
-        for (long long tt = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-             tt < total; tt += static_cast<long long>(nb) * blockDim.x) {
+        // pairs dealt round-robin over the blocks (pair tt -> block tt % nb),
+        // so a few thousand pairs spread over every SM of the grid
+        for (long long tt = static_cast<long long>(threadIdx.x) * nb + blockIdx.x; tt < total;
+             tt += static_cast<long long>(nb) * blockDim.x) {
           const int a = static_cast<int>(tt / ncj);
+          const long long q0 = A.prof ? clock64() : 0;
           if (!__ldcg(&A.ci_by_index[li[a]].ok)) continue;
           const CiData c = ldcg_struct(A.ci_by_index + li[a]);
+          const long long q1 = A.prof ? clock64() : 0;
           double mm;
           int opt;
-          if (wik_test(w, c, lj[tt - static_cast<long long>(a) * ncj], &mm, &opt) &&
-              wik_better(mm, tt, bm, bo)) {
+          const bool hit = wik_test(w, c, lj[tt - static_cast<long long>(a) * ncj], &mm, &opt);
+          if (A.prof && blockIdx.x == 0) {
+            const long long q2 = clock64();
+            atomicMax(reinterpret_cast<unsigned long long*>(A.prof + 8), q1 - q0);
+            atomicMax(reinterpret_cast<unsigned long long*>(A.prof + 9), q2 - q1);
+          }
+          if (hit && wik_better(mm, tt, bm, bo)) {
             bm = mm;
             bo = tt;
             bopt = opt;
@@ -944,6 +966,103 @@ __global__ void k_score_solutions(SolveDev a, const SurvDev* __restrict__ sv,
     const V3 diff = to[l] - from[l];
     for (int k = 1; k <= a.n; ++k) {
       acc += polyline_dist(rpd::walk_sample(from[l], diff, k, a.n), spoly, npoly);
+      ++cnt;
+    }
+  }
+  const double dev = acc / static_cast<double>(cnt);
+  dev_bits[t] = __double_as_longlong(dev);
+  ordinal[t] = ord_base + t;
+}
+
+/// The failed path as a per-launch table in the kernel-parameter constant
+/// bank: segment start a, direction ab = b - a, end a + 1*ab and |ab|^2,
+/// all computed on the host with the same fp64 operations the reference
+/// performs inside point_to_segment.
+constexpr int kPolyMax = 32;  // segments (waypoints <= 33)
+struct PolyTable {
+  int nseg;
+  double p0x, p0y, p0z;
+  double ax[kPolyMax], ay[kPolyMax], az[kPolyMax];
+  double bx[kPolyMax], by[kPolyMax], bz[kPolyMax];
+  double ex[kPolyMax], ey[kPolyMax], ez[kPolyMax];
+  double len2[kPolyMax];
+};
+
+/// polyline_dist with identical results: sqrt is monotone and correctly
+/// rounded, so min_i sqrt(d_i^2) == sqrt(min_i d_i^2); the clamp of
+/// t = dot/len2 is decided from the signs of dot and len2 - dot (dot <= 0
+/// gives t in {-0, 0}, dot >= len2 gives t = 1), so the IEEE division runs
+/// only for interior projections, where it is computed exactly as written.
+__device__ __forceinline__ double polyline_dist_tab(V3 p, const PolyTable& T) {
+  double best;
+  {
+    const double dx = p.x - T.p0x, dy = p.y - T.p0y, dz = p.z - T.p0z;
+    best = (dx * dx + dy * dy) + dz * dz;
+  }
+#pragma unroll
+  for (int i = 0; i < kPolyMax; ++i) {
+    if (i < T.nseg) {
+      const double wx = p.x - T.ax[i], wy = p.y - T.ay[i], wz = p.z - T.az[i];
+      double sq;
+      const double len2 = T.len2[i];
+      if (len2 <= 1e-30) {
+        sq = (wx * wx + wy * wy) + wz * wz;
+      } else {
+        const double dot = (wx * T.bx[i] + wy * T.by[i]) + wz * T.bz[i];
+        if (dot <= 0.0) {
+          sq = (wx * wx + wy * wy) + wz * wz;
+        } else if (dot >= len2) {
+          const double dx = p.x - T.ex[i], dy = p.y - T.ey[i], dz = p.z - T.ez[i];
+          sq = (dx * dx + dy * dy) + dz * dz;
+        } else {
+          const double t = rpd::clampd(dot / len2, 0.0, 1.0);
+          const double dx = p.x - (T.ax[i] + t * T.bx[i]);
+          const double dy = p.y - (T.ay[i] + t * T.by[i]);
+          const double dz = p.z - (T.az[i] + t * T.bz[i]);
+          sq = (dx * dx + dy * dy) + dz * dz;
+        }
+      }
+      best = sq < best ? sq : best;
+    }
+  }
+  return sqrt(best);
+}
+
+/// k_score_solutions with the polyline in the parameter bank (npoly - 1 <=
+/// kPolyMax); bit-identical deviations.
+__global__ void __launch_bounds__(256) k_score_solutions_tab(
+    SolveDev a, const SurvDev* __restrict__ sv, const long long* __restrict__ keys, int64_t count,
+    const __grid_constant__ PolyTable T, int has_lead, V3 lead,
+    unsigned long long* __restrict__ dev_bits, long long* __restrict__ ordinal, long long ord_base) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  const long long key = keys[t];
+  const long long p = key / a.B;
+  const int bi = static_cast<int>(key - p * a.B);
+  const int s = static_cast<int>(p / a.Q);
+  const int j = static_cast<int>(p - static_cast<long long>(s) * a.Q);
+  const SurvDev& h = sv[s];
+  const ArmDev& arm = a.arm;
+  const V3 dir2 = qvec(a, j);
+  V3 link2 = h.p1;
+  if (arm.off[1] > 0.0) {
+    const rpd::FrameStep st2 = rpd::advance_frame(h.frame, dir2);
+    link2 = h.p1 + arm.off[1] * rpd::m_col(st2.after_azimuth, 0);
+  }
+  const V3 p2 = link2 + arm.L[1] * dir2;
+  const V3 from[3] = {h.link_start, link2, p2};
+  const V3 to[3] = {h.p1, p2, a.bpts[bi]};
+  double acc = 0.0;
+  int cnt = 0;
+  if (has_lead) {
+    acc += polyline_dist_tab(lead, T);
+    ++cnt;
+  }
+#pragma unroll
+  for (int l = 0; l < 3; ++l) {
+    const V3 diff = to[l] - from[l];
+    for (int k = 1; k <= a.n; ++k) {
+      acc += polyline_dist_tab(rpd::walk_sample(from[l], diff, k, a.n), T);
       ++cnt;
     }
   }
@@ -1230,7 +1349,7 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
   static const bool profile = std::getenv("RP_PROFILE_PASS") != nullptr;
   DevBuf<long long> prof;
   if (profile) {
-    prof.alloc(8, st);
+    prof.alloc(16, st);
     prof.zero();
     A.prof = prof.p;
   }
@@ -1243,12 +1362,14 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
   int hs[4];
   copy_to_host(ctx, hs, bp_state.p, sizeof(hs));
   if (profile) {
-    long long hp[8];
+    long long hp[16];
     copy_to_host(ctx, hp, prof.p, sizeof(hp));
+    std::fprintf(stderr, "[eval] max cycles: pre %lld walk2 %lld walk3 %lld trail %lld\n", hp[10],
+                 hp[11], hp[12], hp[13]);
     std::fprintf(stderr,
                  "[pass] m=%d attempts=%lld pairs=%lld cyc: filter %lld compact %lld pairs %lld "
-                 "wait %lld publish %lld barrier %lld\n",
-                 m, hp[6], hp[7], hp[0], hp[1], hp[2], hp[3], hp[4], hp[5]);
+                 "wait %lld publish %lld barrier %lld | max ci-load %lld max eval %lld\n",
+                 m, hp[6], hp[7], hp[0], hp[1], hp[2], hp[3], hp[4], hp[5], hp[8], hp[9]);
   }
   out->ok = hs[2] != 0;
   out->failed_index = hs[1];
@@ -1460,6 +1581,25 @@ std::vector<long long> Planner::rank_by_deviation(rp_solution_set* set,
   }
   if (nsol > 0) {
     ensure_keys(set);
+    static const bool no_tab = std::getenv("RP_SCORE_PLAIN") != nullptr;
+    if (poly.size() >= 2 && poly.size() - 1 <= static_cast<size_t>(kPolyMax) && !no_tab) {
+      PolyTable T{};
+      T.nseg = static_cast<int>(poly.size()) - 1;
+      T.p0x = poly[0].x;
+      T.p0y = poly[0].y;
+      T.p0z = poly[0].z;
+      for (int i = 0; i < T.nseg; ++i) {
+        const V3 a = poly[i], ab = poly[i + 1] - poly[i];
+        const V3 e = a + 1.0 * ab;
+        T.ax[i] = a.x; T.ay[i] = a.y; T.az[i] = a.z;
+        T.bx[i] = ab.x; T.by[i] = ab.y; T.bz[i] = ab.z;
+        T.ex[i] = e.x; T.ey[i] = e.y; T.ez[i] = e.z;
+        T.len2[i] = rpd::sqnorm(ab);
+      }
+      launch(ctx, "score", k_score_solutions_tab, dim3(nblk(nsol, 256)), dim3(256), 0, set->sd,
+             static_cast<const SurvDev*>(set->surv.p), static_cast<const long long*>(set->keys.p),
+             nsol, T, lead ? 1 : 0, lead_pt, dev.p + ns, ord.p + ns, static_cast<long long>(ns));
+    } else
     launch(ctx, "score", k_score_solutions, dim3(nblk(nsol, 256)), dim3(256),
            poly.size() * sizeof(V3), set->sd, static_cast<const SurvDev*>(set->surv.p),
            static_cast<const long long*>(set->keys.p), nsol, static_cast<const V3*>(dpoly.p),

@@ -36,6 +36,7 @@ struct WikDev {
   int filter_j;  // conservative cone filter for segment 2 (coaxial arms)
   int cond2, cond3;
   double jbound;
+  long long* prof;  // RP_PROFILE_PASS section maxima (null otherwise)
 };
 
 struct CiData {
