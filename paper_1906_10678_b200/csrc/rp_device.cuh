@@ -182,13 +182,19 @@ __device__ __forceinline__ uint32_t walk_hits(const GridView& g, V3 from, V3 to,
 
 /// walk_first_blocked with the gathers in flight together (n <= 16), the
 /// sequential walk otherwise or when a floor is ambiguous. Identical result.
-static __device__ __noinline__ int walk_first_blocked_par(const GridView& g, V3 from, V3 to, int n) {
+__device__ __forceinline__ int walk_first_blocked_fast(const GridView& g, V3 from, V3 to, int n) {
   bool exact = false;
   uint32_t m = 0;
   if (n == 8) m = walk_hits<8>(g, from, to, 8, &exact);
   else if (n <= kTkMax) m = walk_hits<kTkMax>(g, from, to, n, &exact);
   if (!exact) return walk_first_blocked(g, from, to, n);
   return m ? __ffs(m) : 0;
+}
+
+/// Out-of-line copy for the large planner kernels (one body instead of one
+/// per call site keeps their instruction footprint down).
+static __device__ __noinline__ int walk_first_blocked_par(const GridView& g, V3 from, V3 to, int n) {
+  return walk_first_blocked_fast(g, from, to, n);
 }
 
 /// All n samples clear (segment_clear verdict; walk_points).

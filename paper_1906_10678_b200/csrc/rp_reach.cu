@@ -325,8 +325,16 @@ __global__ void __launch_bounds__(256) k_seg2(SolveDev a, const SurvDev* __restr
 /// and the self-collision check 32 at a time without divergence. Counters,
 /// solution bits (atomicOr into a zeroed set) and the block argmin are the
 /// same as k_seg2's.
+#ifndef RP_SEG2_PAR_WALK
+#define RP_SEG2_PAR_WALK 1
+#endif
+constexpr bool kSeg2ParWalk = RP_SEG2_PAR_WALK;
+#ifndef RP_BQ_MINB
+#define RP_BQ_MINB 4
+#endif
+
 template <bool EIGHT>
-__global__ void __launch_bounds__(256) k_seg2_rows(SolveDev a, const SurvDev* __restrict__ sv, int S1,
+__global__ void __launch_bounds__(256, 2) k_seg2_rows(SolveDev a, const SurvDev* __restrict__ sv, int S1,
                                                    uint32_t* __restrict__ sol_bits,
                                                    unsigned long long* ctr, long long* sc_list,
                                                    unsigned* sc_count, BestRec* __restrict__ block_best) {
@@ -395,7 +403,8 @@ __global__ void __launch_bounds__(256) k_seg2_rows(SolveDev a, const SurvDev* __
         ++c_lim;
         const V3 dir2 = qvec(a, j);
         const V3 p2 = p1 + L2 * dir2;
-        const int fb = rpd::walk_first_blocked(a.g, p1, p2, a.n);
+        const int fb = kSeg2ParWalk ? rpd::walk_first_blocked_fast(a.g, p1, p2, a.n)
+                                    : rpd::walk_first_blocked(a.g, p1, p2, a.n);
         if (row_near && rpd::may_pass_near(a.target, p1, dir2, L2, rnear) &&
             rpd::point_to_segment(a.target, p1, p2) <= a.near_r + 1e-9) {
           const unsigned pos = atomicAdd(sc_count, 1u);
@@ -1262,7 +1271,7 @@ __global__ void __launch_bounds__(256) k_clear2(SolveDev a, const uint32_t* __re
     if (j < a.Q && ((walk1_bits[i >> 5] >> (i & 31)) & 1u)) {
       const V3 p1 = a.arm.root + a.arm.L[0] * qvec(a, i);
       const V3 p2 = p1 + a.arm.L[1] * qvec(a, j);
-      clear = rpd::walk_first_blocked(a.g, p1, p2, a.n) == 0;
+      clear = (kSeg2ParWalk ? rpd::walk_first_blocked_fast(a.g, p1, p2, a.n) : rpd::walk_first_blocked(a.g, p1, p2, a.n)) == 0;
     }
     const unsigned m = __ballot_sync(FULL, clear);
     if (lane == 0) clear2[wd] = m;
@@ -1370,7 +1379,7 @@ __global__ void __launch_bounds__(1024) k_bq_compact(BatchDev d) {
 /// k_seg2_cached for every target of the chunk: blockIdx.y = target,
 /// blockIdx.x strides over that target's (survivor, j) pairs.
 template <bool EIGHT>
-__global__ void __launch_bounds__(256) k_bq_seg2(BatchDev d) {
+__global__ void __launch_bounds__(256, RP_BQ_MINB) k_bq_seg2(BatchDev d) {
   const int t = blockIdx.y;
   const SolveDev& a = d.a;
   const ArmDev& arm = a.arm;
