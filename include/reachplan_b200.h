@@ -198,6 +198,11 @@ void rp_path_params_init(rp_path_params* pp);
 double rp_nominal_spacing(const rp_arm* arm, const rp_reach_params* rp);
 double rp_resolved_epsilon(const rp_arm* arm, const rp_reach_params* rp);
 double rp_resolved_near_radius(const rp_arm* arm, const rp_reach_params* rp);
+/* [ReachParams::validate, src/reach_solver.cpp:45-52] */
+rp_status rp_reach_params_validate(const rp_reach_params* rp);
+/* [PathParams::resolved, src/path_planner.cpp:89-102] derived fields filled in */
+rp_status rp_path_params_resolve(const rp_arm* arm, const rp_reach_params* rp,
+                                 const rp_path_params* pp, rp_path_params* out);
 /* [effective_dilation, src/pipeline.cpp:8-15]; configured < 0 = derive */
 double rp_effective_dilation(const rp_arm* arm, const rp_reach_params* rp, double configured);
 
@@ -212,6 +217,11 @@ rp_status rp_quiver_download(const rp_quiver* q, double* xyz, int32_t cap);
 /* [cone_subset, src/quiver.cpp:53-63] indices ascending; *n_out = count */
 rp_status rp_cone_subset(rp_ctx* ctx, const rp_quiver* q, const double axis[3],
                          double half_angle, int32_t* idx, int32_t cap, int32_t* n_out);
+/* Ring addressing of a generated quiver (Quiver::ring_offsets, ring_elevations,
+ * elev_step, equator_azim_step, min_per_ring); *n_rings = 0 for uploads. */
+rp_status rp_quiver_rings(const rp_quiver* q, int32_t* ring_offsets, double* ring_elevations,
+                          int32_t cap, int32_t* n_rings, double* elev_step,
+                          double* equator_azim_step, int32_t* min_per_ring);
 rp_status rp_quiver_destroy(rp_quiver* q);
 
 /* ---- voxel grid [inc/reachplan/voxgrid.hpp:60-84] ----------------------------- */
@@ -263,6 +273,16 @@ rp_status rp_prune_segment1(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q, 
                             const double* target_points, int32_t n_targets,
                             const rp_reach_params* rp, int32_t* survivors, int32_t cap,
                             int32_t* n_out, rp_solve_stats* stats);
+/* [backward_endpoints, src/reach_solver.cpp:54-83] p3 candidates, end-effector
+ * directions and cone quiver indices (-1 = exact axis); *n_out = count */
+rp_status rp_backward_endpoints(rp_ctx* ctx, const rp_quiver* q, const double target[3], double L4,
+                                const rp_reach_params* rp, double* points, double* dirs,
+                                int32_t* cone_idx, int32_t cap, int32_t* n_out);
+/* [span_gap, src/reach_solver.cpp:85-98] gap vectors p2 -> backward point k
+ * passing the coarse + band test, k ascending (v3_out / idx_out hold n slots) */
+rp_status rp_span_gap(rp_ctx* ctx, const double p2[3], const double* backward_pts, int32_t n,
+                      double L3, double epsilon, double* v3_out, int32_t* idx_out,
+                      int32_t* n_out);
 /* [solve_reach, src/reach_solver.cpp:480-546]; the set stays on the device */
 rp_status rp_solve_reach(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q, const rp_grid* g,
                          const double target[3], const rp_reach_params* rp,
@@ -275,9 +295,15 @@ rp_status rp_solution_set_keys(const rp_solution_set* s, int32_t* keys, int64_t 
 /* Materialise solution k (PoseChain incl. waypoints, reach_solver.cpp:434-449). */
 rp_status rp_solution_set_pose(const rp_solution_set* s, int64_t k, rp_pose* pose,
                                double* waypoints, int32_t cap_waypoints);
+/* Bulk form: solutions [first, first + count) in canonical order; waypoints
+ * (nullable) holds wps_per_pose xyz triples per pose. */
+rp_status rp_solution_set_poses(const rp_solution_set* s, int64_t first, int64_t count,
+                                rp_pose* poses, double* waypoints, int32_t wps_per_pose);
 /* Shortcut k; tip waypoints (root excluded) into wps (ShortcutPath::tip_waypoints). */
 rp_status rp_solution_set_shortcut(const rp_solution_set* s, int64_t k, rp_shortcut* sc,
                                    double* tip_wps, int32_t cap_wps, int32_t* n_wps);
+/* ShortcutPath::basis_pose of shortcut k (the hypothesis segments behind it). */
+rp_status rp_solution_set_shortcut_basis(const rp_solution_set* s, int64_t k, rp_pose* basis);
 rp_status rp_solution_set_destroy(rp_solution_set* s);
 /* [select_solution, src/reach_solver.cpp:548-577] */
 rp_status rp_select_solution(const rp_solution_set* s, rp_chosen* out);
@@ -316,6 +342,14 @@ rp_status rp_plan_from_reach(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q,
                              const rp_solution_set* set, const rp_chosen* chosen,
                              const double target[3], const rp_reach_params* rp,
                              const rp_path_params* pp, rp_plan** out);
+/* [fallback_cascade, src/path_planner.cpp:740-822] after a failed backward
+ * pass of `failed` over `waypoints` (PlanFailure: blocked_index = the
+ * waypoint the pass could not place) */
+rp_status rp_fallback_cascade(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q, const rp_grid* g,
+                              const rp_solution_set* set, const rp_chosen* failed,
+                              const double* waypoints, int32_t n_waypoints, int32_t blocked_index,
+                              const double target[3], const rp_reach_params* rp,
+                              const rp_path_params* pp, rp_plan** out);
 /* [plan_arbitrary, src/path_planner.cpp:906-998]; start_waypoints (nullable)
  * carries start_pose->n_waypoints xyz samples (PoseChain::waypoints) */
 rp_status rp_plan_arbitrary(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q, const rp_grid* g,

@@ -173,6 +173,10 @@ void validate_reach(const rp_reach_params& r) {
   require(r.workers >= 1, RP_E_INVALID_PARAMETER, "workers must be >= 1");
 }
 
+extern "C" rp_status rp_reach_params_validate(const rp_reach_params* rp) {
+  return guarded([&] { validate_reach(*rp); });
+}
+
 ArmDev make_arm_dev(const rp_arm& a) {
   ArmDev d{};
   d.nseg = a.n_segments;
@@ -424,9 +428,11 @@ rp_status rp_quiver_generate(rp_ctx* ctx, double elev_step, double azim_step,
     }
     const long n_eq = std::llround(2.0 * kPi / azim_step);
     std::vector<double> xyz;
+    std::vector<int> offsets;
     for (double phi : rings) {
       const long by_circ = std::llround(static_cast<double>(n_eq) * std::cos(phi));
       const int count = static_cast<int>(std::max<long>(min_per_ring, by_circ));
+      offsets.push_back(static_cast<int>(xyz.size() / 3));
       const double cp = std::cos(phi), sp = std::sin(phi);
       for (int m = 0; m < count; ++m) {
         const double theta = 2.0 * kPi * m / count;
@@ -435,7 +441,30 @@ rp_status rp_quiver_generate(rp_ctx* ctx, double elev_step, double azim_step,
         xyz.push_back(sp);
       }
     }
-    *out = upload_quiver(ctx, xyz);
+    rp_quiver* q = upload_quiver(ctx, xyz);
+    q->ring_offsets = std::move(offsets);
+    q->ring_elevations = std::move(rings);
+    q->elev_step = elev_step;
+    q->equator_azim_step = azim_step;
+    q->min_per_ring = min_per_ring;
+    *out = q;
+  });
+}
+
+rp_status rp_quiver_rings(const rp_quiver* q, int32_t* ring_offsets, double* ring_elevations,
+                          int32_t cap, int32_t* n_rings, double* elev_step,
+                          double* equator_azim_step, int32_t* min_per_ring) {
+  return guarded([&] {
+    const int n = static_cast<int>(q->ring_offsets.size());
+    require(cap >= n || !ring_offsets, RP_E_CAPACITY_EXCEEDED, "ring buffer too small");
+    *n_rings = n;
+    for (int k = 0; ring_offsets && k < n; ++k) {
+      ring_offsets[k] = q->ring_offsets[k];
+      if (ring_elevations) ring_elevations[k] = q->ring_elevations[k];
+    }
+    if (elev_step) *elev_step = q->elev_step;
+    if (equator_azim_step) *equator_azim_step = q->equator_azim_step;
+    if (min_per_ring) *min_per_ring = q->min_per_ring;
   });
 }
 

@@ -78,6 +78,12 @@ struct rp_quiver {
   int n = 0;
   std::vector<double> host_xyz;  // AoS, reference order
   double* d_soa = nullptr;       // x[n], y[n], z[n]
+  // ring addressing (Quiver fields, inc/reachplan/quiver.hpp:16-24); empty
+  // for uploaded quivers
+  std::vector<int> ring_offsets;
+  std::vector<double> ring_elevations;
+  double elev_step = 0.0, equator_azim_step = 0.0;
+  int min_per_ring = 0;
 };
 
 struct rp_grid {

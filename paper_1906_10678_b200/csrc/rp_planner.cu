@@ -806,6 +806,25 @@ rp_status rp_plan_from_reach(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q,
   });
 }
 
+rp_status rp_fallback_cascade(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q, const rp_grid* g,
+                              const rp_solution_set* set, const rp_chosen* failed,
+                              const double* waypoints, int32_t n_waypoints, int32_t blocked_index,
+                              const double target[3], const rp_reach_params* rp,
+                              const rp_path_params* pp, rp_plan** out) {
+  return guarded([&] {
+    require(n_waypoints >= 0 && (n_waypoints == 0 || waypoints), RP_E_INVALID_PARAMETER,
+            "waypoints missing");
+    Planner P(ctx, *arm, q, g, *rp, *pp);
+    auto* s = const_cast<rp_solution_set*>(set);
+    Failure f;
+    f.candidate = chosen_cand(s, *failed);
+    for (int k = 0; k < n_waypoints; ++k)
+      f.waypoints.push_back(V3{waypoints[3 * k], waypoints[3 * k + 1], waypoints[3 * k + 2]});
+    f.blocked_index = blocked_index;
+    *out = fallback_cascade(P, f, s, V3{target[0], target[1], target[2]});
+  });
+}
+
 rp_status rp_plan_arbitrary(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q, const rp_grid* g,
                             const rp_pose* start, const double* start_wps, const double target[3],
                             const rp_reach_params* rp, const rp_path_params* pp, rp_plan** out) {
@@ -856,6 +875,19 @@ rp_status rp_smoothness_ok(const rp_arm* arm, const rp_reach_params* rp, const r
   return guarded([&] {
     const PP r = resolve_path_params(*pp, *arm, *rp);
     *ok = smoothness_ok(from_abi(*prev, nullptr), from_abi(*cand, nullptr), r, relax) ? 1 : 0;
+  });
+}
+
+rp_status rp_path_params_resolve(const rp_arm* arm, const rp_reach_params* rp,
+                                 const rp_path_params* pp, rp_path_params* out) {
+  return guarded([&] {
+    const PP r = resolve_path_params(*pp, *arm, *rp);
+    *out = *pp;
+    out->epsilon_waypoint = r.eps_wp;
+    out->d_w = r.d_w;
+    out->slack = r.slack;
+    out->joint1_max_move = r.j1;
+    out->joint2_max_move = r.j2;
   });
 }
 

@@ -730,6 +730,19 @@ static void backward_endpoints(rp_ctx* ctx, const rp_quiver* q, V3 target, doubl
   }
 }
 
+/// span_gap (src/reach_solver.cpp:85-98) for one p2 over all backward points:
+/// the same coarse + band test k_seg2 inlines.
+__global__ void k_span_gap(V3 p2, const V3* __restrict__ bpts, int n, double L3, double eps,
+                           V3* __restrict__ v3_out, uint8_t* __restrict__ pass) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const V3 v3 = bpts[k] - p2;
+  bool ok = rpd::sqnorm(v3) <= (L3 + eps) * (L3 + eps) * (1.0 + 1e-12);
+  if (ok) ok = !(fabs(rpd::norm(v3) - L3) > eps);
+  v3_out[k] = v3;
+  pass[k] = ok ? 1 : 0;
+}
+
 static HostShortcut host_shortcut(const rp_solution_set* s, const ShortcutRec& r) {
   const SolveDev& a = s->sd;
   const ArmDev& arm = a.arm;
@@ -1197,6 +1210,81 @@ rp_status rp_solution_set_pose(const rp_solution_set* cs, int64_t k, rp_pose* po
     auto* s = const_cast<rp_solution_set*>(cs);
     require(k >= 0 && k < s->n_solutions, RP_E_INVALID_PARAMETER, "solution index out of range");
     to_abi(solution_pose(s, k), pose, wps, cap);
+  });
+}
+
+rp_status rp_solution_set_poses(const rp_solution_set* cs, int64_t first, int64_t count,
+                                rp_pose* poses, double* wps, int32_t wps_per_pose) {
+  return guarded([&] {
+    auto* s = const_cast<rp_solution_set*>(cs);
+    require(first >= 0 && count >= 0 && first + count <= s->n_solutions, RP_E_INVALID_PARAMETER,
+            "solution range out of bounds");
+    if (count == 0) return;
+    ensure_keys(s);
+    constexpr int64_t kChunk = 1 << 16;
+    DevBuf<DevPose> d(std::min(count, kChunk), s->ctx->stream);
+    std::vector<DevPose> h(std::min(count, kChunk));
+    for (int64_t c0 = 0; c0 < count; c0 += kChunk) {
+      const int64_t n = std::min(kChunk, count - c0);
+      materialize_solutions(s, s->keys.p + first + c0, nullptr, n, d.p);
+      copy_to_host(s->ctx, h.data(), d.p, n * sizeof(DevPose));
+      for (int64_t k = 0; k < n; ++k)
+        to_abi(host_pose_from_dev(h[k]), poses + c0 + k,
+               wps ? wps + (c0 + k) * 3 * static_cast<int64_t>(wps_per_pose) : nullptr,
+               wps ? wps_per_pose : 0);
+    }
+  });
+}
+
+rp_status rp_backward_endpoints(rp_ctx* ctx, const rp_quiver* q, const double target[3], double L4,
+                                const rp_reach_params* rp, double* points, double* dirs,
+                                int32_t* cone_idx, int32_t cap, int32_t* n_out) {
+  return guarded([&] {
+    std::vector<V3> pts, ds;
+    std::vector<int> cone;
+    backward_endpoints(ctx, q, V3{target[0], target[1], target[2]}, L4, *rp, pts, ds, cone);
+    require(static_cast<int>(pts.size()) <= cap, RP_E_CAPACITY_EXCEEDED,
+            "backward endpoint buffer too small");
+    *n_out = static_cast<int32_t>(pts.size());
+    for (size_t k = 0; k < pts.size(); ++k) {
+      std::memcpy(points + 3 * k, &pts[k], sizeof(V3));
+      if (dirs) std::memcpy(dirs + 3 * k, &ds[k], sizeof(V3));
+      if (cone_idx) cone_idx[k] = cone[k];
+    }
+  });
+}
+
+rp_status rp_span_gap(rp_ctx* ctx, const double p2[3], const double* backward_pts, int32_t n,
+                      double L3, double epsilon, double* v3_out, int32_t* idx_out,
+                      int32_t* n_out) {
+  return guarded([&] {
+    require(n >= 0, RP_E_INVALID_PARAMETER, "negative point count");
+    *n_out = 0;
+    if (n == 0) return;
+    cudaStream_t st = ctx->stream;
+    DevBuf<V3> b(n, st), v(n, st);
+    DevBuf<uint8_t> pass(n, st);
+    copy_to_device(ctx, b.p, backward_pts, n * sizeof(V3));
+    launch(ctx, "span_gap", k_span_gap, dim3(nblk(n, 128)), dim3(128), 0, V3{p2[0], p2[1], p2[2]},
+           static_cast<const V3*>(b.p), n, L3, epsilon, v.p, pass.p);
+    std::vector<V3> hv(n);
+    std::vector<uint8_t> hp(n);
+    copy_to_host(ctx, hv.data(), v.p, n * sizeof(V3));
+    copy_to_host(ctx, hp.data(), pass.p, n);
+    for (int k = 0; k < n; ++k) {
+      if (!hp[k]) continue;
+      std::memcpy(v3_out + 3 * *n_out, &hv[k], sizeof(V3));
+      idx_out[*n_out] = k;
+      ++*n_out;
+    }
+  });
+}
+
+rp_status rp_solution_set_shortcut_basis(const rp_solution_set* s, int64_t k, rp_pose* basis) {
+  return guarded([&] {
+    require(k >= 0 && k < static_cast<int64_t>(s->shortcuts.size()), RP_E_INVALID_PARAMETER,
+            "shortcut index out of range");
+    to_abi(s->shortcuts[k].basis, basis, nullptr, 0);
   });
 }
 

@@ -1,0 +1,172 @@
+// TEST INFRASTRUCTURE: drives the reachplan C++ API exactly as a reference
+// caller would (the reference's own headers, reachplan:: names and types),
+// linked against the façade (paper_1906_10678_b200/facade) over
+// libreachplan_b200.so instead of the reference's src/*.cpp. Reads a scene
+// description, prints the results as JSON for tests/test_facade.py, which
+// compares them with the reference run through oracle/_ref.
+//
+// scene file (whitespace separated):
+//   lengths <n> L1 .. Ln   radius <r>   mode <0|1>   samples <n>
+//   bounds x0 y0 z0 x1 y1 z1   voxel <vs>   quiver <step_rad> <min_per_ring>
+//   target x y z   second x y z   boxes <k> then k lines "x0 y0 z0 x1 y1 z1"
+#include "reachplan/pipeline.hpp"
+
+#include <cstdio>
+#include <fstream>
+#include <iostream>
+#include <sstream>
+#include <string>
+
+using namespace reachplan;
+
+namespace {
+
+std::string num(double v) {
+  char b[40];
+  std::snprintf(b, sizeof(b), "%.17g", v);
+  return b;
+}
+std::string vec(const Vec3& v) { return "[" + num(v.x()) + "," + num(v.y()) + "," + num(v.z()) + "]"; }
+template <typename T, typename F>
+std::string list(const std::vector<T>& xs, F f) {
+  std::string s = "[";
+  for (std::size_t k = 0; k < xs.size(); ++k) s += (k ? "," : "") + f(xs[k]);
+  return s + "]";
+}
+std::string pose(const PoseChain& p) {
+  return "{\"segments\":" + list(p.segments, vec) + ",\"joints\":" + list(p.joints, vec) +
+         ",\"qidx\":" + list(p.quiver_indices, [](int i) { return std::to_string(i); }) +
+         ",\"n_waypoints\":" + std::to_string(p.waypoints.size()) +
+         ",\"s4dev\":" + num(p.s4_length_dev) + "}";
+}
+std::string plan(const PathPlan& p) {
+  return "{\"kind\":\"" + p.provenance.kind + "\",\"waypoints\":" + list(p.waypoints, vec) +
+         ",\"relax\":" + list(p.provenance.relax_per_waypoint, num) +
+         ",\"notes\":" + list(p.provenance.notes, [](const std::string& s) { return "\"" + s + "\""; }) +
+         ",\"poses\":" + list(p.poses, pose) + ",\"unfold\":" + list(p.unfold_prefix, pose) +
+         ",\"switch\":" + std::to_string(p.provenance.replan_switch_index) + "}";
+}
+std::string stats(const SolveStats& s) {
+  const std::vector<long> v{s.seg1_candidates, s.seg1_limit_pass, s.seg1_reach_pass,
+                            s.seg1_survivors,  s.pair_candidates, s.seg2_limit_pass,
+                            s.seg2_clear_pass, s.gap_tested,      s.gap_pass,
+                            s.joint_pass,      s.v3_clear_pass,   s.solutions,
+                            s.shortcuts_found};
+  return list(v, [](long x) { return std::to_string(x); });
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  if (argc < 2) {
+    std::cerr << "usage: facade_check scene.txt\n";
+    return 2;
+  }
+  std::ifstream in(argv[1]);
+  std::string key;
+  ArmSpec arm;
+  ReachParams rp;
+  Scene scene;
+  double qstep = 0.0;
+  int mpr = 4;
+  Vec3 second = Vec3::Zero();
+  while (in >> key) {
+    if (key == "lengths") {
+      int n;
+      in >> n;
+      arm.lengths.resize(n);
+      for (double& L : arm.lengths) in >> L;
+    } else if (key == "radius") {
+      in >> arm.arm_radius;
+    } else if (key == "mode") {
+      int m;
+      in >> m;
+      rp.mode = m == 0 ? SolveMode::six_dof : SolveMode::eight_dof;
+    } else if (key == "samples") {
+      in >> rp.n_samples_per_segment;
+    } else if (key == "bounds") {
+      double a, b, c, d, e, f;
+      in >> a >> b >> c >> d >> e >> f;
+      scene.grid.bounds_min = Vec3(a, b, c);
+      scene.grid.bounds_max = Vec3(d, e, f);
+    } else if (key == "voxel") {
+      in >> scene.grid.voxel_size;
+    } else if (key == "quiver") {
+      in >> qstep >> mpr;
+    } else if (key == "target") {
+      double a, b, c;
+      in >> a >> b >> c;
+      scene.target = Vec3(a, b, c);
+    } else if (key == "second") {
+      double a, b, c;
+      in >> a >> b >> c;
+      second = Vec3(a, b, c);
+    } else if (key == "boxes") {
+      int k;
+      in >> k;
+      for (int i = 0; i < k; ++i) {
+        SceneObstacle o;
+        double a, b, c, d, e, f;
+        in >> a >> b >> c >> d >> e >> f;
+        o.box_min = Vec3(a, b, c);
+        o.box_max = Vec3(d, e, f);
+        scene.obstacles.push_back(o);
+      }
+    }
+  }
+  try {
+    const Quiver q = generate_quiver(qstep, qstep, mpr);
+    const VoxelGrid grid = build_scene_grid(scene, arm, rp);
+    // the same grid again through the primitive calls
+    VoxelGrid g2 = build_grid(scene.grid.bounds_min, scene.grid.bounds_max, scene.grid.voxel_size);
+    mark_obstacles(g2, scene.obstacles);
+    dilate(g2, effective_dilation(scene, arm, rp));
+    const SolutionSet set = solve_reach(arm, q, grid, scene.target, rp);
+    const ChosenPath chosen = select_solution(set);
+    PathParams pp;
+    // each planner call reports its own outcome (a plan or the Errc it threw)
+    const auto attempt = [](auto&& fn, PathPlan* keep) -> std::string {
+      try {
+        PathPlan p = fn();
+        if (keep) *keep = p;
+        return plan(p);
+      } catch (const Error& e) {
+        return "{\"error\":" + std::to_string(static_cast<int>(e.code()) + 1) + "}";
+      }
+    };
+    PathPlan p1, p3;
+    const std::string j1 = attempt([&] { return plan_reach_then_path(arm, q, grid, scene.target, rp, pp); }, &p1);
+    const std::string j2 = attempt([&] { return plan_from_reach(arm, q, grid, chosen, set, scene.target, rp, pp); }, nullptr);
+    std::string j3 = "null";
+    if (!p1.poses.empty())
+      j3 = attempt([&] { return plan_arbitrary(arm, q, grid, p1.poses.back(), second, rp, pp); }, &p3);
+    const BackwardEndpoints be =
+        backward_endpoints(scene.target, arm.lengths.back(), q, rp.approach_axis, 0.0, rp.mode);
+    const std::vector<GapCandidate> gaps =
+        span_gap(chosen.pose.joints[2], be.points, arm.length(2), rp.resolved_epsilon(arm));
+    const SegmentProbe probe = segment_clear(grid, arm.root, scene.target, 8);
+    std::cout << "{\"quiver\":" << q.size() << ",\"rings\":" << q.ring_count()
+              << ",\"occupied\":" << grid.occupied_count()
+              << ",\"grids_equal\":" << (grid.occupancy == g2.occupancy ? "true" : "false")
+              << ",\"dilation\":" << num(grid.dilation_radius)
+              << ",\"point_clear_target\":" << (point_clear(grid, scene.target) ? 1 : 0)
+              << ",\"segment_clear\":" << (probe.clear ? 1 : 0)
+              << ",\"stats\":" << stats(set.stats) << ",\"n_solutions\":" << set.solutions.size()
+              << ",\"n_shortcuts\":" << set.shortcuts.size()
+              << ",\"first_solution\":" << (set.solutions.empty() ? "null" : pose(set.solutions.front()))
+              << ",\"last_solution\":" << (set.solutions.empty() ? "null" : pose(set.solutions.back()))
+              << ",\"chosen\":{\"kind\":" << (chosen.kind == ChosenPath::Kind::shortcut ? 1 : 0)
+              << ",\"path_length\":" << num(chosen.path_length) << ",\"pose\":" << pose(chosen.pose)
+              << "},\"span_gap\":" << gaps.size()
+              << ",\"mean_dev\":"
+              << (p1.waypoints.empty() || p3.waypoints.empty()
+                      ? std::string("null")
+                      : num(mean_polyline_deviation(p1.waypoints, p3.waypoints)))
+              << ",\"plan\":" << j1 << ",\"plan_from_reach\":" << j2 << ",\"arbitrary\":" << j3
+              << "}\n";
+  } catch (const Error& e) {
+    std::cout << "{\"error\":" << static_cast<int>(e.code()) << ",\"what\":\"" << e.what() << "\"}\n";
+    return 0;
+  }
+  return 0;
+}
