@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 namespace rp {
@@ -167,8 +168,8 @@ constexpr int kRowsTz = 4;  // z-planes per block of k_mark_dilate_rows
 /// thread computes every primitive's x-interval for its row once, builds the
 /// WX words in registers and writes them with 16-byte stores. Block tile =
 /// 32 rows (y) x 8 planes (z); primitives culled to the tile in smem.
-template <int WX>
-__global__ void __launch_bounds__(256) k_mark_dilate_rowwise(uint64_t* __restrict__ bits, GridView g,
+template <int WX, int TY, int NT>
+__global__ void __launch_bounds__(NT) k_mark_dilate_rowwise(uint64_t* __restrict__ bits, GridView g,
                                                              const Prim* __restrict__ prims, int np,
                                                              const int* __restrict__ wtab, int reach,
                                                              int y0, int y1, int z0, int z1,
@@ -177,8 +178,13 @@ __global__ void __launch_bounds__(256) k_mark_dilate_rowwise(uint64_t* __restric
   Prim* sp = sp_all + np;
   int* swt = reinterpret_cast<int*>(sp_all + 2 * np);
   __shared__ int ns;
-  const int yt = y0 + static_cast<int>(blockIdx.x) * 32;
-  const int zt = z0 + static_cast<int>(blockIdx.y) * 8;
+  // Programmatic dependent launch (launch_pdl): let the next update start its
+  // prologue now; this one waits for its predecessor before the first store.
+  // Both are no-ops for an ordinary launch.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  constexpr int TZ = NT / TY;  // tile = TY rows (y) x TZ planes (z), one row per thread
+  const int yt = y0 + static_cast<int>(blockIdx.x) * TY;
+  const int zt = z0 + static_cast<int>(blockIdx.y) * TZ;
   if (threadIdx.x == 0) ns = 0;
   {
     const int* src = reinterpret_cast<const int*>(prims);
@@ -191,13 +197,13 @@ __global__ void __launch_bounds__(256) k_mark_dilate_rowwise(uint64_t* __restric
   for (int k = threadIdx.x; k < np; k += blockDim.x) {
     const Prim p = sp_all[k];
     if (p.a[0] > p.b[0] || p.a[1] > p.b[1] || p.a[2] > p.b[2]) continue;
-    if (p.a[2] - reach > zt + 7 || p.b[2] + reach < zt) continue;
-    if (p.a[1] - reach > yt + 31 || p.b[1] + reach < yt) continue;
+    if (p.a[2] - reach > zt + TZ - 1 || p.b[2] + reach < zt) continue;
+    if (p.a[1] - reach > yt + TY - 1 || p.b[1] + reach < yt) continue;
     sp[atomicAdd(&ns, 1)] = p;
   }
   __syncthreads();
-  const int y = yt + (threadIdx.x & 31);
-  const int z = zt + (threadIdx.x >> 5);
+  const int y = yt + static_cast<int>(threadIdx.x % TY);
+  const int z = zt + static_cast<int>(threadIdx.x / TY);
   const bool valid = !(y > y1 || y >= g.ny || z > z1 || z >= g.nz);
   uint64_t m[WX];
 #pragma unroll
@@ -217,8 +223,12 @@ __global__ void __launch_bounds__(256) k_mark_dilate_rowwise(uint64_t* __restric
     for (int w = 0; w < WX; ++w) m[w] |= range_mask(lo, hi, 64 * w);
   }
   uint64_t* row = bits + (static_cast<size_t>(z) * g.ny + y) * WX;
-  const int rows = min(32, min(y1, g.ny - 1) - yt + 1);
-  const bool bulk = !accumulate && WX >= 2 && (g.ny * WX) % 2 == 0 && rows > 0;
+  const int rows = min(TY, min(y1, g.ny - 1) - yt + 1);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // accumulate: OR into the existing grid (plain stores); otherwise the tile
+  // goes out through TMA bulk stores (measured on B200 at 512^3: 5.4 us per
+  // pass vs 6.1 us for coalesced 16-byte stores and 11.9 us for per-row stores)
+  const bool bulk = !(accumulate & 1) && WX >= 2 && (g.ny * WX) % 2 == 0 && rows > 0;
   if (!bulk) {
     if (!valid) return;
     if (accumulate) {
@@ -229,20 +239,20 @@ __global__ void __launch_bounds__(256) k_mark_dilate_rowwise(uint64_t* __restric
     for (int w = 0; w < WX; ++w) row[w] = m[w];
     return;
   }
-  // Stage the tile (8 planes x 32 rows) in shared memory, then one thread
+  // Stage the tile (TZ planes x TY rows) in shared memory, then one thread
   // per plane streams its contiguous rows*WX*8-byte run out with a TMA bulk
   // store (cp.async.bulk): full-line writes instead of 32 strided stores.
-  __shared__ __align__(128) uint64_t tile[256 * WX];
+  __shared__ __align__(128) uint64_t tile[NT * WX];
 #pragma unroll
   for (int w = 0; w < WX; ++w) tile[threadIdx.x * WX + w] = m[w];
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
-  if (threadIdx.x < 8) {
+  if (threadIdx.x < TZ) {
     const int zz = zt + static_cast<int>(threadIdx.x);
     if (zz <= z1 && zz < g.nz) {
       uint64_t* gdst = bits + (static_cast<size_t>(zz) * g.ny + yt) * WX;
       const uint32_t sa =
-          static_cast<uint32_t>(__cvta_generic_to_shared(&tile[threadIdx.x * 32 * WX]));
+          static_cast<uint32_t>(__cvta_generic_to_shared(&tile[threadIdx.x * TY * WX]));
       const uint32_t nbytes = static_cast<uint32_t>(rows * WX * 8);
       asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
                    "r"(sa), "r"(nbytes)
@@ -251,6 +261,96 @@ __global__ void __launch_bounds__(256) k_mark_dilate_rowwise(uint64_t* __restric
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     }
   }
+}
+
+/// Persistent form of k_mark_dilate_rowwise for full-grid, overwrite passes
+/// (accumulate == 0, WX >= 2): ~2 blocks per SM loop over the 32-row x
+/// 8-plane tiles. The primitive list and width table are staged once per
+/// block; each tile is culled, computed one row per thread, staged in one of
+/// two shared buffers and streamed out with cp.async.bulk while the next tile
+/// is computed (the buffer is reused only after its bulk store has read it).
+/// With launch_pdl the next pass's blocks start as these retire.
+template <int WX>
+__global__ void __launch_bounds__(256) k_mark_dilate_tiles(uint64_t* __restrict__ bits, GridView g,
+                                                           const Prim* __restrict__ prims, int np,
+                                                           const int* __restrict__ wtab,
+                                                           int reach) {
+  extern __shared__ Prim sp_all[];
+  Prim* sp = sp_all + np;
+  int* swt = reinterpret_cast<int*>(sp_all + 2 * np);
+  __shared__ int ns;
+  __shared__ __align__(128) uint64_t tile[2][256 * WX];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  {
+    const int* src = reinterpret_cast<const int*>(prims);
+    int* dst = reinterpret_cast<int*>(sp_all);
+    for (int k = threadIdx.x; k < 6 * np; k += blockDim.x) dst[k] = __ldg(src + k);
+    const int nw = 2 * reach * reach + 1;
+    for (int k = threadIdx.x; k < nw; k += blockDim.x) swt[k] = __ldg(wtab + k);
+  }
+  const int ty = (g.ny + 31) / 32, tz = (g.nz + 7) / 8;
+  const int ntiles = ty * tz;
+  bool waited = false;
+  int buf = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, buf ^= 1) {
+    const int yt = (t % ty) * 32;
+    const int zt = (t / ty) * 8;
+    if (threadIdx.x == 0) ns = 0;
+    __syncthreads();  // also: the staged inputs / previous tile's reads are done
+    for (int k = threadIdx.x; k < np; k += blockDim.x) {
+      const Prim p = sp_all[k];
+      if (p.a[0] > p.b[0] || p.a[1] > p.b[1] || p.a[2] > p.b[2]) continue;
+      if (p.a[2] - reach > zt + 7 || p.b[2] + reach < zt) continue;
+      if (p.a[1] - reach > yt + 31 || p.b[1] + reach < yt) continue;
+      sp[atomicAdd(&ns, 1)] = p;
+    }
+    __syncthreads();
+    const int y = yt + (threadIdx.x & 31);
+    const int z = zt + (threadIdx.x >> 5);
+    const bool valid = y < g.ny && z < g.nz;
+    uint64_t m[WX];
+#pragma unroll
+    for (int w = 0; w < WX; ++w) m[w] = 0;
+    const int n_here = valid ? ns : 0;
+    for (int k = 0; k < n_here; ++k) {
+      const Prim p = sp[k];
+      const int dy = y < p.a[1] ? p.a[1] - y : (y > p.b[1] ? y - p.b[1] : 0);
+      const int dz = z < p.a[2] ? p.a[2] - z : (z > p.b[2] ? z - p.b[2] : 0);
+      if (dy > reach || dz > reach) continue;
+      const int wd = swt[dy * dy + dz * dz];
+      if (wd < 0) continue;
+      int lo = p.a[0] - wd, hi = p.b[0] + wd;
+      lo = lo < 0 ? 0 : lo;
+      hi = hi > g.nx - 1 ? g.nx - 1 : hi;
+#pragma unroll
+      for (int w = 0; w < WX; ++w) m[w] |= range_mask(lo, hi, 64 * w);
+    }
+    // buffer `buf` was last read by the bulk store two tiles ago
+    if (threadIdx.x < 8) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < WX; ++w) tile[buf][threadIdx.x * WX + w] = m[w];
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (!waited) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      waited = true;
+    }
+    if (threadIdx.x < 8) {
+      const int zz = zt + static_cast<int>(threadIdx.x);
+      const int rows = min(32, g.ny - yt);
+      if (zz < g.nz) {
+        uint64_t* gdst = bits + (static_cast<size_t>(zz) * g.ny + yt) * WX;
+        const uint32_t sa =
+            static_cast<uint32_t>(__cvta_generic_to_shared(&tile[buf][threadIdx.x * 32 * WX]));
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+                     "r"(sa), "r"(static_cast<uint32_t>(rows * WX * 8))
+                     : "memory");
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  if (threadIdx.x < 8) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 /// dynamic shared memory of k_mark_dilate_rows: prims, culled prims, widths
@@ -315,7 +415,8 @@ void check_boxes(const rp_obstacle* obs, int n) {
 }
 
 void launch_rows(rp_ctx* ctx, const char* name, rp_grid* g, const Prim* prims, int np,
-                 const int* wtab, int reach, int y0, int y1, int z0, int z1, bool accumulate);
+                 const int* wtab, int reach, int y0, int y1, int z0, int z1, bool accumulate,
+                 bool pdl = false);
 
 /// Rasterise host-computed index boxes (one async upload, no box kernel).
 bool launch_rows_param(rp_ctx* ctx, const char* name, rp_grid* g, const std::vector<Prim>& prims,
@@ -326,26 +427,60 @@ bool launch_rows_param(rp_ctx* ctx, const char* name, rp_grid* g, const std::vec
   DevBuf<int> wtab(t.w.size(), ctx->stream);
   copy_to_device(ctx, wtab.p, t.w.data(), t.w.size() * sizeof(int));
   launch_rows(ctx, name, g, dp.p, static_cast<int>(prims.size()), wtab.p, t.reach, y0, y1, z0, z1,
-              accumulate);
+              accumulate, true);
   return true;
 }
 
 /// Launch the fused rasterise(+dilate) over rows [y0,y1] x [z0,z1].
+/// pdl: prims and wtab are not produced by the preceding kernel (host
+/// uploads), so the prologue may overlap it (launch_pdl).
 void launch_rows(rp_ctx* ctx, const char* name, rp_grid* g, const Prim* prims, int np,
-                 const int* wtab, int reach, int y0, int y1, int z0, int z1, bool accumulate) {
+                 const int* wtab, int reach, int y0, int y1, int z0, int z1, bool accumulate,
+                 bool pdl) {
   const size_t smem = rows_smem(np, reach);
   const int acc = accumulate ? 1 : 0;
+  // tile = 32 rows x 8 planes, 256 threads (16 x 8 / 128 and 32 x 4 / 128,
+  // 64..256-row tiles measured the same at 512^3 with PDL)
+  constexpr int TYv = 32, NTv = 256;
   auto rowwise = [&](auto kern) {
-    const dim3 grid(static_cast<unsigned>((y1 - y0 + 32) / 32),
-                    static_cast<unsigned>((z1 - z0 + 8) / 8));
-    launch(ctx, name, kern, grid, dim3(256), smem, g->bits, g->view(), prims, np, wtab, reach, y0,
-           y1, z0, z1, acc);
+    const int TZv = NTv / TYv;
+    const dim3 grid(static_cast<unsigned>((y1 - y0 + TYv) / TYv),
+                    static_cast<unsigned>((z1 - z0 + TZv) / TZv));
+    if (pdl)
+      launch_pdl(ctx, name, kern, grid, dim3(NTv), smem, g->bits, g->view(), prims, np, wtab,
+                 reach, y0, y1, z0, z1, acc);
+    else
+      launch(ctx, name, kern, grid, dim3(NTv), smem, g->bits, g->view(), prims, np, wtab, reach,
+             y0, y1, z0, z1, acc);
   };
+  static const bool no_tiles = std::getenv("RP_NO_TILE_KERNEL") != nullptr;
+  const bool full = y0 == 0 && z0 == 0 && y1 == g->dims[1] - 1 && z1 == g->dims[2] - 1;
+  // The persistent tile kernel wins while every block owns one tile (256^3:
+  // 1.9 vs 2.2 us per pass); at 512^3 its serial per-block tile loop loses to
+  // one tile per block (8.2 vs 5.4 us), measured on B200.
+  const int ntiles = ((g->dims[1] + 31) / 32) * ((g->dims[2] + 7) / 8);
+  static const int bps = std::getenv("RP_TILE_BPS") ? std::atoi(std::getenv("RP_TILE_BPS")) : 4;
+  if (!accumulate && full && !no_tiles && (g->wx == 2 || g->wx == 4 || g->wx == 8) &&
+      ntiles <= std::max(1, bps) * ctx->sm_count) {
+    const dim3 grid(static_cast<unsigned>(ntiles));
+    auto tiles = [&](auto kern) {
+      if (pdl)
+        launch_pdl(ctx, name, kern, grid, dim3(256), smem, g->bits, g->view(), prims, np, wtab,
+                   reach);
+      else
+        launch(ctx, name, kern, grid, dim3(256), smem, g->bits, g->view(), prims, np, wtab, reach);
+    };
+    switch (g->wx) {
+      case 2: tiles(k_mark_dilate_tiles<2>); return;
+      case 4: tiles(k_mark_dilate_tiles<4>); return;
+      default: tiles(k_mark_dilate_tiles<8>); return;
+    }
+  }
   switch (g->wx) {
-    case 1: rowwise(k_mark_dilate_rowwise<1>); return;
-    case 2: rowwise(k_mark_dilate_rowwise<2>); return;
-    case 4: rowwise(k_mark_dilate_rowwise<4>); return;
-    case 8: rowwise(k_mark_dilate_rowwise<8>); return;
+    case 1: rowwise(k_mark_dilate_rowwise<1, TYv, NTv>); return;
+    case 2: rowwise(k_mark_dilate_rowwise<2, TYv, NTv>); return;
+    case 4: rowwise(k_mark_dilate_rowwise<4, TYv, NTv>); return;
+    case 8: rowwise(k_mark_dilate_rowwise<8, TYv, NTv>); return;
     default: break;
   }
   const int tw = std::min(g->wx, 256);
@@ -755,9 +890,10 @@ rp_status rp_grid_mark_dilate_repeat(rp_grid* g, const rp_obstacle* obs, int32_t
     cudaGraph_t graph;
     cudaGraphExec_t exec;
     RP_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    static const bool no_pdl = std::getenv("RP_NO_PDL") != nullptr;
     for (int r = 0; r < reps; ++r)
       launch_rows(ctx, "mark_dilate", g, prims.p, static_cast<int>(np), wtab.p, t.reach, 0,
-                  g->dims[1] - 1, 0, g->dims[2] - 1, false);
+                  g->dims[1] - 1, 0, g->dims[2] - 1, false, !no_pdl);
     RP_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
     ctx->timing = timing;
     RP_CUDA(cudaGraphInstantiate(&exec, graph, 0));

@@ -182,6 +182,29 @@ inline void launch(rp_ctx* ctx, const char* name, K kernel, dim3 grid, dim3 bloc
   launch_end(ctx, name, ev);
 }
 
+/// launch() with programmatic dependent launch: the kernel may begin while
+/// the previous kernel on the stream drains. The kernel must execute
+/// griddepcontrol.wait before touching memory that kernel writes (or any
+/// memory a preceding kernel produced); see k_mark_dilate_rowwise.
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(rp_ctx* ctx, const char* name, void (*kernel)(KArgs...), dim3 grid,
+                       dim3 block, size_t smem, Args... args) {
+  cudaEvent_t ev = nullptr;
+  launch_begin(ctx, name, &ev);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  RP_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+  launch_end(ctx, name, ev);
+}
+
 /// Stream-ordered device buffer.
 template <typename T>
 struct DevBuf {
