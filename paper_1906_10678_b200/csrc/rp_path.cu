@@ -256,14 +256,6 @@ __device__ __noinline__ bool wik_eval(const WikDev& w, const CiData& c, int j, D
 __device__ bool wik_eval_fast(const WikDev& w, const CiData& c, int j, double* metric_out,
                               int* opt_out) {
   const ArmDev& arm = w.arm;
-  long long tp = w.prof ? clock64() : 0;
-  const auto mark = [&](int slot) {
-    if (w.prof) {
-      const long long t = clock64();
-      atomicMax(reinterpret_cast<unsigned long long*>(w.prof + slot), t - tp);
-      tp = t;
-    }
-  };
   const V3 qj = wq(w, j);
   const V3 p2 = c.p1 + arm.L[1] * qj;
   const double move2 = rpd::norm(p2 - w.prev_j2);
@@ -275,13 +267,10 @@ __device__ bool wik_eval_fast(const WikDev& w, const CiData& c, int j, double* m
   double metric = c.move1 + move2;
   if (w.has_bias) metric += rpd::norm(c.p1 - w.bias_j1) + rpd::norm(p2 - w.bias_j2);
   if (!c.ok) return false;
-  mark(10);
   if (!rpd::walk_clear(w.g, c.p1, p2, w.n)) return false;  // link2 = p1 (coaxial)
-  mark(11);
   const V3 s3 = v3_hat * arm.L[2];
   const V3 p3 = p2 + s3;
   if (!rpd::walk_clear(w.g, p2, p3, w.n)) return false;
-  mark(12);
   V3 J[5];
   J[0] = arm.root;
   J[1] = J[0] + arm.L[0] * wq(w, c.i);
@@ -299,8 +288,7 @@ __device__ bool wik_eval_fast(const WikDev& w, const CiData& c, int j, double* m
       opt = o;
       done = true;
     }
-    mark(13);
-    if (!done) return false;
+      if (!done) return false;
   } else if (!rpd::self_collision_free(J, 3, min_sep)) {
     return false;
   }
@@ -308,6 +296,98 @@ __device__ bool wik_eval_fast(const WikDev& w, const CiData& c, int j, double* m
   *metric_out = metric;
   *opt_out = opt;
   return true;
+}
+
+/// wik_eval_fast's exact prefix (segment-2 move bound, gap band, metric):
+/// false when the pair cannot qualify. Same arithmetic, same order.
+__device__ __forceinline__ bool wik_pre_fast(const WikDev& w, const CiFast& c, int j, double* metric) {
+  const ArmDev& arm = w.arm;
+  const V3 qj = wq(w, j);
+  const V3 p2 = c.p1 + arm.L[1] * qj;
+  const double move2 = rpd::norm(p2 - w.prev_j2);
+  if (move2 > w.j2max) return false;
+  const V3 v3 = w.wp - p2;
+  const double v3_len = rpd::norm(v3);
+  if (fabs(v3_len - arm.L[2]) > w.eps || v3_len < 1e-12) return false;
+  double m = c.move1 + move2;
+  if (w.has_bias) m += rpd::norm(c.p1 - w.bias_j1) + rpd::norm(p2 - w.bias_j2);
+  *metric = m;
+  return c.ok != 0;
+}
+
+/// The remaining tests of wik_eval_fast for a pair that passed wik_pre_fast,
+/// spread over one warp in two data-parallel steps (every lane runs the
+/// same code on its own operands, so nothing serialises on divergence):
+/// walks — lane 0 segment 2, lane 1 segment 3, lanes 2.. the trail segment
+/// of each option; link distances — lane 3*o + p the p-th non-adjacent link
+/// pair of option o's chain. Every test is a pure function of the pose, so
+/// the verdict and the first qualifying trail option equal the sequential
+/// evaluation's. All lanes return the same result.
+__device__ bool wik_full_warp(const WikDev& w, const CiFast& c, int j, int lane, int* opt_out) {
+  const ArmDev& arm = w.arm;
+  const V3 qj = wq(w, j);
+  const V3 p2 = c.p1 + arm.L[1] * qj;
+  const V3 v3 = w.wp - p2;
+  const double v3_len = rpd::norm(v3);
+  const V3 v3_hat = v3 / v3_len;
+  const V3 s3 = v3_hat * arm.L[2];
+  const V3 p3 = p2 + s3;
+  V3 J[4];
+  J[0] = arm.root;
+  J[1] = J[0] + arm.L[0] * wq(w, c.i);
+  J[2] = J[1] + arm.L[1] * qj;
+  J[3] = J[2] + s3;
+  if (!(rpd::norm(J[1] - w.prev_j1) <= w.sm1 && rpd::norm(J[2] - w.prev_j2) <= w.sm2))
+    return false;
+  const double min_sep = 2.0 * arm.arm_radius;
+  const int nopt = w.four ? w.n_opts + 1 : 0;
+  // trail endpoint of option o (lane-selected below)
+  auto tip = [&](int o) {
+    const V3 dir = o < w.n_opts ? w.opt_dir[o] : rpd::normalized(s3);
+    return J[3] + w.L4 * dir;
+  };
+  // step 1: walks
+  bool ok = true;
+  if (lane < 2 + nopt) {
+    V3 from = c.p1, to = p2;
+    if (lane == 1) {
+      from = p2;
+      to = p3;
+    } else if (lane >= 2) {
+      from = J[3];
+      to = tip(lane - 2);
+    }
+    ok = rpd::walk_first_blocked_fast(w.g, from, to, w.n) == 0;
+  }
+  const unsigned walk_fail = __ballot_sync(0xffffffffu, !ok);
+  if (walk_fail & 3u) return false;
+  // step 2: non-adjacent link distances
+  ok = true;
+  const int npairs = w.four ? 3 * nopt : 1;
+  if (lane < npairs) {
+    V3 a0, a1, b0, b1;
+    if (!w.four) {
+      a0 = J[0]; a1 = J[1]; b0 = J[2]; b1 = J[3];
+    } else {
+      const int o = lane / 3, pr = lane % 3;
+      const V3 j4 = tip(o);
+      // pairs of a 4-link chain: (0,2), (0,3), (1,3)
+      a0 = pr == 2 ? J[1] : J[0];
+      a1 = pr == 2 ? J[2] : J[1];
+      b0 = pr == 0 ? J[2] : J[3];
+      b1 = pr == 0 ? J[3] : j4;
+    }
+    ok = !(rpd::seg_seg_distance(a0, a1, b0, b1) < min_sep);
+  }
+  const unsigned dist_fail = __ballot_sync(0xffffffffu, !ok);
+  if (!w.four) return !(dist_fail & 1u);
+  for (int o = 0; o < nopt; ++o) {
+    if (!((walk_fail >> (2 + o)) & 1u) && !((dist_fail >> (3 * o)) & 7u)) {
+      *opt_out = o;
+      return true;
+    }
+  }
+  return false;
 }
 
 __device__ __forceinline__ bool wik_test(const WikDev& w, const CiData& c, int j, double* m,
@@ -400,6 +480,30 @@ __device__ void wik_filter_one(const WikDev& w, double cone1, double cone2, V3 u
   }
   *pi_out = pi;
   *pj_out = pj;
+}
+
+/// wik_filter_one for a coaxial arm without limits: the same tests and
+/// arithmetic, writing the compact CiFast record (no frame).
+__device__ __forceinline__ void wik_filter_fast(const WikDev& w, double cone1, double cone2, V3 u1,
+                                                V3 u2, int i, CiFast* out, bool* pi_out,
+                                                bool* pj_out) {
+  const V3 q = wq(w, i);
+  bool pi = false;
+  if (!w.filter_j || rpd::dot(q, u1) >= cone1) {
+    const V3 p1 = w.arm.root + w.arm.L[0] * q;
+    const double move1 = rpd::norm(p1 - w.prev_j1);
+    pi = !(move1 > w.j1max);
+    if (pi) {
+      CiFast c;
+      c.i = i;
+      c.move1 = move1;
+      c.p1 = p1;
+      c.ok = rpd::walk_first_blocked_fast(w.g, w.arm.root, p1, w.n) == 0 ? 1 : 0;
+      out[i] = c;
+    }
+  }
+  *pi_out = pi;
+  *pj_out = !w.filter_j || rpd::dot(q, u2) >= cone2;
 }
 
 __global__ void k_wik_filter(WikDev w, double cone1, double cone2, V3 u1, V3 u2,
@@ -620,7 +724,7 @@ __device__ __forceinline__ T ldcg_struct(const T* p) {
   return v;
 }
 
-constexpr int kBpThreads = 512;
+constexpr int kBpThreads = 256;
 
 __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_constant__ BpArgs A) {
   extern __shared__ int sh_lists[];
@@ -633,6 +737,12 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
   // (a per-thread copy would be ~700 B of local memory per thread)
   __shared__ WikDev sw;
   __shared__ V3 s_u1, s_u2, s_cu, s_cv, s_wk;
+  // screened candidates of one round (one pair per thread): metric, ordinal
+  __shared__ double s_cm[kBpThreads];
+  __shared__ long long s_ct[kBpThreads];
+  __shared__ int s_nc;
+  __shared__ short s_rank[kBpThreads];
+  const bool fast_eval = !A.arm.any_limit && !A.arm.has_offsets;
   for (int k = A.m - 2; k >= 0; --k) {
     if (k == 0 && A.has_fixed) {
       if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -733,15 +843,27 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
         for (int i0 = blockIdx.x * blockDim.x; i0 < A.Q; i0 += nb * blockDim.x) {
           const int i = i0 + threadIdx.x;
           bool pi = false, pj = false;
-          if (i < A.Q) wik_filter_one(w, A.cone1[fi], A.cone2[fi], u1, u2, i, A.ci_by_index, &pi, &pj);
+          const long long f0 = A.prof ? clock64() : 0;
+          if (i < A.Q) {
+            if (fast_eval)
+              wik_filter_fast(w, A.cone1[fi], A.cone2[fi], u1, u2, i, A.ci_fast, &pi, &pj);
+            else
+              wik_filter_one(w, A.cone1[fi], A.cone2[fi], u1, u2, i, A.ci_by_index, &pi, &pj);
+          }
+          if (A.prof) {
+            atomicMax(reinterpret_cast<unsigned long long*>(A.prof + 12), clock64() - f0);
+            if (pi) atomicAdd(reinterpret_cast<unsigned long long*>(A.prof + 14), 1ull);
+          }
           const unsigned mi = __ballot_sync(FULL, pi), mj = __ballot_sync(FULL, pj);
           if (lane == 0 && (i >> 5) < (A.Q + 31) / 32) {
             A.ibits[i >> 5] = mi;
             A.jbits[i >> 5] = mj;
           }
         }
+        const long long cb = prof ? clock64() : 0;
         grid_barrier(A.bar, nb);
         long long c1 = prof ? clock64() : 0;
+        if (prof) A.prof[13] += c1 - cb;
         // phase B: block-local compaction + this block's share of the pairs
         const int nci = block_compact<kBpThreads>(A.ibits, A.Q, li);
         const int ncj = block_compact<kBpThreads>(A.jbits, A.Q, lj);
@@ -752,6 +874,73 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
         const long long total = static_cast<long long>(nci) * ncj;
         // pairs dealt round-robin over the blocks (pair tt -> block tt % nb),
         // so a few thousand pairs spread over every SM of the grid
+        if (fast_eval) {
+          // Each round every thread screens one pair with the exact prefix
+          // of the test (move bound, gap band, metric); the survivors are
+          // evaluated one warp per pair (wik_full_warp), which cuts the
+          // serial chain of a full evaluation from ~30k to a few k cycles.
+          long long tt = static_cast<long long>(threadIdx.x) * nb + blockIdx.x;
+          const long long stride = static_cast<long long>(nb) * blockDim.x;
+          const int warp = threadIdx.x >> 5;
+          for (;;) {
+            if (threadIdx.x == 0) s_nc = 0;
+            __syncthreads();
+            if (tt < total) {
+              const int a = static_cast<int>(tt / ncj);
+              if (__ldcg(&A.ci_fast[li[a]].ok)) {
+                const CiFast c = ldcg_struct(A.ci_fast + li[a]);
+                double mm;
+                if (wik_pre_fast(w, c, lj[tt - static_cast<long long>(a) * ncj], &mm)) {
+                  const int k = atomicAdd(&s_nc, 1);
+                  s_cm[k] = mm;
+                  s_ct[k] = tt;
+                }
+              }
+              tt += stride;
+            }
+            const bool more = __syncthreads_or(tt < total);
+            const int nc = s_nc;
+            if (A.prof && blockIdx.x == 0 && threadIdx.x == 0) {
+              A.prof[10] += nc;
+              A.prof[11] += 1;
+            }
+            // rank the screened candidates by (metric, ordinal) ...
+            if (threadIdx.x < nc) {
+              const double mm = s_cm[threadIdx.x];
+              const long long t2 = s_ct[threadIdx.x];
+              int r = 0;
+              for (int k = 0; k < nc; ++k) r += wik_better(s_cm[k], s_ct[k], mm, t2) ? 1 : 0;
+              s_rank[r] = static_cast<short>(threadIdx.x);
+            }
+            __syncthreads();
+            // ... and evaluate them in waves of one candidate per warp, best
+            // first: the first wave with a qualifying pair holds the round's
+            // answer (every later candidate ranks below it)
+            for (int w0 = 0; w0 < nc; w0 += kBpThreads / 32) {
+              const int k = w0 + warp;
+              bool hit = false;
+              int opt = -1;
+              if (k < nc) {
+                const int e = s_rank[k];
+                const double mm = s_cm[e];
+                const long long t2 = s_ct[e];
+                if (wik_better(mm, t2, bm, bo)) {
+                  const int a = static_cast<int>(t2 / ncj);
+                  const CiFast c = ldcg_struct(A.ci_fast + li[a]);
+                  hit = wik_full_warp(w, c, lj[t2 - static_cast<long long>(a) * ncj], lane, &opt);
+                  if (hit) {
+                    bm = mm;
+                    bo = t2;
+                    bopt = opt;
+                  }
+                }
+              }
+              if (__syncthreads_or(hit)) break;
+            }
+            __syncthreads();
+            if (!more) break;
+          }
+        } else
         for (long long tt = static_cast<long long>(threadIdx.x) * nb + blockIdx.x; tt < total;
              tt += static_cast<long long>(nb) * blockDim.x) {
           const int a = static_cast<int>(tt / ncj);
@@ -817,8 +1006,19 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
             int ok = 0;
             if (b.ord != LLONG_MAX) {
               const int a = static_cast<int>(b.ord / ncj);
-              A.poses[k] = wik_pose(w, ldcg_struct(A.ci_by_index + li[a]),
-                                    lj[b.ord - static_cast<long long>(a) * ncj], b.opt);
+              CiData cd;
+              if (fast_eval) {
+                const CiFast f = ldcg_struct(A.ci_fast + li[a]);
+                cd.i = f.i;
+                cd.ok = f.ok;
+                cd.move1 = f.move1;
+                cd.p1 = f.p1;
+                cd.link1 = A.arm.root;
+                cd.frame1 = rpd::m_identity();  // unused without offsets
+              } else {
+                cd = ldcg_struct(A.ci_by_index + li[a]);
+              }
+              A.poses[k] = wik_pose(w, cd, lj[b.ord - static_cast<long long>(a) * ncj], b.opt);
               A.relax[k] = f;
               A.kind[k] = t > 0 ? 1 : 0;
               if (t > 0) A.wps[k] = w.wp;
@@ -1163,6 +1363,7 @@ Planner::Planner(rp_ctx* c, const rp_arm& a, const rp_quiver* qv, const rp_grid*
   cj.alloc(q->n + 1, st);
   ci.alloc(q->n + 1, st);
   ci_by_index.alloc(q->n + 1, st);
+  ci_fast.alloc(q->n + 1, st);
   counts.alloc(2, st);
   wik_blocks = ctx->sm_count;
   block_best.alloc(wik_blocks, st);
@@ -1275,7 +1476,7 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
     // dozen resident blocks keep every phase parallel while making the grid
     // barriers cheaper and the grid's L1 reuse higher.
     const char* env = std::getenv("RP_BP_BLOCKS");
-    bp_blocks = std::min(ctx->sm_count * per_sm, env ? std::max(1, std::atoi(env)) : 32);
+    bp_blocks = std::min(ctx->sm_count * per_sm, env ? std::max(1, std::atoi(env)) : 64);
     bp_bar.alloc(2, st);
     bp_state.alloc(4, st);
     bp_best.alloc(bp_blocks, st);
@@ -1343,6 +1544,7 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
   A.ibits = ibits.p;
   A.jbits = jbits.p;
   A.ci_by_index = ci_by_index.p;
+  A.ci_fast = ci_fast.p;
   A.block_best = bp_best.p;
   A.bar = bp_bar.p;
   A.state = bp_state.p;
@@ -1364,8 +1566,8 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
   if (profile) {
     long long hp[16];
     copy_to_host(ctx, hp, prof.p, sizeof(hp));
-    std::fprintf(stderr, "[eval] max cycles: pre %lld walk2 %lld walk3 %lld trail %lld\n", hp[10],
-                 hp[11], hp[12], hp[13]);
+    std::fprintf(stderr, "[eval] block-0 screened candidates %lld over %lld rounds; filter max %lld, "
+                 "filter barrier sum %lld, seg-1 candidates %lld\n", hp[10], hp[11], hp[12], hp[13], hp[14]);
     std::fprintf(stderr,
                  "[pass] m=%d attempts=%lld pairs=%lld cyc: filter %lld compact %lld pairs %lld "
                  "wait %lld publish %lld barrier %lld | max ci-load %lld max eval %lld\n",

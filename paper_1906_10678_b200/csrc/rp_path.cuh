@@ -39,6 +39,15 @@ struct WikDev {
   long long* prof;  // RP_PROFILE_PASS section maxima (null otherwise)
 };
 
+/// Segment-1 record of the coaxial, limit-free fast path (what the pair
+/// tests read): 48 bytes instead of CiData's frame-carrying 152.
+struct CiFast {
+  int i;
+  int ok;
+  double move1;
+  V3 p1;
+};
+
 struct CiData {
   int i;
   int ok;  // walk1 (and offset link) clear
@@ -97,6 +106,7 @@ struct BpArgs {
   uint32_t* ibits;
   uint32_t* jbits;
   CiData* ci_by_index;
+  CiFast* ci_fast;  // fast-path twin of ci_by_index
   WikBest* block_best;
   unsigned* bar;  // [2] barrier count + generation
   int* state;     // [4] found, failed_index, ok

@@ -32,6 +32,7 @@ struct Planner {
   DevBuf<uint32_t> ibits, jbits;
   DevBuf<int> cj, counts;
   DevBuf<CiData> ci, ci_by_index;
+  DevBuf<CiFast> ci_fast;
   DevBuf<WikBest> block_best;
   DevBuf<unsigned> done;
   DevBuf<WikResult> result;
