@@ -378,6 +378,23 @@ rp_status rp_mean_polyline_deviation(rp_ctx* ctx, const double* pts, int32_t n_p
 /* [folded_pose, src/path_planner.cpp:711-727] */
 rp_status rp_folded_pose(rp_ctx* ctx, const rp_arm* arm, rp_pose* out);
 
+/* [validate_plan / check_pose, src/validate.cpp:20-108] independent re-check of
+ * every pose of a delivered plan on the device (collision, segment lengths,
+ * joint limits, self-collision, tracked-point placement, smoothness against
+ * the recorded relaxation, unfold seam). The issues (the reference's wording,
+ * reference order) are '\n'-joined into `issues` (cap bytes incl. NUL;
+ * out->issues_bytes = the size needed). */
+typedef struct rp_validation {
+  int32_t ok;
+  int32_t poses_checked;
+  int32_t relax_events;
+  int32_t n_issues;
+  int64_t issues_bytes;
+} rp_validation;
+rp_status rp_validate_plan(rp_ctx* ctx, const rp_arm* arm, const rp_grid* g, const rp_plan* plan,
+                           const rp_reach_params* rp, const rp_path_params* pp, rp_validation* out,
+                           char* issues, int64_t cap);
+
 rp_status rp_plan_get_info(const rp_plan* p, rp_plan_info* info);
 rp_status rp_plan_waypoints(const rp_plan* p, double* xyz, int32_t cap);
 rp_status rp_plan_relax(const rp_plan* p, double* relax, int32_t cap);

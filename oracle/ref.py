@@ -74,6 +74,11 @@ def lib():
         L.ref_plan_pose.argtypes = [vp, C.c_int, C.c_int, P(abi.Pose), vp, C.c_int]
         L.ref_plan_note.argtypes = [vp, C.c_int, C.c_char_p, C.c_int]
         L.ref_validate_plan.argtypes = [vp, vp, P(abi.PathParams)]
+        L.ref_validate_report.argtypes = [vp, vp, P(abi.PathParams), P(C.c_int32), P(C.c_int32),
+                                          P(C.c_int32), C.c_char_p, C.c_int]
+        L.ref_plan_create.argtypes = [C.c_char_p, vp, P(abi.Pose), vp, C.c_int, vp, C.c_int,
+                                      P(abi.Pose), C.c_int]
+        L.ref_plan_create.restype = vp
         L.ref_waypoint_ik.argtypes = [vp, P(C.c_double), P(abi.Pose), C.c_double, vp, vp,
                                       vp, P(abi.PathParams), P(C.c_int32), P(abi.Pose), vp, C.c_int]
         L.ref_mean_polyline_deviation.argtypes = [vp, C.c_int, vp, C.c_int]
@@ -324,7 +329,34 @@ class RefProblem:
         pp = pp or abi.make_path_params()
         return lib().ref_validate_plan(self.h, plan.ptr, C.byref(pp))
 
+    def validate_report(self, plan: RefPlan, pp=None) -> dict:
+        """validate_plan's whole ValidationReport (src/validate.cpp:53-108)."""
+        pp = pp or abi.make_path_params()
+        ok, pc, re = C.c_int32(), C.c_int32(), C.c_int32()
+        need = lib().ref_validate_report(self.h, plan.ptr, C.byref(pp), C.byref(ok), C.byref(pc),
+                                         C.byref(re), None, 0)
+        buf = C.create_string_buffer(max(1, need))
+        lib().ref_validate_report(self.h, plan.ptr, C.byref(pp), C.byref(ok), C.byref(pc),
+                                  C.byref(re), buf, len(buf))
+        text = buf.value.decode()
+        return {"ok": bool(ok.value), "poses_checked": pc.value, "relax_events": re.value,
+                "issues": text.split("\n") if text else []}
+
 
 def abi_bounds(scene):
     from paper_1906_10678_b200 import scenes
     return scenes.BOUNDS_MIN, scenes.BOUNDS_MAX
+
+
+def plan_create(kind, waypoints, poses, relax=None, unfold=(), pose_wps=None, wps_per_pose=0):
+    """A reference PathPlan from host data (abi.Pose lists)."""
+    w = np.ascontiguousarray(waypoints, np.float64).reshape(-1, 3)
+    n = len(w)
+    parr = (abi.Pose * max(1, n))(*poses)
+    uarr = (abi.Pose * max(1, len(unfold)))(*unfold)
+    r = np.ascontiguousarray(relax if relax is not None else np.ones(n), np.float64)
+    pw = None if pose_wps is None else np.ascontiguousarray(pose_wps, np.float64)
+    ptr = lib().ref_plan_create(kind.encode(), w.ctypes.data, parr,
+                                None if pw is None else pw.ctypes.data, wps_per_pose,
+                                r.ctypes.data, n, uarr, len(unfold))
+    return RefPlan(ptr)

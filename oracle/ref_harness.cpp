@@ -635,4 +635,39 @@ int ref_validate_plan(const ref_problem* p, const ref_plan* plan, const rp_path_
   return static_cast<int>(r.issues.size());
 }
 
+/// validate_plan (src/validate.cpp:53-108) with the whole report: issues
+/// joined by '\n' into buf; returns the byte count needed (incl. NUL).
+int ref_validate_report(const ref_problem* p, const ref_plan* plan, const rp_path_params* pp,
+                        int32_t* ok, int32_t* poses_checked, int32_t* relax_events, char* buf,
+                        int cap) {
+  const ValidationReport r = validate_plan(p->arm, p->grid, plan->plan, p->rp, to_pp(*pp));
+  *ok = r.ok ? 1 : 0;
+  *poses_checked = r.poses_checked;
+  *relax_events = r.relax_events;
+  std::string all;
+  for (size_t k = 0; k < r.issues.size(); ++k) all += (k ? "\n" : "") + r.issues[k];
+  if (buf && cap > 0) {
+    const size_t n = std::min(all.size(), static_cast<size_t>(cap - 1));
+    std::memcpy(buf, all.data(), n);
+    buf[n] = 0;
+  }
+  return static_cast<int>(all.size() + 1);
+}
+
+/// A PathPlan from plain data (plan files / corrupted copies in tests).
+ref_plan* ref_plan_create(const char* kind, const double* waypoints, const rp_pose* poses,
+                          const double* pose_wps, int wps_per_pose, const double* relax, int n,
+                          const rp_pose* unfold, int n_unfold) {
+  auto* out = new ref_plan();
+  out->plan.provenance.kind = kind ? kind : "";
+  for (int k = 0; k < n; ++k) {
+    out->plan.waypoints.push_back(v3(waypoints + 3 * k));
+    out->plan.poses.push_back(
+        from_pose(poses[k], pose_wps ? pose_wps + 3 * static_cast<size_t>(k) * wps_per_pose : nullptr));
+    out->plan.provenance.relax_per_waypoint.push_back(relax ? relax[k] : 1.0);
+  }
+  for (int k = 0; k < n_unfold; ++k) out->plan.unfold_prefix.push_back(from_pose(unfold[k], nullptr));
+  return out;
+}
+
 }  // extern "C"

@@ -137,6 +137,11 @@ class BatchResult(C.Structure):
     ]
 
 
+class Validation(C.Structure):
+    _fields_ = [("ok", C.c_int32), ("poses_checked", C.c_int32), ("relax_events", C.c_int32),
+                ("n_issues", C.c_int32), ("issues_bytes", C.c_int64)]
+
+
 # ---- defaults mirroring the reference member initialisers ----------------------
 
 def make_arm(lengths, root=(0.0, 0.0, 0.0), arm_radius=0.0) -> Arm:

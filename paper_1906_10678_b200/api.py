@@ -118,6 +118,8 @@ def lib():
         "rp_plan_create": ([C.c_char_p, d3, P(abi.Pose), d3, C.c_int32, P(abi.Pose), C.c_int32,
                             P(vp)], C.c_int32),
         "rp_plan_destroy": ([vp], C.c_int32),
+        "rp_validate_plan": ([vp, P(abi.Arm), vp, vp, P(abi.ReachParams), P(abi.PathParams),
+                              P(abi.Validation), C.c_char_p, C.c_int64], C.c_int32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -522,3 +524,31 @@ def header_symbols() -> list:
     hdr = os.path.join(os.path.dirname(HERE), "include", "reachplan_b200.h")
     text = open(hdr).read()
     return sorted(set(re.findall(r"\b(rp_[a-z0-9_]+)\s*\(", text)))
+
+
+def validate_plan(ctx, arm, grid, plan, rp, pp=None) -> dict:
+    """validate_plan (src/validate.cpp:53-108) on the device: the report."""
+    pp = pp or abi.make_path_params()
+    v = abi.Validation()
+    _check(lib().rp_validate_plan(ctx.h, C.byref(arm), grid.h, plan.h, C.byref(rp), C.byref(pp),
+                                  C.byref(v), None, 0))
+    buf = C.create_string_buffer(max(1, int(v.issues_bytes)))
+    _check(lib().rp_validate_plan(ctx.h, C.byref(arm), grid.h, plan.h, C.byref(rp), C.byref(pp),
+                                  C.byref(v), buf, len(buf)))
+    text = buf.value.decode()
+    return {"ok": bool(v.ok), "poses_checked": v.poses_checked, "relax_events": v.relax_events,
+            "issues": text.split("\n") if text else []}
+
+
+def plan_create(kind, waypoints, poses, relax=None, unfold=(), n_samples=8) -> "Plan":
+    """A plan handle from host data (rp_plan_create): poses / unfold are abi.Pose."""
+    w = np.ascontiguousarray(waypoints, np.float64).reshape(-1, 3)
+    n = len(w)
+    parr = (abi.Pose * max(1, n))(*poses)
+    uarr = (abi.Pose * max(1, len(unfold)))(*unfold)
+    r = np.ascontiguousarray(relax if relax is not None else np.ones(n), np.float64)
+    h = C.c_void_p()
+    _check(lib().rp_plan_create(kind.encode(), w.ctypes.data_as(C.POINTER(C.c_double)), parr,
+                                r.ctypes.data_as(C.POINTER(C.c_double)), n, uarr, len(unfold),
+                                C.byref(h)))
+    return Plan(h, n_samples)

@@ -1106,6 +1106,91 @@ __global__ void k_seq_smooth(const DevPose* __restrict__ seq, int count, double 
     atomicExch(rough, 1);
 }
 
+// ---------------------------------------------------------------------------
+// validate_plan / check_pose (src/validate.cpp:20-108): every check of the
+// independent plan validator as one launch, one thread per item: the poses
+// of the executable sequence, the tracked point at each waypoint, each
+// consecutive pose pair's smoothness and the unfold seam. The host turns
+// the flags (and the measured values the messages print) into the report.
+
+struct VPose {
+  double len_diff[4];  // |s_j| - L_j
+  unsigned char len_bad[4], off_hit[4], seg_hit[4];
+  unsigned char limits_bad, self_bad, _pad[6];
+};
+
+struct VArgs {
+  rpd::GridView g;
+  ArmDev arm;
+  const DevPose* seq;  // full_sequence()
+  int nseq;
+  const DevPose* poses;  // plan.poses (tracked points)
+  const V3* wps;
+  const double* relax;       // per waypoint
+  const double* pair_relax;  // per sequence pair
+  int m;
+  int n;
+  double s4tol, eps_wp, j1, j2;
+  int has_unfold;
+  VPose* out_pose;
+  double* out_dist;     // per waypoint: tracked-point distance
+  uint8_t* out_wp_bad;  // per waypoint
+  uint8_t* out_pair_bad;
+  uint8_t* out_seam_bad;
+};
+
+__global__ void k_validate_plan(VArgs a) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < a.nseq) {
+    const DevPose& p = a.seq[t];
+    VPose r{};
+    for (int j = 0; j < p.nseg; ++j) {
+      const double len = rpd::norm(p.seg[j]);
+      const double expected = a.arm.L[j];
+      const double tol = (j == 3) ? a.s4tol : 1e-9 * fmax(1.0, expected);
+      r.len_diff[j] = len - expected;
+      r.len_bad[j] = fabs(len - expected) > tol ? 1 : 0;
+      V3 from = p.joints[j];
+      if (p.has_elbows) {
+        const int n_off = max(1, static_cast<int>(ceil(rpd::norm(p.elbows[j] - p.joints[j]) /
+                                                      fmax(1e-12, expected / a.n))));
+        r.off_hit[j] = rpd::walk_clear(a.g, p.joints[j], p.elbows[j], n_off) ? 0 : 1;
+        from = p.elbows[j];
+      }
+      r.seg_hit[j] = rpd::walk_clear(a.g, from, p.joints[j + 1], a.n) ? 0 : 1;
+    }
+    r.limits_bad = pose_limits_ok(a.arm, p) ? 0 : 1;
+    r.self_bad = pose_self_free(p, 2.0 * a.arm.arm_radius) ? 0 : 1;
+    a.out_pose[t] = r;
+    return;
+  }
+  t -= a.nseq;
+  if (t < a.m) {
+    const DevPose& p = a.poses[t];
+    const int tj = p.nseg < 3 ? p.nseg : 3;  // PoseChain::tracked_point
+    const double dist = rpd::norm(p.joints[tj] - a.wps[t]);
+    a.out_dist[t] = dist;
+    a.out_wp_bad[t] = dist > a.eps_wp * a.relax[t] + 1e-9 ? 1 : 0;
+    return;
+  }
+  t -= a.m;
+  if (t < a.nseq - 1) {
+    const DevPose& p = a.seq[t];
+    const DevPose& q = a.seq[t + 1];
+    const double f = a.pair_relax[t];
+    const bool ok = rpd::norm(q.joints[1] - p.joints[1]) <= a.j1 * f + 1e-12 &&
+                    rpd::norm(q.joints[2] - p.joints[2]) <= a.j2 * f + 1e-12;
+    a.out_pair_bad[t] = ok ? 0 : 1;
+    return;
+  }
+  t -= (a.nseq > 0 ? a.nseq - 1 : 0);
+  if (t == 0 && a.has_unfold) {
+    const DevPose& u = a.seq[a.nseq - a.m];  // unfold.back() sits just before poses[1]
+    const DevPose& p0 = a.poses[0];
+    *a.out_seam_bad = rpd::norm(u.joints[u.nseg] - p0.joints[p0.nseg]) > 1e-9 ? 1 : 0;
+  }
+}
+
 /// pose_clear / pose_valid for a batch (replan collide scan).
 __global__ void k_pose_check(rpd::GridView g, ArmDev arm, const DevPose* __restrict__ poses, int count,
                              int n, double spacing, int full, int* __restrict__ first_bad) {
@@ -1847,6 +1932,126 @@ std::vector<long long> Planner::rank_by_deviation(rp_solution_set* set,
 }  // namespace rp
 
 using namespace rp;
+
+/// validate_plan (src/validate.cpp:53-108): every check on the device
+/// (k_validate_plan), the report assembled here in the reference's order
+/// and wording.
+extern "C" rp_status rp_validate_plan(rp_ctx* ctx, const rp_arm* arm, const rp_grid* g,
+                                      const rp_plan* plan, const rp_reach_params* rp,
+                                      const rp_path_params* pp, rp_validation* out, char* issues,
+                                      int64_t cap) {
+  return guarded([&] {
+    const PP ppr = resolve_path_params(*pp, *arm, *rp);
+    const int n = rp->n_samples;
+    const double s4tol = resolved_epsilon(*arm, *rp) + 1e-9;
+    std::vector<std::string> msgs;
+    int poses_checked = 0, relax_events = 0;
+    const size_t m = plan->waypoints.size();
+    if (plan->poses.size() != m) {
+      msgs.push_back("waypoint and pose counts differ");
+    } else if (plan->relax.size() != m) {
+      msgs.push_back("relaxation record does not cover every waypoint");
+    } else {
+      const auto seq = plan->full_sequence();
+      const int nseq = static_cast<int>(seq.size());
+      cudaStream_t st = ctx->stream;
+      std::vector<DevPose> hseq, hposes;
+      for (const HostPose* p : seq) hseq.push_back(to_dev(*p));
+      for (const HostPose& p : plan->poses) hposes.push_back(to_dev(p));
+      const size_t unfold_len = plan->unfold.empty() ? 0 : plan->unfold.size() - 1;
+      auto wp_relax = [&](size_t k) {
+        if (k < unfold_len) return 1.0;
+        const size_t wp = k - unfold_len;
+        return wp < plan->relax.size() ? plan->relax[wp] : 1.0;
+      };
+      std::vector<double> pair_relax;
+      for (int k = 0; k + 1 < nseq; ++k) pair_relax.push_back(std::max(wp_relax(k), wp_relax(k + 1)));
+      DevBuf<DevPose> dseq(std::max(1, nseq), st), dposes(std::max<size_t>(1, m), st);
+      DevBuf<V3> dw(std::max<size_t>(1, m), st);
+      DevBuf<double> drelax(std::max<size_t>(1, m), st), dpair(std::max<size_t>(1, pair_relax.size()), st),
+          ddist(std::max<size_t>(1, m), st);
+      DevBuf<VPose> dout(std::max(1, nseq), st);
+      DevBuf<uint8_t> dflags(m + pair_relax.size() + 2, st);
+      if (nseq) copy_to_device(ctx, dseq.p, hseq.data(), nseq * sizeof(DevPose));
+      if (m) {
+        copy_to_device(ctx, dposes.p, hposes.data(), m * sizeof(DevPose));
+        copy_to_device(ctx, dw.p, plan->waypoints.data(), m * sizeof(V3));
+        copy_to_device(ctx, drelax.p, plan->relax.data(), m * sizeof(double));
+      }
+      if (!pair_relax.empty())
+        copy_to_device(ctx, dpair.p, pair_relax.data(), pair_relax.size() * sizeof(double));
+      dflags.zero();
+      VArgs a{};
+      a.g = g->view();
+      a.arm = make_arm_dev(*arm);
+      a.seq = dseq.p;
+      a.nseq = nseq;
+      a.poses = dposes.p;
+      a.wps = dw.p;
+      a.relax = drelax.p;
+      a.pair_relax = dpair.p;
+      a.m = static_cast<int>(m);
+      a.n = n;
+      a.s4tol = s4tol;
+      a.eps_wp = ppr.eps_wp;
+      a.j1 = ppr.j1;
+      a.j2 = ppr.j2;
+      a.has_unfold = plan->unfold.empty() ? 0 : 1;
+      a.out_pose = dout.p;
+      a.out_dist = ddist.p;
+      a.out_wp_bad = dflags.p;
+      a.out_pair_bad = dflags.p + m;
+      a.out_seam_bad = dflags.p + m + pair_relax.size();
+      const int items = nseq + static_cast<int>(m) + static_cast<int>(pair_relax.size()) + 1;
+      launch(ctx, "validate", k_validate_plan, dim3(nblk(items, 64)), dim3(64), 0, a);
+      std::vector<VPose> vp(nseq);
+      std::vector<double> dist(m);
+      std::vector<uint8_t> flags(m + pair_relax.size() + 2);
+      if (nseq) copy_to_host(ctx, vp.data(), dout.p, nseq * sizeof(VPose));
+      if (m) copy_to_host(ctx, dist.data(), ddist.p, m * sizeof(double));
+      copy_to_host(ctx, flags.data(), dflags.p, flags.size());
+      for (int k = 0; k < nseq; ++k) {
+        const std::string label = "pose " + std::to_string(k);
+        ++poses_checked;
+        for (int j = 0; j < seq[k]->nseg; ++j) {
+          if (vp[k].len_bad[j])
+            msgs.push_back(label + ": segment " + std::to_string(j + 1) + " length off by " +
+                           std::to_string(vp[k].len_diff[j]));
+          if (seq[k]->has_elbows && vp[k].off_hit[j])
+            msgs.push_back(label + ": offset link " + std::to_string(j + 1) + " collides");
+          if (vp[k].seg_hit[j])
+            msgs.push_back(label + ": segment " + std::to_string(j + 1) + " collides");
+        }
+        if (vp[k].limits_bad) msgs.push_back(label + ": joint limits violated");
+        if (vp[k].self_bad) msgs.push_back(label + ": self-collision");
+      }
+      for (size_t k = 0; k < m; ++k) {
+        if (plan->relax[k] > 1.0) ++relax_events;
+        if (flags[k])
+          msgs.push_back("waypoint " + std::to_string(k) + ": tracked point off by " +
+                         std::to_string(dist[k]));
+      }
+      for (size_t k = 0; k < pair_relax.size(); ++k)
+        if (flags[m + k])
+          msgs.push_back("pose pair " + std::to_string(k) + "-" + std::to_string(k + 1) +
+                         " exceeds the recorded smoothness bounds");
+      if (!plan->unfold.empty() && flags[m + pair_relax.size()])
+        msgs.push_back("unfold prefix does not end at the root-waypoint pose");
+    }
+    std::string all;
+    for (size_t k = 0; k < msgs.size(); ++k) all += (k ? "\n" : "") + msgs[k];
+    out->ok = msgs.empty() ? 1 : 0;
+    out->poses_checked = poses_checked;
+    out->relax_events = relax_events;
+    out->n_issues = static_cast<int32_t>(msgs.size());
+    out->issues_bytes = static_cast<int64_t>(all.size()) + 1;
+    if (issues && cap > 0) {
+      const size_t c = std::min(all.size(), static_cast<size_t>(cap - 1));
+      std::memcpy(issues, all.data(), c);
+      issues[c] = 0;
+    }
+  });
+}
 
 extern "C" rp_status rp_exact_refine(rp_ctx* ctx, const rp_arm* arm, const rp_pose* approx,
                                      const double target[3], int32_t variant, rp_pose* out) {
