@@ -395,6 +395,43 @@ rp_status rp_validate_plan(rp_ctx* ctx, const rp_arm* arm, const rp_grid* g, con
                            const rp_reach_params* rp, const rp_path_params* pp, rp_validation* out,
                            char* issues, int64_t cap);
 
+/* ---- execution simulator [inc/reachplan/motion.hpp] ------------------------- */
+/* [MotionParams, motion.hpp:9-19]; objective: 0 time-of-arrival (default) */
+typedef struct rp_motion_params {
+  double v_w;               /* 0.05 m/s */
+  double sample_rate;       /* 100 Hz */
+  double max_joint_rate;    /* 30 deg/s in rad/s */
+  double arrival_tolerance; /* 0.01 m */
+  int32_t objective;
+  int32_t _pad;
+} rp_motion_params;
+/* [ExecutionTick + JointAngles + JointRates, motion.hpp:28-41] */
+typedef struct rp_tick {
+  double time;
+  double azimuth[RP_MAX_SEGMENTS], elevation[RP_MAX_SEGMENTS];
+  uint8_t degenerate[RP_MAX_SEGMENTS];
+  int32_t n_joints;
+  double tracked[3];
+  int32_t active;       /* active_waypoint_index */
+  int32_t n_rates;      /* 0 for the first tick (no command yet) */
+  int32_t clamped;
+  int32_t _pad;
+  double azimuth_rate[RP_MAX_SEGMENTS], elevation_rate[RP_MAX_SEGMENTS];
+} rp_tick;
+typedef struct rp_trace rp_trace;
+void rp_motion_params_init(rp_motion_params* mp);
+/* [simulate_execution, src/motion.cpp:62-141] grid (nullable) = re-check every
+ * tick for collision on the device (RP_E_EXECUTION_COLLISION at the first
+ * colliding tick); RP_E_TIMEOUT when the tick budget runs out. */
+rp_status rp_simulate_execution(rp_ctx* ctx, const rp_arm* arm, const rp_plan* plan,
+                                const rp_motion_params* mp, const rp_grid* grid, rp_trace** out);
+rp_status rp_trace_info(const rp_trace* t, int64_t* n_ticks, int64_t* n_overshoot,
+                        int64_t* n_clamp, int32_t* reached_goal);
+rp_status rp_trace_ticks(const rp_trace* t, int64_t first, int64_t count, rp_tick* out);
+/* overshoot_events / clamp_events tick indices (sizes from rp_trace_info) */
+rp_status rp_trace_events(const rp_trace* t, int32_t* overshoot, int32_t* clamp);
+rp_status rp_trace_destroy(rp_trace* t);
+
 rp_status rp_plan_get_info(const rp_plan* p, rp_plan_info* info);
 rp_status rp_plan_waypoints(const rp_plan* p, double* xyz, int32_t cap);
 rp_status rp_plan_relax(const rp_plan* p, double* relax, int32_t cap);

@@ -79,6 +79,9 @@ def lib():
         L.ref_plan_create.argtypes = [C.c_char_p, vp, P(abi.Pose), vp, C.c_int, vp, C.c_int,
                                       P(abi.Pose), C.c_int]
         L.ref_plan_create.restype = vp
+        L.ref_simulate.argtypes = [vp, vp, P(abi.MotionParams), C.c_int, P(abi.Tick), C.c_int64,
+                                   P(C.c_int64), vp, P(C.c_int32), vp, P(C.c_int32), P(C.c_int32),
+                                   C.c_char_p, C.c_int]
         L.ref_waypoint_ik.argtypes = [vp, P(C.c_double), P(abi.Pose), C.c_double, vp, vp,
                                       vp, P(abi.PathParams), P(C.c_int32), P(abi.Pose), vp, C.c_int]
         L.ref_mean_polyline_deviation.argtypes = [vp, C.c_int, vp, C.c_int]
@@ -328,6 +331,22 @@ class RefProblem:
     def validate(self, plan: RefPlan, pp=None) -> int:
         pp = pp or abi.make_path_params()
         return lib().ref_validate_plan(self.h, plan.ptr, C.byref(pp))
+
+    def simulate(self, plan: RefPlan, mp=None, use_grid=True, cap=400000):
+        """simulate_execution: (status, trace dict or error message)."""
+        mp = mp or abi.make_motion_params()
+        ticks = (abi.Tick * cap)()
+        over = np.zeros(cap, np.int32)
+        clamp = np.zeros(cap, np.int32)
+        nt, no, nc, reached = C.c_int64(), C.c_int32(), C.c_int32(), C.c_int32()
+        msg = C.create_string_buffer(512)
+        rc = lib().ref_simulate(self.h, plan.ptr, C.byref(mp), 1 if use_grid else 0, ticks, cap,
+                                C.byref(nt), over.ctypes.data, C.byref(no), clamp.ctypes.data,
+                                C.byref(nc), C.byref(reached), msg, 512)
+        if rc != 0:
+            return rc, msg.value.decode()
+        return 0, {"ticks": list(ticks)[:nt.value], "overshoot": over[:no.value].tolist(),
+                   "clamp": clamp[:nc.value].tolist(), "reached": bool(reached.value)}
 
     def validate_report(self, plan: RefPlan, pp=None) -> dict:
         """validate_plan's whole ValidationReport (src/validate.cpp:53-108)."""

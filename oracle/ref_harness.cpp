@@ -10,6 +10,7 @@
 #include "reachplan_b200.h"
 
 #include "reachplan/io.hpp"
+#include "reachplan/motion.hpp"
 #include "reachplan/oracle.hpp"
 #include "reachplan/path_planner.hpp"
 #include "reachplan/pipeline.hpp"
@@ -652,6 +653,58 @@ int ref_validate_report(const ref_problem* p, const ref_plan* plan, const rp_pat
     buf[n] = 0;
   }
   return static_cast<int>(all.size() + 1);
+}
+
+/// simulate_execution (src/motion.cpp:62-141): the trace into rp_tick
+/// records (caller arrays sized by cap), or the error status + message.
+int ref_simulate(const ref_problem* p, const ref_plan* plan, const rp_motion_params* mp,
+                 int use_grid, rp_tick* ticks, int64_t cap, int64_t* n_ticks, int32_t* overshoot,
+                 int32_t* n_over, int32_t* clamp, int32_t* n_clamp, int32_t* reached, char* msg,
+                 int msgcap) {
+  MotionParams m;
+  m.v_w = mp->v_w;
+  m.sample_rate = mp->sample_rate;
+  m.max_joint_rate = mp->max_joint_rate;
+  m.arrival_tolerance = mp->arrival_tolerance;
+  try {
+    const ExecutionTrace tr =
+        simulate_execution(p->arm, plan->plan, m, use_grid ? &p->grid : nullptr);
+    *n_ticks = static_cast<int64_t>(tr.ticks.size());
+    for (size_t k = 0; k < tr.ticks.size() && static_cast<int64_t>(k) < cap; ++k) {
+      const ExecutionTick& t = tr.ticks[k];
+      rp_tick& o = ticks[k];
+      std::memset(&o, 0, sizeof(o));
+      o.time = t.time;
+      o.n_joints = t.q.joint_count();
+      for (int j = 0; j < o.n_joints; ++j) {
+        o.azimuth[j] = t.q.azimuth[j];
+        o.elevation[j] = t.q.elevation[j];
+        o.degenerate[j] = t.q.degenerate[j];
+      }
+      put3(o.tracked, t.tracked_point);
+      o.active = t.active_waypoint_index;
+      o.n_rates = static_cast<int32_t>(t.commanded.azimuth_rate.size());
+      o.clamped = t.commanded.clamped ? 1 : 0;
+      for (int j = 0; j < o.n_rates; ++j) {
+        o.azimuth_rate[j] = t.commanded.azimuth_rate[j];
+        o.elevation_rate[j] = t.commanded.elevation_rate[j];
+      }
+    }
+    *n_over = static_cast<int32_t>(tr.overshoot_events.size());
+    *n_clamp = static_cast<int32_t>(tr.clamp_events.size());
+    for (size_t k = 0; k < tr.overshoot_events.size() && static_cast<int64_t>(k) < cap; ++k)
+      overshoot[k] = tr.overshoot_events[k];
+    for (size_t k = 0; k < tr.clamp_events.size() && static_cast<int64_t>(k) < cap; ++k)
+      clamp[k] = tr.clamp_events[k];
+    *reached = tr.reached_goal ? 1 : 0;
+    return 0;
+  } catch (const Error& e) {
+    if (msg && msgcap > 0) {
+      std::strncpy(msg, e.what(), msgcap - 1);
+      msg[msgcap - 1] = 0;
+    }
+    return status_of(e);
+  }
 }
 
 /// A PathPlan from plain data (plan files / corrupted copies in tests).

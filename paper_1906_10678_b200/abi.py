@@ -26,6 +26,9 @@ RP_E_EMPTY_CONE = 5
 RP_E_NO_SOLUTION = 6
 RP_E_NO_PATH = 7
 RP_E_INFEASIBLE_TIMING = 8
+RP_E_EXECUTION_COLLISION = 9
+RP_E_TIMEOUT = 10
+RP_E_PARSE_ERROR = 11
 RP_E_CUDA = 100
 RP_E_INTERNAL = 101
 
@@ -140,6 +143,31 @@ class BatchResult(C.Structure):
 class Validation(C.Structure):
     _fields_ = [("ok", C.c_int32), ("poses_checked", C.c_int32), ("relax_events", C.c_int32),
                 ("n_issues", C.c_int32), ("issues_bytes", C.c_int64)]
+
+
+class MotionParams(C.Structure):
+    _fields_ = [("v_w", C.c_double), ("sample_rate", C.c_double), ("max_joint_rate", C.c_double),
+                ("arrival_tolerance", C.c_double), ("objective", C.c_int32), ("_pad", C.c_int32)]
+
+
+class Tick(C.Structure):
+    _fields_ = [("time", C.c_double), ("azimuth", C.c_double * RP_MAX_SEGMENTS),
+                ("elevation", C.c_double * RP_MAX_SEGMENTS),
+                ("degenerate", C.c_uint8 * RP_MAX_SEGMENTS), ("n_joints", C.c_int32),
+                ("tracked", C.c_double * 3), ("active", C.c_int32), ("n_rates", C.c_int32),
+                ("clamped", C.c_int32), ("_pad", C.c_int32),
+                ("azimuth_rate", C.c_double * RP_MAX_SEGMENTS),
+                ("elevation_rate", C.c_double * RP_MAX_SEGMENTS)]
+
+
+def make_motion_params(v_w=0.05, sample_rate=100.0, max_joint_rate_deg=30.0,
+                       arrival_tolerance=0.01) -> MotionParams:
+    """MotionParams defaults (inc/reachplan/motion.hpp:9-15)."""
+    m = MotionParams()
+    m.v_w, m.sample_rate = v_w, sample_rate
+    m.max_joint_rate = deg2rad(max_joint_rate_deg)
+    m.arrival_tolerance = arrival_tolerance
+    return m
 
 
 # ---- defaults mirroring the reference member initialisers ----------------------

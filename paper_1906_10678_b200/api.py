@@ -120,6 +120,11 @@ def lib():
         "rp_plan_destroy": ([vp], C.c_int32),
         "rp_validate_plan": ([vp, P(abi.Arm), vp, vp, P(abi.ReachParams), P(abi.PathParams),
                               P(abi.Validation), C.c_char_p, C.c_int64], C.c_int32),
+        "rp_simulate_execution": ([vp, P(abi.Arm), vp, P(abi.MotionParams), vp, P(vp)], C.c_int32),
+        "rp_trace_info": ([vp, P(C.c_int64), P(C.c_int64), P(C.c_int64), P(C.c_int32)], C.c_int32),
+        "rp_trace_ticks": ([vp, C.c_int64, C.c_int64, P(abi.Tick)], C.c_int32),
+        "rp_trace_events": ([vp, vp, vp], C.c_int32),
+        "rp_trace_destroy": ([vp], C.c_int32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -552,3 +557,24 @@ def plan_create(kind, waypoints, poses, relax=None, unfold=(), n_samples=8) -> "
                                 r.ctypes.data_as(C.POINTER(C.c_double)), n, uarr, len(unfold),
                                 C.byref(h)))
     return Plan(h, n_samples)
+
+
+def simulate_execution(ctx, arm, plan, mp=None, grid=None) -> dict:
+    """simulate_execution (src/motion.cpp:62-141); raises ReachplanError with
+    the reference's Errc (execution-collision / timeout) like the reference."""
+    mp = mp or abi.make_motion_params()
+    h = C.c_void_p()
+    _check(lib().rp_simulate_execution(ctx.h, C.byref(arm), plan.h, C.byref(mp),
+                                       grid.h if grid is not None else None, C.byref(h)))
+    try:
+        nt, no, nc, reached = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int32()
+        _check(lib().rp_trace_info(h, C.byref(nt), C.byref(no), C.byref(nc), C.byref(reached)))
+        ticks = (abi.Tick * max(1, nt.value))()
+        _check(lib().rp_trace_ticks(h, 0, nt.value, ticks))
+        over = np.zeros(max(1, no.value), np.int32)
+        clamp = np.zeros(max(1, nc.value), np.int32)
+        _check(lib().rp_trace_events(h, over.ctypes.data, clamp.ctypes.data))
+        return {"ticks": list(ticks)[:nt.value], "overshoot": over[:no.value].tolist(),
+                "clamp": clamp[:nc.value].tolist(), "reached": bool(reached.value)}
+    finally:
+        lib().rp_trace_destroy(h)

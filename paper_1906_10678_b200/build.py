@@ -23,7 +23,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-ffp-contract=off",
          "-Xptxas", "-O3", "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"),
          "-I", CSRC]
-SOURCES = ["rp_core.cu", "rp_grid.cu", "rp_reach.cu", "rp_path.cu", "rp_planner.cu"]
+SOURCES = ["rp_core.cu", "rp_grid.cu", "rp_reach.cu", "rp_path.cu", "rp_planner.cu", "rp_motion.cu"]
 
 
 def _compile(src: str) -> str:

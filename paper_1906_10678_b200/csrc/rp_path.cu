@@ -126,34 +126,6 @@ __host__ __device__ inline V3 pose_plane_normal(const DevPose& p) {
   return rpd::normalized(n);
 }
 
-/// vectors_to_joint_angles (src/arm_model.cpp:163-176)
-__host__ __device__ inline bool to_angles(const ArmDev& arm, const DevPose& p, double* az, double* el) {
-  rpd::M3 frame = arm.base;
-  for (int k = 0; k < p.nseg; ++k) {
-    const double len = rpd::norm(p.seg[k]);
-    if (!(len > 0.0)) return false;
-    const rpd::FrameStep st = rpd::advance_frame(frame, p.seg[k] / len);
-    az[k] = st.theta;
-    el[k] = st.phi;
-    frame = rpd::m_mul(rpd::m_mul(frame, rpd::rot_z(st.theta)), rpd::rot_y(st.phi));
-  }
-  return true;
-}
-
-/// joint_angles_to_vectors (src/arm_model.cpp:178-193)
-__host__ __device__ inline DevPose from_angles(const ArmDev& arm, const double* az, const double* el) {
-  DevPose p{};
-  p.nseg = arm.nseg;
-  rpd::M3 frame = arm.base;
-  for (int j = 0; j < arm.nseg; ++j) {
-    frame = rpd::m_mul(rpd::m_mul(frame, rpd::rot_z(az[j])), rpd::rot_y(el[j]));
-    p.seg[j] = arm.L[j] * rpd::m_col(frame, 2);
-    p.qidx[j] = -1;
-  }
-  build_chain(arm, p);
-  return p;
-}
-
 // ---------------------------------------------------------------------------
 // waypoint_ik (src/path_planner.cpp:167-291)
 
