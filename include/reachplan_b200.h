@@ -125,7 +125,8 @@ typedef struct rp_pose {
   int32_t has_elbows;
   int32_t quiver_indices[RP_MAX_SEGMENTS]; /* -1 = free / refined */
   int32_t n_waypoints;
-  int32_t _pad;
+  int32_t no_indices; /* 1: PoseChain::quiver_indices is empty (joint-space /
+                         folded poses), 0: n_segments indices above */
   double s4_length_dev;
   double segments[RP_MAX_SEGMENTS][3];
   double joints[RP_MAX_SEGMENTS + 1][3];

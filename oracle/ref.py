@@ -79,6 +79,8 @@ def lib():
         L.ref_plan_create.argtypes = [C.c_char_p, vp, P(abi.Pose), vp, C.c_int, vp, C.c_int,
                                       P(abi.Pose), C.c_int]
         L.ref_plan_create.restype = vp
+        L.ref_emit_plan.argtypes = [vp, P(C.c_double), C.c_double, C.c_double, C.c_int,
+                                    C.c_char_p, C.c_int64, P(C.c_int64)]
         L.ref_simulate.argtypes = [vp, vp, P(abi.MotionParams), C.c_int, P(abi.Tick), C.c_int64,
                                    P(C.c_int64), vp, P(C.c_int32), vp, P(C.c_int32), P(C.c_int32),
                                    C.c_char_p, C.c_int]
@@ -347,6 +349,20 @@ class RefProblem:
             return rc, msg.value.decode()
         return 0, {"ticks": list(ticks)[:nt.value], "overshoot": over[:no.value].tolist(),
                    "clamp": clamp[:nc.value].tolist(), "reached": bool(reached.value)}
+
+    def emit_plan(self, target=None):
+        """The reference CLI's `plan` output file (emit_plan) for this scene."""
+        target = self.scene.target if target is None else target
+        deg = self.scene.quiver_deg
+        need = C.c_int64()
+        rc = lib().ref_emit_plan(self.h, _d3(target), deg, deg, self.scene.min_per_ring, None, 0,
+                                 C.byref(need))
+        if rc != 0:
+            return rc, None
+        buf = C.create_string_buffer(need.value)
+        lib().ref_emit_plan(self.h, _d3(target), deg, deg, self.scene.min_per_ring, buf,
+                            need.value, C.byref(need))
+        return 0, buf.value.decode()
 
     def validate_report(self, plan: RefPlan, pp=None) -> dict:
         """validate_plan's whole ValidationReport (src/validate.cpp:53-108)."""

@@ -98,6 +98,7 @@ void to_pose(const PoseChain& p, rp_pose* out, double* wps, int cap) {
   std::memset(out, 0, sizeof(*out));
   out->n_segments = p.segment_count();
   out->has_elbows = p.elbows.empty() ? 0 : 1;
+  out->no_indices = p.quiver_indices.empty() ? 1 : 0;
   for (int k = 0; k < RP_MAX_SEGMENTS; ++k)
     out->quiver_indices[k] = k < static_cast<int>(p.quiver_indices.size()) ? p.quiver_indices[k] : -1;
   out->s4_length_dev = p.s4_length_dev;
@@ -115,7 +116,8 @@ PoseChain from_pose(const rp_pose& p, const double* wps) {
   for (int k = 0; k <= p.n_segments; ++k) c.joints.push_back(v3(p.joints[k]));
   if (p.has_elbows)
     for (int k = 0; k < p.n_segments; ++k) c.elbows.push_back(v3(p.elbows[k]));
-  for (int k = 0; k < p.n_segments; ++k) c.quiver_indices.push_back(p.quiver_indices[k]);
+  if (!p.no_indices)
+    for (int k = 0; k < p.n_segments; ++k) c.quiver_indices.push_back(p.quiver_indices[k]);
   c.s4_length_dev = p.s4_length_dev;
   if (wps)
     for (int k = 0; k < p.n_waypoints; ++k) c.waypoints.push_back(v3(wps + 3 * k));
@@ -703,6 +705,39 @@ int ref_simulate(const ref_problem* p, const ref_plan* plan, const rp_motion_par
       std::strncpy(msg, e.what(), msgcap - 1);
       msg[msgcap - 1] = 0;
     }
+    return status_of(e);
+  }
+}
+
+/// The plan file the reference CLI writes for `plan` (cli.cpp:126-137,
+/// 167-185): solve + select + plan_from_reach + emit_plan. Returns the
+/// status; the text goes to buf (size needed in *need).
+int ref_emit_plan(ref_problem* p, const double* target, double elev_deg, double azim_deg, int mpr,
+                  char* buf, int64_t cap, int64_t* need) {
+  try {
+    const SolutionSet set = solve_reach(p->arm, p->quiver, p->grid, v3(target), p->rp);
+    const ChosenPath chosen = select_solution(set);
+    const PathParams pp;
+    PlanFile pf;
+    pf.quiver.elev_step_deg = elev_deg;
+    pf.quiver.equator_azim_step_deg = azim_deg;
+    pf.quiver.min_per_ring = mpr;
+    pf.reach = p->rp;
+    pf.path = pp.resolved(p->arm, p->rp);
+    pf.arm = p->arm;
+    pf.chosen = chosen;
+    pf.plan = plan_from_reach(p->arm, p->quiver, p->grid, chosen, set, v3(target), p->rp, pp);
+    pf.stats = set.stats;
+    pf.stats.wall_ms = 0.0;
+    const std::string text = emit_plan(pf);
+    *need = static_cast<int64_t>(text.size()) + 1;
+    if (buf && cap > 0) {
+      const size_t n = std::min(text.size(), static_cast<size_t>(cap - 1));
+      std::memcpy(buf, text.data(), n);
+      buf[n] = 0;
+    }
+    return 0;
+  } catch (const Error& e) {
     return status_of(e);
   }
 }

@@ -97,7 +97,7 @@ class Pose(C.Structure):
     _fields_ = [
         ("n_segments", C.c_int32), ("has_elbows", C.c_int32),
         ("quiver_indices", C.c_int32 * RP_MAX_SEGMENTS), ("n_waypoints", C.c_int32),
-        ("_pad", C.c_int32), ("s4_length_dev", C.c_double),
+        ("no_indices", C.c_int32), ("s4_length_dev", C.c_double),
         ("segments", D3 * RP_MAX_SEGMENTS), ("joints", D3 * (RP_MAX_SEGMENTS + 1)),
         ("elbows", D3 * RP_MAX_SEGMENTS),
     ]

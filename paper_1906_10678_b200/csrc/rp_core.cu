@@ -212,6 +212,7 @@ void to_abi(const HostPose& p, rp_pose* out, double* wps, int cap) {
   std::memset(out, 0, sizeof(*out));
   out->n_segments = p.nseg;
   out->has_elbows = p.has_elbows ? 1 : 0;
+  out->no_indices = p.no_qidx ? 1 : 0;
   for (int k = 0; k < 4; ++k) out->quiver_indices[k] = k < p.nseg ? p.qidx[k] : -1;
   out->s4_length_dev = p.s4dev;
   for (int k = 0; k < p.nseg; ++k) {
@@ -242,6 +243,7 @@ HostPose from_abi(const rp_pose& p, const double* wps) {
   HostPose h;
   h.nseg = p.n_segments;
   h.has_elbows = p.has_elbows != 0;
+  h.no_qidx = p.no_indices != 0;
   for (int k = 0; k < p.n_segments; ++k) {
     h.seg[k] = V3{p.segments[k][0], p.segments[k][1], p.segments[k][2]};
     h.elbows[k] = V3{p.elbows[k][0], p.elbows[k][1], p.elbows[k][2]};

@@ -141,6 +141,7 @@ struct HostPose {
   V3 joints[5];
   V3 elbows[4];
   int qidx[4] = {-1, -1, -1, -1};
+  bool no_qidx = false;  // quiver_indices empty in the reference PoseChain
   double s4dev = 0.0;
   std::vector<V3> waypoints;
 };

@@ -103,6 +103,7 @@ __host__ __device__ inline DevPose folded_pose(const ArmDev& arm, V3 n, double f
   V3 dir = rpd::normalized(seed - rpd::dot(seed, n) * n);
   DevPose p{};
   p.nseg = arm.nseg;
+  p.no_qidx = 1;  // chain_from_segments(spec, segs): no indices (path_planner.cpp:726)
   double sign = 1.0;
   for (int j = 0; j < arm.nseg; ++j) {
     p.seg[j] = arm.L[j] * dir;
@@ -1408,6 +1409,7 @@ DevPose to_dev(const HostPose& h) {
   DevPose d{};
   d.nseg = h.nseg;
   d.has_elbows = h.has_elbows ? 1 : 0;
+  d.no_qidx = h.no_qidx ? 1 : 0;
   for (int k = 0; k < 4; ++k) d.qidx[k] = k < h.nseg ? h.qidx[k] : -1;
   for (int k = 0; k < h.nseg; ++k) {
     d.seg[k] = h.seg[k];
@@ -1728,6 +1730,7 @@ std::optional<std::vector<HostPose>> Planner::interpolate(const HostPose* from_o
     const rpd::M3 rot = rpd::m_mul(b, m_transpose(a));
     dfrom = DevPose{};
     dfrom.nseg = fold.nseg;
+    dfrom.no_qidx = 1;  // path_planner.cpp:479
     for (int k = 0; k < fold.nseg; ++k) {
       dfrom.seg[k] = m_vec(rot, fold.seg[k]);
       dfrom.qidx[k] = -1;

@@ -673,6 +673,7 @@ HostPose host_pose_from_dev(const DevPose& d) {
   HostPose h;
   h.nseg = d.nseg;
   h.has_elbows = d.has_elbows != 0;
+  h.no_qidx = d.no_qidx != 0;
   for (int k = 0; k < d.nseg; ++k) {
     h.seg[k] = d.seg[k];
     h.elbows[k] = d.elbows[k];

@@ -80,6 +80,7 @@ struct ShortcutRec {
 struct DevPose {
   int nseg;
   int has_elbows;
+  int no_qidx;  // PoseChain built without quiver indices (joint-space / folded)
   int qidx[4];
   int n_wp_links;
   int n_wp[8];
@@ -166,6 +167,7 @@ __host__ __device__ inline bool to_angles(const ArmDev& arm, const DevPose& p, d
 __host__ __device__ inline DevPose from_angles(const ArmDev& arm, const double* az, const double* el) {
   DevPose p{};
   p.nseg = arm.nseg;
+  p.no_qidx = 1;  // joint_angles_to_vectors builds the chain without indices
   rpd::M3 frame = arm.base;
   for (int j = 0; j < arm.nseg; ++j) {
     frame = rpd::m_mul(rpd::m_mul(frame, rpd::rot_z(az[j])), rpd::rot_y(el[j]));

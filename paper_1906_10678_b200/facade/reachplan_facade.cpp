@@ -152,7 +152,7 @@ PoseChain from_rp(const rp_pose& p, const double* wps) {
   PoseChain c;
   for (int k = 0; k < p.n_segments; ++k) {
     c.segments.push_back(get3(p.segments[k]));
-    c.quiver_indices.push_back(p.quiver_indices[k]);
+    if (!p.no_indices) c.quiver_indices.push_back(p.quiver_indices[k]);
     if (p.has_elbows) c.elbows.push_back(get3(p.elbows[k]));
   }
   for (int k = 0; k <= p.n_segments; ++k) c.joints.push_back(get3(p.joints[k]));
@@ -169,6 +169,7 @@ rp_pose to_rp(const PoseChain& c, std::vector<double>* wps) {
           "pose must have 1..4 segments");
   p.n_segments = c.segment_count();
   p.has_elbows = c.elbows.empty() ? 0 : 1;
+  p.no_indices = c.quiver_indices.empty() ? 1 : 0;
   for (int k = 0; k < RP_MAX_SEGMENTS; ++k)
     p.quiver_indices[k] = k < static_cast<int>(c.quiver_indices.size()) ? c.quiver_indices[k] : -1;
   for (int k = 0; k < p.n_segments; ++k) {

@@ -9,6 +9,7 @@
 //   lengths <n> L1 .. Ln   radius <r>   mode <0|1>   samples <n>
 //   bounds x0 y0 z0 x1 y1 z1   voxel <vs>   quiver <step_rad> <min_per_ring>
 //   target x y z   second x y z   boxes <k> then k lines "x0 y0 z0 x1 y1 z1"
+#include "reachplan/io.hpp"
 #include "reachplan/pipeline.hpp"
 
 #include <cstdio>
@@ -145,6 +146,25 @@ int main(int argc, char** argv) {
     const std::vector<GapCandidate> gaps =
         span_gap(chosen.pose.joints[2], be.points, arm.length(2), rp.resolved_epsilon(arm));
     const SegmentProbe probe = segment_clear(grid, arm.root, scene.target, 8);
+    if (argc > 2) {
+      // the plan file the reference CLI writes for `plan` (cli.cpp:126-137,
+      // 167-185), from the façade's results and the reference's writer
+      try {
+        PlanFile pf;
+        pf.quiver.elev_step_deg = rad2deg(qstep);
+        pf.quiver.equator_azim_step_deg = rad2deg(qstep);
+        pf.quiver.min_per_ring = mpr;
+        pf.reach = rp;
+        pf.path = pp.resolved(arm, rp);
+        pf.arm = arm;
+        pf.chosen = chosen;
+        pf.plan = plan_from_reach(arm, q, grid, chosen, set, scene.target, rp, pp);
+        pf.stats = set.stats;
+        pf.stats.wall_ms = 0.0;
+        std::ofstream(argv[2]) << emit_plan(pf);
+      } catch (const Error&) {
+      }
+    }
     std::cout << "{\"quiver\":" << q.size() << ",\"rings\":" << q.ring_count()
               << ",\"occupied\":" << grid.occupied_count()
               << ",\"grids_equal\":" << (grid.occupancy == g2.occupancy ? "true" : "false")

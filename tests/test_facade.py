@@ -37,7 +37,8 @@ def _scene_file(tmp_path, sc):
 
 def _pose_eq(js, pose, what):
     p, _ = pose
-    assert js["qidx"] == list(p.quiver_indices)[:p.n_segments], what
+    want = [] if p.no_indices else list(p.quiver_indices)[:p.n_segments]
+    assert js["qidx"] == want, what
     assert js["segments"] == [list(p.segments[k]) for k in range(p.n_segments)], what
     assert js["joints"] == [list(p.joints[k]) for k in range(p.n_segments + 1)], what
     assert js["n_waypoints"] == p.n_waypoints, what
@@ -61,8 +62,9 @@ def _plan_eq(js, rc, plan, n, what):
 @pytest.mark.parametrize("name,deg", [("C2", 5.0), ("C1", 5.0)])
 def test_facade_matches_reference(tmp_path, name, deg):
     sc = scenes.config(name, quiver_deg=deg)
-    out = subprocess.run([BIN, _scene_file(tmp_path, sc)], capture_output=True, text=True,
-                         timeout=600)
+    plan_path = tmp_path / "plan.json"
+    out = subprocess.run([BIN, _scene_file(tmp_path, sc), str(plan_path)], capture_output=True,
+                         text=True, timeout=600)
     assert out.returncode == 0, out.stderr
     js = json.loads(out.stdout.strip().splitlines()[-1])
     assert "error" not in js, js
@@ -80,6 +82,11 @@ def test_facade_matches_reference(tmp_path, name, deg):
     assert js["chosen"]["kind"] == c.kind and js["chosen"]["path_length"] == c.path_length
     if c.kind == abi.RP_CHOSEN_REACH_POSE:
         _pose_eq(js["chosen"]["pose"], R.pose(c.index), "chosen")
+    # SPEC acceptance 9: the reference's plan-file writer, fed the façade's
+    # results, produces the reference CLI's file byte for byte
+    rc_file, text = R.emit_plan()
+    if rc_file == 0:
+        assert plan_path.read_text() == text
     rc, plan = R.plan_reach_then_path()
     _plan_eq(js["plan"], rc, plan, sc.n_samples, "plan_reach_then_path")
     _plan_eq(js["plan_from_reach"], rc, plan, sc.n_samples, "plan_from_reach")
