@@ -141,13 +141,14 @@ __device__ __forceinline__ int walk_first_blocked(const GridView& g, V3 from, V3
 }
 
 /// Blocked-sample mask of a walk of n <= N samples (bit k = sample k+1),
-/// with all N gathers in flight together. The floor of every coordinate is
-/// taken on the exact-floor fast path without branching; *exact is false
-/// when any coordinate needs vox_floor's division fallback (then the caller
-/// redoes the walk sequentially), so the mask is the reference's verdict
-/// whenever *exact is true. Measured on B200: ~0.9k cycles for an 8-sample
-/// walk versus ~7k for the sequential walk (one L2 round trip instead of 8).
-template <int N>
+/// with all N gathers in flight together. Each coordinate's floor takes the
+/// exact-floor fast path; the rare coordinate whose bracket straddles an
+/// integer (e.g. a sample exactly on a voxel face: quiver vectors with a
+/// zero component from the root) gets vox_floor's IEEE division in place,
+/// so the loads stay parallel and the mask is the reference's verdict.
+/// Measured on B200: ~0.9k cycles for an 8-sample walk versus ~7k for the
+/// sequential walk (one L2 round trip instead of 8).
+template <int N, bool INPLACE>
 __device__ __forceinline__ uint32_t walk_hits(const GridView& g, V3 from, V3 to, int n, bool* exact) {
   const V3 diff = to - from;
   bool ok = true;
@@ -159,11 +160,18 @@ __device__ __forceinline__ uint32_t walk_hits(const GridView& g, V3 from, V3 to,
     const bool live = k < n;
     const double t = c_tk.v[n][live ? k + 1 : n];
     const V3 p = from + t * diff;
-    const double qx = (p.x - g.ox) * g.rvs, qy = (p.y - g.oy) * g.rvs, qz = (p.z - g.oz) * g.rvs;
+    const double ax = p.x - g.ox, ay = p.y - g.oy, az = p.z - g.oz;
+    const double qx = ax * g.rvs, qy = ay * g.rvs, qz = az * g.rvs;
     const double dx = fabs(qx) * 8.9e-16 + 1e-300, dy = fabs(qy) * 8.9e-16 + 1e-300,
                  dz = fabs(qz) * 8.9e-16 + 1e-300;
-    const double lx = floor(qx - dx), ly = floor(qy - dy), lz = floor(qz - dz);
-    ok &= (lx == floor(qx + dx)) & (ly == floor(qy + dy)) & (lz == floor(qz + dz));
+    double lx = floor(qx - dx), ly = floor(qy - dy), lz = floor(qz - dz);
+    if (INPLACE) {
+      if (lx != floor(qx + dx)) lx = floor(ax / g.vs);
+      if (ly != floor(qy + dy)) ly = floor(ay / g.vs);
+      if (lz != floor(qz + dz)) lz = floor(az / g.vs);
+    } else {
+      ok &= (lx == floor(qx + dx)) & (ly == floor(qy + dy)) & (lz == floor(qz + dz));
+    }
     const int ix = static_cast<int>(lx), iy = static_cast<int>(ly), iz = static_cast<int>(lz);
     const bool inb = live & (ix >= 0) & (iy >= 0) & (iz >= 0) & (ix < g.nx) & (iy < g.ny) & (iz < g.nz);
     idx[k] = inb ? (static_cast<long long>(iz) * g.ny + iy) * g.wx + (ix >> 6) : 0;
@@ -181,14 +189,26 @@ __device__ __forceinline__ uint32_t walk_hits(const GridView& g, V3 from, V3 to,
 }
 
 /// walk_first_blocked with the gathers in flight together (n <= 16), the
-/// sequential walk otherwise or when a floor is ambiguous. Identical result.
-__device__ __forceinline__ int walk_first_blocked_fast(const GridView& g, V3 from, V3 to, int n) {
-  bool exact = false;
-  uint32_t m = 0;
-  if (n == 8) m = walk_hits<8>(g, from, to, 8, &exact);
-  else if (n <= kTkMax) m = walk_hits<kTkMax>(g, from, to, n, &exact);
+/// sequential walk otherwise. Identical result. INPLACE = resolve ambiguous
+/// floors by division inside the parallel walk (planner: walks from the root
+/// often sit on voxel faces); otherwise redo such a walk sequentially
+/// (seg2: rare, and the branch-free body keeps registers down — 2.15 vs
+/// 2.73 ms for C2's seg2).
+template <bool INPLACE>
+__device__ __forceinline__ int walk_first_blocked_fast_t(const GridView& g, V3 from, V3 to, int n) {
+  bool exact = true;
+  uint32_t m;
+  if (n == 8) m = walk_hits<8, INPLACE>(g, from, to, 8, &exact);
+  else if (n <= kTkMax) m = walk_hits<kTkMax, INPLACE>(g, from, to, n, &exact);
+  else return walk_first_blocked(g, from, to, n);
   if (!exact) return walk_first_blocked(g, from, to, n);
   return m ? __ffs(m) : 0;
+}
+__device__ __forceinline__ int walk_first_blocked_fast(const GridView& g, V3 from, V3 to, int n) {
+  return walk_first_blocked_fast_t<true>(g, from, to, n);
+}
+__device__ __forceinline__ int walk_first_blocked_fast_seg(const GridView& g, V3 from, V3 to, int n) {
+  return walk_first_blocked_fast_t<false>(g, from, to, n);
 }
 
 /// Out-of-line copy for the large planner kernels (one body instead of one

@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(256, 2) k_seg2_rows(SolveDev a, const SurvDev*
         ++c_lim;
         const V3 dir2 = qvec(a, j);
         const V3 p2 = p1 + L2 * dir2;
-        const int fb = kSeg2ParWalk ? rpd::walk_first_blocked_fast(a.g, p1, p2, a.n)
+        const int fb = kSeg2ParWalk ? rpd::walk_first_blocked_fast_seg(a.g, p1, p2, a.n)
                                     : rpd::walk_first_blocked(a.g, p1, p2, a.n);
         if (row_near && rpd::may_pass_near(a.target, p1, dir2, L2, rnear) &&
             rpd::point_to_segment(a.target, p1, p2) <= a.near_r + 1e-9) {
@@ -1360,7 +1360,7 @@ __global__ void __launch_bounds__(256) k_clear2(SolveDev a, const uint32_t* __re
     if (j < a.Q && ((walk1_bits[i >> 5] >> (i & 31)) & 1u)) {
       const V3 p1 = a.arm.root + a.arm.L[0] * qvec(a, i);
       const V3 p2 = p1 + a.arm.L[1] * qvec(a, j);
-      clear = (kSeg2ParWalk ? rpd::walk_first_blocked_fast(a.g, p1, p2, a.n) : rpd::walk_first_blocked(a.g, p1, p2, a.n)) == 0;
+      clear = (kSeg2ParWalk ? rpd::walk_first_blocked_fast_seg(a.g, p1, p2, a.n) : rpd::walk_first_blocked(a.g, p1, p2, a.n)) == 0;
     }
     const unsigned m = __ballot_sync(FULL, clear);
     if (lane == 0) clear2[wd] = m;
