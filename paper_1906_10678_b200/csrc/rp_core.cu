@@ -262,6 +262,37 @@ HostPose from_abi(const rp_pose& p, const double* wps) {
 
 using namespace rp;
 
+namespace rp {
+
+rp_ctx* worker_ctx(rp_ctx* parent, int k) {
+  while (static_cast<int>(parent->workers.size()) <= k) {
+    auto* c = new rp_ctx();
+    c->device = parent->device;
+    RP_CUDA(cudaSetDevice(parent->device));
+    RP_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+    c->stream = c->own;
+    c->sm_count = parent->sm_count;
+    parent->workers.push_back(c);
+  }
+  rp_ctx* w = parent->workers[k];
+  w->timing = parent->timing;
+  return w;
+}
+
+void ctx_absorb(rp_ctx* parent, rp_ctx* w) {
+  drain_timing(w);
+  for (const auto& kv : w->kernel_ms) {
+    auto& acc = parent->kernel_ms[kv.first];
+    acc.first += kv.second.first;
+    acc.second += kv.second.second;
+  }
+  w->kernel_ms.clear();
+  parent->launches += w->launches;
+  w->launches = 0;
+}
+
+}  // namespace rp
+
 extern "C" {
 
 int32_t rp_abi_version(void) { return RP_ABI_VERSION; }
@@ -295,6 +326,7 @@ rp_status rp_ctx_create(int32_t device, rp_ctx** out) {
 rp_status rp_ctx_destroy(rp_ctx* ctx) {
   return guarded([&] {
     if (!ctx) return;
+    for (rp_ctx* w : ctx->workers) rp_ctx_destroy(w);
     cudaStreamSynchronize(ctx->stream);
     for (auto& t : ctx->pending) {
       cudaEventDestroy(t.start);

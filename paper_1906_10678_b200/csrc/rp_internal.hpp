@@ -71,7 +71,17 @@ struct rp_ctx {
   // Small pinned staging buffer for scalar read-backs.
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
+  // Worker contexts (own streams, same device) for concurrent planner
+  // attempts; created on first use, folded back by ctx_absorb.
+  std::vector<rp_ctx*> workers;
 };
+
+namespace rp {
+/// The k-th worker context of `parent` (created on first use).
+rp_ctx* worker_ctx(rp_ctx* parent, int k);
+/// Fold a worker's launch count and kernel timings into its parent.
+void ctx_absorb(rp_ctx* parent, rp_ctx* worker);
+}  // namespace rp
 
 struct rp_quiver {
   rp_ctx* ctx = nullptr;

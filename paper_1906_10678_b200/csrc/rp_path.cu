@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 namespace rp {
 
@@ -1423,7 +1424,7 @@ DevPose to_dev(const HostPose& h) {
 
 Planner::Planner(rp_ctx* c, const rp_arm& a, const rp_quiver* qv, const rp_grid* gr,
                  const rp_reach_params& r, const rp_path_params& p)
-    : ctx(c), arm(a), q(qv), g(gr), rp(r) {
+    : ctx(c), arm(a), q(qv), g(gr), rp(r), pp_in(p) {
   HostSpan span_("Planner::Planner");
   ad = make_arm_dev(a);
   pp = resolve_path_params(p, a, r);
@@ -1532,8 +1533,10 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
   const size_t smem = 2 * static_cast<size_t>(q->n) * sizeof(int);
   if (bp_blocks == 0) {
     // kernel attribute + occupancy: once per process and shared-memory size
+    static std::mutex attr_mutex;  // planners may run on several threads
     static size_t configured_smem = 0;
     static int per_sm = 0;
+    std::lock_guard<std::mutex> lock(attr_mutex);
     if (configured_smem < smem) {
       RP_CUDA(cudaFuncSetAttribute(k_backward_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
@@ -1550,6 +1553,7 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
     // barriers cheaper and the grid's L1 reuse higher.
     const char* env = std::getenv("RP_BP_BLOCKS");
     bp_blocks = std::min(ctx->sm_count * per_sm, env ? std::max(1, std::atoi(env)) : 64);
+    if (bp_blocks_cap > 0) bp_blocks = std::min(bp_blocks, bp_blocks_cap);
     bp_bar.alloc(2, st);
     bp_state.alloc(4, st);
     bp_best.alloc(bp_blocks, st);

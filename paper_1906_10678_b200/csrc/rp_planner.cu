@@ -6,6 +6,9 @@
 #include "rp_planner.hpp"
 
 #include <algorithm>
+#include <exception>
+#include <thread>
+#include <functional>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -409,38 +412,9 @@ std::unique_ptr<rp_solution_set> try_solve(rp_ctx* ctx, const rp_arm& arm, const
   }
 }
 
-/// fallback_cascade (src/path_planner.cpp:740-822)
-rp_plan* fallback_cascade(Planner& P, const Failure& failure, rp_solution_set* set, V3 target) {
-  PassOptions esc;
-  esc.factors = with_unit_first(P.pp.relax);
-  if (!P.pp.relax.empty()) {
-    const double last = P.pp.relax.back();
-    for (double s : P.pp.relax) esc.factors.push_back(last * s);
-  }
-  {
-    Attempt r = attempt_candidate(P, failure.candidate, target, esc);
-    if (r.plan) {
-      r.plan->notes.push_back("fallback: relaxation escalation");
-      return r.plan;
-    }
-  }
-  PassOptions cloud = esc;
-  cloud.cloud = true;
-  cloud.cloud_radius = 2.0 * P.pp.eps_wp;
-  {
-    Attempt r = attempt_candidate(P, failure.candidate, target, cloud);
-    if (r.plan) {
-      r.plan->notes.push_back("fallback: target cloud");
-      return r.plan;
-    }
-  }
-  for (const Cand& c : alternate_candidates(P, set, failure.candidate, target)) {
-    Attempt r = attempt_candidate(P, c, target, cloud);
-    if (r.plan) {
-      r.plan->notes.push_back("fallback: alternate solution");
-      return r.plan;
-    }
-  }
+/// Step 3 of fallback_cascade (src/path_planner.cpp:786-820): virtual-arm
+/// detours from the blocked waypoint.
+rp_plan* fallback_detour(Planner& P, const Failure& failure, V3 target, const PassOptions& cloud) {
   Build b = make_candidate_build(P, failure.candidate, target);
   if (b.ok && failure.blocked_index > 0 && !failure.waypoints.empty()) {
     const V3 path_target = tracked_point(b.anchor);
@@ -476,6 +450,150 @@ rp_plan* fallback_cascade(Planner& P, const Failure& failure, rp_solution_set* s
     }
   }
   fail(RP_E_NO_PATH, "no motion plan after relaxation, alternate solutions and detours");
+}
+
+/// One attempt for run_window.
+struct Job {
+  const Cand* cand;
+  const PassOptions* opt;
+};
+
+/// Runs the attempts of `jobs` concurrently, one per worker context (own
+/// stream; every attempt builds its own Planner), while `main_side` runs on
+/// the calling thread against P's context. Results come back in job order.
+/// Each attempt is a pure function of (candidate, options), so taking the
+/// first success in order commits exactly what the reference's sequential
+/// loop commits; exceptions are rethrown in order by the caller.
+struct WindowResult {
+  Attempt attempt;
+  std::exception_ptr error;
+};
+std::vector<WindowResult> run_window(Planner& P, const std::vector<Job>& jobs, V3 target,
+                                     const std::function<void()>& main_side) {
+  HostSpan span_("run_window");
+  std::vector<WindowResult> out(jobs.size());
+  std::vector<rp_ctx*> ws;
+  for (size_t k = 0; k < jobs.size(); ++k) ws.push_back(worker_ctx(P.ctx, static_cast<int>(k)));
+  std::vector<std::thread> threads;
+  for (size_t k = 0; k < jobs.size(); ++k) {
+    threads.emplace_back([&, k] {
+      try {
+        RP_CUDA(cudaSetDevice(P.ctx->device));
+        Planner W(ws[k], P.arm, P.q, P.g, P.rp, P.pp_in);
+        // co-residency of the concurrent cooperative passes (1 block per SM)
+        const int share = P.ctx->sm_count / static_cast<int>(jobs.size());
+        W.bp_blocks_cap = share >= 16 ? (share & ~15) : std::max(1, share);
+        out[k].attempt = attempt_candidate(W, *jobs[k].cand, target, *jobs[k].opt);
+      } catch (...) {
+        out[k].error = std::current_exception();
+      }
+    });
+  }
+  std::exception_ptr main_error;
+  try {
+    if (main_side) main_side();
+  } catch (...) {
+    main_error = std::current_exception();
+  }
+  for (auto& t : threads) t.join();
+  for (rp_ctx* w : ws) ctx_absorb(P.ctx, w);
+  if (main_error) {
+    for (auto& r : out) delete r.attempt.plan;
+    std::rethrow_exception(main_error);
+  }
+  return out;
+}
+
+/// The first success of a window in job order (later plans are dropped);
+/// an attempt that threw before any success rethrows, as the sequential
+/// loop would have.
+rp_plan* first_in_order(std::vector<WindowResult>& w) {
+  rp_plan* found = nullptr;
+  for (auto& r : w) {
+    if (found) {
+      delete r.attempt.plan;
+      continue;
+    }
+    if (r.error) {
+      for (auto& q : w) delete q.attempt.plan;
+      std::rethrow_exception(r.error);
+    }
+    found = r.attempt.plan;
+    r.attempt.plan = nullptr;
+  }
+  return found;
+}
+
+// concurrent attempts per window; each pass then takes sm_count / width
+// blocks (rounded down to 16) so all of them stay co-resident
+static int cascade_width() {
+  static const int w = std::getenv("RP_CASCADE_WIDTH") ? std::atoi(std::getenv("RP_CASCADE_WIDTH")) : 3;
+  return std::max(1, std::min(w, 4));
+}
+
+/// fallback_cascade (src/path_planner.cpp:740-822)
+rp_plan* fallback_cascade(Planner& P, const Failure& failure, rp_solution_set* set, V3 target) {
+  PassOptions esc;
+  esc.factors = with_unit_first(P.pp.relax);
+  if (!P.pp.relax.empty()) {
+    const double last = P.pp.relax.back();
+    for (double s : P.pp.relax) esc.factors.push_back(last * s);
+  }
+  static const bool serial = std::getenv("RP_SERIAL_CASCADE") != nullptr;
+  if (!serial) {
+    // Steps 1a (escalation), 1b (target cloud) and 2 (alternate solutions)
+    // are independent attempts tried in a fixed order: run them two at a
+    // time on worker streams and keep the first success in that order. The
+    // alternates are ranked on the main stream while step 1 runs.
+    PassOptions cloud = esc;
+    cloud.cloud = true;
+    cloud.cloud_radius = 2.0 * P.pp.eps_wp;
+    std::vector<Cand> alts;
+    std::vector<WindowResult> w = run_window(
+        P, {{&failure.candidate, &esc}, {&failure.candidate, &cloud}}, target,
+        [&] { alts = alternate_candidates(P, set, failure.candidate, target); });
+    const bool esc_ok = w[0].attempt.plan != nullptr && !w[0].error;
+    if (rp_plan* plan = first_in_order(w)) {
+      plan->notes.push_back(esc_ok ? "fallback: relaxation escalation" : "fallback: target cloud");
+      return plan;
+    }
+    for (size_t a = 0; a < alts.size(); a += cascade_width()) {
+      std::vector<Job> jobs;
+      for (size_t k = a; k < std::min(alts.size(), a + cascade_width()); ++k)
+        jobs.push_back({&alts[k], &cloud});
+      std::vector<WindowResult> r = run_window(P, jobs, target, {});
+      if (rp_plan* plan = first_in_order(r)) {
+        plan->notes.push_back("fallback: alternate solution");
+        return plan;
+      }
+    }
+    return fallback_detour(P, failure, target, cloud);
+  }
+  {
+    Attempt r = attempt_candidate(P, failure.candidate, target, esc);
+    if (r.plan) {
+      r.plan->notes.push_back("fallback: relaxation escalation");
+      return r.plan;
+    }
+  }
+  PassOptions cloud = esc;
+  cloud.cloud = true;
+  cloud.cloud_radius = 2.0 * P.pp.eps_wp;
+  {
+    Attempt r = attempt_candidate(P, failure.candidate, target, cloud);
+    if (r.plan) {
+      r.plan->notes.push_back("fallback: target cloud");
+      return r.plan;
+    }
+  }
+  for (const Cand& c : alternate_candidates(P, set, failure.candidate, target)) {
+    Attempt r = attempt_candidate(P, c, target, cloud);
+    if (r.plan) {
+      r.plan->notes.push_back("fallback: alternate solution");
+      return r.plan;
+    }
+  }
+  return fallback_detour(P, failure, target, cloud);
 }
 
 Cand chosen_cand(rp_solution_set* set, const rp_chosen& ch) {

@@ -23,6 +23,7 @@ struct Planner {
   const rp_quiver* q;
   const rp_grid* g;
   rp_reach_params rp;
+  rp_path_params pp_in;  // as given (workers build their own Planner from it)
   ArmDev ad;
   PP pp;
   int n;
@@ -74,6 +75,7 @@ struct Planner {
   DevBuf<int> bp_state;
   DevBuf<WikBest> bp_best;
   int bp_blocks = 0;
+  int bp_blocks_cap = 0;  // > 0: at most this many blocks (concurrent passes)
   bool use_device_pass = true;
   std::vector<long long> rank_by_deviation(rp_solution_set* set,
                                            const std::vector<std::vector<V3>>& lists,
