@@ -241,6 +241,11 @@ rp_status rp_grid_mark_dilate_boxes(rp_grid* g, const rp_obstacle* obs, int32_t 
  * `reps` times back to back on the ctx stream; *ms = device time per pass. */
 rp_status rp_grid_mark_dilate_repeat(rp_grid* g, const rp_obstacle* obs, int32_t n, double radius,
                                      int32_t reps, double* ms);
+/* Benchmark helper: `ng` same-shape grids of one context, each updated `reps`
+ * times on its own stream, all streams concurrently; *ms = device time per
+ * update (updates of independent grids overlapping). */
+rp_status rp_grid_mark_dilate_concurrent(rp_grid* const* grids, int32_t ng, const rp_obstacle* obs,
+                                         int32_t n, double radius, int32_t reps, double* ms);
 /* [build_scene_grid, src/pipeline.cpp:17-34] dilation < 0 = effective_dilation */
 rp_status rp_build_scene_grid(rp_ctx* ctx, const double bounds_min[3], const double bounds_max[3],
                               double voxel_size, double dilation, const rp_obstacle* obs,

@@ -118,6 +118,8 @@ def lib():
         "rp_plan_create": ([C.c_char_p, d3, P(abi.Pose), d3, C.c_int32, P(abi.Pose), C.c_int32,
                             P(vp)], C.c_int32),
         "rp_plan_destroy": ([vp], C.c_int32),
+        "rp_grid_mark_dilate_concurrent": ([P(vp), C.c_int32, P(abi.Obstacle), C.c_int32,
+                                            C.c_double, C.c_int32, P(C.c_double)], C.c_int32),
         "rp_validate_plan": ([vp, P(abi.Arm), vp, vp, P(abi.ReachParams), P(abi.PathParams),
                               P(abi.Validation), C.c_char_p, C.c_int64], C.c_int32),
         "rp_simulate_execution": ([vp, P(abi.Arm), vp, P(abi.MotionParams), vp, P(vp)], C.c_int32),
@@ -578,3 +580,14 @@ def simulate_execution(ctx, arm, plan, mp=None, grid=None) -> dict:
                 "clamp": clamp[:nc.value].tolist(), "reached": bool(reached.value)}
     finally:
         lib().rp_trace_destroy(h)
+
+
+def mark_dilate_concurrent(grids, obstacles, radius, reps) -> float:
+    """Per-update device time (ms) of the fused mark+dilate when `grids`
+    (same shape, one context) are updated concurrently, `reps` each."""
+    arr = abi.obstacle_array(obstacles)
+    hs = (C.c_void_p * len(grids))(*[g.h for g in grids])
+    ms = C.c_double()
+    _check(lib().rp_grid_mark_dilate_concurrent(hs, len(grids), arr, len(obstacles), radius,
+                                                reps, C.byref(ms)))
+    return ms.value
