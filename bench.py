@@ -44,6 +44,7 @@ def parse():
     p.add_argument("--cpu-budget-s", type=float, default=150.0)
     p.add_argument("--no-batch", action="store_true", help="skip the C5 batched-query leg")
     p.add_argument("--batch-queries", type=int, default=4096)
+    p.add_argument("--no-configs", action="store_true", help="skip the C1/C3/C4 latency leg")
     return p.parse_args()
 
 
@@ -273,6 +274,8 @@ def run_ours(args, sc):
     vox = voxel_update(ctx, torch, stream)
     # -- C5: 4096 batched reach queries sharded over the ranks
     batch = None if args.no_batch else batch_queries(args, ctx, torch, stream, rank, world)
+    # -- latency of the other BASELINE configurations (rank 0's view)
+    configs = config_latencies(ctx, torch, stream) if not args.no_configs else None
     if rank != 0:
         return None
     line = {
@@ -292,6 +295,7 @@ def run_ours(args, sc):
                             "share": kernel_ms[dominant] / max(ms, 1e-9)},
         "plan": {"kind": last["kind"], "notes": last["notes"], "waypoints": len(last["waypoints"])},
         "batch": batch,
+        "configs": configs,
         "paper_ms": PAPER_MS,
     }
     if world == 1 and not args.no_cpu_baseline:
@@ -361,6 +365,96 @@ def batch_queries(args, ctx, torch, stream, rank, world):
             "wall_ms_per_step": wms, "scaling": "strong",
             "sharding": f"contiguous target blocks x{world}, all-gather of result records",
             "solved": ok, "results_sha256": h.hexdigest()[:16]}
+
+
+def config_latencies(ctx, torch, stream, reps=3):
+    """End-to-end latency of each BASELINE.json configuration on one GPU
+    (SURVEY §8d shapes, 2-degree quiver), device time on the library stream,
+    median of `reps`:
+    C1  6-DOF reach pose (scene grid + solve + select + exact refine), 64^3;
+    C2  8-DOF reach pose + 25-waypoint path, 128^3 (the headline);
+    C3  8-DOF reach + path, then an arbitrary-pose path from its final pose
+        to a second target, 256^3, 40 boxes;
+    C4  one control tick of dynamic-obstacle avoidance on 256^3: re-voxelise
+        (overlay of the moving cube, us) and re-plan (replan_dynamic, ms)."""
+    import numpy as np
+    from paper_1906_10678_b200 import abi, api, scenes
+
+    def timed(fn):
+        out = []
+        res = None
+        for _ in range(reps + 1):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            res = fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            out.append(e0.elapsed_time(e1))
+        return statistics.median(out[1:]), res
+
+    def setup(name):
+        sc = scenes.config(name)
+        arm, rp = sc.arm(), sc.reach_params()
+        q = api.Quiver(ctx, sc.quiver_step(), sc.quiver_step(), sc.min_per_ring)
+        return sc, arm, rp, q
+
+    def grid(sc, arm, rp):
+        return api.Grid.scene(ctx, scenes.BOUNDS_MIN, scenes.BOUNDS_MAX, sc.voxel_size,
+                              sc.obstacles(), arm, rp)
+
+    res = {}
+    sc, arm, rp, q = setup("C1")
+
+    def c1():
+        g = grid(sc, arm, rp)
+        S = api.solve_reach(ctx, arm, q, g, sc.target, rp)
+        c = S.select()
+        if c.kind == abi.RP_CHOSEN_REACH_POSE:
+            api.exact_refine(ctx, arm, S.pose(c.index)[0], sc.target)
+        return S.stats().solutions
+    ms, nsol = timed(c1)
+    res["C1"] = {"what": "6-DOF reach pose (grid + solve + select + refine), 64^3, 3 boxes",
+                 "ms": ms, "solutions": nsol}
+    sc, arm, rp, q = setup("C3")
+
+    def c3():
+        g = grid(sc, arm, rp)
+        return g, api.plan_reach_then_path(ctx, arm, q, g, sc.target, rp)
+    ms, (g3, (rc, plan3)) = timed(c3)
+    res["C3"] = {"what": "8-DOF reach pose + 25-waypoint path (grid + plan_reach_then_path), "
+                         "256^3, 40 boxes", "ms": ms, "rc": rc}
+    if rc == 0:
+        p, w = plan3.summary()["poses"][-1]
+        ms2, (rc2, _) = timed(lambda: api.plan_arbitrary(ctx, arm, q, g3, p, scenes.SECOND_TARGET,
+                                                         rp, start_waypoints=w))
+        res["C3"]["arbitrary"] = {"what": "then plan_arbitrary from its final pose to "
+                                          f"{scenes.SECOND_TARGET} (rc 7 = no-path, as the "
+                                          "reference decides)", "ms": ms2, "rc": rc2}
+    sc, arm, rp, q = setup("C4")
+    g = grid(sc, arm, rp)
+    rc, plan = api.plan_reach_then_path(ctx, arm, q, g, sc.target, rp)
+    if rc == 0:
+        s = plan.summary()
+        at, idx, half = 3, 14, 0.03  # tests/test_gpu_planner.py's Fig-11 geometry
+        c = np.asarray(s["poses"][min(len(s["poses"]) - 1, idx)][0].joints[3][:])
+        ticks = {"overlay_us": [], "replan_ms": [], "rc": []}
+        aug = None
+        for t in range(reps + 1):
+            ctr = c + np.array([0.002 * t, 0.0, 0.0])  # the cube moves 2 mm per tick
+            obs = abi.box(tuple(ctr - half), tuple(ctr + half), dynamic=True)
+            ms_o, aug = timed(lambda: g.overlay(obs, into=aug))
+            ms_r, (rc2, _) = timed(lambda: api.replan_dynamic(ctx, arm, q, g, plan, at, obs, rp))
+            if t:
+                ticks["overlay_us"].append(1e3 * ms_o)
+                ticks["replan_ms"].append(ms_r)
+                ticks["rc"].append(rc2)
+        res["C4"] = {"what": "per control tick on 256^3: re-voxelise the moving cube (overlay) "
+                             "+ replan_dynamic", "overlay_us": statistics.median(ticks["overlay_us"]),
+                     "replan_ms": statistics.median(ticks["replan_ms"]), "rc": ticks["rc"]}
+    else:
+        res["C4"] = {"what": "no first plan on this scene", "rc": rc}
+    return res
 
 
 def voxel_update(ctx, torch, stream):

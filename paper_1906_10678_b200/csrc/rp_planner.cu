@@ -452,38 +452,32 @@ rp_plan* fallback_detour(Planner& P, const Failure& failure, V3 target, const Pa
   fail(RP_E_NO_PATH, "no motion plan after relaxation, alternate solutions and detours");
 }
 
-/// One attempt for run_window.
-struct Job {
-  const Cand* cand;
-  const PassOptions* opt;
-};
-
-/// Runs the attempts of `jobs` concurrently, one per worker context (own
-/// stream; every attempt builds its own Planner), while `main_side` runs on
-/// the calling thread against P's context. Results come back in job order.
-/// Each attempt is a pure function of (candidate, options), so taking the
-/// first success in order commits exactly what the reference's sequential
-/// loop commits; exceptions are rethrown in order by the caller.
-struct WindowResult {
-  Attempt attempt;
+/// Runs work(W, k) for k < n concurrently, one per worker context (own
+/// stream; each call gets its own Planner W over P's arm, grid and quiver),
+/// while `main_side` runs on the calling thread against P's context.
+/// Results come back in index order, with any exception captured per call.
+template <typename R>
+struct Slot {
+  R value{};
   std::exception_ptr error;
 };
-std::vector<WindowResult> run_window(Planner& P, const std::vector<Job>& jobs, V3 target,
-                                     const std::function<void()>& main_side) {
-  HostSpan span_("run_window");
-  std::vector<WindowResult> out(jobs.size());
+template <typename R>
+std::vector<Slot<R>> run_parallel(Planner& P, int n, const std::function<R(Planner&, int)>& work,
+                                  const std::function<void()>& main_side) {
+  HostSpan span_("run_parallel");
+  std::vector<Slot<R>> out(n);
   std::vector<rp_ctx*> ws;
-  for (size_t k = 0; k < jobs.size(); ++k) ws.push_back(worker_ctx(P.ctx, static_cast<int>(k)));
+  for (int k = 0; k < n; ++k) ws.push_back(worker_ctx(P.ctx, k));
   std::vector<std::thread> threads;
-  for (size_t k = 0; k < jobs.size(); ++k) {
+  for (int k = 0; k < n; ++k) {
     threads.emplace_back([&, k] {
       try {
         RP_CUDA(cudaSetDevice(P.ctx->device));
         Planner W(ws[k], P.arm, P.q, P.g, P.rp, P.pp_in);
         // co-residency of the concurrent cooperative passes (1 block per SM)
-        const int share = P.ctx->sm_count / static_cast<int>(jobs.size());
+        const int share = P.ctx->sm_count / n;
         W.bp_blocks_cap = share >= 16 ? (share & ~15) : std::max(1, share);
-        out[k].attempt = attempt_candidate(W, *jobs[k].cand, target, *jobs[k].opt);
+        out[k].value = work(W, k);
       } catch (...) {
         out[k].error = std::current_exception();
       }
@@ -497,9 +491,33 @@ std::vector<WindowResult> run_window(Planner& P, const std::vector<Job>& jobs, V
   }
   for (auto& t : threads) t.join();
   for (rp_ctx* w : ws) ctx_absorb(P.ctx, w);
-  if (main_error) {
-    for (auto& r : out) delete r.attempt.plan;
-    std::rethrow_exception(main_error);
+  if (main_error) std::rethrow_exception(main_error);
+  return out;
+}
+
+/// One attempt of the cascade.
+struct Job {
+  const Cand* cand;
+  const PassOptions* opt;
+};
+struct WindowResult {
+  Attempt attempt;
+  std::exception_ptr error;
+};
+
+/// The cascade's attempts of `jobs` concurrently (run_parallel). Each is a
+/// pure function of (candidate, options), so taking the first success in
+/// job order commits exactly what the reference's sequential loop commits.
+std::vector<WindowResult> run_window(Planner& P, const std::vector<Job>& jobs, V3 target,
+                                     const std::function<void()>& main_side) {
+  std::vector<Slot<Attempt>> r = run_parallel<Attempt>(
+      P, static_cast<int>(jobs.size()),
+      [&](Planner& W, int k) { return attempt_candidate(W, *jobs[k].cand, target, *jobs[k].opt); },
+      main_side);
+  std::vector<WindowResult> out(r.size());
+  for (size_t k = 0; k < r.size(); ++k) {
+    out[k].attempt = std::move(r[k].value);
+    out[k].error = r[k].error;
   }
   return out;
 }
@@ -677,23 +695,44 @@ rp_plan* plan_virtual_path(Planner& P, const HostPose& start, NextBatch next_bat
   PassOptions opt;
   opt.factors = with_unit_first(P.pp.relax);
   opt.fixed_first = &start;
+  auto to_plan = [](PassResult& pass) {
+    auto* plan = new rp_plan();
+    plan->waypoints = std::move(pass.waypoints);
+    plan->poses = std::move(pass.poses);
+    plan->kind = "virtual-arm";
+    plan->relax = std::move(pass.relax);
+    plan->notes = std::move(pass.notes);
+    return plan;
+  };
+  static const bool serial = std::getenv("RP_SERIAL_CASCADE") != nullptr;
+  const int width = serial ? 1 : cascade_width();
   for (;;) {
     const std::vector<HostPose> batch = next_batch();
     if (batch.empty()) return nullptr;
+    // the screened candidates in order; their pinned passes are independent,
+    // so they run `width` at a time and the first success in order wins
+    std::vector<std::vector<V3>> wps_list;
     for (const HostPose& v : batch) {
       if (!screen_real_reach(P.arm, v.waypoints, P.n, P.pp.eps_wp)) continue;
       std::vector<V3> wps{e0};
       wps.insert(wps.end(), v.waypoints.begin(), v.waypoints.end());
       wps.back() = path_target;
-      PassResult pass = backward_pass(P, wps, anchor, opt);
-      if (!pass.ok) continue;
-      auto* plan = new rp_plan();
-      plan->waypoints = std::move(pass.waypoints);
-      plan->poses = std::move(pass.poses);
-      plan->kind = "virtual-arm";
-      plan->relax = std::move(pass.relax);
-      plan->notes = std::move(pass.notes);
-      return plan;
+      wps_list.push_back(std::move(wps));
+    }
+    for (size_t a = 0; a < wps_list.size(); a += width) {
+      const int m = static_cast<int>(std::min<size_t>(width, wps_list.size() - a));
+      if (m == 1) {
+        PassResult pass = backward_pass(P, wps_list[a], anchor, opt);
+        if (pass.ok) return to_plan(pass);
+        continue;
+      }
+      std::vector<Slot<PassResult>> r = run_parallel<PassResult>(
+          P, m, [&](Planner& W, int k) { return backward_pass(W, wps_list[a + k], anchor, opt); },
+          {});
+      for (auto& slot : r) {
+        if (slot.error) std::rethrow_exception(slot.error);
+        if (slot.value.ok) return to_plan(slot.value);
+      }
     }
   }
 }
