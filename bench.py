@@ -326,7 +326,13 @@ def batch_queries(args, ctx, torch, stream, rank, world):
     obs = sc.obstacles()
     dev = "cuda" if world > 1 else "cpu"
 
+    radius = api.lib().rp_effective_dilation(arm, rp, -1.0)
+
     def grid():
+        # N > 1: z-slab partition of the grid build, all-gathered over NCCL
+        if world > 1:
+            return shard.build_grid_sharded(ctx, scenes.BOUNDS_MIN, scenes.BOUNDS_MAX,
+                                            sc.voxel_size, obs, radius, rank, world)
         return api.Grid.scene(ctx, scenes.BOUNDS_MIN, scenes.BOUNDS_MAX, sc.voxel_size, obs, arm, rp)
 
     targets = shard.c5_targets(grid(), args.batch_queries)
@@ -363,7 +369,9 @@ def batch_queries(args, ctx, torch, stream, rank, world):
             "queries": len(targets), "queries_per_rank": hi - lo, "steps": steps,
             "ms_per_step": ms, "queries_per_s": len(targets) / (ms * 1e-3),
             "wall_ms_per_step": wms, "scaling": "strong",
-            "sharding": f"contiguous target blocks x{world}, all-gather of result records",
+            "sharding": f"contiguous target blocks x{world}, all-gather of result records; grid "
+                        + (f"built as {world} z-slabs + NCCL all-gather" if world > 1
+                           else "built whole"),
             "solved": ok, "results_sha256": h.hexdigest()[:16]}
 
 

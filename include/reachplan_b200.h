@@ -237,6 +237,16 @@ rp_status rp_grid_dilate(rp_grid* g, double radius);
  * mark_obstacles(boxes) then dilate(radius) when the grid holds no other
  * occupancy; see DESIGN.md. */
 rp_status rp_grid_mark_dilate_boxes(rp_grid* g, const rp_obstacle* obs, int32_t n, double radius);
+/* z-slab build (multi-GPU grid partitions): planes z0..z1 of the
+ * fused mark + dilate of box obstacles, other planes untouched. Each plane
+ * depends only on the boxes, so slabs need no halo exchange; the union of
+ * slabs equals rp_grid_mark_dilate_boxes on an empty grid bit for bit. */
+rp_status rp_grid_mark_dilate_slab(rp_grid* g, const rp_obstacle* obs, int32_t n, double radius,
+                                   int32_t z0, int32_t z1);
+/* Device pointer of the bit words (for collectives over the grid, e.g. an
+ * all-gather of z-slabs); plane z = words [z*words_per_plane, +words_per_plane). */
+rp_status rp_grid_device_bits(rp_grid* g, void** bits, uint64_t* n_words,
+                              uint64_t* words_per_plane);
 /* Benchmark helper: the fused mark + dilate of `obs` onto g (overwriting it)
  * `reps` times back to back on the ctx stream; *ms = device time per pass. */
 rp_status rp_grid_mark_dilate_repeat(rp_grid* g, const rp_obstacle* obs, int32_t n, double radius,

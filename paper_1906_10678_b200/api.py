@@ -118,6 +118,9 @@ def lib():
         "rp_plan_create": ([C.c_char_p, d3, P(abi.Pose), d3, C.c_int32, P(abi.Pose), C.c_int32,
                             P(vp)], C.c_int32),
         "rp_plan_destroy": ([vp], C.c_int32),
+        "rp_grid_mark_dilate_slab": ([vp, P(abi.Obstacle), C.c_int32, C.c_double, C.c_int32,
+                                      C.c_int32], C.c_int32),
+        "rp_grid_device_bits": ([vp, P(vp), P(C.c_uint64), P(C.c_uint64)], C.c_int32),
         "rp_grid_mark_dilate_concurrent": ([P(vp), C.c_int32, P(abi.Obstacle), C.c_int32,
                                             C.c_double, C.c_int32, P(C.c_double)], C.c_int32),
         "rp_validate_plan": ([vp, P(abi.Arm), vp, vp, P(abi.ReachParams), P(abi.PathParams),
@@ -266,6 +269,25 @@ class Grid:
     def mark_dilate(self, obstacles, radius):
         _check(lib().rp_grid_mark_dilate_boxes(self.h, abi.obstacle_array(obstacles),
                                                len(obstacles), radius))
+
+    def mark_dilate_slab(self, obstacles, radius, z0, z1):
+        """Planes z0..z1 (inclusive) of the fused mark + dilate (z-slab build)."""
+        _check(lib().rp_grid_mark_dilate_slab(self.h, abi.obstacle_array(obstacles),
+                                              len(obstacles), radius, z0, z1))
+
+    def device_words(self):
+        """A torch uint64 tensor view of the device bit words (no copy) and the
+        words per z-plane."""
+        import torch
+        ptr, n, wpp = C.c_void_p(), C.c_uint64(), C.c_uint64()
+        _check(lib().rp_grid_device_bits(self.h, C.byref(ptr), C.byref(n), C.byref(wpp)))
+
+        class _View:  # __cuda_array_interface__ over library-owned memory
+            __cuda_array_interface__ = {"shape": (n.value,), "typestr": "<u8",
+                                        "data": (ptr.value, False), "version": 2}
+        t = torch.as_tensor(_View(), device="cuda")
+        t._rp_owner = self  # keep the grid alive while the view is used
+        return t, wpp.value
 
     def mark_dilate_repeat(self, obstacles, radius, reps) -> float:
         ms = C.c_double()

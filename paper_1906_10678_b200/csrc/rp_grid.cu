@@ -889,6 +889,39 @@ rp_status rp_grid_mark_dilate_boxes(rp_grid* g, const rp_obstacle* obs, int32_t 
   return guarded([&] { grid_mark_dilate_boxes(g, obs, n, radius, true); });
 }
 
+rp_status rp_grid_mark_dilate_slab(rp_grid* g, const rp_obstacle* obs, int32_t n, double radius,
+                                   int32_t z0, int32_t z1) {
+  return guarded([&] {
+    require(radius >= 0.0, RP_E_INVALID_PARAMETER, "dilation radius must be >= 0");
+    require(0 <= z0 && z0 <= z1 && z1 < g->dims[2], RP_E_INVALID_PARAMETER, "slab out of range");
+    check_boxes(obs, n);
+    std::vector<Prim> hp;
+    const DilTable t = make_table(radius, g->voxel_size);
+    require(host_prims(g, obs, n, &hp), RP_E_INVALID_PARAMETER,
+            "slab builds take box obstacles (and small clouds) only");
+    // every plane is a function of the analytic boxes alone, so a slab needs
+    // no halo from its neighbours: exactly the full build's planes z0..z1
+    if (!hp.empty() &&
+        !launch_rows_param(g->ctx, "mark_dilate", g, hp, t, 0, g->dims[1] - 1, z0, z1, false)) {
+      DevBuf<Prim> dp(hp.size(), g->ctx->stream);
+      copy_to_device(g->ctx, dp.p, hp.data(), hp.size() * sizeof(Prim));
+      run_rows(g, dp.p, static_cast<int>(hp.size()), t, 0, g->dims[1] - 1, z0, z1, false,
+               "mark_dilate");
+    }
+    g->empty = false;
+    g->dilation_radius = radius;
+  });
+}
+
+rp_status rp_grid_device_bits(rp_grid* g, void** bits, uint64_t* n_words,
+                              uint64_t* words_per_plane) {
+  return guarded([&] {
+    *bits = g->bits;
+    *n_words = static_cast<uint64_t>(g->n_words);
+    *words_per_plane = static_cast<uint64_t>(g->dims[1]) * g->wx;
+  });
+}
+
 rp_status rp_grid_mark_dilate_repeat(rp_grid* g, const rp_obstacle* obs, int32_t n, double radius,
                                      int32_t reps, double* ms) {
   return guarded([&] {

@@ -1,4 +1,5 @@
-"""Multi-GPU sharding of batched reach queries.
+"""Multi-GPU sharding of batched reach queries and of the grid build
+(SURVEY.md §8e, C5).
 
 The queries are independent, so the targets are split into contiguous
 blocks, one per rank (one process per GPU), each rank solves its block with
@@ -93,3 +94,50 @@ def c5_targets(grid, count: int = 4096, seed: int = 4096) -> np.ndarray:
         over = scenes.batch_targets(len(over) * 2, seed=seed)
         keep = over[grid.point_clear(over) == 1]
     return keep[:count]
+
+
+# ---- z-slab grid partitions ---------------------------------------------------
+
+def gather_slabs(words, words_per_plane: int, nz: int, rank: int, world: int):
+    """All-gather the z-slabs of a grid's words in place: rank r owns planes
+    shard_range(nz, r, world); afterwards every rank holds every plane.
+    `words` is a 1-D torch tensor (CUDA for NCCL, CPU for gloo) of
+    nz * words_per_plane uint64 words (int64 for the collective)."""
+    import torch
+    import torch.distributed as dist
+
+    if world == 1:
+        return words
+    flat = words.view(torch.int64)
+    cap = shard_range(nz, 0, world)[1] * words_per_plane  # rank 0's slab is the largest
+    lo, hi = shard_range(nz, rank, world)
+    send = torch.zeros(cap, dtype=torch.int64, device=flat.device)
+    send[: (hi - lo) * words_per_plane] = flat[lo * words_per_plane: hi * words_per_plane]
+    recv = torch.empty(cap * world, dtype=torch.int64, device=flat.device)
+    dist.all_gather_into_tensor(recv, send)
+    for r in range(world):
+        a, b = shard_range(nz, r, world)
+        if r != rank and b > a:
+            flat[a * words_per_plane: b * words_per_plane] = recv[r * cap: r * cap + (b - a) * words_per_plane]
+    return words
+
+
+def build_grid_sharded(ctx, bmin, bmax, voxel_size, obstacles, radius, rank: int, world: int):
+    """The fused mark + dilate of a box scene split into z-slabs over the
+    ranks (each rank rasterises its own planes; boxes are analytic, so no
+    halo is exchanged) and all-gathered so every rank holds the full grid,
+    bit-identical to a single-GPU build."""
+    from . import api
+
+    g = api.Grid.build(ctx, bmin, bmax, voxel_size)
+    nz = g.info()[0][2]
+    lo, hi = shard_range(nz, rank, world)
+    if hi > lo:
+        g.mark_dilate_slab(obstacles, radius, lo, hi - 1)
+    if world > 1:
+        words, wpp = g.device_words()
+        ctx.synchronize()
+        gather_slabs(words, wpp, nz, rank, world)
+        import torch
+        torch.cuda.synchronize()
+    return g

@@ -225,3 +225,27 @@ def test_plan_reach_then_path(ctx, name, deg):
     assert grc == rrc
     if rrc == 0:
         assert_plan_equal(gplan.summary(), rplan.summary(rp.n_samples), UNFOLD_TOL)
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_zslab_build_equals_full_build(ctx, world):
+    """z-slab grid partitions: the slabs of `world` ranks,
+    assembled, equal the single-GPU build bit for bit (and the reference)."""
+    from paper_1906_10678_b200 import api, shard
+    sc = scenes.config("C3")
+    arm, rp = sc.arm(), sc.reach_params()
+    r = api.lib().rp_effective_dilation(arm, rp, -1.0)
+    full = api.Grid.scene(ctx, scenes.BOUNDS_MIN, scenes.BOUNDS_MAX, sc.voxel_size,
+                          sc.obstacles(), arm, rp)
+    want = full.bits()
+    nz = full.info()[0][2]
+    wpp = want.size // nz
+    got = np.zeros_like(want)
+    for rank in range(world):
+        g = api.Grid.build(ctx, scenes.BOUNDS_MIN, scenes.BOUNDS_MAX, sc.voxel_size)
+        lo, hi = shard.shard_range(nz, rank, world)
+        g.mark_dilate_slab(sc.obstacles(), r, lo, hi - 1)
+        b = g.bits()
+        assert not b[:lo * wpp].any() and not b[hi * wpp:].any()  # other planes untouched
+        got[lo * wpp:hi * wpp] = b[lo * wpp:hi * wpp]
+    assert np.array_equal(got, want)

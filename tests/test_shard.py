@@ -89,3 +89,40 @@ def test_gather_two_gloo_ranks(n):
     want = shard.pack([_record(k) for k in range(n)]).tobytes()
     for r in range(world):
         assert got[r] == want, f"rank {r} gathered a different record list"
+
+
+def _slab_worker(rank, world, port, nz, wpp, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        words = torch.zeros(nz * wpp, dtype=torch.int64)
+        lo, hi = shard.shard_range(nz, rank, world)
+        for z in range(lo, hi):  # this rank's planes only
+            words[z * wpp:(z + 1) * wpp] = torch.arange(wpp) + 1000 * (z + 1)
+        shard.gather_slabs(words, wpp, nz, rank, world)
+        q.put((rank, words.numpy().tobytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("nz", [8, 7, 1])
+def test_gather_slabs_two_gloo_ranks(nz):
+    """z-slab grid partitions: each rank fills its planes, the all-gather
+    leaves every rank with every plane."""
+    world, wpp = 2, 5
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_slab_worker, args=(r, world, port, nz, wpp, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = np.concatenate([np.arange(wpp) + 1000 * (z + 1) for z in range(nz)]).astype(np.int64)
+    for r in range(world):
+        assert got[r] == want.tobytes()
