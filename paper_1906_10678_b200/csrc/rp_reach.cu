@@ -1399,7 +1399,106 @@ struct BatchDev {
   unsigned* sc_count;
   BestRec* bb;    // [T*BPT]
   BestRec* best;  // [T]
+  // quiver rings (generated quivers): ring r = directions
+  // ring_off[r] .. ring_off[r+1]-1 at elevation (cos, sin) = (ring_c, ring_s),
+  // azimuth 2*pi*m/count; nrings == 0 -> sweep every direction
+  int* row_ctr;  // [T] next survivor row (dynamic row assignment in k_bq_seg2)
+  int nrings;
+  const int* ring_off;
+  const double* ring_c;
+  const double* ring_s;
 };
+
+/// Azimuth index arcs of ring (cphi, sphi, cnt) whose directions q satisfy
+/// lo <= q.u <= hi (u unit), widened by 1.5 azimuth steps so that rounding
+/// in the generator or here can only add directions, never drop one. Writes
+/// up to 2 arcs as (first index, length) and returns their number; a full
+/// ring is one arc (0, cnt).
+__device__ __noinline__ int ring_arcs(double cphi, double sphi, int cnt, V3 u, double lo, double hi, int* a0,
+                         int* len) {
+  const double rho = sqrt(u.x * u.x + u.y * u.y);
+  const double A = cphi * rho, B = sphi * u.z;
+  if (!(A > 1e-9)) {  // q.u is B +- A over the whole ring
+    if (B + A >= lo && B - A <= hi) {
+      a0[0] = 0;
+      len[0] = cnt;
+      return 1;
+    }
+    return 0;
+  }
+  const double x_hi = (hi - B) / A, x_lo = (lo - B) / A;
+  if (x_lo > 1.0 || x_hi < -1.0) return 0;
+  const double kPiD = 3.14159265358979323846;
+  const double step = 2.0 * kPiD / cnt;
+  const double marg = 1.5 * step + 1e-7;
+  const double d_lo = fmax(0.0, (x_hi >= 1.0 ? 0.0 : acos(fmax(-1.0, x_hi))) - marg);
+  const double d_hi = fmin(kPiD, (x_lo <= -1.0 ? kPiD : acos(fmin(1.0, x_lo))) + marg);
+  if (d_lo <= 0.0 && d_hi >= kPiD) {
+    a0[0] = 0;
+    len[0] = cnt;
+    return 1;
+  }
+  const double thu = atan2(u.y, u.x);
+  int n = 0;
+  auto arc = [&](double t0, double t1) {
+    const long m0 = static_cast<long>(ceil(t0 / step)), m1 = static_cast<long>(floor(t1 / step));
+    long c = m1 - m0 + 1;
+    if (c <= 0) return;
+    if (c >= cnt) {
+      a0[n] = 0;
+      len[n++] = cnt;
+      return;
+    }
+    long s0 = m0 % cnt;
+    if (s0 < 0) s0 += cnt;
+    a0[n] = static_cast<int>(s0);
+    len[n++] = static_cast<int>(c);
+  };
+  if (d_lo <= 0.0) {
+    arc(thu - d_hi, thu + d_hi);
+  } else {
+    arc(thu + d_lo, thu + d_hi);
+    arc(thu - d_hi, thu - d_lo);
+  }
+  return n;
+}
+
+/// Merged index intervals [s, e) (ring-local, ascending, disjoint) of up to
+/// four arcs; returns the count (<= 8) or -1 for "whole ring".
+__device__ __noinline__ int ring_intervals(int cnt, const int* a0, const int* len, int na, int* is, int* ie) {
+  int s[8], e[8], n = 0;
+  for (int k = 0; k < na; ++k) {
+    if (len[k] >= cnt) return -1;
+    const int st = a0[k], en = a0[k] + len[k];
+    if (en <= cnt) {
+      s[n] = st;
+      e[n++] = en;
+    } else {  // wraps past the last azimuth
+      s[n] = st;
+      e[n++] = cnt;
+      s[n] = 0;
+      e[n++] = en - cnt;
+    }
+  }
+  for (int i = 1; i < n; ++i)  // insertion sort by start
+    for (int j = i; j > 0 && s[j] < s[j - 1]; --j) {
+      const int ts = s[j], te = e[j];
+      s[j] = s[j - 1];
+      e[j] = e[j - 1];
+      s[j - 1] = ts;
+      e[j - 1] = te;
+    }
+  int m = 0;
+  for (int i = 0; i < n; ++i) {
+    if (m > 0 && s[i] <= ie[m - 1]) {
+      if (e[i] > ie[m - 1]) ie[m - 1] = e[i];
+    } else {
+      is[m] = s[i];
+      ie[m++] = e[i];
+    }
+  }
+  return m;
+}
 
 __device__ __forceinline__ void warp_flush_t(unsigned long long* ctr, int idx, unsigned v) {
   v = __reduce_add_sync(FULL, v);
@@ -1491,8 +1590,19 @@ __global__ void __launch_bounds__(256, RP_BQ_MINB) k_bq_seg2(BatchDev d) {
   (void)npairs;
   __shared__ int wqs[8][64];
   int* wq = wqs[threadIdx.x >> 5];
+  __shared__ int wiv[8][32 * 8], wive[8][32 * 8];  // per warp: 32 rings x 8 intervals
+  __shared__ signed char wniv[8][32];
+  __shared__ int wbase[8][32];
   // a warp owns whole survivor rows (s) and sweeps j; row constants hoisted
-  for (int s = warp_id; s < S1; s += nwarps) {
+  (void)warp_id;
+  (void)nwarps;
+  // rows are taken dynamically (per-target counter): row costs differ by
+  // orders of magnitude (rows that cannot reach the gap shell are skipped)
+  for (;;) {
+    int s = 0;
+    if (lane == 0) s = atomicAdd(d.row_ctr + t, 1);
+    s = __shfl_sync(FULL, s, 0);
+    if (s >= S1) break;
     const int i = sidx[s];
     const V3 s1 = L1 * qvec(a, i);
     const V3 p1 = arm.root + s1;
@@ -1546,10 +1656,13 @@ __global__ void __launch_bounds__(256, RP_BQ_MINB) k_bq_seg2(BatchDev d) {
       }
     };
     int qn = 0;
-    for (int j0 = 0; j0 < a.Q; j0 += 32) {
-      const int j = j0 + lane;
+    // every lane calls this with its own j (valid or not) in lockstep; the
+    // queue is run 32 at a time, and emptied when `drain` is set. (One call
+    // site each for visit and heavy keeps the kernel's code footprint small:
+    // ncu showed instruction-fetch stalls dominating with inlined copies.)
+    const auto visit = [&](int j, bool valid, bool drain) {
       bool pass = false;
-      if (j < a.Q) {
+      if (valid) {
         const V3 dir2 = qvec(a, j);
         const V3 p2 = p1 + L2 * dir2;
         if (row_near && rpd::may_pass_near(target, p1, dir2, L2, rnear) &&
@@ -1569,16 +1682,110 @@ __global__ void __launch_bounds__(256, RP_BQ_MINB) k_bq_seg2(BatchDev d) {
       if (pass) wq[qn + __popc(m & ((1u << lane) - 1u))] = j;
       qn += __popc(m);
       __syncwarp();
-      if (qn >= 32) {
-        heavy(wq[lane]);
+      if (qn >= 32 || (drain && qn > 0)) {
+        const int take = qn < 32 ? qn : 32;
+        if (lane < take) heavy(wq[lane]);
         __syncwarp();
-        if (lane < qn - 32) wq[lane] = wq[32 + lane];
-        qn -= 32;
+        if (lane < qn - take) wq[lane] = wq[take + lane];
+        qn -= take;
         __syncwarp();
       }
+    };
+    // Directions visited: with quiver rings, only those that can pass the
+    // gap band (q.u_b within the band's cosine range around
+    // u_b = (b - p1)/|b - p1|) or pass near the target (q.u_t >= cos of the
+    // near cone around u_t): per ring at most four azimuth arcs, found by
+    // lanes in parallel 32 rings at a time and packed densely. Skipped
+    // directions fail both tests outright, so counters, shortcuts and the
+    // argmin are unchanged; the exact tests run on every visited pair.
+    // Without ring data the whole quiver is one "ring".
+    const double L2sq = L2 * L2;
+    double blo = 2.0, bhi = -2.0, clo = 2.0;
+    V3 ub{0, 0, 1}, ut{0, 0, 1};
+    bool band_all = false, cap_all = false;
+    if (row_gap) {
+      if (db > 1e-9) {
+        ub = (b - p1) / db;
+        blo = (db * db + L2sq - a.coarse2) / (2.0 * L2 * db) - 1e-9;
+        bhi = (db * db + L2sq - a.band_lo2) / (2.0 * L2 * db) + 1e-9;
+      } else {
+        band_all = true;
+      }
     }
-    if (lane < qn) heavy(wq[lane]);
-    __syncwarp();
+    if (row_near) {
+      const double dt = sqrt(dt2);
+      if (dt > rnear * (1.0 + 1e-9) + 1e-12) {
+        ut = (target - p1) / dt;
+        const double sr = rnear / dt;
+        clo = sqrt(fmax(0.0, 1.0 - sr * sr)) - 1e-9;
+      } else {
+        cap_all = true;
+      }
+    }
+    int* ivs = wiv[threadIdx.x >> 5];
+    int* ive = wive[threadIdx.x >> 5];
+    signed char* niv = wniv[threadIdx.x >> 5];
+    const int nrt = d.nrings > 0 ? d.nrings : 1;
+    for (int r0 = 0; r0 < nrt; r0 += 32) {
+      const int r = r0 + lane;
+      niv[lane] = 0;
+      if (r < nrt) {
+        const int off = d.nrings ? d.ring_off[r] : 0;
+        const int cnt = d.nrings ? d.ring_off[r + 1] - off : a.Q;
+        int a0[4], ln[4], na = 0;
+        if (d.nrings == 0 || band_all || cap_all) {
+          a0[0] = 0;
+          ln[0] = cnt;
+          na = 1;
+        } else {
+          if (row_gap) na += ring_arcs(d.ring_c[r], d.ring_s[r], cnt, ub, blo, bhi, a0, ln);
+          if (row_near)
+            na += ring_arcs(d.ring_c[r], d.ring_s[r], cnt, ut, clo, 2.0, a0 + na, ln + na);
+        }
+        int m = ring_intervals(cnt, a0, ln, na, ivs + lane * 8, ive + lane * 8);
+        if (m < 0) {
+          ivs[lane * 8] = 0;
+          ive[lane * 8] = cnt;
+          m = 1;
+        }
+        niv[lane] = static_cast<signed char>(m);
+      }
+      // pack the rings' intervals densely: exclusive scan of the per-ring
+      // direction counts, then each lane maps its slot of the packed range
+      // back to (ring, interval, offset)
+      int mine = 0;
+      for (int k = 0; k < niv[lane]; ++k) mine += ive[lane * 8 + k] - ivs[lane * 8 + k];
+      int incl = mine;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += v;
+      }
+      wbase[threadIdx.x >> 5][lane] = incl - mine;
+      const int total = __shfl_sync(FULL, incl, 31);
+      __syncwarp();
+      const int* base = wbase[threadIdx.x >> 5];
+      for (int t0 = 0; t0 < total; t0 += 32) {
+        const int tt = t0 + lane;
+        int j = 0;
+        if (tt < total) {
+          int lo = 0, hi = 31;  // last ring whose base <= tt
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (base[mid] <= tt) lo = mid; else hi = mid - 1;
+          }
+          int rem = tt - base[lo];
+          int k = 0;
+          while (rem >= ive[lo * 8 + k] - ivs[lo * 8 + k]) {
+            rem -= ive[lo * 8 + k] - ivs[lo * 8 + k];
+            ++k;
+          }
+          j = (d.nrings ? d.ring_off[r0 + lo] : 0) + ivs[lo * 8 + k] + rem;
+        }
+        visit(j, tt < total, false);
+      }
+      __syncwarp();
+    }
+    while (qn > 0) visit(0, false, true);
   }
   unsigned long long* c = d.ctr + static_cast<size_t>(t) * C_COUNT;
   warp_flush_t(c, C_SEG2_CLEAR, c_clear);
@@ -1891,6 +2098,24 @@ extern "C" rp_status rp_solve_reach_batch(rp_ctx* ctx, const rp_arm* arm, const 
     DevBuf<BestRec> d_bb(static_cast<size_t>(CH) * BPT, st), d_best(CH, st);
     DevBuf<BatchPose> d_pose(CH, st);
     DevBuf<ScBest> d_scb(CH, st);
+    // quiver rings for the batched seg2's arc culling (generated quivers)
+    static const bool no_cull = std::getenv("RP_BATCH_NO_CULL") != nullptr;
+    const int ring_n = no_cull ? 0 : static_cast<int>(q->ring_offsets.size());
+    DevBuf<int> d_roff(ring_n + 1, st);
+    DevBuf<double> d_rc(std::max(1, ring_n), st), d_rs(std::max(1, ring_n), st);
+    if (ring_n > 0) {
+      std::vector<int> ro(q->ring_offsets);
+      ro.push_back(q->n);
+      std::vector<double> rc(ring_n), rs(ring_n);
+      for (int r = 0; r < ring_n; ++r) {
+        rc[r] = std::cos(q->ring_elevations[r]);
+        rs[r] = std::sin(q->ring_elevations[r]);
+      }
+      copy_to_device(ctx, d_roff.p, ro.data(), ro.size() * sizeof(int));
+      copy_to_device(ctx, d_rc.p, rc.data(), ring_n * sizeof(double));
+      copy_to_device(ctx, d_rs.p, rs.data(), ring_n * sizeof(double));
+    }
+    DevBuf<int> d_rowc(CH, st);
     std::vector<V3> ht, hb;
     for (int c0 = 0; c0 < n_targets; c0 += CH) {
       const int T = std::min(CH, n_targets - c0);
@@ -1924,6 +2149,12 @@ extern "C" rp_status rp_solve_reach_batch(rp_ctx* ctx, const rp_arm* arm, const 
       d.sc_count = d_scc.p;
       d.bb = d_bb.p;
       d.best = d_best.p;
+      d.nrings = ring_n;
+      d.row_ctr = d_rowc.p;
+      RP_CUDA(cudaMemsetAsync(d_rowc.p, 0, T * sizeof(int), st));
+      d.ring_off = d_roff.p;
+      d.ring_c = d_rc.p;
+      d.ring_s = d_rs.p;
       launch(ctx, "walk4", k_bq_walk4, dim3(nblk(T, 128)), dim3(128), 0, d, d_w4.p);
       launch(ctx, "seg1", k_bq_seg1, dim3(nblk(q->n, 256), T), dim3(256), 0, d);
       launch(ctx, "compact", k_bq_compact, dim3(T), dim3(1024), 0, d);
