@@ -337,7 +337,8 @@ template <bool EIGHT>
 __global__ void __launch_bounds__(256, 2) k_seg2_rows(SolveDev a, const SurvDev* __restrict__ sv, int S1,
                                                    uint32_t* __restrict__ sol_bits,
                                                    unsigned long long* ctr, long long* sc_list,
-                                                   unsigned* sc_count, BestRec* __restrict__ block_best) {
+                                                   unsigned* sc_count, BestRec* __restrict__ block_best,
+                                                   int* unit_ctr) {
   unsigned c_lim = 0, c_clear = 0, c_gp = 0, c_jp = 0, c_v3 = 0, c_sol = 0;
   double best_len = 1e308;
   long long best_key = LLONG_MAX;
@@ -355,7 +356,14 @@ __global__ void __launch_bounds__(256, 2) k_seg2_rows(SolveDev a, const SurvDev*
   int* wq = wqs[threadIdx.x >> 5];
   constexpr int kChunk = 1024;  // j per work unit (balances small S1)
   const int nchunk = (a.Q + kChunk - 1) / kChunk;
-  for (int u = warp_id; u < S1 * nchunk; u += nwarps) {
+  (void)warp_id;
+  (void)nwarps;
+  for (;;) {
+    // units are taken dynamically: their cost varies with the row's geometry
+    int u = 0;
+    if (lane == 0) u = atomicAdd(unit_ctr, 1);
+    u = __shfl_sync(FULL, u, 0);
+    if (u >= S1 * nchunk) break;
     const int s = u / nchunk;
     const int jbeg = (u - s * nchunk) * kChunk;
     const int jend = min(a.Q, jbeg + kChunk);
@@ -917,10 +925,12 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
         s->sol_bits.zero();
         const int64_t units = static_cast<int64_t>(S1) * ((q->n + 1023) / 1024);
         const int rblocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks, (units + 7) / 8)));
+        DevBuf<int> unit_ctr(1, st);
+        unit_ctr.zero();
         auto runr = [&](auto kern) {
           launch(ctx, "seg2", kern, dim3(rblocks), dim3(threads), 0, a,
                  static_cast<const SurvDev*>(s->surv.p), S1, s->sol_bits.p, ctr.p, sc_list.p,
-                 sc_count.p, bb.p);
+                 sc_count.p, bb.p, unit_ctr.p);
         };
         eight ? runr(k_seg2_rows<true>) : runr(k_seg2_rows<false>);
         blocks = rblocks;
