@@ -150,11 +150,12 @@ __device__ __forceinline__ int walk_first_blocked(const GridView& g, V3 from, V3
 /// sequential walk (one L2 round trip instead of 8).
 template <int N, bool INPLACE>
 __device__ __forceinline__ uint32_t walk_hits(const GridView& g, V3 from, V3 to, int n, bool* exact) {
+  // One pass, no per-sample arrays: each sample's load is issued as soon as
+  // its index is known and only its bit is kept, so the loads overlap
+  // without holding 3N registers (or spilling them in large kernels).
   const V3 diff = to - from;
   bool ok = true;
-  long long idx[N];
-  int bit[N];
-  uint64_t use[N];
+  uint32_t mask = 0;
 #pragma unroll
   for (int k = 0; k < N; ++k) {
     const bool live = k < n;
@@ -174,15 +175,9 @@ __device__ __forceinline__ uint32_t walk_hits(const GridView& g, V3 from, V3 to,
     }
     const int ix = static_cast<int>(lx), iy = static_cast<int>(ly), iz = static_cast<int>(lz);
     const bool inb = live & (ix >= 0) & (iy >= 0) & (iz >= 0) & (ix < g.nx) & (iy < g.ny) & (iz < g.nz);
-    idx[k] = inb ? (static_cast<long long>(iz) * g.ny + iy) * g.wx + (ix >> 6) : 0;
-    bit[k] = ix & 63;
-    use[k] = static_cast<uint64_t>(inb);
-  }
-  uint32_t mask = 0;
-#pragma unroll
-  for (int k = 0; k < N; ++k) {
-    const uint64_t w = __ldg(g.bits + idx[k]);
-    mask |= static_cast<uint32_t>((w >> bit[k]) & use[k]) << k;
+    const long long idx = inb ? (static_cast<long long>(iz) * g.ny + iy) * g.wx + (ix >> 6) : 0;
+    const uint64_t w = __ldg(g.bits + idx);
+    mask |= static_cast<uint32_t>((w >> (ix & 63)) & static_cast<uint64_t>(inb)) << k;
   }
   *exact = ok;
   return mask;

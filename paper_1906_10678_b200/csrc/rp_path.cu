@@ -460,7 +460,8 @@ __device__ void wik_filter_one(const WikDev& w, double cone1, double cone2, V3 u
 /// arithmetic, writing the compact CiFast record (no frame).
 __device__ __forceinline__ void wik_filter_fast(const WikDev& w, double cone1, double cone2, V3 u1,
                                                 V3 u2, int i, CiFast* out, bool* pi_out,
-                                                bool* pj_out) {
+                                                bool* pj_out, const uint32_t* __restrict__ walk1,
+                                                long long* prof = nullptr) {
   const V3 q = wq(w, i);
   bool pi = false;
   if (!w.filter_j || rpd::dot(q, u1) >= cone1) {
@@ -468,16 +469,36 @@ __device__ __forceinline__ void wik_filter_fast(const WikDev& w, double cone1, d
     const double move1 = rpd::norm(p1 - w.prev_j1);
     pi = !(move1 > w.j1max);
     if (pi) {
+      const long long t1 = prof ? clock64() : 0;
       CiFast c;
       c.i = i;
       c.move1 = move1;
       c.p1 = p1;
-      c.ok = rpd::walk_first_blocked_fast(w.g, w.arm.root, p1, w.n) == 0 ? 1 : 0;
+      // segment 1 from the root is the same walk for every waypoint and
+      // attempt: its verdict comes from the planner's precomputed bitmap
+      c.ok = static_cast<int>((__ldg(walk1 + (i >> 5)) >> (i & 31)) & 1u);
+      if (prof) atomicMax(reinterpret_cast<unsigned long long*>(prof + 11), clock64() - t1);
       out[i] = c;
     }
   }
   *pi_out = pi;
   *pj_out = !w.filter_j || rpd::dot(q, u2) >= cone2;
+}
+
+/// Segment-1 clearance of every quiver direction from the root (coaxial
+/// arms): walk_clear(root, root + L1 q_i) as a bitmap, the verdict
+/// wik_filter_fast reads instead of walking once per attempt.
+__global__ void k_walk1_bits(rpd::GridView g, ArmDev arm, const double* __restrict__ qx,
+                             const double* __restrict__ qy, const double* __restrict__ qz, int Q,
+                             int n, uint32_t* __restrict__ bits) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  bool clear = false;
+  if (i < Q) {
+    const V3 p1 = arm.root + arm.L[0] * V3{qx[i], qy[i], qz[i]};
+    clear = rpd::walk_first_blocked_fast(g, arm.root, p1, n) == 0;
+  }
+  const unsigned m = __ballot_sync(FULL, clear);
+  if ((threadIdx.x & 31) == 0 && i < Q + 31) bits[i >> 5] = m;
 }
 
 __global__ void k_wik_filter(WikDev w, double cone1, double cone2, V3 u1, V3 u2,
@@ -711,6 +732,7 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
   // (a per-thread copy would be ~700 B of local memory per thread)
   __shared__ WikDev sw;
   __shared__ V3 s_u1, s_u2, s_cu, s_cv, s_wk;
+  __shared__ double s_fetch[21];
   // screened candidates of one round (one pair per thread): metric, ordinal
   __shared__ double s_cm[kBpThreads];
   __shared__ long long s_ct[kBpThreads];
@@ -737,30 +759,51 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
       }
       return;  // k == 0 is the last waypoint either way
     }
+    // fetch what this waypoint needs from the previous pose and the waypoint
+    // list in one round trip (21 doubles, one per thread; written by other
+    // blocks in this launch, hence .cg loads), then thread 0 fills in the
+    // per-waypoint fields of the search descriptor
+    {
+      const int t = threadIdx.x;
+      if (t < 12) {
+        const DevPose* pp = A.poses + k + 1;
+        const double* src = t < 6 ? &pp->joints[1 + t / 3].x : &pp->seg[(t - 6) / 3].x;
+        s_fetch[t] = __ldcg(src + t % 3);
+      } else if (t < 21) {
+        const int wi = k - 1 + (t - 12) / 3;  // k-1, k, k+1
+        s_fetch[t] = wi >= 0 ? __ldcg(&A.wps[wi].x + (t - 12) % 3) : 0.0;
+      }
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
       // trail context from the (possibly cloud-substituted) waypoint list
-      const DevPose prev = ldcg_struct(A.poses + k + 1);
-      const V3 wk = ldcg_struct(A.wps + k);
-      const V3 wprev = k > 0 ? ldcg_struct(A.wps + k - 1) : wk;
-      const V3 wnext = ldcg_struct(A.wps + k + 1);
+      const V3 prev_j1{s_fetch[0], s_fetch[1], s_fetch[2]};
+      const V3 prev_j2{s_fetch[3], s_fetch[4], s_fetch[5]};
+      const V3 prev_s0{s_fetch[6], s_fetch[7], s_fetch[8]};
+      const V3 prev_s1{s_fetch[9], s_fetch[10], s_fetch[11]};
+      const V3 wk{s_fetch[15], s_fetch[16], s_fetch[17]};
+      const V3 wprev = k > 0 ? V3{s_fetch[12], s_fetch[13], s_fetch[14]} : wk;
+      const V3 wnext{s_fetch[18], s_fetch[19], s_fetch[20]};
       WikDev& w = sw;
-      w = WikDev{};
-      w.g = A.g;
-      w.arm = A.arm;
-      w.n = A.n;
-      w.Q = A.Q;
-      w.qx = A.qx;
-      w.qy = A.qy;
-      w.qz = A.qz;
-      w.spacing = A.spacing;
-      w.prev_j1 = prev.joints[1];
-      w.prev_j2 = prev.joints[2];
-      w.four = A.four;
-      w.L4 = A.L4;
-      w.cond2 = A.cond2;
-      w.cond3 = A.cond3;
-      w.filter_j = A.filter_j;
-      w.prof = blockIdx.x == 0 ? A.prof : nullptr;
+      if (k == A.m - 2) {  // waypoint-independent fields, once per launch
+        w = WikDev{};
+        w.g = A.g;
+        w.arm = A.arm;
+        w.n = A.n;
+        w.Q = A.Q;
+        w.qx = A.qx;
+        w.qy = A.qy;
+        w.qz = A.qz;
+        w.spacing = A.spacing;
+        w.four = A.four;
+        w.L4 = A.L4;
+        w.cond2 = A.cond2;
+        w.cond3 = A.cond3;
+        w.filter_j = A.filter_j;
+        w.prof = blockIdx.x == 0 ? A.prof : nullptr;
+      }
+      w.prev_j1 = prev_j1;
+      w.prev_j2 = prev_j2;
       w.n_opts = 0;
       if (k > 0) {
         const V3 d = wprev - wk;
@@ -777,8 +820,8 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
         w.bias_j1 = b.joints[1];
         w.bias_j2 = b.joints[2];
       }
-      s_u1 = rpd::normalized(prev.seg[0]);
-      s_u2 = rpd::normalized(prev.seg[1]);
+      s_u1 = rpd::normalized(prev_s0);
+      s_u2 = rpd::normalized(prev_s1);
       s_wk = wk;
       // cloud ring frame (src/path_planner.cpp:368-377)
       s_cu = V3{0, 0, 0};
@@ -820,7 +863,8 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
           const long long f0 = A.prof ? clock64() : 0;
           if (i < A.Q) {
             if (fast_eval)
-              wik_filter_fast(w, A.cone1[fi], A.cone2[fi], u1, u2, i, A.ci_fast, &pi, &pj);
+              wik_filter_fast(w, A.cone1[fi], A.cone2[fi], u1, u2, i, A.ci_fast, &pi, &pj, A.walk1,
+                              A.prof);
             else
               wik_filter_one(w, A.cone1[fi], A.cone2[fi], u1, u2, i, A.ci_by_index, &pi, &pj);
           }
@@ -874,10 +918,7 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
             }
             const bool more = __syncthreads_or(tt < total);
             const int nc = s_nc;
-            if (A.prof && blockIdx.x == 0 && threadIdx.x == 0) {
-              A.prof[10] += nc;
-              A.prof[11] += 1;
-            }
+
             // rank the screened candidates by (metric, ordinal) ...
             if (threadIdx.x < nc) {
               const double mm = s_cm[threadIdx.x];
@@ -1622,6 +1663,14 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
   A.jbits = jbits.p;
   A.ci_by_index = ci_by_index.p;
   A.ci_fast = ci_fast.p;
+  if (!ad.any_limit && !ad.has_offsets && !walk1_ready) {
+    walk1_bits.alloc((q->n + 31) / 32 + 1, st);
+    launch(ctx, "walk1", k_walk1_bits, dim3(nblk(q->n, 128)), dim3(128), 0, g->view(), ad,
+           static_cast<const double*>(A.qx), static_cast<const double*>(A.qy),
+           static_cast<const double*>(A.qz), q->n, n, walk1_bits.p);
+    walk1_ready = true;
+  }
+  A.walk1 = walk1_bits.p;
   A.block_best = bp_best.p;
   A.bar = bp_bar.p;
   A.state = bp_state.p;
@@ -1643,8 +1692,8 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
   if (profile) {
     long long hp[16];
     copy_to_host(ctx, hp, prof.p, sizeof(hp));
-    std::fprintf(stderr, "[eval] block-0 screened candidates %lld over %lld rounds; filter max %lld, "
-                 "filter barrier sum %lld, seg-1 candidates %lld\n", hp[10], hp[11], hp[12], hp[13], hp[14]);
+    std::fprintf(stderr, "[filter] max cycles: walk %lld | thread max %lld, barrier sum %lld, "
+                 "seg-1 candidates %lld\n", hp[11], hp[12], hp[13], hp[14]);
     std::fprintf(stderr,
                  "[pass] m=%d attempts=%lld pairs=%lld cyc: filter %lld compact %lld pairs %lld "
                  "wait %lld publish %lld barrier %lld | max ci-load %lld max eval %lld\n",

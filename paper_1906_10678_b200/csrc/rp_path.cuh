@@ -107,6 +107,7 @@ struct BpArgs {
   uint32_t* jbits;
   CiData* ci_by_index;
   CiFast* ci_fast;  // fast-path twin of ci_by_index
+  const uint32_t* walk1;  // segment-1 clearance bitmap (fast path)
   WikBest* block_best;
   unsigned* bar;  // [2] barrier count + generation
   int* state;     // [4] found, failed_index, ok

@@ -34,6 +34,8 @@ struct Planner {
   DevBuf<int> cj, counts;
   DevBuf<CiData> ci, ci_by_index;
   DevBuf<CiFast> ci_fast;
+  DevBuf<uint32_t> walk1_bits;  // k_walk1_bits, built on the first device pass
+  bool walk1_ready = false;
   DevBuf<WikBest> block_best;
   DevBuf<unsigned> done;
   DevBuf<WikResult> result;
