@@ -334,7 +334,7 @@ constexpr bool kSeg2ParWalk = RP_SEG2_PAR_WALK;
 #endif
 
 template <bool EIGHT>
-__global__ void __launch_bounds__(256, 2) k_seg2_rows(SolveDev a, const SurvDev* __restrict__ sv, int S1,
+__global__ void __launch_bounds__(256, 4) k_seg2_rows(SolveDev a, const SurvDev* __restrict__ sv, int S1,
                                                    uint32_t* __restrict__ sol_bits,
                                                    unsigned long long* ctr, long long* sc_list,
                                                    unsigned* sc_count, BestRec* __restrict__ block_best,
