@@ -1357,7 +1357,7 @@ namespace rp {
 namespace {
 
 /// Row-wise clearance of segment 2 for every (i, j) with a clear segment 1.
-__global__ void __launch_bounds__(256) k_clear2(SolveDev a, const uint32_t* __restrict__ walk1_bits,
+__global__ void __launch_bounds__(256, 4) k_clear2(SolveDev a, const uint32_t* __restrict__ walk1_bits,
                                                 int W, uint32_t* __restrict__ clear2) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
