@@ -733,6 +733,8 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
   __shared__ WikDev sw;
   __shared__ V3 s_u1, s_u2, s_cu, s_cv, s_wk;
   __shared__ double s_fetch[21];
+  __shared__ V3 s_prev[5];  // fast pass: joints[1], joints[2], seg[0], seg[1] of the last pose + its waypoint
+  __shared__ int s_found;
   // screened candidates of one round (one pair per thread): metric, ordinal
   __shared__ double s_cm[kBpThreads];
   __shared__ long long s_ct[kBpThreads];
@@ -763,7 +765,16 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
     // list in one round trip (21 doubles, one per thread; written by other
     // blocks in this launch, hence .cg loads), then thread 0 fills in the
     // per-waypoint fields of the search descriptor
-    {
+    const bool from_block = fast_eval && k < A.m - 2;  // previous pose rebuilt in this block
+    if (from_block) {
+      if (threadIdx.x < 12) s_fetch[threadIdx.x] = (&s_prev[0].x)[threadIdx.x];
+      else if (threadIdx.x < 18) {
+        const int wi = k - 1 + (threadIdx.x - 12) / 3;  // k-1, k
+        s_fetch[threadIdx.x] = wi >= 0 ? __ldcg(&A.wps[wi].x + (threadIdx.x - 12) % 3) : 0.0;
+      } else if (threadIdx.x < 21) {
+        s_fetch[threadIdx.x] = (&s_prev[4].x)[threadIdx.x - 18];
+      }
+    } else {
       const int t = threadIdx.x;
       if (t < 12) {
         const DevPose* pp = A.poses + k + 1;
@@ -987,17 +998,97 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
             bopt = op;
           }
         }
-        if (lane == 0) wb[threadIdx.x >> 5] = WikBest{bm, bo, bopt};
+        if (lane == 0) wb[threadIdx.x >> 5] = WikBest{bm, bo, bopt, -1, -1, V3{0, 0, 0}};
         __syncthreads();
         if (threadIdx.x == 0) {
           WikBest b = wb[0];
           for (int q = 1; q < kBpThreads / 32; ++q)
             if (wik_better(wb[q].metric, wb[q].ord, b.metric, b.ord)) b = wb[q];
+          if (fast_eval && b.ord != LLONG_MAX) {
+            const int a = static_cast<int>(b.ord / ncj);
+            const CiFast cf = ldcg_struct(A.ci_fast + li[a]);
+            b.i = cf.i;
+            b.p1 = cf.p1;
+            b.j = lj[b.ord - static_cast<long long>(a) * ncj];
+          }
           A.block_best[blockIdx.x] = b;
         }
         long long c3 = prof ? clock64() : 0;
         grid_barrier(A.bar, nb);
         long long c4 = prof ? clock64() : 0;
+        if (fast_eval) {
+          // Every block reduces the per-block winners itself and rebuilds the
+          // winning pose (the candidate travels in block_best), so the next
+          // waypoint starts without another grid barrier; block 0 also
+          // records the pose for the host. block_best is rewritten only after
+          // the next attempt's filter barrier, which every block reaches only
+          // after this reduction.
+          WikBest b{1e308, LLONG_MAX, -1, -1, -1, V3{0, 0, 0}};
+          for (unsigned q = threadIdx.x; q < nb; q += blockDim.x) {
+            const WikBest r = ldcg_struct(A.block_best + q);
+            if (wik_better(r.metric, r.ord, b.metric, b.ord)) b = r;
+          }
+          for (int off = 16; off > 0; off >>= 1) {
+            WikBest o;
+            o.metric = __shfl_down_sync(FULL, b.metric, off);
+            o.ord = __shfl_down_sync(FULL, b.ord, off);
+            o.opt = __shfl_down_sync(FULL, b.opt, off);
+            o.i = __shfl_down_sync(FULL, b.i, off);
+            o.j = __shfl_down_sync(FULL, b.j, off);
+            o.p1.x = __shfl_down_sync(FULL, b.p1.x, off);
+            o.p1.y = __shfl_down_sync(FULL, b.p1.y, off);
+            o.p1.z = __shfl_down_sync(FULL, b.p1.z, off);
+            if (wik_better(o.metric, o.ord, b.metric, b.ord)) b = o;
+          }
+          __syncthreads();
+          if (lane == 0) wb[threadIdx.x >> 5] = b;
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            b = wb[0];
+            for (int q = 1; q < kBpThreads / 32; ++q)
+              if (wik_better(wb[q].metric, wb[q].ord, b.metric, b.ord)) b = wb[q];
+            int ok = 0;
+            if (b.ord != LLONG_MAX) {
+              CiData cd;
+              cd.i = b.i;
+              cd.ok = 1;
+              cd.move1 = 0.0;
+              cd.p1 = b.p1;
+              cd.link1 = A.arm.root;
+              cd.frame1 = rpd::m_identity();  // unused without offsets
+              const DevPose pose = wik_pose(w, cd, b.j, b.opt);
+              s_prev[0] = pose.joints[1];
+              s_prev[1] = pose.joints[2];
+              s_prev[2] = pose.seg[0];
+              s_prev[3] = pose.seg[1];
+              s_prev[4] = t > 0 ? w.wp : s_wk;  // waypoint k as the pass leaves it
+              if (blockIdx.x == 0) {
+                A.poses[k] = pose;
+                A.relax[k] = f;
+                A.kind[k] = t > 0 ? 1 : 0;
+                if (t > 0) A.wps[k] = w.wp;
+              }
+              ok = 1;
+            }
+            s_found = ok;
+            if (blockIdx.x == 0) A.state[0] = ok;
+          }
+          __syncthreads();
+        }
+        long long c5f = prof ? clock64() : 0;
+        if (fast_eval && prof) {
+          A.prof[0] += c1 - c0;
+          A.prof[1] += c2 - c1;
+          A.prof[2] += c3 - c2;
+          A.prof[3] += c4 - c3;
+          A.prof[4] += c5f - c4;
+          A.prof[6] += 1;
+          A.prof[7] += static_cast<long long>(nci) * ncj;
+        }
+        if (fast_eval) {
+          found = s_found != 0;
+          continue;
+        }
         // phase C: block 0 picks the first strict minimum and publishes it
         if (blockIdx.x == 0) {
           WikBest b{1e308, LLONG_MAX, -1};

@@ -60,6 +60,10 @@ struct WikBest {
   double metric;
   long long ord;
   int opt;
+  // the candidate itself (fast backward pass: every block rebuilds the
+  // winner's pose from these instead of re-reading the candidate arrays)
+  int i, j;
+  V3 p1;
 };
 
 struct WikResult {
