@@ -719,6 +719,46 @@ __device__ __forceinline__ T ldcg_struct(const T* p) {
   return v;
 }
 
+/// wik_pose's arithmetic for a fast-pass winner (coaxial arm: link2 = p1,
+/// link1 = root), from the record kept during the pass.
+__device__ __noinline__ DevPose pose_from_win(const BpArgs& A, const BpWin& W) {
+  const ArmDev& arm = A.arm;
+  const V3 qi{A.qx[W.i], A.qy[W.i], A.qz[W.i]};
+  const V3 qj{A.qx[W.j], A.qy[W.j], A.qz[W.j]};
+  const V3 p2 = W.p1 + arm.L[1] * qj;
+  const V3 v3 = W.wp - p2;
+  const double v3_len = rpd::norm(v3);
+  const V3 v3_hat = v3 / v3_len;
+  const V3 s3 = v3_hat * arm.L[2];
+  const V3 p3 = p2 + s3;
+  DevPose ch{};
+  ch.nseg = 3;
+  ch.seg[0] = arm.L[0] * qi;
+  ch.seg[1] = arm.L[1] * qj;
+  ch.seg[2] = s3;
+  ch.qidx[0] = W.i;
+  ch.qidx[1] = W.j;
+  ch.qidx[2] = -1;
+  ch.qidx[3] = -1;
+  build_chain(arm, ch);
+  ch.n_wp_links = 3;
+  ch.wp_from[0] = arm.root; ch.wp_to[0] = W.p1;
+  ch.wp_from[1] = W.p1;     ch.wp_to[1] = p2;
+  ch.wp_from[2] = p2;       ch.wp_to[2] = p3;
+  ch.n_wp[0] = ch.n_wp[1] = ch.n_wp[2] = A.n;
+  if (A.four && W.opt >= 0) {
+    const V3 dir = W.opt < W.n_opts ? W.opt_dir[W.opt] : rpd::normalized(ch.seg[2]);
+    ch.nseg = 4;
+    ch.seg[3] = A.L4 * dir;
+    build_chain(arm, ch);
+    ch.n_wp_links = 4;
+    ch.wp_from[3] = ch.joints[3];
+    ch.wp_to[3] = ch.joints[4];
+    ch.n_wp[3] = A.n;
+  }
+  return ch;
+}
+
 constexpr int kBpThreads = 256;
 
 __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_constant__ BpArgs A) {
@@ -741,14 +781,34 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
   __shared__ int s_nc;
   __shared__ short s_rank[kBpThreads];
   const bool fast_eval = !A.arm.any_limit && !A.arm.has_offsets;
+  // fast path: block 0 rebuilds the published poses from their winners
+  // before the kernel ends (every exit below goes through here)
+  const auto rebuild = [&]() {
+    if (!fast_eval || blockIdx.x != 0) return;
+    __syncthreads();
+    for (int q = threadIdx.x; q < A.m; q += blockDim.x)
+      if (A.win[q].i >= 0) A.poses[q] = pose_from_win(A, A.win[q]);
+  };
   for (int k = A.m - 2; k >= 0; --k) {
     if (k == 0 && A.has_fixed) {
       if (blockIdx.x == 0 && threadIdx.x == 0) {
-        const DevPose prev = ldcg_struct(A.poses + 1);
+        // joints 1 and 2 of the pose at waypoint 1 (rebuilt in this block on
+        // the fast path, else the pose in memory)
+        V3 pj1, pj2;
+        if (fast_eval && A.m > 2) {
+          pj1 = s_prev[0];
+          pj2 = s_prev[1];
+        } else {
+          const DevPose prev = ldcg_struct(A.poses + 1);
+          pj1 = prev.joints[1];
+          pj2 = prev.joints[2];
+        }
         int found = 0;
         for (int fi = 0; fi < A.nf && !found; ++fi) {
           const double f = A.factors[fi];
-          if (pose_smooth(prev, A.fixed_first, A.pj1 * f + 1e-12, A.pj2 * f + 1e-12)) {
+          const double b1 = A.pj1 * f + 1e-12, b2 = A.pj2 * f + 1e-12;
+          if (rpd::norm(A.fixed_first.joints[1] - pj1) <= b1 &&
+              rpd::norm(A.fixed_first.joints[2] - pj2) <= b2) {  // pose_smooth
             A.poses[0] = A.fixed_first;
             A.relax[0] = f;
             A.kind[0] = 2;
@@ -759,6 +819,7 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
         A.state[1] = found ? -1 : 0;
         A.state[2] = found;
       }
+      rebuild();
       return;  // k == 0 is the last waypoint either way
     }
     // fetch what this waypoint needs from the previous pose and the waypoint
@@ -1049,21 +1110,27 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
               if (wik_better(wb[q].metric, wb[q].ord, b.metric, b.ord)) b = wb[q];
             int ok = 0;
             if (b.ord != LLONG_MAX) {
-              CiData cd;
-              cd.i = b.i;
-              cd.ok = 1;
-              cd.move1 = 0.0;
-              cd.p1 = b.p1;
-              cd.link1 = A.arm.root;
-              cd.frame1 = rpd::m_identity();  // unused without offsets
-              const DevPose pose = wik_pose(w, cd, b.j, b.opt);
-              s_prev[0] = pose.joints[1];
-              s_prev[1] = pose.joints[2];
-              s_prev[2] = pose.seg[0];
-              s_prev[3] = pose.seg[1];
+              // the fields the next waypoint needs, with wik_pose's
+              // arithmetic (chain = cumulative sums on a coaxial arm)
+              const V3 s0 = A.arm.L[0] * V3{A.qx[b.i], A.qy[b.i], A.qz[b.i]};
+              const V3 s1 = A.arm.L[1] * V3{A.qx[b.j], A.qy[b.j], A.qz[b.j]};
+              const V3 j1 = A.arm.root + s0;
+              s_prev[0] = j1;
+              s_prev[1] = j1 + s1;
+              s_prev[2] = s0;
+              s_prev[3] = s1;
               s_prev[4] = t > 0 ? w.wp : s_wk;  // waypoint k as the pass leaves it
               if (blockIdx.x == 0) {
-                A.poses[k] = pose;
+                BpWin W;
+                W.i = b.i;
+                W.j = b.j;
+                W.opt = b.opt;
+                W.n_opts = w.n_opts;
+                W.p1 = b.p1;
+                W.wp = w.wp;
+                W.opt_dir[0] = w.opt_dir[0];
+                W.opt_dir[1] = w.opt_dir[1];
+                A.win[k] = W;
                 A.relax[k] = f;
                 A.kind[k] = t > 0 ? 1 : 0;
                 if (t > 0) A.wps[k] = w.wp;
@@ -1154,6 +1221,7 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
         A.state[1] = k;
         A.state[2] = 0;
       }
+      rebuild();
       return;
     }
   }
@@ -1161,6 +1229,7 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
     A.state[1] = -1;
     A.state[2] = 1;
   }
+  rebuild();
 }
 
 // ---------------------------------------------------------------------------
@@ -1754,6 +1823,9 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
   A.jbits = jbits.p;
   A.ci_by_index = ci_by_index.p;
   A.ci_fast = ci_fast.p;
+  DevBuf<BpWin> dwin(m, st);
+  RP_CUDA(cudaMemsetAsync(dwin.p, 0xFF, m * sizeof(BpWin), st));  // i = -1: not published
+  A.win = dwin.p;
   if (!ad.any_limit && !ad.has_offsets && !walk1_ready) {
     walk1_bits.alloc((q->n + 31) / 32 + 1, st);
     launch(ctx, "walk1", k_walk1_bits, dim3(nblk(q->n, 128)), dim3(128), 0, g->view(), ad,

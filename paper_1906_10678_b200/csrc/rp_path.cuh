@@ -66,6 +66,14 @@ struct WikBest {
   V3 p1;
 };
 
+/// A waypoint's winning candidate in the fast backward pass; the poses are
+/// rebuilt from these after the pass (pose_from_win), off the serial chain.
+struct BpWin {
+  int i, j, opt, n_opts;  // i < 0: not published
+  V3 p1, wp;
+  V3 opt_dir[2];
+};
+
 struct WikResult {
   int found;
   int i, j, opt;
@@ -112,6 +120,7 @@ struct BpArgs {
   CiData* ci_by_index;
   CiFast* ci_fast;  // fast-path twin of ci_by_index
   const uint32_t* walk1;  // segment-1 clearance bitmap (fast path)
+  BpWin* win;             // [m] fast path: winners, rebuilt into poses at the end
   WikBest* block_best;
   unsigned* bar;  // [2] barrier count + generation
   int* state;     // [4] found, failed_index, ok
