@@ -707,6 +707,38 @@ __device__ int block_compact(const uint32_t* __restrict__ bits, int Q, int* out)
   return result;
 }
 
+/// Both candidate lists in one pass (Q <= 16384, so at most 512 words, two
+/// per thread): one block scan of the packed (i count << 16 | j count) per
+/// thread gives both ordered offsets. Returns (n_i << 16) | n_j.
+template <int NT>
+__device__ int block_compact_pair(const uint32_t* __restrict__ ib, const uint32_t* __restrict__ jb,
+                                  int Q, int* li, int* lj) {
+  typedef cub::BlockScan<int, NT> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  const int nwords = (Q + 31) / 32;
+  const int w0 = 2 * static_cast<int>(threadIdx.x);
+  uint32_t wi[2], wj[2];
+  int cnt = 0;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int w = w0 + r;
+    wi[r] = w < nwords ? __ldcg(ib + w) : 0u;
+    wj[r] = w < nwords ? __ldcg(jb + w) : 0u;
+    cnt += (__popc(wi[r]) << 16) + __popc(wj[r]);
+  }
+  int off = 0, total = 0;
+  Scan(tmp).ExclusiveSum(cnt, off, total);
+  int oi = off >> 16, oj = off & 0xFFFF;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int base = (w0 + r) * 32;
+    for (uint32_t x = wi[r]; x; x &= x - 1) li[oi++] = base + __ffs(x) - 1;
+    for (uint32_t x = wj[r]; x; x &= x - 1) lj[oj++] = base + __ffs(x) - 1;
+  }
+  __syncthreads();  // lists complete; tmp reusable
+  return total;
+}
+
 /// Coherent (L2) read of a struct written by another block in this launch.
 template <typename T>
 __device__ __forceinline__ T ldcg_struct(const T* p) {
@@ -955,8 +987,15 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
         long long c1 = prof ? clock64() : 0;
         if (prof) A.prof[13] += c1 - cb;
         // phase B: block-local compaction + this block's share of the pairs
-        const int nci = block_compact<kBpThreads>(A.ibits, A.Q, li);
-        const int ncj = block_compact<kBpThreads>(A.jbits, A.Q, lj);
+        int nci, ncj;
+        if (A.Q <= 2 * 32 * kBpThreads && A.Q < 65536) {
+          const int both = block_compact_pair<kBpThreads>(A.ibits, A.jbits, A.Q, li, lj);
+          nci = both >> 16;
+          ncj = both & 0xFFFF;
+        } else {
+          nci = block_compact<kBpThreads>(A.ibits, A.Q, li);
+          ncj = block_compact<kBpThreads>(A.jbits, A.Q, lj);
+        }
         long long c2 = prof ? clock64() : 0;
         double bm = 1e308;
         long long bo = LLONG_MAX;
