@@ -364,6 +364,80 @@ __device__ bool wik_full_warp(const WikDev& w, const CiFast& c, int j, int lane,
   return false;
 }
 
+/// wik_full_warp on a half warp (16 lanes: at most 5 walks and 9 link
+/// distances), so a warp evaluates two candidates at once. `sub` = lane in
+/// the half, `half` = 0/1; both halves run the same code in lockstep, and an
+/// idle half passes valid = false. Same verdicts as wik_full_warp.
+__device__ bool wik_full_half(const WikDev& w, const CiFast& c, int j, bool valid, int sub,
+                              int half, int* opt_out) {
+  const ArmDev& arm = w.arm;
+  bool alive = valid;
+  const V3 qj = valid ? wq(w, j) : V3{0, 0, 1};
+  const V3 p1 = valid ? c.p1 : arm.root;
+  const V3 p2 = p1 + arm.L[1] * qj;
+  V3 v3 = w.wp - p2;
+  double v3_len = rpd::norm(v3);
+  if (!(v3_len > 0.0)) {  // only for idle halves (screened pairs have |v3| >= 1e-12)
+    v3 = V3{0, 0, 1};
+    v3_len = 1.0;
+  }
+  const V3 v3_hat = v3 / v3_len;
+  const V3 s3 = v3_hat * arm.L[2];
+  const V3 p3 = p2 + s3;
+  V3 J[4];
+  J[0] = arm.root;
+  J[1] = J[0] + arm.L[0] * (valid ? wq(w, c.i) : V3{0, 0, 1});
+  J[2] = J[1] + arm.L[1] * qj;
+  J[3] = J[2] + s3;
+  alive = alive && rpd::norm(J[1] - w.prev_j1) <= w.sm1 && rpd::norm(J[2] - w.prev_j2) <= w.sm2;
+  const double min_sep = 2.0 * arm.arm_radius;
+  const int nopt = w.four ? w.n_opts + 1 : 0;
+  auto tip = [&](int o) {
+    const V3 dir = o < w.n_opts ? w.opt_dir[o] : rpd::normalized(s3);
+    return J[3] + w.L4 * dir;
+  };
+  bool ok = true;
+  if (alive && sub < 2 + nopt) {
+    V3 from = p1, to = p2;
+    if (sub == 1) {
+      from = p2;
+      to = p3;
+    } else if (sub >= 2) {
+      from = J[3];
+      to = tip(sub - 2);
+    }
+    ok = rpd::walk_first_blocked_fast(w.g, from, to, w.n) == 0;
+  }
+  const unsigned walk_fail = (__ballot_sync(0xffffffffu, !ok) >> (16 * half)) & 0xFFFFu;
+  alive = alive && !(walk_fail & 3u);
+  ok = true;
+  const int npairs = w.four ? 3 * nopt : 1;
+  if (alive && sub < npairs) {
+    V3 a0, a1, b0, b1;
+    if (!w.four) {
+      a0 = J[0]; a1 = J[1]; b0 = J[2]; b1 = J[3];
+    } else {
+      const int o = sub / 3, pr = sub % 3;
+      const V3 j4 = tip(o);
+      a0 = pr == 2 ? J[1] : J[0];
+      a1 = pr == 2 ? J[2] : J[1];
+      b0 = pr == 0 ? J[2] : J[3];
+      b1 = pr == 0 ? J[3] : j4;
+    }
+    ok = !(rpd::seg_seg_distance(a0, a1, b0, b1) < min_sep);
+  }
+  const unsigned dist_fail = (__ballot_sync(0xffffffffu, !ok) >> (16 * half)) & 0xFFFFu;
+  if (!alive) return false;
+  if (!w.four) return !(dist_fail & 1u);
+  for (int o = 0; o < nopt; ++o) {
+    if (!((walk_fail >> (2 + o)) & 1u) && !((dist_fail >> (3 * o)) & 7u)) {
+      *opt_out = o;
+      return true;
+    }
+  }
+  return false;
+}
+
 __device__ __forceinline__ bool wik_test(const WikDev& w, const CiData& c, int j, double* m,
                                          int* opt) {
   if (!w.arm.any_limit && !w.arm.has_offsets) return wik_eval_fast(w, c, j, m, opt);
@@ -460,9 +534,8 @@ __device__ void wik_filter_one(const WikDev& w, double cone1, double cone2, V3 u
 /// arithmetic, writing the compact CiFast record (no frame).
 __device__ __forceinline__ void wik_filter_fast(const WikDev& w, double cone1, double cone2, V3 u1,
                                                 V3 u2, int i, CiFast* out, bool* pi_out,
-                                                bool* pj_out, const uint32_t* __restrict__ walk1,
+                                                bool* pj_out, V3 q, int walk1_ok,
                                                 long long* prof = nullptr) {
-  const V3 q = wq(w, i);
   bool pi = false;
   if (!w.filter_j || rpd::dot(q, u1) >= cone1) {
     const V3 p1 = w.arm.root + w.arm.L[0] * q;
@@ -476,8 +549,8 @@ __device__ __forceinline__ void wik_filter_fast(const WikDev& w, double cone1, d
       c.p1 = p1;
       // segment 1 from the root is the same walk for every waypoint and
       // attempt: its verdict comes from the planner's precomputed bitmap
-      c.ok = static_cast<int>((__ldg(walk1 + (i >> 5)) >> (i & 31)) & 1u);
-      if (prof) atomicMax(reinterpret_cast<unsigned long long*>(prof + 11), clock64() - t1);
+      c.ok = walk1_ok;
+      (void)t1;
       out[i] = c;
     }
   }
@@ -821,6 +894,15 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
     for (int q = threadIdx.x; q < A.m; q += blockDim.x)
       if (A.win[q].i >= 0) A.poses[q] = pose_from_win(A, A.win[q]);
   };
+  V3 my_q{0, 0, 0};
+  int my_w1 = 0;
+  if (fast_eval) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < A.Q) {
+      my_q = V3{A.qx[i], A.qy[i], A.qz[i]};
+      my_w1 = static_cast<int>((__ldg(A.walk1 + (i >> 5)) >> (i & 31)) & 1u);
+    }
+  }
   for (int k = A.m - 2; k >= 0; --k) {
     if (k == 0 && A.has_fixed) {
       if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -967,15 +1049,20 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
           const long long f0 = A.prof ? clock64() : 0;
           if (i < A.Q) {
             if (fast_eval)
-              wik_filter_fast(w, A.cone1[fi], A.cone2[fi], u1, u2, i, A.ci_fast, &pi, &pj, A.walk1,
+            {
+              // this thread's direction and its segment-1 verdict are the same
+              // for the whole pass: kept in registers when the grid covers Q
+              const bool cached = i0 == static_cast<int>(blockIdx.x * blockDim.x);
+              const V3 q = cached ? my_q : wq(w, i);
+              const int ok1 =
+                  cached ? my_w1 : static_cast<int>((__ldg(A.walk1 + (i >> 5)) >> (i & 31)) & 1u);
+              wik_filter_fast(w, A.cone1[fi], A.cone2[fi], u1, u2, i, A.ci_fast, &pi, &pj, q, ok1,
                               A.prof);
+            }
             else
               wik_filter_one(w, A.cone1[fi], A.cone2[fi], u1, u2, i, A.ci_by_index, &pi, &pj);
           }
-          if (A.prof) {
-            atomicMax(reinterpret_cast<unsigned long long*>(A.prof + 12), clock64() - f0);
-            if (pi) atomicAdd(reinterpret_cast<unsigned long long*>(A.prof + 14), 1ull);
-          }
+          (void)f0;
           const unsigned mi = __ballot_sync(FULL, pi), mj = __ballot_sync(FULL, pj);
           if (lane == 0 && (i >> 5) < (A.Q + 31) / 32) {
             A.ibits[i >> 5] = mi;
@@ -1029,6 +1116,7 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
             }
             const bool more = __syncthreads_or(tt < total);
             const int nc = s_nc;
+            const long long ps1 = prof ? clock64() : 0;
 
             // rank the screened candidates by (metric, ordinal) ...
             if (threadIdx.x < nc) {
@@ -1042,28 +1130,43 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
             // ... and evaluate them in waves of one candidate per warp, best
             // first: the first wave with a qualifying pair holds the round's
             // answer (every later candidate ranks below it)
-            for (int w0 = 0; w0 < nc; w0 += kBpThreads / 32) {
-              const int k = w0 + warp;
+            // (two candidates per warp, one per half warp: 16 per wave)
+            const int half = lane >> 4, sub = lane & 15;
+            for (int w0 = 0; w0 < nc; w0 += 2 * (kBpThreads / 32)) {
+              const int k = w0 + 2 * warp + half;
               bool hit = false;
               int opt = -1;
+              bool valid = false;
+              double mm = 0.0;
+              long long t2 = 0;
+              CiFast c{};
+              int jj = 0;
               if (k < nc) {
                 const int e = s_rank[k];
-                const double mm = s_cm[e];
-                const long long t2 = s_ct[e];
-                if (wik_better(mm, t2, bm, bo)) {
+                mm = s_cm[e];
+                t2 = s_ct[e];
+                if (wik_better(mm, t2, bm, bo)) {  // else it cannot improve this half's best
                   const int a = static_cast<int>(t2 / ncj);
-                  const CiFast c = ldcg_struct(A.ci_fast + li[a]);
-                  hit = wik_full_warp(w, c, lj[t2 - static_cast<long long>(a) * ncj], lane, &opt);
-                  if (hit) {
-                    bm = mm;
-                    bo = t2;
-                    bopt = opt;
-                  }
+                  c = ldcg_struct(A.ci_fast + li[a]);
+                  jj = lj[t2 - static_cast<long long>(a) * ncj];
+                  valid = true;
                 }
+              }
+              hit = wik_full_half(w, c, jj, valid, sub, half, &opt);
+              if (hit) {
+                bm = mm;
+                bo = t2;
+                bopt = opt;
               }
               if (__syncthreads_or(hit)) break;
             }
             __syncthreads();
+            if (prof) {
+              const long long ps3 = clock64();
+              A.prof[10] += ps1 - c2;  // screening (first round)
+              A.prof[11] += ps3 - ps1;  // rank + evaluation waves
+              A.prof[12] += nc;
+            }
             if (!more) break;
           }
         } else
@@ -1894,8 +1997,8 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
   if (profile) {
     long long hp[16];
     copy_to_host(ctx, hp, prof.p, sizeof(hp));
-    std::fprintf(stderr, "[filter] max cycles: walk %lld | thread max %lld, barrier sum %lld, "
-                 "seg-1 candidates %lld\n", hp[11], hp[12], hp[13], hp[14]);
+    std::fprintf(stderr, "[pairs] screening %lld, rank+eval %lld cycles; screened %lld\n", hp[10],
+                 hp[11], hp[12]);
     std::fprintf(stderr,
                  "[pass] m=%d attempts=%lld pairs=%lld cyc: filter %lld compact %lld pairs %lld "
                  "wait %lld publish %lld barrier %lld | max ci-load %lld max eval %lld\n",
