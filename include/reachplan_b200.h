@@ -315,6 +315,13 @@ rp_status rp_solution_set_pose(const rp_solution_set* s, int64_t k, rp_pose* pos
  * (nullable) holds wps_per_pose xyz triples per pose. */
 rp_status rp_solution_set_poses(const rp_solution_set* s, int64_t first, int64_t count,
                                 rp_pose* poses, double* waypoints, int32_t wps_per_pose);
+/* Mean polyline deviation (mean_polyline_deviation, src/path_planner.cpp:76-87)
+ * of solutions [first, first+count)'s traversal waypoints (segments 1-3, the
+ * candidate tip path) from poly[n_poly] -- the score alternate_candidates
+ * (src/path_planner.cpp:612-663) ranks by, computed by the same device
+ * kernels the planner uses. */
+rp_status rp_solution_set_deviations(rp_solution_set* s, const double* poly, int32_t n_poly,
+                                     int64_t first, int64_t count, double* out);
 /* Shortcut k; tip waypoints (root excluded) into wps (ShortcutPath::tip_waypoints). */
 rp_status rp_solution_set_shortcut(const rp_solution_set* s, int64_t k, rp_shortcut* sc,
                                    double* tip_wps, int32_t cap_wps, int32_t* n_wps);

@@ -87,6 +87,8 @@ def lib():
         "rp_solution_set_sizes": ([vp, P(C.c_int64), P(C.c_int64)], C.c_int32),
         "rp_solution_set_keys": ([vp, vp, C.c_int64], C.c_int32),
         "rp_solution_set_pose": ([vp, C.c_int64, P(abi.Pose), vp, C.c_int32], C.c_int32),
+        "rp_solution_set_poses": ([vp, C.c_int64, C.c_int64, P(abi.Pose), vp, C.c_int32], C.c_int32),
+        "rp_solution_set_deviations": ([vp, vp, C.c_int32, C.c_int64, C.c_int64, vp], C.c_int32),
         "rp_solution_set_shortcut": ([vp, C.c_int64, P(abi.Shortcut), vp, C.c_int32, P(C.c_int32)],
                                      C.c_int32),
         "rp_solution_set_destroy": ([vp], C.c_int32),
@@ -375,6 +377,24 @@ class SolutionSet:
         buf = np.zeros((64 * self.n_samples, 3))
         _check(lib().rp_solution_set_pose(self.h, k, C.byref(p), buf.ctypes.data, 64 * self.n_samples))
         return p, buf[:p.n_waypoints].copy()
+
+    def poses(self, first, count):
+        """Solutions [first, first+count): (rp_pose array, waypoints [count, 64 n, 3])."""
+        wpp = 64 * self.n_samples
+        ps = (abi.Pose * max(1, count))()
+        buf = np.zeros((max(1, count), wpp, 3))
+        _check(lib().rp_solution_set_poses(self.h, first, count, ps, buf.ctypes.data, wpp))
+        return ps[:count], buf[:count]
+
+    def deviations(self, poly, first=0, count=None):
+        """mean_polyline_deviation of each solution's traversal from `poly`
+        (the planner's alternate ranking score), computed on the device."""
+        count = self.sizes()[0] - first if count is None else count
+        b = np.ascontiguousarray(poly, np.float64).reshape(-1, 3)
+        out = np.zeros(max(1, count))
+        _check(lib().rp_solution_set_deviations(self.h, b.ctypes.data, len(b), first, count,
+                                                out.ctypes.data))
+        return out[:count]
 
     def shortcut(self, k):
         s = abi.Shortcut()

@@ -1579,53 +1579,87 @@ __global__ void k_score_solutions(SolveDev a, const SurvDev* __restrict__ sv,
 /// The failed path as a per-launch table in the kernel-parameter constant
 /// bank: segment start a, direction ab = b - a, end a + 1*ab and |ab|^2,
 /// all computed on the host with the same fp64 operations the reference
-/// performs inside point_to_segment.
+/// performs inside point_to_segment; plus an fp32 copy (a, ab, 1/|ab|^2) for
+/// the screening pass and the screen's error-bound constant.
 constexpr int kPolyMax = 32;  // segments (waypoints <= 33)
 struct PolyTable {
   int nseg;
+  float screen_c;  // max_i (|a_i|_1 + |ab_i|_1), rounded up
   double p0x, p0y, p0z;
   double ax[kPolyMax], ay[kPolyMax], az[kPolyMax];
   double bx[kPolyMax], by[kPolyMax], bz[kPolyMax];
   double ex[kPolyMax], ey[kPolyMax], ez[kPolyMax];
   double len2[kPolyMax];
+  float fax[kPolyMax], fay[kPolyMax], faz[kPolyMax];
+  float fbx[kPolyMax], fby[kPolyMax], fbz[kPolyMax];
+  float finv[kPolyMax];
 };
 
-/// polyline_dist with identical results: sqrt is monotone and correctly
-/// rounded, so min_i sqrt(d_i^2) == sqrt(min_i d_i^2); the clamp of
-/// t = dot/len2 is decided from the signs of dot and len2 - dot (dot <= 0
-/// gives t in {-0, 0}, dot >= len2 gives t = 1), so the IEEE division runs
-/// only for interior projections, where it is computed exactly as written.
+/// point_to_segment^2 for table segment i exactly as the reference computes
+/// it (src/path_planner.cpp point_to_segment): the clamp of t = dot/len2 is
+/// decided from the signs of dot and len2 - dot (dot <= 0 gives t in
+/// {-0, 0}, dot >= len2 gives t = 1), so the IEEE division runs only for
+/// interior projections, where it is computed exactly as written.
+__device__ __forceinline__ double seg_sq_exact(V3 p, const PolyTable& T, int i) {
+  const double wx = p.x - T.ax[i], wy = p.y - T.ay[i], wz = p.z - T.az[i];
+  const double len2 = T.len2[i];
+  if (len2 <= 1e-30) return (wx * wx + wy * wy) + wz * wz;
+  const double dot = (wx * T.bx[i] + wy * T.by[i]) + wz * T.bz[i];
+  if (dot <= 0.0) return (wx * wx + wy * wy) + wz * wz;
+  if (dot >= len2) {
+    const double dx = p.x - T.ex[i], dy = p.y - T.ey[i], dz = p.z - T.ez[i];
+    return (dx * dx + dy * dy) + dz * dz;
+  }
+  const double t = rpd::clampd(dot / len2, 0.0, 1.0);
+  const double dx = p.x - (T.ax[i] + t * T.bx[i]);
+  const double dy = p.y - (T.ay[i] + t * T.by[i]);
+  const double dz = p.z - (T.az[i] + t * T.bz[i]);
+  return (dx * dx + dy * dy) + dz * dz;
+}
+
+/// polyline_dist with identical results. sqrt is monotone and correctly
+/// rounded, so min_i sqrt(d_i^2) == sqrt(min_i d_i^2), and only the minimum
+/// VALUE matters, so any segment that provably cannot hold it may be
+/// skipped. A branch-free fp32 pass computes every segment's squared
+/// distance s_i to within e of the exact one (error analysis in DESIGN.md:
+/// e <= 10 u M^2, u = 2^-24, M = |p|_1 + |a_i|_1 + |ab_i|_1; the clamped
+/// projection parameter only enters to second order); the segment holding
+/// the true minimum then has s_i <= min_j s_j + 2e, so the exact fp64
+/// formula runs only on segments inside that band (tol = 64 u M^2, >3x
+/// margin) -- usually one or two per point.
+template <int NS>
 __device__ __forceinline__ double polyline_dist_tab(V3 p, const PolyTable& T) {
   double best;
   {
     const double dx = p.x - T.p0x, dy = p.y - T.p0y, dz = p.z - T.p0z;
     best = (dx * dx + dy * dy) + dz * dz;
   }
+  const float px = static_cast<float>(p.x), py = static_cast<float>(p.y),
+              pz = static_cast<float>(p.z);
+  // branch-free over NS >= nseg entries (the host pads the table with a
+  // far-away segment whose screen value is +inf), so the segments interleave
+  float sq[NS];
+  float lo = INFINITY;
 #pragma unroll
-  for (int i = 0; i < kPolyMax; ++i) {
-    if (i < T.nseg) {
-      const double wx = p.x - T.ax[i], wy = p.y - T.ay[i], wz = p.z - T.az[i];
-      double sq;
-      const double len2 = T.len2[i];
-      if (len2 <= 1e-30) {
-        sq = (wx * wx + wy * wy) + wz * wz;
-      } else {
-        const double dot = (wx * T.bx[i] + wy * T.by[i]) + wz * T.bz[i];
-        if (dot <= 0.0) {
-          sq = (wx * wx + wy * wy) + wz * wz;
-        } else if (dot >= len2) {
-          const double dx = p.x - T.ex[i], dy = p.y - T.ey[i], dz = p.z - T.ez[i];
-          sq = (dx * dx + dy * dy) + dz * dz;
-        } else {
-          const double t = rpd::clampd(dot / len2, 0.0, 1.0);
-          const double dx = p.x - (T.ax[i] + t * T.bx[i]);
-          const double dy = p.y - (T.ay[i] + t * T.by[i]);
-          const double dz = p.z - (T.az[i] + t * T.bz[i]);
-          sq = (dx * dx + dy * dy) + dz * dz;
-        }
-      }
-      best = sq < best ? sq : best;
-    }
+  for (int i = 0; i < NS; ++i) {
+    const float wx = px - T.fax[i], wy = py - T.fay[i], wz = pz - T.faz[i];
+    const float dot = fmaf(wz, T.fbz[i], fmaf(wy, T.fby[i], wx * T.fbx[i]));
+    const float t = fminf(fmaxf(dot * T.finv[i], 0.0f), 1.0f);
+    const float dx = fmaf(-t, T.fbx[i], wx), dy = fmaf(-t, T.fby[i], wy),
+                dz = fmaf(-t, T.fbz[i], wz);
+    sq[i] = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+    lo = fminf(lo, sq[i]);
+  }
+  const float m = (fabsf(px) + fabsf(py)) + fabsf(pz) + T.screen_c;
+  const float thr = lo + (64.0f * 5.9604645e-8f) * 1.0001f * (m * m);
+  unsigned cand = 0;
+#pragma unroll
+  for (int i = 0; i < NS; ++i) cand |= (sq[i] <= thr ? 1u : 0u) << i;
+  while (cand) {
+    const int i = __ffs(cand) - 1;
+    cand &= cand - 1;
+    const double e = seg_sq_exact(p, T, i);
+    best = e < best ? e : best;
   }
   return sqrt(best);
 }
@@ -1634,6 +1668,7 @@ __device__ __forceinline__ double polyline_dist_tab(V3 p, const PolyTable& T) {
 /// point (replan tip lists) and the n samples of segment 1, accumulated in
 /// the reference's order, so k_score_solutions_tab continues each sum
 /// exactly where the per-solution loop would be.
+template <int NS>
 __global__ void __launch_bounds__(256) k_score_rows(SolveDev a, const SurvDev* __restrict__ sv, int S1,
                                                     const __grid_constant__ PolyTable T, int has_lead,
                                                     V3 lead, double* __restrict__ row_acc) {
@@ -1641,9 +1676,9 @@ __global__ void __launch_bounds__(256) k_score_rows(SolveDev a, const SurvDev* _
   if (s >= S1) return;
   const SurvDev& h = sv[s];
   double acc = 0.0;
-  if (has_lead) acc += polyline_dist_tab(lead, T);
+  if (has_lead) acc += polyline_dist_tab<NS>(lead, T);
   const V3 diff = h.p1 - h.link_start;
-  for (int k = 1; k <= a.n; ++k) acc += polyline_dist_tab(rpd::walk_sample(h.link_start, diff, k, a.n), T);
+  for (int k = 1; k <= a.n; ++k) acc += polyline_dist_tab<NS>(rpd::walk_sample(h.link_start, diff, k, a.n), T);
   row_acc[s] = acc;
 }
 
@@ -1651,6 +1686,7 @@ __global__ void __launch_bounds__(256) k_score_rows(SolveDev a, const SurvDev* _
 /// kPolyMax) and the row-only prefix of each sum from k_score_rows;
 /// bit-identical deviations. (A per-segment bounding-box skip measured
 /// 2.2x slower: it breaks the unrolled constant-operand stream.)
+template <int NS>
 __global__ void __launch_bounds__(256) k_score_solutions_tab(
     SolveDev a, const SurvDev* __restrict__ sv, const long long* __restrict__ keys, int64_t count,
     const __grid_constant__ PolyTable T, int has_lead, const double* __restrict__ row_acc,
@@ -1675,12 +1711,12 @@ __global__ void __launch_bounds__(256) k_score_solutions_tab(
   const int cnt = (has_lead ? 1 : 0) + 3 * a.n;
   {
     const V3 diff = p2 - link2;
-    for (int k = 1; k <= a.n; ++k) acc += polyline_dist_tab(rpd::walk_sample(link2, diff, k, a.n), T);
+    for (int k = 1; k <= a.n; ++k) acc += polyline_dist_tab<NS>(rpd::walk_sample(link2, diff, k, a.n), T);
   }
   {
     const V3 b = a.bpts[bi];
     const V3 diff = b - p2;
-    for (int k = 1; k <= a.n; ++k) acc += polyline_dist_tab(rpd::walk_sample(p2, diff, k, a.n), T);
+    for (int k = 1; k <= a.n; ++k) acc += polyline_dist_tab<NS>(rpd::walk_sample(p2, diff, k, a.n), T);
   }
   const double dev = acc / static_cast<double>(cnt);
   dev_bits[t] = __double_as_longlong(dev);
@@ -2178,6 +2214,67 @@ int Planner::valid_poses(const DevPose* poses, int count) {
   return h == INT_MAX ? -1 : h;
 }
 
+/// Mean polyline deviation of every solution's traversal (segments 1-3,
+/// the reach pose's candidate_tip_path) from `poly`, as ordered bits of the
+/// fp64 value, with ordinals ord_base + t (alternate_candidates' scores,
+/// src/path_planner.cpp:612-663, and mean_polyline_deviation, :76-87).
+void score_set_solutions(rp_ctx* ctx, rp_solution_set* set, const std::vector<V3>& poly,
+                         const V3* dpoly, bool lead, V3 lead_pt, unsigned long long* dev_bits,
+                         long long* ord, long long ord_base) {
+  cudaStream_t st = ctx->stream;
+  const int64_t nsol = set->n_solutions;
+  const long long ns = ord_base;
+  ensure_keys(set);
+  static const bool no_tab = std::getenv("RP_SCORE_PLAIN") != nullptr;
+  if (poly.size() >= 2 && poly.size() - 1 <= static_cast<size_t>(kPolyMax) && !no_tab) {
+    PolyTable T{};
+    T.nseg = static_cast<int>(poly.size()) - 1;
+    T.p0x = poly[0].x;
+    T.p0y = poly[0].y;
+    T.p0z = poly[0].z;
+    for (int i = 0; i < T.nseg; ++i) {
+      const V3 a = poly[i], ab = poly[i + 1] - poly[i];
+      const V3 e = a + 1.0 * ab;
+      T.ax[i] = a.x; T.ay[i] = a.y; T.az[i] = a.z;
+      T.bx[i] = ab.x; T.by[i] = ab.y; T.bz[i] = ab.z;
+      T.ex[i] = e.x; T.ey[i] = e.y; T.ez[i] = e.z;
+      T.len2[i] = rpd::sqnorm(ab);
+      T.fax[i] = static_cast<float>(a.x); T.fay[i] = static_cast<float>(a.y);
+      T.faz[i] = static_cast<float>(a.z);
+      T.fbx[i] = static_cast<float>(ab.x); T.fby[i] = static_cast<float>(ab.y);
+      T.fbz[i] = static_cast<float>(ab.z);
+      T.finv[i] = T.len2[i] > 1e-30 ? static_cast<float>(1.0 / T.len2[i]) : 0.0f;
+      const double c = std::fabs(a.x) + std::fabs(a.y) + std::fabs(a.z) + std::fabs(ab.x) +
+                       std::fabs(ab.y) + std::fabs(ab.z);
+      T.screen_c = std::max(T.screen_c, static_cast<float>(c * (1.0 + 1e-6)));
+    }
+    for (int i = T.nseg; i < kPolyMax; ++i) {  // screen value +inf, never a candidate
+      T.fax[i] = T.fay[i] = T.faz[i] = 1e30f;
+      T.fbx[i] = T.fby[i] = T.fbz[i] = T.finv[i] = 0.0f;
+    }
+    DevBuf<double> row_acc(std::max(1, set->S1), st);
+    auto run = [&](auto rows, auto sols) {
+      launch(ctx, "score", rows, dim3(nblk(std::max(1, set->S1), 256)), dim3(256), 0, set->sd,
+             static_cast<const SurvDev*>(set->surv.p), set->S1, T, lead ? 1 : 0, lead_pt,
+             row_acc.p);
+      launch(ctx, "score", sols, dim3(nblk(nsol, 256)), dim3(256), 0, set->sd,
+             static_cast<const SurvDev*>(set->surv.p), static_cast<const long long*>(set->keys.p),
+             nsol, T, lead ? 1 : 0, static_cast<const double*>(row_acc.p), dev_bits, ord,
+             static_cast<long long>(ns));
+    };
+    if (T.nseg <= 8) run(k_score_rows<8>, k_score_solutions_tab<8>);
+    else if (T.nseg <= 16) run(k_score_rows<16>, k_score_solutions_tab<16>);
+    else if (T.nseg <= 24) run(k_score_rows<24>, k_score_solutions_tab<24>);
+    else run(k_score_rows<32>, k_score_solutions_tab<32>);
+  } else {
+    launch(ctx, "score", k_score_solutions, dim3(nblk(nsol, 256)), dim3(256),
+           poly.size() * sizeof(V3), set->sd, static_cast<const SurvDev*>(set->surv.p),
+           static_cast<const long long*>(set->keys.p), nsol, dpoly,
+           static_cast<int>(poly.size()), lead ? 1 : 0, lead_pt, dev_bits, ord,
+           static_cast<long long>(ns));
+  }
+}
+
 /// Scores of (shortcut tip lists, solutions) against a polyline, sorted by
 /// (deviation, ordinal); returns the ordinals in sorted order.
 std::vector<long long> Planner::rank_by_deviation(rp_solution_set* set,
@@ -2213,38 +2310,9 @@ std::vector<long long> Planner::rank_by_deviation(rp_solution_set* set,
            static_cast<const V3*>(dpts.p), static_cast<const int*>(doffs.p), static_cast<int>(ns),
            static_cast<const V3*>(dpoly.p), static_cast<int>(poly.size()), dev.p, ord.p);
   }
-  if (nsol > 0) {
-    ensure_keys(set);
-    static const bool no_tab = std::getenv("RP_SCORE_PLAIN") != nullptr;
-    if (poly.size() >= 2 && poly.size() - 1 <= static_cast<size_t>(kPolyMax) && !no_tab) {
-      PolyTable T{};
-      T.nseg = static_cast<int>(poly.size()) - 1;
-      T.p0x = poly[0].x;
-      T.p0y = poly[0].y;
-      T.p0z = poly[0].z;
-      for (int i = 0; i < T.nseg; ++i) {
-        const V3 a = poly[i], ab = poly[i + 1] - poly[i];
-        const V3 e = a + 1.0 * ab;
-        T.ax[i] = a.x; T.ay[i] = a.y; T.az[i] = a.z;
-        T.bx[i] = ab.x; T.by[i] = ab.y; T.bz[i] = ab.z;
-        T.ex[i] = e.x; T.ey[i] = e.y; T.ez[i] = e.z;
-        T.len2[i] = rpd::sqnorm(ab);
-      }
-      DevBuf<double> row_acc(std::max(1, set->S1), st);
-      launch(ctx, "score", k_score_rows, dim3(nblk(std::max(1, set->S1), 256)), dim3(256), 0,
-             set->sd, static_cast<const SurvDev*>(set->surv.p), set->S1, T, lead ? 1 : 0, lead_pt,
-             row_acc.p);
-      launch(ctx, "score", k_score_solutions_tab, dim3(nblk(nsol, 256)), dim3(256), 0, set->sd,
-             static_cast<const SurvDev*>(set->surv.p), static_cast<const long long*>(set->keys.p),
-             nsol, T, lead ? 1 : 0, static_cast<const double*>(row_acc.p), dev.p + ns, ord.p + ns,
-             static_cast<long long>(ns));
-    } else
-    launch(ctx, "score", k_score_solutions, dim3(nblk(nsol, 256)), dim3(256),
-           poly.size() * sizeof(V3), set->sd, static_cast<const SurvDev*>(set->surv.p),
-           static_cast<const long long*>(set->keys.p), nsol, static_cast<const V3*>(dpoly.p),
-           static_cast<int>(poly.size()), lead ? 1 : 0, lead_pt, dev.p + ns, ord.p + ns,
-           static_cast<long long>(ns));
-  }
+  if (nsol > 0)
+    score_set_solutions(ctx, set, poly, static_cast<const V3*>(dpoly.p), lead, lead_pt, dev.p + ns,
+                        ord.p + ns, static_cast<long long>(ns));
   size_t tb = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tb, dev.p, dev_sorted.p, ord.p, ord_sorted.p,
                                   static_cast<int>(total), 0, 64, st);
@@ -2265,6 +2333,28 @@ std::vector<long long> Planner::rank_by_deviation(rp_solution_set* set,
 }  // namespace rp
 
 using namespace rp;
+
+/// Deviation scores of solutions [first, first + count) against a polyline
+/// (the quantity alternate_candidates ranks by, src/path_planner.cpp:612-663).
+extern "C" rp_status rp_solution_set_deviations(rp_solution_set* set, const double* poly,
+                                                int32_t n_poly, int64_t first, int64_t count,
+                                                double* out) {
+  return guarded([&] {
+    if (n_poly < 1 || first < 0 || count < 0 || first + count > set->n_solutions)
+      fail(RP_E_INVALID_PARAMETER, "deviation range or polyline");
+    if (count == 0) return;
+    rp_ctx* ctx = set->ctx;
+    cudaStream_t st = ctx->stream;
+    std::vector<V3> pl(n_poly);
+    std::memcpy(pl.data(), poly, n_poly * sizeof(V3));
+    DevBuf<V3> dpoly(n_poly, st);
+    copy_to_device(ctx, dpoly.p, pl.data(), n_poly * sizeof(V3));
+    DevBuf<unsigned long long> dev(set->n_solutions, st);
+    DevBuf<long long> ord(set->n_solutions, st);
+    score_set_solutions(ctx, set, pl, dpoly.p, false, V3{0, 0, 0}, dev.p, ord.p, 0);
+    copy_to_host(ctx, out, dev.p + first, count * sizeof(double));
+  });
+}
 
 /// validate_plan (src/validate.cpp:53-108): every check on the device
 /// (k_validate_plan), the report assembled here in the reference's order

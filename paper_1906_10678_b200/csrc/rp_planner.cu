@@ -6,6 +6,9 @@
 #include "rp_planner.hpp"
 
 #include <algorithm>
+#include <climits>
+#include <condition_variable>
+#include <mutex>
 #include <exception>
 #include <thread>
 #include <functional>
@@ -89,11 +92,15 @@ struct PassResult {
   std::vector<std::string> notes;
 };
 
+struct Build;
 struct Failure {
   Cand candidate;
   std::vector<V3> waypoints;
   int blocked_index = -1;
   std::string reason;
+  // the candidate's build (make_candidate_build is a pure function of the
+  // candidate, so the cascade's attempts on it reuse this one)
+  std::shared_ptr<const Build> build;
 };
 
 /// backward_pass (src/path_planner.cpp:322-400)
@@ -287,22 +294,24 @@ struct Attempt {
 };
 
 /// attempt_candidate (src/path_planner.cpp:580-602)
-Attempt attempt_candidate(Planner& P, const Cand& cand, V3 target, const PassOptions& opt) {
+Attempt attempt_candidate(Planner& P, const Cand& cand, V3 target, const PassOptions& opt,
+                          const Build* prebuilt = nullptr) {
   HostSpan span_("attempt_candidate");
   Attempt r;
-  Build b = make_candidate_build(P, cand, target);
+  const Build b = prebuilt ? *prebuilt : make_candidate_build(P, cand, target);
   if (!b.ok) {
     r.failure = {cand, b.waypoints, -1, b.fail_reason};
     return r;
   }
   PassResult pass = backward_pass(P, b.waypoints, b.anchor, opt);
   if (!pass.ok) {
-    r.failure = {cand, b.waypoints, pass.failed_index, "no pose at waypoint"};
+    r.failure = {cand, b.waypoints, pass.failed_index, "no pose at waypoint",
+                 std::make_shared<const Build>(b)};
     return r;
   }
   auto unfold = P.interpolate(nullptr, pass.poses[0], P.pp.unfold_steps);
   if (!unfold) {
-    r.failure = {cand, b.waypoints, 0, "unfold blocked"};
+    r.failure = {cand, b.waypoints, 0, "unfold blocked", std::make_shared<const Build>(b)};
     return r;
   }
   r.plan = assemble(std::move(pass), std::move(*unfold), b.kind);
@@ -415,7 +424,7 @@ std::unique_ptr<rp_solution_set> try_solve(rp_ctx* ctx, const rp_arm& arm, const
 /// Step 3 of fallback_cascade (src/path_planner.cpp:786-820): virtual-arm
 /// detours from the blocked waypoint.
 rp_plan* fallback_detour(Planner& P, const Failure& failure, V3 target, const PassOptions& cloud) {
-  Build b = make_candidate_build(P, failure.candidate, target);
+  const Build b = failure.build ? *failure.build : make_candidate_build(P, failure.candidate, target);
   if (b.ok && failure.blocked_index > 0 && !failure.waypoints.empty()) {
     const V3 path_target = tracked_point(b.anchor);
     std::vector<V3> work(failure.waypoints.begin(),
@@ -499,6 +508,7 @@ std::vector<Slot<R>> run_parallel(Planner& P, int n, const std::function<R(Plann
 struct Job {
   const Cand* cand;
   const PassOptions* opt;
+  const Build* prebuilt = nullptr;
 };
 struct WindowResult {
   Attempt attempt;
@@ -512,7 +522,9 @@ std::vector<WindowResult> run_window(Planner& P, const std::vector<Job>& jobs, V
                                      const std::function<void()>& main_side) {
   std::vector<Slot<Attempt>> r = run_parallel<Attempt>(
       P, static_cast<int>(jobs.size()),
-      [&](Planner& W, int k) { return attempt_candidate(W, *jobs[k].cand, target, *jobs[k].opt); },
+      [&](Planner& W, int k) {
+        return attempt_candidate(W, *jobs[k].cand, target, *jobs[k].opt, jobs[k].prebuilt);
+      },
       main_side);
   std::vector<WindowResult> out(r.size());
   for (size_t k = 0; k < r.size(); ++k) {
@@ -542,6 +554,123 @@ rp_plan* first_in_order(std::vector<WindowResult>& w) {
   return found;
 }
 
+/// Steps 1a (escalation), 1b (target cloud) and 2 (alternate solutions) of
+/// the cascade as one ordered job list drained by `width` worker contexts
+/// (own stream and Planner each): the first two jobs start at once, the
+/// alternates are appended when the main thread has ranked them (on the
+/// main stream, concurrently) and run in groups of `width`, and a job is
+/// skipped once an earlier one has decided the outcome. Every attempt is a pure function of (candidate,
+/// options), so the lowest-index success -- or the lowest-index error
+/// before any success -- is exactly what the reference's sequential loop
+/// returns (src/path_planner.cpp:740-785). Returns the winning job index
+/// and plan, or (-1, nullptr) when every job failed.
+std::pair<int, rp_plan*> cascade_pool(Planner& P, const Failure& failure, rp_solution_set* set,
+                                      V3 target, const PassOptions& esc, const PassOptions& cloud,
+                                      int width) {
+  const Cand& failed = failure.candidate;
+  const Build* pre = failure.build.get();
+  HostSpan span_("cascade_pool");
+  std::mutex m;
+  std::condition_variable cv;
+  std::vector<Cand> alts;
+  std::vector<Job> jobs{{&failed, &esc, pre}, {&failed, &cloud, pre}};
+  jobs.reserve(64);
+  std::vector<Slot<Attempt>> res(2);
+  std::vector<char> done(2, 0);
+  bool closed = false;
+  size_t next = 0;
+  size_t decided = SIZE_MAX;  // lowest index that succeeded or threw
+  std::vector<rp_ctx*> ws;
+  for (int k = 0; k < width; ++k) ws.push_back(worker_ctx(P.ctx, k));
+  std::vector<std::thread> threads;
+  for (int k = 0; k < width; ++k) {
+    threads.emplace_back([&, k] {
+      std::unique_ptr<Planner> W;
+      std::unique_lock<std::mutex> lk(m);
+      // alternates run in groups of `width`; group g >= 1 starts only when
+      // every earlier job has finished, so no attempt is started that the
+      // outcome of a running one could make moot (none can be cancelled)
+      auto startable = [&] {
+        if (next >= jobs.size()) return closed;
+        if (next < 2) return true;
+        const size_t g = (next - 2) / width;
+        if (g == 0) return true;
+        const size_t lim = 2 + g * width;
+        for (size_t i = 0; i < lim; ++i)
+          if (!done[i]) return false;
+        return true;
+      };
+      for (;;) {
+        cv.wait(lk, startable);
+        if (next >= jobs.size()) return;
+        const size_t j = next++;
+        if (j > decided) {
+          done[j] = 1;
+          cv.notify_all();
+          continue;
+        }
+        const Job job = jobs[j];
+        lk.unlock();
+        Slot<Attempt> out;
+        try {
+          if (!W) {
+            RP_CUDA(cudaSetDevice(P.ctx->device));
+            W = std::make_unique<Planner>(ws[k], P.arm, P.q, P.g, P.rp, P.pp_in);
+            const int share = P.ctx->sm_count / width;
+            W->bp_blocks_cap = share >= 16 ? (share & ~15) : std::max(1, share);
+          }
+          out.value = attempt_candidate(*W, *job.cand, target, *job.opt, job.prebuilt);
+        } catch (...) {
+          out.error = std::current_exception();
+        }
+        lk.lock();
+        if ((out.value.plan || out.error) && j < decided) decided = j;
+        res[j] = std::move(out);
+        done[j] = 1;
+        cv.notify_all();
+      }
+    });
+  }
+  std::exception_ptr main_error;
+  try {
+    alts = alternate_candidates(P, set, failed, target);
+  } catch (...) {
+    main_error = std::current_exception();
+  }
+  {
+    std::lock_guard<std::mutex> lk(m);
+    if (!main_error) {
+      for (const Cand& c : alts) jobs.push_back({&c, &cloud});
+      res.resize(jobs.size());
+      done.resize(jobs.size(), 0);
+    }
+    closed = true;
+  }
+  cv.notify_all();
+  for (auto& t : threads) t.join();
+  for (rp_ctx* w : ws) ctx_absorb(P.ctx, w);
+  int win = -1;
+  rp_plan* plan = nullptr;
+  std::exception_ptr err;
+  for (size_t j = 0; j < res.size(); ++j) {
+    if (win < 0 && !err) {
+      if (res[j].error) err = res[j].error;
+      else if (res[j].value.plan) {
+        win = static_cast<int>(j);
+        plan = res[j].value.plan;
+        continue;
+      }
+    }
+    delete res[j].value.plan;
+  }
+  if (err) {
+    delete plan;
+    std::rethrow_exception(err);
+  }
+  if (win < 0 && main_error) std::rethrow_exception(main_error);
+  return {win, plan};
+}
+
 // concurrent attempts per window; each pass then takes sm_count / width
 // blocks (rounded down to 16) so all of them stay co-resident
 static int cascade_width() {
@@ -566,9 +695,24 @@ rp_plan* fallback_cascade(Planner& P, const Failure& failure, rp_solution_set* s
     PassOptions cloud = esc;
     cloud.cloud = true;
     cloud.cloud_radius = 2.0 * P.pp.eps_wp;
+    static const bool windows = std::getenv("RP_CASCADE_WINDOWS") != nullptr;
+    if (!windows) {
+      const auto [win, plan] =
+          cascade_pool(P, failure, set, target, esc, cloud, cascade_width());
+      if (plan) {
+        plan->notes.push_back(win == 0   ? "fallback: relaxation escalation"
+                              : win == 1 ? "fallback: target cloud"
+                                         : "fallback: alternate solution");
+        return plan;
+      }
+      return fallback_detour(P, failure, target, cloud);
+    }
     std::vector<Cand> alts;
     std::vector<WindowResult> w = run_window(
-        P, {{&failure.candidate, &esc}, {&failure.candidate, &cloud}}, target,
+        P,
+        {{&failure.candidate, &esc, failure.build.get()},
+         {&failure.candidate, &cloud, failure.build.get()}},
+        target,
         [&] { alts = alternate_candidates(P, set, failure.candidate, target); });
     const bool esc_ok = w[0].attempt.plan != nullptr && !w[0].error;
     if (rp_plan* plan = first_in_order(w)) {
@@ -588,7 +732,7 @@ rp_plan* fallback_cascade(Planner& P, const Failure& failure, rp_solution_set* s
     return fallback_detour(P, failure, target, cloud);
   }
   {
-    Attempt r = attempt_candidate(P, failure.candidate, target, esc);
+    Attempt r = attempt_candidate(P, failure.candidate, target, esc, failure.build.get());
     if (r.plan) {
       r.plan->notes.push_back("fallback: relaxation escalation");
       return r.plan;
@@ -598,7 +742,7 @@ rp_plan* fallback_cascade(Planner& P, const Failure& failure, rp_solution_set* s
   cloud.cloud = true;
   cloud.cloud_radius = 2.0 * P.pp.eps_wp;
   {
-    Attempt r = attempt_candidate(P, failure.candidate, target, cloud);
+    Attempt r = attempt_candidate(P, failure.candidate, target, cloud, failure.build.get());
     if (r.plan) {
       r.plan->notes.push_back("fallback: target cloud");
       return r.plan;

@@ -151,3 +151,47 @@ def test_error_classes(ctx):
     with pytest.raises(api.ReachplanError) as e:
         api.Grid.build(ctx, (0, 0, 0), (10, 10, 10), 0.001)
     assert e.value.code == abi.RP_E_CAPACITY_EXCEEDED
+
+
+def _traversal(S, k):
+    p, w = S.pose(k)
+    return w[: min(3, p.n_segments) * S.n_samples]
+
+
+@pytest.mark.parametrize("name,deg", [("C2", 5.0), ("C1", 5.0)])
+def test_alternate_scores_bitexact(ctx, name, deg):
+    """The device deviation score the planner ranks alternates by
+    (alternate_candidates, src/path_planner.cpp:612-663: fp32 screen +
+    exact fp64 on the band) equals mean_polyline_deviation
+    (src/path_planner.cpp:76-87) bit for bit, over polylines that hit the
+    edge cases: zero-length segments, samples lying on vertices (distance
+    0), the 32-segment table limit and the plain-kernel path beyond it."""
+    api = _api()
+    sc = scenes.config(name, quiver_deg=deg)
+    arm, rp, q, g = gpu_problem(ctx, sc)
+    S = api.solve_reach(ctx, arm, q, g, sc.target, rp)
+    ns, _ = S.sizes()
+    assert ns > 0
+    rng = np.random.default_rng(7)
+    t0 = _traversal(S, 0)
+    tm = _traversal(S, ns // 2)
+    polys = {
+        "failed": t0,
+        "degenerate": np.concatenate([tm[:5], tm[4:5], tm[4:5], tm[5:]]),
+        "through": tm,
+        "random33": rng.uniform(-1.2, 1.2, (33, 3)),
+        "random40": rng.uniform(-1.2, 1.2, (40, 3)),
+        "two": np.array([sc.target, (0.0, 0.0, 0.3)]),
+        "point": np.array([sc.target]),
+    }
+    w = min(600, ns)
+    windows = sorted({0, max(0, ns // 2 - w // 2), ns - w})
+    for label, poly in polys.items():
+        for lo in windows:
+            dev = S.deviations(poly, lo, w)
+            ps, wps = S.poses(lo, w)
+            for k in range(w):
+                trav = wps[k][: min(3, ps[k].n_segments) * sc.n_samples]
+                want = ref.mean_polyline_deviation(trav, poly)
+                assert np.float64(dev[k]).tobytes() == np.float64(want).tobytes(), \
+                    (label, lo + k, dev[k], want)
