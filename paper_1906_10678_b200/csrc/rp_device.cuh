@@ -60,6 +60,9 @@ struct GridView {
   double ox, oy, oz;
   double vs;   // voxel_size
   double rvs;  // fl(1/voxel_size), for the exact-floor fast path
+  // floor bracket half-width valid for every |q| <= max(n) + 2 (q = a * rvs):
+  // beyond that a sample is outside the grid whichever integer it floors to
+  double dq;
 };
 
 /// floor(a / vs) exactly as the reference (inc/voxgrid.hpp:46-50): the
@@ -70,8 +73,8 @@ __device__ __forceinline__ int vox_floor(double a, double vs, double rvs) {
   const double q = a * rvs;
   const double d = fabs(q) * 8.9e-16 + 1e-300;
   const double lo = floor(q - d);
-  const double hi = floor(q + d);
-  if (lo == hi) return static_cast<int>(lo);
+  // floor(fl(q + d)) == lo  <=>  fl(q + d) < lo + 1, as fl(q + d) >= fl(q - d) >= lo
+  if (q + d < lo + 1.0) return static_cast<int>(lo);
   return static_cast<int>(floor(a / vs));
 }
 
@@ -142,7 +145,9 @@ __device__ __forceinline__ int walk_first_blocked(const GridView& g, V3 from, V3
 
 /// Blocked-sample mask of a walk of n <= N samples (bit k = sample k+1),
 /// with all N gathers in flight together. Each coordinate's floor takes the
-/// exact-floor fast path; the rare coordinate whose bracket straddles an
+/// exact-floor fast path (with the grid's constant bracket g.dq: a sample
+/// whose |q| exceeds its range is outside the grid on either side of the
+/// bracket, so its verdict is unaffected); the rare coordinate whose bracket straddles an
 /// integer (e.g. a sample exactly on a voxel face: quiver vectors with a
 /// zero component from the root) gets vox_floor's IEEE division in place,
 /// so the loads stay parallel and the mask is the reference's verdict.
@@ -163,15 +168,15 @@ __device__ __forceinline__ uint32_t walk_hits(const GridView& g, V3 from, V3 to,
     const V3 p = from + t * diff;
     const double ax = p.x - g.ox, ay = p.y - g.oy, az = p.z - g.oz;
     const double qx = ax * g.rvs, qy = ay * g.rvs, qz = az * g.rvs;
-    const double dx = fabs(qx) * 8.9e-16 + 1e-300, dy = fabs(qy) * 8.9e-16 + 1e-300,
-                 dz = fabs(qz) * 8.9e-16 + 1e-300;
+    const double dx = g.dq, dy = g.dq, dz = g.dq;
     double lx = floor(qx - dx), ly = floor(qy - dy), lz = floor(qz - dz);
+    // floor(fl(q + d)) == l  <=>  fl(q + d) < l + 1, as fl(q + d) >= fl(q - d) >= l
     if (INPLACE) {
-      if (lx != floor(qx + dx)) lx = floor(ax / g.vs);
-      if (ly != floor(qy + dy)) ly = floor(ay / g.vs);
-      if (lz != floor(qz + dz)) lz = floor(az / g.vs);
+      if (!(qx + dx < lx + 1.0)) lx = floor(ax / g.vs);
+      if (!(qy + dy < ly + 1.0)) ly = floor(ay / g.vs);
+      if (!(qz + dz < lz + 1.0)) lz = floor(az / g.vs);
     } else {
-      ok &= (lx == floor(qx + dx)) & (ly == floor(qy + dy)) & (lz == floor(qz + dz));
+      ok &= (qx + dx < lx + 1.0) & (qy + dy < ly + 1.0) & (qz + dz < lz + 1.0);
     }
     const int ix = static_cast<int>(lx), iy = static_cast<int>(ly), iz = static_cast<int>(lz);
     const bool inb = live & (ix >= 0) & (iy >= 0) & (iz >= 0) & (ix < g.nx) & (iy < g.ny) & (iz < g.nz);

@@ -6,6 +6,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <exception>
 #include <map>
@@ -119,6 +120,7 @@ struct rp_grid {
     v.oz = origin[2];
     v.vs = voxel_size;
     v.rvs = 1.0 / voxel_size;
+    v.dq = (std::max(dims[0], std::max(dims[1], dims[2])) + 2.0) * 8.9e-16 + 1e-300;
     return v;
   }
 };
