@@ -299,6 +299,27 @@ __host__ __device__ __forceinline__ bool self_collision_free(const V3* joints, i
   return true;
 }
 
+/// self_collision_free with a bounding-sphere screen: link k lies in the
+/// ball around its midpoint of radius half[k] (an upper bound of half its
+/// length), so a pair whose midpoints are farther apart than
+/// min_sep + half[i] + half[j] (with margin) is at least min_sep apart and
+/// its exact distance is not needed; every other pair gets
+/// seg_seg_distance. Same verdict as self_collision_free.
+__host__ __device__ __forceinline__ bool self_collision_free_screened(const V3* joints, int n_links,
+                                                                      double min_sep,
+                                                                      const double* half) {
+  for (int i = 0; i + 2 < n_links; ++i)
+    for (int j = i + 2; j < n_links; ++j) {
+      const V3 ci = 0.5 * (joints[i] + joints[i + 1]);
+      const V3 cj = 0.5 * (joints[j] + joints[j + 1]);
+      const double r = min_sep + half[i] + half[j];
+      if (sqnorm(ci - cj) > r * r * (1.0 + 1e-9) + 1e-12) continue;
+      if (seg_seg_distance(joints[i], joints[i + 1], joints[j], joints[j + 1]) < min_sep)
+        return false;
+    }
+  return true;
+}
+
 // ---------------------------------------------------------------------------
 // Frames and joint limits (src/arm_model.cpp:12-70, 195-200). Only used when
 // limits or offsets are active.

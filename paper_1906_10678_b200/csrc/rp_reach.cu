@@ -394,7 +394,10 @@ __global__ void __launch_bounds__(256, 4) k_seg2_rows(SolveDev a, const SurvDev*
       J[2] = J[1] + s2;
       J[3] = J[2] + v3;
       if (EIGHT) J[4] = J[3] + a.L4 * bdir;
-      if (!rpd::self_collision_free(J, EIGHT ? 4 : 3, min_sep)) return;
+      // half-length bounds as in k_bq_tail
+      const double w = 1.0 + 1e-9;
+      const double half[4] = {0.5 * L1 * w, 0.5 * L2 * w, 0.5 * (L3 + a.eps) * w, 0.5 * a.L4 * w};
+      if (!rpd::self_collision_free_screened(J, EIGHT ? 4 : 3, min_sep, half)) return;
       ++c_sol;
       atomicOr(sol_bits + (p >> 5), 1u << (p & 31));
       const double len = (rpd::norm(s1) + rpd::norm(s2)) + rpd::norm(v3);
@@ -1392,6 +1395,9 @@ __global__ void k_walk1(SolveDev a, uint32_t* __restrict__ bits) {
 // ---- multi-query pipeline: every stage covers all targets of a chunk ------
 
 constexpr unsigned kBatchShortcutCap = 1u << 24;  // near-encounter candidates per chunk
+// gap-passing pairs are queued for k_bq_tail in target-tagged blocks of
+// kTailBlock entries taken from a fixed pool (overflow: evaluated in place)
+constexpr int kTailBlock = 256;
 
 struct BatchDev {
   SolveDev a;  // shared constants (target fields unused)
@@ -1413,6 +1419,14 @@ struct BatchDev {
   // ring_off[r] .. ring_off[r+1]-1 at elevation (cos, sin) = (ring_c, ring_s),
   // azimuth 2*pi*m/count; nrings == 0 -> sweep every direction
   int* row_ctr;  // [T] next survivor row (dynamic row assignment in k_bq_seg2)
+  // tail queue: pool[tail_cap * kTailBlock] pair keys s*Q + j, per block its
+  // target and length; tail_ctr = blocks taken (tail_cap == 0: no queue)
+  uint32_t* tail_pool;
+  int* tail_tgt;
+  int* tail_len;
+  unsigned* tail_ctr;
+  int tail_cap;
+  BestRec* tail_best;  // [T] argmin over the queued pairs
   int nrings;
   const int* ring_off;
   const double* ring_c;
@@ -1598,8 +1612,9 @@ __global__ void __launch_bounds__(256, RP_BQ_MINB) k_bq_seg2(BatchDev d) {
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const double rnear = a.near_r + 1e-6;
   (void)npairs;
-  __shared__ int wqs[8][64];
-  int* wq = wqs[threadIdx.x >> 5];
+  // the warp's current tail-queue block (uniform): -2 none taken yet, -1
+  // no pool (or exhausted): evaluate in place
+  int tb = d.tail_cap > 0 ? -2 : -1, tf = 0;
   __shared__ int wiv[8][32 * 8], wive[8][32 * 8];  // per warp: 32 rings x 8 intervals
   __shared__ signed char wniv[8][32];
   __shared__ int wbase[8][32];
@@ -1643,10 +1658,7 @@ __global__ void __launch_bounds__(256, RP_BQ_MINB) k_bq_seg2(BatchDev d) {
       const V3 p2 = p1 + L2 * dir2;
       const V3 v3 = b - p2;
       const double v3_len = rpd::norm(v3);
-      if (fabs(v3_len - L3) > a.eps) return;
-      ++c_gp;
-      if (v3_len < 1e-12) return;
-      ++c_jp;
+      (void)v3_len;  // gap and length tests already passed in visit
       if (rpd::walk_first_blocked(a.g, p2, b, a.n) != 0) return;
       ++c_v3;
       if (!walk4) return;
@@ -1665,12 +1677,13 @@ __global__ void __launch_bounds__(256, RP_BQ_MINB) k_bq_seg2(BatchDev d) {
         best_key = p;
       }
     };
-    int qn = 0;
-    // every lane calls this with its own j (valid or not) in lockstep; the
-    // queue is run 32 at a time, and emptied when `drain` is set. (One call
-    // site each for visit and heavy keeps the kernel's code footprint small:
-    // ncu showed instruction-fetch stalls dominating with inlined copies.)
-    const auto visit = [&](int j, bool valid, bool drain) {
+    // every lane calls this with its own j (valid or not) in lockstep.
+    // Band + clearance passers get the exact gap test here; the pairs that
+    // reach the v3 walk are appended to the warp's block of the tail queue
+    // (k_bq_tail evaluates them with a small code footprint -- ncu showed
+    // instruction-fetch stalls dominating when the tail ran inline) or, if
+    // the pool is exhausted, evaluated in place.
+    const auto visit = [&](int j, bool valid) {
       bool pass = false;
       if (valid) {
         const V3 dir2 = qvec(a, j);
@@ -1686,19 +1699,40 @@ __global__ void __launch_bounds__(256, RP_BQ_MINB) k_bq_seg2(BatchDev d) {
           const double v2 = rpd::sqnorm(b - p2);
           pass = v2 <= a.coarse2 && v2 >= a.band_lo2 &&
                  ((__ldg(crow + (j >> 5)) >> (j & 31)) & 1u);
+          if (pass) {
+            // heavy()'s first tests: v3 = b - p2, |v3| = sqrt(v2)
+            const double v3_len = sqrt(v2);
+            if (fabs(v3_len - L3) > a.eps) {
+              pass = false;
+            } else {
+              ++c_gp;
+              if (v3_len < 1e-12) pass = false;
+              else ++c_jp;
+            }
+          }
         }
       }
       const unsigned m = __ballot_sync(FULL, pass);
-      if (pass) wq[qn + __popc(m & ((1u << lane) - 1u))] = j;
-      qn += __popc(m);
-      __syncwarp();
-      if (qn >= 32 || (drain && qn > 0)) {
-        const int take = qn < 32 ? qn : 32;
-        if (lane < take) heavy(wq[lane]);
-        __syncwarp();
-        if (lane < qn - take) wq[lane] = wq[take + lane];
-        qn -= take;
-        __syncwarp();
+      if (!m) return;
+      const int n = __popc(m);
+      if (tb == -2 || (tb >= 0 && tf + n > kTailBlock)) {  // close the block, take the next
+        int nb = 0;
+        if (lane == 0) {
+          if (tb >= 0) d.tail_len[tb] = tf;
+          nb = static_cast<int>(atomicAdd(d.tail_ctr, 1u));
+          if (nb < d.tail_cap) d.tail_tgt[nb] = t;
+        }
+        nb = __shfl_sync(FULL, nb, 0);
+        tb = nb < d.tail_cap ? nb : -1;
+        tf = 0;
+      }
+      if (tb >= 0) {
+        if (pass)
+          d.tail_pool[static_cast<size_t>(tb) * kTailBlock + tf + __popc(m & ((1u << lane) - 1u))] =
+              static_cast<uint32_t>(static_cast<int64_t>(s) * a.Q + j);
+        tf += n;
+      } else if (pass) {
+        heavy(j);
       }
     };
     // Directions visited: with quiver rings, only those that can pass the
@@ -1791,12 +1825,12 @@ __global__ void __launch_bounds__(256, RP_BQ_MINB) k_bq_seg2(BatchDev d) {
           }
           j = (d.nrings ? d.ring_off[r0 + lo] : 0) + ivs[lo * 8 + k] + rem;
         }
-        visit(j, tt < total, false);
+        visit(j, tt < total);
       }
       __syncwarp();
     }
-    while (qn > 0) visit(0, false, true);
   }
+  if (tb >= 0 && lane == 0) d.tail_len[tb] = tf;
   unsigned long long* c = d.ctr + static_cast<size_t>(t) * C_COUNT;
   warp_flush_t(c, C_SEG2_CLEAR, c_clear);
   warp_flush_t(c, C_GAP_PASS, c_gp);
@@ -1822,9 +1856,117 @@ __global__ void __launch_bounds__(256, RP_BQ_MINB) k_bq_seg2(BatchDev d) {
   }
 }
 
+/// 16-byte compare-and-swap (atom.cas.b128, sm_90+); returns the old value.
+__device__ __forceinline__ BestRec cas_best(BestRec* addr, BestRec cmp, BestRec val) {
+  unsigned long long o0, o1;
+  asm volatile(
+      "{\n\t.reg .b128 c, v, o;\n\t"
+      "mov.b128 c, {%2, %3};\n\t"
+      "mov.b128 v, {%4, %5};\n\t"
+      "atom.global.cas.b128 o, [%6], c, v;\n\t"
+      "mov.b128 {%0, %1}, o;\n\t}"
+      : "=l"(o0), "=l"(o1)
+      : "l"(__double_as_longlong(cmp.len)), "l"(cmp.key), "l"(__double_as_longlong(val.len)),
+        "l"(val.key), "l"(addr)
+      : "memory");
+  return BestRec{__longlong_as_double(static_cast<long long>(o0)), static_cast<long long>(o1)};
+}
+
+__device__ __forceinline__ bool best_less(const BestRec& x, const BestRec& y) {
+  return x.len < y.len || (x.len == y.len && x.key < y.key);
+}
+
+/// The tail of k_bq_seg2's pair test for the queued pairs, one block per
+/// queue block (all of one target): the v3 walk (gathers in flight
+/// together), the fourth-segment verdict and the self-collision check, the
+/// v3-clear / solution counters and the (length, key) argmin -- the same
+/// arithmetic heavy() performs in place.
+template <bool EIGHT>
+__global__ void __launch_bounds__(kTailBlock, 4) k_bq_tail(BatchDev d) {
+  const int c = blockIdx.x;
+  const int t = d.tail_tgt[c];
+  const int len = d.tail_len[c];
+  const SolveDev& a = d.a;
+  const ArmDev& arm = a.arm;
+  const double L1 = arm.L[0], L2 = arm.L[1];
+  const V3 b = d.bpts[t];
+  unsigned c_v3 = 0, c_sol = 0;
+  BestRec best{1e308, LLONG_MAX};
+  if (static_cast<int>(threadIdx.x) < len) {
+    const uint32_t p = d.tail_pool[static_cast<size_t>(c) * kTailBlock + threadIdx.x];
+    const int s = static_cast<int>(p / static_cast<uint32_t>(a.Q));
+    const int j = static_cast<int>(p - static_cast<uint32_t>(s) * static_cast<uint32_t>(a.Q));
+    const int i = d.surv_idx[static_cast<size_t>(t) * a.Q + s];
+    const V3 s1 = L1 * qvec(a, i);
+    const V3 p1 = arm.root + s1;
+    const V3 dir2 = qvec(a, j);
+    const V3 p2 = p1 + L2 * dir2;
+    const V3 v3 = b - p2;
+    if (rpd::walk_first_blocked_fast_seg(a.g, p2, b, a.n) == 0) {
+      ++c_v3;
+      if (!EIGHT || d.walk4_ok[t]) {
+        const V3 s2 = L2 * dir2;
+        V3 J[5];
+        J[0] = arm.root;
+        J[1] = J[0] + s1;
+        J[2] = J[1] + s2;
+        J[3] = J[2] + v3;
+        if (EIGHT) J[4] = J[3] + a.L4 * a.bdirs[0];
+        // half-length bounds: |s1| = L1, |s2| = L2 (unit quiver vectors,
+        // widened for rounding), |v3| <= L3 + eps (gap band), |s4| = L4
+        const double w = 1.0 + 1e-9;
+        const double half[4] = {0.5 * L1 * w, 0.5 * L2 * w, 0.5 * (arm.L[2] + a.eps) * w,
+                                0.5 * a.L4 * w};
+        if (rpd::self_collision_free_screened(J, EIGHT ? 4 : 3, 2.0 * arm.arm_radius, half)) {
+          ++c_sol;
+          best = BestRec{(rpd::norm(s1) + rpd::norm(s2)) + rpd::norm(v3), static_cast<long long>(p)};
+        }
+      }
+    }
+  }
+  c_v3 = __reduce_add_sync(FULL, c_v3);
+  c_sol = __reduce_add_sync(FULL, c_sol);
+  for (int off = 16; off > 0; off >>= 1) {
+    const BestRec o{__shfl_down_sync(FULL, best.len, off), __shfl_down_sync(FULL, best.key, off)};
+    if (best_less(o, best)) best = o;
+  }
+  __shared__ unsigned sv3[kTailBlock / 32], ssol[kTailBlock / 32];
+  __shared__ BestRec sb[kTailBlock / 32];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sv3[w] = c_v3;
+    ssol[w] = c_sol;
+    sb[w] = best;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned tv = 0, ts = 0;
+    BestRec bb = sb[0];
+    for (int k = 0; k < kTailBlock / 32; ++k) {
+      tv += sv3[k];
+      ts += ssol[k];
+      if (best_less(sb[k], bb)) bb = sb[k];
+    }
+    unsigned long long* ctr = d.ctr + static_cast<size_t>(t) * C_COUNT;
+    if (tv) atomicAdd(ctr + C_V3_CLEAR, static_cast<unsigned long long>(tv));
+    if (ts) atomicAdd(ctr + C_SOLUTIONS, static_cast<unsigned long long>(ts));
+    if (ts) {
+      BestRec* dst = d.tail_best + t;
+      const volatile long long* vp = reinterpret_cast<const volatile long long*>(dst);
+      BestRec cur{__longlong_as_double(vp[0]), vp[1]};  // a torn read only fails the CAS
+      while (best_less(bb, cur)) {
+        const BestRec old = cas_best(dst, cur, bb);
+        if (__double_as_longlong(old.len) == __double_as_longlong(cur.len) && old.key == cur.key)
+          break;
+        cur = old;
+      }
+    }
+  }
+}
+
 __global__ void k_bq_best(BatchDev d) {
   const int t = blockIdx.x;
-  BestRec b{1e308, LLONG_MAX};
+  BestRec b = d.tail_cap > 0 ? d.tail_best[t] : BestRec{1e308, LLONG_MAX};
   for (int k = threadIdx.x; k < d.BPT; k += blockDim.x) {
     const BestRec r = d.bb[static_cast<size_t>(t) * d.BPT + k];
     if (r.len < b.len || (r.len == b.len && r.key < b.key)) b = r;
@@ -2103,7 +2245,18 @@ extern "C" rp_status rp_solve_reach_batch(rp_ctx* ctx, const rp_arm* arm, const 
     DevBuf<uint32_t> d_sbits(static_cast<size_t>(CH) * W, st);
     DevBuf<int> d_sidx(static_cast<size_t>(CH) * q->n, st), d_scnt(CH, st);
     DevBuf<unsigned long long> d_ctr(static_cast<size_t>(CH) * C_COUNT, st);
-    DevBuf<unsigned> d_scc(1, st);
+    DevBuf<unsigned> d_scc(2, st);  // [0] near-encounter keys, [1] tail-queue blocks taken
+    // tail queue (k_bq_tail): RP_TAIL_POOL_MB of pair keys (0: evaluate in place)
+    static const long tail_mb =
+        std::getenv("RP_TAIL_POOL_MB") ? std::atol(std::getenv("RP_TAIL_POOL_MB")) : 1024;
+    const bool keys_fit = static_cast<double>(q->n) * q->n < 4294967296.0;
+    const int tail_cap = keys_fit ? static_cast<int>(std::max(0L, tail_mb) * (1L << 20) /
+                                                     (kTailBlock * static_cast<long>(sizeof(uint32_t))))
+                                  : 0;
+    DevBuf<uint32_t> d_tpool(static_cast<size_t>(std::max(1, tail_cap)) * kTailBlock, st);
+    DevBuf<int> d_ttgt(std::max(1, tail_cap), st), d_tlen(std::max(1, tail_cap), st);
+    DevBuf<BestRec> d_tbest(CH, st);
+    const std::vector<BestRec> tbest_init(CH, BestRec{1e308, LLONG_MAX});
     DevBuf<long long> d_scl(kBatchShortcutCap, st);
     DevBuf<BestRec> d_bb(static_cast<size_t>(CH) * BPT, st), d_best(CH, st);
     DevBuf<BatchPose> d_pose(CH, st);
@@ -2165,6 +2318,13 @@ extern "C" rp_status rp_solve_reach_batch(rp_ctx* ctx, const rp_arm* arm, const 
       d.ring_off = d_roff.p;
       d.ring_c = d_rc.p;
       d.ring_s = d_rs.p;
+      d.tail_pool = d_tpool.p;
+      d.tail_tgt = d_ttgt.p;
+      d.tail_len = d_tlen.p;
+      d.tail_ctr = d_scc.p + 1;
+      d.tail_cap = tail_cap;
+      d.tail_best = d_tbest.p;
+      copy_to_device(ctx, d_tbest.p, tbest_init.data(), T * sizeof(BestRec));
       launch(ctx, "walk4", k_bq_walk4, dim3(nblk(T, 128)), dim3(128), 0, d, d_w4.p);
       launch(ctx, "seg1", k_bq_seg1, dim3(nblk(q->n, 256), T), dim3(256), 0, d);
       launch(ctx, "compact", k_bq_compact, dim3(T), dim3(1024), 0, d);
@@ -2172,9 +2332,17 @@ extern "C" rp_status rp_solve_reach_batch(rp_ctx* ctx, const rp_arm* arm, const 
         launch(ctx, "seg2", k_bq_seg2<true>, dim3(BPT, T), dim3(256), 0, d);
       else
         launch(ctx, "seg2", k_bq_seg2<false>, dim3(BPT, T), dim3(256), 0, d);
+      unsigned hcc[2] = {0, 0};
+      copy_to_host(ctx, hcc, d_scc.p, sizeof(hcc));
+      const unsigned nsc = hcc[0];
+      const int ntail = static_cast<int>(std::min<unsigned>(hcc[1], static_cast<unsigned>(tail_cap)));
+      if (ntail > 0) {
+        if (eight)
+          launch(ctx, "seg2", k_bq_tail<true>, dim3(ntail), dim3(kTailBlock), 0, d);
+        else
+          launch(ctx, "seg2", k_bq_tail<false>, dim3(ntail), dim3(kTailBlock), 0, d);
+      }
       launch(ctx, "select", k_bq_best, dim3(T), dim3(64), 0, d);
-      unsigned nsc = 0;
-      copy_to_host(ctx, &nsc, d_scc.p, sizeof(unsigned));
       require(nsc <= kBatchShortcutCap, RP_E_CAPACITY_EXCEEDED,
               "too many near-encounter hypotheses");
       // shortcuts: sorted keys = (target, segment, canonical index), scanned
