@@ -2214,6 +2214,50 @@ int Planner::valid_poses(const DevPose* poses, int count) {
   return h == INT_MAX ? -1 : h;
 }
 
+// ---- head / tail selection of the ranked order (rank_by_deviation) ---------
+constexpr int kRankBinBits = 12;
+constexpr int kRankBins = 1 << kRankBinBits;
+
+__global__ void k_key_range(const unsigned long long* __restrict__ k, int64_t n,
+                            unsigned long long* range) {
+  unsigned long long lo = ~0ull, hi = 0ull;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const unsigned long long v = k[i];
+    lo = v < lo ? v : lo;
+    hi = v > hi ? v : hi;
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    const unsigned long long a = __shfl_down_sync(0xffffffffu, lo, off);
+    const unsigned long long b = __shfl_down_sync(0xffffffffu, hi, off);
+    lo = a < lo ? a : lo;
+    hi = b > hi ? b : hi;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(range, lo);
+    atomicMax(range + 1, hi);
+  }
+}
+
+__global__ void k_key_hist(const unsigned long long* __restrict__ k, int64_t n,
+                           unsigned long long base, int shift, unsigned* hist) {
+  __shared__ unsigned h[kRankBins];
+  for (int b = threadIdx.x; b < kRankBins; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    atomicAdd(&h[static_cast<int>((k[i] - base) >> shift)], 1u);
+  __syncthreads();
+  for (int b = threadIdx.x; b < kRankBins; b += blockDim.x)
+    if (h[b]) atomicAdd(hist + b, h[b]);
+}
+
+__global__ void k_key_flags(const unsigned long long* __restrict__ k, int64_t n,
+                            unsigned long long tlo, unsigned long long thi, uint8_t* flags) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) flags[i] = (k[i] <= tlo || k[i] >= thi) ? 1 : 0;
+}
+
 /// Mean polyline deviation of every solution's traversal (segments 1-3,
 /// the reach pose's candidate_tip_path) from `poly`, as ordered bits of the
 /// fp64 value, with ordinals ord_base + t (alternate_candidates' scores,
@@ -2313,19 +2357,77 @@ std::vector<long long> Planner::rank_by_deviation(rp_solution_set* set,
   if (nsol > 0)
     score_set_solutions(ctx, set, poly, static_cast<const V3*>(dpoly.p), lead, lead_pt, dev.p + ns,
                         ord.p + ns, static_cast<long long>(ns));
-  size_t tb = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tb, dev.p, dev_sorted.p, ord.p, ord_sorted.p,
-                                  static_cast<int>(total), 0, 64, st);
-  DevBuf<unsigned char> tmp(tb, st);
-  RP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, dev.p, dev_sorted.p, ord.p, ord_sorted.p,
-                                          static_cast<int>(total), 0, 64, st));
   const int64_t nh = std::min<int64_t>(head_n, total);
+  const int64_t nt = tail ? std::min<int64_t>(tail_n, total) : 0;
+  // Only the first nh and last nt of the stable (deviation, ordinal) order
+  // are used: bucket the keys (4096 equal-width bins over [min, max]), keep
+  // the bins that hold them and stable-sort just those candidates -- the
+  // same head and tail as the full sort (ordinals ascend with the index).
+  static const bool full_sort = std::getenv("RP_RANK_FULL_SORT") != nullptr;
+  const unsigned long long* keys_in = dev.p;
+  const long long* vals_in = ord.p;
+  int64_t m = total;
+  DevBuf<unsigned long long> ck;
+  DevBuf<long long> cv;
+  if (!full_sort && total > 65536) {
+    DevBuf<unsigned long long> range(2, st);
+    const unsigned long long init[2] = {~0ull, 0ull};
+    copy_to_device(ctx, range.p, init, sizeof(init));
+    const int gb = ctx->sm_count * 4;
+    launch(ctx, "rank", k_key_range, dim3(gb), dim3(256), 0,
+           static_cast<const unsigned long long*>(dev.p), total, range.p);
+    unsigned long long hr[2];
+    copy_to_host(ctx, hr, range.p, sizeof(hr));
+    const unsigned long long span = hr[1] - hr[0];
+    const int bits = span ? 64 - __builtin_clzll(span) : 0;
+    const int shift = std::max(0, bits - kRankBinBits);
+    DevBuf<unsigned> hist(kRankBins, st);
+    hist.zero();
+    launch(ctx, "rank", k_key_hist, dim3(gb), dim3(256), 0,
+           static_cast<const unsigned long long*>(dev.p), total, hr[0], shift, hist.p);
+    std::vector<unsigned> hh(kRankBins);
+    copy_to_host(ctx, hh.data(), hist.p, kRankBins * sizeof(unsigned));
+    int blo = 0, bhi = kRankBins - 1;
+    int64_t clo = 0, chi = 0;
+    for (; blo < kRankBins; ++blo)
+      if ((clo += hh[blo]) >= nh) break;
+    if (nt > 0) {
+      for (; bhi >= 0; --bhi)
+        if ((chi += hh[bhi]) >= nt) break;
+    } else {
+      bhi = kRankBins;  // no tail wanted
+    }
+    if (blo < bhi && clo + chi <= (1 << 20)) {
+      const unsigned long long tlo = hr[0] + ((static_cast<unsigned long long>(blo) + 1) << shift) - 1;
+      const unsigned long long thi =
+          bhi < kRankBins ? hr[0] + (static_cast<unsigned long long>(bhi) << shift) : ~0ull;
+      DevBuf<uint8_t> flags(total, st);
+      launch(ctx, "rank", k_key_flags, dim3(nblk(total, 256)), dim3(256), 0,
+             static_cast<const unsigned long long*>(dev.p), total, tlo, thi, flags.p);
+      m = clo + chi;
+      ck.alloc(m, st);
+      cv.alloc(m, st);
+      DevBuf<int> nsel(1, st);
+      size_t tbs = 0;
+      cub::DeviceSelect::Flagged(nullptr, tbs, dev.p, flags.p, ck.p, nsel.p, total, st);
+      DevBuf<unsigned char> tsel(tbs, st);
+      RP_CUDA(cub::DeviceSelect::Flagged(tsel.p, tbs, dev.p, flags.p, ck.p, nsel.p, total, st));
+      RP_CUDA(cub::DeviceSelect::Flagged(tsel.p, tbs, ord.p, flags.p, cv.p, nsel.p, total, st));
+      keys_in = ck.p;
+      vals_in = cv.p;
+    }
+  }
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, keys_in, dev_sorted.p, vals_in, ord_sorted.p,
+                                  static_cast<int>(m), 0, 64, st);
+  DevBuf<unsigned char> tmp(tb, st);
+  RP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys_in, dev_sorted.p, vals_in, ord_sorted.p,
+                                          static_cast<int>(m), 0, 64, st));
   head.resize(nh);
   copy_to_host(ctx, head.data(), ord_sorted.p, nh * sizeof(long long));
   if (tail) {
-    const int64_t nt = std::min<int64_t>(tail_n, total);
     tail->resize(nt);
-    copy_to_host(ctx, tail->data(), ord_sorted.p + (total - nt), nt * sizeof(long long));
+    copy_to_host(ctx, tail->data(), ord_sorted.p + (m - nt), nt * sizeof(long long));
   }
   return head;
 }
