@@ -299,6 +299,16 @@ __host__ __device__ __forceinline__ bool self_collision_free(const V3* joints, i
   return true;
 }
 
+/// True when links [a0, a1] and [b0, b1] (half-length bounds ha, hb) are
+/// provably at least min_sep apart: their midpoints are farther apart than
+/// min_sep + ha + hb (with margin), so seg_seg_distance >= min_sep.
+__host__ __device__ __forceinline__ bool links_clear_screen(V3 a0, V3 a1, V3 b0, V3 b1, double ha,
+                                                            double hb, double min_sep) {
+  const V3 d = 0.5 * (a0 + a1) - 0.5 * (b0 + b1);
+  const double r = min_sep + ha + hb;
+  return sqnorm(d) > r * r * (1.0 + 1e-9) + 1e-12;
+}
+
 /// self_collision_free with a bounding-sphere screen: link k lies in the
 /// ball around its midpoint of radius half[k] (an upper bound of half its
 /// length), so a pair whose midpoints are farther apart than

@@ -340,6 +340,7 @@ __device__ bool wik_full_warp(const WikDev& w, const CiFast& c, int j, int lane,
   const int npairs = w.four ? 3 * nopt : 1;
   if (lane < npairs) {
     V3 a0, a1, b0, b1;
+    double ha = 0.5 * arm.L[0], hb = 0.5 * arm.L[2];
     if (!w.four) {
       a0 = J[0]; a1 = J[1]; b0 = J[2]; b1 = J[3];
     } else {
@@ -350,8 +351,12 @@ __device__ bool wik_full_warp(const WikDev& w, const CiFast& c, int j, int lane,
       a1 = pr == 2 ? J[2] : J[1];
       b0 = pr == 0 ? J[2] : J[3];
       b1 = pr == 0 ? J[3] : j4;
+      ha = 0.5 * (pr == 2 ? arm.L[1] : arm.L[0]);
+      hb = 0.5 * (pr == 0 ? arm.L[2] : w.L4);
     }
-    ok = !(rpd::seg_seg_distance(a0, a1, b0, b1) < min_sep);
+    // unit directions: |link| = L up to rounding, absorbed by the widening
+    ok = rpd::links_clear_screen(a0, a1, b0, b1, ha * (1.0 + 1e-9), hb * (1.0 + 1e-9), min_sep) ||
+         !(rpd::seg_seg_distance(a0, a1, b0, b1) < min_sep);
   }
   const unsigned dist_fail = __ballot_sync(0xffffffffu, !ok);
   if (!w.four) return !(dist_fail & 1u);
@@ -414,6 +419,7 @@ __device__ bool wik_full_half(const WikDev& w, const CiFast& c, int j, bool vali
   const int npairs = w.four ? 3 * nopt : 1;
   if (alive && sub < npairs) {
     V3 a0, a1, b0, b1;
+    double ha = 0.5 * arm.L[0], hb = 0.5 * arm.L[2];
     if (!w.four) {
       a0 = J[0]; a1 = J[1]; b0 = J[2]; b1 = J[3];
     } else {
@@ -423,8 +429,11 @@ __device__ bool wik_full_half(const WikDev& w, const CiFast& c, int j, bool vali
       a1 = pr == 2 ? J[2] : J[1];
       b0 = pr == 0 ? J[2] : J[3];
       b1 = pr == 0 ? J[3] : j4;
+      ha = 0.5 * (pr == 2 ? arm.L[1] : arm.L[0]);
+      hb = 0.5 * (pr == 0 ? arm.L[2] : w.L4);
     }
-    ok = !(rpd::seg_seg_distance(a0, a1, b0, b1) < min_sep);
+    ok = rpd::links_clear_screen(a0, a1, b0, b1, ha * (1.0 + 1e-9), hb * (1.0 + 1e-9), min_sep) ||
+         !(rpd::seg_seg_distance(a0, a1, b0, b1) < min_sep);
   }
   const unsigned dist_fail = (__ballot_sync(0xffffffffu, !ok) >> (16 * half)) & 0xFFFFu;
   if (!alive) return false;
