@@ -331,7 +331,7 @@ __device__ bool wik_full_warp(const WikDev& w, const CiFast& c, int j, int lane,
       from = J[3];
       to = tip(lane - 2);
     }
-    ok = rpd::walk_first_blocked_fast(w.g, from, to, w.n) == 0;
+    ok = rpd::walk_first_blocked_fast_seg(w.g, from, to, w.n) == 0;
   }
   const unsigned walk_fail = __ballot_sync(0xffffffffu, !ok);
   if (walk_fail & 3u) return false;
@@ -376,6 +376,8 @@ __device__ bool wik_full_warp(const WikDev& w, const CiFast& c, int j, int lane,
 __device__ bool wik_full_half(const WikDev& w, const CiFast& c, int j, bool valid, int sub,
                               int half, int* opt_out) {
   const ArmDev& arm = w.arm;
+  const bool pr = w.prof && blockIdx.x == 0 && threadIdx.x == 0;
+  long long t0 = pr ? clock64() : 0;
   bool alive = valid;
   const V3 qj = valid ? wq(w, j) : V3{0, 0, 1};
   const V3 p1 = valid ? c.p1 : arm.root;
@@ -402,6 +404,7 @@ __device__ bool wik_full_half(const WikDev& w, const CiFast& c, int j, bool vali
     return J[3] + w.L4 * dir;
   };
   bool ok = true;
+  long long t1 = pr ? clock64() : 0;
   if (alive && sub < 2 + nopt) {
     V3 from = p1, to = p2;
     if (sub == 1) {
@@ -411,9 +414,10 @@ __device__ bool wik_full_half(const WikDev& w, const CiFast& c, int j, bool vali
       from = J[3];
       to = tip(sub - 2);
     }
-    ok = rpd::walk_first_blocked_fast(w.g, from, to, w.n) == 0;
+    ok = rpd::walk_first_blocked_fast_seg(w.g, from, to, w.n) == 0;
   }
   const unsigned walk_fail = (__ballot_sync(0xffffffffu, !ok) >> (16 * half)) & 0xFFFFu;
+  long long t2 = pr ? clock64() : 0;
   alive = alive && !(walk_fail & 3u);
   ok = true;
   const int npairs = w.four ? 3 * nopt : 1;
@@ -436,6 +440,12 @@ __device__ bool wik_full_half(const WikDev& w, const CiFast& c, int j, bool vali
          !(rpd::seg_seg_distance(a0, a1, b0, b1) < min_sep);
   }
   const unsigned dist_fail = (__ballot_sync(0xffffffffu, !ok) >> (16 * half)) & 0xFFFFu;
+  if (pr) {
+    const long long t3 = clock64();
+    atomicAdd(reinterpret_cast<unsigned long long*>(w.prof + 16), t1 - t0);
+    atomicAdd(reinterpret_cast<unsigned long long*>(w.prof + 17), t2 - t1);
+    atomicAdd(reinterpret_cast<unsigned long long*>(w.prof + 18), t3 - t2);
+  }
   if (!alive) return false;
   if (!w.four) return !(dist_fail & 1u);
   for (int o = 0; o < nopt; ++o) {
@@ -1136,6 +1146,7 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
               s_rank[r] = static_cast<short>(threadIdx.x);
             }
             __syncthreads();
+            if (prof) A.prof[15] += clock64() - ps1;
             // ... and evaluate them in waves of one candidate per warp, best
             // first: the first wave with a qualifying pair holds the round's
             // answer (every later candidate ranks below it)
@@ -1162,6 +1173,7 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
                 }
               }
               hit = wik_full_half(w, c, jj, valid, sub, half, &opt);
+              if (prof) A.prof[14] += 1;
               if (hit) {
                 bm = mm;
                 bo = t2;
@@ -2027,7 +2039,7 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
   static const bool profile = std::getenv("RP_PROFILE_PASS") != nullptr;
   DevBuf<long long> prof;
   if (profile) {
-    prof.alloc(16, st);
+    prof.alloc(24, st);
     prof.zero();
     A.prof = prof.p;
   }
@@ -2040,10 +2052,11 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
   int hs[4];
   copy_to_host(ctx, hs, bp_state.p, sizeof(hs));
   if (profile) {
-    long long hp[16];
+    long long hp[24];
     copy_to_host(ctx, hp, prof.p, sizeof(hp));
-    std::fprintf(stderr, "[pairs] screening %lld, rank+eval %lld cycles; screened %lld\n", hp[10],
-                 hp[11], hp[12]);
+    std::fprintf(stderr, "[half] setup %lld walks %lld dists %lld cycles\n", hp[16], hp[17], hp[18]);
+    std::fprintf(stderr, "[pairs] screening %lld, rank+eval %lld cycles (rank %lld, waves %lld); screened %lld\n", hp[10],
+                 hp[11], hp[15], hp[14], hp[12]);
     std::fprintf(stderr,
                  "[pass] m=%d attempts=%lld pairs=%lld cyc: filter %lld compact %lld pairs %lld "
                  "wait %lld publish %lld barrier %lld | max ci-load %lld max eval %lld\n",
