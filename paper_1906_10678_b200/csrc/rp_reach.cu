@@ -2247,8 +2247,8 @@ extern "C" rp_status rp_solve_reach_batch(rp_ctx* ctx, const rp_arm* arm, const 
     DevBuf<unsigned long long> d_ctr(static_cast<size_t>(CH) * C_COUNT, st);
     DevBuf<unsigned> d_scc(2, st);  // [0] near-encounter keys, [1] tail-queue blocks taken
     // tail queue (k_bq_tail): RP_TAIL_POOL_MB of pair keys (0: evaluate in place)
-    static const long tail_mb =
-        std::getenv("RP_TAIL_POOL_MB") ? std::atol(std::getenv("RP_TAIL_POOL_MB")) : 1024;
+    const char* tail_env = std::getenv("RP_TAIL_POOL_MB");  // read per call (tests vary it)
+    const long tail_mb = tail_env ? std::atol(tail_env) : 1024;
     const bool keys_fit = static_cast<double>(q->n) * q->n < 4294967296.0;
     const int tail_cap = keys_fit ? static_cast<int>(std::max(0L, tail_mb) * (1L << 20) /
                                                      (kTailBlock * static_cast<long>(sizeof(uint32_t))))

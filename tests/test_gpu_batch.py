@@ -67,3 +67,21 @@ def test_batch_equals_single_solves(ctx):
         if ns + nc:
             c = S.select()
             assert r.kind == c.kind and r.path_length == c.path_length
+
+
+@pytest.mark.parametrize("pool_mb", ["1", "0"])
+def test_batch_tail_pool_overflow_identical(ctx, monkeypatch, pool_mb):
+    """The pair tail queued for k_bq_tail (default pool), spilling over a
+    1 MiB pool (most pairs evaluated in place) and with no pool at all give
+    identical records: counters, counts, chosen key, length and pose."""
+    api = _api()
+    sc = scenes.config("C2", quiver_deg=3.0)
+    arm, rp, q, g = gpu_problem(ctx, sc)
+    targets = scenes.batch_targets(12, seed=11)
+    monkeypatch.delenv("RP_TAIL_POOL_MB", raising=False)
+    want = api.solve_reach_batch(ctx, arm, q, g, targets, rp)
+    monkeypatch.setenv("RP_TAIL_POOL_MB", pool_mb)
+    got = api.solve_reach_batch(ctx, arm, q, g, targets, rp)
+    assert any(r.n_solutions > 0 for r in want)
+    for a, b in zip(want, got):
+        assert bytes(a) == bytes(b)
