@@ -154,7 +154,8 @@ __device__ __forceinline__ int walk_first_blocked(const GridView& g, V3 from, V3
 /// Measured on B200: ~0.9k cycles for an 8-sample walk versus ~7k for the
 /// sequential walk (one L2 round trip instead of 8).
 template <int N, bool INPLACE>
-__device__ __forceinline__ uint32_t walk_hits(const GridView& g, V3 from, V3 to, int n, bool* exact) {
+__device__ __forceinline__ uint32_t walk_hits(const GridView& g, V3 from, V3 to, int n, bool* exact,
+                                              int kstart = 0) {
   // One pass, no per-sample arrays: each sample's load is issued as soon as
   // its index is known and only its bit is kept, so the loads overlap
   // without holding 3N registers (or spilling them in large kernels).
@@ -163,6 +164,7 @@ __device__ __forceinline__ uint32_t walk_hits(const GridView& g, V3 from, V3 to,
   uint32_t mask = 0;
 #pragma unroll
   for (int k = 0; k < N; ++k) {
+    if (k < kstart) continue;  // caller-proven free samples (warp-uniform)
     const bool live = k < n;
     const double t = c_tk.v[n][live ? k + 1 : n];
     const V3 p = from + t * diff;
@@ -195,11 +197,12 @@ __device__ __forceinline__ uint32_t walk_hits(const GridView& g, V3 from, V3 to,
 /// (seg2: rare, and the branch-free body keeps registers down — 2.15 vs
 /// 2.73 ms for C2's seg2).
 template <bool INPLACE>
-__device__ __forceinline__ int walk_first_blocked_fast_t(const GridView& g, V3 from, V3 to, int n) {
+__device__ __forceinline__ int walk_first_blocked_fast_t(const GridView& g, V3 from, V3 to, int n,
+                                                         int kstart = 0) {
   bool exact = true;
   uint32_t m;
-  if (n == 8) m = walk_hits<8, INPLACE>(g, from, to, 8, &exact);
-  else if (n <= kTkMax) m = walk_hits<kTkMax, INPLACE>(g, from, to, n, &exact);
+  if (n == 8) m = walk_hits<8, INPLACE>(g, from, to, 8, &exact, kstart);
+  else if (n <= kTkMax) m = walk_hits<kTkMax, INPLACE>(g, from, to, n, &exact, kstart);
   else return walk_first_blocked(g, from, to, n);
   if (!exact) return walk_first_blocked(g, from, to, n);
   return m ? __ffs(m) : 0;
@@ -209,6 +212,12 @@ __device__ __forceinline__ int walk_first_blocked_fast(const GridView& g, V3 fro
 }
 __device__ __forceinline__ int walk_first_blocked_fast_seg(const GridView& g, V3 from, V3 to, int n) {
   return walk_first_blocked_fast_t<false>(g, from, to, n);
+}
+/// The same verdict when the caller has proven samples 1..kstart free (they
+/// are not looked up; the sequential fallback still walks every sample).
+__device__ __forceinline__ int walk_first_blocked_fast_seg_from(const GridView& g, V3 from, V3 to,
+                                                                int n, int kstart) {
+  return walk_first_blocked_fast_t<false>(g, from, to, n, kstart);
 }
 
 /// Out-of-line copy for the large planner kernels (one body instead of one

@@ -333,12 +333,69 @@ constexpr bool kSeg2ParWalk = RP_SEG2_PAR_WALK;
 #define RP_BQ_MINB 4
 #endif
 
+/// Occupied coarse blocks (edge bk voxels) of a grid, as packed
+/// (bx | by << 10 | bz << 20), in any order.
+__global__ void k_occ_blocks(rpd::GridView g, int bk, int nbx, int nby, int nbz, int* __restrict__ list,
+                             int* __restrict__ count) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nbx * nby * nbz) return;
+  const int bx = b % nbx, by = (b / nbx) % nby, bz = b / (nbx * nby);
+  const int x0 = bx * bk;
+  const uint64_t m = (bk >= 64 ? ~0ull : ((1ull << bk) - 1ull)) << (x0 & 63);
+  bool occ = false;
+  for (int z = bz * bk; z < min(g.nz, (bz + 1) * bk) && !occ; ++z)
+    for (int y = by * bk; y < min(g.ny, (by + 1) * bk); ++y)
+      if (__ldg(g.bits + (static_cast<size_t>(z) * g.ny + y) * g.wx + (x0 >> 6)) & m) {
+        occ = true;
+        break;
+      }
+  if (occ) list[atomicAdd(count, 1)] = bx | (by << 10) | (bz << 20);
+}
+
+/// Per survivor row: how many leading segment-2 samples are provably free.
+/// D = distance from p1 to the nearest occupied block box (a lower bound on
+/// the distance to any occupied cell). Sample k lies within t_k * L2 of p1
+/// (|q_j| = 1 up to rounding), and the cell the reference floors it to
+/// (off by at most one per axis from the cell holding it) lies within
+/// sqrt(3) * vs of it, so samples with t_k * L2 + sqrt(3) * vs < D (with
+/// margins) are free. One warp per row.
+__global__ void k_row_skip(SolveDev a, const SurvDev* __restrict__ sv, int S1, int bk,
+                           const int* __restrict__ list, const int* __restrict__ count,
+                           uint8_t* __restrict__ kskip) {
+  const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= S1) return;
+  const V3 p1 = sv[s].p1;
+  const rpd::GridView& g = a.g;
+  const double side = bk * g.vs;
+  double d2 = 1e300;
+  const int nb = *count;
+  for (int k = lane; k < nb; k += 32) {
+    const int c = list[k];
+    const double lx = g.ox + (c & 1023) * side, ly = g.oy + ((c >> 10) & 1023) * side,
+                 lz = g.oz + (c >> 20) * side;
+    const double dx = fmax(0.0, fmax(lx - p1.x, p1.x - (lx + side)));
+    const double dy = fmax(0.0, fmax(ly - p1.y, p1.y - (ly + side)));
+    const double dz = fmax(0.0, fmax(lz - p1.z, p1.z - (lz + side)));
+    d2 = fmin(d2, dx * dx + dy * dy + dz * dz);
+  }
+  for (int off = 16; off > 0; off >>= 1) d2 = fmin(d2, __shfl_down_sync(FULL, d2, off));
+  if (lane == 0) {
+    const double D = sqrt(d2) * (1.0 - 1e-9) - 1e-9;
+    const double L2 = a.arm.L[1] * (1.0 + 1e-9) + 1e-9;
+    const double cell = 1.7320508075688772 * g.vs * (1.0 + 1e-9) + 1e-9;
+    int k = 0;
+    while (k < a.n && (static_cast<double>(k + 1) / a.n) * L2 + cell < D) ++k;
+    kskip[s] = static_cast<uint8_t>(k);
+  }
+}
+
 template <bool EIGHT>
 __global__ void __launch_bounds__(256, 4) k_seg2_rows(SolveDev a, const SurvDev* __restrict__ sv, int S1,
                                                    uint32_t* __restrict__ sol_bits,
                                                    unsigned long long* ctr, long long* sc_list,
                                                    unsigned* sc_count, BestRec* __restrict__ block_best,
-                                                   int* unit_ctr) {
+                                                   int* unit_ctr, const uint8_t* __restrict__ kskip) {
   unsigned c_lim = 0, c_clear = 0, c_gp = 0, c_jp = 0, c_v3 = 0, c_sol = 0;
   double best_len = 1e308;
   long long best_key = LLONG_MAX;
@@ -370,6 +427,7 @@ __global__ void __launch_bounds__(256, 4) k_seg2_rows(SolveDev a, const SurvDev*
     const SurvDev& h = sv[s];
     const V3 p1 = h.p1;
     const V3 s1 = L1 * qvec(a, h.i);
+    const int ks = kskip[s];  // leading samples of every segment-2 walk of this row that are free
     const bool row_near = rpd::sqnorm(a.target - p1) <= (L2 + rnear) * (L2 + rnear);
     const double db = sqrt(rpd::sqnorm(b - p1));
     const bool row_gap = db <= (sqrt(a.coarse2) + L2) * (1.0 + 1e-9) + 1e-12 &&
@@ -414,8 +472,9 @@ __global__ void __launch_bounds__(256, 4) k_seg2_rows(SolveDev a, const SurvDev*
         ++c_lim;
         const V3 dir2 = qvec(a, j);
         const V3 p2 = p1 + L2 * dir2;
-        const int fb = kSeg2ParWalk ? rpd::walk_first_blocked_fast_seg(a.g, p1, p2, a.n)
-                                    : rpd::walk_first_blocked(a.g, p1, p2, a.n);
+        const int fb = ks >= a.n   ? 0
+                       : kSeg2ParWalk ? rpd::walk_first_blocked_fast_seg_from(a.g, p1, p2, a.n, ks)
+                                      : rpd::walk_first_blocked(a.g, p1, p2, a.n);
         if (row_near && rpd::may_pass_near(a.target, p1, dir2, L2, rnear) &&
             rpd::point_to_segment(a.target, p1, p2) <= a.near_r + 1e-9) {
           const unsigned pos = atomicAdd(sc_count, 1u);
@@ -930,10 +989,30 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
         const int rblocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks, (units + 7) / 8)));
         DevBuf<int> unit_ctr(1, st);
         unit_ctr.zero();
+        // free leading samples per row (k_row_skip) from the occupied coarse
+        // blocks (edge: 4 voxels, or dims/32 for larger grids)
+        const int dmax = std::max(g->dims[0], std::max(g->dims[1], g->dims[2]));
+        int bk = 4;
+        while (bk < 64 && bk * 32 < dmax) bk *= 2;
+        const int nbx = (g->dims[0] + bk - 1) / bk, nby = (g->dims[1] + bk - 1) / bk,
+                  nbz = (g->dims[2] + bk - 1) / bk;
+        DevBuf<int> blist(static_cast<size_t>(nbx) * nby * nbz, st), bcount(1, st);
+        DevBuf<uint8_t> kskip(std::max(1, S1), st);
+        static const bool no_skip = std::getenv("RP_NO_ROW_SKIP") != nullptr;
+        if (no_skip) {
+          kskip.zero();
+        } else {
+          bcount.zero();
+          launch(ctx, "seg2", k_occ_blocks, dim3(nblk(static_cast<int64_t>(nbx) * nby * nbz, 256)),
+                 dim3(256), 0, a.g, bk, nbx, nby, nbz, blist.p, bcount.p);
+          launch(ctx, "seg2", k_row_skip, dim3(nblk(static_cast<int64_t>(S1) * 32, 256)), dim3(256), 0,
+                 a, static_cast<const SurvDev*>(s->surv.p), S1, bk,
+                 static_cast<const int*>(blist.p), static_cast<const int*>(bcount.p), kskip.p);
+        }
         auto runr = [&](auto kern) {
           launch(ctx, "seg2", kern, dim3(rblocks), dim3(threads), 0, a,
                  static_cast<const SurvDev*>(s->surv.p), S1, s->sol_bits.p, ctr.p, sc_list.p,
-                 sc_count.p, bb.p, unit_ctr.p);
+                 sc_count.p, bb.p, unit_ctr.p, static_cast<const uint8_t*>(kskip.p));
         };
         eight ? runr(k_seg2_rows<true>) : runr(k_seg2_rows<false>);
         blocks = rblocks;
