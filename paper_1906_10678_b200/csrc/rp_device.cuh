@@ -133,9 +133,10 @@ __device__ __forceinline__ long long cell_word(const GridView& g, V3 p, int* bit
 /// src/voxgrid.cpp:100-112): the 1-based first blocked sample, 0 when fully
 /// clear (sequential with early exit: the search kernels are fp64-bound and
 /// most rejected walks stop at their first samples).
-__device__ __forceinline__ int walk_first_blocked(const GridView& g, V3 from, V3 to, int n) {
+__device__ __forceinline__ int walk_first_blocked(const GridView& g, V3 from, V3 to, int n,
+                                                  int kmax = 1 << 30) {
   const V3 diff = to - from;
-  for (int k = 1; k <= n; ++k) {
+  for (int k = 1; k <= n && k <= kmax; ++k) {
     int bit = 0;
     const long long idx = cell_word(g, walk_sample(from, diff, k, n), &bit);
     if (idx >= 0 && ((__ldg(g.bits + idx) >> bit) & 1ull)) return k;
@@ -155,7 +156,7 @@ __device__ __forceinline__ int walk_first_blocked(const GridView& g, V3 from, V3
 /// sequential walk (one L2 round trip instead of 8).
 template <int N, bool INPLACE>
 __device__ __forceinline__ uint32_t walk_hits(const GridView& g, V3 from, V3 to, int n, bool* exact,
-                                              int kstart = 0) {
+                                              int kstart = 0, int kend = N) {
   // One pass, no per-sample arrays: each sample's load is issued as soon as
   // its index is known and only its bit is kept, so the loads overlap
   // without holding 3N registers (or spilling them in large kernels).
@@ -164,7 +165,7 @@ __device__ __forceinline__ uint32_t walk_hits(const GridView& g, V3 from, V3 to,
   uint32_t mask = 0;
 #pragma unroll
   for (int k = 0; k < N; ++k) {
-    if (k < kstart) continue;  // caller-proven free samples (warp-uniform)
+    if (k < kstart || k >= kend) continue;  // caller-proven free samples (warp-uniform)
     const bool live = k < n;
     const double t = c_tk.v[n][live ? k + 1 : n];
     const V3 p = from + t * diff;
@@ -198,11 +199,11 @@ __device__ __forceinline__ uint32_t walk_hits(const GridView& g, V3 from, V3 to,
 /// 2.73 ms for C2's seg2).
 template <bool INPLACE>
 __device__ __forceinline__ int walk_first_blocked_fast_t(const GridView& g, V3 from, V3 to, int n,
-                                                         int kstart = 0) {
+                                                         int kstart = 0, int kend = kTkMax) {
   bool exact = true;
   uint32_t m;
-  if (n == 8) m = walk_hits<8, INPLACE>(g, from, to, 8, &exact, kstart);
-  else if (n <= kTkMax) m = walk_hits<kTkMax, INPLACE>(g, from, to, n, &exact, kstart);
+  if (n == 8) m = walk_hits<8, INPLACE>(g, from, to, 8, &exact, kstart, kend);
+  else if (n <= kTkMax) m = walk_hits<kTkMax, INPLACE>(g, from, to, n, &exact, kstart, kend);
   else return walk_first_blocked(g, from, to, n);
   if (!exact) return walk_first_blocked(g, from, to, n);
   return m ? __ffs(m) : 0;
@@ -218,6 +219,12 @@ __device__ __forceinline__ int walk_first_blocked_fast_seg(const GridView& g, V3
 __device__ __forceinline__ int walk_first_blocked_fast_seg_from(const GridView& g, V3 from, V3 to,
                                                                 int n, int kstart) {
   return walk_first_blocked_fast_t<false>(g, from, to, n, kstart);
+}
+/// Clear verdict (0 / nonzero, not the index) when samples kend+1..n are
+/// proven free: only samples 1..kend are looked up.
+__device__ __forceinline__ int walk_any_blocked_upto(const GridView& g, V3 from, V3 to, int n,
+                                                     int kend) {
+  return walk_first_blocked_fast_t<false>(g, from, to, n, 0, kend);
 }
 
 /// Out-of-line copy for the large planner kernels (one body instead of one

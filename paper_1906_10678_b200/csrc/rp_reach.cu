@@ -352,6 +352,46 @@ __global__ void k_occ_blocks(rpd::GridView g, int bk, int nbx, int nby, int nbz,
   if (occ) list[atomicAdd(count, 1)] = bx | (by << 10) | (bz << 20);
 }
 
+/// Squared distance from p to the nearest occupied block box (warp-reduced;
+/// every lane gets the result).
+__device__ double occ_block_d2(const rpd::GridView& g, V3 p, int bk, const int* __restrict__ list,
+                               int nb) {
+  const int lane = threadIdx.x & 31;
+  const double side = bk * g.vs;
+  double d2 = 1e300;
+  for (int k = lane; k < nb; k += 32) {
+    const int c = list[k];
+    const double lx = g.ox + (c & 1023) * side, ly = g.oy + ((c >> 10) & 1023) * side,
+                 lz = g.oz + (c >> 20) * side;
+    const double dx = fmax(0.0, fmax(lx - p.x, p.x - (lx + side)));
+    const double dy = fmax(0.0, fmax(ly - p.y, p.y - (ly + side)));
+    const double dz = fmax(0.0, fmax(lz - p.z, p.z - (lz + side)));
+    d2 = fmin(d2, dx * dx + dy * dy + dz * dz);
+  }
+  for (int off = 16; off > 0; off >>= 1) d2 = fmin(d2, __shfl_xor_sync(FULL, d2, off));
+  return d2;
+}
+
+/// Per end point b (one warp each): kend = the samples 1..kend of a walk
+/// [p2, b] with |b - p2| <= L that are not proven free; sample j lies within
+/// (1 - j/n) * L of b, so it is free when that plus sqrt(3) * vs is below the
+/// distance from b to the nearest occupied block (see k_row_skip).
+__global__ void k_tail_skip(rpd::GridView g, const V3* __restrict__ pts, int T, double L, int n,
+                            int bk, const int* __restrict__ list, const int* __restrict__ count,
+                            uint8_t* __restrict__ kend) {
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (t >= T) return;
+  const double d2 = occ_block_d2(g, pts[t], bk, list, *count);
+  if ((threadIdx.x & 31) == 0) {
+    const double D = sqrt(d2) * (1.0 - 1e-9) - 1e-9;
+    const double Lm = L * (1.0 + 1e-9) + 1e-9;
+    const double cell = 1.7320508075688772 * g.vs * (1.0 + 1e-9) + 1e-9;
+    int j = n;
+    while (j >= 1 && (1.0 - static_cast<double>(j) / n) * Lm + cell < D) --j;
+    kend[t] = static_cast<uint8_t>(j);
+  }
+}
+
 /// Per survivor row: how many leading segment-2 samples are provably free.
 /// D = distance from p1 to the nearest occupied block box (a lower bound on
 /// the distance to any occupied cell). Sample k lies within t_k * L2 of p1
@@ -365,21 +405,8 @@ __global__ void k_row_skip(SolveDev a, const SurvDev* __restrict__ sv, int S1, i
   const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (s >= S1) return;
-  const V3 p1 = sv[s].p1;
   const rpd::GridView& g = a.g;
-  const double side = bk * g.vs;
-  double d2 = 1e300;
-  const int nb = *count;
-  for (int k = lane; k < nb; k += 32) {
-    const int c = list[k];
-    const double lx = g.ox + (c & 1023) * side, ly = g.oy + ((c >> 10) & 1023) * side,
-                 lz = g.oz + (c >> 20) * side;
-    const double dx = fmax(0.0, fmax(lx - p1.x, p1.x - (lx + side)));
-    const double dy = fmax(0.0, fmax(ly - p1.y, p1.y - (ly + side)));
-    const double dz = fmax(0.0, fmax(lz - p1.z, p1.z - (lz + side)));
-    d2 = fmin(d2, dx * dx + dy * dy + dz * dz);
-  }
-  for (int off = 16; off > 0; off >>= 1) d2 = fmin(d2, __shfl_down_sync(FULL, d2, off));
+  const double d2 = occ_block_d2(g, sv[s].p1, bk, list, *count);
   if (lane == 0) {
     const double D = sqrt(d2) * (1.0 - 1e-9) - 1e-9;
     const double L2 = a.arm.L[1] * (1.0 + 1e-9) + 1e-9;
@@ -395,7 +422,8 @@ __global__ void __launch_bounds__(256, 4) k_seg2_rows(SolveDev a, const SurvDev*
                                                    uint32_t* __restrict__ sol_bits,
                                                    unsigned long long* ctr, long long* sc_list,
                                                    unsigned* sc_count, BestRec* __restrict__ block_best,
-                                                   int* unit_ctr, const uint8_t* __restrict__ kskip) {
+                                                   int* unit_ctr, const uint8_t* __restrict__ kskip,
+                                                   const uint8_t* __restrict__ kend_b) {
   unsigned c_lim = 0, c_clear = 0, c_gp = 0, c_jp = 0, c_v3 = 0, c_sol = 0;
   double best_len = 1e308;
   long long best_key = LLONG_MAX;
@@ -409,6 +437,7 @@ __global__ void __launch_bounds__(256, 4) k_seg2_rows(SolveDev a, const SurvDev*
   const V3 bdir = a.bdirs[0];
   const bool walk4 = !EIGHT || a.walk4_ok[0];
   const double rnear = a.near_r + 1e-6;
+  const int kend_bv = *kend_b;  // samples of the v3 walks [p2, b] not proven free
   __shared__ int wqs[8][64];
   int* wq = wqs[threadIdx.x >> 5];
   constexpr int kChunk = 1024;  // j per work unit (balances small S1)
@@ -442,7 +471,7 @@ __global__ void __launch_bounds__(256, 4) k_seg2_rows(SolveDev a, const SurvDev*
       ++c_gp;
       if (v3_len < 1e-12) return;
       ++c_jp;
-      if (rpd::walk_first_blocked(a.g, p2, b, a.n) != 0) return;
+      if (rpd::walk_first_blocked(a.g, p2, b, a.n, kend_bv) != 0) return;
       ++c_v3;
       if (EIGHT && !walk4) return;
       const V3 s2 = L2 * dir2;
@@ -1009,10 +1038,20 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
                  a, static_cast<const SurvDev*>(s->surv.p), S1, bk,
                  static_cast<const int*>(blist.p), static_cast<const int*>(bcount.p), kskip.p);
         }
+        DevBuf<uint8_t> kend_b(1, st);
+        if (no_skip) {
+          const uint8_t full = static_cast<uint8_t>(rp.n_samples);
+          copy_to_device(ctx, kend_b.p, &full, 1);
+        } else {
+          launch(ctx, "seg2", k_tail_skip, dim3(1), dim3(32), 0, a.g,
+                 static_cast<const V3*>(s->bpts.p), 1, L3 + eps, rp.n_samples, bk,
+                 static_cast<const int*>(blist.p), static_cast<const int*>(bcount.p), kend_b.p);
+        }
         auto runr = [&](auto kern) {
           launch(ctx, "seg2", kern, dim3(rblocks), dim3(threads), 0, a,
                  static_cast<const SurvDev*>(s->surv.p), S1, s->sol_bits.p, ctr.p, sc_list.p,
-                 sc_count.p, bb.p, unit_ctr.p, static_cast<const uint8_t*>(kskip.p));
+                 sc_count.p, bb.p, unit_ctr.p, static_cast<const uint8_t*>(kskip.p),
+                 static_cast<const uint8_t*>(kend_b.p));
         };
         eight ? runr(k_seg2_rows<true>) : runr(k_seg2_rows<false>);
         blocks = rblocks;
@@ -1506,6 +1545,7 @@ struct BatchDev {
   unsigned* tail_ctr;
   int tail_cap;
   BestRec* tail_best;  // [T] argmin over the queued pairs
+  const uint8_t* kend_b;  // [T] samples of the v3 walks [p2, b] not proven free (k_tail_skip)
   int nrings;
   const int* ring_off;
   const double* ring_c;
@@ -1738,7 +1778,7 @@ __global__ void __launch_bounds__(256, RP_BQ_MINB) k_bq_seg2(BatchDev d) {
       const V3 v3 = b - p2;
       const double v3_len = rpd::norm(v3);
       (void)v3_len;  // gap and length tests already passed in visit
-      if (rpd::walk_first_blocked(a.g, p2, b, a.n) != 0) return;
+      if (rpd::walk_first_blocked(a.g, p2, b, a.n, d.kend_b[t]) != 0) return;
       ++c_v3;
       if (!walk4) return;
       const V3 s2 = L2 * dir2;
@@ -1981,7 +2021,7 @@ __global__ void __launch_bounds__(kTailBlock, 4) k_bq_tail(BatchDev d) {
     const V3 dir2 = qvec(a, j);
     const V3 p2 = p1 + L2 * dir2;
     const V3 v3 = b - p2;
-    if (rpd::walk_first_blocked_fast_seg(a.g, p2, b, a.n) == 0) {
+    if (rpd::walk_any_blocked_upto(a.g, p2, b, a.n, d.kend_b[t]) == 0) {
       ++c_v3;
       if (!EIGHT || d.walk4_ok[t]) {
         const V3 s2 = L2 * dir2;
@@ -2336,6 +2376,19 @@ extern "C" rp_status rp_solve_reach_batch(rp_ctx* ctx, const rp_arm* arm, const 
     DevBuf<int> d_ttgt(std::max(1, tail_cap), st), d_tlen(std::max(1, tail_cap), st);
     DevBuf<BestRec> d_tbest(CH, st);
     const std::vector<BestRec> tbest_init(CH, BestRec{1e308, LLONG_MAX});
+    // occupied coarse blocks of the grid (once per call) for k_tail_skip
+    const int dmax = std::max(g->dims[0], std::max(g->dims[1], g->dims[2]));
+    int bk = 4;
+    while (bk < 64 && bk * 32 < dmax) bk *= 2;
+    const int nbx = (g->dims[0] + bk - 1) / bk, nby = (g->dims[1] + bk - 1) / bk,
+              nbz = (g->dims[2] + bk - 1) / bk;
+    DevBuf<int> blist(static_cast<size_t>(nbx) * nby * nbz, st), bcount(1, st);
+    bcount.zero();
+    static const bool no_skip = std::getenv("RP_NO_ROW_SKIP") != nullptr;
+    if (!no_skip)
+      launch(ctx, "seg2", k_occ_blocks, dim3(nblk(static_cast<int64_t>(nbx) * nby * nbz, 256)),
+             dim3(256), 0, a.g, bk, nbx, nby, nbz, blist.p, bcount.p);
+    DevBuf<uint8_t> d_kend(CH, st);
     DevBuf<long long> d_scl(kBatchShortcutCap, st);
     DevBuf<BestRec> d_bb(static_cast<size_t>(CH) * BPT, st), d_best(CH, st);
     DevBuf<BatchPose> d_pose(CH, st);
@@ -2404,6 +2457,14 @@ extern "C" rp_status rp_solve_reach_batch(rp_ctx* ctx, const rp_arm* arm, const 
       d.tail_cap = tail_cap;
       d.tail_best = d_tbest.p;
       copy_to_device(ctx, d_tbest.p, tbest_init.data(), T * sizeof(BestRec));
+      if (no_skip) {
+        RP_CUDA(cudaMemsetAsync(d_kend.p, rp->n_samples, T, st));
+      } else {
+        launch(ctx, "seg2", k_tail_skip, dim3(nblk(static_cast<int64_t>(T) * 32, 256)), dim3(256),
+               0, a.g, static_cast<const V3*>(d_b.p), T, L3 + eps, rp->n_samples, bk,
+               static_cast<const int*>(blist.p), static_cast<const int*>(bcount.p), d_kend.p);
+      }
+      d.kend_b = d_kend.p;
       launch(ctx, "walk4", k_bq_walk4, dim3(nblk(T, 128)), dim3(128), 0, d, d_w4.p);
       launch(ctx, "seg1", k_bq_seg1, dim3(nblk(q->n, 256), T), dim3(256), 0, d);
       launch(ctx, "compact", k_bq_compact, dim3(T), dim3(1024), 0, d);
