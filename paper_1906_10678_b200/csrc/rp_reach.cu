@@ -2356,7 +2356,7 @@ extern "C" rp_status rp_solve_reach_batch(rp_ctx* ctx, const rp_arm* arm, const 
     proto.bdirs.alloc(1, st);
     copy_to_device(ctx, proto.bdirs.p, &bdir, sizeof(V3));
     a.bdirs = proto.bdirs.p;
-    const int CH = 256;
+    static const int CH = std::getenv("RP_BATCH_CHUNK") ? std::atoi(std::getenv("RP_BATCH_CHUNK")) : 128;
     const int BPT = 64;
     const int refine_mode = eight ? (rp->refine_triangle_8dof ? 1 : 0) : 2;
     DevBuf<V3> d_t(CH, st), d_b(CH, st);
