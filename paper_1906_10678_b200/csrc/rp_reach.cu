@@ -2150,7 +2150,7 @@ struct ScBest {
 };
 
 /// One block per target over its (key-sorted) shortcut records.
-__global__ void k_bq_sc_reduce(const long long* __restrict__ keys, const ShortcutRec* __restrict__ recs,
+__global__ void __launch_bounds__(1024) k_bq_sc_reduce(const long long* __restrict__ keys, const ShortcutRec* __restrict__ recs,
                                int n, ScBest* __restrict__ out, uint8_t* __restrict__ has_sc) {
   const long long t = blockIdx.x;
   // [lo, hi) of keys with target t (keys sorted ascending)
@@ -2499,7 +2499,7 @@ extern "C" rp_status rp_solve_reach_batch(rp_ctx* ctx, const rp_arm* arm, const 
         DevBuf<ShortcutRec> recs(nsc, st);
         launch(ctx, "shortcuts", k_bq_shortcuts, dim3(nblk(nsc, 128)), dim3(128), 0, d,
                static_cast<const long long*>(sorted.p), static_cast<int>(nsc), recs.p);
-        launch(ctx, "shortcuts", k_bq_sc_reduce, dim3(T), dim3(128), 0,
+        launch(ctx, "shortcuts", k_bq_sc_reduce, dim3(T), dim3(1024), 0,
                static_cast<const long long*>(sorted.p), static_cast<const ShortcutRec*>(recs.p),
                static_cast<int>(nsc), d_scb.p, d_hs.p);
       }
