@@ -1557,47 +1557,55 @@ struct BatchDev {
 /// in the generator or here can only add directions, never drop one. Writes
 /// up to 2 arcs as (first index, length) and returns their number; a full
 /// ring is one arc (0, cnt).
-__device__ __noinline__ int ring_arcs(double cphi, double sphi, int cnt, V3 u, double lo, double hi, int* a0,
-                         int* len) {
-  const double rho = sqrt(u.x * u.x + u.y * u.y);
-  const double A = cphi * rho, B = sphi * u.z;
-  if (!(A > 1e-9)) {  // q.u is B +- A over the whole ring
-    if (B + A >= lo && B - A <= hi) {
+__device__ __noinline__ int ring_arcs(double cphi_d, double sphi_d, int cnt, V3 u, double lo_d,
+                                     double hi_d, int* a0, int* len) {
+  // Evaluated in fp32: the arcs only choose which directions are visited
+  // (every visited pair gets the exact tests), so they need to be a
+  // superset, not exact. The band is widened by 1e-5 for the fp32 dot
+  // product and the angular margin by 2e-3 rad for fp32 acos/atan2 (its
+  // error near |x| = 1 is below 4e-4 rad) on top of the 1.5-step margin.
+  const float cphi = static_cast<float>(cphi_d), sphi = static_cast<float>(sphi_d);
+  const float ux = static_cast<float>(u.x), uy = static_cast<float>(u.y), uz = static_cast<float>(u.z);
+  const float lo = static_cast<float>(lo_d) - 1e-5f, hi = static_cast<float>(hi_d) + 1e-5f;
+  const float rho = sqrtf(ux * ux + uy * uy);
+  const float A = cphi * rho, B = sphi * uz;
+  if (!(A > 1e-5f)) {  // q.u is B +- A over the whole ring
+    if (B + A + 1e-5f >= lo && B - A - 1e-5f <= hi) {
       a0[0] = 0;
       len[0] = cnt;
       return 1;
     }
     return 0;
   }
-  const double x_hi = (hi - B) / A, x_lo = (lo - B) / A;
-  if (x_lo > 1.0 || x_hi < -1.0) return 0;
-  const double kPiD = 3.14159265358979323846;
-  const double step = 2.0 * kPiD / cnt;
-  const double marg = 1.5 * step + 1e-7;
-  const double d_lo = fmax(0.0, (x_hi >= 1.0 ? 0.0 : acos(fmax(-1.0, x_hi))) - marg);
-  const double d_hi = fmin(kPiD, (x_lo <= -1.0 ? kPiD : acos(fmin(1.0, x_lo))) + marg);
-  if (d_lo <= 0.0 && d_hi >= kPiD) {
+  const float x_hi = (hi - B) / A, x_lo = (lo - B) / A;
+  if (x_lo > 1.0f || x_hi < -1.0f) return 0;
+  const float kPiF = 3.14159265358979323846f;
+  const float step = 2.0f * kPiF / cnt;
+  const float marg = 1.5f * step + 2e-3f;
+  const float d_lo = fmaxf(0.0f, (x_hi >= 1.0f ? 0.0f : acosf(fmaxf(-1.0f, x_hi))) - marg);
+  const float d_hi = fminf(kPiF, (x_lo <= -1.0f ? kPiF : acosf(fminf(1.0f, x_lo))) + marg);
+  if (d_lo <= 0.0f && d_hi >= kPiF) {
     a0[0] = 0;
     len[0] = cnt;
     return 1;
   }
-  const double thu = atan2(u.y, u.x);
+  const float thu = atan2f(uy, ux);
   int n = 0;
-  auto arc = [&](double t0, double t1) {
-    const long m0 = static_cast<long>(ceil(t0 / step)), m1 = static_cast<long>(floor(t1 / step));
-    long c = m1 - m0 + 1;
+  auto arc = [&](float t0, float t1) {
+    const int m0 = static_cast<int>(ceilf(t0 / step)), m1 = static_cast<int>(floorf(t1 / step));
+    const int c = m1 - m0 + 1;
     if (c <= 0) return;
     if (c >= cnt) {
       a0[n] = 0;
       len[n++] = cnt;
       return;
     }
-    long s0 = m0 % cnt;
+    int s0 = m0 % cnt;
     if (s0 < 0) s0 += cnt;
-    a0[n] = static_cast<int>(s0);
-    len[n++] = static_cast<int>(c);
+    a0[n] = s0;
+    len[n++] = c;
   };
-  if (d_lo <= 0.0) {
+  if (d_lo <= 0.0f) {
     arc(thu - d_hi, thu + d_hi);
   } else {
     arc(thu + d_lo, thu + d_hi);
