@@ -1780,7 +1780,7 @@ __global__ void __launch_bounds__(256, RP_BQ_MINB) k_bq_seg2(BatchDev d) {
     // self-collision check 32 queued pairs at a time, so the heavy tail
     // (a few % of pairs) executes without divergence.
     const auto heavy = [&](int j) {
-      const int64_t p = static_cast<int64_t>(s) * a.Q + j;
+      const int64_t p = static_cast<int64_t>(i) * a.Q + j;  // key i * Q + j (see k_bq_tail)
       const V3 dir2 = qvec(a, j);
       const V3 p2 = p1 + L2 * dir2;
       const V3 v3 = b - p2;
@@ -1856,7 +1856,7 @@ __global__ void __launch_bounds__(256, RP_BQ_MINB) k_bq_seg2(BatchDev d) {
       if (tb >= 0) {
         if (pass)
           d.tail_pool[static_cast<size_t>(tb) * kTailBlock + tf + __popc(m & ((1u << lane) - 1u))] =
-              static_cast<uint32_t>(static_cast<int64_t>(s) * a.Q + j);
+              static_cast<uint32_t>(static_cast<int64_t>(i) * a.Q + j);
         tf += n;
       } else if (pass) {
         heavy(j);
@@ -2020,10 +2020,10 @@ __global__ void __launch_bounds__(kTailBlock, 4) k_bq_tail(BatchDev d) {
   unsigned c_v3 = 0, c_sol = 0;
   BestRec best{1e308, LLONG_MAX};
   if (static_cast<int>(threadIdx.x) < len) {
+    // queued key i * Q + j (ordered as the canonical (s, j): i ascends with s)
     const uint32_t p = d.tail_pool[static_cast<size_t>(c) * kTailBlock + threadIdx.x];
-    const int s = static_cast<int>(p / static_cast<uint32_t>(a.Q));
-    const int j = static_cast<int>(p - static_cast<uint32_t>(s) * static_cast<uint32_t>(a.Q));
-    const int i = d.surv_idx[static_cast<size_t>(t) * a.Q + s];
+    const int i = static_cast<int>(p / static_cast<uint32_t>(a.Q));
+    const int j = static_cast<int>(p - static_cast<uint32_t>(i) * static_cast<uint32_t>(a.Q));
     const V3 s1 = L1 * qvec(a, i);
     const V3 p1 = arm.root + s1;
     const V3 dir2 = qvec(a, j);
@@ -2241,9 +2241,8 @@ __global__ void k_bq_finish(BatchDev d, const uint8_t* has_shortcut, int refine_
   }
   const SolveDev& a = d.a;
   const ArmDev& arm = a.arm;
-  const int s = static_cast<int>(b.key / a.Q);
-  const int j = static_cast<int>(b.key - static_cast<long long>(s) * a.Q);
-  const int i = d.surv_idx[static_cast<size_t>(t) * a.Q + s];
+  const int i = static_cast<int>(b.key / a.Q);  // batch keys are i * Q + j
+  const int j = static_cast<int>(b.key - static_cast<long long>(i) * a.Q);
   const V3 p1 = arm.root + arm.L[0] * qvec(a, i);
   const V3 p2 = p1 + arm.L[1] * qvec(a, j);
   DevPose p{};
