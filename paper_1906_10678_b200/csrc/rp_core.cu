@@ -272,6 +272,8 @@ rp_ctx* worker_ctx(rp_ctx* parent, int k) {
     RP_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
     c->stream = c->own;
     c->sm_count = parent->sm_count;
+    RP_CUDA(cudaMalloc(reinterpret_cast<void**>(&c->cancel_flag), sizeof(int)));
+    RP_CUDA(cudaMemset(c->cancel_flag, 0, sizeof(int)));
     parent->workers.push_back(c);
   }
   rp_ctx* w = parent->workers[k];
@@ -334,6 +336,8 @@ rp_status rp_ctx_destroy(rp_ctx* ctx) {
     }
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->cancel_flag) cudaFree(ctx->cancel_flag);
+    if (ctx->aux) cudaStreamDestroy(ctx->aux);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;
   });

@@ -75,6 +75,11 @@ struct rp_ctx {
   // Worker contexts (own streams, same device) for concurrent planner
   // attempts; created on first use, folded back by ctx_absorb.
   std::vector<rp_ctx*> workers;
+  // Worker contexts: a device flag that stops this worker's cooperative pass
+  // (set and cleared by DMA copies), and the auxiliary stream those copies
+  // use on the parent.
+  int* cancel_flag = nullptr;
+  cudaStream_t aux = nullptr;
 };
 
 namespace rp {

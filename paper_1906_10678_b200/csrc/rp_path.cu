@@ -1236,10 +1236,18 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
             b.j = lj[b.ord - static_cast<long long>(a) * ncj];
           }
           A.block_best[blockIdx.x] = b;
+          // cancellation is sampled by block 0 before the barrier and read
+          // by every block after it, so all blocks leave together
+          if (fast_eval && A.cancel && blockIdx.x == 0)
+            A.state[3] = *reinterpret_cast<const volatile int*>(A.cancel);
         }
         long long c3 = prof ? clock64() : 0;
         grid_barrier(A.bar, nb);
         long long c4 = prof ? clock64() : 0;
+        if (fast_eval && A.cancel && __ldcg(A.state + 3)) {
+          rebuild();
+          return;  // state[3] != 0 tells the host the pass was cancelled
+        }
         if (fast_eval) {
           // Every block reduces the per-block winners itself and rebuilds the
           // winning pose (the candidate travels in block_best), so the next
@@ -2036,6 +2044,7 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
   A.block_best = bp_best.p;
   A.bar = bp_bar.p;
   A.state = bp_state.p;
+  A.cancel = cancel_flag;
   static const bool profile = std::getenv("RP_PROFILE_PASS") != nullptr;
   DevBuf<long long> prof;
   if (profile) {
@@ -2064,6 +2073,11 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
   }
   out->ok = hs[2] != 0;
   out->failed_index = hs[1];
+  out->cancelled = hs[3] != 0;
+  if (out->cancelled) {
+    out->ok = false;
+    return true;
+  }
   out->poses.resize(m);
   out->relax.resize(m);
   out->kind.resize(m);

@@ -123,7 +123,8 @@ struct BpArgs {
   BpWin* win;             // [m] fast path: winners, rebuilt into poses at the end
   WikBest* block_best;
   unsigned* bar;  // [2] barrier count + generation
-  int* state;     // [4] found, failed_index, ok
+  int* state;     // [4] found, failed_index, ok, cancelled
+  const int* cancel;  // device flag set (by a host DMA) to stop the pass early; may be null
   long long* prof;  // optional [8] phase cycle counters (RP_PROFILE_PASS)
 };
 

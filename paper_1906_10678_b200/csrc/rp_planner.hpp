@@ -69,6 +69,7 @@ struct Planner {
     std::vector<double> relax;
     std::vector<int> kind;
     std::vector<V3> wps;
+    bool cancelled = false;
   };
   bool backward_pass_device(const std::vector<V3>& wps, const HostPose& anchor,
                             const std::vector<double>& factors, bool cloud, double cloud_radius,
@@ -79,6 +80,8 @@ struct Planner {
   int bp_blocks = 0;
   int bp_blocks_cap = 0;  // > 0: at most this many blocks (concurrent passes)
   bool use_device_pass = true;
+  /// device flag polled by the cooperative pass (set to stop it; null: never)
+  const int* cancel_flag = nullptr;
   std::vector<long long> rank_by_deviation(rp_solution_set* set,
                                            const std::vector<std::vector<V3>>& lists,
                                            const std::vector<V3>& poly, bool lead, V3 lead_pt,
