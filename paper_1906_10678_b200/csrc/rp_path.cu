@@ -904,6 +904,9 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
   __shared__ long long s_ct[kBpThreads];
   __shared__ int s_nc;
   __shared__ short s_rank[kBpThreads];
+  // the screened pairs' segment-1 data and j, kept for the evaluation waves
+  __shared__ CiFast s_cf[kBpThreads];
+  __shared__ int s_cj[kBpThreads];
   const bool fast_eval = !A.arm.any_limit && !A.arm.has_offsets;
   // fast path: block 0 rebuilds the published poses from their winners
   // before the kernel ends (every exit below goes through here)
@@ -1124,11 +1127,14 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
               const int a = static_cast<int>(tt / ncj);
               if (__ldcg(&A.ci_fast[li[a]].ok)) {
                 const CiFast c = ldcg_struct(A.ci_fast + li[a]);
+                const int jj = lj[tt - static_cast<long long>(a) * ncj];
                 double mm;
-                if (wik_pre_fast(w, c, lj[tt - static_cast<long long>(a) * ncj], &mm)) {
+                if (wik_pre_fast(w, c, jj, &mm)) {
                   const int k = atomicAdd(&s_nc, 1);
                   s_cm[k] = mm;
                   s_ct[k] = tt;
+                  s_cf[k] = c;
+                  s_cj[k] = jj;
                 }
               }
               tt += stride;
@@ -1166,9 +1172,8 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
                 mm = s_cm[e];
                 t2 = s_ct[e];
                 if (wik_better(mm, t2, bm, bo)) {  // else it cannot improve this half's best
-                  const int a = static_cast<int>(t2 / ncj);
-                  c = ldcg_struct(A.ci_fast + li[a]);
-                  jj = lj[t2 - static_cast<long long>(a) * ncj];
+                  c = s_cf[e];
+                  jj = s_cj[e];
                   valid = true;
                 }
               }
