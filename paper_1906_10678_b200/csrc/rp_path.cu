@@ -393,7 +393,8 @@ __device__ bool wik_full_half(const WikDev& w, const CiFast& c, int j, bool vali
   const V3 p3 = p2 + s3;
   V3 J[4];
   J[0] = arm.root;
-  J[1] = J[0] + arm.L[0] * (valid ? wq(w, c.i) : V3{0, 0, 1});
+  // root + L1 * q_i: the filter's p1 (wik_filter_fast), same operations
+  J[1] = valid ? c.p1 : J[0] + arm.L[0] * V3{0, 0, 1};
   J[2] = J[1] + arm.L[1] * qj;
   J[3] = J[2] + s3;
   alive = alive && rpd::norm(J[1] - w.prev_j1) <= w.sm1 && rpd::norm(J[2] - w.prev_j2) <= w.sm2;
