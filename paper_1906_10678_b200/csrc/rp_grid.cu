@@ -15,6 +15,9 @@
 // integers), so every kernel below decides membership identically.
 #include "rp_internal.hpp"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -277,6 +280,119 @@ __global__ void __launch_bounds__(NT) k_mark_dilate_rowwise(uint64_t* __restrict
   }
 }
 
+/// Plane-run form for overwrite passes over full planes (y0 = 0, y1 = ny - 1):
+/// the planes z0..z1 are one contiguous run of rows in (z, y) order, and a
+/// block owns PR consecutive rows of it (one row per thread, usually one
+/// plane segment), so its whole tile leaves through ONE bulk store
+/// (PR * WX * 8 bytes: 16 KB at 512^3). Measured on B200 at 512^3 / 40 boxes:
+/// 4.34 vs 5.10 us per pass for the 32-row x 8-plane tiles (8 bulk stores of
+/// 2 KB per block). `bulk` = 0 when the run is not 16-byte aligned (odd
+/// rows * WX): plain stores then.
+template <int WX, int PR, bool TMAP>
+__global__ void __launch_bounds__(PR) k_mark_dilate_plane(uint64_t* __restrict__ bits, GridView g,
+                                                          const Prim* __restrict__ prims, int np,
+                                                          const int* __restrict__ wtab, int reach,
+                                                          int z0, int z1, int bulk,
+                                                          const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ Prim sp_all[];
+  Prim* sp = sp_all + np;
+  int* swt = reinterpret_cast<int*>(sp_all + 2 * np);
+  __shared__ int ns;
+  __shared__ __align__(1024) uint64_t tile[PR * WX];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // flat rows fit int32: ny * nz <= the 2^27 cell budget
+  const int run0 = z0 * g.ny;
+  const int nrun = (z1 - z0 + 1) * g.ny;
+  const int r0 = static_cast<int>(blockIdx.x) * PR;
+  const int rows = min(PR, nrun - r0);
+  // the tile's z range, and its y range when it stays in one plane (block-uniform divisions)
+  const int zf = z0 + r0 / g.ny, yf0 = r0 % g.ny;
+  const int zl = z0 + (r0 + rows - 1) / g.ny;
+  const int yf = zf == zl ? yf0 : 0;
+  const int yl = zf == zl ? yf0 + rows - 1 : g.ny - 1;
+  if (threadIdx.x == 0) ns = 0;
+  {
+    const int* src = reinterpret_cast<const int*>(prims);
+    int* dst = reinterpret_cast<int*>(sp_all);
+    for (int k = threadIdx.x; k < 6 * np; k += blockDim.x) dst[k] = __ldg(src + k);
+    const int nw = 2 * reach * reach + 1;
+    for (int k = threadIdx.x; k < nw; k += blockDim.x) swt[k] = __ldg(wtab + k);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < np; k += blockDim.x) {
+    const Prim p = sp_all[k];
+    if (p.a[0] > p.b[0] || p.a[1] > p.b[1] || p.a[2] > p.b[2]) continue;
+    if (p.a[2] - reach > zl || p.b[2] + reach < zf) continue;
+    if (p.a[1] - reach > yl || p.b[1] + reach < yf) continue;
+    sp[atomicAdd(&ns, 1)] = p;
+  }
+  __syncthreads();
+  const bool valid = static_cast<int>(threadIdx.x) < rows;
+  int z = zf, y = yf0 + static_cast<int>(threadIdx.x);
+  while (y >= g.ny) {  // at most PR / ny steps (none for ny >= PR within a plane)
+    y -= g.ny;
+    ++z;
+  }
+  uint64_t m[WX];
+#pragma unroll
+  for (int w = 0; w < WX; ++w) m[w] = 0;
+  const int n_here = valid ? ns : 0;
+  for (int k = 0; k < n_here; ++k) {
+    const Prim p = sp[k];
+    const int dy = y < p.a[1] ? p.a[1] - y : (y > p.b[1] ? y - p.b[1] : 0);
+    const int dz = z < p.a[2] ? p.a[2] - z : (z > p.b[2] ? z - p.b[2] : 0);
+    if (dy > reach || dz > reach) continue;
+    const int wd = swt[dy * dy + dz * dz];
+    if (wd < 0) continue;
+    int lo = p.a[0] - wd, hi = p.b[0] + wd;
+    lo = lo < 0 ? 0 : lo;
+    hi = hi > g.nx - 1 ? g.nx - 1 : hi;
+#pragma unroll
+    for (int w = 0; w < WX; ++w) m[w] |= range_mask(lo, hi, 64 * w);
+  }
+  uint64_t* gdst = bits + (static_cast<size_t>(run0) + r0) * WX;
+  if (!bulk) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (valid) {
+#pragma unroll
+      for (int w = 0; w < WX; ++w) gdst[static_cast<size_t>(threadIdx.x) * WX + w] = m[w];
+    }
+    return;
+  }
+  if (TMAP) {
+    // 64-byte rows staged in the tensor map's 64B-swizzled layout (16-byte
+    // chunk c of row r at chunk c ^ ((r >> 1) & 3)): the 16-byte stores of a
+    // quarter-warp hit 8 distinct bank groups instead of 2; the TMA tensor
+    // store un-swizzles on the way out and clips the run's last tile.
+    static_assert(!TMAP || WX == 8, "swizzled staging assumes 64-byte rows");
+    const int rr = static_cast<int>(threadIdx.x);
+    ulonglong2* row = reinterpret_cast<ulonglong2*>(&tile[rr * WX]);
+#pragma unroll
+    for (int c = 0; c < WX / 2; ++c) row[c ^ ((rr >> 1) & 3)] = make_ulonglong2(m[2 * c], m[2 * c + 1]);
+  } else {
+#pragma unroll
+    for (int w = 0; w < WX; ++w) tile[threadIdx.x * WX + w] = m[w];
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0) {
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(&tile[0]));
+    if (TMAP)
+      asm volatile(
+          "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+              reinterpret_cast<uint64_t>(&tmap)),
+          "r"(0), "r"(r0), "r"(sa)
+          : "memory");
+    else
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+                   "r"(sa), "r"(static_cast<uint32_t>(rows * WX * 8))
+                   : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+}
+
 /// Persistent form of k_mark_dilate_rowwise for full-grid, overwrite passes
 /// (accumulate == 0, WX >= 2): ~2 blocks per SM loop over the 32-row x
 /// 8-plane tiles. The primitive list and width table are staged once per
@@ -432,6 +548,30 @@ void launch_rows(rp_ctx* ctx, const char* name, rp_grid* g, const Prim* prims, i
                  const int* wtab, int reach, int y0, int y1, int z0, int z1, bool accumulate,
                  bool pdl = false);
 
+/// TMA tensor map of a run of `nrows` 64-byte rows (8 x u64) starting at
+/// `base`, box = `box_rows` rows, 64B swizzle (k_mark_dilate_plane's staging
+/// layout). cuTensorMapEncodeTiled comes from the driver through the
+/// runtime's entry-point query (no -lcuda). False if unavailable.
+bool encode_run_map(CUtensorMap* map, uint64_t* base, uint64_t nrows, int box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+  const cuuint64_t dims[2] = {8, nrows};
+  const cuuint64_t strides[1] = {64};
+  const cuuint32_t box[2] = {8, static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, base, dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 /// Rasterise host-computed index boxes (one async upload, no box kernel).
 bool launch_rows_param(rp_ctx* ctx, const char* name, rp_grid* g, const std::vector<Prim>& prims,
                        const DilTable& t, int y0, int y1, int z0, int z1, bool accumulate) {
@@ -470,14 +610,51 @@ void launch_rows(rp_ctx* ctx, const char* name, rp_grid* g, const Prim* prims, i
              y0, y1, z0, z1, acc);
   };
   static const bool no_tiles = std::getenv("RP_NO_TILE_KERNEL") != nullptr;
+  // RP_DIL_KERNEL=plane|tiles|rowwise forces a variant where it applies (A/B)
+  static const std::string force = std::getenv("RP_DIL_KERNEL") ? std::getenv("RP_DIL_KERNEL") : "";
   const bool full = y0 == 0 && z0 == 0 && y1 == g->dims[1] - 1 && z1 == g->dims[2] - 1;
+  const bool planes = y0 == 0 && y1 == g->dims[1] - 1;
   // The persistent tile kernel wins while every block owns one tile (256^3:
   // 1.9 vs 2.2 us per pass); at 512^3 its serial per-block tile loop loses to
   // one tile per block (8.2 vs 5.4 us), measured on B200.
   const int ntiles = ((g->dims[1] + 31) / 32) * ((g->dims[2] + 7) / 8);
   static const int bps = std::getenv("RP_TILE_BPS") ? std::atoi(std::getenv("RP_TILE_BPS")) : 4;
-  if (!accumulate && full && !no_tiles && (g->wx == 2 || g->wx == 4 || g->wx == 8) &&
-      ntiles <= std::max(1, bps) * ctx->sm_count) {
+  const bool wx_ok = g->wx == 1 || g->wx == 2 || g->wx == 4 || g->wx == 8;
+  const bool tiles_ok = !accumulate && full && !no_tiles && wx_ok && g->wx >= 2;
+  const bool tiles_small = ntiles <= std::max(1, bps) * ctx->sm_count;
+  if (!accumulate && planes && wx_ok && force != "tiles" && force != "rowwise" &&
+      (force == "plane" || !(tiles_ok && tiles_small))) {
+    constexpr int PR = 256;
+    const int64_t nrun = static_cast<int64_t>(z1 - z0 + 1) * g->dims[1];
+    const int bulk = (static_cast<int64_t>(z0) * g->dims[1] * g->wx) % 2 == 0 &&
+                     (nrun * g->wx) % 2 == 0;
+    const dim3 grid(static_cast<unsigned>((nrun + PR - 1) / PR));
+    CUtensorMap tmap{};
+    static const bool no_tmap = std::getenv("RP_NO_TMAP") != nullptr;
+    const bool use_tmap = g->wx == 8 && bulk && !no_tmap &&
+                          encode_run_map(&tmap, g->bits + static_cast<size_t>(z0) * g->dims[1] * 8,
+                                         static_cast<uint64_t>(nrun), PR);
+    auto plane = [&](auto kern) {
+      if (pdl)
+        launch_pdl(ctx, name, kern, grid, dim3(PR), smem, g->bits, g->view(), prims, np, wtab,
+                   reach, z0, z1, bulk, tmap);
+      else
+        launch(ctx, name, kern, grid, dim3(PR), smem, g->bits, g->view(), prims, np, wtab, reach,
+               z0, z1, bulk, tmap);
+    };
+    switch (g->wx) {
+      case 1: plane(k_mark_dilate_plane<1, PR, false>); return;
+      case 2: plane(k_mark_dilate_plane<2, PR, false>); return;
+      case 4: plane(k_mark_dilate_plane<4, PR, false>); return;
+      default:
+        if (use_tmap)
+          plane(k_mark_dilate_plane<8, PR, true>);
+        else
+          plane(k_mark_dilate_plane<8, PR, false>);
+        return;
+    }
+  }
+  if (tiles_ok && force != "rowwise" && (force == "tiles" || tiles_small)) {
     const dim3 grid(static_cast<unsigned>(ntiles));
     auto tiles = [&](auto kern) {
       if (pdl)
