@@ -347,8 +347,22 @@ __global__ void __launch_bounds__(PR) k_mark_dilate_plane(uint64_t* __restrict__
     int lo = p.a[0] - wd, hi = p.b[0] + wd;
     lo = lo < 0 ? 0 : lo;
     hi = hi > g.nx - 1 ? g.nx - 1 : hi;
+    if (WX == 8) {
+      // one coarse test per half row: most intervals touch 1-3 words of one
+      // half, and a warp's rows mostly agree, so the skip is warp-uniform
+      // (4.60 -> 4.39 us per 512^3 pass; quarter rows measured 4.45 us)
+      if (lo < 256) {
 #pragma unroll
-    for (int w = 0; w < WX; ++w) m[w] |= range_mask(lo, hi, 64 * w);
+        for (int w = 0; w < WX / 2; ++w) m[w] |= range_mask(lo, hi, 64 * w);
+      }
+      if (hi >= 256) {
+#pragma unroll
+        for (int w = WX / 2; w < WX; ++w) m[w] |= range_mask(lo, hi, 64 * w);
+      }
+    } else {
+#pragma unroll
+      for (int w = 0; w < WX; ++w) m[w] |= range_mask(lo, hi, 64 * w);
+    }
   }
   uint64_t* gdst = bits + (static_cast<size_t>(run0) + r0) * WX;
   if (!bulk) {
