@@ -501,9 +501,9 @@ def voxel_update(ctx, torch, stream):
     achieved = bytes_alg / (per_launch * 1e-3) / 1e9
     traffic, traffic_src = None, None
     try:
-        prof = _json.load(open(os.path.join(ROOT, "profiles", "r1i_dilate512_ncu.json")))
+        prof = _json.load(open(os.path.join(ROOT, "profiles", "r1j_dilate512_ncu.json")))
         traffic = prof["dram_bytes_per_launch"]
-        traffic_src = "profiles/r1i_dilate512_ncu.json (ncu --set full, one launch)"
+        traffic_src = "profiles/r1j_dilate512_ncu.json (ncu --set full, one launch)"
     except (OSError, KeyError, ValueError):
         pass
     return {"roofline": {"kernel": "k_mark_dilate_plane<8,256,true> (fused box rasterise + ball "
