@@ -1,24 +1,42 @@
 #!/usr/bin/env python
 """Benchmark: 8-DOF reach-pose + path latency (BASELINE.json metric) on B200.
 
-Workload (BASELINE.json configs[1]): 8-DOF arm
-L = (0.5, 0.5, 0.5, 0.125), 128^3 grid over [-1.6, 1.6]^3, 12 synthetic box
-obstacles (seed 1236), 2-degree quiver (10,324 directions), n = 8
-(25 waypoints = root + 3n), target (1.0, 0.35, 0.3), approach +x.
-One step = build the scene grid (voxelize + dilate) -> solve_reach ->
-select_solution -> plan_from_reach (backward pass, unfold, fallback cascade).
+Workload (BASELINE.json configs[2], SURVEY.md §8d C3 — the north star's
+"8-DOF reach pose plus a 20-waypoint obstacle-avoiding path on a 256^3
+grid"): 8-DOF arm L = (0.5, 0.5, 0.5, 0.125), 256^3 grid over
+[-1.6, 1.6]^3, 40 synthetic box obstacles, 2-degree quiver (10,324
+directions), n = 8 (25 waypoints = root + 3n; exactly 20 is not producible,
+SURVEY §0.1.4). One step =
+  build the scene grid (voxelize + dilate)
+  -> plan_reach_then_path to the target (1.0, 0.35, 0.3)
+     (solve_reach, select_solution, plan_from_reach: backward pass, unfold,
+     fallback cascade)
+  -> plan_arbitrary from that plan's final pose to the second target
+     (anchor solve, virtual-arm solve, pinned backward passes),
+which the reference delivers as a 25-waypoint "virtual-arm" path
+(tests/golden/configs/C3_2.json pins both plans bit for bit).
 
-The line also reports the voxel-update throughput of the shell-dilation
-kernel (the metric's second half) on a 512^3 / 40-box scene with its HBM
-roofline, and the reference CPU solver timed on this host.
+The line also carries the voxel-update throughput of the shell-dilation
+kernel (the metric's second half) on 512^3 with its HBM roofline, the C5
+batched queries, the other configurations' latencies, and the reference CPU
+solver timed on this host (cmd_bench's stage columns, workers = 1 and all
+cores).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config C3|C2]
+
+--gpus N > 1 without torchrun re-launches itself under
+torch.distributed.run with N ranks (one per GPU, NCCL). The planner path does
+not shard (the backward pass is sequential), so the headline runs
+as N replicas; the C5 batch leg shards its targets over the ranks.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -38,13 +56,14 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="C2")
+    p.add_argument("--config", default="C3", choices=["C3", "C2"])
     p.add_argument("--quiver-deg", type=float, default=2.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-budget-s", type=float, default=150.0)
     p.add_argument("--no-batch", action="store_true", help="skip the C5 batched-query leg")
     p.add_argument("--batch-queries", type=int, default=4096)
-    p.add_argument("--no-configs", action="store_true", help="skip the C1/C3/C4 latency leg")
+    p.add_argument("--no-configs", action="store_true", help="skip the C1/C2/C4 latency leg")
+    p.add_argument("--no-voxel", action="store_true", help="skip the 512^3 dilation leg")
     return p.parse_args()
 
 
@@ -55,24 +74,105 @@ def dist_env():
     return rank, world, local
 
 
+def maybe_spawn(args):
+    """--gpus N > 1 outside torchrun: run this script under
+    torch.distributed.run with N ranks and exit with its status. Under
+    torchrun, WORLD_SIZE must equal --gpus."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            sys.exit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+        return
+    if args.gpus <= 1:
+        return
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator lines show nranks
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={29500 + os.getpid() % 1000}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd, env=env))
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
 def workload_desc(sc) -> dict:
-    return {"workload": f"{sc.name}: 8-DOF reach pose + {1 + 3 * sc.n_samples}-waypoint path "
-                        f"(plan_reach_then_path), {sc.n}^3 grid, {len(sc.boxes)} boxes, "
-                        f"{sc.quiver_deg:g}-deg quiver",
-            "grid": sc.n, "boxes": len(sc.boxes), "quiver_deg": sc.quiver_deg,
-            "waypoints": 1 + 3 * sc.n_samples, "samples_per_segment": sc.n_samples}
+    wp = 1 + 3 * sc.n_samples
+    if sc.name == "C3":
+        what = (f"C3: 8-DOF reach pose + {wp}-waypoint path (plan_reach_then_path), then a "
+                f"{wp}-waypoint arbitrary-pose path (plan_arbitrary) from its final pose to "
+                f"{tuple(round(x, 4) for x in sc.extra['second_target'])}, {sc.n}^3 grid built "
+                f"each step, {len(sc.boxes)} boxes, {sc.quiver_deg:g}-deg quiver")
+    else:
+        what = (f"{sc.name}: 8-DOF reach pose + {wp}-waypoint path (plan_reach_then_path), "
+                f"{sc.n}^3 grid built each step, {len(sc.boxes)} boxes, "
+                f"{sc.quiver_deg:g}-deg quiver")
+    d = {"workload": what, "grid": sc.n, "boxes": len(sc.boxes), "quiver_deg": sc.quiver_deg,
+         "waypoints": wp, "samples_per_segment": sc.n_samples, "target": list(sc.target)}
+    if sc.name == "C3":
+        d["second_target"] = list(sc.extra["second_target"])
+    return d
+
+
+def plan_digest(summaries) -> str:
+    """World-size and implementation invariant digest of the step's answer:
+    per plan the kind, notes, waypoints and every per-waypoint pose (indices,
+    segments, joints). Both arms print it; equal digests = equal plans."""
+    import numpy as np
+    h = hashlib.sha256()
+    for s in summaries:
+        if s is None:
+            h.update(b"<no plan>")
+            continue
+        h.update(s["kind"].encode())
+        h.update("\n".join(s["notes"]).encode())
+        h.update(np.ascontiguousarray(s["waypoints"], np.float64).tobytes())
+        for p, _ in s["poses"]:
+            n = p.n_segments
+            h.update(np.array(p.quiver_indices[:n], np.int32).tobytes())
+            h.update(np.array([p.segments[k][:] for k in range(n)]).tobytes())
+            h.update(np.array([p.joints[k][:] for k in range(n + 1)]).tobytes())
+    return h.hexdigest()[:16]
 
 
 # ----------------------------------------------------------------------------
 # Reference arm: the reference's own CPU implementation on this host's cores.
 
-def ref_step(sc, workers):
+def ref_step(sc, workers, stages=False):
+    """One step of the workload on the reference (oracle/_ref): scene grid
+    (build_scene_grid), plan_reach_then_path (as cmd_bench's stages when
+    `stages`), then plan_arbitrary for C3. Returns (seconds, rc, summaries,
+    stage ms)."""
     import ref
+    st = {}
     t0 = time.perf_counter()
     R = ref.RefProblem(sc, workers=workers)
-    rc, plan = R.plan_reach_then_path()
+    t1 = time.perf_counter()
+    st["grid_ms"] = 1e3 * (t1 - t0)
+    if stages:
+        rc, plan, s, _ = R.bench_stages(workers=workers)
+        st.update(s)
+    else:
+        rc, plan = R.plan_reach_then_path()
+        st["reach_path_ms"] = 1e3 * (time.perf_counter() - t1)
+    sums = [plan.summary(sc.n_samples) if rc == 0 else None]
+    if sc.name == "C3" and rc == 0:
+        t2 = time.perf_counter()
+        p, w = sums[0]["poses"][-1]
+        rc2, plan2 = R.plan_arbitrary(p, w, sc.extra["second_target"])
+        st["arbitrary_ms"] = 1e3 * (time.perf_counter() - t2)
+        sums.append(plan2.summary(sc.n_samples) if rc2 == 0 else None)
+        rc = rc or rc2
     dt = time.perf_counter() - t0
-    return dt, rc, plan
+    st["total_ms"] = 1e3 * dt
+    return dt, rc, sums, st
 
 
 def run_reference(args, sc):
@@ -90,56 +190,70 @@ def run_reference(args, sc):
     times = []
     warm = 0
     # the reference needs no warm-up; one is run when the budget allows
-    dt, rc, _ = ref_step(sc, cores)
+    dt, rc, sums, st = ref_step(sc, cores)
     per = dt
     if per * (args.steps + 1) <= budget:
         warm = 1
     else:
         times.append(dt)
     while len(times) < args.steps and time.perf_counter() - t_start + per <= budget:
-        dt, rc, _ = ref_step(sc, cores)
+        dt, rc, sums, st = ref_step(sc, cores)
         times.append(dt)
     if not times:
         times.append(dt)
     ms = 1e3 * statistics.mean(times)
-    line = {"metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": args.gpus,
+    line = {"metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": world,
             "steps": len(times), "warmup": warm, "ms_per_step": ms, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {**workload_desc(sc), "parallelism": "cpu-threads"},
             "impl": "reference",
             "cpu_baseline": {"value": ms, "unit": UNIT, "cores": cores, "kind": "reference",
+                             "cpu_model": cpu_model(),
                              "sample": f"full workload, {len(times)} step(s), workers={cores}, "
                                        f"budget {budget:.0f}s"},
             "e2e": {"value": ms, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "plan_rc": rc}
+            "plan_rc": rc, "result_digest": plan_digest(sums), "last_step_stages_ms": st}
     print(json.dumps(line))
     return line
 
 
+_CPU_CODE = (
+    "import sys,json; sys.path.insert(0,%r); sys.path.insert(0,%r)\n"
+    "from paper_1906_10678_b200 import scenes\nimport bench\n"
+    "sc = scenes.config(%r, quiver_deg=%r)\n"
+    "dt, rc, sums, st = bench.ref_step(sc, %d, stages=True)\n"
+    "print(json.dumps({'ms': dt*1e3, 'rc': rc, 'stages': st,"
+    " 'digest': bench.plan_digest(sums)}))\n")
+
+
 def cpu_baseline(sc, budget_s):
-    """Reference CPU solver on this host (rank 0, N=1), bounded: the full
-    workload once if it fits the budget, else a 5-degree-quiver sample."""
+    """The reference CPU solver on this host (rank 0, N=1), as cmd_bench's
+    stage columns (src/cli.cpp:272-308) plus the grid build and, for C3,
+    plan_arbitrary: one full step at workers = all cores (the headline
+    baseline) and one at workers = 1, each bounded by the budget."""
     cores = os.cpu_count() or 1
-    code = (
-        "import sys,json,time; sys.path.insert(0,%r); sys.path.insert(0,%r)\n"
-        "from paper_1906_10678_b200 import scenes\nimport bench\n"
-        "sc = scenes.config(%r, quiver_deg=%r)\n"
-        "dt, rc, _ = bench.ref_step(sc, %d)\nprint(json.dumps({'ms': dt*1e3, 'rc': rc}))\n"
-    )
-    for deg, sample in ((sc.quiver_deg, "full workload (1 step)"),
-                        (5.0, "5-degree-quiver sample of the workload (1 step)")):
+    runs = {}
+    for workers in (cores, 1):
         try:
-            r = subprocess.run([sys.executable, "-c", code % (ROOT, os.path.join(ROOT, "oracle"),
-                                                               sc.name, deg, cores)],
-                               capture_output=True, text=True, timeout=budget_s)
+            r = subprocess.run([sys.executable, "-c", _CPU_CODE % (
+                ROOT, os.path.join(ROOT, "oracle"), sc.name, sc.quiver_deg, workers)],
+                capture_output=True, text=True, timeout=budget_s)
             if r.returncode == 0:
-                out = json.loads(r.stdout.strip().splitlines()[-1])
-                return {"value": out["ms"], "unit": UNIT, "cores": cores, "kind": "reference",
-                        "sample": f"{sample}, workers={cores}, rc={out['rc']}"}
+                runs[workers] = json.loads(r.stdout.strip().splitlines()[-1])
+            else:
+                runs[workers] = {"error": r.stderr.strip().splitlines()[-1:] or ["failed"]}
         except subprocess.TimeoutExpired:
-            continue
-    return {"value": None, "unit": UNIT, "cores": cores, "kind": "reference",
-            "sample": "timed out"}
+            runs[workers] = {"error": f"timed out after {budget_s:.0f}s"}
+    full = runs.get(cores, {})
+    return {"value": full.get("ms"), "unit": UNIT, "cores": cores, "kind": "reference",
+            "cpu_model": cpu_model(),
+            "sample": f"one full step of the workload (grid + cmd_bench stages + "
+                      f"plan_arbitrary), workers={cores}",
+            "stages_ms": {f"workers={w}": {k: round(v, 2) for k, v in r.get("stages", {}).items()}
+                          for w, r in runs.items()},
+            "workers_1_ms": runs.get(1, {}).get("ms"),
+            "rc": full.get("rc"), "result_digest": full.get("digest"),
+            "errors": {w: r["error"] for w, r in runs.items() if "error" in r} or None}
 
 
 # ----------------------------------------------------------------------------
@@ -187,6 +301,12 @@ def plan_bytes(summary) -> int:
     return n
 
 
+KERNEL_GROUPS = ["voxelize", "mark_dilate", "dilate", "overlay", "seg1", "walk1", "compact",
+                 "seg2", "clear2", "select", "shortcuts", "walk4", "backward_pass", "wik_filter",
+                 "wik_compact", "wik_pairs", "score", "rank", "materialize", "unfold",
+                 "pose_check", "refine", "trail", "cone", "finish"]
+
+
 def run_ours(args, sc):
     import numpy as np
     import torch
@@ -207,14 +327,29 @@ def run_ours(args, sc):
     q = api.Quiver(ctx, sc.quiver_step(), sc.quiver_step(), sc.min_per_ring)
     obstacles = sc.obstacles()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    t2 = sc.extra.get("second_target")
 
     def step(read_back: bool):
+        """One step through the public API (C ABI): boxes (host) in, plans out."""
         g = api.Grid.scene(ctx, scenes.BOUNDS_MIN, scenes.BOUNDS_MAX, sc.voxel_size, obstacles,
                            arm, rp)
         rc, plan = api.plan_reach_then_path(ctx, arm, q, g, sc.target, rp)
         if rc != 0:
             raise RuntimeError(f"plan failed rc={rc}")
-        return plan.summary() if read_back else plan
+        out = [plan]
+        if t2 is not None:
+            # the start pose (final pose of the first plan) is read back to
+            # the host and passed in: plan_arbitrary's own API takes a pose
+            s = plan.summary()
+            p, w = s["poses"][-1]
+            rc2, plan2 = api.plan_arbitrary(ctx, arm, q, g, p, t2, rp, start_waypoints=w)
+            if rc2 != 0:
+                raise RuntimeError(f"plan_arbitrary failed rc={rc2}")
+            out = [s, plan2] if read_back else [plan, plan2]
+            if read_back:
+                out[1] = plan2.summary()
+            return out
+        return [plan.summary()] if read_back else out
 
     def barrier():
         if world > 1:
@@ -223,7 +358,7 @@ def run_ours(args, sc):
 
     for _ in range(args.warmup):
         step(False)
-    # -- device-timed K steps (inputs resident: quiver on device, L2 flushed between steps)
+    # -- device-timed K steps (quiver resident; L2 flushed between steps)
     launches0 = ctx.launch_count()
     clocks = Clocks(local)
     per = []
@@ -238,10 +373,9 @@ def run_ours(args, sc):
         per.append((e0, e1))
     barrier()
     clk = clocks.stop()
-    gpu_launches = ctx.launch_count() - launches0
-    total_ms = sum(a.elapsed_time(b) for a, b in per)
-    ms = total_ms / args.steps
-    # -- end to end through the C ABI with host buffers: boxes in, plan out
+    gpu_launches = (ctx.launch_count() - launches0) // max(1, args.steps)
+    ms = sum(a.elapsed_time(b) for a, b in per) / args.steps
+    # -- end to end through the C ABI with host buffers: boxes in, plans out
     barrier()
     e2e_t = []
     last = None
@@ -253,25 +387,27 @@ def run_ours(args, sc):
         e2e_t.append(time.perf_counter() - t0)
     barrier()
     e2e_ms = 1e3 * statistics.mean(e2e_t)
-    h2d = len(obstacles) * C_SIZEOF_OBSTACLE() + 3 * 8
-    d2h = plan_bytes(last)
+    # in: the boxes and the target(s), and for C3 the start pose (with its
+    # waypoint samples) read back from the first plan; out: every plan
+    h2d = len(obstacles) * C_SIZEOF_OBSTACLE() + 3 * 8 * (2 if t2 else 1)
+    d2h = sum(plan_bytes(s) for s in last)
+    if t2 is not None:
+        h2d += plan_bytes({"waypoints": [], "relax": [], "unfold": [],
+                           "poses": [last[0]["poses"][-1]]})
     if world > 1:
         t = torch.tensor([ms, e2e_ms], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms, e2e_ms = float(t[0]), float(t[1])
-    # -- per-kernel breakdown of one instrumented step
+    # -- per-kernel breakdown of one instrumented step (events per launch)
     ctx.enable_timing(True)
     ctx.reset_timing()
     step(False)
-    names = ["voxelize", "mark_dilate", "seg1", "compact", "seg2", "select", "shortcuts", "walk4",
-             "backward_pass", "wik_filter", "wik_compact", "wik_pairs", "score", "materialize",
-             "unfold", "pose_check", "refine", "trail"]
-    kt = {n: ctx.kernel_time(n) for n in names}
+    kt = {n: ctx.kernel_time(n) for n in KERNEL_GROUPS}
     ctx.enable_timing(False)
     kernel_ms = {n: round(v[0], 4) for n, v in kt.items() if v[1]}
+    kernel_launches = {n: int(v[1]) for n, v in kt.items() if v[1]}
     dominant = max(kernel_ms, key=kernel_ms.get)
-    # -- voxel update throughput of the fused shell-dilation kernel at 512^3
-    vox = voxel_update(ctx, torch, stream)
+    vox = None if args.no_voxel else voxel_update(ctx, torch, stream)
     # -- C5: 4096 batched reach queries sharded over the ranks
     batch = None if args.no_batch else batch_queries(args, ctx, torch, stream, rank, world)
     # -- latency of the other BASELINE configurations (rank 0's view)
@@ -282,18 +418,22 @@ def run_ours(args, sc):
         "metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {**workload_desc(sc), "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+        "config": {**workload_desc(sc),
+                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
                    "l2": "flushed between timed steps (256 MiB write)"},
         "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": gpu_launches,
         "clocks": clk,
-        "roofline": vox["roofline"],
-        "voxel_update": vox["summary"],
+        "roofline": vox["roofline"] if vox else None,
+        "voxel_update": vox["summary"] if vox else None,
         "kernel_ms_per_step": kernel_ms,
+        "kernel_launches_per_step": kernel_launches,
         "dominant_kernel": {"name": dominant, "ms": kernel_ms[dominant],
                             "share": kernel_ms[dominant] / max(ms, 1e-9)},
-        "plan": {"kind": last["kind"], "notes": last["notes"], "waypoints": len(last["waypoints"])},
+        "plans": [{"kind": s["kind"], "notes": s["notes"], "waypoints": len(s["waypoints"])}
+                  for s in last],
+        "result_digest": plan_digest(last),
         "batch": batch,
         "configs": configs,
         "paper_ms": PAPER_MS,
@@ -376,15 +516,14 @@ def batch_queries(args, ctx, torch, stream, rank, world):
 
 
 def config_latencies(ctx, torch, stream, reps=3):
-    """End-to-end latency of each BASELINE.json configuration on one GPU
+    """End-to-end latency of the other BASELINE.json configurations on one GPU
     (SURVEY §8d shapes, 2-degree quiver), device time on the library stream,
-    median of `reps`:
+    median of `reps` (parity: tests/test_gpu_parity_configs.py):
     C1  6-DOF reach pose (scene grid + solve + select + exact refine), 64^3;
-    C2  8-DOF reach pose + 25-waypoint path, 128^3 (the headline);
-    C3  8-DOF reach + path, then an arbitrary-pose path from its final pose
-        to a second target, 256^3, 40 boxes;
-    C4  one control tick of dynamic-obstacle avoidance on 256^3: re-voxelise
-        (overlay of the moving cube, us) and re-plan (replan_dynamic, ms)."""
+    C2  8-DOF reach pose + 25-waypoint path, 128^3, 12 boxes;
+    C4  control ticks of dynamic-obstacle avoidance on 256^3: re-voxelise
+        (overlay of the moving cube, us; GB/s against 3 N^3/8 bytes) and
+        re-plan (replan_dynamic, ms)."""
     import numpy as np
     from paper_1906_10678_b200 import abi, api, scenes
 
@@ -424,45 +563,41 @@ def config_latencies(ctx, torch, stream, reps=3):
     ms, nsol = timed(c1)
     res["C1"] = {"what": "6-DOF reach pose (grid + solve + select + refine), 64^3, 3 boxes",
                  "ms": ms, "solutions": nsol}
-    sc, arm, rp, q = setup("C3")
+    sc, arm, rp, q = setup("C2")
 
-    def c3():
+    def c2():
         g = grid(sc, arm, rp)
-        return g, api.plan_reach_then_path(ctx, arm, q, g, sc.target, rp)
-    ms, (g3, (rc, plan3)) = timed(c3)
-    res["C3"] = {"what": "8-DOF reach pose + 25-waypoint path (grid + plan_reach_then_path), "
-                         "256^3, 40 boxes", "ms": ms, "rc": rc}
-    if rc == 0:
-        p, w = plan3.summary()["poses"][-1]
-        ms2, (rc2, _) = timed(lambda: api.plan_arbitrary(ctx, arm, q, g3, p, scenes.SECOND_TARGET,
-                                                         rp, start_waypoints=w))
-        res["C3"]["arbitrary"] = {"what": "then plan_arbitrary from its final pose to "
-                                          f"{scenes.SECOND_TARGET} (rc 7 = no-path, as the "
-                                          "reference decides)", "ms": ms2, "rc": rc2}
+        return api.plan_reach_then_path(ctx, arm, q, g, sc.target, rp)
+    ms, (rc, plan2) = timed(c2)
+    res["C2"] = {"what": "8-DOF reach pose + 25-waypoint path (grid + plan_reach_then_path), "
+                         "128^3, 12 boxes", "ms": ms, "rc": rc,
+                 "result_digest": plan_digest([plan2.summary()]) if rc == 0 else None}
     sc, arm, rp, q = setup("C4")
     g = grid(sc, arm, rp)
     rc, plan = api.plan_reach_then_path(ctx, arm, q, g, sc.target, rp)
     if rc == 0:
         s = plan.summary()
-        # a 2 cm cube on waypoint 13's tracked point while the arm is at waypoint 5
-        # (the reference decides no-path here at 2 degrees after its anchor and
-        # virtual solves; at 5 degrees tests/test_gpu_planner.py covers successes)
-        at, idx, half = 5, 13, 0.02
+        # a 2 cm cube on waypoint 13's tracked point while the arm is at
+        # waypoint 5, moving 2 mm per tick (tests/golden/configs/C4_2.json
+        # pins the overlay bytes and the reference's decision per tick)
+        at, idx, half, dx = 5, 13, 0.02, 0.002
         c = np.asarray(s["poses"][min(len(s["poses"]) - 1, idx)][0].joints[3][:])
         ticks = {"overlay_us": [], "replan_ms": [], "rc": []}
         aug = None
         for t in range(reps + 1):
-            ctr = c + np.array([0.002 * t, 0.0, 0.0])  # the cube moves 2 mm per tick
+            ctr = c + np.array([dx * t, 0.0, 0.0])
             obs = abi.box(tuple(ctr - half), tuple(ctr + half), dynamic=True)
             ms_o, aug = timed(lambda: g.overlay(obs, into=aug))
             ms_r, (rc2, _) = timed(lambda: api.replan_dynamic(ctx, arm, q, g, plan, at, obs, rp))
-            if t:
-                ticks["overlay_us"].append(1e3 * ms_o)
-                ticks["replan_ms"].append(ms_r)
-                ticks["rc"].append(rc2)
+            ticks["overlay_us"].append(1e3 * ms_o)
+            ticks["replan_ms"].append(ms_r)
+            ticks["rc"].append(rc2)
+        ov = statistics.median(ticks["overlay_us"])
+        nbytes = 3 * sc.n ** 3 / 8
         res["C4"] = {"what": "per control tick on 256^3: re-voxelise the moving cube (overlay) "
-                             "+ replan_dynamic (rc 7 = no-path decision)",
-                     "overlay_us": statistics.median(ticks["overlay_us"]),
+                             "+ replan_dynamic (rc 7 = no-path, rc 8 = infeasible-timing, as "
+                             "the reference decides)",
+                     "overlay_us": ov, "overlay_gbs_vs_3N3_8": nbytes / (ov * 1e-6) / 1e9,
                      "replan_ms": statistics.median(ticks["replan_ms"]), "rc": ticks["rc"]}
     else:
         res["C4"] = {"what": "no first plan on this scene", "rc": rc}
@@ -532,6 +667,7 @@ def voxel_update(ctx, torch, stream):
 
 def main():
     args = parse()
+    maybe_spawn(args)
     from paper_1906_10678_b200 import scenes
     sc = scenes.config(args.config, quiver_deg=args.quiver_deg)
     if args.impl == "reference":

@@ -40,6 +40,11 @@ def lib():
                                          P(abi.Obstacle), C.c_int, P(abi.Arm),
                                          P(abi.ReachParams), C.c_double, C.c_double, C.c_int,
                                          P(vp)]
+        L.ref_problem_create_u8.argtypes = [P(C.c_double), C.c_double, P(C.c_int32), vp,
+                                            C.c_double, P(abi.Arm), P(abi.ReachParams),
+                                            C.c_double, C.c_double, C.c_int, P(vp)]
+        L.ref_bench_stages.argtypes = [vp, P(C.c_double), P(abi.PathParams), C.c_int,
+                                       P(C.c_double), P(C.c_int64), P(vp)]
         L.ref_problem_destroy.argtypes = [vp]
         L.ref_problem_set_params.argtypes = [vp, P(abi.ReachParams)]
         L.ref_problem_grid.argtypes = [vp, vp, C.c_uint64, P(C.c_int32), P(C.c_double)]
@@ -175,18 +180,28 @@ class RefPlan:
 class RefProblem:
     """A scene + arm + quiver + params on the reference (build_scene_grid)."""
 
-    def __init__(self, scene, dilation=-1.0, workers=1):
+    def __init__(self, scene, dilation=-1.0, workers=1, grid_u8=None):
+        """grid_u8 = (origin, dims, occupancy bytes, dilation_radius): use this
+        occupancy instead of build_scene_grid (ref_problem_create_u8)."""
         self.scene = scene
         self.arm = scene.arm()
         self.rp = scene.reach_params(workers)
-        obs = scene.obstacles()
-        arr = abi.obstacle_array(obs)
         h = C.c_void_p()
         step = scene.quiver_step()
-        _check(lib().ref_problem_create(_d3(abi_bounds(scene)[0]), _d3(abi_bounds(scene)[1]),
-                                        scene.voxel_size, dilation, arr, len(obs),
-                                        C.byref(self.arm), C.byref(self.rp), step, step,
-                                        scene.min_per_ring, C.byref(h)))
+        if grid_u8 is not None:
+            origin, dims, occ, dil = grid_u8
+            occ = np.ascontiguousarray(occ, np.uint8)
+            _check(lib().ref_problem_create_u8(_d3(origin), scene.voxel_size,
+                                               (C.c_int32 * 3)(*dims), occ.ctypes.data, dil,
+                                               C.byref(self.arm), C.byref(self.rp), step, step,
+                                               scene.min_per_ring, C.byref(h)))
+        else:
+            obs = scene.obstacles()
+            arr = abi.obstacle_array(obs)
+            _check(lib().ref_problem_create(_d3(abi_bounds(scene)[0]), _d3(abi_bounds(scene)[1]),
+                                            scene.voxel_size, dilation, arr, len(obs),
+                                            C.byref(self.arm), C.byref(self.rp), step, step,
+                                            scene.min_per_ring, C.byref(h)))
         self.h = h
 
     def __del__(self):
@@ -292,6 +307,19 @@ class RefProblem:
         if rc != 0:
             return rc, None
         return 0, RefPlan(h)
+
+    def bench_stages(self, target=None, pp=None, workers=0):
+        """cmd_bench's columns (src/cli.cpp:272-308): (rc, plan, {seg1_ms,
+        solve_ms, path_ms (select + plan_from_reach), path_only_ms}, n_solutions)."""
+        target = self.scene.target if target is None else target
+        pp = pp or abi.make_path_params()
+        ms = (C.c_double * 4)()
+        ns = C.c_int64()
+        h = C.c_void_p()
+        rc = lib().ref_bench_stages(self.h, _d3(target), C.byref(pp), workers, ms, C.byref(ns),
+                                    C.byref(h))
+        stages = {"seg1_ms": ms[0], "solve_ms": ms[1], "path_ms": ms[2], "path_only_ms": ms[3]}
+        return rc, (RefPlan(h) if rc == 0 else None), stages, ns.value
 
     def plan_arbitrary(self, start_pose, start_wps, target, pp=None):
         pp = pp or abi.make_path_params()

@@ -170,6 +170,32 @@ int ref_problem_create(const double* bmin, const double* bmax, double voxel_size
   }
 }
 
+/// A problem over a caller-supplied occupancy (x fastest, the VoxelGrid
+/// layout of inc/reachplan/voxgrid.hpp:28-55) instead of build_scene_grid:
+/// lets the 512^3 batched-query parity skip the reference's minutes-long
+/// dilation once the grid itself is pinned.
+int ref_problem_create_u8(const double* origin, double voxel_size, const int32_t* dims,
+                          const uint8_t* occ, double dilation_radius, const rp_arm* arm,
+                          const rp_reach_params* rp, double elev_step, double azim_step,
+                          int min_per_ring, ref_problem** out) {
+  try {
+    auto p = std::make_unique<ref_problem>();
+    p->arm = to_arm(*arm);
+    p->rp = to_rp(*rp);
+    p->quiver = generate_quiver(elev_step, azim_step, min_per_ring);
+    p->grid.origin = v3(origin);
+    p->grid.voxel_size = voxel_size;
+    for (int a = 0; a < 3; ++a) p->grid.dims[a] = dims[a];
+    const std::size_t n = static_cast<std::size_t>(dims[0]) * dims[1] * dims[2];
+    p->grid.occupancy.assign(occ, occ + n);
+    p->grid.dilation_radius = dilation_radius;
+    *out = p.release();
+    return 0;
+  } catch (const Error& e) {
+    return status_of(e);
+  }
+}
+
 void ref_problem_destroy(ref_problem* p) { delete p; }
 
 void ref_problem_set_params(ref_problem* p, const rp_reach_params* rp) { p->rp = to_rp(*rp); }
@@ -418,6 +444,44 @@ int ref_plan_reach_then_path(ref_problem* p, const double* target, const rp_path
     return plan_result(plan_reach_then_path(p->arm, p->quiver, p->grid, v3(target), p->rp,
                                             to_pp(*pp)),
                        out);
+  } catch (const Error& e) {
+    return status_of(e);
+  }
+}
+
+/// The reference's own stage timer, cmd_bench (src/cli.cpp:272-308), on this
+/// problem: ms[0] = prune_segment1 alone, ms[1] = solve_reach, ms[2] =
+/// select_solution + plan_from_reach (cmd_bench's path-ms excludes the
+/// select; ms[3] is that exclusive figure). The plan is returned (or the
+/// planner's status) so the caller can chain plan_arbitrary from it.
+int ref_bench_stages(ref_problem* p, const double* target, const rp_path_params* pp,
+                     int workers, double* ms, int64_t* n_solutions, ref_plan** out) {
+  using clk = std::chrono::steady_clock;
+  auto dms = [](clk::time_point a, clk::time_point b) {
+    return std::chrono::duration<double, std::milli>(b - a).count();
+  };
+  try {
+    ReachParams rp = p->rp;
+    if (workers > 0) rp.workers = workers;
+    const Vec3 t = v3(target);
+    const auto t0 = clk::now();
+    SolveStats s1;
+    const auto seg1 = prune_segment1(p->arm, p->quiver, p->grid, {t}, rp, nullptr, &s1, nullptr);
+    const auto t1 = clk::now();
+    SolutionSet set = solve_reach(p->arm, p->quiver, p->grid, t, rp);
+    const auto t2 = clk::now();
+    ms[0] = dms(t0, t1);
+    ms[1] = dms(t1, t2);
+    ms[2] = ms[3] = 0.0;
+    *n_solutions = static_cast<int64_t>(set.solutions.size());
+    (void)seg1;
+    const ChosenPath chosen = select_solution(set);
+    const auto t3 = clk::now();
+    PathPlan plan = plan_from_reach(p->arm, p->quiver, p->grid, chosen, set, t, rp, to_pp(*pp));
+    const auto t4 = clk::now();
+    ms[2] = dms(t2, t4);
+    ms[3] = dms(t3, t4);
+    return plan_result(std::move(plan), out);
   } catch (const Error& e) {
     return status_of(e);
   }

@@ -108,11 +108,40 @@ void copy_to_host(rp_ctx* ctx, void* dst, const void* src, size_t bytes) {
   RP_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
+namespace {
+constexpr int kUploadSlots = 64;
+constexpr size_t kUploadSlotBytes = 64 << 10;
+}  // namespace
+
+/// Host -> device copy in stream order without synchronising the stream:
+/// the source (often a temporary) is staged into the next slot of the
+/// context's pinned ring and the DMA reads it from there. A pageable
+/// cudaMemcpyAsync would synchronise the stream before it starts; only
+/// uploads larger than a slot (a quiver or a uint8 grid, once) still do.
 void copy_to_device(rp_ctx* ctx, void* dst, const void* src, size_t bytes) {
   if (!bytes) return;
-  RP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
-  // The source may be a temporary host buffer: make the copy complete.
-  RP_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (bytes > kUploadSlotBytes) {
+    ++ctx->upload_syncs;
+    RP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    // The source may be a temporary host buffer: make the copy complete.
+    RP_CUDA(cudaStreamSynchronize(ctx->stream));
+    return;
+  }
+  if (!ctx->upload_ring) {
+    RP_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ctx->upload_ring),
+                           kUploadSlots * kUploadSlotBytes));
+    ctx->upload_ev.assign(kUploadSlots, nullptr);
+    for (auto& e : ctx->upload_ev) RP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : ctx->upload_ev) RP_CUDA(cudaEventRecord(e, ctx->stream));
+  }
+  const int k = ctx->upload_next;
+  ctx->upload_next = (k + 1) % kUploadSlots;
+  // the slot's previous copy has long finished in practice (63 copies ago)
+  RP_CUDA(cudaEventSynchronize(ctx->upload_ev[k]));
+  char* slot = ctx->upload_ring + static_cast<size_t>(k) * kUploadSlotBytes;
+  std::memcpy(slot, src, bytes);
+  RP_CUDA(cudaMemcpyAsync(dst, slot, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  RP_CUDA(cudaEventRecord(ctx->upload_ev[k], ctx->stream));
 }
 
 double nominal_spacing(const rp_arm& a, const rp_reach_params& r) {
@@ -336,6 +365,8 @@ rp_status rp_ctx_destroy(rp_ctx* ctx) {
     }
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    for (cudaEvent_t e : ctx->upload_ev) cudaEventDestroy(e);
+    if (ctx->upload_ring) cudaFreeHost(ctx->upload_ring);
     if (ctx->cancel_flag) cudaFree(ctx->cancel_flag);
     if (ctx->aux) cudaStreamDestroy(ctx->aux);
     if (ctx->own) cudaStreamDestroy(ctx->own);

@@ -503,6 +503,24 @@ inline size_t rows_smem(int np, int reach) {
          static_cast<size_t>(2 * reach * reach + 1) * sizeof(int);
 }
 
+/// Largest static shared memory of the row rasterisers (k_mark_dilate_tiles<8>:
+/// 2 x 256 x 8 words) and the per-block opt-in limit of sm_100.
+constexpr size_t kRowsStaticSmemMax = 33 * 1024;
+constexpr size_t kSmemOptin = 227 * 1024;
+/// Whether a fused rasterise(+dilate) launch of np primitives at this reach
+/// fits one block's shared memory (otherwise: mark, then dilate_general).
+inline bool rows_fit(int64_t np, int reach) {
+  return rows_smem(static_cast<int>(np), reach) + kRowsStaticSmemMax <= kSmemOptin;
+}
+/// Opt the kernel in to more than the default 48 KB of dynamic shared
+/// memory (per device: called before each such launch).
+template <typename K>
+inline void allow_smem(K kern, size_t smem) {
+  if (smem > 48 * 1024)
+    RP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+}
+
 /// Box / cloud -> index boxes on the host with the reference's arithmetic
 /// (world_to_index floor of the IEEE quotient, cell-centre test); returns
 /// false when there are more primitives than the parameter block holds.
@@ -589,7 +607,8 @@ bool encode_run_map(CUtensorMap* map, uint64_t* base, uint64_t nrows, int box_ro
 /// Rasterise host-computed index boxes (one async upload, no box kernel).
 bool launch_rows_param(rp_ctx* ctx, const char* name, rp_grid* g, const std::vector<Prim>& prims,
                        const DilTable& t, int y0, int y1, int z0, int z1, bool accumulate) {
-  if (prims.empty() || prims.size() > kHostPrimLimit) return false;
+  if (prims.empty() || prims.size() > kHostPrimLimit || !rows_fit(prims.size(), t.reach))
+    return false;
   DevBuf<Prim> dp(prims.size(), ctx->stream);
   copy_to_device(ctx, dp.p, prims.data(), prims.size() * sizeof(Prim));
   DevBuf<int> wtab(t.w.size(), ctx->stream);
@@ -613,6 +632,7 @@ void launch_rows(rp_ctx* ctx, const char* name, rp_grid* g, const Prim* prims, i
   constexpr int TYv = 32, NTv = 256;
   constexpr int RPTv = 1;  // 2 rows per thread (half the blocks) measured 6.1 vs 5.4 us at 512^3
   auto rowwise = [&](auto kern) {
+    allow_smem(kern, smem);
     const int PLv = NTv / TYv * RPTv;
     const dim3 grid(static_cast<unsigned>((y1 - y0 + TYv) / TYv),
                     static_cast<unsigned>((z1 - z0 + PLv) / PLv));
@@ -649,6 +669,7 @@ void launch_rows(rp_ctx* ctx, const char* name, rp_grid* g, const Prim* prims, i
                           encode_run_map(&tmap, g->bits + static_cast<size_t>(z0) * g->dims[1] * 8,
                                          static_cast<uint64_t>(nrun), PR);
     auto plane = [&](auto kern) {
+      allow_smem(kern, smem);
       if (pdl)
         launch_pdl(ctx, name, kern, grid, dim3(PR), smem, g->bits, g->view(), prims, np, wtab,
                    reach, z0, z1, bulk, tmap);
@@ -671,6 +692,7 @@ void launch_rows(rp_ctx* ctx, const char* name, rp_grid* g, const Prim* prims, i
   if (tiles_ok && force != "rowwise" && (force == "tiles" || tiles_small)) {
     const dim3 grid(static_cast<unsigned>(ntiles));
     auto tiles = [&](auto kern) {
+      allow_smem(kern, smem);
       if (pdl)
         launch_pdl(ctx, name, kern, grid, dim3(256), smem, g->bits, g->view(), prims, np, wtab,
                    reach);
@@ -698,17 +720,19 @@ void launch_rows(rp_ctx* ctx, const char* name, rp_grid* g, const Prim* prims, i
   const dim3 grid(static_cast<unsigned>((g->wx + tw - 1) / tw),
                   static_cast<unsigned>((y1 - y0 + ty) / ty),
                   static_cast<unsigned>((z1 - z0 + tz) / tz));
+  allow_smem(k_mark_dilate_rows, smem);
   launch(ctx, name, k_mark_dilate_rows, grid, dim3(tw * ty), smem, g->bits, g->view(), prims, np,
          wtab, reach, y0, y1, z0, z1, tw, ty, tz, acc);
 }
 
-/// Scatter-mark single cells (cloud points) with atomicOr.
+/// Scatter-mark single cells (cloud points) with atomicOr. Only for
+/// one-cell primitives (a == b); boxes go through the row rasteriser.
 __global__ void k_mark_cells(uint64_t* bits, GridView g, const Prim* __restrict__ prims,
                              int64_t n) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const Prim p = prims[k];
-  if (p.a[0] > p.b[0]) return;
+  if (p.a[0] > p.b[0] || p.a[1] > p.b[1] || p.a[2] > p.b[2]) return;
   const size_t idx = (static_cast<size_t>(p.a[2]) * g.ny + p.a[1]) * g.wx + (p.a[0] >> 6);
   atomicOr(reinterpret_cast<unsigned long long*>(bits + idx), 1ull << (p.a[0] & 63));
 }
@@ -873,8 +897,9 @@ inline unsigned blocks_for(int64_t n, int threads) {
 constexpr int kFusedPrimLimit = 512;
 
 /// Build the index-box list of the obstacles on the device.
+/// Boxes come first ([0, *nb_out)), then the cloud cells.
 DevBuf<Prim> obstacles_to_prims(rp_grid* g, const rp_obstacle* obs, int n, int64_t* n_out,
-                                bool* only_boxes) {
+                                bool* only_boxes, int64_t* nb_out = nullptr) {
   rp_ctx* ctx = g->ctx;
   std::vector<double> boxes;
   std::vector<double> cloud;
@@ -908,6 +933,7 @@ DevBuf<Prim> obstacles_to_prims(rp_grid* g, const rp_obstacle* obs, int n, int64
            prims.p + nb);
   }
   *n_out = nb + nc;
+  if (nb_out) *nb_out = nb;
   return prims;
 }
 
@@ -922,6 +948,24 @@ void run_rows(rp_grid* g, const Prim* prims, int np, const DilTable& t, int y0, 
   DevBuf<int> wtab(t.w.size(), ctx->stream);
   copy_to_device(ctx, wtab.p, t.w.data(), t.w.size() * sizeof(int));
   launch_rows(ctx, name, g, prims, np, wtab.p, t.reach, y0, y1, z0, z1, accumulate);
+}
+
+/// mark_obstacles of device primitives: boxes [0, nb) drawn by the row
+/// rasteriser in chunks of kFusedPrimLimit, cloud cells [nb, np) scattered
+/// (src/voxgrid.cpp:35-62: marking only sets cells).
+void mark_prims(rp_grid* g, const Prim* prims, int64_t nb, int64_t np, const char* name) {
+  DilTable t0;
+  t0.reach = 0;
+  t0.w = {0};
+  for (int64_t k = 0; k < nb; k += kFusedPrimLimit) {
+    const int c = static_cast<int>(std::min<int64_t>(kFusedPrimLimit, nb - k));
+    run_rows(g, prims + k, c, t0, 0, g->dims[1] - 1, 0, g->dims[2] - 1, !(g->empty && k == 0),
+             name);
+  }
+  if (np > nb)
+    launch(g->ctx, name, k_mark_cells, dim3(blocks_for(np - nb, 256)), dim3(256), 0, g->bits,
+           g->view(), prims + nb, np - nb);
+  if (np > 0) g->empty = false;
 }
 
 void dilate_general(rp_grid* g, double radius) {
@@ -979,27 +1023,19 @@ void grid_mark_dilate_boxes(rp_grid* g, const rp_obstacle* obs, int n, double ra
       return;
     }
   }
-  int64_t np = 0;
+  int64_t np = 0, nb = 0;
   bool only_boxes = true;
-  DevBuf<Prim> prims = obstacles_to_prims(g, obs, n, &np, &only_boxes);
-  const bool fused_ok = (!or_into_existing || g->empty) && np <= kFusedPrimLimit;
+  DevBuf<Prim> prims = obstacles_to_prims(g, obs, n, &np, &only_boxes, &nb);
+  const DilTable t = make_table(radius, g->voxel_size);
+  const bool fused_ok =
+      (!or_into_existing || g->empty) && np <= kFusedPrimLimit && rows_fit(np, t.reach);
   if (np > 0 && fused_ok) {
-    const DilTable t = make_table(radius, g->voxel_size);
     run_rows(g, prims.p, static_cast<int>(np), t, 0, g->dims[1] - 1, 0, g->dims[2] - 1,
              or_into_existing && !g->empty, "mark_dilate");
   } else if (np > 0) {
-    // many primitives or pre-existing occupancy: mark, then general dilation
-    DilTable t0;
-    t0.reach = 0;
-    t0.w = {0};
-    if (only_boxes || np <= kFusedPrimLimit) {
-      run_rows(g, prims.p, static_cast<int>(np), t0, 0, g->dims[1] - 1, 0, g->dims[2] - 1, true,
-               "voxelize");
-    } else {
-      launch(g->ctx, "voxelize", k_mark_cells, dim3(blocks_for(np, 256)), dim3(256), 0, g->bits,
-             g->view(), static_cast<const Prim*>(prims.p), np);
-    }
-    g->empty = false;
+    // many primitives, a large reach or pre-existing occupancy: mark, then
+    // the general dilation of the whole occupancy
+    mark_prims(g, prims.p, nb, np, "voxelize");
     if (radius != 0.0) dilate_general(g, radius);
   }
   if (np > 0) g->empty = false;
@@ -1049,21 +1085,11 @@ rp_status rp_grid_mark(rp_grid* g, const rp_obstacle* obs, int32_t n) {
         }
       }
     }
-    int64_t np = 0;
+    int64_t np = 0, nb = 0;
     bool only_boxes = true;
-    DevBuf<Prim> prims = obstacles_to_prims(g, obs, n, &np, &only_boxes);
+    DevBuf<Prim> prims = obstacles_to_prims(g, obs, n, &np, &only_boxes, &nb);
     if (np == 0) return;
-    if (np <= kFusedPrimLimit) {
-      DilTable t0;
-      t0.reach = 0;
-      t0.w = {0};
-      run_rows(g, prims.p, static_cast<int>(np), t0, 0, g->dims[1] - 1, 0, g->dims[2] - 1,
-               !g->empty, "voxelize");
-    } else {
-      launch(g->ctx, "voxelize", k_mark_cells, dim3(blocks_for(np, 256)), dim3(256), 0, g->bits,
-             g->view(), static_cast<const Prim*>(prims.p), np);
-    }
-    g->empty = false;
+    mark_prims(g, prims.p, nb, np, "voxelize");
   });
 }
 
@@ -1084,22 +1110,26 @@ rp_status rp_grid_mark_dilate_slab(rp_grid* g, const rp_obstacle* obs, int32_t n
                                    int32_t z0, int32_t z1) {
   return guarded([&] {
     require(radius >= 0.0, RP_E_INVALID_PARAMETER, "dilation radius must be >= 0");
-    require(0 <= z0 && z0 <= z1 && z1 < g->dims[2], RP_E_INVALID_PARAMETER, "slab out of range");
+    // z1 = z0 - 1 is an empty slab (a rank that owns no planes): no launch,
+    // but the grid records the radius like every other rank's
+    require(0 <= z0 && z0 <= z1 + 1 && z1 < g->dims[2], RP_E_INVALID_PARAMETER,
+            "slab out of range");
     check_boxes(obs, n);
     std::vector<Prim> hp;
     const DilTable t = make_table(radius, g->voxel_size);
-    require(host_prims(g, obs, n, &hp), RP_E_INVALID_PARAMETER,
+    require(host_prims(g, obs, n, &hp) && rows_fit(static_cast<int64_t>(hp.size()), t.reach),
+            RP_E_INVALID_PARAMETER,
             "slab builds take box obstacles (and small clouds) only");
     // every plane is a function of the analytic boxes alone, so a slab needs
     // no halo from its neighbours: exactly the full build's planes z0..z1
-    if (!hp.empty() &&
+    if (!hp.empty() && z0 <= z1 &&
         !launch_rows_param(g->ctx, "mark_dilate", g, hp, t, 0, g->dims[1] - 1, z0, z1, false)) {
       DevBuf<Prim> dp(hp.size(), g->ctx->stream);
       copy_to_device(g->ctx, dp.p, hp.data(), hp.size() * sizeof(Prim));
       run_rows(g, dp.p, static_cast<int>(hp.size()), t, 0, g->dims[1] - 1, z0, z1, false,
                "mark_dilate");
     }
-    g->empty = false;
+    if (!hp.empty()) g->empty = false;
     g->dilation_radius = radius;
   });
 }
@@ -1299,12 +1329,12 @@ rp_status rp_grid_overlay(const rp_grid* base, const rp_obstacle* obs, rp_grid**
         }
       }
     }
-    int64_t np = 0;
+    int64_t np = 0, nb = 0;
     bool only_boxes = true;
-    DevBuf<Prim> prims = obstacles_to_prims(g, obs, 1, &np, &only_boxes);
+    DevBuf<Prim> prims = obstacles_to_prims(g, obs, 1, &np, &only_boxes, &nb);
     if (np > 0) {
       const DilTable t = make_table(base->dilation_radius, base->voxel_size);
-      if (np <= kFusedPrimLimit) {
+      if (np <= kFusedPrimLimit && rows_fit(np, t.reach)) {
         // bbox-limited: only rows within reach of the obstacle are touched
         std::vector<Prim> hp(np);
         copy_to_host(ctx, hp.data(), prims.p, np * sizeof(Prim));
@@ -1322,9 +1352,7 @@ rp_status rp_grid_overlay(const rp_grid* base, const rp_obstacle* obs, rp_grid**
       } else {
         rp_grid* ov = grid_alloc_like(base);
         ov->dilation_radius = 0.0;
-        launch(ctx, "voxelize", k_mark_cells, dim3(blocks_for(np, 256)), dim3(256), 0, ov->bits,
-               ov->view(), static_cast<const Prim*>(prims.p), np);
-        ov->empty = false;
+        mark_prims(ov, prims.p, nb, np, "voxelize");
         if (base->dilation_radius != 0.0) dilate_general(ov, base->dilation_radius);
         launch(ctx, "overlay", k_or_into, dim3(blocks_for(static_cast<int64_t>(g->n_words), 256)),
                dim3(256), 0, g->bits, static_cast<const uint64_t*>(ov->bits), g->n_words);

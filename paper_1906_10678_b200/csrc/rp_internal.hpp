@@ -80,6 +80,13 @@ struct rp_ctx {
   // use on the parent.
   int* cancel_flag = nullptr;
   cudaStream_t aux = nullptr;
+  // Pinned upload ring (copy_to_device): kUploadSlots slots of
+  // kUploadSlotBytes; a slot is reused only after the event recorded behind
+  // its last copy completed, so uploads never synchronise the stream.
+  char* upload_ring = nullptr;
+  std::vector<cudaEvent_t> upload_ev;
+  int upload_next = 0;
+  int64_t upload_syncs = 0;  // uploads that still had to synchronise (too large)
 };
 
 namespace rp {

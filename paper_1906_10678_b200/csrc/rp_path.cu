@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 
 namespace rp {
@@ -1946,18 +1947,20 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
   cudaStream_t st = ctx->stream;
   const size_t smem = 2 * static_cast<size_t>(q->n) * sizeof(int);
   if (bp_blocks == 0) {
-    // kernel attribute + occupancy: once per process and shared-memory size
-    static std::mutex attr_mutex;  // planners may run on several threads
-    static size_t configured_smem = 0;
-    static int per_sm = 0;
+    // kernel attribute + occupancy: once per device and shared-memory size
+    // (the attribute is per device; planners may run on several threads)
+    static std::mutex attr_mutex;
+    static std::map<int, std::pair<size_t, int>> configured;  // device -> (smem, per_sm)
     std::lock_guard<std::mutex> lock(attr_mutex);
-    if (configured_smem < smem) {
+    auto& cfg = configured[ctx->device];
+    if (cfg.first < smem) {
       RP_CUDA(cudaFuncSetAttribute(k_backward_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
-      RP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_backward_pass, kBpThreads,
-                                                            smem));
-      configured_smem = smem;
+      RP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cfg.second, k_backward_pass,
+                                                            kBpThreads, smem));
+      cfg.first = smem;
     }
+    const int per_sm = cfg.second;
     if (per_sm < 1) {
       use_device_pass = false;
       return false;

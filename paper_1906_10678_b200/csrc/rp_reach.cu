@@ -2376,10 +2376,18 @@ extern "C" rp_status rp_solve_reach_batch(rp_ctx* ctx, const rp_arm* arm, const 
     const char* tail_env = std::getenv("RP_TAIL_POOL_MB");  // read per call (tests vary it)
     const long tail_mb = tail_env ? std::atol(tail_env) : 1024;
     const bool keys_fit = static_cast<double>(q->n) * q->n < 4294967296.0;
-    const int tail_cap = keys_fit ? static_cast<int>(std::max(0L, tail_mb) * (1L << 20) /
-                                                     (kTailBlock * static_cast<long>(sizeof(uint32_t))))
-                                  : 0;
-    DevBuf<uint32_t> d_tpool(static_cast<size_t>(std::max(1, tail_cap)) * kTailBlock, st);
+    int tail_cap = keys_fit ? static_cast<int>(std::max(0L, tail_mb) * (1L << 20) /
+                                               (kTailBlock * static_cast<long>(sizeof(uint32_t))))
+                            : 0;
+    DevBuf<uint32_t> d_tpool;
+    try {
+      d_tpool.alloc(static_cast<size_t>(std::max(1, tail_cap)) * kTailBlock, st);
+    } catch (const Fail&) {
+      // short on device memory: evaluate every pair in place (tail_cap = 0)
+      cudaGetLastError();
+      tail_cap = 0;
+      d_tpool.alloc(kTailBlock, st);
+    }
     DevBuf<int> d_ttgt(std::max(1, tail_cap), st), d_tlen(std::max(1, tail_cap), st);
     DevBuf<BestRec> d_tbest(CH, st);
     const std::vector<BestRec> tbest_init(CH, BestRec{1e308, LLONG_MAX});

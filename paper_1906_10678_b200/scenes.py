@@ -20,6 +20,11 @@ BOUNDS_MIN = (-1.6, -1.6, -1.6)
 BOUNDS_MAX = (1.6, 1.6, 1.6)
 TARGET = (1.0, 0.35, 0.3)
 SECOND_TARGET = (-0.6, 0.9, 0.5)
+# C3's plan_arbitrary target: the first (seed offset 0) of the second targets
+# scripts/scan_scenes.py found for which the reference delivers a path at 2
+# degrees ("choose seeds where the oracle succeeds"); the
+# reference's verdict on it is pinned in tests/golden/configs/C3_2.json.
+C3_SECOND_TARGET = (0.48836139696567815, 0.18893114584450932, 0.7008486055538292)
 L8 = (0.5, 0.5, 0.5, 0.125)
 L6 = (0.5, 0.5, 0.5)
 ARM_RADIUS = 0.02
@@ -74,7 +79,8 @@ def random_boxes(count: int, seed: int, targets=(TARGET,), root=(0.0, 0.0, 0.0),
     return boxes
 
 
-def config(name: str, quiver_deg: float = 2.0, seed_offset: int = 0) -> Scene:
+def config(name: str, quiver_deg: float = 2.0, seed_offset: int = 0,
+           second_target=None) -> Scene:
     """C1..C5 of BASELINE.json (SURVEY.md §8 shorthand)."""
     if name == "C1":  # 6DOF stand-in for the inexpressible 4-DOF arm (SURVEY §0.1.3)
         return Scene("C1", 64, random_boxes(3, 1234 + 1 + seed_offset), L6, abi.RP_MODE_6DOF,
@@ -83,10 +89,11 @@ def config(name: str, quiver_deg: float = 2.0, seed_offset: int = 0) -> Scene:
         return Scene("C2", 128, random_boxes(12, 1234 + 2 + seed_offset), L8, abi.RP_MODE_8DOF,
                      quiver_deg=quiver_deg)
     if name == "C3":
+        t2 = tuple(second_target) if second_target is not None else C3_SECOND_TARGET
         return Scene("C3", 256,
-                     random_boxes(40, 1234 + 3 + seed_offset, targets=(TARGET, SECOND_TARGET)),
+                     random_boxes(40, 1234 + 3 + seed_offset, targets=(TARGET, t2)),
                      L8, abi.RP_MODE_8DOF, quiver_deg=quiver_deg,
-                     extra={"second_target": SECOND_TARGET})
+                     extra={"second_target": t2})
     if name == "C4":
         return Scene("C4", 256, random_boxes(40, 1234 + 4 + seed_offset), L8, abi.RP_MODE_8DOF,
                      quiver_deg=quiver_deg)

@@ -132,8 +132,8 @@ def build_grid_sharded(ctx, bmin, bmax, voxel_size, obstacles, radius, rank: int
     g = api.Grid.build(ctx, bmin, bmax, voxel_size)
     nz = g.info()[0][2]
     lo, hi = shard_range(nz, rank, world)
-    if hi > lo:
-        g.mark_dilate_slab(obstacles, radius, lo, hi - 1)
+    # an empty range (hi == lo) still records the radius on this rank
+    g.mark_dilate_slab(obstacles, radius, lo, hi - 1)
     if world > 1:
         words, wpp = g.device_words()
         ctx.synchronize()

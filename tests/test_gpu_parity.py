@@ -94,6 +94,63 @@ def test_mark_and_cloud(ctx):
         assert np.array_equal(g2.to_u8(), occ), radius
 
 
+def _cloud(pts):
+    cloud = abi.Obstacle()
+    cloud.shape = abi.RP_SHAPE_CLOUD
+    buf = np.ascontiguousarray(pts, np.float64)
+    cloud.points = buf.ctypes.data_as(C.POINTER(C.c_double))
+    cloud.n_points = len(buf)
+    return cloud, buf
+
+
+@pytest.mark.parametrize("radius", [0.0, 0.07])
+def test_boxes_plus_large_cloud(ctx, radius):
+    """Boxes next to a cloud of more than 512 points (the mark-then-dilate
+    path): every box is filled whole, not as its corner cell, and boxes
+    clipped empty on y or z do not scatter out of range."""
+    api = _api()
+    rng = np.random.default_rng(21)
+    cloud, buf = _cloud(rng.uniform(-1.1, 1.25, (600, 3)))
+    bmin, bmax, vs = (-1, -1, -1), (1.2, 1.1, 1.05), 0.029
+    obs = [abi.box((-0.5, -0.4, -0.45), (0.1, 0.2, 0.3)), cloud,
+           abi.box((0.7, 0.65, 0.6), (1.0, 0.9, 0.8)),
+           abi.box((0.0, 1.5, 0.0), (0.3, 1.9, 0.2)),     # in range in x, empty in y
+           abi.box((0.1, 0.1, -2.5), (0.4, 0.3, -1.8))]   # in range in x, empty in z
+    dims, occ = ref.grid_ops(bmin, bmax, vs, obs, radius)
+    g = api.Grid.build(ctx, bmin, bmax, vs)
+    g.mark(obs)
+    g.dilate(radius)
+    assert np.array_equal(g.to_u8(), occ)
+    g2 = api.Grid.build(ctx, bmin, bmax, vs)
+    g2.mark_dilate(obs, radius)
+    assert np.array_equal(g2.to_u8(), occ)
+
+
+def test_many_boxes_large_reach(ctx):
+    """More boxes than one fused launch takes (> 512) and a reach whose width
+    table outgrows the default 48 KB of shared memory: chunked marking, then
+    the general dilation, equal to the reference."""
+    api = _api()
+    rng = np.random.default_rng(5)
+    bmin, bmax, vs = (-0.4, -0.4, -0.4), (0.4, 0.4, 0.4), 0.01
+    obs = []
+    for _ in range(700):
+        c = rng.uniform(-0.38, 0.38, 3)
+        h = rng.uniform(0.0, 0.006, 3)
+        obs.append(abi.box(tuple(c - h), tuple(c + h)))
+    dims, occ0 = ref.grid_ops(bmin, bmax, vs, obs, 0.0)
+    g = api.Grid.build(ctx, bmin, bmax, vs)
+    g.mark(obs)
+    assert np.array_equal(g.to_u8(), occ0)
+    # reach 70 voxels: width table (2*70^2+1)*4 B = 39 KB + 2 prims * 24 B
+    r = 0.7005
+    few = obs[:2]
+    dims, occ = ref.grid_ops(bmin, bmax, vs, few, r)
+    g3 = api.Grid.build(ctx, bmin, bmax, vs)
+    g3.mark_dilate(few, r)
+    assert np.array_equal(g3.to_u8(), occ)
+
+
 def test_point_and_segment_clear(ctx):
     sc = scenes.config("C2")
     arm, rp, q, g = gpu_problem(ctx, sc)

@@ -1,0 +1,158 @@
+"""Parity on exactly the workloads bench.py times (BASELINE configs at a
+2-degree quiver), against fixtures the UNMODIFIED reference
+produced (scripts/make_golden_configs.py -> tests/golden/configs/):
+
+  C2_2  128^3 / 12 boxes: occupancy, 13 SolveStats counters, the canonical
+        solution-key list (sha256 of the (i, j, l) int32 triples), the chosen
+        solution (kind, index, path_length bits), the full plan
+  C3_2  256^3 / 40 boxes (the headline): the same, then plan_arbitrary from
+        the plan's final pose to the second target (rc and the full plan)
+  C4_2  256^3 / 40 boxes: the first plan, then per control tick the overlay
+        occupancy (sha256) and replan_dynamic's outcome (and plan)
+  C5_2  512^3 / 40 boxes: the grid (sha256 of 128 MiB of reference bytes)
+        and the first 16 of the 4096 batched targets: counters, solution and
+        shortcut counts, chosen kind, path-length bits, segment-1/2 indices,
+        refined pose bits
+
+Exactness: everything bit-exact (fp64 with the reference's operation order)
+except the unfold prefix of a plan, whose joint-space interpolation goes
+through atan2/sin/cos: compared at UNFOLD_TOL = 1e-9 m (the tests pass
+bit-exact today; the tolerance is the stated contract, far inside 1e-3 of a
+voxel). The fixtures need no reference sources, so these run on the GPU box.
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from helpers import assert_plan_matches_fixture, gpu_problem
+from paper_1906_10678_b200 import abi, scenes
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+FIX = os.path.join(HERE, "golden", "configs")
+UNFOLD_TOL = 1e-9
+
+
+def _api():
+    from paper_1906_10678_b200 import api
+    return api
+
+
+def _load(name):
+    meta = json.load(open(os.path.join(FIX, f"{name}.json")))
+    npz = os.path.join(FIX, f"{name}.npz")
+    return meta, (np.load(npz) if os.path.exists(npz) else None)
+
+
+def _sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _check_grid(g, want):
+    dims, _, _, dil = g.info()
+    assert list(dims) == want["dims"]
+    assert dil == want["dilation_radius"]
+    occ = g.to_u8()
+    assert int(occ.sum()) == want["occupied"]
+    assert _sha(occ) == want["occupancy_sha256"]
+
+
+def _check_solve(S, want):
+    st = S.stats()
+    assert st.counters() == want["counters"]
+    assert S.sizes() == (want["n_solutions"], want["n_shortcuts"])
+    assert _sha(S.keys().astype(np.int32)) == want["keys_sha256"]
+    if "chosen" in want:
+        c = S.select()
+        assert c.kind == want["chosen"]["kind"]
+        assert int(c.index) == want["chosen"]["index"]
+        assert np.float64(c.path_length).tobytes().hex() == want["chosen"]["path_length_hex"]
+
+
+def _reach_path(ctx, name):
+    api = _api()
+    meta, fx = _load(name)
+    sc = scenes.config(name.split("_")[0], quiver_deg=2.0)
+    arm, rp, q, g = gpu_problem(ctx, sc)
+    _check_grid(g, meta["grid"])
+    _check_solve(api.solve_reach(ctx, arm, q, g, sc.target, rp), meta["solve"])
+    rc, plan = api.plan_reach_then_path(ctx, arm, q, g, sc.target, rp)
+    assert rc == meta["plan_rc"]
+    s = None
+    if rc == 0:
+        s = plan.summary()
+        assert_plan_matches_fixture(s, fx, meta["plan"], "plan0_", UNFOLD_TOL)
+    return api, sc, arm, rp, q, g, meta, fx, plan, s
+
+
+def test_c2_2deg_solve_and_plan(ctx):
+    _reach_path(ctx, "C2_2")
+
+
+def test_c3_2deg_reach_path_and_arbitrary(ctx):
+    api, sc, arm, rp, q, g, meta, fx, plan, s = _reach_path(ctx, "C3_2")
+    assert list(sc.extra["second_target"]) == meta["second_target"]
+    assert s is not None
+    p, w = s["poses"][-1]
+    rc2, plan2 = api.plan_arbitrary(ctx, arm, q, g, p, sc.extra["second_target"], rp,
+                                    start_waypoints=w)
+    assert rc2 == meta["arbitrary_rc"]
+    if rc2 == 0:
+        assert_plan_matches_fixture(plan2.summary(), fx, meta["arbitrary"], "plan1_", UNFOLD_TOL)
+
+
+def test_c4_2deg_ticks(ctx):
+    api, sc, arm, rp, q, g, meta, fx, plan, s = _reach_path(ctx, "C4_2")
+    tp = meta["tick_params"]
+    c = np.asarray(s["poses"][min(len(s["poses"]) - 1, tp["idx"])][0].joints[3][:])
+    aug = None
+    for t, want in enumerate(meta["ticks"]):
+        ctr = c + np.array([tp["step"] * t, 0.0, 0.0])
+        assert list(ctr) == want["center"]
+        obs = abi.box(tuple(ctr - tp["half"]), tuple(ctr + tp["half"]), dynamic=True)
+        aug = g.overlay(obs, into=aug)
+        occ = aug.to_u8()
+        assert int(occ.sum()) == want["overlay_occupied"]
+        assert _sha(occ) == want["overlay_sha256"]
+        rc, p2 = api.replan_dynamic(ctx, arm, q, g, plan, tp["at"], obs, rp)
+        assert rc == want["replan_rc"], t
+        if rc == 0:
+            assert_plan_matches_fixture(p2.summary(), fx, want["plan"], f"tick{t}_", UNFOLD_TOL)
+
+
+def test_c5_2deg_grid_and_batch_subset(ctx):
+    api = _api()
+    meta, _ = _load("C5_2")
+    sc = scenes.config("C5", quiver_deg=2.0)
+    arm, rp, q, g = gpu_problem(ctx, sc)
+    _check_grid(g, meta["grid"])
+    from paper_1906_10678_b200 import shard
+    targets = shard.c5_targets(g, 4096)[:len(meta["targets"])]
+    for t, want in zip(targets, meta["targets"]):
+        assert list(t) == want["target"]
+    res = api.solve_reach_batch(ctx, arm, q, g, targets, rp)
+    for r, want in zip(res, meta["targets"]):
+        assert r.stats.counters() == want["counters"]
+        assert (r.n_solutions, r.n_shortcuts) == (want["n_solutions"], want["n_shortcuts"])
+        if want["n_solutions"] + want["n_shortcuts"] == 0:
+            assert r.status == abi.RP_E_NO_SOLUTION
+            continue
+        assert r.kind == want["kind"]
+        assert np.float64(r.path_length).tobytes().hex() == want["path_length_hex"]
+        if "seg12" in want:
+            assert [r.seg1, r.seg2] == want["seg12"]
+        if "refine_rc" in want:
+            assert r.status == want["refine_rc"]
+        elif "refined" in want:
+            assert r.status == 0
+            p, n = r.refined, r.refined.n_segments
+            assert list(p.quiver_indices[:n]) == want["refined"]["qidx"]
+            assert np.array([p.segments[k][:] for k in range(n)]).tobytes().hex() == \
+                want["refined"]["segments_hex"]
+            assert np.array([p.joints[k][:] for k in range(n + 1)]).tobytes().hex() == \
+                want["refined"]["joints_hex"]
+            assert np.float64(p.s4_length_dev).tobytes().hex() == want["refined"]["s4_hex"]
