@@ -277,6 +277,10 @@ rp_status rp_grid_upload_u8(rp_ctx* ctx, const double origin[3], double voxel_si
 rp_status rp_grid_occupied_count(rp_grid* g, uint64_t* count);
 /* [point_clear, src/voxgrid.cpp:94-98] batched: out[k] = 1 if clear */
 rp_status rp_grid_point_clear(rp_grid* g, const double* xyz, int64_t n, uint8_t* out);
+/* No reference counterpart (introspection of the solver's free-sample skip):
+   out[k] = the cached coarse clearance field's lower bound (m) on the
+   distance from xyz[k] to any occupied cell. */
+rp_status rp_grid_clearance(rp_grid* g, const double* xyz, int64_t n, double* out);
 /* [segment_clear, src/voxgrid.cpp:100-112] batched segments (from,to pairs) */
 rp_status rp_grid_segment_clear(rp_grid* g, const double* from_xyz, const double* to_xyz,
                                 int64_t n, int32_t n_samples, uint8_t* out);

@@ -77,6 +77,7 @@ def lib():
         "rp_grid_upload_u8": ([vp, d3, C.c_double, P(C.c_int32), vp, C.c_double, P(vp)], C.c_int32),
         "rp_grid_occupied_count": ([vp, P(C.c_uint64)], C.c_int32),
         "rp_grid_point_clear": ([vp, vp, C.c_int64, vp], C.c_int32),
+        "rp_grid_clearance": ([vp, vp, C.c_int64, vp], C.c_int32),
         "rp_grid_segment_clear": ([vp, vp, vp, C.c_int64, C.c_int32, vp], C.c_int32),
         "rp_grid_copy": ([vp, P(vp)], C.c_int32),
         "rp_grid_destroy": ([vp], C.c_int32),
@@ -153,16 +154,40 @@ def d3(v):
     return (C.c_double * 3)(*[float(x) for x in v])
 
 
+class _Owned:
+    """A library object that lives on a context: released by its own
+    destructor or, at the latest, when the context closes (the C ABI objects
+    keep a pointer to their rp_ctx)."""
+    _destroy = ""
+
+    def _own(self, ctx, h):
+        self.ctx = ctx
+        self.h = h
+        ctx._children.add(self)
+
+    def free(self):
+        if getattr(self, "h", None) and _lib is not None:
+            getattr(_lib, self._destroy)(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.free()
+
+
 class Context:
     """rp_ctx: one CUDA device + stream."""
 
     def __init__(self, device: int = 0):
+        import weakref
         h = C.c_void_p()
         _check(lib().rp_ctx_create(device, C.byref(h)))
         self.h = h
+        self._children = weakref.WeakSet()
 
     def close(self):
         if getattr(self, "h", None) and _lib is not None:
+            for child in list(self._children):
+                child.free()
             _lib.rp_ctx_destroy(self.h)
             self.h = None
 
@@ -191,11 +216,11 @@ class Context:
         return lib().rp_ctx_launch_count(self.h)
 
 
-class Quiver:
+class Quiver(_Owned):
     """rp_quiver (Quiver, inc/reachplan/quiver.hpp:16-36)."""
+    _destroy = "rp_quiver_destroy"
 
     def __init__(self, ctx: Context, elev_step=None, azim_step=None, min_per_ring=4, vectors=None):
-        self.ctx = ctx
         h = C.c_void_p()
         if vectors is not None:
             v = np.ascontiguousarray(vectors, np.float64)
@@ -203,12 +228,7 @@ class Quiver:
                                           C.byref(h)))
         else:
             _check(lib().rp_quiver_generate(ctx.h, elev_step, azim_step, min_per_ring, C.byref(h)))
-        self.h = h
-
-    def __del__(self):
-        if getattr(self, "h", None) and _lib is not None:
-            _lib.rp_quiver_destroy(self.h)
-            self.h = None
+        self._own(ctx, h)
 
     def __len__(self):
         return lib().rp_quiver_size(self.h)
@@ -228,12 +248,12 @@ class Quiver:
         return idx[:cnt.value].copy()
 
 
-class Grid:
+class Grid(_Owned):
     """rp_grid: bit-packed device occupancy (VoxelGrid, inc/reachplan/voxgrid.hpp:28-55)."""
+    _destroy = "rp_grid_destroy"
 
     def __init__(self, ctx: Context, h):
-        self.ctx = ctx
-        self.h = h
+        self._own(ctx, h)
 
     @classmethod
     def build(cls, ctx, bmin, bmax, voxel_size, budget=0):
@@ -256,11 +276,6 @@ class Grid:
         _check(lib().rp_grid_upload_u8(ctx.h, d3(origin), voxel_size, (C.c_int32 * 3)(*dims),
                                        occ.ctypes.data, dilation, C.byref(h)))
         return cls(ctx, h)
-
-    def __del__(self):
-        if getattr(self, "h", None) and _lib is not None:
-            _lib.rp_grid_destroy(self.h)
-            self.h = None
 
     def mark(self, obstacles):
         _check(lib().rp_grid_mark(self.h, abi.obstacle_array(obstacles), len(obstacles)))
@@ -333,6 +348,14 @@ class Grid:
         _check(lib().rp_grid_point_clear(self.h, pts.ctypes.data, len(pts), out.ctypes.data))
         return out
 
+    def clearance(self, pts) -> np.ndarray:
+        """Lower bound (m) on the distance from each point to any occupied
+        cell, from the grid's cached coarse clearance field."""
+        pts = np.ascontiguousarray(pts, np.float64).reshape(-1, 3)
+        out = np.zeros(len(pts))
+        _check(lib().rp_grid_clearance(self.h, pts.ctypes.data, len(pts), out.ctypes.data))
+        return out
+
     def segment_clear(self, a, b, n) -> np.ndarray:
         a = np.ascontiguousarray(a, np.float64)
         b = np.ascontiguousarray(b, np.float64)
@@ -342,19 +365,14 @@ class Grid:
         return out
 
 
-class SolutionSet:
+class SolutionSet(_Owned):
     """rp_solution_set: device-resident solve_reach result."""
+    _destroy = "rp_solution_set_destroy"
 
     def __init__(self, ctx, h, target, n_samples):
-        self.ctx = ctx
-        self.h = h
+        self._own(ctx, h)
         self.target = tuple(target)
         self.n_samples = n_samples
-
-    def __del__(self):
-        if getattr(self, "h", None) and _lib is not None:
-            _lib.rp_solution_set_destroy(self.h)
-            self.h = None
 
     def stats(self) -> abi.SolveStats:
         s = abi.SolveStats()

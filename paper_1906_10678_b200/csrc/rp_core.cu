@@ -475,7 +475,31 @@ static rp_quiver* upload_quiver(rp_ctx* ctx, const std::vector<double>& xyz) {
   }
   RP_CUDA(cudaMalloc(&q->d_soa, soa.size() * sizeof(double) + 8));
   copy_to_device(ctx, q->d_soa, soa.data(), soa.size() * sizeof(double));
+  std::vector<float4> qf(q->n);
+  for (int k = 0; k < q->n; ++k)
+    qf[k] = make_float4(static_cast<float>(xyz[3 * k]), static_cast<float>(xyz[3 * k + 1]),
+                        static_cast<float>(xyz[3 * k + 2]), 0.0f);
+  RP_CUDA(cudaMalloc(&q->d_qf, std::max<size_t>(1, qf.size()) * sizeof(float4)));
+  copy_to_device(ctx, q->d_qf, qf.data(), qf.size() * sizeof(float4));
   return q;
+}
+
+static void upload_rings(rp_ctx* ctx, rp_quiver* q) {
+  const int nr = static_cast<int>(q->ring_offsets.size());
+  std::vector<int> off(q->ring_offsets);
+  off.push_back(q->n);
+  std::vector<double> c(nr), s(nr);
+  for (int r = 0; r < nr; ++r) {
+    c[r] = std::cos(q->ring_elevations[r]);
+    s[r] = std::sin(q->ring_elevations[r]);
+  }
+  RP_CUDA(cudaMalloc(&q->d_ring_off, off.size() * sizeof(int)));
+  RP_CUDA(cudaMalloc(&q->d_ring_c, std::max(1, nr) * sizeof(double)));
+  RP_CUDA(cudaMalloc(&q->d_ring_s, std::max(1, nr) * sizeof(double)));
+  copy_to_device(ctx, q->d_ring_off, off.data(), off.size() * sizeof(int));
+  copy_to_device(ctx, q->d_ring_c, c.data(), nr * sizeof(double));
+  copy_to_device(ctx, q->d_ring_s, s.data(), nr * sizeof(double));
+  q->n_rings = nr;
 }
 
 rp_status rp_quiver_generate(rp_ctx* ctx, double elev_step, double azim_step,
@@ -516,6 +540,7 @@ rp_status rp_quiver_generate(rp_ctx* ctx, double elev_step, double azim_step,
     q->elev_step = elev_step;
     q->equator_azim_step = azim_step;
     q->min_per_ring = min_per_ring;
+    upload_rings(ctx, q);
     *out = q;
   });
 }
@@ -557,6 +582,10 @@ rp_status rp_quiver_destroy(rp_quiver* q) {
   return guarded([&] {
     if (!q) return;
     if (q->d_soa) cudaFree(q->d_soa);
+    if (q->d_qf) cudaFree(q->d_qf);
+    if (q->d_ring_off) cudaFree(q->d_ring_off);
+    if (q->d_ring_c) cudaFree(q->d_ring_c);
+    if (q->d_ring_s) cudaFree(q->d_ring_s);
     delete q;
   });
 }

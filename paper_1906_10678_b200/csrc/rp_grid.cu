@@ -725,6 +725,73 @@ void launch_rows(rp_ctx* ctx, const char* name, rp_grid* g, const Prim* prims, i
          wtab, reach, y0, y1, z0, z1, tw, ty, tz, acc);
 }
 
+/// One launch of replan_dynamic's per-tick re-voxelisation
+/// (src/path_planner.cpp:1011-1021: aug = static grid; overlay = the new
+/// obstacle marked and dilated by the static radius; aug |= overlay): every
+/// word of the static grid is copied, and the words of rows within reach of
+/// the obstacle get its dilated intervals ORed in on the way. The obstacle's
+/// index boxes and the width table travel in the kernel parameters, so the
+/// tick needs no upload, allocation or device-to-device copy.
+constexpr int kOverlayPrims = 8;
+constexpr int kOverlayTab = 2048;  // 2 reach^2 + 1 <= 2048: reach <= 31
+struct OverlayArgs {
+  const uint64_t* base;
+  uint64_t* out;
+  int nx, ny, wx;
+  int64_t n_words;
+  int y0, y1, z0, z1;  // rows that can change (bbox + reach)
+  int np, reach;
+  Prim prims[kOverlayPrims];
+  int wtab[kOverlayTab];
+};
+
+__global__ void __launch_bounds__(256) k_overlay_fused(const __grid_constant__ OverlayArgs A) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t w0 = 2 * t;
+  if (w0 >= A.n_words) return;
+  // two words per thread: one 16-byte load and store when aligned
+  uint64_t v[2];
+  const bool pair = w0 + 1 < A.n_words;
+  if (pair) {
+    const ulonglong2 b = __ldcs(reinterpret_cast<const ulonglong2*>(A.base) + t);
+    v[0] = b.x;
+    v[1] = b.y;
+  } else {
+    v[0] = __ldcs(A.base + w0);
+    v[1] = 0;
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int64_t w = w0 + h;
+    if (w >= A.n_words) break;
+    const int64_t row = w / A.wx;
+    const int y = static_cast<int>(row % A.ny);
+    const int z = static_cast<int>(row / A.ny);
+    if (y < A.y0 || y > A.y1 || z < A.z0 || z > A.z1) continue;
+    const int base = static_cast<int>(w - row * A.wx) * 64;
+    uint64_t m = 0;
+    for (int k = 0; k < A.np; ++k) {
+      const Prim& p = A.prims[k];
+      if (p.a[0] > p.b[0] || p.a[1] > p.b[1] || p.a[2] > p.b[2]) continue;
+      const int dy = y < p.a[1] ? p.a[1] - y : (y > p.b[1] ? y - p.b[1] : 0);
+      const int dz = z < p.a[2] ? p.a[2] - z : (z > p.b[2] ? z - p.b[2] : 0);
+      if (dy > A.reach || dz > A.reach) continue;
+      const int wd = A.wtab[dy * dy + dz * dz];
+      if (wd < 0) continue;
+      int lo = p.a[0] - wd, hi = p.b[0] + wd;
+      lo = lo < 0 ? 0 : lo;
+      hi = hi > A.nx - 1 ? A.nx - 1 : hi;
+      m |= range_mask(lo, hi, base);
+    }
+    v[h] |= m;
+  }
+  if (pair) {
+    __stcs(reinterpret_cast<ulonglong2*>(A.out) + t, make_ulonglong2(v[0], v[1]));
+  } else {
+    A.out[w0] = v[0];
+  }
+}
+
 /// Scatter-mark single cells (cloud points) with atomicOr. Only for
 /// one-cell primitives (a == b); boxes go through the row rasteriser.
 __global__ void k_mark_cells(uint64_t* bits, GridView g, const Prim* __restrict__ prims,
@@ -874,6 +941,134 @@ __global__ void k_popcount(const uint64_t* __restrict__ bits, size_t n, unsigned
   if ((threadIdx.x & 31) == 0) atomicAdd(out, c);
 }
 
+// ---------------------------------------------------------------------------
+// Coarse clearance field (see ClearanceField): coarse occupancy of bk^3
+// blocks, box-dilated by one block (so that the point-to-block lower bound
+// max(0, |c-b|-1) becomes a plain cell distance), then an exact squared
+// Euclidean distance transform, one pass per axis (Felzenszwalb-Huttenlocher
+// lower envelope per line).
+
+constexpr unsigned kCfInf = 0x3FFFFFFFu;
+
+/// Coarse occupancy: one thread per coarse cell, OR of its bk^3 voxels
+/// (bk a power of two <= 64, so a block's x-run sits in one word).
+__global__ void k_cf_occ(GridView g, int bk, int ncx, int ncy, int ncz, uint8_t* __restrict__ occ) {
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= static_cast<int64_t>(ncx) * ncy * ncz) return;
+  const int cx = static_cast<int>(c % ncx);
+  const int cy = static_cast<int>((c / ncx) % ncy);
+  const int cz = static_cast<int>(c / (static_cast<int64_t>(ncx) * ncy));
+  const int x0 = cx * bk;
+  const uint64_t m = (bk >= 64 ? ~0ull : ((1ull << bk) - 1ull)) << (x0 & 63);
+  uint64_t acc = 0;
+  for (int z = cz * bk; z < min(g.nz, (cz + 1) * bk); ++z)
+    for (int y = cy * bk; y < min(g.ny, (cy + 1) * bk); ++y)
+      acc |= __ldg(g.bits + (static_cast<size_t>(z) * g.ny + y) * g.wx + (x0 >> 6));
+  occ[c] = (acc & m) ? 1 : 0;
+}
+
+/// x pass: per (y, z) line, occupancy dilated by one cell in y, z and x,
+/// then the squared distance along x to the nearest such cell (two scans).
+__global__ void k_cf_pass_x(const uint8_t* __restrict__ occ, int ncx, int ncy, int ncz,
+                            unsigned* __restrict__ out) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= ncy * ncz) return;
+  const int y = l % ncy, z = l / ncy;
+  unsigned* o = out + static_cast<size_t>(l) * ncx;
+  auto site = [&](int x) {
+    for (int dz = -1; dz <= 1; ++dz) {
+      const int zz = z + dz;
+      if (zz < 0 || zz >= ncz) continue;
+      for (int dy = -1; dy <= 1; ++dy) {
+        const int yy = y + dy;
+        if (yy < 0 || yy >= ncy) continue;
+        const uint8_t* r = occ + (static_cast<size_t>(zz) * ncy + yy) * ncx;
+        for (int dx = -1; dx <= 1; ++dx) {
+          const int xx = x + dx;
+          if (xx >= 0 && xx < ncx && r[xx]) return true;
+        }
+      }
+    }
+    return false;
+  };
+  int last = -1 << 20;
+  for (int x = 0; x < ncx; ++x) {
+    if (site(x)) last = x;
+    o[x] = last < -(1 << 19) ? kCfInf : static_cast<unsigned>(x - last);
+  }
+  last = 1 << 20;
+  for (int x = ncx - 1; x >= 0; --x) {
+    if (o[x] == 0) last = x;
+    unsigned d = o[x];
+    if (last < (1 << 19) && static_cast<unsigned>(last - x) < d) d = static_cast<unsigned>(last - x);
+    o[x] = d >= kCfInf ? kCfInf : d * d;
+  }
+}
+
+/// y / z pass: exact 1-D squared distance transform of the previous pass's
+/// values along `stride` (Felzenszwalb-Huttenlocher lower envelope; lines
+/// of at most 128 cells).
+__global__ void k_cf_pass(unsigned* __restrict__ f, int n, int64_t stride, int nlines,
+                          int64_t line_a, int64_t line_b, int na, uint16_t* __restrict__ out16) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= nlines) return;
+  const int64_t base = static_cast<int64_t>(l % na) * line_a + static_cast<int64_t>(l / na) * line_b;
+  int v[128];
+  double zz[129];
+  unsigned fv[128];
+  for (int q = 0; q < n; ++q) fv[q] = f[base + q * stride];
+  int k = -1;
+  for (int q = 0; q < n; ++q) {
+    if (fv[q] >= kCfInf) continue;
+    const double fq = static_cast<double>(fv[q]) + static_cast<double>(q) * q;
+    double sx = 0.0;
+    while (k >= 0) {
+      const int r = v[k];
+      sx = (fq - (static_cast<double>(fv[r]) + static_cast<double>(r) * r)) / (2.0 * (q - r));
+      if (sx > zz[k]) break;
+      --k;
+    }
+    ++k;
+    v[k] = q;
+    zz[k] = k == 0 ? -1e300 : sx;
+    zz[k + 1] = 1e300;
+  }
+  int j = 0;
+  for (int q = 0; q < n; ++q) {
+    unsigned d = kCfInf;
+    if (k >= 0) {
+      while (zz[j + 1] < q) ++j;
+      const int r = v[j];
+      // exact integer value at the envelope's parabola; the fp64 breakpoints
+      // only pick it, and a neighbour's value is never smaller than the min
+      const int64_t a = static_cast<int64_t>(fv[r]) + static_cast<int64_t>(q - r) * (q - r);
+      int64_t best = a;
+      if (j > 0) {
+        const int r0 = v[j - 1];
+        const int64_t b = static_cast<int64_t>(fv[r0]) + static_cast<int64_t>(q - r0) * (q - r0);
+        best = b < best ? b : best;
+      }
+      if (j < k) {
+        const int r1 = v[j + 1];
+        const int64_t b = static_cast<int64_t>(fv[r1]) + static_cast<int64_t>(q - r1) * (q - r1);
+        best = b < best ? b : best;
+      }
+      d = best >= kCfInf ? kCfInf : static_cast<unsigned>(best);
+    }
+    if (out16)
+      out16[base + q * stride] = static_cast<uint16_t>(d > 65535u ? 65535u : d);
+    else
+      f[base + q * stride] = d;
+  }
+}
+
+__global__ void k_clearance(GridView g, ClearanceField f, const double* __restrict__ xyz, int64_t n,
+                            double* __restrict__ out) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  out[k] = cf_distance(f, g, V3{xyz[3 * k], xyz[3 * k + 1], xyz[3 * k + 2]});
+}
+
 __global__ void k_point_clear(GridView g, const double* __restrict__ xyz, int64_t n,
                               uint8_t* __restrict__ out) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1007,6 +1202,48 @@ rp_grid* grid_alloc_like(const rp_grid* src) {
   return g;
 }
 
+ClearanceField grid_clearance_field(const rp_grid* g) {
+  rp_ctx* ctx = g->ctx;
+  const int dmax = std::max(g->dims[0], std::max(g->dims[1], g->dims[2]));
+  int bk = 1;
+  while (dmax > 128 * bk) bk *= 2;  // coarse lines of <= 128 cells
+  require(bk <= 64, RP_E_INTERNAL, "clearance field: grid too large");
+  ClearanceField f{};
+  f.bk = bk;
+  f.ncx = (g->dims[0] + bk - 1) / bk;
+  f.ncy = (g->dims[1] + bk - 1) / bk;
+  f.ncz = (g->dims[2] + bk - 1) / bk;
+  f.side = bk * g->voxel_size;
+  f.inv_side = 1.0 / f.side;
+  const size_t cells = static_cast<size_t>(f.ncx) * f.ncy * f.ncz;
+  if (g->cf && g->cf_version == g->version && !g->exported && g->cf_bk == bk) {
+    f.d2 = g->cf;
+    return f;
+  }
+  cudaStream_t st = ctx->stream;
+  if (!g->cf) RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&g->cf), cells * sizeof(uint16_t), st));
+  DevBuf<uint8_t> occ(cells, st);
+  DevBuf<unsigned> work(cells, st);
+  launch(ctx, "clearance", k_cf_occ, dim3(blocks_for(static_cast<int64_t>(cells), 256)), dim3(256),
+         0, g->view(), bk, f.ncx, f.ncy, f.ncz, occ.p);
+  launch(ctx, "clearance", k_cf_pass_x, dim3(blocks_for(static_cast<int64_t>(f.ncy) * f.ncz, 64)),
+         dim3(64), 0, static_cast<const uint8_t*>(occ.p), f.ncx, f.ncy, f.ncz, work.p);
+  // y pass: lines over (x, z); z pass: lines over (x, y) -> 16-bit field
+  launch(ctx, "clearance", k_cf_pass, dim3(blocks_for(static_cast<int64_t>(f.ncx) * f.ncz, 64)),
+         dim3(64), 0, work.p, f.ncy, static_cast<int64_t>(f.ncx), f.ncx * f.ncz, int64_t{1},
+         static_cast<int64_t>(f.ncx) * f.ncy, f.ncx, static_cast<uint16_t*>(nullptr));
+  launch(ctx, "clearance", k_cf_pass, dim3(blocks_for(static_cast<int64_t>(f.ncx) * f.ncy, 64)),
+         dim3(64), 0, work.p, f.ncz, static_cast<int64_t>(f.ncx) * f.ncy, f.ncx * f.ncy,
+         int64_t{1}, static_cast<int64_t>(f.ncx), f.ncx, g->cf);
+  g->cf_bk = bk;
+  g->cf_nc[0] = f.ncx;
+  g->cf_nc[1] = f.ncy;
+  g->cf_nc[2] = f.ncz;
+  g->cf_version = g->version;
+  f.d2 = g->cf;
+  return f;
+}
+
 /// mark_obstacles + dilate(radius) for box / cloud obstacles (see file head).
 void grid_mark_dilate_boxes(rp_grid* g, const rp_obstacle* obs, int n, double radius,
                             bool or_into_existing) {
@@ -1020,6 +1257,7 @@ void grid_mark_dilate_boxes(rp_grid* g, const rp_obstacle* obs, int n, double ra
                           false)) {
       if (!hp.empty()) g->empty = false;
       if (radius != 0.0) g->dilation_radius += radius;
+      ++g->version;
       return;
     }
   }
@@ -1040,6 +1278,7 @@ void grid_mark_dilate_boxes(rp_grid* g, const rp_obstacle* obs, int n, double ra
   }
   if (np > 0) g->empty = false;
   if (radius != 0.0) g->dilation_radius += radius;
+  ++g->version;
 }
 
 }  // namespace rp
@@ -1070,6 +1309,7 @@ rp_status rp_grid_build(rp_ctx* ctx, const double bmin[3], const double bmax[3],
 rp_status rp_grid_mark(rp_grid* g, const rp_obstacle* obs, int32_t n) {
   return guarded([&] {
     if (n <= 0) return;
+    ++g->version;
     check_boxes(obs, n);
     {
       std::vector<Prim> hp;
@@ -1097,6 +1337,7 @@ rp_status rp_grid_dilate(rp_grid* g, double radius) {
   return guarded([&] {
     require(radius >= 0.0, RP_E_INVALID_PARAMETER, "dilation radius must be >= 0");
     if (radius == 0.0) return;
+    ++g->version;
     if (!g->empty) dilate_general(g, radius);
     g->dilation_radius += radius;
   });
@@ -1131,12 +1372,14 @@ rp_status rp_grid_mark_dilate_slab(rp_grid* g, const rp_obstacle* obs, int32_t n
     }
     if (!hp.empty()) g->empty = false;
     g->dilation_radius = radius;
+    ++g->version;
   });
 }
 
 rp_status rp_grid_device_bits(rp_grid* g, void** bits, uint64_t* n_words,
                               uint64_t* words_per_plane) {
   return guarded([&] {
+    g->exported = true;  // written from outside: no cached derived data
     *bits = g->bits;
     *n_words = static_cast<uint64_t>(g->n_words);
     *words_per_plane = static_cast<uint64_t>(g->dims[1]) * g->wx;
@@ -1185,6 +1428,7 @@ rp_status rp_grid_mark_dilate_repeat(rp_grid* g, const rp_obstacle* obs, int32_t
     cudaGraphDestroy(graph);
     *ms = total / std::max(1, reps);
     g->empty = false;
+    ++g->version;
   });
 }
 
@@ -1255,6 +1499,7 @@ rp_status rp_grid_mark_dilate_concurrent(rp_grid* const* grids, int32_t ng, cons
       cudaEventDestroy(joins[k]);
       cudaStreamDestroy(ss[k]);
       grids[k]->empty = false;
+      ++grids[k]->version;
     }
     cudaGraphExecDestroy(exec);
     cudaGraphDestroy(graph);
@@ -1299,12 +1544,46 @@ rp_status rp_grid_overlay(const rp_grid* base, const rp_obstacle* obs, rp_grid**
                   g->dims[2] == base->dims[2],
               RP_E_INVALID_PARAMETER, "overlay target grid has a different shape");
     }
-    RP_CUDA(cudaMemcpyAsync(g->bits, base->bits, base->n_words * sizeof(uint64_t),
-                            cudaMemcpyDeviceToDevice, ctx->stream));
     g->dilation_radius = base->dilation_radius;
     g->empty = base->empty;
+    ++g->version;
     *aug = g;
     check_boxes(obs, 1);
+    {
+      // the common tick: a box (or a few cloud points) within reach 31 ->
+      // one fused copy + raster launch, everything in the parameters
+      std::vector<Prim> hp;
+      const DilTable t = make_table(base->dilation_radius, base->voxel_size);
+      if (host_prims(g, obs, 1, &hp) && hp.size() <= static_cast<size_t>(kOverlayPrims) &&
+          t.w.size() <= static_cast<size_t>(kOverlayTab)) {
+        OverlayArgs A{};
+        A.base = base->bits;
+        A.out = g->bits;
+        A.nx = g->dims[0];
+        A.ny = g->dims[1];
+        A.wx = g->wx;
+        A.n_words = static_cast<int64_t>(g->n_words);
+        A.y0 = A.z0 = 1 << 30;
+        A.y1 = A.z1 = -1;
+        for (const Prim& p : hp) {
+          if (p.a[0] > p.b[0] || p.a[1] > p.b[1] || p.a[2] > p.b[2]) continue;
+          A.y0 = std::min(A.y0, p.a[1] - t.reach);
+          A.y1 = std::max(A.y1, p.b[1] + t.reach);
+          A.z0 = std::min(A.z0, p.a[2] - t.reach);
+          A.z1 = std::max(A.z1, p.b[2] + t.reach);
+        }
+        A.np = static_cast<int>(hp.size());
+        A.reach = t.reach;
+        std::copy(hp.begin(), hp.end(), A.prims);
+        std::copy(t.w.begin(), t.w.end(), A.wtab);
+        const int64_t threads = (A.n_words + 1) / 2;
+        launch(ctx, "overlay", k_overlay_fused, dim3(blocks_for(threads, 256)), dim3(256), 0, A);
+        if (A.y1 >= 0) g->empty = false;
+        return;
+      }
+    }
+    RP_CUDA(cudaMemcpyAsync(g->bits, base->bits, base->n_words * sizeof(uint64_t),
+                            cudaMemcpyDeviceToDevice, ctx->stream));
     {
       // bbox-limited overlay: only rows within reach of the obstacle change
       std::vector<Prim> hp;
@@ -1435,6 +1714,18 @@ rp_status rp_grid_point_clear(rp_grid* g, const double* xyz, int64_t n, uint8_t*
   });
 }
 
+rp_status rp_grid_clearance(rp_grid* g, const double* xyz, int64_t n, double* out) {
+  return guarded([&] {
+    if (n <= 0) return;
+    const ClearanceField f = grid_clearance_field(g);
+    DevBuf<double> d(3 * n, g->ctx->stream), o(n, g->ctx->stream);
+    copy_to_device(g->ctx, d.p, xyz, 3 * n * sizeof(double));
+    launch(g->ctx, "clearance", k_clearance, dim3(blocks_for(n, 256)), dim3(256), 0, g->view(), f,
+           static_cast<const double*>(d.p), n, o.p);
+    copy_to_host(g->ctx, out, o.p, n * sizeof(double));
+  });
+}
+
 rp_status rp_grid_segment_clear(rp_grid* g, const double* a, const double* b, int64_t n,
                                 int32_t ns, uint8_t* out) {
   return guarded([&] {
@@ -1465,6 +1756,7 @@ rp_status rp_grid_destroy(rp_grid* g) {
   return guarded([&] {
     if (!g) return;
     if (g->bits) RP_CUDA(cudaFreeAsync(g->bits, g->ctx->stream));
+    if (g->cf) RP_CUDA(cudaFreeAsync(g->cf, g->ctx->stream));
     delete g;
   });
 }

@@ -107,6 +107,15 @@ struct rp_quiver {
   std::vector<double> ring_elevations;
   double elev_step = 0.0, equator_azim_step = 0.0;
   int min_per_ring = 0;
+  // device copies for direction culling (rp_rings.cuh): ring offsets
+  // [n_rings + 1] and cos/sin of the ring elevations (host glibc); 0 rings
+  // for uploaded quivers. d_qf = the directions as fp32 float4 (prefilters
+  // only; every decision is re-taken on the fp64 SoA).
+  int n_rings = 0;
+  int* d_ring_off = nullptr;
+  double* d_ring_c = nullptr;
+  double* d_ring_s = nullptr;
+  float4* d_qf = nullptr;
 };
 
 struct rp_grid {
@@ -119,6 +128,15 @@ struct rp_grid {
   uint64_t* bits = nullptr;
   size_t n_words = 0;
   bool empty = true;  // no occupancy since build: fused mark+dilate is exact
+  // Coarse clearance field (grid_clearance_field): built lazily, cached
+  // until the next modification (version) and never cached once the words
+  // were exported for external writes (rp_grid_device_bits).
+  uint64_t version = 0;
+  bool exported = false;
+  mutable uint64_t cf_version = ~0ull;
+  mutable uint16_t* cf = nullptr;
+  mutable int cf_bk = 0;
+  mutable int cf_nc[3] = {0, 0, 0};
 
   rpd::GridView view() const {
     rpd::GridView v;
@@ -280,6 +298,37 @@ void copy_to_device(rp_ctx* ctx, void* dst, const void* src, size_t bytes);
 double nominal_spacing(const rp_arm& a, const rp_reach_params& r);
 double resolved_epsilon(const rp_arm& a, const rp_reach_params& r);
 double resolved_near_radius(const rp_arm& a, const rp_reach_params& r);
+
+/// Lower bound on the distance from any point to the grid's occupied cells:
+/// a squared distance d2[c] (in units of `side`^2) per coarse cell c of
+/// bk^3 voxels, d2 = min over occupied blocks b of sum_i max(0, |c_i-b_i|-1)^2
+/// (UINT16_MAX-ish when the grid is empty). A point p in (or projected onto)
+/// cell c is at least side*sqrt(d2[c]) from every occupied cell.
+struct ClearanceField {
+  const uint16_t* d2;
+  int bk, ncx, ncy, ncz;
+  double side, inv_side;
+};
+ClearanceField grid_clearance_field(const rp_grid* g);
+
+/// side * sqrt(d2) of the coarse cell holding p projected onto the grid box
+/// (projection onto a convex set never increases distances to points in it),
+/// shrunk by 1e-9 relative + 1e-9 m for the fp64 rounding of the cell index.
+__device__ __forceinline__ double cf_distance(const ClearanceField& f, const rpd::GridView& g,
+                                              V3 p) {
+  int c[3];
+  const double o[3] = {g.ox, g.oy, g.oz};
+  const double pv[3] = {p.x, p.y, p.z};
+  const int n[3] = {f.ncx, f.ncy, f.ncz};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double u = (pv[a] - o[a]) * f.inv_side;
+    int k = u <= 0.0 ? 0 : (u >= n[a] ? n[a] - 1 : static_cast<int>(u));
+    c[a] = k;
+  }
+  const unsigned d2 = __ldg(f.d2 + (static_cast<size_t>(c[2]) * f.ncy + c[1]) * f.ncx + c[0]);
+  return f.side * sqrt(static_cast<double>(d2)) * (1.0 - 1e-9) - 1e-9;
+}
 
 // Grid entry points used across translation units.
 rp_grid* grid_alloc_like(const rp_grid* g);

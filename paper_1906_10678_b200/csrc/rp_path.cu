@@ -4,7 +4,9 @@
 #include "rp_path.cuh"
 #include "rp_planner.hpp"
 #include "rp_refine.cuh"
+#include "rp_rings.cuh"
 
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -1411,6 +1413,773 @@ __global__ void __launch_bounds__(kBpThreads, 1) k_backward_pass(const __grid_co
 }
 
 // ---------------------------------------------------------------------------
+// Cluster backward pass (coaxial arms without joint limits, generated
+// quivers): the whole sequential pass (src/path_planner.cpp:322-400) in ONE
+// thread-block cluster of CL CTAs. Per (waypoint, target, factor) attempt:
+//  F  every CTA builds both candidate lists itself (no exchange): the
+//     cones around the previous segment directions are enumerated ring by
+//     ring (rp_rings.cuh: <= 2 azimuth arcs per latitude ring, a superset)
+//     and each visited direction gets waypoint_ik's exact fp64 cone and
+//     move1 tests; ordered compaction by block scans of packed counts.
+//  S  the (i, j) pairs are dealt over the cluster's warps (32 j per warp
+//     item); an fp32 prefilter with 1e-5 m margins drops the pairs that
+//     cannot pass the move2 bound or the gap band, the rest queue in shared
+//     memory (warp-aggregated appends).
+//  E  the queue is evaluated data-parallel in flat item lists instead of
+//     candidate by candidate: the exact prefix (wik_pre_fast) and the
+//     smoothness bound per candidate, then every walk of every live
+//     candidate (segments 2, 3 and each trail option) one per thread, then
+//     every non-adjacent link distance, then the verdicts (the first trail
+//     option whose walk and links are clear, as append_trail takes it) and
+//     the CTA's (metric, ordinal) minimum.
+//  R  one cluster barrier; lane r of warp 0 reads CTA r's winner over DSMEM
+//     and every CTA reduces identically, so all continue with the same pose
+//     and no second barrier is needed (slots are double-buffered by attempt
+//     parity).
+// Exactness: the lists are supersets filtered by the reference's own fp64
+// tests (ascending index order, so ordinals compare like the reference's
+// (cand_i, cand_j) scan), the prefilter only drops pairs the exact prefix
+// would reject, every test is the reference's predicate on the same fp64
+// pose, and the winner is the (metric, ordinal) minimum over every
+// qualifying pair -- the first strict minimum of the reference's loop.
+
+namespace cg = cooperative_groups;
+
+constexpr int kBpcThreads = 512;
+constexpr int kBpcWarps = kBpcThreads / 32;
+constexpr int kBpcQueue = 768;   // prefiltered pairs per round per CTA (> 32 x warps)
+constexpr int kBpcRings = 256;   // latitude rings (2 deg: 91, 1 deg: 181)
+constexpr int kBpcCiCap = 1024;  // segment-1 points cached as fp32 in shared memory
+constexpr int kBpcBatch = 64;    // candidates evaluated together (best first)
+static_assert(kBpcQueue > 32 * kBpcWarps, "a round must fit every warp's last item");
+
+struct BpcSlot {  // one CTA's winner of an attempt
+  double metric;
+  long long ord;
+  int opt, i, j;
+  V3 p1;
+};
+
+struct BpcShared {
+  WikDev sw;
+  V3 u1, u2, cu, cv, wk;
+  double fetch[21];
+  V3 prev[5];
+  int found;
+  int nci, ncj;
+  int tot[2];
+  int nq, nl;  // queued pairs, live candidates
+  int win_rank;
+  // cluster-visible, [attempt parity]: best-hit bound (metric bits),
+  // winner slot, cancel flag
+  unsigned long long bound[2];
+  BpcSlot slot[2];
+  int cancel[2];
+  // ring intervals of both cones
+  int rcnt[2 * kBpcRings];
+  int rbase[2 * kBpcRings + 1];
+  int2 riv[2 * kBpcRings][4];
+  signed char rniv[2 * kBpcRings];
+  // prefiltered pairs of a round: ordinal a * ncj + b, exact metric,
+  // candidate geometry (p2, s3) and walk / distance failure bits
+  double qm[kBpcQueue];
+  unsigned qo[kBpcQueue];
+  V3 cj2[kBpcQueue];
+  V3 cs3[kBpcQueue];
+  V3 cdl[kBpcQueue];  // normalized(s3): the straight trail option
+  int cflag[kBpcQueue];
+  short qs[kBpcQueue];  // the current batch
+  short ql[kBpcQueue];  // live candidates (any order)
+  unsigned char cbin[kBpcQueue];
+  int hist[256], cum[256];
+  unsigned long long mlo, mhi, bmin;
+  int nb;
+  float4 p1f[kBpcCiCap];
+  WikBest wb[kBpcWarps];
+};
+
+
+__device__ __forceinline__ unsigned long long metric_bits(double m) {
+  return static_cast<unsigned long long>(__double_as_longlong(m));  // m >= 0: monotone
+}
+
+__global__ void __launch_bounds__(kBpcThreads, 1) k_bp_cluster(const __grid_constant__ BpArgs A) {
+  // dynamic shared memory: [BpcShared][li: Q x u16][lj: Q x u16]
+  extern __shared__ __align__(16) unsigned char bpc_smem[];
+  BpcShared& S = *reinterpret_cast<BpcShared*>(bpc_smem);
+  unsigned short* li = reinterpret_cast<unsigned short*>(bpc_smem + sizeof(BpcShared));
+  unsigned short* lj = li + A.Q;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = static_cast<int>(cluster.block_rank());
+  const int CL = static_cast<int>(cluster.num_blocks());
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool prof = A.prof && rank == 0 && tid == 0;
+  const ArmDev& arm = A.arm;
+  const auto rebuild = [&]() {
+    if (rank != 0) return;
+    __syncthreads();
+    for (int q = tid; q < A.m; q += blockDim.x)
+      if (A.win[q].i >= 0) A.poses[q] = pose_from_win(A, A.win[q]);
+  };
+  if (tid == 0) {
+    S.bound[0] = S.bound[1] = metric_bits(1e308);
+    S.cancel[0] = S.cancel[1] = 0;
+  }
+  cluster.sync();  // bound and flags initialised before any CTA reads CTA 0's
+  unsigned long long* bound0 = cluster.map_shared_rank(&S.bound[0], 0);
+  const int* cancel0 = cluster.map_shared_rank(&S.cancel[0], 0);
+  int par = 0;  // attempt parity (identical in every CTA)
+  const int nr = A.nrings;
+  for (int k = A.m - 2; k >= 0; --k) {
+    if (k == 0 && A.has_fixed) {
+      if (rank == 0 && tid == 0) {
+        V3 pj1, pj2;
+        if (A.m > 2) {
+          pj1 = S.prev[0];
+          pj2 = S.prev[1];
+        } else {
+          const DevPose pv = ldcg_struct(A.poses + 1);
+          pj1 = pv.joints[1];
+          pj2 = pv.joints[2];
+        }
+        int found = 0;
+        for (int fi = 0; fi < A.nf && !found; ++fi) {
+          const double f = A.factors[fi];
+          const double b1 = A.pj1 * f + 1e-12, b2 = A.pj2 * f + 1e-12;
+          if (rpd::norm(A.fixed_first.joints[1] - pj1) <= b1 &&
+              rpd::norm(A.fixed_first.joints[2] - pj2) <= b2) {  // pose_smooth
+            A.poses[0] = A.fixed_first;
+            A.relax[0] = f;
+            A.kind[0] = 2;
+            found = 1;
+          }
+        }
+        A.state[0] = found;
+        A.state[1] = found ? -1 : 0;
+        A.state[2] = found;
+      }
+      rebuild();
+      cluster.sync();  // no CTA leaves while another may still read its slots
+      return;
+    }
+    // previous pose (anchor from memory, later ones from the last winner)
+    // and the waypoint list around k
+    if (k == A.m - 2) {
+      if (tid < 12) {
+        const DevPose* pp = A.poses + k + 1;
+        const double* src = tid < 6 ? &pp->joints[1 + tid / 3].x : &pp->seg[(tid - 6) / 3].x;
+        S.fetch[tid] = __ldcg(src + tid % 3);
+      }
+    } else if (tid < 12) {
+      S.fetch[tid] = (&S.prev[0].x)[tid];
+    }
+    if (tid >= 12 && tid < 21) {
+      const int wi = k - 1 + (tid - 12) / 3;  // k-1, k, k+1
+      S.fetch[tid] = wi >= 0 ? __ldcg(&A.wps[wi].x + (tid - 12) % 3) : 0.0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const V3 prev_j1{S.fetch[0], S.fetch[1], S.fetch[2]};
+      const V3 prev_j2{S.fetch[3], S.fetch[4], S.fetch[5]};
+      const V3 prev_s0{S.fetch[6], S.fetch[7], S.fetch[8]};
+      const V3 prev_s1{S.fetch[9], S.fetch[10], S.fetch[11]};
+      const V3 wk{S.fetch[15], S.fetch[16], S.fetch[17]};
+      const V3 wprev = k > 0 ? V3{S.fetch[12], S.fetch[13], S.fetch[14]} : wk;
+      const V3 wnext{S.fetch[18], S.fetch[19], S.fetch[20]};
+      WikDev& w = S.sw;
+      if (k == A.m - 2) {
+        w = WikDev{};
+        w.g = A.g;
+        w.arm = A.arm;
+        w.n = A.n;
+        w.Q = A.Q;
+        w.qx = A.qx;
+        w.qy = A.qy;
+        w.qz = A.qz;
+        w.spacing = A.spacing;
+        w.four = A.four;
+        w.L4 = A.L4;
+        w.cond2 = A.cond2;
+        w.cond3 = A.cond3;
+        w.filter_j = A.filter_j;
+        w.prof = nullptr;
+      }
+      w.prev_j1 = prev_j1;
+      w.prev_j2 = prev_j2;
+      w.n_opts = 0;
+      if (k > 0) {
+        const V3 d = wprev - wk;
+        if (rpd::norm(d) > 1e-12) w.opt_dir[w.n_opts++] = rpd::normalized(d);
+      }
+      if (k + 1 < A.m) {
+        const V3 d = wnext - wk;
+        if (rpd::norm(d) > 1e-12) w.opt_dir[w.n_opts++] = rpd::normalized(d);
+      }
+      const bool fixed_bias = A.has_fixed && k == 1;
+      w.has_bias = (fixed_bias || A.has_bias) ? 1 : 0;
+      if (w.has_bias) {
+        const DevPose& b = fixed_bias ? A.fixed_first : A.bias;
+        w.bias_j1 = b.joints[1];
+        w.bias_j2 = b.joints[2];
+      }
+      S.u1 = rpd::normalized(prev_s0);
+      S.u2 = rpd::normalized(prev_s1);
+      S.wk = wk;
+      S.cu = V3{0, 0, 0};
+      S.cv = V3{0, 0, 0};
+      if (A.cloud) {
+        V3 dir = wnext - wk;
+        if (rpd::norm(dir) < 1e-12 && k > 0) dir = wk - wprev;
+        if (rpd::norm(dir) < 1e-12) dir = V3{0, 0, 1};
+        dir = rpd::normalized(dir);
+        S.cu = perpendicular_of(dir);
+        S.cv = rpd::cross(dir, S.cu);
+      }
+    }
+    __syncthreads();
+    const WikDev& w = S.sw;
+    bool found = false;
+    const int n_targets = A.cloud ? 9 : 1;
+    for (int t = 0; t < n_targets && !found; ++t) {
+      for (int fi = 0; fi < A.nf && !found; ++fi, par ^= 1) {
+        const double f = A.factors[fi];
+        long long c0 = prof ? clock64() : 0;
+        if (tid == 0) {
+          S.sw.wp = t == 0 ? S.wk : S.wk + A.cloud_radius * (A.ring_c[t - 1] * S.cu +
+                                                           A.ring_s[t - 1] * S.cv);
+          S.sw.eps = A.eps_wp * f + 1e-12;
+          S.sw.j1max = A.pj1 * f + 1e-12;
+          S.sw.j2max = A.pj2 * f + 1e-12;
+          S.sw.sm1 = S.sw.j1max;
+          S.sw.sm2 = S.sw.j2max;
+          S.nq = 0;
+          S.nl = 0;
+          S.mlo = metric_bits(1e308);
+          S.mhi = 0ull;
+          // the other parity's bound is free: every CTA passed the barrier of
+          // the attempt that used it
+          if (rank == 0) S.bound[par ^ 1] = metric_bits(1e308);
+        }
+        if (tid < 256) S.hist[tid] = 0;
+        __syncthreads();
+        const V3 u1 = S.u1, u2 = S.u2;
+        const double cone1 = A.cone1[fi], cone2 = A.cone2[fi];
+        // ---- F: ring intervals of both cones
+        for (int r2 = tid; r2 < 2 * nr; r2 += blockDim.x) {
+          const int cone = r2 >= nr, r = cone ? r2 - nr : r2;
+          const int off = __ldg(A.ring_off + r), cnt = __ldg(A.ring_off + r + 1) - off;
+          int a0[2], ln[2], is[4], ie[4];
+          const int na = ring_arcs(__ldg(A.qring_c + r), __ldg(A.qring_s + r), cnt, cone ? u2 : u1,
+                                   cone ? cone2 : cone1, 2.0, a0, ln);
+          int m = ring_intervals(cnt, a0, ln, na, is, ie);
+          if (m < 0) {
+            m = 1;
+            is[0] = 0;
+            ie[0] = cnt;
+          }
+          int c = 0;
+          for (int q = 0; q < m; ++q) {
+            S.riv[r2][q] = make_int2(off + is[q], ie[q] - is[q]);
+            c += ie[q] - is[q];
+          }
+          S.rniv[r2] = static_cast<signed char>(m);
+          S.rcnt[r2] = c;
+        }
+        __syncthreads();
+        if (prof) A.prof[16] += clock64() - c0;
+        {
+          typedef cub::BlockScan<int, kBpcThreads> Scan;
+          __shared__ typename Scan::TempStorage scan_tmp;
+          int v = 0;
+          const int per = (2 * nr + kBpcThreads - 1) / kBpcThreads;  // <= 1 for nr <= 256
+          (void)per;
+          v = tid < 2 * nr ? S.rcnt[tid] : 0;
+          int ex = 0, tot = 0;
+          Scan(scan_tmp).ExclusiveSum(v, ex, tot);
+          if (tid < 2 * nr) S.rbase[tid] = ex;
+          if (tid == 0) S.rbase[2 * nr] = tot;
+          __syncthreads();
+          if (tid == 0) {
+            S.tot[0] = S.rbase[nr];
+            S.tot[1] = tot;  // positions [tot0, tot) are the j cone's
+            S.nci = 0;
+            S.ncj = 0;
+          }
+          __syncthreads();
+          if (prof) {
+            A.prof[17] += clock64() - c0;
+            A.prof[18] += S.tot[1];
+          }
+          // expand positions in order, exact tests, ordered compaction with
+          // packed (i count << 16 | j count) block scans
+          const int total = S.tot[1], tot0 = S.tot[0];
+          int carry = 0;  // packed running counts (every thread holds it)
+          for (int p0 = 0; p0 < total; p0 += kBpcThreads) {
+            const int p = p0 + tid;
+            int flag = 0, idx = 0;
+            V3 p1{0, 0, 0};
+            if (p < total) {
+              // ring-interval of position p: binary search over the bases
+              int lo = p < tot0 ? 0 : nr, hi = p < tot0 ? nr - 1 : 2 * nr - 1;
+              while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (S.rbase[mid] <= p) lo = mid;
+                else hi = mid - 1;
+              }
+              int rem = p - S.rbase[lo];
+              int q = 0;
+              while (rem >= S.riv[lo][q].y) {
+                rem -= S.riv[lo][q].y;
+                ++q;
+              }
+              idx = S.riv[lo][q].x + rem;
+              const V3 qv{A.qx[idx], A.qy[idx], A.qz[idx]};
+              if (p < tot0) {
+                // wik_filter_fast: cone, then the move1 bound
+                if (rpd::dot(qv, u1) >= cone1) {
+                  p1 = arm.root + arm.L[0] * qv;
+                  const double move1 = rpd::norm(p1 - w.prev_j1);
+                  flag = !(move1 > w.j1max) ? (1 << 16) : 0;
+                }
+              } else {
+                flag = rpd::dot(qv, u2) >= cone2 ? 1 : 0;
+              }
+            }
+            int ex2 = 0, tot2 = 0;
+            Scan(scan_tmp).ExclusiveSum(flag, ex2, tot2);
+            const int pos = carry + ex2;
+            if (flag >> 16) {
+              const int a = pos >> 16;
+              li[a] = static_cast<unsigned short>(idx);
+              if (a < kBpcCiCap) {
+                const float ok = static_cast<float>((__ldg(A.walk1 + (idx >> 5)) >> (idx & 31)) & 1u);
+                S.p1f[a] = make_float4(static_cast<float>(p1.x), static_cast<float>(p1.y),
+                                       static_cast<float>(p1.z), ok);
+              }
+            } else if (flag) {
+              lj[pos & 0xFFFF] = static_cast<unsigned short>(idx);
+            }
+            carry += tot2;
+            __syncthreads();  // scan_tmp reuse
+          }
+          if (tid == 0) {
+            S.nci = carry >> 16;
+            S.ncj = carry & 0xFFFF;
+          }
+          __syncthreads();
+        }
+        long long c1 = prof ? clock64() : 0;
+        const int nci = S.nci, ncj = S.ncj;
+        // ---- S + E in rounds of at most kBpcQueue prefiltered pairs per CTA
+        double bm = 1e308;
+        long long bo = LLONG_MAX;
+        int bopt = -1;
+        const int nbj = (ncj + 31) >> 5;
+        const long long items = static_cast<long long>(nci) * nbj;
+        long long it = static_cast<long long>(rank) * kBpcWarps + warp;
+        const long long istride = static_cast<long long>(CL) * kBpcWarps;
+        const float L1f = static_cast<float>(arm.L[0]), L2f = static_cast<float>(arm.L[1]);
+        const float rx = static_cast<float>(arm.root.x), ry = static_cast<float>(arm.root.y),
+                    rz = static_cast<float>(arm.root.z);
+        const float pjx = static_cast<float>(w.prev_j2.x), pjy = static_cast<float>(w.prev_j2.y),
+                    pjz = static_cast<float>(w.prev_j2.z);
+        const float wpx = static_cast<float>(w.wp.x), wpy = static_cast<float>(w.wp.y),
+                    wpz = static_cast<float>(w.wp.z);
+        const float m2max = static_cast<float>((w.j2max + 1e-5) * (w.j2max + 1e-5));
+        const double bhi = arm.L[2] + w.eps + 1e-5, blo = fmax(0.0, arm.L[2] - w.eps - 1e-5);
+        const float b2hi = static_cast<float>(bhi * bhi), b2lo = static_cast<float>(blo * blo);
+        const int thresh = kBpcQueue - 32 * kBpcWarps;
+        // walk / distance items per candidate: walks = segment 2, segment 3
+        // and (8DOF) the trail segment of each option; distances = link pair
+        // (0,2) and per option (0,3), (1,3) -- or (0,2) alone for 6DOF
+        const int nopt = A.four ? w.n_opts + 1 : 0;
+        const int nwalk = 2 + nopt, ndist = 1 + 2 * nopt;
+        const double min_sep = 2.0 * arm.arm_radius;
+        long long cs = 0, ce = 0;
+        for (;;) {
+          const long long s0 = prof ? clock64() : 0;
+          // S: fp32 prefilter, survivors' ordinals queued
+          while (it < items && *reinterpret_cast<volatile int*>(&S.nq) < thresh) {
+            const int a = static_cast<int>(it / nbj);
+            const int b = static_cast<int>(it - static_cast<long long>(a) * nbj) * 32 + lane;
+            it += istride;
+            float4 pf;
+            if (a < kBpcCiCap) {
+              pf = S.p1f[a];
+            } else {
+              const int i = li[a];
+              const float4 qi = __ldg(A.qf + i);
+              pf = make_float4(rx + L1f * qi.x, ry + L1f * qi.y, rz + L1f * qi.z,
+                               static_cast<float>((__ldg(A.walk1 + (i >> 5)) >> (i & 31)) & 1u));
+            }
+            if (pf.w == 0.0f) continue;  // segment 1 blocked: no pair of this i qualifies
+            bool keep = false;
+            if (b < ncj) {
+              const float4 qj = __ldg(A.qf + lj[b]);
+              const float x2 = pf.x + L2f * qj.x, y2 = pf.y + L2f * qj.y, z2 = pf.z + L2f * qj.z;
+              const float dx = x2 - pjx, dy = y2 - pjy, dz = z2 - pjz;
+              const float vx = wpx - x2, vy = wpy - y2, vz = wpz - z2;
+              const float m2 = dx * dx + dy * dy + dz * dz;
+              const float v2 = vx * vx + vy * vy + vz * vz;
+              keep = m2 <= m2max && v2 <= b2hi && v2 >= b2lo;
+            }
+            const unsigned km = __ballot_sync(FULL, keep);
+            if (km) {
+              int base = 0;
+              if (lane == 0) base = atomicAdd(&S.nq, __popc(km));
+              base = __shfl_sync(FULL, base, 0);
+              if (keep)
+                S.qo[base + __popc(km & ((1u << lane) - 1u))] =
+                    static_cast<unsigned>(a) * static_cast<unsigned>(ncj) + static_cast<unsigned>(b);
+            }
+          }
+          const bool more = __syncthreads_or(it < items);
+          const int nq = S.nq;
+          const long long s1 = prof ? clock64() : 0;
+          if (nq > 0) {
+            // E0: exact prefix (wik_pre_fast) + smoothness bound per candidate;
+            // geometry kept for the walk and distance items; dead = +inf
+            long long t_e = prof ? clock64() : 0;
+            for (int e = tid; e < nq; e += kBpcThreads) {
+              const unsigned od = S.qo[e];
+              const int a = static_cast<int>(od / static_cast<unsigned>(ncj));
+              const int j = lj[od - static_cast<unsigned>(a) * static_cast<unsigned>(ncj)];
+              const int i = li[a];
+              CiFast c;
+              c.i = i;
+              c.ok = 1;
+              c.p1 = arm.root + arm.L[0] * V3{A.qx[i], A.qy[i], A.qz[i]};
+              c.move1 = rpd::norm(c.p1 - w.prev_j1);
+              double mm = 1e308;
+              int flag = 1 << 30;  // dead
+              if (wik_pre_fast(w, c, j, &mm)) {
+                const V3 qj{A.qx[j], A.qy[j], A.qz[j]};
+                const V3 p2 = c.p1 + arm.L[1] * qj;
+                const V3 v3 = w.wp - p2;
+                const V3 s3 = (v3 / rpd::norm(v3)) * arm.L[2];
+                S.cj2[e] = p2;
+                S.cs3[e] = s3;
+                S.cdl[e] = A.four ? rpd::normalized(s3) : V3{0, 0, 0};  // straight trail
+                // chain joints 1, 2 are p1, p2 (cumulative sums)
+                if (rpd::norm(c.p1 - w.prev_j1) <= w.sm1 && rpd::norm(p2 - w.prev_j2) <= w.sm2)
+                  flag = 0;
+              }
+              if (flag) mm = 1e308;
+              S.qm[e] = mm;
+              S.cflag[e] = flag;
+              if (!flag) {
+                S.ql[atomicAdd(&S.nl, 1)] = static_cast<short>(e);
+                atomicMin(&S.mlo, metric_bits(mm));
+                atomicMax(&S.mhi, metric_bits(mm));
+              }
+            }
+            __syncthreads();
+            // best first: (metric, ordinal) order, evaluated kBpcBatch at a
+            // time; the first batch with a hit holds this CTA's answer, and a
+            // batch starting above the cluster's best hit cannot win
+            if (prof) { A.prof[19] += clock64() - t_e; t_e = clock64(); }
+            // best first without sorting: the live metrics go into 256 equal
+            // bins over [min, max]; batch t = the candidates of the bins after
+            // batch t-1's up to the first bin that brings >= kBpcBatch more.
+            // A bin index is monotone in the metric, so every candidate of a
+            // later batch has a strictly larger metric than every candidate
+            // of an earlier one: the first batch with a hit holds this CTA's
+            // (metric, ordinal) minimum.
+            const int nl = S.nl;
+            const double mlo = __longlong_as_double(static_cast<long long>(S.mlo));
+            const double bw = (__longlong_as_double(static_cast<long long>(S.mhi)) - mlo) / 256.0;
+            for (int x = tid; x < nl; x += kBpcThreads) {
+              const int e = S.ql[x];
+              const int bin = bw > 0.0 ? min(255, static_cast<int>((S.qm[e] - mlo) / bw)) : 0;
+              S.cbin[e] = static_cast<unsigned char>(bin);
+              atomicAdd(&S.hist[bin], 1);
+            }
+            __syncthreads();
+            if (warp == 0) {  // inclusive prefix sums of the 256 bins
+              int run = 0;
+              for (int c = 0; c < 256; c += 32) {
+                int v = S.hist[c + lane];
+                for (int off = 1; off < 32; off <<= 1) {
+                  const int u = __shfl_up_sync(FULL, v, off);
+                  if (lane >= off) v += u;
+                }
+                S.cum[c + lane] = run + v;
+                run += __shfl_sync(FULL, v, 31);
+              }
+            }
+            __syncthreads();
+            if (prof) { A.prof[20] += clock64() - t_e; t_e = clock64(); }
+            int prev = -1, done = 0;
+            while (done < nl) {
+              // last bin of this batch: the first whose cumulative count
+              // reaches done + kBpcBatch (binary search, block-uniform)
+              int lo = prev + 1, hi = 255;
+              while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (S.cum[mid] >= done + kBpcBatch) hi = mid;
+                else lo = mid + 1;
+              }
+              const int kb = lo;
+              if (tid == 0) {
+                S.nb = 0;
+                S.bmin = metric_bits(1e308);
+              }
+              __syncthreads();
+              for (int x = tid; x < nl; x += kBpcThreads) {
+                const int e = S.ql[x];
+                const int bin = S.cbin[e];
+                if (bin > prev && bin <= kb) {
+                  S.qs[atomicAdd(&S.nb, 1)] = static_cast<short>(e);
+                  atomicMin(&S.bmin, metric_bits(S.qm[e]));
+                }
+              }
+              __syncthreads();
+              const int nb = S.nb;
+              prev = kb;
+              done = S.cum[kb];
+              // the bound moves under other CTAs' hits: decide it block-uniformly
+              const double first = __longlong_as_double(static_cast<long long>(S.bmin));
+              const double gb = __longlong_as_double(static_cast<long long>(
+                  *reinterpret_cast<volatile unsigned long long*>(bound0 + par)));
+              if (__syncthreads_or(first > gb)) break;
+              // E1: every walk of the batch's live candidates, one per thread
+              for (int t = tid; t < nb * nwalk; t += kBpcThreads) {
+                const int e = S.qs[t / nwalk], k = t % nwalk;
+                if (S.cflag[e]) continue;
+                const V3 p2 = S.cj2[e], s3 = S.cs3[e];
+                const V3 j3 = p2 + s3;
+                V3 from, to;
+                if (k == 0) {
+                  const int i = li[S.qo[e] / static_cast<unsigned>(ncj)];
+                  from = arm.root + arm.L[0] * V3{A.qx[i], A.qy[i], A.qz[i]};
+                  to = p2;
+                } else if (k == 1) {
+                  from = p2;
+                  to = j3;
+                } else {
+                  const int o = k - 2;
+                  const V3 dir = o < w.n_opts ? w.opt_dir[o] : S.cdl[e];
+                  from = j3;
+                  to = j3 + w.L4 * dir;
+                }
+                if (rpd::walk_first_blocked_fast_seg(w.g, from, to, w.n) != 0)
+                  atomicOr(&S.cflag[e], 1 << k);
+              }
+              __syncthreads();
+              if (prof) { A.prof[21] += clock64() - t_e; t_e = clock64(); }
+              // E2: the non-adjacent link distances of candidates whose
+              // segment-2/3 walks are clear (per option only if its trail is)
+              for (int t = tid; t < nb * ndist; t += kBpcThreads) {
+                const int e = S.qs[t / ndist], d = t % ndist;
+                const int fl = S.cflag[e];
+                if (fl & ((1 << 30) | 3)) continue;
+                const int o = d == 0 ? -1 : (d - 1) >> 1;
+                if (o >= 0 && ((fl >> (2 + o)) & 1)) continue;
+                const V3 p2 = S.cj2[e], s3 = S.cs3[e];
+                const V3 j3 = p2 + s3;
+                const int i = li[S.qo[e] / static_cast<unsigned>(ncj)];
+                const V3 j1 = arm.root + arm.L[0] * V3{A.qx[i], A.qy[i], A.qz[i]};
+                V3 a0, a1, b0v, b1;
+                double ha, hb;
+                if (d == 0) {  // links 0 and 2
+                  a0 = arm.root; a1 = j1; b0v = p2; b1 = j3;
+                  ha = 0.5 * arm.L[0];
+                  hb = 0.5 * arm.L[2];
+                } else {
+                  const V3 dir = o < w.n_opts ? w.opt_dir[o] : S.cdl[e];
+                  const V3 j4 = j3 + w.L4 * dir;
+                  const bool p03 = ((d - 1) & 1) == 0;  // links 0 and 3, else 1 and 3
+                  a0 = p03 ? arm.root : j1;
+                  a1 = p03 ? j1 : p2;
+                  b0v = j3;
+                  b1 = j4;
+                  ha = 0.5 * (p03 ? arm.L[0] : arm.L[1]);
+                  hb = 0.5 * w.L4;
+                }
+                const bool ok =
+                    rpd::links_clear_screen(a0, a1, b0v, b1, ha * (1.0 + 1e-9), hb * (1.0 + 1e-9),
+                                            min_sep) ||
+                    !(rpd::seg_seg_distance(a0, a1, b0v, b1) < min_sep);
+                if (!ok) atomicOr(&S.cflag[e], 1 << (8 + d));
+              }
+              __syncthreads();
+              if (prof) { A.prof[22] += clock64() - t_e; t_e = clock64(); }
+              // E3: verdicts (the first trail option whose walk and links are
+              // clear, like append_trail) and this thread's (metric, ordinal) min
+              bool hit = false;
+              for (int x = tid; x < nb; x += kBpcThreads) {
+                const int e = S.qs[x];
+                const int fl = S.cflag[e];
+                if (fl & ((1 << 30) | 3)) continue;
+                int opt = -1;
+                bool h = false;
+                if (!A.four) {
+                  h = !((fl >> 8) & 1);
+                } else if (!((fl >> 8) & 1)) {
+                  for (int o = 0; o < nopt && !h; ++o)
+                    if (!((fl >> (2 + o)) & 1) && !((fl >> (9 + 2 * o)) & 3)) {
+                      h = true;
+                      opt = o;
+                    }
+                }
+                const double mm = S.qm[e];
+                const long long od = S.qo[e];
+                if (h && wik_better(mm, od, bm, bo)) {
+                  bm = mm;
+                  bo = od;
+                  bopt = opt;
+                  atomicMin(bound0 + par, metric_bits(mm));
+                }
+                hit |= h;
+              }
+              if (prof) A.prof[14] += 1;
+              if (__syncthreads_or(hit)) break;
+            }
+            if (prof) A.prof[12] += nq;
+          }
+          __syncthreads();
+          if (tid == 0) {
+            S.nq = 0;
+            S.nl = 0;
+            S.mlo = metric_bits(1e308);
+            S.mhi = 0ull;
+          }
+          if (tid < 256) S.hist[tid] = 0;
+          __syncthreads();
+          if (prof) {
+            cs += s1 - s0;
+            ce += clock64() - s1;
+          }
+          if (!more) break;
+        }
+        long long c2 = prof ? clock64() : 0;
+        // ---- R: this CTA's winner -> its slot; cluster barrier; reduce
+        for (int off = 16; off > 0; off >>= 1) {
+          const double om = __shfl_down_sync(FULL, bm, off);
+          const long long oo = __shfl_down_sync(FULL, bo, off);
+          const int op = __shfl_down_sync(FULL, bopt, off);
+          if (wik_better(om, oo, bm, bo)) {
+            bm = om;
+            bo = oo;
+            bopt = op;
+          }
+        }
+        if (lane == 0) S.wb[warp] = WikBest{bm, bo, bopt, -1, -1, V3{0, 0, 0}};
+        __syncthreads();
+        if (tid == 0) {
+          WikBest b = S.wb[0];
+          for (int q = 1; q < kBpcWarps; ++q)
+            if (wik_better(S.wb[q].metric, S.wb[q].ord, b.metric, b.ord)) b = S.wb[q];
+          BpcSlot sl{b.metric, b.ord, b.opt, -1, -1, V3{0, 0, 0}};
+          if (b.ord != LLONG_MAX) {
+            const int a = static_cast<int>(b.ord / ncj);
+            sl.i = li[a];
+            sl.j = lj[b.ord - static_cast<long long>(a) * ncj];
+            sl.p1 = arm.root + arm.L[0] * V3{A.qx[sl.i], A.qy[sl.i], A.qz[sl.i]};
+          }
+          S.slot[par] = sl;
+          if (rank == 0 && A.cancel) S.cancel[par] = *reinterpret_cast<const volatile int*>(A.cancel);
+        }
+        long long c3 = prof ? clock64() : 0;
+        cluster.sync();
+        long long c4 = prof ? clock64() : 0;
+        if (A.cancel && cancel0[par]) {
+          rebuild();
+          if (rank == 0 && tid == 0) A.state[3] = 1;
+          cluster.sync();
+          return;
+        }
+        if (warp == 0) {
+          // lane r reads CTA r's winner; the lanes reduce (metric, ordinal)
+          double rm = 1e308;
+          long long ro = LLONG_MAX;
+          int rr = -1;
+          if (lane < CL) {
+            const BpcSlot* o = cluster.map_shared_rank(&S.slot[par], lane);
+            rm = o->metric;
+            ro = o->ord;
+            rr = lane;
+          }
+          for (int off = 16; off > 0; off >>= 1) {
+            const double om = __shfl_down_sync(FULL, rm, off);
+            const long long oo = __shfl_down_sync(FULL, ro, off);
+            const int orr = __shfl_down_sync(FULL, rr, off);
+            if (wik_better(om, oo, rm, ro)) {
+              rm = om;
+              ro = oo;
+              rr = orr;
+            }
+          }
+          if (lane == 0) S.win_rank = ro != LLONG_MAX ? rr : -1;
+        }
+        __syncthreads();
+        if (tid == 0) {
+          BpcSlot b{1e308, LLONG_MAX, -1, -1, -1, V3{0, 0, 0}};
+          if (S.win_rank >= 0) b = *cluster.map_shared_rank(&S.slot[par], S.win_rank);
+          int ok = 0;
+          if (b.ord != LLONG_MAX) {
+            const V3 s0 = arm.L[0] * V3{A.qx[b.i], A.qy[b.i], A.qz[b.i]};
+            const V3 s1 = arm.L[1] * V3{A.qx[b.j], A.qy[b.j], A.qz[b.j]};
+            const V3 j1 = arm.root + s0;
+            S.prev[0] = j1;
+            S.prev[1] = j1 + s1;
+            S.prev[2] = s0;
+            S.prev[3] = s1;
+            S.prev[4] = t > 0 ? w.wp : S.wk;
+            if (rank == 0) {
+              BpWin W;
+              W.i = b.i;
+              W.j = b.j;
+              W.opt = b.opt;
+              W.n_opts = w.n_opts;
+              W.p1 = b.p1;
+              W.wp = w.wp;
+              W.opt_dir[0] = w.opt_dir[0];
+              W.opt_dir[1] = w.opt_dir[1];
+              A.win[k] = W;
+              A.relax[k] = f;
+              A.kind[k] = t > 0 ? 1 : 0;
+              if (t > 0) A.wps[k] = w.wp;
+              A.state[0] = 1;
+            }
+            ok = 1;
+          }
+          S.found = ok;
+        }
+        __syncthreads();
+        found = S.found != 0;
+        if (prof) {
+          const long long c5 = clock64();
+          A.prof[0] += c1 - c0;  // F: lists
+          A.prof[10] += cs;      // S: screening
+          A.prof[11] += ce;      // E: sort + evaluation waves
+          A.prof[2] += c2 - c1;  // S + E
+          A.prof[3] += c4 - c3;  // cluster barrier
+          A.prof[4] += c5 - c4;  // reduce + publish
+          A.prof[6] += 1;
+          A.prof[7] += static_cast<long long>(nci) * ncj;
+        }
+      }
+    }
+    if (!found) {
+      if (rank == 0 && tid == 0) {
+        A.state[1] = k;
+        A.state[2] = 0;
+      }
+      rebuild();
+      cluster.sync();
+      return;
+    }
+  }
+  if (rank == 0 && tid == 0) {
+    A.state[1] = -1;
+    A.state[2] = 1;
+  }
+  rebuild();
+  cluster.sync();
+}
+
+// ---------------------------------------------------------------------------
 // Single-pose operations (one thread): refinement and trail folding.
 
 /// mode 0: exact_refine_8dof, 1: _8dof_triangle, 2: exact_refine_6dof
@@ -1946,7 +2715,13 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
     return false;
   cudaStream_t st = ctx->stream;
   const size_t smem = 2 * static_cast<size_t>(q->n) * sizeof(int);
-  if (bp_blocks == 0) {
+  // the cluster pass (k_bp_cluster) takes coaxial limit-free arms on
+  // generated quivers; RP_BP_COOP=1 forces the cooperative grid pass
+  static const bool force_coop = std::getenv("RP_BP_COOP") != nullptr;
+  const bool cluster = !force_coop && !ad.any_limit && !ad.has_offsets && q->n_rings > 0 &&
+                       q->n_rings <= kBpcRings;
+  if (cluster && !bp_state.p) bp_state.alloc(4, st);
+  if (!cluster && bp_blocks == 0) {
     // kernel attribute + occupancy: once per device and shared-memory size
     // (the attribute is per device; planners may run on several threads)
     static std::mutex attr_mutex;
@@ -2061,18 +2836,67 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
     prof.zero();
     A.prof = prof.p;
   }
-  void* args[] = {&A};
   cudaEvent_t ev = nullptr;
-  launch_begin(ctx, "backward_pass", &ev);
-  RP_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_backward_pass), dim3(bp_blocks),
-                                      dim3(kBpThreads), args, smem, st));
-  launch_end(ctx, "backward_pass", ev);
+  if (cluster) {
+    A.nrings = q->n_rings;
+    A.ring_off = q->d_ring_off;
+    A.qring_c = q->d_ring_c;
+    A.qring_s = q->d_ring_s;
+    A.qf = q->d_qf;
+    const size_t csmem = sizeof(BpcShared) + 2 * static_cast<size_t>(q->n) * sizeof(unsigned short);
+    static const int ctas = [] {
+      const char* e = std::getenv("RP_BPC_CTAS");
+      const int c = e ? std::atoi(e) : 16;
+      return c >= 16 ? 16 : (c >= 8 ? 8 : (c >= 4 ? 4 : (c >= 2 ? 2 : 1)));
+    }();
+    {
+      // per device and shared-memory size (planners may run on several threads)
+      static std::mutex attr_mutex;
+      static std::map<int, size_t> configured;
+      std::lock_guard<std::mutex> lock(attr_mutex);
+      size_t& have = configured[ctx->device];
+      if (have < csmem) {
+        RP_CUDA(cudaFuncSetAttribute(k_bp_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(csmem)));
+        RP_CUDA(cudaFuncSetAttribute(k_bp_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                                     1));
+        have = csmem;
+      }
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ctas);
+    cfg.blockDim = dim3(kBpcThreads);
+    cfg.dynamicSmemBytes = csmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = ctas;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    launch_begin(ctx, "backward_pass", &ev);
+    RP_CUDA(cudaLaunchKernelEx(&cfg, k_bp_cluster, A));
+    launch_end(ctx, "backward_pass", ev);
+  } else {
+    void* args[] = {&A};
+    launch_begin(ctx, "backward_pass", &ev);
+    RP_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_backward_pass), dim3(bp_blocks),
+                                        dim3(kBpThreads), args, smem, st));
+    launch_end(ctx, "backward_pass", ev);
+  }
   int hs[4];
   copy_to_host(ctx, hs, bp_state.p, sizeof(hs));
   if (profile) {
     long long hp[24];
     copy_to_host(ctx, hp, prof.p, sizeof(hp));
-    std::fprintf(stderr, "[half] setup %lld walks %lld dists %lld cycles\n", hp[16], hp[17], hp[18]);
+    if (cluster)
+      std::fprintf(stderr,
+                   "[bpc] lists: arcs %lld arcs+scan %lld cycles, %lld positions | E0 %lld sort "
+                   "%lld walks %lld dists %lld\n",
+                   hp[16], hp[17], hp[18], hp[19], hp[20], hp[21], hp[22]);
+    else
+      std::fprintf(stderr, "[half] setup %lld walks %lld dists %lld cycles\n", hp[16], hp[17], hp[18]);
     std::fprintf(stderr, "[pairs] screening %lld, rank+eval %lld cycles (rank %lld, waves %lld); screened %lld\n", hp[10],
                  hp[11], hp[15], hp[14], hp[12]);
     std::fprintf(stderr,

@@ -126,6 +126,13 @@ struct BpArgs {
   int* state;     // [4] found, failed_index, ok, cancelled
   const int* cancel;  // device flag set (by a host DMA) to stop the pass early; may be null
   long long* prof;  // optional [8] phase cycle counters (RP_PROFILE_PASS)
+  // cluster pass (k_bp_cluster): quiver rings for the candidate cones and
+  // the fp32 directions for the pair prefilter
+  int nrings;
+  const int* ring_off;
+  const double* qring_c;  // cos / sin of the ring elevations
+  const double* qring_s;
+  const float4* qf;
 };
 
 /// Device scratch reused by every waypoint_ik call of a planner.

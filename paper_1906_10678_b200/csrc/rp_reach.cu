@@ -15,6 +15,7 @@
 // solution set, the shortcut set and all 13 SolveStats counters are
 // bit-identical to the reference.
 #include "rp_reach.cuh"
+#include "rp_rings.cuh"
 #include "rp_refine.cuh"
 
 #include <cub/cub.cuh>
@@ -333,88 +334,41 @@ constexpr bool kSeg2ParWalk = RP_SEG2_PAR_WALK;
 #define RP_BQ_MINB 4
 #endif
 
-/// Occupied coarse blocks (edge bk voxels) of a grid, as packed
-/// (bx | by << 10 | bz << 20), in any order.
-__global__ void k_occ_blocks(rpd::GridView g, int bk, int nbx, int nby, int nbz, int* __restrict__ list,
-                             int* __restrict__ count) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= nbx * nby * nbz) return;
-  const int bx = b % nbx, by = (b / nbx) % nby, bz = b / (nbx * nby);
-  const int x0 = bx * bk;
-  const uint64_t m = (bk >= 64 ? ~0ull : ((1ull << bk) - 1ull)) << (x0 & 63);
-  bool occ = false;
-  for (int z = bz * bk; z < min(g.nz, (bz + 1) * bk) && !occ; ++z)
-    for (int y = by * bk; y < min(g.ny, (by + 1) * bk); ++y)
-      if (__ldg(g.bits + (static_cast<size_t>(z) * g.ny + y) * g.wx + (x0 >> 6)) & m) {
-        occ = true;
-        break;
-      }
-  if (occ) list[atomicAdd(count, 1)] = bx | (by << 10) | (bz << 20);
-}
-
-/// Squared distance from p to the nearest occupied block box (warp-reduced;
-/// every lane gets the result).
-__device__ double occ_block_d2(const rpd::GridView& g, V3 p, int bk, const int* __restrict__ list,
-                               int nb) {
-  const int lane = threadIdx.x & 31;
-  const double side = bk * g.vs;
-  double d2 = 1e300;
-  for (int k = lane; k < nb; k += 32) {
-    const int c = list[k];
-    const double lx = g.ox + (c & 1023) * side, ly = g.oy + ((c >> 10) & 1023) * side,
-                 lz = g.oz + (c >> 20) * side;
-    const double dx = fmax(0.0, fmax(lx - p.x, p.x - (lx + side)));
-    const double dy = fmax(0.0, fmax(ly - p.y, p.y - (ly + side)));
-    const double dz = fmax(0.0, fmax(lz - p.z, p.z - (lz + side)));
-    d2 = fmin(d2, dx * dx + dy * dy + dz * dz);
-  }
-  for (int off = 16; off > 0; off >>= 1) d2 = fmin(d2, __shfl_xor_sync(FULL, d2, off));
-  return d2;
-}
-
-/// Per end point b (one warp each): kend = the samples 1..kend of a walk
-/// [p2, b] with |b - p2| <= L that are not proven free; sample j lies within
-/// (1 - j/n) * L of b, so it is free when that plus sqrt(3) * vs is below the
-/// distance from b to the nearest occupied block (see k_row_skip).
+/// Per end point b: kend = the samples 1..kend of a walk [p2, b] with
+/// |b - p2| <= L that are not proven free; sample j lies within
+/// (1 - j/n) * L of b, so it is free when that plus sqrt(3) * vs is below
+/// the clearance-field lower bound D on the distance from b to any occupied
+/// cell (see k_row_skip).
 __global__ void k_tail_skip(rpd::GridView g, const V3* __restrict__ pts, int T, double L, int n,
-                            int bk, const int* __restrict__ list, const int* __restrict__ count,
-                            uint8_t* __restrict__ kend) {
-  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+                            ClearanceField f, uint8_t* __restrict__ kend) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
-  const double d2 = occ_block_d2(g, pts[t], bk, list, *count);
-  if ((threadIdx.x & 31) == 0) {
-    const double D = sqrt(d2) * (1.0 - 1e-9) - 1e-9;
-    const double Lm = L * (1.0 + 1e-9) + 1e-9;
-    const double cell = 1.7320508075688772 * g.vs * (1.0 + 1e-9) + 1e-9;
-    int j = n;
-    while (j >= 1 && (1.0 - static_cast<double>(j) / n) * Lm + cell < D) --j;
-    kend[t] = static_cast<uint8_t>(j);
-  }
+  const double D = cf_distance(f, g, pts[t]);
+  const double Lm = L * (1.0 + 1e-9) + 1e-9;
+  const double cell = 1.7320508075688772 * g.vs * (1.0 + 1e-9) + 1e-9;
+  int j = n;
+  while (j >= 1 && (1.0 - static_cast<double>(j) / n) * Lm + cell < D) --j;
+  kend[t] = static_cast<uint8_t>(j);
 }
 
 /// Per survivor row: how many leading segment-2 samples are provably free.
-/// D = distance from p1 to the nearest occupied block box (a lower bound on
-/// the distance to any occupied cell). Sample k lies within t_k * L2 of p1
+/// D = the clearance field's lower bound on the distance from p1 to any
+/// occupied cell (grid_clearance_field). Sample k lies within t_k * L2 of p1
 /// (|q_j| = 1 up to rounding), and the cell the reference floors it to
 /// (off by at most one per axis from the cell holding it) lies within
 /// sqrt(3) * vs of it, so samples with t_k * L2 + sqrt(3) * vs < D (with
-/// margins) are free. One warp per row.
-__global__ void k_row_skip(SolveDev a, const SurvDev* __restrict__ sv, int S1, int bk,
-                           const int* __restrict__ list, const int* __restrict__ count,
+/// margins) are free. One thread per row.
+__global__ void k_row_skip(SolveDev a, const SurvDev* __restrict__ sv, int S1, ClearanceField f,
                            uint8_t* __restrict__ kskip) {
-  const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= S1) return;
   const rpd::GridView& g = a.g;
-  const double d2 = occ_block_d2(g, sv[s].p1, bk, list, *count);
-  if (lane == 0) {
-    const double D = sqrt(d2) * (1.0 - 1e-9) - 1e-9;
-    const double L2 = a.arm.L[1] * (1.0 + 1e-9) + 1e-9;
-    const double cell = 1.7320508075688772 * g.vs * (1.0 + 1e-9) + 1e-9;
-    int k = 0;
-    while (k < a.n && (static_cast<double>(k + 1) / a.n) * L2 + cell < D) ++k;
-    kskip[s] = static_cast<uint8_t>(k);
-  }
+  const double D = cf_distance(f, g, sv[s].p1);
+  const double L2 = a.arm.L[1] * (1.0 + 1e-9) + 1e-9;
+  const double cell = 1.7320508075688772 * g.vs * (1.0 + 1e-9) + 1e-9;
+  int k = 0;
+  while (k < a.n && (static_cast<double>(k + 1) / a.n) * L2 + cell < D) ++k;
+  kskip[s] = static_cast<uint8_t>(k);
 }
 
 template <bool EIGHT>
@@ -1018,34 +972,20 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
         const int rblocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks, (units + 7) / 8)));
         DevBuf<int> unit_ctr(1, st);
         unit_ctr.zero();
-        // free leading samples per row (k_row_skip) from the occupied coarse
-        // blocks (edge: 4 voxels, or dims/32 for larger grids)
-        const int dmax = std::max(g->dims[0], std::max(g->dims[1], g->dims[2]));
-        int bk = 4;
-        while (bk < 64 && bk * 32 < dmax) bk *= 2;
-        const int nbx = (g->dims[0] + bk - 1) / bk, nby = (g->dims[1] + bk - 1) / bk,
-                  nbz = (g->dims[2] + bk - 1) / bk;
-        DevBuf<int> blist(static_cast<size_t>(nbx) * nby * nbz, st), bcount(1, st);
+        // free leading samples per row (k_row_skip) and trailing samples of
+        // the v3 walks (k_tail_skip) from the grid's cached clearance field
         DevBuf<uint8_t> kskip(std::max(1, S1), st);
         static const bool no_skip = std::getenv("RP_NO_ROW_SKIP") != nullptr;
-        if (no_skip) {
-          kskip.zero();
-        } else {
-          bcount.zero();
-          launch(ctx, "seg2", k_occ_blocks, dim3(nblk(static_cast<int64_t>(nbx) * nby * nbz, 256)),
-                 dim3(256), 0, a.g, bk, nbx, nby, nbz, blist.p, bcount.p);
-          launch(ctx, "seg2", k_row_skip, dim3(nblk(static_cast<int64_t>(S1) * 32, 256)), dim3(256), 0,
-                 a, static_cast<const SurvDev*>(s->surv.p), S1, bk,
-                 static_cast<const int*>(blist.p), static_cast<const int*>(bcount.p), kskip.p);
-        }
         DevBuf<uint8_t> kend_b(1, st);
         if (no_skip) {
-          const uint8_t full = static_cast<uint8_t>(rp.n_samples);
-          copy_to_device(ctx, kend_b.p, &full, 1);
+          kskip.zero();
+          RP_CUDA(cudaMemsetAsync(kend_b.p, rp.n_samples, 1, st));
         } else {
+          const ClearanceField cf = grid_clearance_field(g);
+          launch(ctx, "seg2", k_row_skip, dim3(nblk(S1, 128)), dim3(128), 0, a,
+                 static_cast<const SurvDev*>(s->surv.p), S1, cf, kskip.p);
           launch(ctx, "seg2", k_tail_skip, dim3(1), dim3(32), 0, a.g,
-                 static_cast<const V3*>(s->bpts.p), 1, L3 + eps, rp.n_samples, bk,
-                 static_cast<const int*>(blist.p), static_cast<const int*>(bcount.p), kend_b.p);
+                 static_cast<const V3*>(s->bpts.p), 1, L3 + eps, rp.n_samples, cf, kend_b.p);
         }
         auto runr = [&](auto kern) {
           launch(ctx, "seg2", kern, dim3(rblocks), dim3(threads), 0, a,
@@ -1551,105 +1491,6 @@ struct BatchDev {
   const double* ring_c;
   const double* ring_s;
 };
-
-/// Azimuth index arcs of ring (cphi, sphi, cnt) whose directions q satisfy
-/// lo <= q.u <= hi (u unit), widened by 1.5 azimuth steps so that rounding
-/// in the generator or here can only add directions, never drop one. Writes
-/// up to 2 arcs as (first index, length) and returns their number; a full
-/// ring is one arc (0, cnt).
-__device__ __noinline__ int ring_arcs(double cphi_d, double sphi_d, int cnt, V3 u, double lo_d,
-                                     double hi_d, int* a0, int* len) {
-  // Evaluated in fp32: the arcs only choose which directions are visited
-  // (every visited pair gets the exact tests), so they need to be a
-  // superset, not exact. The band is widened by 1e-5 for the fp32 dot
-  // product and the angular margin by 2e-3 rad for fp32 acos/atan2 (its
-  // error near |x| = 1 is below 4e-4 rad) on top of the 1.5-step margin.
-  const float cphi = static_cast<float>(cphi_d), sphi = static_cast<float>(sphi_d);
-  const float ux = static_cast<float>(u.x), uy = static_cast<float>(u.y), uz = static_cast<float>(u.z);
-  const float lo = static_cast<float>(lo_d) - 1e-5f, hi = static_cast<float>(hi_d) + 1e-5f;
-  const float rho = sqrtf(ux * ux + uy * uy);
-  const float A = cphi * rho, B = sphi * uz;
-  if (!(A > 1e-5f)) {  // q.u is B +- A over the whole ring
-    if (B + A + 1e-5f >= lo && B - A - 1e-5f <= hi) {
-      a0[0] = 0;
-      len[0] = cnt;
-      return 1;
-    }
-    return 0;
-  }
-  const float x_hi = (hi - B) / A, x_lo = (lo - B) / A;
-  if (x_lo > 1.0f || x_hi < -1.0f) return 0;
-  const float kPiF = 3.14159265358979323846f;
-  const float step = 2.0f * kPiF / cnt;
-  const float marg = 1.5f * step + 2e-3f;
-  const float d_lo = fmaxf(0.0f, (x_hi >= 1.0f ? 0.0f : acosf(fmaxf(-1.0f, x_hi))) - marg);
-  const float d_hi = fminf(kPiF, (x_lo <= -1.0f ? kPiF : acosf(fminf(1.0f, x_lo))) + marg);
-  if (d_lo <= 0.0f && d_hi >= kPiF) {
-    a0[0] = 0;
-    len[0] = cnt;
-    return 1;
-  }
-  const float thu = atan2f(uy, ux);
-  int n = 0;
-  auto arc = [&](float t0, float t1) {
-    const int m0 = static_cast<int>(ceilf(t0 / step)), m1 = static_cast<int>(floorf(t1 / step));
-    const int c = m1 - m0 + 1;
-    if (c <= 0) return;
-    if (c >= cnt) {
-      a0[n] = 0;
-      len[n++] = cnt;
-      return;
-    }
-    int s0 = m0 % cnt;
-    if (s0 < 0) s0 += cnt;
-    a0[n] = s0;
-    len[n++] = c;
-  };
-  if (d_lo <= 0.0f) {
-    arc(thu - d_hi, thu + d_hi);
-  } else {
-    arc(thu + d_lo, thu + d_hi);
-    arc(thu - d_hi, thu - d_lo);
-  }
-  return n;
-}
-
-/// Merged index intervals [s, e) (ring-local, ascending, disjoint) of up to
-/// four arcs; returns the count (<= 8) or -1 for "whole ring".
-__device__ __noinline__ int ring_intervals(int cnt, const int* a0, const int* len, int na, int* is, int* ie) {
-  int s[8], e[8], n = 0;
-  for (int k = 0; k < na; ++k) {
-    if (len[k] >= cnt) return -1;
-    const int st = a0[k], en = a0[k] + len[k];
-    if (en <= cnt) {
-      s[n] = st;
-      e[n++] = en;
-    } else {  // wraps past the last azimuth
-      s[n] = st;
-      e[n++] = cnt;
-      s[n] = 0;
-      e[n++] = en - cnt;
-    }
-  }
-  for (int i = 1; i < n; ++i)  // insertion sort by start
-    for (int j = i; j > 0 && s[j] < s[j - 1]; --j) {
-      const int ts = s[j], te = e[j];
-      s[j] = s[j - 1];
-      e[j] = e[j - 1];
-      s[j - 1] = ts;
-      e[j - 1] = te;
-    }
-  int m = 0;
-  for (int i = 0; i < n; ++i) {
-    if (m > 0 && s[i] <= ie[m - 1]) {
-      if (e[i] > ie[m - 1]) ie[m - 1] = e[i];
-    } else {
-      is[m] = s[i];
-      ie[m++] = e[i];
-    }
-  }
-  return m;
-}
 
 __device__ __forceinline__ void warp_flush_t(unsigned long long* ctr, int idx, unsigned v) {
   v = __reduce_add_sync(FULL, v);
@@ -2391,18 +2232,9 @@ extern "C" rp_status rp_solve_reach_batch(rp_ctx* ctx, const rp_arm* arm, const 
     DevBuf<int> d_ttgt(std::max(1, tail_cap), st), d_tlen(std::max(1, tail_cap), st);
     DevBuf<BestRec> d_tbest(CH, st);
     const std::vector<BestRec> tbest_init(CH, BestRec{1e308, LLONG_MAX});
-    // occupied coarse blocks of the grid (once per call) for k_tail_skip
-    const int dmax = std::max(g->dims[0], std::max(g->dims[1], g->dims[2]));
-    int bk = 4;
-    while (bk < 64 && bk * 32 < dmax) bk *= 2;
-    const int nbx = (g->dims[0] + bk - 1) / bk, nby = (g->dims[1] + bk - 1) / bk,
-              nbz = (g->dims[2] + bk - 1) / bk;
-    DevBuf<int> blist(static_cast<size_t>(nbx) * nby * nbz, st), bcount(1, st);
-    bcount.zero();
+    // the grid's clearance field (cached) for k_tail_skip
     static const bool no_skip = std::getenv("RP_NO_ROW_SKIP") != nullptr;
-    if (!no_skip)
-      launch(ctx, "seg2", k_occ_blocks, dim3(nblk(static_cast<int64_t>(nbx) * nby * nbz, 256)),
-             dim3(256), 0, a.g, bk, nbx, nby, nbz, blist.p, bcount.p);
+    const ClearanceField cf = no_skip ? ClearanceField{} : grid_clearance_field(g);
     DevBuf<uint8_t> d_kend(CH, st);
     DevBuf<long long> d_scl(kBatchShortcutCap, st);
     DevBuf<BestRec> d_bb(static_cast<size_t>(CH) * BPT, st), d_best(CH, st);
@@ -2475,9 +2307,8 @@ extern "C" rp_status rp_solve_reach_batch(rp_ctx* ctx, const rp_arm* arm, const 
       if (no_skip) {
         RP_CUDA(cudaMemsetAsync(d_kend.p, rp->n_samples, T, st));
       } else {
-        launch(ctx, "seg2", k_tail_skip, dim3(nblk(static_cast<int64_t>(T) * 32, 256)), dim3(256),
-               0, a.g, static_cast<const V3*>(d_b.p), T, L3 + eps, rp->n_samples, bk,
-               static_cast<const int*>(blist.p), static_cast<const int*>(bcount.p), d_kend.p);
+        launch(ctx, "seg2", k_tail_skip, dim3(nblk(T, 128)), dim3(128), 0, a.g,
+               static_cast<const V3*>(d_b.p), T, L3 + eps, rp->n_samples, cf, d_kend.p);
       }
       d.kend_b = d_kend.p;
       launch(ctx, "walk4", k_bq_walk4, dim3(nblk(T, 128)), dim3(128), 0, d, d_w4.p);
