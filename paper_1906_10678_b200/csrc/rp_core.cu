@@ -67,9 +67,20 @@ void launch_end(rp_ctx* ctx, const char* name, cudaEvent_t ev) {
 static void drain_timing(rp_ctx* ctx) {
   if (ctx->pending.empty()) return;
   RP_CUDA(cudaStreamSynchronize(ctx->stream));
+  // RP_TIMELINE=1: the device timeline of the timed launches (offsets from
+  // the first launch, and the idle gap before each one)
+  static const bool timeline = std::getenv("RP_TIMELINE") != nullptr;
+  float prev_end = 0.f;
   for (auto& t : ctx->pending) {
     float ms = 0.f;
     RP_CUDA(cudaEventElapsedTime(&ms, t.start, t.stop));
+    if (timeline) {
+      float at = 0.f;
+      RP_CUDA(cudaEventElapsedTime(&at, ctx->pending.front().start, t.start));
+      std::fprintf(stderr, "[tl] %9.3f ms +%8.3f gap %8.3f %s\n", at, ms, at - prev_end,
+                   t.name.c_str());
+      prev_end = at + ms;
+    }
     auto& acc = ctx->kernel_ms[t.name];
     acc.first += ms;
     acc.second += 1;
@@ -366,6 +377,10 @@ rp_status rp_ctx_destroy(rp_ctx* ctx) {
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     for (cudaEvent_t e : ctx->upload_ev) cudaEventDestroy(e);
+    for (auto& b : ctx->s2_pool) {
+      cudaFree(b.bits);
+      cudaFree(b.ok);
+    }
     if (ctx->upload_ring) cudaFreeHost(ctx->upload_ring);
     if (ctx->cancel_flag) cudaFree(ctx->cancel_flag);
     if (ctx->aux) cudaStreamDestroy(ctx->aux);

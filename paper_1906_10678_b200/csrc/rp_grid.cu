@@ -943,10 +943,12 @@ __global__ void k_popcount(const uint64_t* __restrict__ bits, size_t n, unsigned
 
 // ---------------------------------------------------------------------------
 // Coarse clearance field (see ClearanceField): coarse occupancy of bk^3
-// blocks, box-dilated by one block (so that the point-to-block lower bound
-// max(0, |c-b|-1) becomes a plain cell distance), then an exact squared
-// Euclidean distance transform, one pass per axis (Felzenszwalb-Huttenlocher
-// lower envelope per line).
+// blocks, then d2(c) = min over occupied blocks b of sum_i max(0, |c_i-b_i|-1)^2,
+// which is separable: three passes of a 1-D min-plus transform with the cost
+// c(d) = max(0, |d| - 1)^2, one warp per line (lines of <= 64 cells staged
+// in shared memory), each value capped at W^2 where W is the window the pass
+// scans -- sites beyond it cost at least that, so the result stays a lower
+// bound (saturating at W coarse cells, >= 0.6 m).
 
 constexpr unsigned kCfInf = 0x3FFFFFFFu;
 
@@ -967,98 +969,45 @@ __global__ void k_cf_occ(GridView g, int bk, int ncx, int ncy, int ncz, uint8_t*
   occ[c] = (acc & m) ? 1 : 0;
 }
 
-/// x pass: per (y, z) line, occupancy dilated by one cell in y, z and x,
-/// then the squared distance along x to the nearest such cell (two scans).
-__global__ void k_cf_pass_x(const uint8_t* __restrict__ occ, int ncx, int ncy, int ncz,
-                            unsigned* __restrict__ out) {
-  const int l = blockIdx.x * blockDim.x + threadIdx.x;
-  if (l >= ncy * ncz) return;
-  const int y = l % ncy, z = l / ncy;
-  unsigned* o = out + static_cast<size_t>(l) * ncx;
-  auto site = [&](int x) {
-    for (int dz = -1; dz <= 1; ++dz) {
-      const int zz = z + dz;
-      if (zz < 0 || zz >= ncz) continue;
-      for (int dy = -1; dy <= 1; ++dy) {
-        const int yy = y + dy;
-        if (yy < 0 || yy >= ncy) continue;
-        const uint8_t* r = occ + (static_cast<size_t>(zz) * ncy + yy) * ncx;
-        for (int dx = -1; dx <= 1; ++dx) {
-          const int xx = x + dx;
-          if (xx >= 0 && xx < ncx && r[xx]) return true;
-        }
-      }
-    }
-    return false;
-  };
-  int last = -1 << 20;
-  for (int x = 0; x < ncx; ++x) {
-    if (site(x)) last = x;
-    o[x] = last < -(1 << 19) ? kCfInf : static_cast<unsigned>(x - last);
-  }
-  last = 1 << 20;
-  for (int x = ncx - 1; x >= 0; --x) {
-    if (o[x] == 0) last = x;
-    unsigned d = o[x];
-    if (last < (1 << 19) && static_cast<unsigned>(last - x) < d) d = static_cast<unsigned>(last - x);
-    o[x] = d >= kCfInf ? kCfInf : d * d;
-  }
-}
-
-/// y / z pass: exact 1-D squared distance transform of the previous pass's
-/// values along `stride` (Felzenszwalb-Huttenlocher lower envelope; lines
-/// of at most 128 cells).
-__global__ void k_cf_pass(unsigned* __restrict__ f, int n, int64_t stride, int nlines,
-                          int64_t line_a, int64_t line_b, int na, uint16_t* __restrict__ out16) {
-  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+/// One pass of the separable transform along `stride`: out[q] = min(W^2,
+/// min over |q - r| <= W of in[r] + max(0, |q - r| - 1)^2) (the first pass
+/// reads the occupancy: 0 or "infinite"). One warp per line (<= 64 cells),
+/// 8 per block.
+template <bool FIRST, bool LAST>
+__global__ void __launch_bounds__(256) k_cf_pass(const void* __restrict__ in_v, void* __restrict__ out_v,
+                                                 int n, int64_t stride, int nlines, int64_t line_a,
+                                                 int64_t line_b, int na, int W) {
+  __shared__ unsigned line[8][64];
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int l = blockIdx.x * 8 + wl;
   if (l >= nlines) return;
   const int64_t base = static_cast<int64_t>(l % na) * line_a + static_cast<int64_t>(l / na) * line_b;
-  int v[128];
-  double zz[129];
-  unsigned fv[128];
-  for (int q = 0; q < n; ++q) fv[q] = f[base + q * stride];
-  int k = -1;
-  for (int q = 0; q < n; ++q) {
-    if (fv[q] >= kCfInf) continue;
-    const double fq = static_cast<double>(fv[q]) + static_cast<double>(q) * q;
-    double sx = 0.0;
-    while (k >= 0) {
-      const int r = v[k];
-      sx = (fq - (static_cast<double>(fv[r]) + static_cast<double>(r) * r)) / (2.0 * (q - r));
-      if (sx > zz[k]) break;
-      --k;
-    }
-    ++k;
-    v[k] = q;
-    zz[k] = k == 0 ? -1e300 : sx;
-    zz[k + 1] = 1e300;
-  }
-  int j = 0;
-  for (int q = 0; q < n; ++q) {
-    unsigned d = kCfInf;
-    if (k >= 0) {
-      while (zz[j + 1] < q) ++j;
-      const int r = v[j];
-      // exact integer value at the envelope's parabola; the fp64 breakpoints
-      // only pick it, and a neighbour's value is never smaller than the min
-      const int64_t a = static_cast<int64_t>(fv[r]) + static_cast<int64_t>(q - r) * (q - r);
-      int64_t best = a;
-      if (j > 0) {
-        const int r0 = v[j - 1];
-        const int64_t b = static_cast<int64_t>(fv[r0]) + static_cast<int64_t>(q - r0) * (q - r0);
-        best = b < best ? b : best;
-      }
-      if (j < k) {
-        const int r1 = v[j + 1];
-        const int64_t b = static_cast<int64_t>(fv[r1]) + static_cast<int64_t>(q - r1) * (q - r1);
-        best = b < best ? b : best;
-      }
-      d = best >= kCfInf ? kCfInf : static_cast<unsigned>(best);
-    }
-    if (out16)
-      out16[base + q * stride] = static_cast<uint16_t>(d > 65535u ? 65535u : d);
+  unsigned* f = line[wl];
+  for (int q = lane; q < n; q += 32) {
+    if (FIRST)
+      f[q] = static_cast<const uint8_t*>(in_v)[base + q * stride] ? 0u : kCfInf;
     else
-      f[base + q * stride] = d;
+      f[q] = static_cast<const unsigned*>(in_v)[base + q * stride];
+  }
+  __syncwarp();
+  for (int q = lane; q < n; q += 32) {
+    unsigned best = kCfInf;
+    const int r0 = max(0, q - W), r1 = min(n - 1, q + W);
+    for (int r = r0; r <= r1; ++r) {
+      const int d = abs(q - r) - 1;
+      const unsigned c = d > 0 ? static_cast<unsigned>(d * d) : 0u;
+      const unsigned v = f[r] + c;  // f <= kCfInf < 2^30: no overflow
+      best = v < best ? v : best;
+    }
+    // a site farther than W along this axis costs >= W^2 on its own, so
+    // min(window, W^2) never exceeds the true minimum
+    const unsigned lim = static_cast<unsigned>(W * W);
+    const unsigned out = best < lim ? best : lim;
+    if (LAST)
+      static_cast<uint16_t*>(out_v)[base + q * stride] =
+          static_cast<uint16_t>(out > 65535u ? 65535u : out);
+    else
+      static_cast<unsigned*>(out_v)[base + q * stride] = out;
   }
 }
 
@@ -1206,9 +1155,9 @@ ClearanceField grid_clearance_field(const rp_grid* g) {
   rp_ctx* ctx = g->ctx;
   const int dmax = std::max(g->dims[0], std::max(g->dims[1], g->dims[2]));
   int bk = 1;
-  while (dmax > 128 * bk) bk *= 2;  // coarse lines of <= 128 cells
-  require(bk <= 64, RP_E_INTERNAL, "clearance field: grid too large");
+  while (dmax > 64 * bk) bk *= 2;  // coarse lines of <= 64 cells
   ClearanceField f{};
+  if (bk > 64) return f;  // a very elongated grid: no field (d2 = null: nothing skipped)
   f.bk = bk;
   f.ncx = (g->dims[0] + bk - 1) / bk;
   f.ncy = (g->dims[1] + bk - 1) / bk;
@@ -1223,18 +1172,25 @@ ClearanceField grid_clearance_field(const rp_grid* g) {
   cudaStream_t st = ctx->stream;
   if (!g->cf) RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&g->cf), cells * sizeof(uint16_t), st));
   DevBuf<uint8_t> occ(cells, st);
-  DevBuf<unsigned> work(cells, st);
+  DevBuf<unsigned> work(cells, st), work2(cells, st);
   launch(ctx, "clearance", k_cf_occ, dim3(blocks_for(static_cast<int64_t>(cells), 256)), dim3(256),
          0, g->view(), bk, f.ncx, f.ncy, f.ncz, occ.p);
-  launch(ctx, "clearance", k_cf_pass_x, dim3(blocks_for(static_cast<int64_t>(f.ncy) * f.ncz, 64)),
-         dim3(64), 0, static_cast<const uint8_t*>(occ.p), f.ncx, f.ncy, f.ncz, work.p);
-  // y pass: lines over (x, z); z pass: lines over (x, y) -> 16-bit field
-  launch(ctx, "clearance", k_cf_pass, dim3(blocks_for(static_cast<int64_t>(f.ncx) * f.ncz, 64)),
-         dim3(64), 0, work.p, f.ncy, static_cast<int64_t>(f.ncx), f.ncx * f.ncz, int64_t{1},
-         static_cast<int64_t>(f.ncx) * f.ncy, f.ncx, static_cast<uint16_t*>(nullptr));
-  launch(ctx, "clearance", k_cf_pass, dim3(blocks_for(static_cast<int64_t>(f.ncx) * f.ncy, 64)),
-         dim3(64), 0, work.p, f.ncz, static_cast<int64_t>(f.ncx) * f.ncy, f.ncx * f.ncy,
-         int64_t{1}, static_cast<int64_t>(f.ncx), f.ncx, g->cf);
+  // window: distances saturate at W coarse cells (>= 0.6 m: beyond the
+  // default arm's segments plus their sample-cell slack, so every sample is
+  // skippable there; longer segments just skip fewer)
+  const int W = std::min(63, static_cast<int>(std::ceil(0.6 / f.side)) + 1);
+  auto pass = [&](auto kern, const void* in, void* out, int n, int64_t stride, int64_t lines,
+                  int64_t la, int64_t lb, int na) {
+    launch(ctx, "clearance", kern, dim3(blocks_for(lines, 8)), dim3(256), 0, in, out, n, stride,
+           static_cast<int>(lines), la, lb, na, W);
+  };
+  // x: lines over (y, z); y: lines over (x, z); z: lines over (x, y)
+  pass(k_cf_pass<true, false>, occ.p, work.p, f.ncx, 1, static_cast<int64_t>(f.ncy) * f.ncz,
+       static_cast<int64_t>(f.ncx), static_cast<int64_t>(f.ncx) * f.ncy, f.ncy);
+  pass(k_cf_pass<false, false>, work.p, work2.p, f.ncy, f.ncx, static_cast<int64_t>(f.ncx) * f.ncz,
+       1, static_cast<int64_t>(f.ncx) * f.ncy, f.ncx);
+  pass(k_cf_pass<false, true>, work2.p, g->cf, f.ncz, static_cast<int64_t>(f.ncx) * f.ncy,
+       static_cast<int64_t>(f.ncx) * f.ncy, 1, f.ncx, f.ncx);
   g->cf_bk = bk;
   g->cf_nc[0] = f.ncx;
   g->cf_nc[1] = f.ncy;
@@ -1242,6 +1198,68 @@ ClearanceField grid_clearance_field(const rp_grid* g) {
   g->cf_version = g->version;
   f.d2 = g->cf;
   return f;
+}
+
+namespace {
+std::mutex s2_pool_mutex;  // rp_ctx::s2_pool (grids of one context may live on several threads)
+
+void s2_release(const rp_grid* g) {
+  std::lock_guard<std::mutex> lock(s2_pool_mutex);
+  for (auto& e : g->s2) g->ctx->s2_pool.push_back({e.q->n, e.bits, e.ok});
+  g->s2.clear();
+}
+}  // namespace
+
+bool grid_seg2_cache(const rp_grid* g, const rp_quiver* q, const rp_arm& arm, int n,
+                     uint32_t** bits, uint8_t** ok) {
+  // the planner's repeated solves are 8DOF ones on one grid (reach, then
+  // the arbitrary-pose anchor); 6DOF / virtual-arm solves are not cached
+  static const bool off = std::getenv("RP_NO_SEG2_CACHE") != nullptr;
+  if (off || g->exported || q->n > 16384 || arm.n_offsets > 0 || arm.n_segments != 4)
+    return false;
+  std::lock_guard<std::mutex> lock(*g->s2_mutex);
+  if (g->s2_version != g->version) {  // the grid changed: drop every entry
+    s2_release(g);
+    g->s2_version = g->version;
+  }
+  const double key[5] = {arm.root[0], arm.root[1], arm.root[2], arm.lengths[0], arm.lengths[1]};
+  for (auto& e : g->s2)
+    if (e.q == q && e.n == n && std::memcmp(e.key, key, sizeof(key)) == 0) {
+      *bits = e.bits;
+      *ok = e.ok;
+      return true;
+    }
+  if (g->s2.size() >= 4) return false;
+  rp_grid::Seg2Cache e{};
+  std::memcpy(e.key, key, sizeof(key));
+  e.n = n;
+  e.q = q;
+  const size_t W = (q->n + 31) / 32, C = (q->n + 1023) / 1024;
+  {
+    // buffers released by earlier grids of this context, else new ones;
+    // plain (device-wide) allocations: solves on other streams may share them
+    std::lock_guard<std::mutex> plock(s2_pool_mutex);
+    auto& pool = g->ctx->s2_pool;
+    for (size_t k = 0; k < pool.size(); ++k)
+      if (pool[k].q == q->n) {
+        e.bits = pool[k].bits;
+        e.ok = pool[k].ok;
+        pool.erase(pool.begin() + static_cast<long>(k));
+        break;
+      }
+  }
+  if (!e.bits) {
+    RP_CUDA(cudaMalloc(reinterpret_cast<void**>(&e.bits), q->n * W * sizeof(uint32_t)));
+    RP_CUDA(cudaMalloc(reinterpret_cast<void**>(&e.ok), q->n * C));
+  }
+  // reset in this stream's order; the synchronisation makes the reset
+  // visible to solves on the other streams of the context too
+  RP_CUDA(cudaMemsetAsync(e.ok, 0, q->n * C, g->ctx->stream));
+  RP_CUDA(cudaStreamSynchronize(g->ctx->stream));
+  g->s2.push_back(e);
+  *bits = e.bits;
+  *ok = e.ok;
+  return true;
 }
 
 /// mark_obstacles + dilate(radius) for box / cloud obstacles (see file head).
@@ -1757,6 +1775,7 @@ rp_status rp_grid_destroy(rp_grid* g) {
     if (!g) return;
     if (g->bits) RP_CUDA(cudaFreeAsync(g->bits, g->ctx->stream));
     if (g->cf) RP_CUDA(cudaFreeAsync(g->cf, g->ctx->stream));
+    if (!g->s2.empty()) s2_release(g);  // reused by the context's next grids
     delete g;
   });
 }

@@ -10,6 +10,8 @@
 #include <cstdint>
 #include <exception>
 #include <map>
+#include <memory>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -87,6 +89,14 @@ struct rp_ctx {
   std::vector<cudaEvent_t> upload_ev;
   int upload_next = 0;
   int64_t upload_syncs = 0;  // uploads that still had to synchronise (too large)
+  // released segment-2 cache buffers (rp_grid::Seg2Cache) for reuse by the
+  // next grid: {quiver size, bits, ok}
+  struct S2Buf {
+    int q;
+    uint32_t* bits;
+    uint8_t* ok;
+  };
+  std::vector<S2Buf> s2_pool;
 };
 
 namespace rp {
@@ -137,6 +147,18 @@ struct rp_grid {
   mutable uint16_t* cf = nullptr;
   mutable int cf_bk = 0;
   mutable int cf_nc[3] = {0, 0, 0};
+  // Segment-2 clearance cache (grid_seg2_cache): walk verdicts of
+  // [root + L1 q_i, + L2 q_j] shared by the solves on this grid version.
+  struct Seg2Cache {
+    double key[5];  // root xyz, L1, L2
+    int n;
+    const rp_quiver* q;
+    uint32_t* bits;  // [Q][ceil(Q/32)]: bit j of row i = clear
+    uint8_t* ok;     // [Q][ceil(Q/1024)]: row chunk computed
+  };
+  mutable std::vector<Seg2Cache> s2;
+  mutable uint64_t s2_version = ~0ull;
+  mutable std::unique_ptr<std::mutex> s2_mutex = std::make_unique<std::mutex>();
 
   rpd::GridView view() const {
     rpd::GridView v;
@@ -302,8 +324,9 @@ double resolved_near_radius(const rp_arm& a, const rp_reach_params& r);
 /// Lower bound on the distance from any point to the grid's occupied cells:
 /// a squared distance d2[c] (in units of `side`^2) per coarse cell c of
 /// bk^3 voxels, d2 = min over occupied blocks b of sum_i max(0, |c_i-b_i|-1)^2
-/// (UINT16_MAX-ish when the grid is empty). A point p in (or projected onto)
-/// cell c is at least side*sqrt(d2[c]) from every occupied cell.
+/// (saturated at the transform's window). A point p in (or projected onto)
+/// cell c is at least side*sqrt(d2[c]) from every occupied cell. d2 is null
+/// for grids too elongated for the coarse lines (then nothing is skipped).
 struct ClearanceField {
   const uint16_t* d2;
   int bk, ncx, ncy, ncz;
@@ -311,11 +334,21 @@ struct ClearanceField {
 };
 ClearanceField grid_clearance_field(const rp_grid* g);
 
+/// The grid's cache of segment-2 walk verdicts for an arm (root, L1, L2, n)
+/// and quiver: bits[i * ceil(Q/32) + j/32] bit j%32 = walk clear, valid for
+/// row i's chunk c (1024 directions) once ok[i * ceil(Q/1024) + c] != 0.
+/// Walks depend on neither the target nor the rest of the arm
+/// (src/reach_solver.cpp:368), so every solve on this grid version with the
+/// same first two segments reuses them. False when not cacheable.
+bool grid_seg2_cache(const rp_grid* g, const rp_quiver* q, const rp_arm& arm, int n,
+                     uint32_t** bits, uint8_t** ok);
+
 /// side * sqrt(d2) of the coarse cell holding p projected onto the grid box
 /// (projection onto a convex set never increases distances to points in it),
 /// shrunk by 1e-9 relative + 1e-9 m for the fp64 rounding of the cell index.
 __device__ __forceinline__ double cf_distance(const ClearanceField& f, const rpd::GridView& g,
                                               V3 p) {
+  if (!f.d2) return -1.0;  // no field: no sample is proven free
   int c[3];
   const double o[3] = {g.ox, g.oy, g.oz};
   const double pv[3] = {p.x, p.y, p.z};

@@ -377,7 +377,8 @@ __global__ void __launch_bounds__(256, 4) k_seg2_rows(SolveDev a, const SurvDev*
                                                    unsigned long long* ctr, long long* sc_list,
                                                    unsigned* sc_count, BestRec* __restrict__ block_best,
                                                    int* unit_ctr, const uint8_t* __restrict__ kskip,
-                                                   const uint8_t* __restrict__ kend_b) {
+                                                   const uint8_t* __restrict__ kend_b,
+                                                   uint32_t* __restrict__ c2bits, uint8_t* c2ok) {
   unsigned c_lim = 0, c_clear = 0, c_gp = 0, c_jp = 0, c_v3 = 0, c_sol = 0;
   double best_len = 1e308;
   long long best_key = LLONG_MAX;
@@ -405,9 +406,15 @@ __global__ void __launch_bounds__(256, 4) k_seg2_rows(SolveDev a, const SurvDev*
     u = __shfl_sync(FULL, u, 0);
     if (u >= S1 * nchunk) break;
     const int s = u / nchunk;
-    const int jbeg = (u - s * nchunk) * kChunk;
+    const int chunk = u - s * nchunk;
+    const int jbeg = chunk * kChunk;
     const int jend = min(a.Q, jbeg + kChunk);
     const SurvDev& h = sv[s];
+    // segment-2 walk verdicts of this row chunk from an earlier solve on
+    // the same grid (grid_seg2_cache), or computed here and recorded
+    const size_t c2row = static_cast<size_t>(h.i) * ((a.Q + 31) >> 5);
+    uint8_t* const c2flag = c2ok ? c2ok + static_cast<size_t>(h.i) * nchunk + chunk : nullptr;
+    const bool cached = c2flag && __ldcg(c2flag) != 0;
     const V3 p1 = h.p1;
     const V3 s1 = L1 * qvec(a, h.i);
     const int ks = kskip[s];  // leading samples of every segment-2 walk of this row that are free
@@ -455,9 +462,16 @@ __global__ void __launch_bounds__(256, 4) k_seg2_rows(SolveDev a, const SurvDev*
         ++c_lim;
         const V3 dir2 = qvec(a, j);
         const V3 p2 = p1 + L2 * dir2;
-        const int fb = ks >= a.n   ? 0
-                       : kSeg2ParWalk ? rpd::walk_first_blocked_fast_seg_from(a.g, p1, p2, a.n, ks)
-                                      : rpd::walk_first_blocked(a.g, p1, p2, a.n);
+        const int fb =
+            cached ? static_cast<int>(((__ldcg(c2bits + c2row + (j >> 5)) >> (j & 31)) & 1u) ^ 1u)
+            : ks >= a.n     ? 0
+            : kSeg2ParWalk ? rpd::walk_first_blocked_fast_seg_from(a.g, p1, p2, a.n, ks)
+                           : rpd::walk_first_blocked(a.g, p1, p2, a.n);
+        if (c2flag && !cached) {
+          const unsigned cm = __activemask();
+          const unsigned clear = __ballot_sync(cm, fb == 0);
+          if (lane == 0) c2bits[c2row + (j >> 5)] = clear;
+        }
         if (row_near && rpd::may_pass_near(a.target, p1, dir2, L2, rnear) &&
             rpd::point_to_segment(a.target, p1, p2) <= a.near_r + 1e-9) {
           const unsigned pos = atomicAdd(sc_count, 1u);
@@ -485,6 +499,10 @@ __global__ void __launch_bounds__(256, 4) k_seg2_rows(SolveDev a, const SurvDev*
     }
     if (lane < qn) heavy(wq[lane]);
     __syncwarp();
+    if (c2flag && !cached) {  // the chunk's words are written: publish it
+      __threadfence();
+      if (lane == 0) *reinterpret_cast<volatile uint8_t*>(c2flag) = 1;
+    }
   }
   warp_flush(ctr, C_SEG2_LIMIT, c_lim);
   warp_flush(ctr, C_SEG2_CLEAR, c_clear);
@@ -987,11 +1005,14 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
           launch(ctx, "seg2", k_tail_skip, dim3(1), dim3(32), 0, a.g,
                  static_cast<const V3*>(s->bpts.p), 1, L3 + eps, rp.n_samples, cf, kend_b.p);
         }
+        uint32_t* c2bits = nullptr;
+        uint8_t* c2ok = nullptr;
+        if (!grid_seg2_cache(g, q, arm, rp.n_samples, &c2bits, &c2ok)) c2bits = nullptr, c2ok = nullptr;
         auto runr = [&](auto kern) {
           launch(ctx, "seg2", kern, dim3(rblocks), dim3(threads), 0, a,
                  static_cast<const SurvDev*>(s->surv.p), S1, s->sol_bits.p, ctr.p, sc_list.p,
                  sc_count.p, bb.p, unit_ctr.p, static_cast<const uint8_t*>(kskip.p),
-                 static_cast<const uint8_t*>(kend_b.p));
+                 static_cast<const uint8_t*>(kend_b.p), c2bits, c2ok);
         };
         eight ? runr(k_seg2_rows<true>) : runr(k_seg2_rows<false>);
         blocks = rblocks;
