@@ -415,6 +415,9 @@ __global__ void __launch_bounds__(256, 4) k_seg2_rows(SolveDev a, const SurvDev*
     const size_t c2row = static_cast<size_t>(h.i) * ((a.Q + 31) >> 5);
     uint8_t* const c2flag = c2ok ? c2ok + static_cast<size_t>(h.i) * nchunk + chunk : nullptr;
     const bool cached = c2flag && __ldcg(c2flag) != 0;
+    // a cached chunk's 32 words, one per lane (shuffled out per 32 j)
+    const uint32_t c2mine =
+        cached && jbeg + 32 * lane < jend ? __ldcg(c2bits + c2row + (jbeg >> 5) + lane) : 0u;
     const V3 p1 = h.p1;
     const V3 s1 = L1 * qvec(a, h.i);
     const int ks = kskip[s];  // leading samples of every segment-2 walk of this row that are free
@@ -458,12 +461,13 @@ __global__ void __launch_bounds__(256, 4) k_seg2_rows(SolveDev a, const SurvDev*
     for (int j0 = jbeg; j0 < jend; j0 += 32) {
       const int j = j0 + lane;
       bool pass = false;
+      const uint32_t c2w = __shfl_sync(FULL, c2mine, (j0 - jbeg) >> 5);
       if (j < jend) {
         ++c_lim;
         const V3 dir2 = qvec(a, j);
         const V3 p2 = p1 + L2 * dir2;
         const int fb =
-            cached ? static_cast<int>(((__ldcg(c2bits + c2row + (j >> 5)) >> (j & 31)) & 1u) ^ 1u)
+            cached ? static_cast<int>(((c2w >> lane) & 1u) ^ 1u)
             : ks >= a.n     ? 0
             : kSeg2ParWalk ? rpd::walk_first_blocked_fast_seg_from(a.g, p1, p2, a.n, ks)
                            : rpd::walk_first_blocked(a.g, p1, p2, a.n);
