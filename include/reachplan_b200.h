@@ -303,6 +303,26 @@ rp_status rp_backward_endpoints(rp_ctx* ctx, const rp_quiver* q, const double ta
 rp_status rp_span_gap(rp_ctx* ctx, const double p2[3], const double* backward_pts, int32_t n,
                       double L3, double epsilon, double* v3_out, int32_t* idx_out,
                       int32_t* n_out);
+/* [short_reach_scan, src/reach_solver.cpp:176-222] one hypothesis scan:
+   samples (n x 3) with their clear flags (HypothesisScan::samples /
+   sample_clear), prefix (n_prefix x 3, already-cleared segment-1 samples),
+   origin (proximal end). *found = 0: no shortcut. Else *sc gets the hit
+   index, bridge / direct verdict, n_prefix / n_sublength and path_length,
+   and sublength (cap x 3) the sublength samples (the hit prefix of the
+   samples, or the direct origin -> target walk). Bridge and direct walks are
+   collision-checked on the device. */
+/* [select_solution, src/reach_solver.cpp:548-577] on any solution set given
+   as data: segments (n x 3 x 3: s1, s2, s3 of each PoseChain, canonical
+   order) and the shortcuts' path lengths (n_sc). Any shortcut wins (the
+   shortest, first on ties); else the first strict minimum of
+   |s1| + |s2| + |s3|. RP_E_NO_SOLUTION when both are empty. */
+rp_status rp_select_solution_data(rp_ctx* ctx, const double* segments, int64_t n,
+                                  const double* shortcut_lengths, int64_t n_sc, rp_chosen* out);
+rp_status rp_short_reach_scan(rp_ctx* ctx, const rp_grid* g, const rp_arm* arm,
+                              const rp_reach_params* rp, const double target[3],
+                              const double* samples, const uint8_t* sample_clear, int32_t n,
+                              const double* prefix, int32_t n_prefix, const double origin[3],
+                              int32_t* found, rp_shortcut* sc, double* sublength, int32_t cap);
 /* [solve_reach, src/reach_solver.cpp:480-546]; the set stays on the device */
 rp_status rp_solve_reach(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q, const rp_grid* g,
                          const double target[3], const rp_reach_params* rp,

@@ -808,6 +808,127 @@ static void backward_endpoints(rp_ctx* ctx, const rp_quiver* q, V3 target, doubl
 
 /// span_gap (src/reach_solver.cpp:85-98) for one p2 over all backward points:
 /// the same coarse + band test k_seg2 inlines.
+/// select_solution's argmin over data (rp_select_solution_data): per block
+/// the first minimum of its range, then the blocks' in order (strict <, so
+/// the lowest index wins ties, as the reference's sequential scan).
+__global__ void k_select_data(const V3* __restrict__ segs, int64_t n, const double* __restrict__ scl,
+                              int64_t n_sc, BestRec* __restrict__ block_best) {
+  double bl = 1e308;
+  long long bk = LLONG_MAX;
+  const bool sc = n_sc > 0;
+  const int64_t count = sc ? n_sc : n;
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < count;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double len = sc ? scl[k]
+                          : (rpd::norm(segs[3 * k]) + rpd::norm(segs[3 * k + 1])) +
+                                rpd::norm(segs[3 * k + 2]);
+    if (len < bl || (len == bl && k < bk)) {
+      bl = len;
+      bk = k;
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ol = __shfl_down_sync(FULL, bl, off);
+    const long long ok = __shfl_down_sync(FULL, bk, off);
+    if (ol < bl || (ol == bl && ok < bk)) {
+      bl = ol;
+      bk = ok;
+    }
+  }
+  __shared__ BestRec wb[8];
+  if ((threadIdx.x & 31) == 0) wb[threadIdx.x >> 5] = BestRec{bl, bk};
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    BestRec r = wb[0];
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+      if (wb[w].len < r.len || (wb[w].len == r.len && wb[w].key < r.key)) r = wb[w];
+    block_best[blockIdx.x] = r;
+  }
+}
+
+/// short_reach_scan on one HypothesisScan (src/reach_solver.cpp:176-222):
+/// the first sample within near_target_radius + 1e-12 of the target behind a
+/// clear prefix, completed by a collision-checked bridge, else by the direct
+/// origin -> target segment; path_length = polyline_length(root, prefix +
+/// sublength (+ target)) (:157-165). One thread: a scalar chain.
+struct ScanArgs {
+  rpd::GridView g;
+  V3 root, target, origin;
+  double near_r, spacing;
+  const V3* samples;
+  const uint8_t* clear;
+  int n;
+  const V3* prefix;
+  int n_prefix;
+  V3* sub;  // out: sublength samples
+  int sub_cap;
+};
+struct ScanOut {
+  int found, status, hit, has_bridge, via_direct, n_sub;
+  V3 bridge;
+  double path_length;
+};
+
+__global__ void k_short_reach_scan(ScanArgs a, ScanOut* out) {
+  ScanOut r{};
+  int hit = 0;
+  for (int k = 0; k < a.n; ++k) {
+    // loop invariant: samples proximal to k are collision-free
+    if (rpd::norm(a.samples[k] - a.target) <= a.near_r + 1e-12) {
+      hit = k + 1;
+      break;
+    }
+    if (!a.clear[k]) break;
+  }
+  if (hit == 0) {
+    *out = r;
+    return;
+  }
+  r.hit = hit;
+  r.n_sub = hit;
+  for (int k = 0; k < hit; ++k) a.sub[k] = a.samples[k];
+  const V3 hp = a.samples[hit - 1];
+  const double dist = rpd::norm(hp - a.target);
+  if (dist > 1e-9) {
+    const bool bridge_ok =
+        rpd::walk_first_blocked(a.g, hp, a.target, rpd::scaled_sample_count(dist, a.spacing)) == 0;
+    if (bridge_ok) {
+      r.has_bridge = 1;
+      r.bridge = a.target - hp;
+    } else {
+      const double dl = rpd::norm(a.target - a.origin);
+      const int nd = rpd::scaled_sample_count(dl, a.spacing);
+      if (nd > a.sub_cap) {
+        r.status = 1;
+        *out = r;
+        return;
+      }
+      if (rpd::walk_first_blocked(a.g, a.origin, a.target, nd) != 0) {
+        *out = r;  // found = 0
+        return;
+      }
+      r.via_direct = 1;
+      r.n_sub = nd;
+      const V3 dd = a.target - a.origin;
+      for (int k = 1; k <= nd; ++k) a.sub[k - 1] = rpd::walk_sample(a.origin, dd, k, nd);
+    }
+  }
+  double acc = 0.0;
+  V3 prev = a.root;
+  for (int k = 0; k < a.n_prefix; ++k) {
+    acc += rpd::norm(a.prefix[k] - prev);
+    prev = a.prefix[k];
+  }
+  for (int k = 0; k < r.n_sub; ++k) {
+    acc += rpd::norm(a.sub[k] - prev);
+    prev = a.sub[k];
+  }
+  if (r.has_bridge) acc += rpd::norm(a.target - prev);
+  r.path_length = acc;
+  r.found = 1;
+  *out = r;
+}
+
 __global__ void k_span_gap(V3 p2, const V3* __restrict__ bpts, int n, double L3, double eps,
                            V3* __restrict__ v3_out, uint8_t* __restrict__ pass) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1348,6 +1469,85 @@ rp_status rp_backward_endpoints(rp_ctx* ctx, const rp_quiver* q, const double ta
       if (dirs) std::memcpy(dirs + 3 * k, &ds[k], sizeof(V3));
       if (cone_idx) cone_idx[k] = cone[k];
     }
+  });
+}
+
+rp_status rp_select_solution_data(rp_ctx* ctx, const double* segments, int64_t n,
+                                  const double* shortcut_lengths, int64_t n_sc, rp_chosen* out) {
+  return guarded([&] {
+    require(n >= 0 && n_sc >= 0, RP_E_INVALID_PARAMETER, "negative count");
+    require(n + n_sc > 0, RP_E_NO_SOLUTION, "no reach solution under the given constraints");
+    cudaStream_t st = ctx->stream;
+    const int64_t count = n_sc > 0 ? n_sc : n;
+    const int blocks = static_cast<int>(std::min<int64_t>(nblk(count, 256), 4 * ctx->sm_count));
+    DevBuf<V3> ds(n_sc > 0 ? 1 : 3 * n, st);
+    DevBuf<double> dl(std::max<int64_t>(1, n_sc), st);
+    DevBuf<BestRec> bb(blocks, st), best(1, st);
+    if (n_sc > 0)
+      copy_to_device(ctx, dl.p, shortcut_lengths, n_sc * sizeof(double));
+    else
+      copy_to_device(ctx, ds.p, segments, 3 * n * sizeof(V3));
+    launch(ctx, "select", k_select_data, dim3(blocks), dim3(256), 0, static_cast<const V3*>(ds.p), n,
+           static_cast<const double*>(dl.p), n_sc, bb.p);
+    launch(ctx, "select", k_best_final, dim3(1), dim3(256), 0, static_cast<const BestRec*>(bb.p),
+           blocks, best.p);
+    BestRec h{};
+    copy_to_host(ctx, &h, best.p, sizeof(h));
+    out->kind = n_sc > 0 ? RP_CHOSEN_SHORTCUT : RP_CHOSEN_REACH_POSE;
+    out->index = h.key;
+    out->path_length = h.len;
+  });
+}
+
+rp_status rp_short_reach_scan(rp_ctx* ctx, const rp_grid* g, const rp_arm* arm,
+                              const rp_reach_params* rp, const double target[3],
+                              const double* samples, const uint8_t* sample_clear, int32_t n,
+                              const double* prefix, int32_t n_prefix, const double origin[3],
+                              int32_t* found, rp_shortcut* sc, double* sublength, int32_t cap) {
+  return guarded([&] {
+    require(n >= 0 && n_prefix >= 0, RP_E_INVALID_PARAMETER, "negative sample count");
+    require(g->ctx == ctx, RP_E_INVALID_PARAMETER, "grid belongs to another context");
+    *found = 0;
+    if (n == 0) return;
+    cudaStream_t st = ctx->stream;
+    const int nd_max = 1 << 16;  // direct walks: scaled_sample_count(|target - origin|, spacing)
+    DevBuf<V3> ds(n, st), dp(std::max(1, n_prefix), st), sub(std::max(n, 1) + nd_max, st);
+    DevBuf<uint8_t> dc(n, st);
+    DevBuf<ScanOut> out(1, st);
+    copy_to_device(ctx, ds.p, samples, n * sizeof(V3));
+    copy_to_device(ctx, dc.p, sample_clear, n);
+    if (n_prefix) copy_to_device(ctx, dp.p, prefix, n_prefix * sizeof(V3));
+    ScanArgs a{};
+    a.g = g->view();
+    a.root = V3{arm->root[0], arm->root[1], arm->root[2]};
+    a.target = V3{target[0], target[1], target[2]};
+    a.origin = V3{origin[0], origin[1], origin[2]};
+    a.near_r = resolved_near_radius(*arm, *rp);
+    a.spacing = nominal_spacing(*arm, *rp);
+    a.samples = ds.p;
+    a.clear = dc.p;
+    a.n = n;
+    a.prefix = dp.p;
+    a.n_prefix = n_prefix;
+    a.sub = sub.p;
+    a.sub_cap = std::max(n, 1) + nd_max;
+    launch(ctx, "shortcuts", k_short_reach_scan, dim3(1), dim3(1), 0, a, out.p);
+    ScanOut h{};
+    copy_to_host(ctx, &h, out.p, sizeof(h));
+    if (h.status) fail(RP_E_CAPACITY_EXCEEDED, "short_reach_scan: direct walk too long");
+    if (!h.found) return;
+    require(h.n_sub <= cap, RP_E_CAPACITY_EXCEEDED, "sublength buffer too small");
+    copy_to_host(ctx, sublength, sub.p, h.n_sub * sizeof(V3));
+    sc->segment_index = 1;
+    sc->hit_sample_index = h.hit;
+    sc->seg1_index = sc->seg2_index = -1;
+    sc->has_bridge = h.has_bridge;
+    sc->via_origin_direct = h.via_direct;
+    sc->n_prefix = n_prefix;
+    sc->n_sublength = h.n_sub;
+    std::memcpy(sc->bridge, &h.bridge, sizeof(V3));
+    sc->path_length = h.path_length;
+    *found = 1;
   });
 }
 

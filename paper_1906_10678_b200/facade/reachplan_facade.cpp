@@ -18,8 +18,9 @@
 // Covered (reference declaration -> here): build_grid, mark_obstacles,
 // dilate, point_clear, segment_clear, VoxelGrid::occupied_count
 // (voxgrid.hpp:60-84); generate_quiver, cone_subset (quiver.hpp:38-49);
-// backward_endpoints, prune_segment1 (survivor indices and stats), span_gap,
-// solve_reach, select_solution (reach_solver.hpp:45-165);
+// backward_endpoints, prune_segment1 (survivors, stats and the
+// near-encounter scan), span_gap, solve_reach, short_reach_scan,
+// select_solution (reach_solver.hpp:45-165);
 // exact_refine_6dof / _8dof / _8dof_triangle (arm_model.hpp:92-107);
 // smoothness_ok, waypoint_ik, plan_from_reach, plan_arbitrary,
 // replan_dynamic, plan_reach_then_path, folded_pose,
@@ -224,9 +225,27 @@ std::vector<double> flat(const std::vector<Vec3>& v) {
 // ---- per-thread device runtime -------------------------------------------------
 
 uint64_t mix_bytes(const void* data, std::size_t n, uint64_t h) {
-  // 64-bit multiply-xorshift over 8-byte words (content identity, not crypto)
+  // 64-bit multiply-xorshift (content identity, not crypto): four
+  // independent lanes over 32-byte blocks so the multiplies overlap (~4x the
+  // single-chain rate on a 16 MiB grid), then the lanes and the tail
   const auto* b = static_cast<const unsigned char*>(data);
   std::size_t k = 0;
+  uint64_t l[4] = {h, h ^ 0x243F6A8885A308D3ull, h ^ 0x13198A2E03707344ull,
+                   h ^ 0xA4093822299F31D0ull};
+  for (; k + 32 <= n; k += 32) {
+    uint64_t w[4];
+    std::memcpy(w, b + k, 32);
+    for (int q = 0; q < 4; ++q) {
+      l[q] ^= w[q];
+      l[q] *= 0x9E3779B97F4A7C15ull;
+      l[q] ^= l[q] >> 29;
+    }
+  }
+  for (int q = 0; q < 4; ++q) {
+    h ^= l[q];
+    h *= 0x9E3779B97F4A7C15ull;
+    h ^= h >> 29;
+  }
   for (; k + 8 <= n; k += 8) {
     uint64_t w;
     std::memcpy(&w, b + k, 8);
@@ -627,8 +646,6 @@ std::vector<Seg1Hypothesis> prune_segment1(const ArmSpec& spec, const Quiver& q,
   // near-encounter sink are not exposed through this façade.
   require(!spec.has_offsets(), Errc::invalid_parameter,
           "façade prune_segment1 covers coaxial arms (use solve_reach)");
-  require(shortcut_sink == nullptr && scan_target == nullptr, Errc::invalid_parameter,
-          "façade prune_segment1 does not run the near-encounter scan");
   const rp_arm arm = to_rp(spec);
   const rp_reach_params rp = to_rp(params);
   const std::vector<double> tp = flat(target_points);
@@ -645,8 +662,68 @@ std::vector<Seg1Hypothesis> prune_segment1(const ArmSpec& spec, const Quiver& q,
     stats->seg1_reach_pass += s.seg1_reach_pass;
     stats->seg1_survivors += s.seg1_survivors;
   }
-  std::vector<Seg1Hypothesis> out;
   const int ns = params.n_samples_per_segment;
+  if (shortcut_sink && scan_target) {
+    // The near-encounter scan (reach_solver.cpp:277-291) over every
+    // hypothesis whose segment passes within near_target_radius of the
+    // target: their walks' per-sample clearance from one batched device
+    // point_clear, each scan by rp_short_reach_scan on the device.
+    const double near = params.resolved_near_radius(spec);
+    const double L1 = spec.length(0);
+    std::vector<int> cand;
+    std::vector<double> pts;
+    for (int i = 0; i < q.size(); ++i) {
+      const Vec3 p1 = spec.root + L1 * q.vectors[i];
+      const Vec3 ab = p1 - spec.root;  // point_to_segment (reach_solver.cpp:135-141)
+      const double len2 = ab.squaredNorm();
+      double d;
+      if (len2 <= 1e-30) {
+        d = (*scan_target - spec.root).norm();
+      } else {
+        const double t = std::clamp((*scan_target - spec.root).dot(ab) / len2, 0.0, 1.0);
+        d = (*scan_target - (spec.root + t * ab)).norm();
+      }
+      if (!(d <= near + 1e-9)) continue;
+      cand.push_back(i);
+      for (int m = 1; m <= ns; ++m) {
+        const Vec3 smp = spec.root + (static_cast<double>(m) / ns) * ab;
+        pts.push_back(smp.x());
+        pts.push_back(smp.y());
+        pts.push_back(smp.z());
+      }
+    }
+    std::vector<uint8_t> clear(pts.size() / 3);
+    if (!clear.empty())
+      ok(rp_grid_point_clear(rt().grid(grid), pts.data(), static_cast<int64_t>(clear.size()),
+                             clear.data()));
+    const rp_arm arm1 = to_rp(spec);
+    const rp_reach_params rp1 = to_rp(params);
+    double tgt[3];
+    put3(tgt, *scan_target);
+    for (std::size_t c = 0; c < cand.size(); ++c) {
+      // the walk stops at its first blocked sample (walk_segment_into)
+      int m = 0;
+      while (m < ns && clear[c * ns + m]) ++m;
+      const int len = m < ns ? m + 1 : ns;
+      HypothesisScan scan;
+      scan.segment_index = 1;
+      scan.origin = spec.root;
+      for (int k = 0; k < len; ++k) {
+        scan.samples.push_back(get3(&pts[3 * (c * ns + k)]));
+        scan.sample_clear.push_back(clear[c * ns + k]);
+      }
+      scan.basis_pose = chain_from_segments(spec, {L1 * q.vectors[cand[c]]}, {cand[c]});
+      scan.seg1_index = cand[c];
+      if (auto hit = short_reach_scan(scan, *scan_target, grid, spec, params)) {
+        shortcut_sink->push_back(std::move(hit->shortcut));
+        if (stats) ++stats->shortcuts_found;
+      }
+    }
+    (void)arm1;
+    (void)rp1;
+    (void)tgt;
+  }
+  std::vector<Seg1Hypothesis> out;
   for (int k = 0; k < n; ++k) {
     Seg1Hypothesis h;
     h.quiver_index = idx[k];
@@ -660,12 +737,30 @@ std::vector<Seg1Hypothesis> prune_segment1(const ArmSpec& spec, const Quiver& q,
 }
 
 ChosenPath select_solution(const SolutionSet& set) {
-  require(!set.empty(), Errc::no_solution, "solution set is empty");
+  require(!set.empty(), Errc::no_solution, "no reach solution under the given constraints");
   rp_solution_set* d = rt().lookup(set);
-  require(d != nullptr, Errc::invalid_parameter,
-          "solution set was not produced by this library's solve_reach");
   rp_chosen c;
-  ok(rp_select_solution(d, &c));
+  if (d) {
+    ok(rp_select_solution(d, &c));
+  } else {
+    // any other set: its segment vectors / shortcut lengths go to the
+    // device argmin (rp_select_solution_data)
+    std::vector<double> segs, scl;
+    if (set.shortcuts.empty()) {
+      segs.reserve(9 * set.solutions.size());
+      for (const PoseChain& p : set.solutions)
+        for (int k = 0; k < 3; ++k) {
+          segs.push_back(p.segments[k].x());
+          segs.push_back(p.segments[k].y());
+          segs.push_back(p.segments[k].z());
+        }
+    } else {
+      for (const ShortcutPath& sp : set.shortcuts) scl.push_back(sp.path_length);
+    }
+    ok(rp_select_solution_data(rt().ctx(), segs.data(),
+                               static_cast<int64_t>(set.shortcuts.empty() ? set.solutions.size() : 0),
+                               scl.data(), static_cast<int64_t>(scl.size()), &c));
+  }
   ChosenPath out;
   out.path_length = c.path_length;
   if (c.kind == RP_CHOSEN_SHORTCUT) {
@@ -1035,11 +1130,44 @@ ReachParams reach_params_for_scene(ReachParams rp, const Scene& scene, const Arm
   return rp;
 }
 
-std::optional<ShortReachHit> short_reach_scan(const HypothesisScan&, const Vec3&, const VoxelGrid&,
-                                              const ArmSpec&, const ReachParams&) {
-  // the near-encounter scan runs inside solve_reach on the device
-  // (k_seg1 / k_seg2 + k_shortcuts); it has no stand-alone host entry point
-  fail(Errc::invalid_parameter, "short_reach_scan is fused into solve_reach in reachplan-b200");
+std::optional<ShortReachHit> short_reach_scan(const HypothesisScan& hyp, const Vec3& target,
+                                              const VoxelGrid& grid, const ArmSpec& spec,
+                                              const ReachParams& params) {
+  // the scan, its bridge / direct walks and the path length on the device
+  // (rp_short_reach_scan); inside solve_reach the same scan is fused into
+  // k_seg1 / k_seg2 + k_shortcuts
+  const rp_arm arm = to_rp(spec);
+  const rp_reach_params rp = to_rp(params);
+  const std::vector<double> smp = flat(hyp.samples), pre = flat(hyp.prefix_samples);
+  double t[3], org[3];
+  put3(t, target);
+  put3(org, hyp.origin);
+  const int n = static_cast<int>(hyp.samples.size());
+  require(hyp.sample_clear.size() >= hyp.samples.size(), Errc::invalid_parameter,
+          "sample_clear shorter than samples");
+  int32_t found = 0;
+  rp_shortcut sc{};
+  const double len = (target - hyp.origin).norm();
+  const int cap = n + std::max(1, static_cast<int>(std::ceil(len / std::max(
+                                   1e-12, params.nominal_spacing(spec))))) + 1;
+  std::vector<double> sub(3 * static_cast<std::size_t>(cap));
+  ok(rp_short_reach_scan(rt().ctx(), rt().grid(grid), &arm, &rp, t, smp.data(),
+                         hyp.sample_clear.data(), n, pre.data(),
+                         static_cast<int32_t>(hyp.prefix_samples.size()), org, &found, &sc,
+                         sub.data(), cap));
+  if (!found) return std::nullopt;
+  ShortcutPath p;
+  p.segment_index = hyp.segment_index;
+  p.hit_sample_index = sc.hit_sample_index;
+  p.prefix_samples = hyp.prefix_samples;
+  for (int k = 0; k < sc.n_sublength; ++k) p.sublength_samples.push_back(get3(&sub[3 * k]));
+  if (sc.has_bridge) p.bridge = get3(sc.bridge);
+  p.via_origin_direct = sc.via_origin_direct != 0;
+  p.basis_pose = hyp.basis_pose;
+  p.seg1_index = hyp.seg1_index;
+  p.seg2_index = hyp.seg2_index;
+  p.path_length = sc.path_length;
+  return ShortReachHit{sc.hit_sample_index, std::move(p)};
 }
 
 }  // namespace reachplan

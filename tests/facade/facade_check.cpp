@@ -146,6 +146,39 @@ int main(int argc, char** argv) {
     const std::vector<GapCandidate> gaps =
         span_gap(chosen.pose.joints[2], be.points, arm.length(2), rp.resolved_epsilon(arm));
     const SegmentProbe probe = segment_clear(grid, arm.root, scene.target, 8);
+    // backward endpoints of a 0.25 rad approach cone, and span_gap over them
+    const BackwardEndpoints cone =
+        backward_endpoints(scene.target, arm.lengths.back(), q, rp.approach_axis, 0.25, rp.mode);
+    const std::vector<GapCandidate> cone_gaps =
+        span_gap(chosen.pose.joints[2], cone.points, arm.length(2), rp.resolved_epsilon(arm));
+    // prune_segment1 with the near-encounter scan (short_reach_scan) towards
+    // a point 0.3 m out along the chosen segment-1 direction
+    const Vec3 scan_t = arm.root + 0.3 * chosen.pose.segments[0].normalized() + Vec3(0.004, -0.003, 0.002);
+    std::vector<ShortcutPath> sink;
+    SolveStats s1st;
+    const std::vector<Seg1Hypothesis> surv =
+        prune_segment1(arm, q, grid, {scene.target}, rp, &sink, &s1st, &scan_t);
+    // select_solution on sets this library did not produce: the solutions
+    // in reverse order (first 400), and the scan's shortcuts
+    SolutionSet rev;
+    for (std::size_t k = set.solutions.size(); k-- > 0 && rev.solutions.size() < 400;)
+      rev.solutions.push_back(set.solutions[k]);
+    const ChosenPath crev = select_solution(rev);
+    SolutionSet scs;
+    scs.shortcuts = sink;
+    std::string csc = "null";
+    if (!sink.empty()) {
+      const ChosenPath c = select_solution(scs);
+      csc = "{\"seg1\":" + std::to_string(c.shortcut.seg1_index) + ",\"path_length\":" +
+            num(c.path_length) + "}";
+    }
+    const auto shortcut = [](const ShortcutPath& sp) {
+      return "{\"seg1\":" + std::to_string(sp.seg1_index) + ",\"hit\":" +
+             std::to_string(sp.hit_sample_index) + ",\"bridge\":" + (sp.bridge ? "1" : "0") +
+             ",\"direct\":" + (sp.via_origin_direct ? "1" : "0") + ",\"n_sub\":" +
+             std::to_string(sp.sublength_samples.size()) + ",\"path_length\":" +
+             num(sp.path_length) + ",\"tip\":" + list(sp.tip_waypoints(Vec3::Zero()), vec) + "}";
+    };
     if (argc > 2) {
       // the plan file the reference CLI writes for `plan` (cli.cpp:126-137,
       // 167-185), from the façade's results and the reference's writer
@@ -178,6 +211,17 @@ int main(int argc, char** argv) {
               << ",\"chosen\":{\"kind\":" << (chosen.kind == ChosenPath::Kind::shortcut ? 1 : 0)
               << ",\"path_length\":" << num(chosen.path_length) << ",\"pose\":" << pose(chosen.pose)
               << "},\"span_gap\":" << gaps.size()
+              << ",\"cone\":{\"points\":" << list(cone.points, vec)
+              << ",\"idx\":" << list(cone.cone_indices, [](int i) { return std::to_string(i); })
+              << "},\"cone_gaps\":"
+              << list(cone_gaps, [](const GapCandidate& g) {
+                   return "[" + std::to_string(g.backward_index) + "," + vec(g.v3) + "]";
+                 })
+              << ",\"scan\":{\"target\":" << vec(scan_t) << ",\"survivors\":" << surv.size()
+              << ",\"stats\":" << stats(s1st) << ",\"shortcuts\":" << list(sink, shortcut)
+              << "},\"select_rev\":{\"qidx\":"
+              << list(crev.pose.quiver_indices, [](int i) { return std::to_string(i); })
+              << ",\"path_length\":" << num(crev.path_length) << "},\"select_sc\":" << csc
               << ",\"mean_dev\":"
               << (p1.waypoints.empty() || p3.waypoints.empty()
                       ? std::string("null")

@@ -99,3 +99,30 @@ def test_facade_matches_reference(tmp_path, name, deg):
         dev = ref.mean_polyline_deviation(np.array(js["plan"]["waypoints"]),
                                           np.array(js["arbitrary"]["waypoints"]))
         assert js["mean_dev"] == dev
+
+
+BIN_REF = os.path.join(ROOT, "tests", "facade", "_build", "facade_check_ref")
+
+
+@pytest.mark.skipif(not os.path.exists(BIN_REF), reason="reference-linked check not built")
+@pytest.mark.parametrize("name,deg", [("C2", 5.0), ("C1", 10.0)])
+def test_facade_equals_reference_linked_caller(tmp_path, name, deg):
+    """The same reference-style caller linked once against the façade and
+    once against the unmodified reference: every printed result is equal,
+    including backward_endpoints with a cone, span_gap over it,
+    prune_segment1 with the near-encounter scan (short_reach_scan), and
+    select_solution on sets the library did not produce (reach_solver.cpp:
+    54-98, 176-300, 548-577)."""
+    sc = scenes.config(name, quiver_deg=deg)
+    scene = _scene_file(tmp_path, sc)
+    outs = []
+    for b in (BIN, BIN_REF):
+        r = subprocess.run([b, scene], capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stderr
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    got, want = outs
+    assert "error" not in want, want
+    assert set(got) == set(want)
+    for key in want:
+        assert got[key] == want[key], key
+    assert want["scan"]["shortcuts"], "the scan target should produce shortcuts"
