@@ -245,6 +245,12 @@ rp_status rp_grid_mark_dilate_slab(rp_grid* g, const rp_obstacle* obs, int32_t n
                                    int32_t z0, int32_t z1);
 /* Device pointer of the bit words (for collectives over the grid, e.g. an
  * all-gather of z-slabs); plane z = words [z*words_per_plane, +words_per_plane). */
+/* z-slab step of a partitioned dilate (src/voxgrid.cpp:64-92): planes
+   z0..z1 are dilated from the current occupancy of planes z0-R..z1+R (R =
+   floor(radius/voxel_size + 1e-9): the caller's own slab plus the halo
+   planes exchanged with its neighbours); other planes keep their words.
+   The grid records dilation_radius = radius. z1 = z0 - 1: no planes. */
+rp_status rp_grid_dilate_slab(rp_grid* g, double radius, int32_t z0, int32_t z1);
 rp_status rp_grid_device_bits(rp_grid* g, void** bits, uint64_t* n_words,
                               uint64_t* words_per_plane);
 /* Benchmark helper: the fused mark + dilate of `obs` onto g (overwriting it)

@@ -78,6 +78,7 @@ def lib():
         "rp_grid_occupied_count": ([vp, P(C.c_uint64)], C.c_int32),
         "rp_grid_point_clear": ([vp, vp, C.c_int64, vp], C.c_int32),
         "rp_grid_clearance": ([vp, vp, C.c_int64, vp], C.c_int32),
+        "rp_grid_dilate_slab": ([vp, C.c_double, C.c_int32, C.c_int32], C.c_int32),
         "rp_grid_segment_clear": ([vp, vp, vp, C.c_int64, C.c_int32, vp], C.c_int32),
         "rp_grid_copy": ([vp, P(vp)], C.c_int32),
         "rp_grid_destroy": ([vp], C.c_int32),
@@ -286,6 +287,11 @@ class Grid(_Owned):
     def mark_dilate(self, obstacles, radius):
         _check(lib().rp_grid_mark_dilate_boxes(self.h, abi.obstacle_array(obstacles),
                                                len(obstacles), radius))
+
+    def dilate_slab(self, radius, z0, z1):
+        """Dilate planes z0..z1 from planes z0-R..z1+R (halo exchanged by the
+        caller); the other planes keep their words."""
+        _check(lib().rp_grid_dilate_slab(self.h, radius, z0, z1))
 
     def mark_dilate_slab(self, obstacles, radius, z0, z1):
         """Planes z0..z1 (inclusive) of the fused mark + dilate (z-slab build)."""

@@ -862,9 +862,12 @@ __device__ uint64_t xdilate_any(const uint64_t* __restrict__ row, int wx, int nx
 /// OR over row offsets (dy, dz) of the source row x-dilated by wtab.
 __global__ void __launch_bounds__(256) k_dilate_general(const uint64_t* __restrict__ in,
                                                         uint64_t* __restrict__ out, GridView g,
-                                                        const int* __restrict__ wtab, int reach) {
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t total = static_cast<int64_t>(g.nz) * g.ny * g.wx;
+                                                        const int* __restrict__ wtab, int reach,
+                                                        int z0, int z1) {
+  // output planes z0..z1 (reading z0 - reach .. z1 + reach)
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x +
+                    static_cast<int64_t>(z0) * g.ny * g.wx;
+  const int64_t total = static_cast<int64_t>(z1 + 1) * g.ny * g.wx;
   if (t >= total) return;
   const int ww = static_cast<int>(t % g.wx);
   const int64_t row = t / g.wx;
@@ -1112,17 +1115,26 @@ void mark_prims(rp_grid* g, const Prim* prims, int64_t nb, int64_t np, const cha
   if (np > 0) g->empty = false;
 }
 
-void dilate_general(rp_grid* g, double radius) {
+/// dilate (src/voxgrid.cpp:64-92) of the whole occupancy, or only of the
+/// planes z0..z1 (the other planes keep their occupancy): out of place, so
+/// every output word reads the pre-dilation snapshot like the reference.
+void dilate_general(rp_grid* g, double radius, int z0 = 0, int z1 = -1) {
   rp_ctx* ctx = g->ctx;
+  if (z1 < 0) z1 = g->dims[2] - 1;
   const DilTable t = make_table(radius, g->voxel_size);
   DevBuf<int> wtab(t.w.size(), ctx->stream);
   copy_to_device(ctx, wtab.p, t.w.data(), t.w.size() * sizeof(int));
   uint64_t* out = nullptr;
   RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&out), g->n_words * sizeof(uint64_t) + 8,
                           ctx->stream));
-  launch(ctx, "dilate", k_dilate_general, dim3(blocks_for(static_cast<int64_t>(g->n_words), 256)),
-         dim3(256), 0, static_cast<const uint64_t*>(g->bits), out, g->view(),
-         static_cast<const int*>(wtab.p), t.reach);
+  const bool all = z0 == 0 && z1 == g->dims[2] - 1;
+  if (!all)
+    RP_CUDA(cudaMemcpyAsync(out, g->bits, g->n_words * sizeof(uint64_t), cudaMemcpyDeviceToDevice,
+                            ctx->stream));
+  const int64_t words = static_cast<int64_t>(z1 - z0 + 1) * g->dims[1] * g->wx;
+  launch(ctx, "dilate", k_dilate_general, dim3(blocks_for(words, 256)), dim3(256), 0,
+         static_cast<const uint64_t*>(g->bits), out, g->view(), static_cast<const int*>(wtab.p),
+         t.reach, z0, z1);
   RP_CUDA(cudaFreeAsync(g->bits, ctx->stream));
   g->bits = out;
 }
@@ -1391,6 +1403,18 @@ rp_status rp_grid_mark_dilate_slab(rp_grid* g, const rp_obstacle* obs, int32_t n
     if (!hp.empty()) g->empty = false;
     g->dilation_radius = radius;
     ++g->version;
+  });
+}
+
+rp_status rp_grid_dilate_slab(rp_grid* g, double radius, int32_t z0, int32_t z1) {
+  return guarded([&] {
+    require(radius >= 0.0, RP_E_INVALID_PARAMETER, "dilation radius must be >= 0");
+    require(0 <= z0 && z0 <= z1 + 1 && z1 < g->dims[2], RP_E_INVALID_PARAMETER,
+            "slab out of range");
+    ++g->version;
+    if (radius != 0.0 && z0 <= z1) dilate_general(g, radius, z0, z1);
+    g->dilation_radius = radius;
+    g->empty = false;
   });
 }
 

@@ -141,3 +141,78 @@ def build_grid_sharded(ctx, bmin, bmax, voxel_size, obstacles, radius, rank: int
         import torch
         torch.cuda.synchronize()
     return g
+
+
+# ---- z-slab dilation of a partitioned occupancy (halo exchange) ----------------
+
+def halo_plan(nz: int, reach: int, world: int):
+    """The plane transfers of a z-slab dilation: rank d needs planes
+    [lo_d - R, hi_d + R) ∩ [0, nz) and owns [lo_d, hi_d) (shard_range). Returns
+    [(src, dst, z0, z1)]: src sends its planes z0..z1-1 to dst (a slab
+    thinner than R takes halo planes from several ranks)."""
+    out = []
+    for d in range(world):
+        lo, hi = shard_range(nz, d, world)
+        need_lo, need_hi = max(0, lo - reach), min(nz, hi + reach)
+        for s in range(world):
+            if s == d:
+                continue
+            slo, shi = shard_range(nz, s, world)
+            a, b = max(slo, need_lo), min(shi, need_hi)
+            if a < b:
+                out.append((s, d, a, b))
+    return out
+
+
+def exchange_halos(words, words_per_plane: int, nz: int, reach: int, rank: int, world: int):
+    """Point-to-point exchange of the halo planes (NCCL send/recv over
+    NVLink on GPUs, gloo on CPU): afterwards this rank's buffer holds every
+    plane within `reach` of its slab. `words` is the full-size 1-D tensor of
+    the grid's uint64 words (own slab valid)."""
+    import torch
+    import torch.distributed as dist
+
+    if world == 1:
+        return words
+    flat = words.view(torch.int64)
+    ops = []
+    for s, d, a, b in halo_plan(nz, reach, world):
+        seg = flat[a * words_per_plane: b * words_per_plane]
+        if s == rank:
+            ops.append(dist.P2POp(dist.isend, seg.contiguous(), d))
+        elif d == rank:
+            ops.append(dist.P2POp(dist.irecv, seg, s))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    return words
+
+
+def dilate_grid_sharded(ctx, grid, radius: float, rank: int, world: int):
+    """dilate (src/voxgrid.cpp:64-92) of a grid whose occupancy is
+    partitioned in z-slabs (rank r holds the marked planes
+    shard_range(nz, r, world); any occupancy: boxes, clouds, uploaded
+    sensor slabs): halo exchange of R = floor(radius/vs + 1e-9) planes with
+    the neighbours, dilation of the own slab on the device
+    (rp_grid_dilate_slab), then the slab all-gather, so every rank holds
+    the dilated grid, bit-identical to a single-GPU dilate."""
+    import math
+
+    dims, _, vs, _ = grid.info()
+    nz = dims[2]
+    reach = int(math.floor(radius / vs + 1e-9))
+    lo, hi = shard_range(nz, rank, world)
+    if world > 1:
+        import torch
+        words, wpp = grid.device_words()
+        ctx.synchronize()
+        exchange_halos(words, wpp, nz, reach, rank, world)
+        torch.cuda.synchronize()
+    grid.dilate_slab(radius, lo, hi - 1)
+    if world > 1:
+        words, wpp = grid.device_words()
+        ctx.synchronize()
+        gather_slabs(words, wpp, nz, rank, world)
+        import torch
+        torch.cuda.synchronize()
+    return grid

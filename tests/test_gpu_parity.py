@@ -306,3 +306,41 @@ def test_zslab_build_equals_full_build(ctx, world):
         assert not b[:lo * wpp].any() and not b[hi * wpp:].any()  # other planes untouched
         got[lo * wpp:hi * wpp] = b[lo * wpp:hi * wpp]
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_zslab_dilation_with_halos_equals_reference(ctx, world):
+    """A partitioned occupancy (boxes + a 600-point cloud, each rank holding
+    only its z-slab's marked planes): halo planes moved as shard.halo_plan
+    says (the NCCL send/recv of shard.exchange_halos, emulated between the
+    ranks' buffers here), each rank's slab dilated on the device
+    (rp_grid_dilate_slab), the slabs assembled: equal to the reference's
+    mark + dilate of the whole grid."""
+    api = _api()
+    from paper_1906_10678_b200 import shard
+    rng = np.random.default_rng(29)
+    cloud, buf = _cloud(rng.uniform(-0.9, 1.0, (600, 3)))
+    bmin, bmax, vs, r = (-1, -1, -1), (1.1, 1.05, 1.0), 0.0205, 0.095
+    obs = [abi.box((-0.5, -0.4, -0.45), (0.1, 0.2, 0.3)), cloud]
+    dims, marked = ref.grid_ops(bmin, bmax, vs, obs, 0.0)
+    _, want = ref.grid_ops(bmin, bmax, vs, obs, r)
+    nx, ny, nz = dims
+    reach = int(np.floor(r / vs + 1e-9))
+    plane = nx * ny
+    # each rank's buffer: its own marked planes only
+    bufs = []
+    for k in range(world):
+        lo, hi = shard.shard_range(nz, k, world)
+        b = np.zeros_like(marked)
+        b[lo * plane:hi * plane] = marked[lo * plane:hi * plane]
+        bufs.append(b)
+    for s, d, a, b in shard.halo_plan(nz, reach, world):
+        bufs[d][a * plane:b * plane] = bufs[s][a * plane:b * plane]
+    got = np.zeros_like(marked)
+    for k in range(world):
+        lo, hi = shard.shard_range(nz, k, world)
+        g = api.Grid.from_u8(ctx, bmin, vs, dims, bufs[k])
+        g.dilate_slab(r, lo, hi - 1)
+        assert g.info()[3] == r
+        got[lo * plane:hi * plane] = g.to_u8()[lo * plane:hi * plane]
+    assert np.array_equal(got, want)

@@ -126,3 +126,64 @@ def test_gather_slabs_two_gloo_ranks(nz):
     want = np.concatenate([np.arange(wpp) + 1000 * (z + 1) for z in range(nz)]).astype(np.int64)
     for r in range(world):
         assert got[r] == want.tobytes()
+
+
+@pytest.mark.parametrize("nz,reach,world", [(16, 3, 2), (16, 5, 3), (7, 4, 3), (9, 2, 4),
+                                            (5, 0, 2)])
+def test_halo_plan_covers_every_needed_plane(nz, reach, world):
+    """Every plane within `reach` of a rank's slab arrives exactly once from
+    its owner; nothing else is sent."""
+    plan = shard.halo_plan(nz, reach, world)
+    for d in range(world):
+        lo, hi = shard.shard_range(nz, d, world)
+        need = set(range(max(0, lo - reach), min(nz, hi + reach))) - set(range(lo, hi))
+        got = []
+        for s, dd, a, b in plan:
+            if dd != d:
+                continue
+            slo, shi = shard.shard_range(nz, s, world)
+            assert slo <= a < b <= shi  # only owned planes are sent
+            got.extend(range(a, b))
+        assert sorted(got) == sorted(need)
+
+
+def _halo_worker(rank, world, port, nz, wpp, reach, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        words = torch.zeros(nz * wpp, dtype=torch.int64)
+        lo, hi = shard.shard_range(nz, rank, world)
+        for z in range(lo, hi):
+            words[z * wpp:(z + 1) * wpp] = torch.arange(wpp) + 1000 * (z + 1)
+        shard.exchange_halos(words, wpp, nz, reach, rank, world)
+        q.put((rank, words.numpy().tobytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("nz,reach", [(12, 2), (5, 3)])
+def test_exchange_halos_two_gloo_ranks(nz, reach):
+    """z-slab dilation halos over point-to-point send/recv (gloo here, NCCL
+    on GPUs): each rank ends with its slab plus the R planes on each side,
+    and nothing beyond."""
+    world, wpp = 2, 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, world, port, nz, wpp, reach, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        lo, hi = shard.shard_range(nz, r, world)
+        arr = np.frombuffer(got[r], np.int64).reshape(nz, wpp)
+        for z in range(nz):
+            have = max(0, lo - reach) <= z < min(nz, hi + reach)
+            want = np.arange(wpp) + 1000 * (z + 1) if have else np.zeros(wpp, np.int64)
+            assert np.array_equal(arr[z], want), (r, z)
