@@ -16,6 +16,7 @@
 #include "rp_internal.hpp"
 
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -50,6 +51,10 @@ DilTable make_table(double radius, double vs) {
     for (int dx = 0; dx <= t.reach; ++dx)
       if (double(dx) * dx + double(s) <= r2) t.w[s] = dx;
   return t;
+}
+
+inline unsigned blocks_for(int64_t n, int threads) {
+  return static_cast<unsigned>((n + threads - 1) / threads);
 }
 
 /// Box -> clipped index ranges, exactly the loop bounds and the cell-centre
@@ -899,6 +904,209 @@ __global__ void __launch_bounds__(256) k_dilate_general(const uint64_t* __restri
   out[t] = m;
 }
 
+// ---------------------------------------------------------------------------
+// Separable general dilation (any occupancy): dilate's ball (voxgrid.cpp:
+// 64-92: |d_i| <= R, dx^2 + dy^2 + dz^2 <= r_c^2 + 1e-9, i.e. <= T =
+// floor(r_c^2 + 1e-9) for integer offsets) is the threshold of a squared
+// distance transform restricted to the R-box, and that transform separates:
+//   g1(x, y, z) = min over set bits x' with |x - x'| <= R of (x - x')^2
+//   g2(x, y, z) = min over |dy| <= R of g1(x, y + dy, z) + dy^2
+//   out(x, y, z) = OR over |dz| <= R of [g2(x, y, z + dz) <= T - dz^2]
+// g1 and g2 are saturating bytes (255 = farther than T; T <= 254, else the
+// per-(dy, dz) kernel k_dilate_general), four voxels per 32-bit SIMD word,
+// rows padded to whole 64-voxel words (16 groups per word): O(R) per voxel
+// instead of the O(R^2) row ORs of k_dilate_general.
+
+/// x pass: bits -> g1. Thread per 4 voxels: the nearest set bit on each
+/// side from the words around it (find-first-set / count-leading-zeros),
+/// capped at R. Padding voxels (x >= nx) are 255.
+__global__ void __launch_bounds__(256) k_sdil_x(const uint64_t* __restrict__ bits, GridView g,
+                                               uint32_t* __restrict__ g1, int reach) {
+  const int nqp = g.wx * 16;  // 4-voxel groups per padded row
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t total = static_cast<int64_t>(g.ny) * g.nz * nqp;
+  if (t >= total) return;
+  const int qx = static_cast<int>(t % nqp);
+  const int64_t row = t / nqp;
+  const uint64_t* r = bits + row * g.wx;
+  const int w = qx >> 4;
+  const uint64_t cur = __ldg(r + w);
+  uint32_t out = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int x = 4 * qx + k;
+    int best = 255;
+    if (x < g.nx) {
+      const int b = x & 63;
+      // right: bits >= x in this word, else the next words within reach
+      uint64_t m = cur >> b;
+      int d = m ? __ffsll(static_cast<long long>(m)) - 1 : 1 << 20;
+      for (int ww = w + 1; d > reach && ww < g.wx && (ww << 6) - x <= reach; ++ww) {
+        const uint64_t v = __ldg(r + ww);
+        if (v) d = (ww << 6) + __ffsll(static_cast<long long>(v)) - 1 - x;
+      }
+      // left: bits <= x in this word, else the previous words
+      m = cur << (63 - b);
+      int e = m ? __clzll(static_cast<long long>(m)) : 1 << 20;
+      for (int ww = w - 1; e > reach && ww >= 0 && x - ((ww << 6) + 63) <= reach; --ww) {
+        const uint64_t v = __ldg(r + ww);
+        if (v) e = x - ((ww << 6) + 63 - __clzll(static_cast<long long>(v)));
+      }
+      const int dm = d < e ? d : e;
+      if (dm <= reach) best = dm * dm;
+    }
+    out |= static_cast<uint32_t>(best) << (8 * k);
+  }
+  g1[t] = out;
+}
+
+// The y and z passes compute in fp16x2 (native HADD2 / HMNMX2; the byte
+// SIMD intrinsics are emulated): a byte k becomes the fp16 1024 + k (bits
+// 0x6400 | k, one PRMT for two voxels), every sum stays an integer below
+// 2048 (exact in fp16), and the low byte of the bits is k again.
+__device__ __forceinline__ uint2 bytes_to_h2(uint32_t b) {
+  return make_uint2(__byte_perm(b, 0x6464u, 0x4140), __byte_perm(b, 0x6464u, 0x4342));
+}
+__device__ __forceinline__ __half2 as_h2(uint32_t u) {
+  __half2 h;
+  memcpy(&h, &u, 4);
+  return h;
+}
+__device__ __forceinline__ uint32_t as_u32(__half2 h) {
+  uint32_t u;
+  memcpy(&u, &h, 4);
+  return u;
+}
+
+/// y pass: g2 = min(255, min over |dy| <= R of g1(y + dy) + dy^2).
+/// Block = 64 groups x TY rows of one plane, staged (as fp16x2 pairs) with
+/// the R halo rows in shared memory.
+template <int TY>
+__global__ void __launch_bounds__(256) k_sdil_y(const uint32_t* __restrict__ g1, GridView g,
+                                               uint32_t* __restrict__ g2, int reach) {
+  extern __shared__ uint2 sy[];  // [(TY + 2R) rows][64 groups]
+  const int nqp = g.wx * 16;
+  const int q0 = blockIdx.x * 64, y0 = blockIdx.y * TY, z = blockIdx.z;
+  const int rows = TY + 2 * reach;
+  const size_t plane = static_cast<size_t>(g.ny) * nqp;
+  for (int k = threadIdx.x; k < rows * 64; k += blockDim.x) {
+    const int yy = y0 - reach + k / 64, qq = q0 + (k & 63);
+    const uint32_t b = (yy >= 0 && yy < g.ny && qq < nqp)
+                           ? __ldg(g1 + z * plane + static_cast<size_t>(yy) * nqp + qq)
+                           : 0xFFFFFFFFu;
+    sy[k] = bytes_to_h2(b);
+  }
+  __syncthreads();
+  const int qq = threadIdx.x & 63;
+  const __half2 cap = __float2half2_rn(1024.0f + 255.0f);
+  for (int ly = threadIdx.x >> 6; ly < TY; ly += blockDim.x >> 6) {
+    const int y = y0 + ly;
+    if (y >= g.ny || q0 + qq >= nqp) continue;
+    __half2 lo = cap, hi = cap;
+    for (int dy = -reach; dy <= reach; ++dy) {
+      const __half2 add = __float2half2_rn(static_cast<float>(dy * dy));
+      const uint2 v = sy[(ly + reach + dy) * 64 + qq];
+      lo = __hmin2(lo, __hadd2(as_h2(v.x), add));
+      hi = __hmin2(hi, __hadd2(as_h2(v.y), add));
+    }
+    g2[z * plane + static_cast<size_t>(y) * nqp + q0 + qq] =
+        __byte_perm(as_u32(lo), as_u32(hi), 0x6420);
+  }
+}
+
+/// z pass + threshold: thread per 4-voxel group of a plane, sliding along z
+/// over a chunk of ZC output planes with the 2R + 1 input planes around the
+/// current one in a shared-memory ring (fp16x2 pairs): bit = [min over
+/// |dz| <= R of g2(z + dz) - (T - dz^2) <= 0]. A half-warp holds the 16
+/// groups of one output word (rows are padded to whole words) and ORs their
+/// nibbles by shuffles.
+template <int ZC>
+__global__ void __launch_bounds__(256) k_sdil_z(const uint32_t* __restrict__ g2, GridView g,
+                                               uint64_t* __restrict__ out, int reach, int T,
+                                               int z_lo, int z_hi) {
+  extern __shared__ uint2 ring[];  // [2R + 1][256]
+  const int64_t gpl = static_cast<int64_t>(g.ny) * g.wx * 16;  // groups per plane
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
+  const bool live = q < gpl;
+  const int za = z_lo + blockIdx.y * ZC;
+  const int zb = min(z_hi, za + ZC - 1);
+  const int win = 2 * reach + 1;
+  for (int zz = za - reach; zz < za + reach; ++zz) {
+    const int slot = (zz - (za - reach)) % win;
+    ring[slot * 256 + threadIdx.x] =
+        bytes_to_h2((live && zz >= 0 && zz < g.nz) ? __ldg(g2 + zz * gpl + q) : 0xFFFFFFFFu);
+  }
+  const int lane = threadIdx.x & 31;
+  const __half2 zero = __float2half2_rn(0.0f);
+  for (int z = za; z <= zb; ++z) {
+    const int zn = z + reach;  // newest plane of the window
+    ring[((zn - (za - reach)) % win) * 256 + threadIdx.x] =
+        bytes_to_h2((live && zn < g.nz) ? __ldg(g2 + zn * gpl + q) : 0xFFFFFFFFu);
+    __half2 lo = __float2half2_rn(1.0f), hi = lo;
+    int slot = (z - reach - (za - reach)) % win;
+    for (int dz = -reach; dz <= reach; ++dz, slot = slot + 1 == win ? 0 : slot + 1) {
+      const int lim = T - dz * dz;
+      if (lim < 0) continue;
+      const __half2 sub = __float2half2_rn(-(1024.0f + static_cast<float>(lim)));
+      const uint2 v = ring[slot * 256 + threadIdx.x];
+      lo = __hmin2(lo, __hadd2(as_h2(v.x), sub));
+      hi = __hmin2(hi, __hadd2(as_h2(v.y), sub));
+    }
+    const uint32_t ml = as_u32(__hle2(lo, zero)), mh = as_u32(__hle2(hi, zero));
+    const uint32_t nib = ((ml & 0xFFFFu) ? 1u : 0u) | ((ml >> 16) ? 2u : 0u) |
+                         ((mh & 0xFFFFu) ? 4u : 0u) | ((mh >> 16) ? 8u : 0u);
+    uint64_t v = static_cast<uint64_t>(nib) << (4 * (q & 15));
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) v |= __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if (live && (lane & 15) == 0) out[(z * gpl + q) >> 4] = v;
+  }
+}
+
+/// dilate via the separable byte transform (see above); false when T is
+/// too large for bytes (then the caller uses k_dilate_general).
+bool dilate_separable(rp_grid* g, double radius, int z0, int z1) {
+  rp_ctx* ctx = g->ctx;
+  const double r_cells = radius / g->voxel_size;
+  const int reach = static_cast<int>(std::floor(r_cells + 1e-9));
+  const double r2 = r_cells * r_cells + 1e-9;
+  // T = the largest integer s with double(s) <= r2 (the reference compares
+  // exact integer sums against r2 in double)
+  int64_t T = static_cast<int64_t>(std::floor(r2));
+  while (static_cast<double>(T + 1) <= r2) ++T;
+  while (T >= 0 && !(static_cast<double>(T) <= r2)) --T;
+  static const bool off = std::getenv("RP_DILATE_NAIVE") != nullptr;
+  if (off || T > 254 || reach > 63 || reach < 1) return false;
+  cudaStream_t st = ctx->stream;
+  const int64_t groups = static_cast<int64_t>(g->dims[2]) * g->dims[1] * g->wx * 16;
+  DevBuf<uint32_t> g1(groups, st), g2(groups, st);
+  const GridView v = g->view();
+  launch(ctx, "dilate", k_sdil_x, dim3(blocks_for(groups, 256)), dim3(256), 0,
+         static_cast<const uint64_t*>(g->bits), v, g1.p, reach);
+  constexpr int TY = 16;
+  const size_t smy = static_cast<size_t>(TY + 2 * reach) * 64 * sizeof(uint2);
+  allow_smem(k_sdil_y<TY>, smy);
+  launch(ctx, "dilate", k_sdil_y<TY>,
+         dim3(static_cast<unsigned>((g->wx * 16 + 63) / 64), static_cast<unsigned>((g->dims[1] + TY - 1) / TY),
+              static_cast<unsigned>(g->dims[2])),
+         dim3(256), smy, static_cast<const uint32_t*>(g1.p), v, g2.p, reach);
+  uint64_t* out = nullptr;
+  RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&out), g->n_words * sizeof(uint64_t) + 8, st));
+  const bool all = z0 == 0 && z1 == g->dims[2] - 1;
+  if (!all)
+    RP_CUDA(cudaMemcpyAsync(out, g->bits, g->n_words * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+  // ZC output planes per thread (the 2R halo planes are re-read per chunk)
+  constexpr int ZC = 32;
+  const size_t smz = static_cast<size_t>(2 * reach + 1) * 256 * sizeof(uint2);
+  const int64_t gpl = static_cast<int64_t>(g->dims[1]) * g->wx * 16;
+  const dim3 grid(static_cast<unsigned>((gpl + 255) / 256), static_cast<unsigned>((z1 - z0 + ZC) / ZC));
+  allow_smem(k_sdil_z<ZC>, smz);
+  launch(ctx, "dilate", k_sdil_z<ZC>, grid, dim3(256), smz, static_cast<const uint32_t*>(g2.p), v,
+         out, reach, static_cast<int>(T), z0, z1);
+  RP_CUDA(cudaFreeAsync(g->bits, st));
+  g->bits = out;
+  return true;
+}
+
 __global__ void k_or_into(uint64_t* __restrict__ dst, const uint64_t* __restrict__ src, size_t n) {
   const size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k < n) dst[k] |= src[k];
@@ -1037,9 +1245,6 @@ __global__ void k_segment_clear(GridView g, const double* __restrict__ a, const 
   out[k] = rpd::walk_clear(g, f, t, ns) ? 1 : 0;
 }
 
-inline unsigned blocks_for(int64_t n, int threads) {
-  return static_cast<unsigned>((n + threads - 1) / threads);
-}
 
 constexpr int kFusedPrimLimit = 512;
 
@@ -1121,6 +1326,7 @@ void mark_prims(rp_grid* g, const Prim* prims, int64_t nb, int64_t np, const cha
 void dilate_general(rp_grid* g, double radius, int z0 = 0, int z1 = -1) {
   rp_ctx* ctx = g->ctx;
   if (z1 < 0) z1 = g->dims[2] - 1;
+  if (dilate_separable(g, radius, z0, z1)) return;
   const DilTable t = make_table(radius, g->voxel_size);
   DevBuf<int> wtab(t.w.size(), ctx->stream);
   copy_to_device(ctx, wtab.p, t.w.data(), t.w.size() * sizeof(int));
