@@ -587,7 +587,12 @@ def config_latencies(ctx, torch, stream, reps=3):
         for t in range(reps + 1):
             ctr = c + np.array([dx * t, 0.0, 0.0])
             obs = abi.box(tuple(ctr - half), tuple(ctr + half), dynamic=True)
+            ctx.enable_timing(True)
+            ctx.reset_timing()
             ms_o, aug = timed(lambda: g.overlay(obs, into=aug))
+            ticks.setdefault("overlay_kernel_us", []).append(
+                1e3 * ctx.kernel_time("overlay")[0] / max(1, ctx.kernel_time("overlay")[1]))
+            ctx.enable_timing(False)
             ms_r, (rc2, _) = timed(lambda: api.replan_dynamic(ctx, arm, q, g, plan, at, obs, rp))
             ticks["overlay_us"].append(1e3 * ms_o)
             ticks["replan_ms"].append(ms_r)
@@ -598,6 +603,11 @@ def config_latencies(ctx, torch, stream, reps=3):
                              "+ replan_dynamic (rc 7 = no-path, rc 8 = infeasible-timing, as "
                              "the reference decides)",
                      "overlay_us": ov, "overlay_gbs_vs_3N3_8": nbytes / (ov * 1e-6) / 1e9,
+                     "overlay_kernel_us": statistics.median(ticks["overlay_kernel_us"]),
+                     "overlay_kernel_gbs_vs_3N3_8":
+                         nbytes / (statistics.median(ticks["overlay_kernel_us"]) * 1e-6) / 1e9,
+                     "overlay_note": "overlay_us = events around the whole API call (host work "
+                                     "included); overlay_kernel_us = the one fused launch",
                      "replan_ms": statistics.median(ticks["replan_ms"]), "rc": ticks["rc"]}
     else:
         res["C4"] = {"what": "no first plan on this scene", "rc": rc}
@@ -631,6 +641,26 @@ def voxel_update(ctx, torch, stream):
           for _ in range(4)]
     api.mark_dilate_concurrent(gs, obs, radius, 20)  # warm-up
     per_update_conc = api.mark_dilate_concurrent(gs, obs, radius, 100)
+    # one update alone (a single launch between synchronisations): the
+    # latency of a tick that rebuilds the grid once
+    iso = sorted(g.mark_dilate_repeat(obs, radius, 1) for _ in range(21))[10]
+    # the general (any-occupancy) dilation of the same scene's marked cells
+    # (the path of clouds and uploaded grids): N^3/8 read + N^3/8 written
+    gm = api.Grid.build(ctx, scenes.BOUNDS_MIN, scenes.BOUNDS_MAX, sc.voxel_size)
+    gm.mark(obs)
+    occ = gm.to_u8()
+    dims, origin, vs, _ = gm.info()
+    gen = []
+    for _ in range(4):
+        gd = api.Grid.from_u8(ctx, origin, vs, dims, occ)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        gd.dilate(radius)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        gen.append(e0.elapsed_time(e1))
+    gen_ms = sorted(gen[1:])[1]
     N3 = sc.n ** 3
     bytes_alg = N3 / 8
     achieved = bytes_alg / (per_launch * 1e-3) / 1e9
@@ -658,6 +688,12 @@ def voxel_update(ctx, torch, stream):
             "summary": {"grid": f"{sc.n}^3", "boxes": len(obs), "radius_voxels": radius / sc.voxel_size,
                         "us_per_update": per_launch * 1e3,
                         "voxels_per_s": N3 / (per_launch * 1e-3),
+                        "isolated_us_per_update": iso * 1e3,
+                        "isolated_frac": bytes_alg / (iso * 1e-3) / 1e9 / peak,
+                        "general_dilation": {
+                            "what": "dilate of the scene's marked occupancy as uploaded bytes "
+                                    "(separable squared-distance transform, any occupancy)",
+                            "ms": gen_ms, "gbs_read_plus_write": 2 * bytes_alg / (gen_ms * 1e-3) / 1e9},
                         "concurrent_4_grids": {
                             "us_per_update": per_update_conc * 1e3,
                             "voxels_per_s": N3 / (per_update_conc * 1e-3),

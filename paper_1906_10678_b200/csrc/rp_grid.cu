@@ -767,13 +767,14 @@ __global__ void __launch_bounds__(256) k_overlay_fused(const __grid_constant__ O
   }
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    const int64_t w = w0 + h;
-    if (w >= A.n_words) break;
-    const int64_t row = w / A.wx;
-    const int y = static_cast<int>(row % A.ny);
-    const int z = static_cast<int>(row / A.ny);
+    // 32-bit index math (n_words <= 2^27 / 64 * 8): no 64-bit divisions
+    const unsigned w = static_cast<unsigned>(w0) + h;
+    if (w >= static_cast<unsigned>(A.n_words)) break;
+    const unsigned row = w / static_cast<unsigned>(A.wx);
+    const int y = static_cast<int>(row % static_cast<unsigned>(A.ny));
+    const int z = static_cast<int>(row / static_cast<unsigned>(A.ny));
     if (y < A.y0 || y > A.y1 || z < A.z0 || z > A.z1) continue;
-    const int base = static_cast<int>(w - row * A.wx) * 64;
+    const int base = static_cast<int>(w - row * static_cast<unsigned>(A.wx)) * 64;
     uint64_t m = 0;
     for (int k = 0; k < A.np; ++k) {
       const Prim& p = A.prims[k];
