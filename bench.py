@@ -340,15 +340,11 @@ def run_ours(args, sc):
         if t2 is not None:
             # the start pose (final pose of the first plan) is read back to
             # the host and passed in: plan_arbitrary's own API takes a pose
-            s = plan.summary()
-            p, w = s["poses"][-1]
+            p, w = plan.final_pose()
             rc2, plan2 = api.plan_arbitrary(ctx, arm, q, g, p, t2, rp, start_waypoints=w)
             if rc2 != 0:
                 raise RuntimeError(f"plan_arbitrary failed rc={rc2}")
-            out = [s, plan2] if read_back else [plan, plan2]
-            if read_back:
-                out[1] = plan2.summary()
-            return out
+            return [plan.summary(), plan2.summary()] if read_back else [plan, plan2]
         return [plan.summary()] if read_back else out
 
     def barrier():
@@ -391,7 +387,7 @@ def run_ours(args, sc):
     # waypoint samples) read back from the first plan; out: every plan
     h2d = len(obstacles) * C_SIZEOF_OBSTACLE() + 3 * 8 * (2 if t2 else 1)
     d2h = sum(plan_bytes(s) for s in last)
-    if t2 is not None:
+    if t2 is not None:  # the start pose goes back in
         h2d += plan_bytes({"waypoints": [], "relax": [], "unfold": [],
                            "poses": [last[0]["poses"][-1]]})
     if world > 1:

@@ -451,6 +451,17 @@ class Plan:
         _check(lib().rp_plan_get_info(self.h, C.byref(i)))
         return i
 
+    def final_pose(self):
+        """The plan's last per-waypoint pose and its waypoint samples (the
+        start pose of a follow-on plan_arbitrary), without the rest of the
+        summary."""
+        i = self.info()
+        p = abi.Pose()
+        cap = 64 * self.n_samples
+        buf = np.zeros((cap, 3))
+        _check(lib().rp_plan_pose(self.h, 0, i.n_poses - 1, C.byref(p), buf.ctypes.data, cap))
+        return p, buf[:p.n_waypoints].copy()
+
     def summary(self) -> dict:
         i = self.info()
         n = max(1, i.n_waypoints)

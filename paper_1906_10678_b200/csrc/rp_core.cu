@@ -113,10 +113,48 @@ HostSpan::~HostSpan() {
   if (dt >= th) std::fprintf(stderr, "[span] %-24s %9.3f ms\n", name, dt);
 }
 
+namespace {
+constexpr size_t kReadbackBytes = 256 << 10;
+}  // namespace
+
+/// Device -> host copy that completes before returning. Reads up to 256 KiB
+/// go through the context's pinned staging buffer (a true async DMA plus one
+/// synchronisation, cheaper than a pageable copy's staging path); larger
+/// ones copy straight to the destination.
 void copy_to_host(rp_ctx* ctx, void* dst, const void* src, size_t bytes) {
   if (!bytes) return;
+  if (bytes <= kReadbackBytes) {
+    if (!ctx->readback) RP_CUDA(cudaMallocHost(&ctx->readback, kReadbackBytes));
+    RP_CUDA(cudaMemcpyAsync(ctx->readback, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    RP_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(dst, ctx->readback, bytes);
+    return;
+  }
   RP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
   RP_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void copy_to_host_many(rp_ctx* ctx, std::initializer_list<HostRead> reads) {
+  size_t total = 0;
+  for (const HostRead& r : reads) total += (r.bytes + 15) & ~size_t{15};
+  if (total > kReadbackBytes) {
+    for (const HostRead& r : reads) copy_to_host(ctx, r.dst, r.src, r.bytes);
+    return;
+  }
+  if (!ctx->readback) RP_CUDA(cudaMallocHost(&ctx->readback, kReadbackBytes));
+  size_t off = 0;
+  for (const HostRead& r : reads) {
+    if (r.bytes)
+      RP_CUDA(cudaMemcpyAsync(static_cast<char*>(ctx->readback) + off, r.src, r.bytes,
+                              cudaMemcpyDeviceToHost, ctx->stream));
+    off += (r.bytes + 15) & ~size_t{15};
+  }
+  RP_CUDA(cudaStreamSynchronize(ctx->stream));
+  off = 0;
+  for (const HostRead& r : reads) {
+    if (r.bytes) std::memcpy(r.dst, static_cast<char*>(ctx->readback) + off, r.bytes);
+    off += (r.bytes + 15) & ~size_t{15};
+  }
 }
 
 namespace {
@@ -376,6 +414,7 @@ rp_status rp_ctx_destroy(rp_ctx* ctx) {
     }
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->readback) cudaFreeHost(ctx->readback);
     for (cudaEvent_t e : ctx->upload_ev) cudaEventDestroy(e);
     for (auto& b : ctx->s2_pool) {
       cudaFree(b.bits);

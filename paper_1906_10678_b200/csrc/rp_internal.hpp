@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <exception>
+#include <initializer_list>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -97,6 +98,8 @@ struct rp_ctx {
     uint8_t* ok;
   };
   std::vector<S2Buf> s2_pool;
+  // pinned read-back staging of copy_to_host (small reads)
+  void* readback = nullptr;
 };
 
 namespace rp {
@@ -314,6 +317,13 @@ struct HostSpan {
 };
 
 void copy_to_host(rp_ctx* ctx, void* dst, const void* src, size_t bytes);  // syncs
+/// Several device -> host reads behind one synchronisation.
+struct HostRead {
+  void* dst;
+  const void* src;
+  size_t bytes;
+};
+void copy_to_host_many(rp_ctx* ctx, std::initializer_list<HostRead> reads);
 void copy_to_device(rp_ctx* ctx, void* dst, const void* src, size_t bytes);
 
 // Derived reach parameters (src/reach_solver.cpp:28-43).

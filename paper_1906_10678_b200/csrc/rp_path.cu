@@ -2885,8 +2885,17 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
                                         dim3(kBpThreads), args, smem, st));
     launch_end(ctx, "backward_pass", ev);
   }
+  // the state and the pass's outputs in one read-back
   int hs[4];
-  copy_to_host(ctx, hs, bp_state.p, sizeof(hs));
+  out->poses.resize(m);
+  out->relax.resize(m);
+  out->kind.resize(m);
+  out->wps.resize(m);
+  copy_to_host_many(ctx, {{hs, bp_state.p, sizeof(hs)},
+                          {out->poses.data(), dp.p, m * sizeof(DevPose)},
+                          {out->relax.data(), dr.p, m * sizeof(double)},
+                          {out->kind.data(), dk.p, m * sizeof(int)},
+                          {out->wps.data(), dw.p, m * sizeof(V3)}});
   if (profile) {
     long long hp[24];
     copy_to_host(ctx, hp, prof.p, sizeof(hp));
@@ -2911,14 +2920,6 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
     out->ok = false;
     return true;
   }
-  out->poses.resize(m);
-  out->relax.resize(m);
-  out->kind.resize(m);
-  out->wps.resize(m);
-  copy_to_host(ctx, out->poses.data(), dp.p, m * sizeof(DevPose));
-  copy_to_host(ctx, out->relax.data(), dr.p, m * sizeof(double));
-  copy_to_host(ctx, out->kind.data(), dk.p, m * sizeof(int));
-  copy_to_host(ctx, out->wps.data(), dw.p, m * sizeof(V3));
   return true;
 }
 

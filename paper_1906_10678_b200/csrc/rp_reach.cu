@@ -1081,14 +1081,16 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
     launch(ctx, "compact", k_compact_small, dim3(1), dim3(1024), 0,
            static_cast<const uint32_t*>(surv_bits.p), q->n, surv_idx.p, surv_cnt.p);
     int S1 = 0;
-    copy_to_host(ctx, &S1, surv_cnt.p, sizeof(int));
+    // the survivor count and list in one read-back (the list is at most Q)
+    std::vector<int> surv_all(q->n);
+    copy_to_host_many(ctx, {{&S1, surv_cnt.p, sizeof(int)},
+                            {surv_all.data(), surv_idx.p, q->n * sizeof(int)}});
     s->S1 = S1;
     s->surv.alloc(S1 + 1, st);
     if (S1 > 0)
       launch(ctx, "seg1", k_surv_data, dim3(nblk(S1, 128)), dim3(128), 0, a,
              static_cast<const int*>(surv_idx.p), S1, s->surv.p);
-    s->surv_i.resize(S1);
-    copy_to_host(ctx, s->surv_i.data(), surv_idx.p, S1 * sizeof(int));
+    s->surv_i.assign(surv_all.begin(), surv_all.begin() + S1);
 
     s->n_pairs = static_cast<int64_t>(S1) * q->n;
     const int64_t nbits = s->n_pairs * s->B;
@@ -1152,12 +1154,12 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
              static_cast<const BestRec*>(bb.p), blocks, best.p);
     }
     unsigned long long hc[C_COUNT];
-    copy_to_host(ctx, hc, ctr.p, sizeof(hc));
     unsigned nsc = 0;
-    copy_to_host(ctx, &nsc, sc_count.p, sizeof(unsigned));
-    require(nsc <= kShortcutCap, RP_E_CAPACITY_EXCEEDED, "too many near-encounter hypotheses");
     BestRec hb{0.0, -1};
-    if (s->n_pairs > 0) copy_to_host(ctx, &hb, best.p, sizeof(BestRec));
+    copy_to_host_many(ctx, {{hc, ctr.p, sizeof(hc)},
+                            {&nsc, sc_count.p, sizeof(unsigned)},
+                            {&hb, best.p, s->n_pairs > 0 ? sizeof(BestRec) : 0}});
+    require(nsc <= kShortcutCap, RP_E_CAPACITY_EXCEEDED, "too many near-encounter hypotheses");
 
     rp_solve_stats& S = s->stats;
     std::memset(&S, 0, sizeof(S));

@@ -27,8 +27,7 @@ def step():
     rc, plan = api.plan_reach_then_path(ctx, arm, q, g, sc.target, rp)
     out = [rc]
     if rc == 0 and "second_target" in sc.extra:
-        s = plan.summary()
-        p, w = s["poses"][-1]
+        p, w = plan.final_pose()
         print("---- plan_arbitrary", file=sys.stderr, flush=True)
         rc2, plan2 = api.plan_arbitrary(ctx, arm, q, g, p, sc.extra["second_target"], rp,
                                         start_waypoints=w)
