@@ -595,6 +595,25 @@ def config_latencies(ctx, torch, stream, reps=3):
             ticks["rc"].append(rc2)
         ov = statistics.median(ticks["overlay_us"])
         nbytes = 3 * sc.n ** 3 / 8
+        # back-to-back ticks: the stream is held by a sleep kernel while the
+        # host queues K overlay calls, so the events see the device cost per
+        # tick without the host's launch latency in it
+        K = 64
+        obs_k = [abi.box(tuple(c + np.array([dx * t, 0.0, 0.0]) - half),
+                         tuple(c + np.array([dx * t, 0.0, 0.0]) + half), dynamic=True)
+                 for t in range(K)]
+        pipe = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            torch.cuda._sleep(20_000_000)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for o in obs_k:
+                aug = g.overlay(o, into=aug)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            pipe.append(1e3 * e0.elapsed_time(e1) / K)
+        ov_pipe = min(pipe)
         res["C4"] = {"what": "per control tick on 256^3: re-voxelise the moving cube (overlay) "
                              "+ replan_dynamic (rc 7 = no-path, rc 8 = infeasible-timing, as "
                              "the reference decides)",
@@ -602,12 +621,27 @@ def config_latencies(ctx, torch, stream, reps=3):
                      "overlay_kernel_us": statistics.median(ticks["overlay_kernel_us"]),
                      "overlay_kernel_gbs_vs_3N3_8":
                          nbytes / (statistics.median(ticks["overlay_kernel_us"]) * 1e-6) / 1e9,
+                     "overlay_pipelined_us": ov_pipe,
+                     "overlay_pipelined_gbs_vs_3N3_8": nbytes / (ov_pipe * 1e-6) / 1e9,
+                     "overlay_pipelined_frac": nbytes / (ov_pipe * 1e-6) / 1e9 / hbm_peak(),
                      "overlay_note": "overlay_us = events around the whole API call (host work "
-                                     "included); overlay_kernel_us = the one fused launch",
+                                     "included); overlay_kernel_us = events around the one fused "
+                                     "launch (launch latency included when the stream was idle); "
+                                     "overlay_pipelined_us = 64 calls queued behind a sleep "
+                                     "kernel, device time per tick",
                      "replan_ms": statistics.median(ticks["replan_ms"]), "rc": ticks["rc"]}
     else:
         res["C4"] = {"what": "no first plan on this scene", "rc": rc}
     return res
+
+
+def hbm_peak():
+    """MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)."""
+    import json as _json
+    try:
+        return _json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except (OSError, KeyError):
+        return 6650.0
 
 
 def voxel_update(ctx, torch, stream):
@@ -637,6 +671,14 @@ def voxel_update(ctx, torch, stream):
           for _ in range(4)]
     api.mark_dilate_concurrent(gs, obs, radius, 20)  # warm-up
     per_update_conc = api.mark_dilate_concurrent(gs, obs, radius, 100)
+    del gs
+    # the same chain over 16 grids (256 MiB, twice L2): pass r writes grid
+    # r % 16, so the words cannot stay L2-resident and every pass reaches HBM
+    gr = [api.Grid.build(ctx, scenes.BOUNDS_MIN, scenes.BOUNDS_MAX, sc.voxel_size)
+          for _ in range(16)]
+    api.mark_dilate_rotating(gr, obs, radius, 32)  # warm-up
+    per_rot = api.mark_dilate_rotating(gr, obs, radius, 320)
+    del gr
     # one update alone (a single launch between synchronisations): the
     # latency of a tick that rebuilds the grid once
     iso = sorted(g.mark_dilate_repeat(obs, radius, 1) for _ in range(21))[10]
@@ -690,6 +732,12 @@ def voxel_update(ctx, torch, stream):
                             "what": "dilate of the scene's marked occupancy as uploaded bytes "
                                     "(separable squared-distance transform, any occupancy)",
                             "ms": gen_ms, "gbs_read_plus_write": 2 * bytes_alg / (gen_ms * 1e-3) / 1e9},
+                        "rotating_16_grids": {
+                            "what": "the pipelined chain with pass r writing grid r % 16 (256 MiB "
+                                    "working set > 126 MB L2): the HBM-resident update rate",
+                            "us_per_update": per_rot * 1e3,
+                            "achieved_gbs": bytes_alg / (per_rot * 1e-3) / 1e9,
+                            "frac": bytes_alg / (per_rot * 1e-3) / 1e9 / peak},
                         "concurrent_4_grids": {
                             "us_per_update": per_update_conc * 1e3,
                             "voxels_per_s": N3 / (per_update_conc * 1e-3),

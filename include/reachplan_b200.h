@@ -257,6 +257,11 @@ rp_status rp_grid_device_bits(rp_grid* g, void** bits, uint64_t* n_words,
  * `reps` times back to back on the ctx stream; *ms = device time per pass. */
 rp_status rp_grid_mark_dilate_repeat(rp_grid* g, const rp_obstacle* obs, int32_t n, double radius,
                                      int32_t reps, double* ms);
+/* Benchmark helper: `reps` passes back to back on the ctx stream, pass r
+ * writing grids[r % ng] (same shape, one context); *ms = device time per
+ * pass. With ng grids larger than L2 together, every pass's words reach HBM. */
+rp_status rp_grid_mark_dilate_rotating(rp_grid* const* grids, int32_t ng, const rp_obstacle* obs,
+                                       int32_t n, double radius, int32_t reps, double* ms);
 /* Benchmark helper: `ng` same-shape grids of one context, each updated `reps`
  * times on its own stream, all streams concurrently; *ms = device time per
  * update (updates of independent grids overlapping). */

@@ -127,6 +127,8 @@ def lib():
         "rp_grid_device_bits": ([vp, P(vp), P(C.c_uint64), P(C.c_uint64)], C.c_int32),
         "rp_grid_mark_dilate_concurrent": ([P(vp), C.c_int32, P(abi.Obstacle), C.c_int32,
                                             C.c_double, C.c_int32, P(C.c_double)], C.c_int32),
+        "rp_grid_mark_dilate_rotating": ([P(vp), C.c_int32, P(abi.Obstacle), C.c_int32,
+                                          C.c_double, C.c_int32, P(C.c_double)], C.c_int32),
         "rp_validate_plan": ([vp, P(abi.Arm), vp, vp, P(abi.ReachParams), P(abi.PathParams),
                               P(abi.Validation), C.c_char_p, C.c_int64], C.c_int32),
         "rp_simulate_execution": ([vp, P(abi.Arm), vp, P(abi.MotionParams), vp, P(vp)], C.c_int32),
@@ -657,6 +659,17 @@ def simulate_execution(ctx, arm, plan, mp=None, grid=None) -> dict:
                 "clamp": clamp[:nc.value].tolist(), "reached": bool(reached.value)}
     finally:
         lib().rp_trace_destroy(h)
+
+
+def mark_dilate_rotating(grids, obstacles, radius, reps) -> float:
+    """Per-pass device time (ms) of `reps` fused mark+dilate passes back to
+    back on one stream, pass r writing grids[r % len(grids)]."""
+    arr = abi.obstacle_array(obstacles)
+    hs = (C.c_void_p * len(grids))(*[g.h for g in grids])
+    ms = C.c_double()
+    _check(lib().rp_grid_mark_dilate_rotating(hs, len(grids), arr, len(obstacles), radius,
+                                              reps, C.byref(ms)))
+    return ms.value
 
 
 def mark_dilate_concurrent(grids, obstacles, radius, reps) -> float:

@@ -110,6 +110,22 @@ def test_overlay_bitexact(ctx):
         assert np.array_equal(aug.to_u8(), R.overlay(obs))
 
 
+@pytest.mark.parametrize("n", [45, 100, 200])
+def test_overlay_ragged_bitexact(ctx, n):
+    """Odd plane sizes (the fused tick's 8-byte path), partial blocks, and
+    an obstacle straddling the grid's corner."""
+    api = _api()
+    base = scenes.config("C2")
+    sc = scenes.Scene(f"ragged{n}", n, base.boxes, base.lengths, base.mode)
+    arm, rp, q, g = gpu_problem(ctx, sc)
+    R = ref.RefProblem(sc)
+    aug = None
+    for c, h in (((0.3, 0.2, 0.1), 0.05), ((1.58, 1.57, -1.59), 0.07), ((0.0, -0.7, 0.9), 0.02)):
+        obs = abi.box(tuple(x - h for x in c), tuple(x + h for x in c), dynamic=True)
+        aug = g.overlay(obs, into=aug)
+        assert np.array_equal(aug.to_u8(), R.overlay(obs)), (n, c)
+
+
 def test_waypoint_ik_matches_reference(ctx):
     api = _api()
     sc = scenes.config("C2", quiver_deg=5.0)
