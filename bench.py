@@ -302,7 +302,7 @@ def plan_bytes(summary) -> int:
 
 
 KERNEL_GROUPS = ["voxelize", "mark_dilate", "dilate", "overlay", "seg1", "walk1", "compact",
-                 "seg2", "clear2", "select", "shortcuts", "walk4", "backward_pass", "wik_filter",
+                 "seg2", "tail", "clear2", "select", "shortcuts", "walk4", "backward_pass", "wik_filter",
                  "wik_compact", "wik_pairs", "score", "rank", "materialize", "unfold",
                  "pose_check", "refine", "trail", "cone", "finish"]
 
@@ -500,6 +500,9 @@ def batch_queries(args, ctx, torch, stream, rank, world):
         h.update(np.float64(r.path_length).tobytes())
         h.update(bytes(r.refined))
     ok = sum(1 for r in res if r.status == 0)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_batch_subset(grid(), targets[:4], min(args.cpu_budget_s, 90.0))
     return {"workload": f"C5: {len(targets)} 8-DOF reach queries (solve + select + refine), "
                         f"{sc.n}^3 grid, {len(obs)} boxes, {sc.quiver_deg:g}-deg quiver",
             "queries": len(targets), "queries_per_rank": hi - lo, "steps": steps,
@@ -508,7 +511,66 @@ def batch_queries(args, ctx, torch, stream, rank, world):
             "sharding": f"contiguous target blocks x{world}, all-gather of result records; grid "
                         + (f"built as {world} z-slabs + NCCL all-gather" if world > 1
                            else "built whole"),
-            "solved": ok, "results_sha256": h.hexdigest()[:16]}
+            "solved": ok, "results_sha256": h.hexdigest()[:16], "cpu_subset": cpu}
+
+
+_CPU_BATCH_CODE = (
+    "import sys,json,time; sys.path.insert(0,%r); sys.path.insert(0,%r)\n"
+    "import numpy as np\nfrom paper_1906_10678_b200 import abi, scenes\nimport ref\n"
+    "z = np.load(%r)\nsc = scenes.config('C5')\nW = %d\n"
+    "R = ref.RefProblem(sc, workers=W, grid_u8=(tuple(z['origin']), tuple(int(v) for v in "
+    "z['dims']), z['occ'], float(z['dil'])))\n"
+    "rp = sc.reach_params()\nout = []\n"
+    "for t in z['targets']:\n"
+    "    t0 = time.perf_counter()\n"
+    "    st, ns, nc = R.solve(tuple(t), workers=W)\n"
+    "    if ns + nc:\n"
+    "        c = R.select()\n"
+    "        if c.kind == abi.RP_CHOSEN_REACH_POSE:\n"
+    "            pose, _ = R.pose(c.index)\n"
+    "            try:\n"
+    "                R.refine(pose, tuple(t), triangle=bool(rp.refine_triangle_8dof))\n"
+    "            except ref.RefError:\n"
+    "                pass\n"
+    "    out.append(1e3 * (time.perf_counter() - t0))\n"
+    "    print(json.dumps(out), flush=True)\n")
+
+
+def cpu_batch_subset(g, targets, budget_s):
+    """The reference's per-query work of the C5 batch (solve_reach + select +
+    exact refine, src/reach_solver.cpp:480-577, src/arm_model.cpp:278-302) on
+    this host for the first few targets, all cores, fed the GPU-built 512^3
+    grid (pinned equal to the reference's by tests/test_gpu_parity_configs.py)
+    so its 6-minute dilation is skipped; extrapolated linearly to queries/s."""
+    import tempfile
+    import numpy as np
+    cores = os.cpu_count() or 1
+    dims, origin, vs, dil = g.info()
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "c5.npz")
+        np.savez(path, occ=g.to_u8(), dims=np.array(dims), origin=np.array(origin), dil=dil,
+                 targets=np.asarray(targets))
+        code = _CPU_BATCH_CODE % (ROOT, os.path.join(ROOT, "oracle"), path, cores)
+        times = []
+        try:
+            r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                               timeout=budget_s)
+            out = r.stdout
+        except subprocess.TimeoutExpired as e:
+            out = e.stdout.decode() if isinstance(e.stdout, bytes) else (e.stdout or "")
+        for ln in out.strip().splitlines():
+            try:
+                times = json.loads(ln)
+            except ValueError:
+                pass
+    if not times:
+        return {"error": "no query finished within the budget"}
+    per = statistics.mean(times)
+    return {"kind": "reference", "cores": cores, "cpu_model": cpu_model(),
+            "queries": len(times), "ms_per_query": per, "ms": times,
+            "queries_per_s": 1e3 / per,
+            "sample": f"the first {len(times)} of the C5 targets, solve + select + refine each, "
+                      f"workers={cores}, on the GPU-built grid; queries/s extrapolated linearly"}
 
 
 def config_latencies(ctx, torch, stream, reps=3):

@@ -2551,9 +2551,9 @@ extern "C" rp_status rp_solve_reach_batch(rp_ctx* ctx, const rp_arm* arm, const 
       const int ntail = static_cast<int>(std::min<unsigned>(hcc[1], static_cast<unsigned>(tail_cap)));
       if (ntail > 0) {
         if (eight)
-          launch(ctx, "seg2", k_bq_tail<true>, dim3(ntail), dim3(kTailBlock), 0, d);
+          launch(ctx, "tail", k_bq_tail<true>, dim3(ntail), dim3(kTailBlock), 0, d);
         else
-          launch(ctx, "seg2", k_bq_tail<false>, dim3(ntail), dim3(kTailBlock), 0, d);
+          launch(ctx, "tail", k_bq_tail<false>, dim3(ntail), dim3(kTailBlock), 0, d);
       }
       launch(ctx, "select", k_bq_best, dim3(T), dim3(64), 0, d);
       require(nsc <= kBatchShortcutCap, RP_E_CAPACITY_EXCEEDED,
