@@ -434,10 +434,51 @@ def run_ours(args, sc):
         "configs": configs,
         "paper_ms": PAPER_MS,
     }
+    if world == 1:
+        line["facade_e2e"] = facade_e2e(sc)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(sc, args.cpu_budget_s)
     print(json.dumps(line))
     return line
+
+
+def facade_e2e(sc, steps=5):
+    """The same step through the C++ façade (the reference's own reachplan::
+    declarations over the C ABI; tests/facade/facade_check --bench): what a
+    reference caller that swaps the library sees, host wall clock per step,
+    VoxelGrid bytes on the host included (build_scene_grid returns them)."""
+    import tempfile
+    from paper_1906_10678_b200 import scenes
+    exe = os.path.join(ROOT, "tests", "facade", "_build", "facade_check")
+    if not os.path.exists(exe):
+        return {"error": "tests/facade/_build/facade_check not built"}
+    t2 = sc.extra.get("second_target", scenes.SECOND_TARGET)
+    lines = [f"lengths {len(sc.lengths)} " + " ".join(repr(x) for x in sc.lengths),
+             f"radius {scenes.ARM_RADIUS!r}", f"mode {sc.mode}", f"samples {sc.n_samples}",
+             "bounds " + " ".join(repr(x) for x in scenes.BOUNDS_MIN + scenes.BOUNDS_MAX),
+             f"voxel {sc.voxel_size!r}", f"quiver {sc.quiver_step()!r} {sc.min_per_ring}",
+             "target " + " ".join(repr(x) for x in sc.target),
+             "second " + " ".join(repr(float(x)) for x in t2), f"boxes {len(sc.boxes)}"]
+    lines += [" ".join(repr(float(x)) for x in (*lo, *hi)) for lo, hi in sc.boxes]
+    with tempfile.NamedTemporaryFile("w", suffix=".txt", delete=False) as f:
+        f.write("\n".join(lines) + "\n")
+        path = f.name
+    try:
+        r = subprocess.run([exe, path, "--bench", str(steps)], capture_output=True, text=True,
+                           timeout=300)
+        js = json.loads(r.stdout.strip().splitlines()[-1])
+    except (subprocess.TimeoutExpired, ValueError, IndexError) as e:
+        return {"error": str(e)[:200]}
+    finally:
+        os.unlink(path)
+    if "bench_ms" not in js:
+        return {"error": js}
+    return {"what": "build_scene_grid + plan_reach_then_path + plan_arbitrary through the C++ "
+                    "facade (reference reachplan:: API), host wall clock",
+            "ms_per_step": statistics.median(js["bench_ms"]), "ms": js["bench_ms"],
+            "stages_ms": {k: statistics.median(js[k]) for k in ("grid_ms", "reach_path_ms",
+                                                                  "arbitrary_ms") if k in js},
+            "waypoints": js["waypoints"]}
 
 
 def C_SIZEOF_OBSTACLE():

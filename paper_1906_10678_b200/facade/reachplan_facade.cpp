@@ -30,12 +30,19 @@
 #include "reachplan_b200.h"
 
 #include <algorithm>
+#include <array>
+#include <chrono>
+#include <condition_variable>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <functional>
 #include <memory>
+#include <mutex>
 #include <ostream>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace reachplan {
@@ -260,6 +267,137 @@ uint64_t mix_bytes(const void* data, std::size_t n, uint64_t h) {
   return h;
 }
 
+/// RP_FACADE_TRACE=1: per-step host times of the façade's own work (stderr).
+struct Trace {
+  const char* what;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  explicit Trace(const char* w) : what(w) {}
+  ~Trace() {
+    static const bool on = std::getenv("RP_FACADE_TRACE") != nullptr;
+    if (on)
+      std::fprintf(stderr, "[facade] %-22s %9.3f ms\n", what,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                       .count());
+  }
+};
+
+/// A persistent pool of host threads for the façade's O(N^3) byte work
+/// (expanding and hashing VoxelGrid bytes): spawning threads per call cost
+/// more than the work at 256^3.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool p;
+    return p;
+  }
+  std::size_t size() const { return workers_.size() + 1; }
+  /// f(t) for t in [0, n): the caller and the workers take indices in turn.
+  void run(std::size_t n, const std::function<void(std::size_t)>& f) {
+    if (n <= 1 || workers_.empty()) {
+      for (std::size_t t = 0; t < n; ++t) f(t);
+      return;
+    }
+    std::lock_guard<std::mutex> one(call_);  // one job at a time across caller threads
+    std::unique_lock<std::mutex> lk(m_);
+    job_ = &f;
+    n_ = n;
+    next_ = 0;
+    left_ = n;
+    ++gen_;
+    cv_.notify_all();
+    drain(lk);
+    done_.wait(lk, [&] { return left_ == 0; });
+    job_ = nullptr;
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& w : workers_) w.join();
+  }
+
+ private:
+  HostPool() {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    for (unsigned k = 1; k < std::min(hw, 32u); ++k)
+      workers_.emplace_back([this] {
+        std::unique_lock<std::mutex> lk(m_);
+        uint64_t seen = 0;
+        for (;;) {
+          cv_.wait(lk, [&] { return stop_ || (gen_ != seen && job_ && next_ < n_); });
+          if (stop_) return;
+          seen = gen_;
+          drain(lk);
+        }
+      });
+  }
+  // with m_ held: run indices until none is left to take
+  void drain(std::unique_lock<std::mutex>& lk) {
+    while (job_ && next_ < n_) {
+      const std::size_t t = next_++;
+      const auto* f = job_;
+      lk.unlock();
+      (*f)(t);
+      lk.lock();
+      if (--left_ == 0) done_.notify_all();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex call_, m_;
+  std::condition_variable cv_, done_;
+  const std::function<void(std::size_t)>* job_ = nullptr;
+  std::size_t n_ = 0, next_ = 0, left_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+/// Runs f(begin, end) over [0, n) split into up to one range per pool
+/// thread, each of at least `min_chunk` items.
+template <typename F>
+void parallel_ranges(std::size_t n, std::size_t min_chunk, F f) {
+  HostPool& pool = HostPool::get();
+  const std::size_t T =
+      std::max<std::size_t>(1, std::min(pool.size(), n / std::max<std::size_t>(1, min_chunk)));
+  if (T <= 1) {
+    f(std::size_t{0}, n);
+    return;
+  }
+  const std::size_t per = (n + T - 1) / T;
+  pool.run(T, [&](std::size_t t) {
+    const std::size_t a = t * per, b = std::min(n, a + per);
+    if (a < b) f(a, b);
+  });
+}
+
+/// Content hash of a large buffer: mix_bytes of fixed 1 MiB blocks (seeded
+/// by h and the block index) computed in parallel, then mixed in order --
+/// the same value for any thread count. fill(begin, end) runs on a block's
+/// bytes just before they are hashed (while they are in this core's cache),
+/// so a producer can write and hash in one pass.
+template <typename Fill>
+uint64_t hash_blocks(const uint8_t* data, std::size_t n, uint64_t h, Fill fill) {
+  constexpr std::size_t kBlock = std::size_t{1} << 20;
+  const std::size_t nb = (n + kBlock - 1) / kBlock;
+  if (nb <= 1) {
+    fill(std::size_t{0}, n);
+    return mix_bytes(data, n, h);
+  }
+  std::vector<uint64_t> bh(nb);
+  parallel_ranges(nb, 1, [&](std::size_t k0, std::size_t k1) {
+    for (std::size_t k = k0; k < k1; ++k) {
+      const std::size_t off = k * kBlock, len = std::min(kBlock, n - off);
+      fill(off, off + len);
+      bh[k] = mix_bytes(data + off, len, h ^ (k * 0x9E37ull));
+    }
+  });
+  return mix_bytes(bh.data(), nb * sizeof(uint64_t), h);
+}
+uint64_t mix_bytes_parallel(const uint8_t* data, std::size_t n, uint64_t h) {
+  return hash_blocks(data, n, h, [](std::size_t, std::size_t) {});
+}
+
 struct GridEntry {
   uint64_t hash;
   rp_grid* g;
@@ -287,19 +425,24 @@ class Runtime {
   }
   rp_ctx* ctx() { return ctx_; }
 
-  static uint64_t grid_hash(const VoxelGrid& g) {
+  static uint64_t grid_meta_hash(const VoxelGrid& g) {
     uint64_t h = mix_bytes(g.dims.data(), sizeof(int) * 3, 0x51ED27ull);
     const double meta[5] = {g.origin.x(), g.origin.y(), g.origin.z(), g.voxel_size,
                             g.dilation_radius};
-    h = mix_bytes(meta, sizeof(meta), h);
-    return mix_bytes(g.occupancy.data(), g.occupancy.size(), h);
+    return mix_bytes(meta, sizeof(meta), h);
+  }
+  static uint64_t grid_hash(const VoxelGrid& g) {
+    return mix_bytes_parallel(g.occupancy.data(), g.occupancy.size(), grid_meta_hash(g));
   }
 
   /// Device mirror of a host grid (uploaded on a cache miss).
   rp_grid* grid(const VoxelGrid& g) {
     require(g.occupancy.size() == g.cell_count(), Errc::invalid_parameter,
             "grid occupancy size does not match its dims");
-    const uint64_t h = grid_hash(g);
+    const uint64_t h = [&] {
+      Trace t_("grid lookup hash");
+      return grid_hash(g);
+    }();
     for (auto& e : grids_)
       if (e.hash == h) return e.g;
     double org[3];
@@ -321,9 +464,47 @@ class Runtime {
     out.origin = get3(org);
     out.voxel_size = vs;
     out.dilation_radius = rad;
-    out.occupancy.assign(out.cell_count(), 0);
-    ok(rp_grid_download_u8(d, out.occupancy.data(), out.occupancy.size()));
-    remember(grid_hash(out), d);
+    // the bit words (1/8 of the bytes) cross PCIe and are expanded to the
+    // reference's byte layout on the host, rows in parallel
+    const std::size_t nx = dims[0], rows = static_cast<std::size_t>(dims[1]) * dims[2];
+    const std::size_t wx = (nx + 63) / 64;
+    std::vector<uint64_t> bits(rows * wx);
+    {
+      Trace t_("adopt download bits");
+      ok(rp_grid_download_bits(d, bits.data(), bits.size()));
+    }
+    {
+      Trace t_("adopt resize");
+      out.occupancy.resize(out.cell_count());
+    }
+    Trace t_("adopt expand+hash");
+    static const auto expand = [] {
+      std::array<uint64_t, 256> t{};
+      for (int v = 0; v < 256; ++v)
+        for (int k = 0; k < 8; ++k)
+          if ((v >> k) & 1) t[v] |= uint64_t{1} << (8 * k);  // little-endian byte k
+      return t;
+    }();
+    uint8_t* dst = out.occupancy.data();
+    // expand each 1 MiB block of the byte grid from the bit words and hash
+    // it while it is in cache (grid_hash's value, one pass)
+    const auto fill = [&](std::size_t o0, std::size_t o1) {
+      while (o0 < o1) {
+        const std::size_t r = o0 / nx, x0 = o0 - r * nx;
+        const std::size_t x1 = std::min(nx, x0 + (o1 - o0));
+        uint8_t* row = dst + r * nx;
+        const uint64_t* wr = bits.data() + r * wx;
+        std::size_t x = x0;
+        for (; x < x1 && (x & 7); ++x) row[x] = static_cast<uint8_t>((wr[x >> 6] >> (x & 63)) & 1);
+        for (; x + 8 <= x1; x += 8) {
+          const uint64_t bytes = expand[(wr[x >> 6] >> (x & 63)) & 0xFF];
+          std::memcpy(row + x, &bytes, 8);
+        }
+        for (; x < x1; ++x) row[x] = static_cast<uint8_t>((wr[x >> 6] >> (x & 63)) & 1);
+        o0 += x1 - x0;
+      }
+    };
+    remember(hash_blocks(dst, out.occupancy.size(), grid_meta_hash(out), fill), d);
   }
 
   rp_quiver* quiver(const Quiver& q) {
@@ -392,6 +573,7 @@ class Runtime {
       }
     grids_.push_front({h, d});
     if (grids_.size() > 4) {
+      Trace t_("evict grid");
       rp_grid_destroy(grids_.back().g);
       grids_.pop_back();
     }
@@ -931,8 +1113,15 @@ PathPlan plan_arbitrary(const ArmSpec& spec, const Quiver& q, const VoxelGrid& g
   double t[3];
   put3(t, target);
   rp_plan* h = nullptr;
-  const rp_status st = rp_plan_arbitrary(rt().ctx(), &arm, rt().quiver(q), rt().grid(grid), &sp,
-                                         sw.empty() ? nullptr : sw.data(), t, &r, &p, &h);
+  rp_quiver* dq = rt().quiver(q);
+  rp_grid* dg = rt().grid(grid);
+  rp_status st;
+  {
+    Trace t_("rp_plan_arbitrary");
+    st = rp_plan_arbitrary(rt().ctx(), &arm, dq, dg, &sp, sw.empty() ? nullptr : sw.data(), t, &r,
+                           &p, &h);
+  }
+  Trace t_("take_plan");
   return take_plan(st, h);
 }
 
@@ -969,8 +1158,14 @@ PathPlan plan_reach_then_path(const ArmSpec& spec, const Quiver& q, const VoxelG
   double t[3];
   put3(t, target);
   rp_plan* h = nullptr;
-  const rp_status st =
-      rp_plan_reach_then_path(rt().ctx(), &arm, rt().quiver(q), rt().grid(grid), t, &r, &p, &h);
+  rp_quiver* dq = rt().quiver(q);
+  rp_grid* dg = rt().grid(grid);
+  rp_status st;
+  {
+    Trace t_("rp_plan_reach_then_path");
+    st = rp_plan_reach_then_path(rt().ctx(), &arm, dq, dg, t, &r, &p, &h);
+  }
+  Trace t_("take_plan");
   return take_plan(st, h);
 }
 
@@ -1006,8 +1201,11 @@ VoxelGrid build_scene_grid(const Scene& scene, const ArmSpec& arm, const ReachPa
   put3(hi, scene.grid.bounds_max);
   const ObstacleBuf ob(scene.obstacles);
   rp_grid* d = nullptr;
-  ok(rp_build_scene_grid(rt().ctx(), lo, hi, scene.grid.voxel_size, scene.grid.dilation_radius,
-                         ob.obs.data(), ob.size(), &a, &r, &d));
+  {
+    Trace t_("device build");
+    ok(rp_build_scene_grid(rt().ctx(), lo, hi, scene.grid.voxel_size, scene.grid.dilation_radius,
+                           ob.obs.data(), ob.size(), &a, &r, &d));
+  }
   VoxelGrid g;
   rt().adopt(d, g);
   if (warnings) {

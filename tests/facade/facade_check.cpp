@@ -9,10 +9,15 @@
 //   lengths <n> L1 .. Ln   radius <r>   mode <0|1>   samples <n>
 //   bounds x0 y0 z0 x1 y1 z1   voxel <vs>   quiver <step_rad> <min_per_ring>
 //   target x y z   second x y z   boxes <k> then k lines "x0 y0 z0 x1 y1 z1"
+//
+// facade_check scene.txt [plan_file]    results as JSON (tests/test_facade.py)
+// facade_check scene.txt --bench K      K timed C3-style steps (bench.py)
 #include "reachplan/io.hpp"
 #include "reachplan/pipeline.hpp"
 
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <fstream>
 #include <iostream>
 #include <sstream>
@@ -114,6 +119,44 @@ int main(int argc, char** argv) {
         scene.obstacles.push_back(o);
       }
     }
+  }
+  if (argc > 3 && std::string(argv[2]) == "--bench") {
+    // the C3 step through the reference API, host wall clock per step:
+    // build_scene_grid + plan_reach_then_path + plan_arbitrary (from its
+    // final pose to `second`); the first step is a warm-up
+    const int K = std::atoi(argv[3]);
+    try {
+      const Quiver q = generate_quiver(qstep, qstep, mpr);
+      PathParams pp;
+      std::vector<double> ms, parts[3];
+      std::size_t wps = 0;
+      const auto since = [](auto t) {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
+      };
+      for (int k = 0; k <= K; ++k) {
+        const auto t0 = std::chrono::steady_clock::now();
+        const VoxelGrid grid = build_scene_grid(scene, arm, rp);
+        const double a = since(t0);
+        const PathPlan p1 = plan_reach_then_path(arm, q, grid, scene.target, rp, pp);
+        const double b = since(t0);
+        const PathPlan p2 = plan_arbitrary(arm, q, grid, p1.poses.back(), second, rp, pp);
+        const double c = since(t0);
+        wps = p1.waypoints.size() + p2.waypoints.size();
+        if (k > 0) {
+          ms.push_back(c);
+          parts[0].push_back(a);
+          parts[1].push_back(b - a);
+          parts[2].push_back(c - b);
+        }
+      }
+      std::cout << "{\"bench_ms\":" << list(ms, num) << ",\"grid_ms\":" << list(parts[0], num)
+                << ",\"reach_path_ms\":" << list(parts[1], num)
+                << ",\"arbitrary_ms\":" << list(parts[2], num) << ",\"waypoints\":" << wps
+                << "}\n";
+    } catch (const Error& e) {
+      std::cout << "{\"error\":" << static_cast<int>(e.code()) + 1 << "}\n";
+    }
+    return 0;
   }
   try {
     const Quiver q = generate_quiver(qstep, qstep, mpr);
