@@ -107,6 +107,13 @@ static double now_ms() {
 HostSpan::HostSpan(const char* n) : name(n), t0(trace_threshold_ms() >= 0 ? now_ms() : 0.0) {}
 
 HostSpan::~HostSpan() {
+  // RP_CHECK_SPANS=1: report a CUDA error left pending inside the span
+  // (debugging aid: names the host stage whose call went unchecked)
+  static const bool check = std::getenv("RP_CHECK_SPANS") != nullptr;
+  if (check) {
+    const cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess) std::fprintf(stderr, "[span] %s: pending %s\n", name, cudaGetErrorString(e));
+  }
   const double th = trace_threshold_ms();
   if (th < 0) return;
   const double dt = now_ms() - t0;

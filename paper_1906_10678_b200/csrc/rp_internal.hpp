@@ -44,6 +44,9 @@ inline rp_status guarded(F&& f) {
     return RP_OK;
   } catch (const Fail& e) {
     set_last_error(e.msg);
+    // a failed launch or API call leaves its (non-sticky) error pending on
+    // this thread; clear it so the next call does not report it again
+    if (e.code == RP_E_CUDA) (void)cudaGetLastError();
     return e.code;
   } catch (const std::bad_alloc&) {
     set_last_error("internal: host allocation failed");

@@ -1504,11 +1504,11 @@ __device__ __forceinline__ unsigned long long metric_bits(double m) {
 }
 
 __global__ void __launch_bounds__(kBpcThreads, 1) k_bp_cluster(const __grid_constant__ BpArgs A) {
-  // dynamic shared memory: [BpcShared][li: Q x u16][lj: Q x u16]
+  // dynamic shared memory: [BpcShared][li: list_cap x u16][lj: list_cap x u16]
   extern __shared__ __align__(16) unsigned char bpc_smem[];
   BpcShared& S = *reinterpret_cast<BpcShared*>(bpc_smem);
   unsigned short* li = reinterpret_cast<unsigned short*>(bpc_smem + sizeof(BpcShared));
-  unsigned short* lj = li + A.Q;
+  unsigned short* lj = li + A.list_cap;
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = static_cast<int>(cluster.block_rank());
   const int CL = static_cast<int>(cluster.num_blocks());
@@ -1750,14 +1750,14 @@ __global__ void __launch_bounds__(kBpcThreads, 1) k_bp_cluster(const __grid_cons
             const int pos = carry + ex2;
             if (flag >> 16) {
               const int a = pos >> 16;
-              li[a] = static_cast<unsigned short>(idx);
+              if (a < A.list_cap) li[a] = static_cast<unsigned short>(idx);
               if (a < kBpcCiCap) {
                 const float ok = static_cast<float>((__ldg(A.walk1 + (idx >> 5)) >> (idx & 31)) & 1u);
                 S.p1f[a] = make_float4(static_cast<float>(p1.x), static_cast<float>(p1.y),
                                        static_cast<float>(p1.z), ok);
               }
             } else if (flag) {
-              lj[pos & 0xFFFF] = static_cast<unsigned short>(idx);
+              if ((pos & 0xFFFF) < A.list_cap) lj[pos & 0xFFFF] = static_cast<unsigned short>(idx);
             }
             carry += tot2;
             __syncthreads();  // scan_tmp reuse
@@ -1770,6 +1770,15 @@ __global__ void __launch_bounds__(kBpcThreads, 1) k_bp_cluster(const __grid_cons
         }
         long long c1 = prof ? clock64() : 0;
         const int nci = S.nci, ncj = S.ncj;
+        if (nci > A.list_cap || ncj > A.list_cap) {
+          // a cone larger than the shared-memory lists (1-degree quivers
+          // with large relax factors): every CTA built the same lists, so
+          // all leave here together; the host reruns the pass sequenced
+          rebuild();
+          if (rank == 0 && tid == 0) A.state[3] = 2;
+          cluster.sync();
+          return;
+        }
         // ---- S + E in rounds of at most kBpcQueue prefiltered pairs per CTA
         double bm = 1e308;
         long long bo = LLONG_MAX;
@@ -2710,16 +2719,38 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
                                    double cloud_radius, const HostPose* fixed_first,
                                    const HostPose* bias, BpOut* out) {
   HostSpan span_("Planner::backward_pass_device");
-  if (!use_device_pass || factors.size() > static_cast<size_t>(kBpMaxFactors) || q->n > 16384 ||
-      wps.size() < 2)
+  if (!use_device_pass || factors.size() > static_cast<size_t>(kBpMaxFactors) || wps.size() < 2)
     return false;
   cudaStream_t st = ctx->stream;
   const size_t smem = 2 * static_cast<size_t>(q->n) * sizeof(int);
   // the cluster pass (k_bp_cluster) takes coaxial limit-free arms on
-  // generated quivers; RP_BP_COOP=1 forces the cooperative grid pass
+  // generated quivers (up to 65535 directions: 16-bit list entries; the
+  // lists hold what shared memory allows, ~20k entries each, and a cone
+  // larger than that falls back below); RP_BP_COOP=1 forces the
+  // cooperative grid pass (Q <= 16384: two int arrays of Q in shared memory)
   static const bool force_coop = std::getenv("RP_BP_COOP") != nullptr;
+  // shared memory left for the lists: the opt-in maximum per block minus
+  // the kernel's static and BpcShared parts (once per device)
+  static std::mutex cap_mutex;
+  static std::map<int, size_t> list_room;
+  size_t room = 0;
+  {
+    std::lock_guard<std::mutex> lock(cap_mutex);
+    auto it = list_room.find(ctx->device);
+    if (it == list_room.end()) {
+      int optin = 0;
+      RP_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+      cudaFuncAttributes fa{};
+      RP_CUDA(cudaFuncGetAttributes(&fa, k_bp_cluster));
+      const size_t fixed = sizeof(BpcShared) + fa.sharedSizeBytes + 256;
+      it = list_room.emplace(ctx->device, static_cast<size_t>(optin) > fixed ? optin - fixed : 0).first;
+    }
+    room = it->second;
+  }
+  const int list_cap = std::min<int>(q->n, static_cast<int>(room / (2 * sizeof(unsigned short))) & ~7);
   const bool cluster = !force_coop && !ad.any_limit && !ad.has_offsets && q->n_rings > 0 &&
-                       q->n_rings <= kBpcRings;
+                       q->n_rings <= kBpcRings && q->n <= 65535 && list_cap >= 1024;
+  if (!cluster && q->n > 16384) return false;
   if (cluster && !bp_state.p) bp_state.alloc(4, st);
   if (!cluster && bp_blocks == 0) {
     // kernel attribute + occupancy: once per device and shared-memory size
@@ -2843,7 +2874,8 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
     A.qring_c = q->d_ring_c;
     A.qring_s = q->d_ring_s;
     A.qf = q->d_qf;
-    const size_t csmem = sizeof(BpcShared) + 2 * static_cast<size_t>(q->n) * sizeof(unsigned short);
+    A.list_cap = list_cap;
+    const size_t csmem = sizeof(BpcShared) + 2 * static_cast<size_t>(list_cap) * sizeof(unsigned short);
     static const int ctas = [] {
       const char* e = std::getenv("RP_BPC_CTAS");
       const int c = e ? std::atoi(e) : 16;
@@ -2913,6 +2945,7 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
                  "wait %lld publish %lld barrier %lld | max ci-load %lld max eval %lld\n",
                  m, hp[6], hp[7], hp[0], hp[1], hp[2], hp[3], hp[4], hp[5], hp[8], hp[9]);
   }
+  if (hs[3] == 2) return false;  // list overflow: the sequenced pass decides
   out->ok = hs[2] != 0;
   out->failed_index = hs[1];
   out->cancelled = hs[3] != 0;

@@ -133,6 +133,7 @@ struct BpArgs {
   const double* qring_c;  // cos / sin of the ring elevations
   const double* qring_s;
   const float4* qf;
+  int list_cap;  // k_bp_cluster: entries of each shared-memory candidate list (<= Q)
 };
 
 /// Device scratch reused by every waypoint_ik call of a planner.

@@ -12,8 +12,11 @@
   C5_2   512^3, 40 boxes: the grid (sha256) and the first 16 of the bench's
          4096 batched targets: counters, chosen key, path length, refined pose
 
-Run here (where /root/reference exists; minutes of CPU, C5's 512^3 dilation
-alone takes ~4.5 min): python scripts/make_golden_configs.py [case ...]
+  C2_1   C2 at a 1-degree quiver (Q = 41,264): grid, counters, keys, plan
+
+Run where oracle/_ref is built (minutes of CPU; C5's 512^3 dilation alone
+takes ~4.5 min): python scripts/make_golden_configs.py [case ...]
+(GOLDEN_OUT=dir writes elsewhere, e.g. gpurun_out/ on a box with more cores)
 tests/test_gpu_parity_configs.py compares the CUDA path with these files on
 the GPU box, where the reference sources do not exist.
 """
@@ -33,7 +36,7 @@ import ref  # noqa: E402
 from helpers import plan_arrays  # noqa: E402
 from paper_1906_10678_b200 import abi, scenes  # noqa: E402
 
-OUT = os.path.join(ROOT, "tests", "golden", "configs")
+OUT = os.environ.get("GOLDEN_OUT", os.path.join(ROOT, "tests", "golden", "configs"))
 WORKERS = os.cpu_count() or 1
 
 # C4's control ticks (bench.py config_latencies / c4_ticks)
@@ -165,7 +168,16 @@ def c5(arrays):
     return e
 
 
-CASES = {"C2_2": c2, "C3_2": c3, "C4_2": c4, "C5_2": c5}
+def c2_1deg(arrays):
+    """C2 at the paper's finer 1-degree quiver (Q = 41,264): the solve and
+    the plan (the backward pass's cluster kernel with lists sized by shared
+    memory instead of Q)."""
+    sc = scenes.config("C2", 1.0)
+    _, e, _, _ = case_reach_path("C2_1", sc, arrays)
+    return e
+
+
+CASES = {"C2_2": c2, "C3_2": c3, "C4_2": c4, "C5_2": c5, "C2_1": c2_1deg}
 
 
 def main():

@@ -9,6 +9,7 @@ produced (scripts/make_golden_configs.py -> tests/golden/configs/):
         the plan's final pose to the second target (rc and the full plan)
   C4_2  256^3 / 40 boxes: the first plan, then per control tick the overlay
         occupancy (sha256) and replan_dynamic's outcome (and plan)
+  C2_1  C2 at the paper's finer 1-degree quiver (Q = 41,264)
   C5_2  512^3 / 40 boxes: the grid (sha256 of 128 MiB of reference bytes)
         and the first 16 of the 4096 batched targets: counters, solution and
         shortcut counts, chosen kind, path-length bits, segment-1/2 indices,
@@ -76,7 +77,8 @@ def _check_solve(S, want):
 def _reach_path(ctx, name):
     api = _api()
     meta, fx = _load(name)
-    sc = scenes.config(name.split("_")[0], quiver_deg=2.0)
+    cfg, deg = name.split("_")
+    sc = scenes.config(cfg, quiver_deg=float(deg))
     arm, rp, q, g = gpu_problem(ctx, sc)
     _check_grid(g, meta["grid"])
     _check_solve(api.solve_reach(ctx, arm, q, g, sc.target, rp), meta["solve"])
@@ -91,6 +93,13 @@ def _reach_path(ctx, name):
 
 def test_c2_2deg_solve_and_plan(ctx):
     _reach_path(ctx, "C2_2")
+
+
+def test_c2_1deg_solve_and_plan(ctx):
+    """The paper's finer quiver (Q = 41,264, 754 M pairs, 27.5 M solutions):
+    every key and the plan, through the cluster backward pass whose
+    candidate lists are sized by shared memory rather than Q."""
+    _reach_path(ctx, "C2_1")
 
 
 def test_c3_2deg_reach_path_and_arbitrary(ctx):
