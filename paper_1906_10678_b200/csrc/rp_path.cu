@@ -2747,10 +2747,12 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
     }
     room = it->second;
   }
-  const int list_cap = std::min<int>(q->n, static_cast<int>(room / (2 * sizeof(unsigned short))) & ~7);
+  int list_cap = std::min<int>(q->n, static_cast<int>(room / (2 * sizeof(unsigned short))) & ~7);
   const bool cluster = !force_coop && !ad.any_limit && !ad.has_offsets && q->n_rings > 0 &&
                        q->n_rings <= kBpcRings && q->n <= 65535 && list_cap >= 1024;
   if (!cluster && q->n > 16384) return false;
+  if (const char* e = std::getenv("RP_BPC_LIST_CAP"))  // tests: force the overflow fallback
+    list_cap = std::min(list_cap, std::max(64, std::atoi(e)));
   if (cluster && !bp_state.p) bp_state.alloc(4, st);
   if (!cluster && bp_blocks == 0) {
     // kernel attribute + occupancy: once per device and shared-memory size

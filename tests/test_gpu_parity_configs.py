@@ -102,6 +102,25 @@ def test_c2_1deg_solve_and_plan(ctx):
     _reach_path(ctx, "C2_1")
 
 
+def test_c2_1deg_list_overflow_falls_back(ctx, monkeypatch):
+    """Candidate cones larger than the cluster pass's shared-memory lists
+    (forced here with a 256-entry cap; the 1-degree segment-2 cone holds
+    ~1k directions) leave the pass early and the sequenced pass decides:
+    the same plan as the reference's."""
+    api = _api()
+    meta, fx = _load("C2_1")
+    sc = scenes.config("C2", quiver_deg=1.0)
+    arm, rp, q, g = gpu_problem(ctx, sc)
+    monkeypatch.setenv("RP_BPC_LIST_CAP", "256")
+    ctx.enable_timing(True)
+    ctx.reset_timing()
+    rc, plan = api.plan_reach_then_path(ctx, arm, q, g, sc.target, rp)
+    assert rc == meta["plan_rc"] == 0
+    assert ctx.kernel_time("wik_pairs")[1] > 0  # the sequenced pass ran
+    ctx.enable_timing(False)
+    assert_plan_matches_fixture(plan.summary(), fx, meta["plan"], "plan0_", UNFOLD_TOL)
+
+
 def test_c3_2deg_reach_path_and_arbitrary(ctx):
     api, sc, arm, rp, q, g, meta, fx, plan, s = _reach_path(ctx, "C3_2")
     assert list(sc.extra["second_target"]) == meta["second_target"]
