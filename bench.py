@@ -406,6 +406,8 @@ def run_ours(args, sc):
     vox = None if args.no_voxel else voxel_update(ctx, torch, stream)
     # -- C5: 4096 batched reach queries sharded over the ranks
     batch = None if args.no_batch else batch_queries(args, ctx, torch, stream, rank, world)
+    # -- one solve_reach split over the ranks (C2 at the 1-degree quiver)
+    split = None if args.no_batch else split_solve(ctx, torch, stream, rank, world)
     # -- latency of the other BASELINE configurations (rank 0's view)
     configs = config_latencies(ctx, torch, stream) if not args.no_configs else None
     if rank != 0:
@@ -431,6 +433,7 @@ def run_ours(args, sc):
                   for s in last],
         "result_digest": plan_digest(last),
         "batch": batch,
+        "split_solve": split,
         "configs": configs,
         "paper_ms": PAPER_MS,
     }
@@ -553,6 +556,42 @@ def batch_queries(args, ctx, torch, stream, rank, world):
                         + (f"built as {world} z-slabs + NCCL all-gather" if world > 1
                            else "built whole"),
             "solved": ok, "results_sha256": h.hexdigest()[:16], "cpu_subset": cpu}
+
+
+def split_solve(ctx, torch, stream, rank, world, reps=5):
+    """SURVEY §8e's single-solve split: C2's solve_reach at the paper's
+    1-degree quiver (Q = 41,264: 754 M pairs, 27.5 M solutions), survivor
+    rows split over the ranks (rp_solve_reach_part), the parts' summaries
+    all-gathered and merged (shard.solve_reach_split; parity:
+    tests/test_gpu_split.py). Device time per solve, max over ranks."""
+    from paper_1906_10678_b200 import api, scenes, shard
+    sc = scenes.config("C2", quiver_deg=1.0)
+    arm, rp = sc.arm(), sc.reach_params()
+    q = api.Quiver(ctx, sc.quiver_step(), sc.quiver_step(), sc.min_per_ring)
+    g = api.Grid.scene(ctx, scenes.BOUNDS_MIN, scenes.BOUNDS_MAX, sc.voxel_size, sc.obstacles(),
+                       arm, rp)
+    shard.solve_reach_split(ctx, arm, q, g, sc.target, rp, rank, world)  # warm-up
+    ms, m = [], None
+    for _ in range(reps):
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        m = shard.solve_reach_split(ctx, arm, q, g, sc.target, rp, rank, world)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    t = statistics.median(ms)
+    if world > 1:
+        tt = torch.tensor([t], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t = float(tt[0])
+    return {"workload": "C2 solve_reach (128^3, 12 boxes) at a 1-degree quiver, survivor rows "
+                        f"split over {world} rank(s), summaries all-gathered and merged",
+            "ms": t, "pairs": m["counters"]["pair_candidates"], "solutions": m["n_solutions"],
+            "chosen_index": m["chosen"]["index"] if m["chosen"] else None,
+            "gpairs_per_s": m["counters"]["pair_candidates"] / (t * 1e-3) / 1e9}
 
 
 _CPU_BATCH_CODE = (

@@ -338,6 +338,20 @@ rp_status rp_short_reach_scan(rp_ctx* ctx, const rp_grid* g, const rp_arm* arm,
 rp_status rp_solve_reach(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q, const rp_grid* g,
                          const double target[3], const rp_reach_params* rp,
                          rp_solution_set** out);
+/* One part of a solve split over devices [solve_reach's worker split,
+ * src/reach_solver.cpp:503-535, by segment-1 survivor rows instead of j]:
+ * part p of P solves the rows [S1*p/P, S1*(p+1)/P). Its set holds the part's
+ * keys (global indices; the parts' key lists concatenate, in part order, to
+ * the whole set's canonical list), segment-2 counters and best solution;
+ * segment-1 counters are the whole prune's in every part and segment-1
+ * shortcuts are part 0's. Merging (paper_1906_10678_b200/shard.py
+ * solve_reach_split): counters = part 0's segment-1 fields + the sums of the
+ * rest; the chosen solution = the parts' select_solution results compared
+ * as the reference does (any shortcut first, by path_length then part;
+ * else (length, key)). parts = 1 is rp_solve_reach. */
+rp_status rp_solve_reach_part(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q,
+                              const rp_grid* g, const double target[3], const rp_reach_params* rp,
+                              int32_t part, int32_t parts, rp_solution_set** out);
 rp_status rp_solution_set_stats(const rp_solution_set* s, rp_solve_stats* stats);
 rp_status rp_solution_set_sizes(const rp_solution_set* s, int64_t* n_solutions,
                                 int64_t* n_shortcuts);

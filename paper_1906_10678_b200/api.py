@@ -85,6 +85,8 @@ def lib():
         "rp_prune_segment1": ([vp, P(abi.Arm), vp, vp, vp, C.c_int32, P(abi.ReachParams),
                                P(C.c_int32), C.c_int32, P(C.c_int32), P(abi.SolveStats)], C.c_int32),
         "rp_solve_reach": ([vp, P(abi.Arm), vp, vp, d3, P(abi.ReachParams), P(vp)], C.c_int32),
+        "rp_solve_reach_part": ([vp, P(abi.Arm), vp, vp, d3, P(abi.ReachParams), C.c_int32,
+                                 C.c_int32, P(vp)], C.c_int32),
         "rp_solution_set_stats": ([vp, P(abi.SolveStats)], C.c_int32),
         "rp_solution_set_sizes": ([vp, P(C.c_int64), P(C.c_int64)], C.c_int32),
         "rp_solution_set_keys": ([vp, vp, C.c_int64], C.c_int32),
@@ -493,6 +495,16 @@ def solve_reach(ctx, arm, quiver, grid, target, rp) -> SolutionSet:
     h = C.c_void_p()
     _check(lib().rp_solve_reach(ctx.h, C.byref(arm), quiver.h, grid.h, d3(target), C.byref(rp),
                                 C.byref(h)))
+    return SolutionSet(ctx, h, target, rp.n_samples)
+
+
+def solve_reach_part(ctx, arm, quiver, grid, target, rp, part, parts) -> SolutionSet:
+    """Part `part` of `parts` of solve_reach (rp_solve_reach_part): the
+    segment-1 survivor rows [S1*part/parts, S1*(part+1)/parts); see
+    shard.solve_reach_split for the merge."""
+    h = C.c_void_p()
+    _check(lib().rp_solve_reach_part(ctx.h, C.byref(arm), quiver.h, grid.h, d3(target),
+                                     C.byref(rp), part, parts, C.byref(h)))
     return SolutionSet(ctx, h, target, rp.n_samples)
 
 

@@ -162,7 +162,8 @@ __global__ void k_surv_data(SolveDev a, const int* __restrict__ idx, int S1, Sur
 /// seg2_worker over all (survivor, j) pairs; see the file head.
 template <bool EIGHT, bool GENERAL, bool B1>
 __global__ void __launch_bounds__(256) k_seg2(SolveDev a, const SurvDev* __restrict__ sv,
-                                              int64_t npairs, uint32_t* __restrict__ sol_bits,
+                                              int64_t p_lo, int64_t npairs,
+                                              uint32_t* __restrict__ sol_bits,
                                               unsigned long long* ctr, long long* sc_list,
                                               unsigned* sc_count, BestRec* __restrict__ block_best) {
   unsigned c_lim = 0, c_clear = 0, c_gt = 0, c_gp = 0, c_jp = 0, c_v3 = 0, c_sol = 0;
@@ -175,10 +176,12 @@ __global__ void __launch_bounds__(256) k_seg2(SolveDev a, const SurvDev* __restr
   const double L1 = arm.L[0], L2 = arm.L[1], L3 = arm.L[2];
   const double min_sep = 2.0 * arm.arm_radius;
 
-  for (int64_t base = warp_id * 32; base < npairs; base += nwarps * 32) {
+  // pairs [p_lo, npairs) (a part of the solve: whole survivor rows); warps
+  // start at 32-aligned pair indices so the B == 1 ballot stores whole words
+  for (int64_t base = (p_lo & ~int64_t{31}) + warp_id * 32; base < npairs; base += nwarps * 32) {
     const int64_t p = base + lane;
     bool solbit = false;
-    if (p < npairs) {
+    if (p >= p_lo && p < npairs) {
       const int s = static_cast<int>(p / a.Q);
       const int j = static_cast<int>(p - static_cast<int64_t>(s) * a.Q);
       const V3 dir2 = qvec(a, j);
@@ -372,7 +375,7 @@ __global__ void k_row_skip(SolveDev a, const SurvDev* __restrict__ sv, int S1, C
 }
 
 template <bool EIGHT>
-__global__ void __launch_bounds__(256, 4) k_seg2_rows(SolveDev a, const SurvDev* __restrict__ sv, int S1,
+__global__ void __launch_bounds__(256, 4) k_seg2_rows(SolveDev a, const SurvDev* __restrict__ sv, int s_lo, int s_hi,
                                                    uint32_t* __restrict__ sol_bits,
                                                    unsigned long long* ctr, long long* sc_list,
                                                    unsigned* sc_count, BestRec* __restrict__ block_best,
@@ -404,9 +407,9 @@ __global__ void __launch_bounds__(256, 4) k_seg2_rows(SolveDev a, const SurvDev*
     int u = 0;
     if (lane == 0) u = atomicAdd(unit_ctr, 1);
     u = __shfl_sync(FULL, u, 0);
-    if (u >= S1 * nchunk) break;
-    const int s = u / nchunk;
-    const int chunk = u - s * nchunk;
+    if (u >= (s_hi - s_lo) * nchunk) break;
+    const int s = s_lo + u / nchunk;  // survivor rows [s_lo, s_hi): this part's
+    const int chunk = u - (s - s_lo) * nchunk;
     const int jbeg = chunk * kChunk;
     const int jend = min(a.Q, jbeg + kChunk);
     const SurvDev& h = sv[s];
@@ -994,8 +997,10 @@ static HostShortcut host_shortcut(const rp_solution_set* s, const ShortcutRec& r
 }
 
 rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q, const rp_grid* g,
-                             V3 target, const rp_reach_params& rp) {
+                             V3 target, const rp_reach_params& rp, int part, int parts) {
   HostSpan span_("solve_reach");
+  require(parts >= 1 && part >= 0 && part < parts, RP_E_INVALID_PARAMETER,
+          "part must be in [0, parts)");
   validate_arm(arm);
   validate_reach(rp);
   if (rp.mode == RP_MODE_8DOF) {
@@ -1091,29 +1096,37 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
       launch(ctx, "seg1", k_surv_data, dim3(nblk(S1, 128)), dim3(128), 0, a,
              static_cast<const int*>(surv_idx.p), S1, s->surv.p);
     s->surv_i.assign(surv_all.begin(), surv_all.begin() + S1);
+    // this part's survivor rows (the whole set for parts == 1); the pair and
+    // key indices stay global, so parts' keys concatenate in canonical order
+    const int s_lo = static_cast<int>(static_cast<int64_t>(S1) * part / parts);
+    const int s_hi = static_cast<int>(static_cast<int64_t>(S1) * (part + 1) / parts);
+    s->part = part;
+    s->parts = parts;
+    if (part != 0) sc_count.zero();  // segment-1 hypotheses belong to part 0
 
     s->n_pairs = static_cast<int64_t>(S1) * q->n;
     const int64_t nbits = s->n_pairs * s->B;
     const int64_t nwords = (nbits + 31) / 32 + 1;
     s->sol_bits.alloc(nwords, st);
     const bool B1 = s->B == 1;
-    if (!B1) s->sol_bits.zero();
+    if (!B1 || parts > 1) s->sol_bits.zero();
     const bool general = a.arm.any_limit || a.arm.has_offsets || (rp.cone_precheck && eight);
     const int threads = 256;
     int blocks = ctx->sm_count * 8;
-    const int64_t need = (s->n_pairs + threads - 1) / threads;
+    const int64_t p_lo = static_cast<int64_t>(s_lo) * q->n, p_hi = static_cast<int64_t>(s_hi) * q->n;
+    const int64_t need = (p_hi - p_lo + threads - 1) / threads;
     if (need < blocks) blocks = static_cast<int>(std::max<int64_t>(1, need));
     DevBuf<BestRec> bb(blocks, st), best(1, st);
-    if (s->n_pairs > 0) {
+    if (p_hi > p_lo) {
       auto run = [&](auto kern) {
         launch(ctx, "seg2", kern, dim3(blocks), dim3(threads), 0, a,
-               static_cast<const SurvDev*>(s->surv.p), s->n_pairs, s->sol_bits.p, ctr.p,
+               static_cast<const SurvDev*>(s->surv.p), p_lo, p_hi, s->sol_bits.p, ctr.p,
                sc_list.p, sc_count.p, bb.p);
       };
       static const bool flat = std::getenv("RP_SEG2_FLAT") != nullptr;
       if (!general && B1 && !flat) {
         s->sol_bits.zero();
-        const int64_t units = static_cast<int64_t>(S1) * ((q->n + 1023) / 1024);
+        const int64_t units = static_cast<int64_t>(s_hi - s_lo) * ((q->n + 1023) / 1024);
         const int rblocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks, (units + 7) / 8)));
         DevBuf<int> unit_ctr(1, st);
         unit_ctr.zero();
@@ -1137,7 +1150,7 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
         if (!grid_seg2_cache(g, q, arm, rp.n_samples, &c2bits, &c2ok)) c2bits = nullptr, c2ok = nullptr;
         auto runr = [&](auto kern) {
           launch(ctx, "seg2", kern, dim3(rblocks), dim3(threads), 0, a,
-                 static_cast<const SurvDev*>(s->surv.p), S1, s->sol_bits.p, ctr.p, sc_list.p,
+                 static_cast<const SurvDev*>(s->surv.p), s_lo, s_hi, s->sol_bits.p, ctr.p, sc_list.p,
                  sc_count.p, bb.p, unit_ctr.p, static_cast<const uint8_t*>(kskip.p),
                  static_cast<const uint8_t*>(kend_b.p), c2bits, c2ok);
         };
@@ -1158,7 +1171,7 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
     BestRec hb{0.0, -1};
     copy_to_host_many(ctx, {{hc, ctr.p, sizeof(hc)},
                             {&nsc, sc_count.p, sizeof(unsigned)},
-                            {&hb, best.p, s->n_pairs > 0 ? sizeof(BestRec) : 0}});
+                            {&hb, best.p, p_hi > p_lo ? sizeof(BestRec) : 0}});
     require(nsc <= kShortcutCap, RP_E_CAPACITY_EXCEEDED, "too many near-encounter hypotheses");
 
     rp_solve_stats& S = s->stats;
@@ -1167,7 +1180,7 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
     S.seg1_limit_pass = hc[C_SEG1_LIMIT];
     S.seg1_reach_pass = hc[C_SEG1_REACH];
     S.seg1_survivors = hc[C_SEG1_SURV];
-    S.pair_candidates = s->n_pairs;
+    S.pair_candidates = p_hi - p_lo;
     S.seg2_limit_pass = hc[C_SEG2_LIMIT];
     S.seg2_clear_pass = hc[C_SEG2_CLEAR];
     S.gap_tested = hc[C_GAP_TESTED];
@@ -1392,6 +1405,14 @@ rp_status rp_solve_reach(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q, con
                          const double target[3], const rp_reach_params* rp, rp_solution_set** out) {
   return guarded([&] {
     *out = solve_reach(ctx, *arm, q, g, V3{target[0], target[1], target[2]}, *rp);
+  });
+}
+
+rp_status rp_solve_reach_part(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q,
+                              const rp_grid* g, const double target[3], const rp_reach_params* rp,
+                              int32_t part, int32_t parts, rp_solution_set** out) {
+  return guarded([&] {
+    *out = solve_reach(ctx, *arm, q, g, V3{target[0], target[1], target[2]}, *rp, part, parts);
   });
 }
 

@@ -194,6 +194,7 @@ struct rp_solution_set {
   rp::SolveDev sd{};
   double target[3] = {0, 0, 0};
   int S1 = 0;
+  int part = 0, parts = 1;  // a part of a split solve (solve_reach)
   rp::DevBuf<rp::SurvDev> surv;
   std::vector<int> surv_i;
   int B = 0;
@@ -215,8 +216,15 @@ struct rp_solution_set {
 
 namespace rp {
 /// solve_reach into a fresh set (throws Fail).
+/// solve_reach (src/reach_solver.cpp:480-546); part / parts > 1 solves the
+/// survivor rows [S1 * part / parts, S1 * (part + 1) / parts) only (the
+/// reference's worker split, src/reach_solver.cpp:503-516, by rows instead
+/// of j so that the parts' keys concatenate in canonical order): segment-1
+/// counters are the whole prune's, segment-2 counters, keys, the best
+/// solution and the segment-2 shortcuts the part's, and segment-1 shortcuts
+/// belong to part 0.
 rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q, const rp_grid* g,
-                             V3 target, const rp_reach_params& rp);
+                             V3 target, const rp_reach_params& rp, int part = 0, int parts = 1);
 void ensure_keys(rp_solution_set* s);
 /// Materialise solutions by canonical ordinal into device poses.
 void materialize_solutions(rp_solution_set* s, const long long* d_ordinals_or_null,

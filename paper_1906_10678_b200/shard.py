@@ -1,5 +1,5 @@
-"""Multi-GPU sharding of batched reach queries and of the grid build
-(SURVEY.md §8e, C5).
+"""Multi-GPU sharding of batched reach queries, of one reach solve and of
+the grid build.
 
 The queries are independent, so the targets are split into contiguous
 blocks, one per rank (one process per GPU), each rank solves its block with
@@ -216,3 +216,99 @@ def dilate_grid_sharded(ctx, grid, radius: float, rank: int, world: int):
         import torch
         torch.cuda.synchronize()
     return grid
+
+
+# ---- one solve_reach split over ranks (SURVEY §8e "single solve_reach") ----
+#
+# The reference splits a solve's j range over worker threads and merges the
+# workers' solutions by key (src/reach_solver.cpp:503-535). Here each rank
+# solves a contiguous block of segment-1 survivor rows on its own GPU
+# (rp_solve_reach_part): rows ascend with the key's leading index, so the
+# parts' key lists concatenated in rank order ARE the canonical list, and
+# the merge is a gather of small per-part summaries, no k-way merge.
+
+SEG1_FIELDS = ("seg1_candidates", "seg1_limit_pass", "seg1_reach_pass", "seg1_survivors")
+
+
+def part_summary(S, part: int, with_keys: bool = False) -> dict:
+    """What a part contributes to the merge: its counters, sizes, its own
+    select_solution (the reference's rule within the part) with the chosen
+    pose or shortcut, and optionally its canonical keys."""
+    from . import abi
+    ns, nc = S.sizes()
+    out = {"part": part, "counters": S.stats().counters(), "n_solutions": ns,
+           "n_shortcuts": nc, "chosen": None}
+    if ns + nc:
+        c = S.select()
+        out["chosen"] = {"kind": int(c.kind), "index": int(c.index),
+                         "path_length": float(c.path_length)}
+        if c.kind == abi.RP_CHOSEN_REACH_POSE:
+            p, w = S.pose(c.index)
+            out["chosen"]["pose"] = (bytes(p), w)
+        else:
+            sc, w = S.shortcut(c.index)
+            out["chosen"]["shortcut"] = (bytes(sc), w)
+    if with_keys:
+        out["keys"] = S.keys()
+    return out
+
+
+def merge_parts(parts: list[dict]) -> dict:
+    """The whole solve from its parts (in part order): counters = part 0's
+    segment-1 fields + the sums of the others; solutions and shortcuts
+    indexed globally (earlier parts' counts first); the chosen solution by
+    select_solution's rule (src/reach_solver.cpp:548-577): any shortcut wins
+    by smallest path_length, ties to the earlier in canonical order (the
+    earlier part); else the smallest path length, ties to the earlier key
+    (the earlier part)."""
+    from . import abi
+    parts = sorted(parts, key=lambda p: p["part"])
+    if [p["part"] for p in parts] != list(range(len(parts))):
+        raise ValueError("parts must be 0..P-1")
+    counters = {}
+    for name in parts[0]["counters"]:
+        if name in SEG1_FIELDS:
+            counters[name] = parts[0]["counters"][name]
+        else:
+            counters[name] = sum(p["counters"][name] for p in parts)
+    n_sol = sum(p["n_solutions"] for p in parts)
+    n_sc = sum(p["n_shortcuts"] for p in parts)
+    best = None
+    sol_base = sc_base = 0
+    for p in parts:
+        c = p["chosen"]
+        if c is not None:
+            sc = c["kind"] != abi.RP_CHOSEN_REACH_POSE
+            cand = (0 if sc else 1, c["path_length"], p["part"])
+            if best is None or cand < best[0]:
+                g = dict(c, part=p["part"],
+                         index=c["index"] + (sc_base if sc else sol_base))
+                best = (cand, g)
+        sol_base += p["n_solutions"]
+        sc_base += p["n_shortcuts"]
+    out = {"counters": counters, "n_solutions": n_sol, "n_shortcuts": n_sc,
+           "chosen": best[1] if best else None}
+    if all("keys" in p for p in parts):
+        out["keys"] = np.concatenate([p["keys"] for p in parts]) if parts else np.zeros((0, 3))
+    return out
+
+
+def solve_reach_split(ctx, arm, quiver, grid, target, rp, rank: int, world: int,
+                      with_keys: bool = False) -> dict:
+    """solve_reach over `world` ranks (one GPU each, every rank holding the
+    grid and quiver): this rank's part, then an all-gather of the parts'
+    summaries (torch.distributed object collective; a few hundred bytes per
+    part unless with_keys) and the merge on every rank."""
+    from . import api
+    S = api.solve_reach_part(ctx, arm, quiver, grid, target, rp, rank, world)
+    return gather_merge(part_summary(S, rank, with_keys), world)
+
+
+def gather_merge(mine: dict, world: int) -> dict:
+    """All-gather the parts' summaries and merge them (every rank)."""
+    if world == 1:
+        return merge_parts([mine])
+    import torch.distributed as dist
+    allp = [None] * world
+    dist.all_gather_object(allp, mine)
+    return merge_parts(allp)

@@ -187,3 +187,84 @@ def test_exchange_halos_two_gloo_ranks(nz, reach):
             have = max(0, lo - reach) <= z < min(nz, hi + reach)
             want = np.arange(wpp) + 1000 * (z + 1) if have else np.zeros(wpp, np.int64)
             assert np.array_equal(arr[z], want), (r, z)
+
+
+# ---- one solve_reach split over ranks: the merge of the parts' summaries ----
+
+def _counters(**over):
+    c = {n: 0 for n, _ in abi.SolveStats._fields_ if n != "wall_ms"}
+    c.update(over)
+    return c
+
+
+def _part(part, n_sol, n_sc, chosen, **ctr):
+    seg1 = dict(seg1_candidates=100, seg1_limit_pass=100, seg1_reach_pass=40, seg1_survivors=30)
+    return {"part": part, "counters": _counters(**seg1, **ctr), "n_solutions": n_sol,
+            "n_shortcuts": n_sc, "chosen": chosen,
+            "keys": np.array([[part, k, -1] for k in range(n_sol)], np.int32).reshape(-1, 3)}
+
+
+def _pose(index, length):
+    return {"kind": abi.RP_CHOSEN_REACH_POSE, "index": index, "path_length": length}
+
+
+def _short(index, length):
+    return {"kind": 1, "index": index, "path_length": length}
+
+
+def test_merge_parts_counters_and_reach_pose():
+    parts = [_part(0, 10, 0, _pose(5, 2.0), pair_candidates=3000, solutions=10),
+             _part(1, 7, 0, _pose(3, 1.5), pair_candidates=3100, solutions=7),
+             _part(2, 0, 0, None, pair_candidates=2900)]
+    m = shard.merge_parts(list(reversed(parts)))  # any gather order
+    assert m["counters"]["seg1_survivors"] == 30  # segment-1 fields once
+    assert m["counters"]["pair_candidates"] == 9000 and m["counters"]["solutions"] == 17
+    assert (m["n_solutions"], m["n_shortcuts"]) == (17, 0)
+    assert m["chosen"]["part"] == 1 and m["chosen"]["index"] == 10 + 3
+    assert [tuple(k) for k in m["keys"][:11]][-1] == (1, 0, -1)
+
+
+def test_merge_parts_ties_and_shortcuts():
+    # equal lengths: the earlier part (smaller canonical key) wins
+    m = shard.merge_parts([_part(0, 4, 0, _pose(2, 1.25)), _part(1, 9, 0, _pose(0, 1.25))])
+    assert m["chosen"]["part"] == 0 and m["chosen"]["index"] == 2
+    # any shortcut beats every reach pose; shortcuts are indexed across parts
+    m = shard.merge_parts([_part(0, 4, 2, _short(1, 3.0)), _part(1, 9, 1, _short(0, 3.0)),
+                           _part(2, 5, 0, _pose(0, 0.1))])
+    assert m["chosen"]["kind"] != abi.RP_CHOSEN_REACH_POSE
+    assert m["chosen"]["part"] == 0 and m["chosen"]["index"] == 1
+    m = shard.merge_parts([_part(0, 4, 0, _pose(0, 0.5)), _part(1, 9, 1, _short(0, 3.0))])
+    assert m["chosen"]["part"] == 1 and m["chosen"]["index"] == 0
+
+
+def _split_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mine = _part(rank, 3 + rank, 0, _pose(rank, 2.0 - 0.25 * rank), solutions=3 + rank)
+        m = shard.gather_merge(mine, world)
+        q.put((rank, m["n_solutions"], m["chosen"]["part"], m["chosen"]["index"],
+               m["keys"].tobytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_split_solve_merge_gloo_ranks(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_split_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = shard.merge_parts([_part(r, 3 + r, 0, _pose(r, 2.0 - 0.25 * r), solutions=3 + r)
+                              for r in range(world)])
+    for rank, n, part, index, keys in got:
+        assert n == want["n_solutions"] == sum(3 + r for r in range(world))
+        assert (part, index) == (world - 1, want["chosen"]["index"])
+        assert keys == want["keys"].tobytes()
