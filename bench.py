@@ -403,6 +403,7 @@ def run_ours(args, sc):
     kernel_ms = {n: round(v[0], 4) for n, v in kt.items() if v[1]}
     kernel_launches = {n: int(v[1]) for n, v in kt.items() if v[1]}
     dominant = max(kernel_ms, key=kernel_ms.get)
+    dom_roof = dominant_roofline(ctx, arm, q, sc, api, scenes)
     vox = None if args.no_voxel else voxel_update(ctx, torch, stream)
     # -- C5: 4096 batched reach queries sharded over the ranks
     batch = None if args.no_batch else batch_queries(args, ctx, torch, stream, rank, world)
@@ -427,6 +428,7 @@ def run_ours(args, sc):
         "voxel_update": vox["summary"] if vox else None,
         "kernel_ms_per_step": kernel_ms,
         "kernel_launches_per_step": kernel_launches,
+        "roofline_dominant": dom_roof,
         "dominant_kernel": {"name": dominant, "ms": kernel_ms[dominant],
                             "share": kernel_ms[dominant] / max(ms, 1e-9)},
         "plans": [{"kind": s["kind"], "notes": s["notes"], "waypoints": len(s["waypoints"])}
@@ -482,6 +484,43 @@ def facade_e2e(sc, steps=5):
             "stages_ms": {k: statistics.median(js[k]) for k in ("grid_ms", "reach_path_ms",
                                                                   "arbitrary_ms") if k in js},
             "waypoints": js["waypoints"]}
+
+
+def dominant_roofline(ctx, arm, q, sc, api, scenes):
+    """The step's dominant kernel, the segment-2 expansion (k_seg2_rows), on
+    its own roofline: SURVEY §8d bounds seg1/seg2 by fp64 issue + L2 gathers
+    (the 2 MiB grid is L2-resident), not HBM, so the live rate is pairs/s of
+    the step's first solve (cold walk cache) and the fraction is ncu's
+    issue-slot utilisation of the same launch (profiles/)."""
+    rp = sc.reach_params()
+    g = api.Grid.scene(ctx, scenes.BOUNDS_MIN, scenes.BOUNDS_MAX, sc.voxel_size, sc.obstacles(),
+                       arm, rp)
+    ctx.enable_timing(True)
+    ctx.reset_timing()
+    S = api.solve_reach(ctx, arm, q, g, sc.target, rp)
+    ctx.synchronize()
+    ms, _ = ctx.kernel_time("seg2")
+    ctx.enable_timing(False)
+    pairs = S.stats().pair_candidates
+    out = {"kernel": "k_seg2_rows<EIGHT> (segment-2 expansion + gap intersection, first solve "
+                     "of the step)", "bound": "issue (fp64 + L2 gathers, SURVEY 8d)",
+           "achieved": pairs / (ms * 1e-3) / 1e9, "unit": "G pairs/s", "pairs": pairs,
+           "ms": ms, "algorithmic_bytes_per_launch": sc.n ** 3 / 8 + pairs / 8,
+           "algorithmic_bytes_def": "the bit grid once + one result bit per pair"}
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "r2_c3_seg2_ncu.json")))
+        m = prof["launches"][0]["metrics"]
+        out.update({
+            "frac": float(m["smsp__issue_active.avg.pct_of_peak_sustained_active"][0]) / 100,
+            "frac_def": "ncu smsp__issue_active: the share of issue slots used (the issue "
+                        "roofline); fp64 pipe " + prof["launches"][0]["pipes_pct_of_peak"]["fp64"][:4]
+                        + "% of peak",
+            "traffic": 1e6 * (float(m["dram__bytes_read.sum"][0])
+                              + float(m["dram__bytes_write.sum"][0])),
+            "traffic_source": "profiles/r2_c3_seg2_ncu.json (ncu --set full, one launch)"})
+    except (OSError, KeyError, ValueError, IndexError):
+        pass
+    return out
 
 
 def C_SIZEOF_OBSTACLE():
