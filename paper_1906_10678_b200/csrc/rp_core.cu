@@ -47,6 +47,11 @@ void launch_begin(rp_ctx* ctx, const char* name, cudaEvent_t* ev) {
   }
   RP_CUDA(cudaEventRecord(e, ctx->stream));
   *ev = e;
+  if (!ctx->tl_armed) {  // the timeline's origin: this launch's start
+    if (!ctx->tl_base) RP_CUDA(cudaEventCreate(&ctx->tl_base));
+    RP_CUDA(cudaEventRecord(ctx->tl_base, ctx->stream));
+    ctx->tl_armed = true;
+  }
   (void)name;
 }
 
@@ -70,16 +75,17 @@ static void drain_timing(rp_ctx* ctx) {
   // RP_TIMELINE=1: the device timeline of the timed launches (offsets from
   // the first launch, and the idle gap before each one)
   static const bool timeline = std::getenv("RP_TIMELINE") != nullptr;
-  float prev_end = 0.f;
   for (auto& t : ctx->pending) {
     float ms = 0.f;
     RP_CUDA(cudaEventElapsedTime(&ms, t.start, t.stop));
     if (timeline) {
+      // offsets from the first launch since reset_timing (across drains),
+      // and the idle gap since the previous launch ended on this stream
       float at = 0.f;
-      RP_CUDA(cudaEventElapsedTime(&at, ctx->pending.front().start, t.start));
-      std::fprintf(stderr, "[tl] %9.3f ms +%8.3f gap %8.3f %s\n", at, ms, at - prev_end,
+      RP_CUDA(cudaEventElapsedTime(&at, ctx->tl_base, t.start));
+      std::fprintf(stderr, "[tl] %9.3f ms +%8.3f gap %8.3f %s\n", at, ms, at - ctx->tl_prev_end,
                    t.name.c_str());
-      prev_end = at + ms;
+      ctx->tl_prev_end = at + ms;
     }
     auto& acc = ctx->kernel_ms[t.name];
     acc.first += ms;
@@ -420,6 +426,7 @@ rp_status rp_ctx_destroy(rp_ctx* ctx) {
       cudaEventDestroy(t.stop);
     }
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
+    if (ctx->tl_base) cudaEventDestroy(ctx->tl_base);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->readback) cudaFreeHost(ctx->readback);
     for (cudaEvent_t e : ctx->upload_ev) cudaEventDestroy(e);
@@ -469,6 +476,8 @@ rp_status rp_ctx_reset_timing(rp_ctx* ctx) {
   return guarded([&] {
     drain_timing(ctx);
     ctx->kernel_ms.clear();
+    ctx->tl_armed = false;
+    ctx->tl_prev_end = 0.f;
   });
 }
 

@@ -73,6 +73,9 @@ struct rp_ctx {
   int64_t launches = 0;
   std::vector<rp::TimedLaunch> pending;
   std::vector<cudaEvent_t> event_pool;
+  cudaEvent_t tl_base = nullptr;  // RP_TIMELINE: start of the first launch since reset_timing
+  bool tl_armed = false;
+  float tl_prev_end = 0.f;
   std::map<std::string, std::pair<double, int64_t>> kernel_ms;
   int sm_count = 148;
   // Small pinned staging buffer for scalar read-backs.

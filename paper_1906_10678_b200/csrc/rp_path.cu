@@ -2199,6 +2199,13 @@ __global__ void k_refine(ArmDev arm, DevPose ap, V3 target, int mode, PoseOpOut*
   r.status = refine_pose(arm, r.pose, target, mode, &r.msg);
   *out = r;
 }
+/// k_refine of a pose already on the device (a materialised solution).
+__global__ void k_refine_from(ArmDev arm, const DevPose* ap, V3 target, int mode, PoseOpOut* out) {
+  PoseOpOut r{};
+  r.pose = *ap;
+  r.status = refine_pose(arm, r.pose, target, mode, &r.msg);
+  *out = r;
+}
 
 /// append_trail on a 3-segment chain (src/path_planner.cpp:127-150).
 __global__ void k_append_trail(rpd::GridView g, ArmDev arm, DevPose ch, int n_opts, V3 o0, V3 o1,
@@ -2969,6 +2976,17 @@ HostPose Planner::refine(const HostPose& approx, V3 target, int mode) {
   launch(ctx, "refine", k_refine, dim3(1), dim3(1), 0, ad, to_dev(approx), target, mode,
          opout.p);
   PoseOpOut r = run_pose_op(*this);
+  if (r.status) fail(r.status, refine_msg(r.msg));
+  HostPose h = host_pose_from_dev(r.pose);
+  h.waypoints = approx.waypoints;  // PoseChain out = approx
+  return h;
+}
+
+void Planner::refine_launch(const DevPose* d_approx, V3 target, int mode) {
+  launch(ctx, "refine", k_refine_from, dim3(1), dim3(1), 0, ad, d_approx, target, mode, opout.p);
+}
+
+HostPose Planner::refine_result(const PoseOpOut& r, const HostPose& approx) {
   if (r.status) fail(r.status, refine_msg(r.msg));
   HostPose h = host_pose_from_dev(r.pose);
   h.waypoints = approx.waypoints;  // PoseChain out = approx

@@ -73,6 +73,12 @@ struct Cand {
   int64_t ordinal = -1;  // in its solution set (reach) or shortcut list
   HostPose pose;         // unrefined solution pose with its 4n waypoints
   HostShortcut sc;
+  // exact_refine of `pose` toward `refined_target` in `refined_mode`,
+  // computed in the same device round trip as the selection (select_cand)
+  bool has_refined = false;
+  int refined_mode = -1;
+  V3 refined_target{0, 0, 0};
+  PoseOpOut refined{};
 };
 
 struct PassOptions {
@@ -225,7 +231,12 @@ Build make_candidate_build(Planner& P, const Cand& cand, V3 target) {
       out.waypoints.insert(out.waypoints.end(), cand.pose.waypoints.begin(),
                            cand.pose.waypoints.begin() + traversal * n);
       if (cand.pose.nseg == 4) {
-        out.anchor = P.refine(cand.pose, target, P.rp.refine_triangle_8dof ? 1 : 0);
+        const int mode = P.rp.refine_triangle_8dof ? 1 : 0;
+        out.anchor = cand.has_refined && cand.refined_mode == mode &&
+                             cand.refined_target.x == target.x && cand.refined_target.y == target.y &&
+                             cand.refined_target.z == target.z
+                         ? P.refine_result(cand.refined, cand.pose)
+                         : P.refine(cand.pose, target, mode);
       } else {
         HostPose refined = P.refine(cand.pose, target, 2);
         if (P.arm.n_segments == 4) {
@@ -809,14 +820,52 @@ Cand chosen_cand(rp_solution_set* set, const rp_chosen& ch) {
   return c;
 }
 
-/// plan_from_reach (src/path_planner.cpp:729-738)
-rp_plan* plan_from_reach(Planner& P, rp_solution_set* set, const rp_chosen& ch, V3 target) {
+/// select_solution + chosen_cand + the 8DOF pose's exact refinement in one
+/// device round trip when the choice is a reach pose: the canonical ordinal
+/// of the best key (k_rank), its pose (k_materialize from the key, no key
+/// compaction) and refine(pose, target, mode) are launched back to back and
+/// read together. Otherwise (shortcuts, 6DOF, nothing found) the plain
+/// select + chosen_cand (which throw as the reference does).
+Cand select_cand(Planner& P, rp_solution_set* set, V3 target, int mode) {
+  if (!set->shortcuts.empty() || set->n_solutions == 0 || set->rp.mode != RP_MODE_8DOF ||
+      set->arm.n_segments != 4)
+    return chosen_cand(set, select(set));
+  HostSpan span_("select_cand");
+  rp_ctx* ctx = set->ctx;
+  cudaStream_t st = ctx->stream;
+  DevBuf<unsigned long long> rank(1, st);
+  launch_rank_of_key(set, set->best_key, rank.p);
+  DevBuf<long long> key(1, st);
+  copy_to_device(ctx, key.p, &set->best_key, sizeof(long long));
+  DevBuf<DevPose> d(1, st);
+  materialize_solutions(set, key.p, nullptr, 1, d.p);
+  P.refine_launch(d.p, target, mode);
+  unsigned long long hr = 0;
+  DevPose hp{};
+  Cand c;
+  copy_to_host_many(ctx, {{&hr, rank.p, sizeof(hr)},
+                          {&hp, d.p, sizeof(DevPose)},
+                          {&c.refined, P.opout.p, sizeof(PoseOpOut)}});
+  c.kind = RP_CHOSEN_REACH_POSE;
+  c.ordinal = static_cast<int64_t>(hr);
+  c.pose = host_pose_from_dev(hp);
+  c.has_refined = true;
+  c.refined_mode = mode;
+  c.refined_target = target;
+  return c;
+}
+
+rp_plan* plan_from_cand(Planner& P, rp_solution_set* set, const Cand& c, V3 target) {
   PassOptions opt;
   opt.factors = with_unit_first(P.pp.relax);
-  const Cand c = chosen_cand(set, ch);
   Attempt r = attempt_candidate(P, c, target, opt);
   if (r.plan) return r.plan;
   return fallback_cascade(P, r.failure, set, target);
+}
+
+/// plan_from_reach (src/path_planner.cpp:729-738)
+rp_plan* plan_from_reach(Planner& P, rp_solution_set* set, const rp_chosen& ch, V3 target) {
+  return plan_from_cand(P, set, chosen_cand(set, ch), target);
 }
 
 /// build_target_anchor (src/path_planner.cpp:872-902)
@@ -825,6 +874,17 @@ bool build_target_anchor(Planner& P, V3 target, const rp_reach_params& rp, V3 hi
   rpa.near_target_radius = 0.0;
   auto set = try_solve(P.ctx, P.arm, P.q, P.g, target, rpa);
   if (!set || set->n_solutions == 0) return false;
+  try {
+    if (set->shortcuts.empty() && set->rp.mode == RP_MODE_8DOF && set->arm.n_segments == 4) {
+      // the reach pose, its ordinal and refine(pose, target, 0) in one round trip
+      const Cand c = select_cand(P, set.get(), target, 0);
+      *out = P.refine_result(c.refined, c.pose);
+      return true;
+    }
+  } catch (const Fail& e) {
+    if (e.code == RP_E_CUDA || e.code == RP_E_INTERNAL) throw;
+    return false;
+  }
   const rp_chosen ch = select(set.get());
   if (ch.kind != RP_CHOSEN_REACH_POSE) return false;  // refine of an empty pose throws
   try {
@@ -975,9 +1035,10 @@ std::vector<HostPose> solution_poses(rp_solution_set* s, const std::vector<long 
 rp_plan* plan_reach_then_path(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q, const rp_grid* g,
                               V3 target, const rp_reach_params& rp, const rp_path_params& pp) {
   std::unique_ptr<rp_solution_set> set(solve_reach(ctx, arm, q, g, target, rp));
-  const rp_chosen ch = select(set.get());
+  if (set->n_solutions == 0 && set->shortcuts.empty()) select(set.get());  // no_solution first
   Planner P(ctx, arm, q, g, rp, pp);
-  return plan_from_reach(P, set.get(), ch, target);
+  const Cand c = select_cand(P, set.get(), target, P.rp.refine_triangle_8dof ? 1 : 0);
+  return plan_from_cand(P, set.get(), c, target);
 }
 
 /// plan_arbitrary (src/path_planner.cpp:906-998)

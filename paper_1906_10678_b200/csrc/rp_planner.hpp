@@ -51,6 +51,10 @@ struct Planner {
   bool waypoint_ik(V3 wp, const HostPose& prev, double relax, const Trail& tr,
                    const HostPose* bias, HostPose* out);
   HostPose refine(const HostPose& approx, V3 target, int mode);
+  /// refine split around one read-back: launch on a device pose (result in
+  /// opout), then turn the read PoseOpOut into the refined pose (or throw).
+  void refine_launch(const DevPose* d_approx, V3 target, int mode);
+  HostPose refine_result(const PoseOpOut& r, const HostPose& approx);
   bool append_trail(const HostPose& chain3, const Trail& tr, HostPose* out);
   /// from == nullptr: build_unfold (rotated folded pose); else interpolate_poses.
   std::optional<std::vector<HostPose>> interpolate(const HostPose* from, const HostPose& to,

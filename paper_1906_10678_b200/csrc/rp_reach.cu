@@ -1276,6 +1276,12 @@ HostPose solution_pose(rp_solution_set* s, int64_t ordinal) {
   return host_pose_from_dev(solution_dev_pose(s, ordinal));
 }
 
+void launch_rank_of_key(const rp_solution_set* s, long long key, unsigned long long* d_rank) {
+  RP_CUDA(cudaMemsetAsync(d_rank, 0, sizeof(unsigned long long), s->ctx->stream));
+  launch(s->ctx, "select", k_rank, dim3(s->ctx->sm_count), dim3(256), 0,
+         static_cast<const uint32_t*>(s->sol_bits.p), key, d_rank);
+}
+
 static int64_t rank_of_key(const rp_solution_set* s, long long key) {
   DevBuf<unsigned long long> c(1, s->ctx->stream);
   c.zero();

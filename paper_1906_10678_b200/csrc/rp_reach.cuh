@@ -233,5 +233,8 @@ HostPose solution_pose(rp_solution_set* s, int64_t ordinal);
 DevPose solution_dev_pose(rp_solution_set* s, int64_t ordinal);
 /// select_solution; returns kind and ordinal (throws no_solution on empty).
 rp_chosen select(const rp_solution_set* s);
+/// The canonical ordinal of a solution key, counted on the device into
+/// *d_rank (stream order, no synchronisation).
+void launch_rank_of_key(const rp_solution_set* s, long long key, unsigned long long* d_rank);
 std::vector<V3> dev_pose_waypoints(const DevPose& p);
 }  // namespace rp
