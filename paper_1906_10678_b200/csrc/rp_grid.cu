@@ -2067,6 +2067,11 @@ rp_status rp_grid_destroy(rp_grid* g) {
     if (!g) return;
     if (g->bits) RP_CUDA(cudaFreeAsync(g->bits, g->ctx->stream));
     if (g->cf) RP_CUDA(cudaFreeAsync(g->cf, g->ctx->stream));
+    if (g->w1.bits) {
+      if (g->w1.ready) RP_CUDA(cudaStreamWaitEvent(g->ctx->stream, g->w1.ready, 0));
+      RP_CUDA(cudaFreeAsync(g->w1.bits, g->ctx->stream));
+    }
+    if (g->w1.ready) cudaEventDestroy(g->w1.ready);
     if (!g->s2.empty()) s2_release(g);  // reused by the context's next grids
     delete g;
   });

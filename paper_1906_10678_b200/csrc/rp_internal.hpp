@@ -166,6 +166,19 @@ struct rp_grid {
     uint8_t* ok;     // [Q][ceil(Q/1024)]: row chunk computed
   };
   mutable std::vector<Seg2Cache> s2;
+  // Segment-1 walk verdicts from the root (k_walk1_bits) for an arm (root,
+  // L1, n) and quiver, shared by the planners on this grid version; `ready`
+  // is recorded after the kernel on the computing stream (others wait on it).
+  struct Walk1Cache {
+    double key[4];
+    int n = 0;
+    const rp_quiver* q = nullptr;
+    uint64_t version = ~0ull;
+    uint32_t* bits = nullptr;
+    size_t words = 0;
+    cudaEvent_t ready = nullptr;
+  };
+  mutable Walk1Cache w1;
   mutable uint64_t s2_version = ~0ull;
   mutable std::unique_ptr<std::mutex> s2_mutex = std::make_unique<std::mutex>();
 

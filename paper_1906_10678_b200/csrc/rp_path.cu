@@ -583,7 +583,9 @@ __device__ __forceinline__ void wik_filter_fast(const WikDev& w, double cone1, d
 
 /// Segment-1 clearance of every quiver direction from the root (coaxial
 /// arms): walk_clear(root, root + L1 q_i) as a bitmap, the verdict
-/// wik_filter_fast reads instead of walking once per attempt.
+/// wik_filter_fast reads instead of walking once per attempt. Cached on the
+/// grid (Planner::walk1_device) for every planner of the same arm root, L1,
+/// n and quiver.
 __global__ void k_walk1_bits(rpd::GridView g, ArmDev arm, const double* __restrict__ qx,
                              const double* __restrict__ qy, const double* __restrict__ qz, int Q,
                              int n, uint32_t* __restrict__ bits) {
@@ -2631,19 +2633,7 @@ Planner::Planner(rp_ctx* c, const rp_arm& a, const rp_quiver* qv, const rp_grid*
   n = r.n_samples;
   spacing = nominal_spacing(a, r);
   cudaStream_t st = ctx->stream;
-  const int qw = (q->n + 31) / 32 + 1;
-  ibits.alloc(qw, st);
-  jbits.alloc(qw, st);
-  cj.alloc(q->n + 1, st);
-  ci.alloc(q->n + 1, st);
-  ci_by_index.alloc(q->n + 1, st);
-  ci_fast.alloc(q->n + 1, st);
-  counts.alloc(2, st);
   wik_blocks = ctx->sm_count;
-  block_best.alloc(wik_blocks, st);
-  done.alloc(1, st);
-  done.zero();
-  result.alloc(1, st);
   opout.alloc(1, st);
   // pinned read-back slot: one per context, reused by every planner
   if (!ctx->pinned || ctx->pinned_bytes < sizeof(WikResult)) {
@@ -2655,6 +2645,26 @@ Planner::Planner(rp_ctx* c, const rp_arm& a, const rp_quiver* qv, const rp_grid*
 }
 
 Planner::~Planner() {}
+
+void Planner::ensure_scratch() {
+  // the sequenced waypoint_ik's and the cooperative pass's scratch (the
+  // cluster pass keeps its lists in shared memory): allocated on first use
+  if (scratch_ready) return;
+  cudaStream_t st = ctx->stream;
+  const int qw = (q->n + 31) / 32 + 1;
+  ibits.alloc(qw, st);
+  jbits.alloc(qw, st);
+  cj.alloc(q->n + 1, st);
+  ci.alloc(q->n + 1, st);
+  ci_by_index.alloc(q->n + 1, st);
+  ci_fast.alloc(q->n + 1, st);
+  counts.alloc(2, st);
+  block_best.alloc(wik_blocks, st);
+  done.alloc(1, st);
+  done.zero();
+  result.alloc(1, st);
+  scratch_ready = true;
+}
 
 bool Planner::waypoint_ik(V3 wp, const HostPose& prev, double relax, const Trail& tr,
                           const HostPose* bias, HostPose* out) {
@@ -2706,6 +2716,7 @@ bool Planner::waypoint_ik(V3 wp, const HostPose& prev, double relax, const Trail
     cone1 = cone_cos(std::min(kPi, ang1) + 1e-12);
     cone2 = cone_cos(std::min(kPi, ang2) + 1e-12);
   }
+  ensure_scratch();
   WikScratch s{ibits.p, jbits.p, cj.p, ci.p, ci_by_index.p, counts.p, block_best.p, done.p,
                result.p, wik_blocks};
   launch(ctx, "wik_filter", k_wik_filter, dim3(nblk(q->n, 256)), dim3(256), 0, w, cone1, cone2, u1,
@@ -2850,6 +2861,7 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
   A.poses = dp.p;
   A.relax = dr.p;
   A.kind = dk.p;
+  if (!cluster) ensure_scratch();
   A.ibits = ibits.p;
   A.jbits = jbits.p;
   A.ci_by_index = ci_by_index.p;
@@ -2857,14 +2869,7 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
   DevBuf<BpWin> dwin(m, st);
   RP_CUDA(cudaMemsetAsync(dwin.p, 0xFF, m * sizeof(BpWin), st));  // i = -1: not published
   A.win = dwin.p;
-  if (!ad.any_limit && !ad.has_offsets && !walk1_ready) {
-    walk1_bits.alloc((q->n + 31) / 32 + 1, st);
-    launch(ctx, "walk1", k_walk1_bits, dim3(nblk(q->n, 128)), dim3(128), 0, g->view(), ad,
-           static_cast<const double*>(A.qx), static_cast<const double*>(A.qy),
-           static_cast<const double*>(A.qz), q->n, n, walk1_bits.p);
-    walk1_ready = true;
-  }
-  A.walk1 = walk1_bits.p;
+  A.walk1 = (!ad.any_limit && !ad.has_offsets) ? walk1_device() : walk1_bits.p;
   A.block_best = bp_best.p;
   A.bar = bp_bar.p;
   A.state = bp_state.p;
@@ -2980,6 +2985,52 @@ HostPose Planner::refine(const HostPose& approx, V3 target, int mode) {
   HostPose h = host_pose_from_dev(r.pose);
   h.waypoints = approx.waypoints;  // PoseChain out = approx
   return h;
+}
+
+const uint32_t* Planner::walk1_device() {
+  cudaStream_t st = ctx->stream;
+  if (walk1_ready) return walk1_ptr;
+  const double key[4] = {arm.root[0], arm.root[1], arm.root[2], arm.lengths[0]};
+  auto& c = g->w1;
+  std::lock_guard<std::mutex> lock(*g->s2_mutex);
+  const bool current = c.bits && c.version == g->version && !g->exported;
+  const bool hit = current && c.q == q && c.n == n && std::memcmp(c.key, key, sizeof(key)) == 0;
+  if (current && !hit) {
+    // another arm's verdicts are cached for this grid version (planners may
+    // be reading them): compute this planner's own copy
+    walk1_bits.alloc((q->n + 31) / 32 + 1, st);
+    launch(ctx, "walk1", k_walk1_bits, dim3(nblk(q->n, 128)), dim3(128), 0, g->view(), ad,
+           static_cast<const double*>(q->d_soa), static_cast<const double*>(q->d_soa + q->n),
+           static_cast<const double*>(q->d_soa + 2 * static_cast<size_t>(q->n)), q->n, n,
+           walk1_bits.p);
+    walk1_ptr = walk1_bits.p;
+    walk1_ready = true;
+    return walk1_ptr;
+  }
+  if (!hit) {
+    const size_t words = (q->n + 31) / 32 + 1;
+    if (c.words < words) {
+      if (c.bits) RP_CUDA(cudaFreeAsync(c.bits, st));
+      RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&c.bits), words * sizeof(uint32_t), st));
+      c.words = words;
+    } else if (c.ready) {
+      RP_CUDA(cudaStreamWaitEvent(st, c.ready, 0));  // readers of the old verdicts
+    }
+    launch(ctx, "walk1", k_walk1_bits, dim3(nblk(q->n, 128)), dim3(128), 0, g->view(), ad,
+           static_cast<const double*>(q->d_soa), static_cast<const double*>(q->d_soa + q->n),
+           static_cast<const double*>(q->d_soa + 2 * static_cast<size_t>(q->n)), q->n, n, c.bits);
+    if (!c.ready) RP_CUDA(cudaEventCreateWithFlags(&c.ready, cudaEventDisableTiming));
+    RP_CUDA(cudaEventRecord(c.ready, st));
+    std::memcpy(c.key, key, sizeof(key));
+    c.n = n;
+    c.q = q;
+    c.version = g->version;
+  } else {
+    RP_CUDA(cudaStreamWaitEvent(st, c.ready, 0));  // computed on another stream
+  }
+  walk1_ptr = c.bits;
+  walk1_ready = true;
+  return walk1_ptr;
 }
 
 void Planner::refine_launch(const DevPose* d_approx, V3 target, int mode) {

@@ -34,12 +34,18 @@ struct Planner {
   DevBuf<int> cj, counts;
   DevBuf<CiData> ci, ci_by_index;
   DevBuf<CiFast> ci_fast;
-  DevBuf<uint32_t> walk1_bits;  // k_walk1_bits, built on the first device pass
+  DevBuf<uint32_t> walk1_bits;  // unused when walk1_device() serves the pass
   bool walk1_ready = false;
+  const uint32_t* walk1_ptr = nullptr;
+  /// The grid's cached segment-1 verdicts from the root (k_walk1_bits), in
+  /// this planner's stream order.
+  const uint32_t* walk1_device();
   DevBuf<WikBest> block_best;
   DevBuf<unsigned> done;
   DevBuf<WikResult> result;
   DevBuf<PoseOpOut> opout;
+  bool scratch_ready = false;
+  void ensure_scratch();
   WikResult* h_result = nullptr;
 
   Planner(rp_ctx* c, const rp_arm& a, const rp_quiver* qv, const rp_grid* gr,
