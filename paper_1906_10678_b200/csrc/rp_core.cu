@@ -82,9 +82,10 @@ static void drain_timing(rp_ctx* ctx) {
       // offsets from the first launch since reset_timing (across drains),
       // and the idle gap since the previous launch ended on this stream
       float at = 0.f;
-      RP_CUDA(cudaEventElapsedTime(&at, ctx->tl_base, t.start));
-      std::fprintf(stderr, "[tl] %9.3f ms +%8.3f gap %8.3f %s\n", at, ms, at - ctx->tl_prev_end,
-                   t.name.c_str());
+      const rp_ctx* o = ctx->tl_parent && ctx->tl_parent->tl_armed ? ctx->tl_parent : ctx;
+      RP_CUDA(cudaEventElapsedTime(&at, o->tl_base, t.start));
+      std::fprintf(stderr, "[tl] %9.3f ms +%8.3f gap %8.3f %s%s\n", at, ms, at - ctx->tl_prev_end,
+                   t.name.c_str(), o != ctx ? " (worker)" : "");
       ctx->tl_prev_end = at + ms;
     }
     auto& acc = ctx->kernel_ms[t.name];
@@ -369,6 +370,7 @@ rp_ctx* worker_ctx(rp_ctx* parent, int k) {
   }
   rp_ctx* w = parent->workers[k];
   w->timing = parent->timing;
+  w->tl_parent = parent;  // RP_TIMELINE offsets from the parent's origin
   return w;
 }
 

@@ -76,6 +76,7 @@ struct rp_ctx {
   cudaEvent_t tl_base = nullptr;  // RP_TIMELINE: start of the first launch since reset_timing
   bool tl_armed = false;
   float tl_prev_end = 0.f;
+  const rp_ctx* tl_parent = nullptr;  // worker contexts: the context they serve
   std::map<std::string, std::pair<double, int64_t>> kernel_ms;
   int sm_count = 148;
   // Small pinned staging buffer for scalar read-backs.

@@ -2771,7 +2771,6 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
   if (!cluster && q->n > 16384) return false;
   if (const char* e = std::getenv("RP_BPC_LIST_CAP"))  // tests: force the overflow fallback
     list_cap = std::min(list_cap, std::max(64, std::atoi(e)));
-  if (cluster && !bp_state.p) bp_state.alloc(4, st);
   if (!cluster && bp_blocks == 0) {
     // kernel attribute + occupancy: once per device and shared-memory size
     // (the attribute is per device; planners may run on several threads)
@@ -2798,7 +2797,6 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
     bp_blocks = std::min(ctx->sm_count * per_sm, env ? std::max(1, std::atoi(env)) : 64);
     if (bp_blocks_cap > 0) bp_blocks = std::min(bp_blocks, bp_blocks_cap);
     bp_bar.alloc(2, st);
-    bp_state.alloc(4, st);
     bp_best.alloc(bp_blocks, st);
   }
   const int m = static_cast<int>(wps.size());
@@ -2845,34 +2843,44 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
   if (fixed_first) A.fixed_first = to_dev(*fixed_first);
   A.has_bias = bias ? 1 : 0;
   if (bias) A.bias = to_dev(*bias);
-  DevBuf<V3> dw(m, st);
-  DevBuf<DevPose> dp(m, st);
-  DevBuf<double> dr(m, st);
-  DevBuf<int> dk(m, st);
-  copy_to_device(ctx, dw.p, wps.data(), m * sizeof(V3));
-  const DevPose da = to_dev(anchor);
-  copy_to_device(ctx, dp.p + (m - 1), &da, sizeof(DevPose));
-  std::vector<double> ones(m, 1.0);
-  copy_to_device(ctx, dr.p, ones.data(), m * sizeof(double));
-  dk.zero();
-  bp_bar.zero();
-  bp_state.zero();
-  A.wps = dw.p;
-  A.poses = dp.p;
-  A.relax = dr.p;
-  A.kind = dk.p;
+  // The pass's inputs and outputs in one device block, filled by one upload
+  // and read back by one copy: [state][wps][poses][relax][kind][win]
+  auto al = [](size_t x) { return (x + 15) & ~size_t{15}; };
+  const size_t o_wps = al(4 * sizeof(int));
+  const size_t o_poses = o_wps + al(m * sizeof(V3));
+  const size_t o_relax = o_poses + al(m * sizeof(DevPose));
+  const size_t o_kind = o_relax + al(m * sizeof(double));
+  const size_t o_win = o_kind + al(m * sizeof(int));
+  const size_t io_bytes = o_win + al(m * sizeof(BpWin));
+  if (bp_io.n < io_bytes) bp_io.alloc(io_bytes, st);
+  {
+    std::vector<unsigned char> h(io_bytes, 0);
+    std::memcpy(h.data() + o_wps, wps.data(), m * sizeof(V3));
+    const DevPose da = to_dev(anchor);
+    std::memcpy(h.data() + o_poses + (m - 1) * sizeof(DevPose), &da, sizeof(DevPose));
+    for (int k = 0; k < m; ++k) {
+      const double one = 1.0;
+      std::memcpy(h.data() + o_relax + k * sizeof(double), &one, sizeof(double));
+    }
+    std::memset(h.data() + o_win, 0xFF, m * sizeof(BpWin));  // i = -1: not published
+    copy_to_device(ctx, bp_io.p, h.data(), io_bytes);
+  }
+  unsigned char* io = bp_io.p;
+  if (!cluster) bp_bar.zero();
+  A.wps = reinterpret_cast<V3*>(io + o_wps);
+  A.poses = reinterpret_cast<DevPose*>(io + o_poses);
+  A.relax = reinterpret_cast<double*>(io + o_relax);
+  A.kind = reinterpret_cast<int*>(io + o_kind);
   if (!cluster) ensure_scratch();
   A.ibits = ibits.p;
   A.jbits = jbits.p;
   A.ci_by_index = ci_by_index.p;
   A.ci_fast = ci_fast.p;
-  DevBuf<BpWin> dwin(m, st);
-  RP_CUDA(cudaMemsetAsync(dwin.p, 0xFF, m * sizeof(BpWin), st));  // i = -1: not published
-  A.win = dwin.p;
+  A.win = reinterpret_cast<BpWin*>(io + o_win);
   A.walk1 = (!ad.any_limit && !ad.has_offsets) ? walk1_device() : walk1_bits.p;
   A.block_best = bp_best.p;
   A.bar = bp_bar.p;
-  A.state = bp_state.p;
+  A.state = reinterpret_cast<int*>(io);
   A.cancel = cancel_flag;
   static const bool profile = std::getenv("RP_PROFILE_PASS") != nullptr;
   DevBuf<long long> prof;
@@ -2933,15 +2941,19 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
   }
   // the state and the pass's outputs in one read-back
   int hs[4];
-  out->poses.resize(m);
-  out->relax.resize(m);
-  out->kind.resize(m);
-  out->wps.resize(m);
-  copy_to_host_many(ctx, {{hs, bp_state.p, sizeof(hs)},
-                          {out->poses.data(), dp.p, m * sizeof(DevPose)},
-                          {out->relax.data(), dr.p, m * sizeof(double)},
-                          {out->kind.data(), dk.p, m * sizeof(int)},
-                          {out->wps.data(), dw.p, m * sizeof(V3)}});
+  {
+    std::vector<unsigned char> h(o_win);
+    copy_to_host(ctx, h.data(), io, o_win);
+    std::memcpy(hs, h.data(), sizeof(hs));
+    out->poses.resize(m);
+    out->relax.resize(m);
+    out->kind.resize(m);
+    out->wps.resize(m);
+    std::memcpy(out->wps.data(), h.data() + o_wps, m * sizeof(V3));
+    std::memcpy(out->poses.data(), h.data() + o_poses, m * sizeof(DevPose));
+    std::memcpy(out->relax.data(), h.data() + o_relax, m * sizeof(double));
+    std::memcpy(out->kind.data(), h.data() + o_kind, m * sizeof(int));
+  }
   if (profile) {
     long long hp[24];
     copy_to_host(ctx, hp, prof.p, sizeof(hp));

@@ -84,8 +84,8 @@ struct Planner {
   bool backward_pass_device(const std::vector<V3>& wps, const HostPose& anchor,
                             const std::vector<double>& factors, bool cloud, double cloud_radius,
                             const HostPose* fixed_first, const HostPose* bias, BpOut* out);
+  DevBuf<unsigned char> bp_io;  // a pass's inputs + outputs (backward_pass_device)
   DevBuf<unsigned> bp_bar;
-  DevBuf<int> bp_state;
   DevBuf<WikBest> bp_best;
   int bp_blocks = 0;
   int bp_blocks_cap = 0;  // > 0: at most this many blocks (concurrent passes)
