@@ -515,6 +515,19 @@ std::vector<Slot<R>> run_parallel(Planner& P, int n, const std::function<R(Plann
   return out;
 }
 
+/// {0, 1} in pinned memory: DMA sources for clearing / setting a pass's
+/// cancellation flag (a later pass is stopped by a copy, no SMs needed).
+int* pinned_01() {
+  static int* p = [] {
+    int* h = nullptr;
+    RP_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h), 2 * sizeof(int), cudaHostAllocDefault));
+    h[0] = 0;
+    h[1] = 1;
+    return h;
+  }();
+  return p;
+}
+
 /// One attempt of the cascade.
 struct Job {
   const Cand* cand;
@@ -597,13 +610,7 @@ std::pair<int, rp_plan*> cascade_pool(Planner& P, const Failure& failure, rp_sol
   // pass; a later job still running when an earlier one decides the outcome
   // is stopped by a DMA write of 1 on an auxiliary stream (no SMs needed).
   static const bool groups = std::getenv("RP_CASCADE_EAGER") == nullptr;
-  static int* pinned01 = [] {  // {0, 1}: DMA sources for clearing / setting a flag
-    int* h = nullptr;
-    RP_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h), 2 * sizeof(int), cudaHostAllocDefault));
-    h[0] = 0;
-    h[1] = 1;
-    return h;
-  }();
+  int* const pinned01 = pinned_01();
   if (!P.ctx->aux) RP_CUDA(cudaStreamCreateWithFlags(&P.ctx->aux, cudaStreamNonBlocking));
   cudaStream_t aux = P.ctx->aux;
   std::vector<long long> running(width, -1);
@@ -969,9 +976,40 @@ rp_plan* plan_virtual_path(Planner& P, const HostPose& start, NextBatch next_bat
         if (pass.ok) return to_plan(pass);
         continue;
       }
+      // a success cancels the later candidates' passes (they would lose to
+      // it anyway): a DMA of 1 into their flags on the context's aux stream
+      if (!P.ctx->aux) RP_CUDA(cudaStreamCreateWithFlags(&P.ctx->aux, cudaStreamNonBlocking));
+      std::vector<int*> flags(m);
+      for (int k = 0; k < m; ++k) {
+        flags[k] = worker_ctx(P.ctx, k)->cancel_flag;
+        RP_CUDA(cudaMemcpyAsync(flags[k], pinned_01(), sizeof(int), cudaMemcpyHostToDevice,
+                                P.ctx->aux));
+      }
+      RP_CUDA(cudaStreamSynchronize(P.ctx->aux));  // cleared before any pass reads them
+      std::mutex cm;
+      int first_ok = m;
       std::vector<Slot<PassResult>> r = run_parallel<PassResult>(
-          P, m, [&](Planner& W, int k) { return backward_pass(W, wps_list[a + k], anchor, opt); },
+          P, m,
+          [&](Planner& W, int k) {
+            {
+              std::lock_guard<std::mutex> lk(cm);
+              if (k > first_ok) return PassResult{};  // an earlier candidate already won
+            }
+            W.cancel_flag = flags[k];
+            PassResult pr = backward_pass(W, wps_list[a + k], anchor, opt);
+            if (pr.ok) {
+              std::lock_guard<std::mutex> lk(cm);
+              if (k < first_ok) {
+                for (int j = k + 1; j < first_ok; ++j)
+                  RP_CUDA(cudaMemcpyAsync(flags[j], pinned_01() + 1, sizeof(int),
+                                          cudaMemcpyHostToDevice, P.ctx->aux));
+                first_ok = k;
+              }
+            }
+            return pr;
+          },
           {});
+      RP_CUDA(cudaStreamSynchronize(P.ctx->aux));
       for (auto& slot : r) {
         if (slot.error) std::rethrow_exception(slot.error);
         if (slot.value.ok) return to_plan(slot.value);
