@@ -3118,13 +3118,19 @@ std::optional<std::vector<HostPose>> Planner::interpolate(const HostPose* from_o
     build_chain(ad, dfrom);
     from = host_pose_from_dev(dfrom);
     from.waypoints.clear();
-    const bool ok = valid_poses(&dfrom, 1) < 0;
-    if (rotated_valid) *rotated_valid = ok;
-    if (!ok) return std::nullopt;
+    // the rotated pose's validity is checked with the first interpolation
+    // (same launch, same read-back): index 0 of the checked range
   }
+  bool check_from = from_or_null == nullptr;
   double qa_az[4], qa_el[4], qb_az[4], qb_el[4];
-  if (!to_angles(ad, dfrom, qa_az, qa_el) || !to_angles(ad, to_dev(to), qb_az, qb_el))
+  if (!to_angles(ad, dfrom, qa_az, qa_el) || !to_angles(ad, to_dev(to), qb_az, qb_el)) {
+    if (check_from) {  // the reference checks the rotated pose first
+      const bool ok = valid_poses(&dfrom, 1) < 0;
+      if (rotated_valid) *rotated_valid = ok;
+      if (!ok) return std::nullopt;
+    }
     fail(RP_E_DEGENERATE_INPUT, "zero-length segment");
+  }
   for (int steps = std::max(1, base_steps); steps <= 4096; steps *= 2) {
     std::vector<DevPose> seq(steps + 1);
     seq[0] = dfrom;
@@ -3138,20 +3144,34 @@ std::optional<std::vector<HostPose>> Planner::interpolate(const HostPose* from_o
       }
       seq[s] = from_angles(ad, az, el);
     }
-    DevBuf<DevPose> dseq(steps + 1, st);
-    DevBuf<int> flags(2, st);
-    flags.zero();
-    const int init = INT_MAX;
-    copy_to_device(ctx, flags.p, &init, sizeof(int));
-    copy_to_device(ctx, dseq.p, seq.data(), (steps + 1) * sizeof(DevPose));
-    if (steps > 1)
-      launch(ctx, "unfold", k_pose_check, dim3(nblk(steps - 1, 64)), dim3(64), 0, g->view(), ad,
-             static_cast<const DevPose*>(dseq.p + 1), steps - 1, n, spacing, 1, flags.p);
-    launch(ctx, "unfold", k_seq_smooth, dim3(nblk(steps, 128)), dim3(128), 0,
-           static_cast<const DevPose*>(dseq.p), steps + 1, pp.j1 * 1.0 + 1e-12,
-           pp.j2 * 1.0 + 1e-12, flags.p + 1);
+    // flags (first invalid pose, smoothness failure) and the sequence in
+    // one block and one upload
+    const size_t o_seq = 16, bytes = o_seq + (steps + 1) * sizeof(DevPose);
+    DevBuf<unsigned char> blk(bytes, st);
+    {
+      std::vector<unsigned char> h(bytes, 0);
+      const int init[2] = {INT_MAX, 0};
+      std::memcpy(h.data(), init, sizeof(init));
+      std::memcpy(h.data() + o_seq, seq.data(), (steps + 1) * sizeof(DevPose));
+      copy_to_device(ctx, blk.p, h.data(), bytes);
+    }
+    int* flags = reinterpret_cast<int*>(blk.p);
+    const DevPose* dseq = reinterpret_cast<const DevPose*>(blk.p + o_seq);
+    // poses 1..steps-1 (and 0, the rotated folded pose, on the first round)
+    const int c0 = check_from ? 0 : 1;
+    if (steps - c0 > 0)
+      launch(ctx, "unfold", k_pose_check, dim3(nblk(steps - c0, 64)), dim3(64), 0, g->view(), ad,
+             dseq + c0, steps - c0, n, spacing, 1, flags);
+    launch(ctx, "unfold", k_seq_smooth, dim3(nblk(steps, 128)), dim3(128), 0, dseq, steps + 1,
+           pp.j1 * 1.0 + 1e-12, pp.j2 * 1.0 + 1e-12, flags + 1);
     int hf[2];
-    copy_to_host(ctx, hf, flags.p, sizeof(hf));
+    copy_to_host(ctx, hf, flags, sizeof(hf));
+    if (check_from) {
+      const bool ok = hf[0] != 0;  // index 0 = the rotated pose
+      if (rotated_valid) *rotated_valid = ok;
+      if (!ok) return std::nullopt;
+      check_from = false;
+    }
     if (hf[0] != INT_MAX) return std::nullopt;
     if (!hf[1]) {
       std::vector<HostPose> out;

@@ -138,9 +138,10 @@ __global__ void k_compact_small(const uint32_t* __restrict__ bits, int nbits, in
   if (threadIdx.x == 0) *count = carry;
 }
 
-__global__ void k_surv_data(SolveDev a, const int* __restrict__ idx, int S1, SurvDev* __restrict__ out) {
+__global__ void k_surv_data(SolveDev a, const int* __restrict__ idx, const int* __restrict__ S1p,
+                            SurvDev* __restrict__ out) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= S1) return;
+  if (s >= *S1p) return;
   const ArmDev& arm = a.arm;
   SurvDev h{};
   h.i = idx[s];
@@ -361,10 +362,10 @@ __global__ void k_tail_skip(rpd::GridView g, const V3* __restrict__ pts, int T, 
 /// (off by at most one per axis from the cell holding it) lies within
 /// sqrt(3) * vs of it, so samples with t_k * L2 + sqrt(3) * vs < D (with
 /// margins) are free. One thread per row.
-__global__ void k_row_skip(SolveDev a, const SurvDev* __restrict__ sv, int S1, ClearanceField f,
-                           uint8_t* __restrict__ kskip) {
+__global__ void k_row_skip(SolveDev a, const SurvDev* __restrict__ sv, const int* __restrict__ S1p,
+                           ClearanceField f, uint8_t* __restrict__ kskip) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= S1) return;
+  if (s >= *S1p) return;
   const rpd::GridView& g = a.g;
   const double D = cf_distance(f, g, sv[s].p1);
   const double L2 = a.arm.L[1] * (1.0 + 1e-9) + 1e-9;
@@ -375,7 +376,8 @@ __global__ void k_row_skip(SolveDev a, const SurvDev* __restrict__ sv, int S1, C
 }
 
 template <bool EIGHT>
-__global__ void __launch_bounds__(256, 4) k_seg2_rows(SolveDev a, const SurvDev* __restrict__ sv, int s_lo, int s_hi,
+__global__ void __launch_bounds__(256, 4) k_seg2_rows(SolveDev a, const SurvDev* __restrict__ sv,
+                                                   const int* __restrict__ S1p, int part, int parts,
                                                    uint32_t* __restrict__ sol_bits,
                                                    unsigned long long* ctr, long long* sc_list,
                                                    unsigned* sc_count, BestRec* __restrict__ block_best,
@@ -400,6 +402,11 @@ __global__ void __launch_bounds__(256, 4) k_seg2_rows(SolveDev a, const SurvDev*
   int* wq = wqs[threadIdx.x >> 5];
   constexpr int kChunk = 1024;  // j per work unit (balances small S1)
   const int nchunk = (a.Q + kChunk - 1) / kChunk;
+  // this part's survivor rows [s_lo, s_hi) of the S1 the prune left on the
+  // device (no host read-back between the prune and this kernel)
+  const int S1 = *S1p;
+  const int s_lo = static_cast<int>(static_cast<int64_t>(S1) * part / parts);
+  const int s_hi = static_cast<int>(static_cast<int64_t>(S1) * (part + 1) / parts);
   (void)warp_id;
   (void)nwarps;
   for (;;) {
@@ -1056,22 +1063,30 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
     a.qx = q->d_soa;
     a.qy = q->d_soa + q->n;
     a.qz = q->d_soa + 2 * static_cast<size_t>(q->n);
-    s->bpts.alloc(s->B + 1, st);
-    s->bdirs.alloc(s->B + 1, st);
-    s->bcone.alloc(s->B + 1, st);
-    s->walk4.alloc(s->B + 1, st);
-    copy_to_device(ctx, s->bpts.p, s->h_bpts.data(), s->B * sizeof(V3));
-    copy_to_device(ctx, s->bdirs.p, s->h_bdirs.data(), s->B * sizeof(V3));
-    copy_to_device(ctx, s->bcone.p, s->h_bcone.data(), s->B * sizeof(int));
-    a.bpts = s->bpts.p;
-    a.bdirs = s->bdirs.p;
-    a.bcone = s->bcone.p;
-    a.walk4_ok = s->walk4.p;
-    DevBuf<V3> tg(1, st);
-    copy_to_device(ctx, tg.p, &target, sizeof(V3));
-    a.targets = tg.p;
+    {
+      // the backward points, directions, cone indices and the target in one
+      // device block and one upload: [bpts][bdirs][target][bcone][walk4]
+      const size_t nb = s->B + 1;
+      const size_t o_dirs = nb * sizeof(V3), o_tg = 2 * nb * sizeof(V3);
+      const size_t o_cone = o_tg + sizeof(V3), o_w4 = o_cone + nb * sizeof(int);
+      const size_t bytes = o_w4 + nb;
+      s->bblock.alloc(bytes, st);
+      std::vector<unsigned char> h(o_w4, 0);
+      std::memcpy(h.data(), s->h_bpts.data(), s->B * sizeof(V3));
+      std::memcpy(h.data() + o_dirs, s->h_bdirs.data(), s->B * sizeof(V3));
+      std::memcpy(h.data() + o_tg, &target, sizeof(V3));
+      std::memcpy(h.data() + o_cone, s->h_bcone.data(), s->B * sizeof(int));
+      copy_to_device(ctx, s->bblock.p, h.data(), o_w4);
+      a.bpts = reinterpret_cast<V3*>(s->bblock.p);
+      a.bdirs = reinterpret_cast<V3*>(s->bblock.p + o_dirs);
+      a.targets = reinterpret_cast<V3*>(s->bblock.p + o_tg);
+      a.bcone = reinterpret_cast<int*>(s->bblock.p + o_cone);
+      a.walk4_ok = s->bblock.p + o_w4;
+    }
     a.n_targets = 1;
-    if (eight) launch(ctx, "walk4", k_walk4, dim3(nblk(s->B, 128)), dim3(128), 0, a, s->walk4.p);
+    if (eight)
+      launch(ctx, "walk4", k_walk4, dim3(nblk(s->B, 128)), dim3(128), 0, a,
+             const_cast<uint8_t*>(a.walk4_ok));
 
     DevBuf<unsigned long long> ctr(C_COUNT, st);
     ctr.zero();
@@ -1085,54 +1100,61 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
     DevBuf<int> surv_idx(q->n + 1, st), surv_cnt(1, st);
     launch(ctx, "compact", k_compact_small, dim3(1), dim3(1024), 0,
            static_cast<const uint32_t*>(surv_bits.p), q->n, surv_idx.p, surv_cnt.p);
+    const bool B1 = s->B == 1;
+    const bool general = a.arm.any_limit || a.arm.has_offsets || (rp.cone_precheck && eight);
+    static const bool flat = std::getenv("RP_SEG2_FLAT") != nullptr;
+    // The row kernel path (default arms, one backward point) runs without a
+    // host read-back between the prune and segment 2: buffers are sized for
+    // S1 <= Q and the kernels read S1 on the device; the count and the
+    // survivor list come back with the solve's counters. Other paths (and
+    // quivers past 16384 directions, whose Q^2 bit set would be large) read
+    // S1 first.
+    const bool rows_path = !general && B1 && !flat && q->n <= 16384;
     int S1 = 0;
-    // the survivor count and list in one read-back (the list is at most Q)
     std::vector<int> surv_all(q->n);
-    copy_to_host_many(ctx, {{&S1, surv_cnt.p, sizeof(int)},
-                            {surv_all.data(), surv_idx.p, q->n * sizeof(int)}});
-    s->S1 = S1;
-    s->surv.alloc(S1 + 1, st);
-    if (S1 > 0)
-      launch(ctx, "seg1", k_surv_data, dim3(nblk(S1, 128)), dim3(128), 0, a,
-             static_cast<const int*>(surv_idx.p), S1, s->surv.p);
-    s->surv_i.assign(surv_all.begin(), surv_all.begin() + S1);
+    if (!rows_path)
+      copy_to_host_many(ctx, {{&S1, surv_cnt.p, sizeof(int)},
+                              {surv_all.data(), surv_idx.p, q->n * sizeof(int)}});
+    const int cap_rows = rows_path ? q->n : S1;
+    s->surv.alloc(cap_rows + 1, st);
+    if (cap_rows > 0)
+      launch(ctx, "seg1", k_surv_data, dim3(nblk(cap_rows, 128)), dim3(128), 0, a,
+             static_cast<const int*>(surv_idx.p), static_cast<const int*>(surv_cnt.p), s->surv.p);
     // this part's survivor rows (the whole set for parts == 1); the pair and
     // key indices stay global, so parts' keys concatenate in canonical order
-    const int s_lo = static_cast<int>(static_cast<int64_t>(S1) * part / parts);
-    const int s_hi = static_cast<int>(static_cast<int64_t>(S1) * (part + 1) / parts);
+    int s_lo = static_cast<int>(static_cast<int64_t>(S1) * part / parts);
+    int s_hi = static_cast<int>(static_cast<int64_t>(S1) * (part + 1) / parts);
     s->part = part;
     s->parts = parts;
     if (part != 0) sc_count.zero();  // segment-1 hypotheses belong to part 0
 
-    s->n_pairs = static_cast<int64_t>(S1) * q->n;
+    s->n_pairs = static_cast<int64_t>(cap_rows) * q->n;  // exact once S1 is known
     const int64_t nbits = s->n_pairs * s->B;
     const int64_t nwords = (nbits + 31) / 32 + 1;
     s->sol_bits.alloc(nwords, st);
-    const bool B1 = s->B == 1;
     if (!B1 || parts > 1) s->sol_bits.zero();
-    const bool general = a.arm.any_limit || a.arm.has_offsets || (rp.cone_precheck && eight);
     const int threads = 256;
     int blocks = ctx->sm_count * 8;
     const int64_t p_lo = static_cast<int64_t>(s_lo) * q->n, p_hi = static_cast<int64_t>(s_hi) * q->n;
     const int64_t need = (p_hi - p_lo + threads - 1) / threads;
-    if (need < blocks) blocks = static_cast<int>(std::max<int64_t>(1, need));
+    if (!rows_path && need < blocks) blocks = static_cast<int>(std::max<int64_t>(1, need));
     DevBuf<BestRec> bb(blocks, st), best(1, st);
-    if (p_hi > p_lo) {
+    if (rows_path || p_hi > p_lo) {
       auto run = [&](auto kern) {
         launch(ctx, "seg2", kern, dim3(blocks), dim3(threads), 0, a,
                static_cast<const SurvDev*>(s->surv.p), p_lo, p_hi, s->sol_bits.p, ctr.p,
                sc_list.p, sc_count.p, bb.p);
       };
-      static const bool flat = std::getenv("RP_SEG2_FLAT") != nullptr;
-      if (!general && B1 && !flat) {
+      if (rows_path) {
         s->sol_bits.zero();
-        const int64_t units = static_cast<int64_t>(s_hi - s_lo) * ((q->n + 1023) / 1024);
-        const int rblocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks, (units + 7) / 8)));
+        const int64_t units = static_cast<int64_t>(cap_rows) * ((q->n + 1023) / 1024);
+        const int rblocks = static_cast<int>(
+            std::max<int64_t>(1, std::min<int64_t>(ctx->sm_count * 8, (units + 7) / 8)));
         DevBuf<int> unit_ctr(1, st);
         unit_ctr.zero();
         // free leading samples per row (k_row_skip) and trailing samples of
         // the v3 walks (k_tail_skip) from the grid's cached clearance field
-        DevBuf<uint8_t> kskip(std::max(1, S1), st);
+        DevBuf<uint8_t> kskip(std::max(1, cap_rows), st);
         static const bool no_skip = std::getenv("RP_NO_ROW_SKIP") != nullptr;
         DevBuf<uint8_t> kend_b(1, st);
         if (no_skip) {
@@ -1140,17 +1162,19 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
           RP_CUDA(cudaMemsetAsync(kend_b.p, rp.n_samples, 1, st));
         } else {
           const ClearanceField cf = grid_clearance_field(g);
-          launch(ctx, "seg2", k_row_skip, dim3(nblk(S1, 128)), dim3(128), 0, a,
-                 static_cast<const SurvDev*>(s->surv.p), S1, cf, kskip.p);
+          launch(ctx, "seg2", k_row_skip, dim3(nblk(std::max(1, cap_rows), 128)), dim3(128), 0, a,
+                 static_cast<const SurvDev*>(s->surv.p), static_cast<const int*>(surv_cnt.p), cf,
+                 kskip.p);
           launch(ctx, "seg2", k_tail_skip, dim3(1), dim3(32), 0, a.g,
-                 static_cast<const V3*>(s->bpts.p), 1, L3 + eps, rp.n_samples, cf, kend_b.p);
+                 static_cast<const V3*>(a.bpts), 1, L3 + eps, rp.n_samples, cf, kend_b.p);
         }
         uint32_t* c2bits = nullptr;
         uint8_t* c2ok = nullptr;
         if (!grid_seg2_cache(g, q, arm, rp.n_samples, &c2bits, &c2ok)) c2bits = nullptr, c2ok = nullptr;
         auto runr = [&](auto kern) {
           launch(ctx, "seg2", kern, dim3(rblocks), dim3(threads), 0, a,
-                 static_cast<const SurvDev*>(s->surv.p), s_lo, s_hi, s->sol_bits.p, ctr.p, sc_list.p,
+                 static_cast<const SurvDev*>(s->surv.p), static_cast<const int*>(surv_cnt.p), part,
+                 parts, s->sol_bits.p, ctr.p, sc_list.p,
                  sc_count.p, bb.p, unit_ctr.p, static_cast<const uint8_t*>(kskip.p),
                  static_cast<const uint8_t*>(kend_b.p), c2bits, c2ok);
         };
@@ -1169,9 +1193,24 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
     unsigned long long hc[C_COUNT];
     unsigned nsc = 0;
     BestRec hb{0.0, -1};
-    copy_to_host_many(ctx, {{hc, ctr.p, sizeof(hc)},
-                            {&nsc, sc_count.p, sizeof(unsigned)},
-                            {&hb, best.p, p_hi > p_lo ? sizeof(BestRec) : 0}});
+    if (rows_path) {
+      // the solve's one read-back: counters, shortcut count, best, S1 and
+      // the survivor list
+      copy_to_host_many(ctx, {{hc, ctr.p, sizeof(hc)},
+                              {&nsc, sc_count.p, sizeof(unsigned)},
+                              {&hb, best.p, sizeof(BestRec)},
+                              {&S1, surv_cnt.p, sizeof(int)},
+                              {surv_all.data(), surv_idx.p, q->n * sizeof(int)}});
+      s_lo = static_cast<int>(static_cast<int64_t>(S1) * part / parts);
+      s_hi = static_cast<int>(static_cast<int64_t>(S1) * (part + 1) / parts);
+      s->n_pairs = static_cast<int64_t>(S1) * q->n;
+    } else {
+      copy_to_host_many(ctx, {{hc, ctr.p, sizeof(hc)},
+                              {&nsc, sc_count.p, sizeof(unsigned)},
+                              {&hb, best.p, p_hi > p_lo ? sizeof(BestRec) : 0}});
+    }
+    s->S1 = S1;
+    s->surv_i.assign(surv_all.begin(), surv_all.begin() + S1);
     require(nsc <= kShortcutCap, RP_E_CAPACITY_EXCEEDED, "too many near-encounter hypotheses");
 
     rp_solve_stats& S = s->stats;
@@ -1180,7 +1219,7 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
     S.seg1_limit_pass = hc[C_SEG1_LIMIT];
     S.seg1_reach_pass = hc[C_SEG1_REACH];
     S.seg1_survivors = hc[C_SEG1_SURV];
-    S.pair_candidates = p_hi - p_lo;
+    S.pair_candidates = static_cast<int64_t>(s_hi - s_lo) * q->n;
     S.seg2_limit_pass = hc[C_SEG2_LIMIT];
     S.seg2_clear_pass = hc[C_SEG2_CLEAR];
     S.gap_tested = hc[C_GAP_TESTED];
@@ -2455,9 +2494,9 @@ extern "C" rp_status rp_solve_reach_batch(rp_ctx* ctx, const rp_arm* arm, const 
     // ---- all targets of a chunk go through each stage together
     const V3 axis{rp->approach_axis[0], rp->approach_axis[1], rp->approach_axis[2]};
     const V3 bdir = eight ? axis : V3{0, 0, 0};
-    proto.bdirs.alloc(1, st);
-    copy_to_device(ctx, proto.bdirs.p, &bdir, sizeof(V3));
-    a.bdirs = proto.bdirs.p;
+    proto.bblock.alloc(sizeof(V3), st);
+    copy_to_device(ctx, proto.bblock.p, &bdir, sizeof(V3));
+    a.bdirs = reinterpret_cast<const V3*>(proto.bblock.p);
     static const int CH = std::getenv("RP_BATCH_CHUNK") ? std::atoi(std::getenv("RP_BATCH_CHUNK")) : 128;
     const int BPT = 64;
     const int refine_mode = eight ? (rp->refine_triangle_8dof ? 1 : 0) : 2;

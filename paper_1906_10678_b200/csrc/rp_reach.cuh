@@ -198,9 +198,9 @@ struct rp_solution_set {
   rp::DevBuf<rp::SurvDev> surv;
   std::vector<int> surv_i;
   int B = 0;
-  rp::DevBuf<rp::V3> bpts, bdirs;
-  rp::DevBuf<int> bcone;
-  rp::DevBuf<uint8_t> walk4;
+  // backward points, directions, the target, cone indices and walk4 flags
+  // (SolveDev bpts / bdirs / targets / bcone / walk4_ok point into it)
+  rp::DevBuf<unsigned char> bblock;
   std::vector<rp::V3> h_bpts, h_bdirs;
   std::vector<int> h_bcone;
   int64_t n_pairs = 0;

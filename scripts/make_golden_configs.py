@@ -13,6 +13,7 @@
          4096 batched targets: counters, chosen key, path length, refined pose
 
   C2_1   C2 at a 1-degree quiver (Q = 41,264): grid, counters, keys, plan
+  C3_1   C3 at a 1-degree quiver: the same, then plan_arbitrary
 
 Run where oracle/_ref is built (minutes of CPU; C5's 512^3 dilation alone
 takes ~4.5 min): python scripts/make_golden_configs.py [case ...]
@@ -177,7 +178,25 @@ def c2_1deg(arrays):
     return e
 
 
-CASES = {"C2_2": c2, "C3_2": c3, "C4_2": c4, "C5_2": c5, "C2_1": c2_1deg}
+def c3_1deg(arrays):
+    """C3 (the headline scene) at the 1-degree quiver: reach + path through
+    the fallback cascade, then plan_arbitrary to the 2-degree second target."""
+    sc = scenes.config("C3", 1.0)
+    R, e, plan, s = case_reach_path("C3_1", sc, arrays)
+    t2 = sc.extra["second_target"]
+    e["second_target"] = list(t2)
+    if s is not None:
+        p, w = s["poses"][-1]
+        rc2, plan2 = R.plan_arbitrary(p, w, t2)
+        e["arbitrary_rc"] = rc2
+        if rc2 == 0:
+            a, m = plan_arrays(plan2.summary(sc.n_samples), "plan1_")
+            arrays.update(a)
+            e["arbitrary"] = m
+    return e
+
+
+CASES = {"C2_2": c2, "C3_2": c3, "C4_2": c4, "C5_2": c5, "C2_1": c2_1deg, "C3_1": c3_1deg}
 
 
 def main():

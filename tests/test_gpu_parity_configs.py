@@ -10,6 +10,8 @@ produced (scripts/make_golden_configs.py -> tests/golden/configs/):
   C4_2  256^3 / 40 boxes: the first plan, then per control tick the overlay
         occupancy (sha256) and replan_dynamic's outcome (and plan)
   C2_1  C2 at the paper's finer 1-degree quiver (Q = 41,264)
+  C3_1  C3 at the 1-degree quiver: reach + path (fallback cascade) and the
+        arbitrary leg's outcome
   C5_2  512^3 / 40 boxes: the grid (sha256 of 128 MiB of reference bytes)
         and the first 16 of the 4096 batched targets: counters, solution and
         shortcut counts, chosen kind, path-length bits, segment-1/2 indices,
@@ -121,8 +123,13 @@ def test_c2_1deg_list_overflow_falls_back(ctx, monkeypatch):
     assert_plan_matches_fixture(plan.summary(), fx, meta["plan"], "plan0_", UNFOLD_TOL)
 
 
-def test_c3_2deg_reach_path_and_arbitrary(ctx):
-    api, sc, arm, rp, q, g, meta, fx, plan, s = _reach_path(ctx, "C3_2")
+@pytest.mark.parametrize("name", ["C3_2", "C3_1"])
+def test_c3_reach_path_and_arbitrary(ctx, name):
+    """The headline scene at the 2-degree quiver (delivered arbitrary-pose
+    path) and at the paper's 1-degree quiver (Q = 41,264: the first plan goes
+    through the fallback cascade to an alternate solution, and the arbitrary
+    leg is no-path, as the reference decides after 750 s of 16-core CPU)."""
+    api, sc, arm, rp, q, g, meta, fx, plan, s = _reach_path(ctx, name)
     assert list(sc.extra["second_target"]) == meta["second_target"]
     assert s is not None
     p, w = s["poses"][-1]
