@@ -356,6 +356,67 @@ using namespace rp;
 
 namespace rp {
 
+HostWorkers::~HostWorkers() {
+  {
+    std::lock_guard<std::mutex> lk(m_);
+    stop_ = true;
+  }
+  cv_.notify_all();
+  for (auto& t : threads_) t.join();
+}
+
+void HostWorkers::grow(int n) {
+  while (static_cast<int>(threads_.size()) < n) {
+    const int k = static_cast<int>(threads_.size());
+    const uint64_t g0 = gen_;  // before run() publishes the job: the new thread takes it
+    threads_.emplace_back([this, k, g0] {
+      cudaSetDevice(device_);
+      std::unique_lock<std::mutex> lk(m_);
+      uint64_t seen = g0;
+      for (;;) {
+        cv_.wait(lk, [&] { return stop_ || (gen_ != seen && k < n_); });
+        if (stop_) return;
+        seen = gen_;
+        const auto* f = job_;
+        lk.unlock();
+        try {
+          (*f)(k);  // callers capture their own exceptions; this only keeps the thread alive
+        } catch (...) {
+        }
+        lk.lock();
+        if (--left_ == 0) done_.notify_all();
+      }
+    });
+  }
+}
+
+void HostWorkers::run(int n, const std::function<void(int)>& f,
+                      const std::function<void()>& main_side) {
+  std::lock_guard<std::mutex> one(call_);  // one window at a time per context
+  std::unique_lock<std::mutex> lk(m_);
+  if (n > 0) {
+    grow(n);
+    job_ = &f;
+    n_ = n;
+    left_ = n;
+    ++gen_;
+    cv_.notify_all();
+  }
+  if (main_side) {  // on the calling thread, while the workers run
+    lk.unlock();
+    main_side();  // must not throw (callers capture their exceptions)
+    lk.lock();
+  }
+  done_.wait(lk, [&] { return left_ == 0; });
+  job_ = nullptr;
+  n_ = 0;
+}
+
+HostWorkers& host_workers(rp_ctx* ctx) {
+  if (!ctx->pool) ctx->pool = std::make_unique<HostWorkers>(ctx->device);
+  return *ctx->pool;
+}
+
 rp_ctx* worker_ctx(rp_ctx* parent, int k) {
   while (static_cast<int>(parent->workers.size()) <= k) {
     auto* c = new rp_ctx();
@@ -421,6 +482,7 @@ rp_status rp_ctx_create(int32_t device, rp_ctx** out) {
 rp_status rp_ctx_destroy(rp_ctx* ctx) {
   return guarded([&] {
     if (!ctx) return;
+    ctx->pool.reset();  // joins the worker threads
     for (rp_ctx* w : ctx->workers) rp_ctx_destroy(w);
     cudaStreamSynchronize(ctx->stream);
     for (auto& t : ctx->pending) {

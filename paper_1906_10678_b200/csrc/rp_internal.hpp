@@ -4,17 +4,20 @@
 #include "reachplan_b200.h"
 #include "rp_device.cuh"
 
-#include <cuda_runtime.h>
-
 #include <algorithm>
+
+#include <condition_variable>
 #include <cstdint>
+#include <cuda_runtime.h>
 #include <exception>
+#include <functional>
 #include <initializer_list>
 #include <map>
 #include <memory>
 #include <mutex>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace rp {
@@ -65,6 +68,30 @@ struct TimedLaunch {
 
 }  // namespace rp
 
+namespace rp {
+/// Persistent host threads of a context (one per worker slot), started on
+/// first use: run(n, f) executes f(k) on thread k for k < n and returns when
+/// all are done. Spawning threads per planner call cost ~0.1 ms per window.
+class HostWorkers {
+ public:
+  explicit HostWorkers(int device) : device_(device) {}
+  ~HostWorkers();
+  void run(int n, const std::function<void(int)>& f,
+           const std::function<void()>& main_side = {});
+
+ private:
+  void grow(int n);
+  int device_;
+  std::vector<std::thread> threads_;
+  std::mutex m_, call_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* job_ = nullptr;
+  int n_ = 0, left_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+}  // namespace rp
+
 struct rp_ctx {
   int device = 0;
   cudaStream_t own = nullptr;
@@ -85,6 +112,7 @@ struct rp_ctx {
   // Worker contexts (own streams, same device) for concurrent planner
   // attempts; created on first use, folded back by ctx_absorb.
   std::vector<rp_ctx*> workers;
+  std::unique_ptr<rp::HostWorkers> pool;  // threads for the concurrent planner attempts
   // Worker contexts: a device flag that stops this worker's cooperative pass
   // (set and cleared by DMA copies), and the auxiliary stream those copies
   // use on the parent.
@@ -112,6 +140,8 @@ struct rp_ctx {
 namespace rp {
 /// The k-th worker context of `parent` (created on first use).
 rp_ctx* worker_ctx(rp_ctx* parent, int k);
+/// The context's persistent worker threads (created on first use).
+rp::HostWorkers& host_workers(rp_ctx* ctx);
 /// Fold a worker's launch count and kernel timings into its parent.
 void ctx_absorb(rp_ctx* parent, rp_ctx* worker);
 }  // namespace rp

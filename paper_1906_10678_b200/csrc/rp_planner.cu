@@ -488,28 +488,27 @@ std::vector<Slot<R>> run_parallel(Planner& P, int n, const std::function<R(Plann
   std::vector<Slot<R>> out(n);
   std::vector<rp_ctx*> ws;
   for (int k = 0; k < n; ++k) ws.push_back(worker_ctx(P.ctx, k));
-  std::vector<std::thread> threads;
-  for (int k = 0; k < n; ++k) {
-    threads.emplace_back([&, k] {
-      try {
-        RP_CUDA(cudaSetDevice(P.ctx->device));
-        Planner W(ws[k], P.arm, P.q, P.g, P.rp, P.pp_in);
-        // co-residency of the concurrent cooperative passes (1 block per SM)
-        const int share = P.ctx->sm_count / n;
-        W.bp_blocks_cap = share >= 16 ? (share & ~15) : std::max(1, share);
-        out[k].value = work(W, k);
-      } catch (...) {
-        out[k].error = std::current_exception();
-      }
-    });
-  }
   std::exception_ptr main_error;
-  try {
-    if (main_side) main_side();
-  } catch (...) {
-    main_error = std::current_exception();
-  }
-  for (auto& t : threads) t.join();
+  host_workers(P.ctx).run(
+      n,
+      [&](int k) {
+        try {
+          Planner W(ws[k], P.arm, P.q, P.g, P.rp, P.pp_in);
+          // co-residency of the concurrent cooperative passes (1 block per SM)
+          const int share = P.ctx->sm_count / n;
+          W.bp_blocks_cap = share >= 16 ? (share & ~15) : std::max(1, share);
+          out[k].value = work(W, k);
+        } catch (...) {
+          out[k].error = std::current_exception();
+        }
+      },
+      [&] {
+        try {
+          if (main_side) main_side();
+        } catch (...) {
+          main_error = std::current_exception();
+        }
+      });
   for (rp_ctx* w : ws) ctx_absorb(P.ctx, w);
   if (main_error) std::rethrow_exception(main_error);
   return out;
@@ -624,9 +623,7 @@ std::pair<int, rp_plan*> cascade_pool(Planner& P, const Failure& failure, rp_sol
                                 cudaMemcpyHostToDevice, aux));
       }
   };
-  std::vector<std::thread> threads;
-  for (int k = 0; k < width; ++k) {
-    threads.emplace_back([&, k] {
+  const std::function<void(int)> worker = [&](int k) {
       std::unique_ptr<Planner> W;
       std::unique_lock<std::mutex> lk(m);
       // Alternates run in groups of `width`: group g >= 1 starts only when
@@ -685,25 +682,27 @@ std::pair<int, rp_plan*> cascade_pool(Planner& P, const Failure& failure, rp_sol
         done[j] = 1;
         cv.notify_all();
       }
-    });
-  }
+  };
   std::exception_ptr main_error;
-  try {
-    alts = alternate_candidates(P, set, failed, target);
-  } catch (...) {
-    main_error = std::current_exception();
-  }
-  {
-    std::lock_guard<std::mutex> lk(m);
-    if (!main_error) {
-      for (const Cand& c : alts) jobs.push_back({&c, &cloud});
-      res.resize(jobs.size());
-      done.resize(jobs.size(), 0);
+  host_workers(P.ctx).run(width, worker, [&] {
+    // the alternates are ranked on the calling thread while the first two
+    // jobs run on the workers
+    try {
+      alts = alternate_candidates(P, set, failed, target);
+    } catch (...) {
+      main_error = std::current_exception();
     }
-    closed = true;
-  }
-  cv.notify_all();
-  for (auto& t : threads) t.join();
+    {
+      std::lock_guard<std::mutex> lk(m);
+      if (!main_error) {
+        for (const Cand& c : alts) jobs.push_back({&c, &cloud});
+        res.resize(jobs.size());
+        done.resize(jobs.size(), 0);
+      }
+      closed = true;
+    }
+    cv.notify_all();
+  });
   RP_CUDA(cudaStreamSynchronize(aux));
   for (rp_ctx* w : ws) ctx_absorb(P.ctx, w);
   int win = -1;
