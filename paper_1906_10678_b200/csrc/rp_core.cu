@@ -501,6 +501,7 @@ rp_status rp_ctx_destroy(rp_ctx* ctx) {
     if (ctx->upload_ring) cudaFreeHost(ctx->upload_ring);
     if (ctx->cancel_flag) cudaFree(ctx->cancel_flag);
     if (ctx->aux) cudaStreamDestroy(ctx->aux);
+    if (ctx->aux_ev) cudaEventDestroy(ctx->aux_ev);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;
   });

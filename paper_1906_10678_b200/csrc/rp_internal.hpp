@@ -118,6 +118,7 @@ struct rp_ctx {
   // use on the parent.
   int* cancel_flag = nullptr;
   cudaStream_t aux = nullptr;
+  cudaEvent_t aux_ev = nullptr;  // "cancel flags cleared" on aux
   // Pinned upload ring (copy_to_device): kUploadSlots slots of
   // kUploadSlotBytes; a slot is reused only after the event recorded behind
   // its last copy completed, so uploads never synchronise the stream.

@@ -984,7 +984,11 @@ rp_plan* plan_virtual_path(Planner& P, const HostPose& start, NextBatch next_bat
         RP_CUDA(cudaMemcpyAsync(flags[k], pinned_01(), sizeof(int), cudaMemcpyHostToDevice,
                                 P.ctx->aux));
       }
-      RP_CUDA(cudaStreamSynchronize(P.ctx->aux));  // cleared before any pass reads them
+      // the passes wait for the clears on the device (no host synchronisation);
+      // later cancel copies follow them in the aux stream's order
+      if (!P.ctx->aux_ev) RP_CUDA(cudaEventCreateWithFlags(&P.ctx->aux_ev, cudaEventDisableTiming));
+      RP_CUDA(cudaEventRecord(P.ctx->aux_ev, P.ctx->aux));
+      cudaEvent_t cleared = P.ctx->aux_ev;
       std::mutex cm;
       int first_ok = m;
       std::vector<Slot<PassResult>> r = run_parallel<PassResult>(
@@ -995,6 +999,7 @@ rp_plan* plan_virtual_path(Planner& P, const HostPose& start, NextBatch next_bat
               if (k > first_ok) return PassResult{};  // an earlier candidate already won
             }
             W.cancel_flag = flags[k];
+            RP_CUDA(cudaStreamWaitEvent(W.ctx->stream, cleared, 0));
             PassResult pr = backward_pass(W, wps_list[a + k], anchor, opt);
             if (pr.ok) {
               std::lock_guard<std::mutex> lk(cm);
