@@ -508,16 +508,17 @@ def dominant_roofline(ctx, arm, q, sc, api, scenes):
            "ms": ms, "algorithmic_bytes_per_launch": sc.n ** 3 / 8 + pairs / 8,
            "algorithmic_bytes_def": "the bit grid once + one result bit per pair"}
     try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "r2_c3_seg2_ncu.json")))
+        prof = json.load(open(os.path.join(ROOT, "profiles", "r2b_c3_seg2_ncu.json")))
         m = prof["launches"][0]["metrics"]
         out.update({
             "frac": float(m["smsp__issue_active.avg.pct_of_peak_sustained_active"][0]) / 100,
             "frac_def": "ncu smsp__issue_active: the share of issue slots used (the issue "
                         "roofline); fp64 pipe " + prof["launches"][0]["pipes_pct_of_peak"]["fp64"][:4]
                         + "% of peak",
-            "traffic": 1e6 * (float(m["dram__bytes_read.sum"][0])
-                              + float(m["dram__bytes_write.sum"][0])),
-            "traffic_source": "profiles/r2_c3_seg2_ncu.json (ncu --set full, one launch)"})
+            "traffic": sum(float(m[k][0]) * {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6,
+                                               "Gbyte": 1e9}.get(m[k][1], 1.0)
+                           for k in ("dram__bytes_read.sum", "dram__bytes_write.sum")),
+            "traffic_source": "profiles/r2b_c3_seg2_ncu.json (ncu --set full, one launch)"})
     except (OSError, KeyError, ValueError, IndexError):
         pass
     return out
@@ -885,10 +886,13 @@ def voxel_update(ctx, torch, stream):
     achieved = bytes_alg / (per_launch * 1e-3) / 1e9
     traffic, traffic_src = None, None
     try:
-        prof = _json.load(open(os.path.join(ROOT, "profiles", "r1j_dilate512_ncu.json")))
-        traffic = prof["dram_bytes_per_launch"]
-        traffic_src = "profiles/r1j_dilate512_ncu.json (ncu --set full, one launch)"
-    except (OSError, KeyError, ValueError):
+        prof = _json.load(open(os.path.join(ROOT, "profiles", "r2b_dilate512_ncu.json")))
+        m = prof["launches"][0]["metrics"]
+        unit = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        traffic = sum(float(m[k][0]) * unit.get(m[k][1], 1.0)
+                      for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        traffic_src = "profiles/r2b_dilate512_ncu.json (ncu --set full, one launch)"
+    except (OSError, KeyError, ValueError, IndexError):
         pass
     return {"roofline": {"kernel": "k_mark_dilate_plane<8,256,true> (fused box rasterise + ball "
                                    "dilation, 512^3, 256-row plane runs staged 64B-swizzled, one "
