@@ -41,7 +41,28 @@ def _scene(case):
         sc = scenes.config("C2", quiver_deg=5.0)
         sc.target = (0.62, 0.35, 0.3)
         return sc
+    if case == "spec":  # SPEC.md:389's straight chain: few survivor rows
+        return scenes.Scene("spec", 64, [], (1.0, 1.0, 1.0, 0.25), abi.RP_MODE_8DOF,
+                            target=(3.25, 0.0, 0.0), quiver_deg=10.0)
     raise ValueError(case)
+
+
+def test_more_parts_than_rows(ctx):
+    """Parts beyond the survivor count are empty and merge away."""
+    api = _api()
+    sc = _scene("spec")
+    arm, rp, q, g = gpu_problem(ctx, sc)
+    whole = api.solve_reach(ctx, arm, q, g, sc.target, rp)
+    S1 = whole.stats().seg1_survivors
+    parts = 4 * S1 + 3
+    got = shard.merge_parts([
+        shard.part_summary(api.solve_reach_part(ctx, arm, q, g, sc.target, rp, k, parts), k,
+                           with_keys=True) for k in range(parts)])
+    want = shard.part_summary(whole, 0, with_keys=True)
+    assert got["counters"] == want["counters"]
+    assert np.array_equal(got["keys"], want["keys"])
+    assert (got["chosen"]["index"], got["chosen"]["path_length"]) == \
+        (want["chosen"]["index"], want["chosen"]["path_length"])
 
 
 @pytest.mark.parametrize("case", ["C2", "C3", "C2_1deg", "limits", "cone", "shortcuts"])
