@@ -68,6 +68,8 @@ def lib():
         L.ref_select.argtypes = [vp, P(abi.Chosen)]
         L.ref_refine.argtypes = [vp, P(abi.Pose), P(C.c_double), C.c_int, P(abi.Pose)]
         L.ref_plan_reach_then_path.argtypes = [vp, P(C.c_double), P(abi.PathParams), P(vp)]
+        L.ref_plan_from_chosen.argtypes = [vp, C.c_int, C.c_int64, P(C.c_double),
+                                           P(abi.PathParams), P(vp)]
         L.ref_plan_arbitrary.argtypes = [vp, P(abi.Pose), vp, P(C.c_double), P(abi.PathParams),
                                          P(vp)]
         L.ref_replan_dynamic.argtypes = [vp, vp, C.c_int, P(abi.Obstacle), C.c_double,
@@ -304,6 +306,16 @@ class RefProblem:
         pp = pp or abi.make_path_params()
         h = C.c_void_p()
         rc = lib().ref_plan_reach_then_path(self.h, _d3(target), C.byref(pp), C.byref(h))
+        if rc != 0:
+            return rc, None
+        return 0, RefPlan(h)
+
+    def plan_from_chosen(self, kind, index, target=None, pp=None):
+        """plan_from_reach from solution / shortcut `index` of the last solve."""
+        target = self.scene.target if target is None else target
+        pp = pp or abi.make_path_params()
+        h = C.c_void_p()
+        rc = lib().ref_plan_from_chosen(self.h, kind, index, _d3(target), C.byref(pp), C.byref(h))
         if rc != 0:
             return rc, None
         return 0, RefPlan(h)

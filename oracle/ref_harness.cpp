@@ -449,6 +449,28 @@ int ref_plan_reach_then_path(ref_problem* p, const double* target, const rp_path
   }
 }
 
+/// plan_from_reach (src/path_planner.cpp:729-738) from a chosen candidate of
+/// the last solve: solution `index` (kind 0) or shortcut `index` (kind 1).
+int ref_plan_from_chosen(ref_problem* p, int kind, int64_t index, const double* target,
+                         const rp_path_params* pp, ref_plan** out) {
+  try {
+    ChosenPath c;
+    if (kind == RP_CHOSEN_REACH_POSE) {
+      c.kind = ChosenPath::Kind::reach_pose;
+      c.pose = p->last.solutions.at(static_cast<std::size_t>(index));
+    } else {
+      c.kind = ChosenPath::Kind::shortcut;
+      c.shortcut = p->last.shortcuts.at(static_cast<std::size_t>(index));
+      c.path_length = c.shortcut.path_length;
+    }
+    return plan_result(plan_from_reach(p->arm, p->quiver, p->grid, c, p->last, v3(target), p->rp,
+                                       to_pp(*pp)),
+                       out);
+  } catch (const Error& e) {
+    return status_of(e);
+  }
+}
+
 /// The reference's own stage timer, cmd_bench (src/cli.cpp:272-308), on this
 /// problem: ms[0] = prune_segment1 alone, ms[1] = solve_reach, ms[2] =
 /// select_solution + plan_from_reach (cmd_bench's path-ms excludes the

@@ -425,6 +425,7 @@ rp_ctx* worker_ctx(rp_ctx* parent, int k) {
     RP_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
     c->stream = c->own;
     c->sm_count = parent->sm_count;
+    c->parent = parent;
     RP_CUDA(cudaMalloc(reinterpret_cast<void**>(&c->cancel_flag), sizeof(int)));
     RP_CUDA(cudaMemset(c->cancel_flag, 0, sizeof(int)));
     parent->workers.push_back(c);

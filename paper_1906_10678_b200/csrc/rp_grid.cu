@@ -1401,8 +1401,12 @@ rp_grid* grid_alloc_like(const rp_grid* src) {
   return g;
 }
 
-ClearanceField grid_clearance_field(const rp_grid* g) {
-  rp_ctx* ctx = g->ctx;
+ClearanceField grid_clearance_field(const rp_grid* g, rp_ctx* caller) {
+  // built (once per grid version) in the caller's stream order; a caller on
+  // another stream of the same device (a worker context) waits for the
+  // build's event instead
+  rp_ctx* ctx = caller ? caller : g->ctx;
+  std::lock_guard<std::mutex> lock(*g->s2_mutex);
   const int dmax = std::max(g->dims[0], std::max(g->dims[1], g->dims[2]));
   int bk = 1;
   while (dmax > 64 * bk) bk *= 2;  // coarse lines of <= 64 cells
@@ -1417,9 +1421,11 @@ ClearanceField grid_clearance_field(const rp_grid* g) {
   const size_t cells = static_cast<size_t>(f.ncx) * f.ncy * f.ncz;
   if (g->cf && g->cf_version == g->version && !g->exported && g->cf_bk == bk) {
     f.d2 = g->cf;
+    if (g->cf_ready) RP_CUDA(cudaStreamWaitEvent(ctx->stream, g->cf_ready, 0));
     return f;
   }
   cudaStream_t st = ctx->stream;
+  if (g->cf_ready) RP_CUDA(cudaStreamWaitEvent(st, g->cf_ready, 0));  // readers of the old field
   if (!g->cf) RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&g->cf), cells * sizeof(uint16_t), st));
   DevBuf<uint8_t> occ(cells, st);
   DevBuf<unsigned> work(cells, st), work2(cells, st);
@@ -1441,6 +1447,8 @@ ClearanceField grid_clearance_field(const rp_grid* g) {
        1, static_cast<int64_t>(f.ncx) * f.ncy, f.ncx);
   pass(k_cf_pass<false, true>, work2.p, g->cf, f.ncz, static_cast<int64_t>(f.ncx) * f.ncy,
        static_cast<int64_t>(f.ncx) * f.ncy, 1, f.ncx, f.ncx);
+  if (!g->cf_ready) RP_CUDA(cudaEventCreateWithFlags(&g->cf_ready, cudaEventDisableTiming));
+  RP_CUDA(cudaEventRecord(g->cf_ready, st));
   g->cf_bk = bk;
   g->cf_nc[0] = f.ncx;
   g->cf_nc[1] = f.ncy;
@@ -2066,7 +2074,9 @@ rp_status rp_grid_destroy(rp_grid* g) {
   return guarded([&] {
     if (!g) return;
     if (g->bits) RP_CUDA(cudaFreeAsync(g->bits, g->ctx->stream));
+    if (g->cf_ready) RP_CUDA(cudaStreamWaitEvent(g->ctx->stream, g->cf_ready, 0));
     if (g->cf) RP_CUDA(cudaFreeAsync(g->cf, g->ctx->stream));
+    if (g->cf_ready) cudaEventDestroy(g->cf_ready);
     if (g->w1.bits) {
       if (g->w1.ready) RP_CUDA(cudaStreamWaitEvent(g->ctx->stream, g->w1.ready, 0));
       RP_CUDA(cudaFreeAsync(g->w1.bits, g->ctx->stream));

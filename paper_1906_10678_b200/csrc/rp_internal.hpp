@@ -112,6 +112,7 @@ struct rp_ctx {
   // Worker contexts (own streams, same device) for concurrent planner
   // attempts; created on first use, folded back by ctx_absorb.
   std::vector<rp_ctx*> workers;
+  rp_ctx* parent = nullptr;  // worker contexts: the context they serve (same device)
   std::unique_ptr<rp::HostWorkers> pool;  // threads for the concurrent planner attempts
   // Worker contexts: a device flag that stops this worker's cooperative pass
   // (set and cleared by DMA copies), and the auxiliary stream those copies
@@ -141,6 +142,13 @@ struct rp_ctx {
 namespace rp {
 /// The k-th worker context of `parent` (created on first use).
 rp_ctx* worker_ctx(rp_ctx* parent, int k);
+/// True when objects of context `owner` may be used on context `user`: the
+/// same context, or worker contexts of one parent (same device).
+inline bool ctx_shares(const rp_ctx* user, const rp_ctx* owner) {
+  const rp_ctx* a = user->parent ? user->parent : user;
+  const rp_ctx* b = owner->parent ? owner->parent : owner;
+  return a == b;
+}
 /// The context's persistent worker threads (created on first use).
 rp::HostWorkers& host_workers(rp_ctx* ctx);
 /// Fold a worker's launch count and kernel timings into its parent.
@@ -186,6 +194,7 @@ struct rp_grid {
   bool exported = false;
   mutable uint64_t cf_version = ~0ull;
   mutable uint16_t* cf = nullptr;
+  mutable cudaEvent_t cf_ready = nullptr;  // recorded after the field's build
   mutable int cf_bk = 0;
   mutable int cf_nc[3] = {0, 0, 0};
   // Segment-2 clearance cache (grid_seg2_cache): walk verdicts of
@@ -393,7 +402,7 @@ struct ClearanceField {
   int bk, ncx, ncy, ncz;
   double side, inv_side;
 };
-ClearanceField grid_clearance_field(const rp_grid* g);
+ClearanceField grid_clearance_field(const rp_grid* g, rp_ctx* caller = nullptr);
 
 /// The grid's cache of segment-2 walk verdicts for an arm (root, L1, L2, n)
 /// and quiver: bits[i * ceil(Q/32) + j/32] bit j%32 = walk clear, valid for

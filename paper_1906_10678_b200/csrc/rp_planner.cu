@@ -6,6 +6,7 @@
 #include "rp_planner.hpp"
 
 #include <algorithm>
+#include <cstdio>
 #include <climits>
 #include <condition_variable>
 #include <mutex>
@@ -678,6 +679,12 @@ std::pair<int, rp_plan*> cascade_pool(Planner& P, const Failure& failure, rp_sol
           decided = j;
           cancel_later();
         }
+        static const bool dbg = std::getenv("RP_DEBUG_CASCADE") != nullptr;
+        if (dbg)
+          std::fprintf(stderr, "[cascade] job %zu kind %d ordinal %lld -> %s%s\n", j, job.cand->kind,
+                       static_cast<long long>(job.cand->ordinal),
+                       out.value.plan ? "plan" : (out.error ? "error" : "fail: "),
+                       out.value.plan || out.error ? "" : out.value.failure.reason.c_str());
         res[j] = std::move(out);
         done[j] = 1;
         cv.notify_all();

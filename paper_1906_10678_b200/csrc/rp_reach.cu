@@ -1019,7 +1019,7 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
   const double off3 = arm.n_offsets > 3 ? arm.offsets[3] : 0.0;
   require(off2 == 0.0 && off3 == 0.0, RP_E_INVALID_PARAMETER,
           "reach solving supports joint offsets at joints 1 and 2 only");
-  require(q && g && q->ctx == ctx && g->ctx == ctx, RP_E_INVALID_PARAMETER,
+  require(q && g && ctx_shares(ctx, q->ctx) && ctx_shares(ctx, g->ctx), RP_E_INVALID_PARAMETER,
           "quiver / grid belong to another context");
 
   auto* s = new rp_solution_set();
@@ -1161,7 +1161,7 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
           kskip.zero();
           RP_CUDA(cudaMemsetAsync(kend_b.p, rp.n_samples, 1, st));
         } else {
-          const ClearanceField cf = grid_clearance_field(g);
+          const ClearanceField cf = grid_clearance_field(g, ctx);
           launch(ctx, "seg2", k_row_skip, dim3(nblk(std::max(1, cap_rows), 128)), dim3(128), 0, a,
                  static_cast<const SurvDev*>(s->surv.p), static_cast<const int*>(surv_cnt.p), cf,
                  kskip.p);
@@ -2527,7 +2527,7 @@ extern "C" rp_status rp_solve_reach_batch(rp_ctx* ctx, const rp_arm* arm, const 
     const std::vector<BestRec> tbest_init(CH, BestRec{1e308, LLONG_MAX});
     // the grid's clearance field (cached) for k_tail_skip
     static const bool no_skip = std::getenv("RP_NO_ROW_SKIP") != nullptr;
-    const ClearanceField cf = no_skip ? ClearanceField{} : grid_clearance_field(g);
+    const ClearanceField cf = no_skip ? ClearanceField{} : grid_clearance_field(g, ctx);
     DevBuf<uint8_t> d_kend(CH, st);
     DevBuf<long long> d_scl(kBatchShortcutCap, st);
     DevBuf<BestRec> d_bb(static_cast<size_t>(CH) * BPT, st), d_best(CH, st);
