@@ -8,6 +8,7 @@ outcome (error class or the whole plan) and, after a delivered plan,
 plan_arbitrary from its final pose to a second random target. The scenes are small (32-96^3,
 5-12 degrees) so each reference run takes well under a second."""
 import math
+import os
 
 import numpy as np
 import pytest
@@ -20,7 +21,7 @@ from test_gpu_general import ArmScene
 pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")]
 
-SEEDS = list(range(48))
+SEEDS = list(range(int(os.environ.get("RP_FUZZ_SEEDS", "48"))))
 
 
 def _scene(seed):
@@ -94,3 +95,60 @@ def test_random_scene_solve_and_plan(ctx, seed):
     assert grc2 == rrc2, (seed, grc2, rrc2)
     if rrc2 == 0:
         assert_plan_equal(gplan2.summary(), rplan2.summary(rp.n_samples), 1e-9)
+    # one replan_dynamic tick: a cube on a later waypoint's tracked point
+    # while the arm is early on the path (outcome class and plan)
+    m = len(rs["poses"])
+    if m >= 6:
+        at = int(rng.integers(0, max(1, m // 3)))
+        idx = int(rng.integers(at + 3, m))
+        c = np.asarray(rs["poses"][idx][0].joints[rs["poses"][idx][0].n_segments][:])
+        half = float(rng.uniform(0.01, 0.05))
+        obs = abi.box(tuple(c - half), tuple(c + half), dynamic=True)
+        rrc3, rplan3 = R.replan(rplan, at, obs)
+        grc3, gplan3 = api.replan_dynamic(ctx, arm, q, g, gplan, at, obs, rp)
+        assert grc3 == rrc3, (seed, "replan", grc3, rrc3)
+        if rrc3 == 0:
+            assert_plan_equal(gplan3.summary(), rplan3.summary(rp.n_samples), 1e-9)
+
+
+@pytest.mark.parametrize("seed", SEEDS[:16])
+def test_random_scene_batch(ctx, seed):
+    """The batched pipeline (rp_solve_reach_batch: its own kernels) against the
+    reference's solve + select + refine per target, 6 random targets."""
+    api = _api()
+    sc = _scene(seed)
+    if sc.mode != abi.RP_MODE_8DOF or getattr(sc, "_rp_over", None):
+        pytest.skip("the batch covers default 8-DOF queries")
+    arm, rp, q, g = gpu_problem(ctx, sc)
+    R = ref.RefProblem(sc)
+    R.set_params(rp)
+    rng = np.random.default_rng(3000 + seed)
+    ts = []
+    while len(ts) < 6:
+        d = rng.normal(size=3)
+        t = d / np.linalg.norm(d) * rng.uniform(0.3, 1.45)
+        if R.point_clear(t[None, :])[0]:
+            ts.append(t)
+    res = api.solve_reach_batch(ctx, arm, q, g, np.array(ts), rp)
+    for t, r in zip(ts, res):
+        st, ns, nc = R.solve(tuple(t))
+        assert r.stats.counters() == st.counters(), (seed, t)
+        assert (r.n_solutions, r.n_shortcuts) == (ns, nc)
+        if ns + nc == 0:
+            assert r.status == abi.RP_E_NO_SOLUTION
+            continue
+        c = R.select()
+        assert r.kind == c.kind
+        assert np.float64(r.path_length).tobytes() == np.float64(c.path_length).tobytes()
+        if c.kind == abi.RP_CHOSEN_REACH_POSE:
+            p, _ = R.pose(c.index)
+            assert [r.seg1, r.seg2] == [p.quiver_indices[0], p.quiver_indices[1]]
+            try:
+                want = R.refine(p, tuple(t), triangle=bool(rp.refine_triangle_8dof))
+            except ref.RefError as err:
+                assert r.status == err.code
+                continue
+            assert r.status == 0
+            n = want.n_segments
+            assert np.array([r.refined.segments[k][:] for k in range(n)]).tobytes() == \
+                np.array([want.segments[k][:] for k in range(n)]).tobytes()
