@@ -1,12 +1,15 @@
 """Randomised parity: seeded random scenes (box count, sizes, grid size,
-quiver step, 6/8-DOF, target anywhere in the reach shell, a 15-degree
-approach cone now and then) solved and planned on the GPU and by the
-reference (oracle/_ref), everything compared bit for bit as in
+quiver step, samples per segment, 6/8-DOF, target anywhere in the reach
+shell, a 15-degree approach cone now and then) solved and planned on the GPU
+and by the reference (oracle/_ref), everything compared bit for bit as in
 test_gpu_parity.py: the 13 counters, every canonical key, every shortcut,
 the chosen solution, sampled solution poses, the plan_reach_then_path
-outcome (error class or the whole plan) and, after a delivered plan,
-plan_arbitrary from its final pose to a second random target. The scenes are small (32-96^3,
-5-12 degrees) so each reference run takes well under a second."""
+outcome (error class or the whole plan), plan_arbitrary from its final pose
+to a second random target and one replan_dynamic tick; the batched pipeline
+on a few targets. The small scenes (32-96^3, 5-12 degrees) take well under a
+second of reference CPU each; a few medium ones (128^3, 3-4 degrees, more
+boxes) reach the fallback cascade more often.
+RP_FUZZ_SEEDS / RP_FUZZ_MEDIUM set the counts (48 / 3; 160 / 6 pass)."""
 import math
 import os
 
@@ -40,8 +43,14 @@ def _scene(seed):
     base = scenes.Scene(f"fuzz{seed}", n, boxes, lengths,
                         abi.RP_MODE_8DOF if eight else abi.RP_MODE_6DOF, target=t,
                         quiver_deg=deg)
+    # samples per segment: 8 in half the scenes (the default everywhere else),
+    # else 4-12 (other walk and waypoint counts); drawn apart so the scene
+    # layout above does not depend on it
+    base.n_samples = int(np.random.default_rng(11000 + seed).choice([8, 8, 8, 4, 5, 6, 10, 12]))
     if eight and rng.integers(0, 4) == 0:
-        return ArmScene(base, approach_half_angle=math.radians(15.0))
+        sc = ArmScene(base, approach_half_angle=math.radians(15.0))
+        sc.n_samples = base.n_samples
+        return sc
     return base
 
 
@@ -50,10 +59,30 @@ def _api():
     return api
 
 
+MEDIUM = list(range(int(os.environ.get("RP_FUZZ_MEDIUM", "3"))))
+
+
+def _medium_scene(seed):
+    rng = np.random.default_rng(21000 + seed)
+    base = _scene(1000 + seed)
+    boxes = scenes.random_boxes(int(rng.integers(8, 25)), 22000 + seed, targets=(base.target,))
+    sc = scenes.Scene(f"medium{seed}", 128, boxes, scenes.L8, abi.RP_MODE_8DOF,
+                      target=base.target, quiver_deg=float(rng.choice([3.0, 4.0])))
+    return sc
+
+
+@pytest.mark.parametrize("seed", MEDIUM)
+def test_random_medium_scene_plan(ctx, seed):
+    _solve_and_plan(ctx, _medium_scene(seed), 1000 + seed)
+
+
 @pytest.mark.parametrize("seed", SEEDS)
 def test_random_scene_solve_and_plan(ctx, seed):
+    _solve_and_plan(ctx, _scene(seed), seed)
+
+
+def _solve_and_plan(ctx, sc, seed):
     api = _api()
-    sc = _scene(seed)
     arm, rp, q, g = gpu_problem(ctx, sc)
     R = ref.RefProblem(sc)
     R.set_params(rp)
