@@ -2737,6 +2737,14 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
                                    double cloud_radius, const HostPose* fixed_first,
                                    const HostPose* bias, BpOut* out) {
   HostSpan span_("Planner::backward_pass_device");
+  if (!bp_launch(wps, anchor, factors, cloud, cloud_radius, fixed_first, bias)) return false;
+  return bp_finish(out);
+}
+
+bool Planner::bp_launch(const std::vector<V3>& wps, const HostPose& anchor,
+                        const std::vector<double>& factors, bool cloud, double cloud_radius,
+                        const HostPose* fixed_first, const HostPose* bias) {
+  HostSpan span_("bp launch");
   if (!use_device_pass || factors.size() > static_cast<size_t>(kBpMaxFactors) || wps.size() < 2)
     return false;
   cudaStream_t st = ctx->stream;
@@ -2883,7 +2891,7 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
   A.state = reinterpret_cast<int*>(io);
   A.cancel = cancel_flag;
   static const bool profile = std::getenv("RP_PROFILE_PASS") != nullptr;
-  DevBuf<long long> prof;
+  DevBuf<long long>& prof = bp_prof;
   if (profile) {
     prof.alloc(24, st);
     prof.zero();
@@ -2939,6 +2947,22 @@ bool Planner::backward_pass_device(const std::vector<V3>& wps, const HostPose& a
                                         dim3(kBpThreads), args, smem, st));
     launch_end(ctx, "backward_pass", ev);
   }
+  bp_pend = BpPending{true, m, o_wps, o_poses, o_relax, o_kind, o_win, cluster};
+  return true;
+}
+
+bool Planner::bp_finish(BpOut* out) {
+  HostSpan span_("bp finish");
+  require(bp_pend.active, RP_E_INTERNAL, "no backward pass in flight");
+  const BpPending pd = bp_pend;
+  bp_pend.active = false;
+  const int m = pd.m;
+  const size_t o_wps = pd.o_wps, o_poses = pd.o_poses, o_relax = pd.o_relax, o_kind = pd.o_kind,
+               o_win = pd.o_win;
+  const bool cluster = pd.cluster;
+  unsigned char* io = bp_io.p;
+  static const bool profile = std::getenv("RP_PROFILE_PASS") != nullptr;
+  DevBuf<long long>& prof = bp_prof;
   // the state and the pass's outputs in one read-back
   int hs[4];
   {

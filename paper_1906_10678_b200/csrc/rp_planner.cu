@@ -110,19 +110,16 @@ struct Failure {
   std::shared_ptr<const Build> build;
 };
 
-/// backward_pass (src/path_planner.cpp:322-400)
-PassResult backward_pass(Planner& P, const std::vector<V3>& waypoints, const HostPose& anchor,
-                         const PassOptions& opt) {
-  HostSpan span_("backward_pass");
+/// backward_pass's result from a finished device pass.
+PassResult pass_from_device(const Planner::BpOut& bo, const std::vector<V3>& waypoints,
+                            const HostPose& anchor, const PassOptions& opt) {
   PassResult res;
   const size_t m = waypoints.size();
   res.poses.assign(m, HostPose{});
   res.relax.assign(m, 1.0);
   res.waypoints = waypoints;
   res.poses[m - 1] = anchor;
-  Planner::BpOut bo;
-  if (P.backward_pass_device(waypoints, anchor, opt.factors, opt.cloud, opt.cloud_radius,
-                             opt.fixed_first, opt.junction_bias, &bo)) {
+  {
     res.waypoints = bo.wps;
     res.relax = bo.relax;
     if (!bo.ok) {
@@ -146,6 +143,18 @@ PassResult backward_pass(Planner& P, const std::vector<V3>& waypoints, const Hos
     res.ok = true;
     return res;
   }
+}
+
+/// The host-sequenced backward pass (configurations past the device pass's
+/// limits): one waypoint_ik launch sequence per waypoint.
+PassResult backward_pass_sequenced(Planner& P, const std::vector<V3>& waypoints,
+                                   const HostPose& anchor, const PassOptions& opt) {
+  PassResult res;
+  const size_t m = waypoints.size();
+  res.poses.assign(m, HostPose{});
+  res.relax.assign(m, 1.0);
+  res.waypoints = waypoints;
+  res.poses[m - 1] = anchor;
   for (size_t k = m - 1; k-- > 0;) {
     const HostPose prev = res.poses[k + 1];
     bool found = false;
@@ -207,6 +216,18 @@ PassResult backward_pass(Planner& P, const std::vector<V3>& waypoints, const Hos
   }
   res.ok = true;
   return res;
+}
+
+/// backward_pass (src/path_planner.cpp:322-400): the device pass, or the
+/// sequenced one where the device pass does not apply.
+PassResult backward_pass(Planner& P, const std::vector<V3>& waypoints, const HostPose& anchor,
+                         const PassOptions& opt) {
+  HostSpan span_("backward_pass");
+  Planner::BpOut bo;
+  if (P.backward_pass_device(waypoints, anchor, opt.factors, opt.cloud, opt.cloud_radius,
+                             opt.fixed_first, opt.junction_bias, &bo))
+    return pass_from_device(bo, waypoints, anchor, opt);
+  return backward_pass_sequenced(P, waypoints, anchor, opt);
 }
 
 struct Build {
@@ -996,35 +1017,60 @@ rp_plan* plan_virtual_path(Planner& P, const HostPose& start, NextBatch next_bat
       if (!P.ctx->aux_ev) RP_CUDA(cudaEventCreateWithFlags(&P.ctx->aux_ev, cudaEventDisableTiming));
       RP_CUDA(cudaEventRecord(P.ctx->aux_ev, P.ctx->aux));
       cudaEvent_t cleared = P.ctx->aux_ev;
-      std::mutex cm;
-      int first_ok = m;
-      std::vector<Slot<PassResult>> r = run_parallel<PassResult>(
-          P, m,
-          [&](Planner& W, int k) {
-            {
-              std::lock_guard<std::mutex> lk(cm);
-              if (k > first_ok) return PassResult{};  // an earlier candidate already won
+      // Every candidate's pass is set up and launched from this thread on
+      // its worker context's stream (no host threads: the passes' host
+      // setup is short and serial anyway), then the results are taken in
+      // candidate order; the first success cancels the passes after it.
+      std::vector<std::unique_ptr<Planner>> Ws(m);
+      std::vector<char> launched(m, 0), finished(m, 0);
+      auto settle = [&] {  // no pass may outlive its planner's buffers
+        for (int k = 0; k < m; ++k)
+          if (launched[k] && !finished[k]) {
+            Planner::BpOut bo;
+            try {
+              Ws[k]->bp_finish(&bo);
+            } catch (...) {
             }
-            W.cancel_flag = flags[k];
-            RP_CUDA(cudaStreamWaitEvent(W.ctx->stream, cleared, 0));
-            PassResult pr = backward_pass(W, wps_list[a + k], anchor, opt);
-            if (pr.ok) {
-              std::lock_guard<std::mutex> lk(cm);
-              if (k < first_ok) {
-                for (int j = k + 1; j < first_ok; ++j)
-                  RP_CUDA(cudaMemcpyAsync(flags[j], pinned_01() + 1, sizeof(int),
-                                          cudaMemcpyHostToDevice, P.ctx->aux));
-                first_ok = k;
-              }
-            }
-            return pr;
-          },
-          {});
-      RP_CUDA(cudaStreamSynchronize(P.ctx->aux));
-      for (auto& slot : r) {
-        if (slot.error) std::rethrow_exception(slot.error);
-        if (slot.value.ok) return to_plan(slot.value);
+            finished[k] = 1;
+          }
+        cudaStreamSynchronize(P.ctx->aux);
+        for (int k = 0; k < m; ++k) ctx_absorb(P.ctx, worker_ctx(P.ctx, k));
+      };
+      rp_plan* won = nullptr;
+      try {
+        for (int k = 0; k < m; ++k) {
+          rp_ctx* wc = worker_ctx(P.ctx, k);
+          Ws[k] = std::make_unique<Planner>(wc, P.arm, P.q, P.g, P.rp, P.pp_in);
+          const int share = P.ctx->sm_count / m;
+          Ws[k]->bp_blocks_cap = share >= 16 ? (share & ~15) : std::max(1, share);
+          Ws[k]->cancel_flag = flags[k];
+          RP_CUDA(cudaStreamWaitEvent(wc->stream, cleared, 0));
+          launched[k] = Ws[k]->bp_launch(wps_list[a + k], anchor, opt.factors, opt.cloud,
+                                         opt.cloud_radius, opt.fixed_first, opt.junction_bias)
+                            ? 1
+                            : 0;
+        }
+        for (int k = 0; k < m && !won; ++k) {
+          PassResult pr;
+          Planner::BpOut bo;
+          const bool dev = launched[k] && Ws[k]->bp_finish(&bo);
+          finished[k] = 1;
+          pr = dev ? pass_from_device(bo, wps_list[a + k], anchor, opt)
+                   : backward_pass_sequenced(*Ws[k], wps_list[a + k], anchor, opt);
+          if (pr.ok) {
+            for (int j = k + 1; j < m; ++j)
+              if (launched[j])
+                RP_CUDA(cudaMemcpyAsync(flags[j], pinned_01() + 1, sizeof(int),
+                                        cudaMemcpyHostToDevice, P.ctx->aux));
+            won = to_plan(pr);
+          }
+        }
+      } catch (...) {
+        settle();
+        throw;
       }
+      settle();
+      if (won) return won;
     }
   }
 }

@@ -85,6 +85,22 @@ struct Planner {
                             const std::vector<double>& factors, bool cloud, double cloud_radius,
                             const HostPose* fixed_first, const HostPose* bias, BpOut* out);
   DevBuf<unsigned char> bp_io;  // a pass's inputs + outputs (backward_pass_device)
+  DevBuf<long long> bp_prof;    // RP_PROFILE_PASS counters
+  /// backward_pass_device split around the kernel: bp_launch enqueues the
+  /// pass on this planner's stream (false: not supported, nothing done),
+  /// bp_finish waits for it and reads the result (false: the sequenced pass
+  /// must decide). Several planners' passes can be in flight at once.
+  struct BpPending {
+    bool active = false;
+    int m = 0;
+    size_t o_wps = 0, o_poses = 0, o_relax = 0, o_kind = 0, o_win = 0;
+    bool cluster = false;
+  };
+  BpPending bp_pend;
+  bool bp_launch(const std::vector<V3>& wps, const HostPose& anchor,
+                 const std::vector<double>& factors, bool cloud, double cloud_radius,
+                 const HostPose* fixed_first, const HostPose* bias);
+  bool bp_finish(BpOut* out);
   DevBuf<unsigned> bp_bar;
   DevBuf<WikBest> bp_best;
   int bp_blocks = 0;
