@@ -376,7 +376,7 @@ __global__ void k_row_skip(SolveDev a, const SurvDev* __restrict__ sv, const int
 }
 
 template <bool EIGHT>
-__global__ void __launch_bounds__(256, 4) k_seg2_rows(SolveDev a, const SurvDev* __restrict__ sv,
+__global__ void __launch_bounds__(256, 5) k_seg2_rows(SolveDev a, const SurvDev* __restrict__ sv,
                                                    const int* __restrict__ S1p, int part, int parts,
                                                    uint32_t* __restrict__ sol_bits,
                                                    unsigned long long* ctr, long long* sc_list,
@@ -2143,7 +2143,7 @@ __device__ __forceinline__ bool best_less(const BestRec& x, const BestRec& y) {
 /// v3-clear / solution counters and the (length, key) argmin -- the same
 /// arithmetic heavy() performs in place.
 template <bool EIGHT>
-__global__ void __launch_bounds__(kTailBlock, 4) k_bq_tail(BatchDev d) {
+__global__ void __launch_bounds__(kTailBlock, 5) k_bq_tail(BatchDev d) {
   const int c = blockIdx.x;
   const int t = d.tail_tgt[c];
   const int len = d.tail_len[c];
