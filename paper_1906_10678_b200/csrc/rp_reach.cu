@@ -1103,19 +1103,20 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
     const bool B1 = s->B == 1;
     const bool general = a.arm.any_limit || a.arm.has_offsets || (rp.cone_precheck && eight);
     static const bool flat = std::getenv("RP_SEG2_FLAT") != nullptr;
-    // The row kernel path (default arms, one backward point) runs without a
-    // host read-back between the prune and segment 2: buffers are sized for
+    // The row kernel (default arms, one backward point) runs without a host
+    // read-back between the prune and segment 2: buffers are sized for
     // S1 <= Q and the kernels read S1 on the device; the count and the
-    // survivor list come back with the solve's counters. Other paths (and
-    // quivers past 16384 directions, whose Q^2 bit set would be large) read
-    // S1 first.
-    const bool rows_path = !general && B1 && !flat && q->n <= 16384;
+    // survivor list come back with the solve's counters. The flat kernel
+    // (limits, offsets, cones) and quivers past 16384 directions (whose Q^2
+    // bit set would be large) read S1 first.
+    const bool rows_kernel = !general && B1 && !flat;
+    const bool sync_free = rows_kernel && q->n <= 16384;
     int S1 = 0;
     std::vector<int> surv_all(q->n);
-    if (!rows_path)
+    if (!sync_free)
       copy_to_host_many(ctx, {{&S1, surv_cnt.p, sizeof(int)},
                               {surv_all.data(), surv_idx.p, q->n * sizeof(int)}});
-    const int cap_rows = rows_path ? q->n : S1;
+    const int cap_rows = sync_free ? q->n : S1;
     s->surv.alloc(cap_rows + 1, st);
     if (cap_rows > 0)
       launch(ctx, "seg1", k_surv_data, dim3(nblk(cap_rows, 128)), dim3(128), 0, a,
@@ -1137,15 +1138,15 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
     int blocks = ctx->sm_count * 8;
     const int64_t p_lo = static_cast<int64_t>(s_lo) * q->n, p_hi = static_cast<int64_t>(s_hi) * q->n;
     const int64_t need = (p_hi - p_lo + threads - 1) / threads;
-    if (!rows_path && need < blocks) blocks = static_cast<int>(std::max<int64_t>(1, need));
+    if (!rows_kernel && need < blocks) blocks = static_cast<int>(std::max<int64_t>(1, need));
     DevBuf<BestRec> bb(blocks, st), best(1, st);
-    if (rows_path || p_hi > p_lo) {
+    if (sync_free || p_hi > p_lo) {
       auto run = [&](auto kern) {
         launch(ctx, "seg2", kern, dim3(blocks), dim3(threads), 0, a,
                static_cast<const SurvDev*>(s->surv.p), p_lo, p_hi, s->sol_bits.p, ctr.p,
                sc_list.p, sc_count.p, bb.p);
       };
-      if (rows_path) {
+      if (rows_kernel) {
         s->sol_bits.zero();
         const int64_t units = static_cast<int64_t>(cap_rows) * ((q->n + 1023) / 1024);
         const int rblocks = static_cast<int>(
@@ -1193,7 +1194,7 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
     unsigned long long hc[C_COUNT];
     unsigned nsc = 0;
     BestRec hb{0.0, -1};
-    if (rows_path) {
+    if (sync_free) {
       // the solve's one read-back: counters, shortcut count, best, S1 and
       // the survivor list
       copy_to_host_many(ctx, {{hc, ctr.p, sizeof(hc)},
