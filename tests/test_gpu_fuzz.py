@@ -10,6 +10,7 @@ on a few targets. The small scenes (32-96^3, 5-12 degrees) take well under a
 second of reference CPU each; a few medium ones (128^3, 3-4 degrees, more
 boxes) reach the fallback cascade more often.
 RP_FUZZ_SEEDS / RP_FUZZ_MEDIUM set the counts (48 / 3; 160 / 6 pass)."""
+import ctypes as C
 import math
 import os
 
@@ -181,3 +182,47 @@ def test_random_scene_batch(ctx, seed):
             n = want.n_segments
             assert np.array([r.refined.segments[k][:] for k in range(n)]).tobytes() == \
                 np.array([want.segments[k][:] for k in range(n)]).tobytes()
+
+
+def _grid_case(seed):
+    rng = np.random.default_rng(41000 + seed)
+    bmin = tuple(float(x) for x in rng.uniform(-1.6, -0.4, 3))
+    bmax = tuple(float(b + x) for b, x in zip(bmin, rng.uniform(0.5, 2.6, 3)))
+    vs = float(rng.uniform(0.012, 0.05))
+    obs, keep = [], []
+    for _ in range(int(rng.integers(0, 10))):
+        c = np.array([rng.uniform(lo - 0.2, hi + 0.2) for lo, hi in zip(bmin, bmax)])
+        h = rng.uniform(0.0, 0.3, 3)
+        obs.append(abi.box(tuple(c - h), tuple(c + h)))
+    if rng.integers(0, 2):
+        n = int(rng.choice([5, 40, 300, 700]))
+        pts = np.array([[rng.uniform(lo - 0.1, hi + 0.1) for lo, hi in zip(bmin, bmax)]
+                        for _ in range(n)])
+        cloud = abi.Obstacle()
+        cloud.shape = abi.RP_SHAPE_CLOUD
+        buf = np.ascontiguousarray(pts, np.float64)
+        cloud.points = buf.ctypes.data_as(C.POINTER(C.c_double))
+        cloud.n_points = len(buf)
+        obs.append(cloud)
+        keep.append(buf)
+    radius = float(rng.choice([0.0, rng.uniform(0.0, 4 * vs), rng.uniform(0.0, 0.25)]))
+    return bmin, bmax, vs, obs, radius, keep
+
+
+@pytest.mark.parametrize("seed", list(range(int(os.environ.get("RP_FUZZ_GRIDS", "32")))))
+def test_random_grid_build(ctx, seed):
+    """Occupancy bit for bit on random bounds (ragged, non-cubic), voxel
+    sizes, boxes (some clipped or outside), clouds (small and past the fused
+    path's 512-primitive limit) and radii: build + mark + dilate, the fused
+    mark_dilate, and the scene grid with an explicit radius."""
+    api = _api()
+    bmin, bmax, vs, obs, radius, _keep = _grid_case(seed)
+    dims, occ = ref.grid_ops(bmin, bmax, vs, obs, radius)
+    g = api.Grid.build(ctx, bmin, bmax, vs)
+    g.mark(obs)
+    g.dilate(radius)
+    assert g.info()[0] == dims
+    assert np.array_equal(g.to_u8(), occ), (seed, "mark + dilate")
+    g2 = api.Grid.build(ctx, bmin, bmax, vs)
+    g2.mark_dilate(obs, radius)
+    assert np.array_equal(g2.to_u8(), occ), (seed, "mark_dilate")
