@@ -4,8 +4,9 @@ shell, a 15-degree approach cone now and then) solved and planned on the GPU
 and by the reference (oracle/_ref), everything compared bit for bit as in
 test_gpu_parity.py: the 13 counters, every canonical key, every shortcut,
 the chosen solution, sampled solution poses, the plan_reach_then_path
-outcome (error class or the whole plan), plan_arbitrary from its final pose
-to a second random target and one replan_dynamic tick; the batched pipeline
+outcome (error class or the whole plan) with its validator report and
+execution trace, plan_arbitrary from its final pose to a second random
+target and one replan_dynamic tick; the batched pipeline
 on a few targets. The small scenes (32-96^3, 5-12 degrees) take well under a
 second of reference CPU each; a few medium ones (128^3, 3-4 degrees, more
 boxes) reach the fallback cascade more often.
@@ -113,7 +114,24 @@ def _solve_and_plan(ctx, sc, seed):
     if rrc != 0:
         return
     rs = rplan.summary(rp.n_samples)
-    assert_plan_equal(gplan.summary(), rs, 1e-9)
+    gs = gplan.summary()
+    assert_plan_equal(gs, rs, 1e-9)
+    # the plan validator's report and the execution simulator's trace
+    rp_plan = ref.plan_create(gs["kind"], gs["waypoints"], [p for p, _ in gs["poses"]],
+                              gs["relax"], [p for p, _ in gs["unfold"]])
+    assert api.validate_plan(ctx, arm, g, gplan, rp) == R.validate_report(rp_plan), seed
+    mp = abi.make_motion_params(v_w=float(np.random.default_rng(8000 + seed).uniform(0.05, 1.0)))
+    try:
+        ours, orc = api.simulate_execution(ctx, arm, gplan, mp, g), 0
+    except api.ReachplanError as err:  # execution-collision / timeout, as the reference
+        ours, orc = None, err.code
+    src, theirs = R.simulate(rplan, mp, use_grid=True)
+    assert orc == src, (seed, orc, src)
+    if src == 0:
+        assert ours["reached"] == theirs["reached"], seed
+        assert len(ours["ticks"]) == len(theirs["ticks"]), seed
+        for k, (a, b) in enumerate(zip(ours["ticks"], theirs["ticks"])):
+            assert bytes(a) == bytes(b), (seed, k)
     # plan_arbitrary from the plan's final pose to a second random target
     rng = np.random.default_rng(7000 + seed)
     d = rng.normal(size=3)
