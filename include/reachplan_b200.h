@@ -352,6 +352,15 @@ rp_status rp_solve_reach(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q, con
 rp_status rp_solve_reach_part(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q,
                               const rp_grid* g, const double target[3], const rp_reach_params* rp,
                               int32_t part, int32_t parts, rp_solution_set** out);
+/* [revalidate_solution, src/reach_solver.cpp:458-476] the reference's
+ * merge-time self-check of every solution of the set (gap band, joint
+ * limits, self-collision, every waypoint sample clear, closure on the
+ * target) against `grid` (null: the solve's grid): *n_bad failures, the
+ * first failing ordinal and its reason (1 band, 2 limits, 3 self-collision,
+ * 4 sample in an obstacle, 5 closure). RP_REVALIDATE=1 runs it inside every
+ * solve and raises no-solution "internal: ..." as the reference does. */
+rp_status rp_solution_set_revalidate(rp_solution_set* s, const rp_grid* grid, int64_t* n_bad,
+                                     int64_t* first_bad, int32_t* reason);
 rp_status rp_solution_set_stats(const rp_solution_set* s, rp_solve_stats* stats);
 rp_status rp_solution_set_sizes(const rp_solution_set* s, int64_t* n_solutions,
                                 int64_t* n_shortcuts);

@@ -88,6 +88,8 @@ def lib():
         "rp_solve_reach_part": ([vp, P(abi.Arm), vp, vp, d3, P(abi.ReachParams), C.c_int32,
                                  C.c_int32, P(vp)], C.c_int32),
         "rp_solution_set_stats": ([vp, P(abi.SolveStats)], C.c_int32),
+        "rp_solution_set_revalidate": ([vp, vp, P(C.c_int64), P(C.c_int64), P(C.c_int32)],
+                                       C.c_int32),
         "rp_solution_set_sizes": ([vp, P(C.c_int64), P(C.c_int64)], C.c_int32),
         "rp_solution_set_keys": ([vp, vp, C.c_int64], C.c_int32),
         "rp_solution_set_pose": ([vp, C.c_int64, P(abi.Pose), vp, C.c_int32], C.c_int32),
@@ -431,6 +433,13 @@ class SolutionSet(_Owned):
         _check(lib().rp_solution_set_shortcut(self.h, k, C.byref(s), buf.ctypes.data, 1024,
                                               C.byref(n)))
         return s, buf[:n.value].copy()
+
+    def revalidate(self, grid=None):
+        """revalidate_solution over every solution: (n_bad, first_bad, reason)."""
+        n, f, r = C.c_int64(), C.c_int64(), C.c_int32()
+        _check(lib().rp_solution_set_revalidate(self.h, grid.h if grid is not None else None,
+                                                C.byref(n), C.byref(f), C.byref(r)))
+        return n.value, f.value, r.value
 
     def select(self) -> abi.Chosen:
         c = abi.Chosen()

@@ -712,11 +712,53 @@ __global__ void k_rank(const uint32_t* __restrict__ w, long long key, unsigned l
 }  // namespace
 
 /// Materialise solution poses from canonical keys (reach_solver.cpp:434-449).
+__device__ DevPose materialize_key(const SolveDev& a, const SurvDev* __restrict__ sv, long long key);
+
 __global__ void k_materialize(SolveDev a, const SurvDev* __restrict__ sv,
                               const long long* __restrict__ keys, int64_t n, DevPose* __restrict__ out) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= n) return;
-  const long long key = keys[t];
+  out[t] = materialize_key(a, sv, keys[t]);
+}
+
+/// revalidate_solution (src/reach_solver.cpp:458-476) for every solution of
+/// a set: the gap band, joint limits, self-collision, every waypoint sample
+/// clear of `g`, closure on the target. Counts the failures and keeps the
+/// first failing ordinal and its reason (1 band, 2 limits, 3 self, 4 sample,
+/// 5 closure).
+__global__ void k_revalidate(SolveDev a, const SurvDev* __restrict__ sv,
+                             const long long* __restrict__ keys, int64_t n, rpd::GridView g,
+                             double total_len, unsigned long long* __restrict__ bad,
+                             unsigned long long* __restrict__ first) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const DevPose d = materialize_key(a, sv, keys[t]);
+  const ArmDev& arm = a.arm;
+  int why = 0;
+  if (fabs(rpd::norm(d.seg[2]) - arm.L[2]) > a.eps + 1e-12) why = 1;
+  else if (!pose_limits_ok(arm, d)) why = 2;
+  else if (!pose_self_free(d, 2.0 * arm.arm_radius)) why = 3;
+  if (!why) {
+    for (int l = 0; l < d.n_wp_links && !why; ++l) {
+      const V3 diff = d.wp_to[l] - d.wp_from[l];
+      for (int k = 1; k <= d.n_wp[l]; ++k) {
+        int bit = 0;
+        const long long w = rpd::cell_word(g, rpd::walk_sample(d.wp_from[l], diff, k, d.n_wp[l]), &bit);
+        if (w >= 0 && ((__ldg(g.bits + w) >> bit) & 1ull)) {
+          why = 4;
+          break;
+        }
+      }
+    }
+  }
+  if (!why && !(rpd::norm(d.joints[d.nseg] - a.target) <= 1e-9 * fmax(1.0, total_len))) why = 5;
+  if (why) {
+    atomicAdd(bad, 1ull);
+    atomicMin(first, (static_cast<unsigned long long>(t) << 3) | static_cast<unsigned long long>(why));
+  }
+}
+
+__device__ DevPose materialize_key(const SolveDev& a, const SurvDev* __restrict__ sv, long long key) {
   const long long p = key / a.B;
   const int bi = static_cast<int>(key - p * a.B);
   const int s = static_cast<int>(p / a.Q);
@@ -751,7 +793,7 @@ __global__ void k_materialize(SolveDev a, const SurvDev* __restrict__ sv,
   d.wp_from[2] = p2;           d.wp_to[2] = b;
   d.wp_from[3] = b;            d.wp_to[3] = a.target;
   for (int k = 0; k < 4; ++k) d.n_wp[k] = a.n;
-  out[t] = d;
+  return d;
 }
 
 HostPose host_pose_from_dev(const DevPose& d) {
@@ -1250,6 +1292,18 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
         if (r.valid) s->shortcuts.push_back(host_shortcut(s, r));
     }
     S.shortcuts_found = static_cast<int64_t>(s->shortcuts.size());
+    // RP_REVALIDATE=1: the reference's merge-time self-check of every
+    // solution (src/reach_solver.cpp:537-540), raising as it does
+    static const bool reval = std::getenv("RP_REVALIDATE") != nullptr;
+    if (reval) {
+      static const char* what[] = {"", "internal: solution violates the gap band",
+                                   "internal: solution violates joint limits",
+                                   "internal: solution self-collides",
+                                   "internal: solution sample inside an obstacle",
+                                   "internal: solution does not close on the target"};
+      const RevalidateOut r = revalidate(s, nullptr);
+      if (r.n_bad) fail(RP_E_NO_SOLUTION, what[r.reason]);
+    }
   } catch (...) {
     delete s;
     throw;
@@ -1330,6 +1384,31 @@ static int64_t rank_of_key(const rp_solution_set* s, long long key) {
   unsigned long long h = 0;
   copy_to_host(s->ctx, &h, c.p, sizeof(h));
   return static_cast<int64_t>(h);
+}
+
+RevalidateOut revalidate(rp_solution_set* s, const rp_grid* grid) {
+  HostSpan span_("revalidate");
+  RevalidateOut r;
+  if (s->n_solutions == 0) return r;
+  ensure_keys(s);
+  rp_ctx* ctx = s->ctx;
+  DevBuf<unsigned long long> out(2, ctx->stream);
+  const unsigned long long init[2] = {0ull, ~0ull};
+  copy_to_device(ctx, out.p, init, sizeof(init));
+  double total = 0.0;
+  for (int k = 0; k < s->arm.n_segments; ++k) total += s->arm.lengths[k];
+  launch(ctx, "revalidate", k_revalidate, dim3(static_cast<unsigned>((s->n_solutions + 127) / 128)),
+         dim3(128), 0, s->sd, static_cast<const SurvDev*>(s->surv.p),
+         static_cast<const long long*>(s->keys.p), s->n_solutions,
+         grid ? grid->view() : s->sd.g, total, out.p, out.p + 1);
+  unsigned long long h[2];
+  copy_to_host(ctx, h, out.p, sizeof(h));
+  r.n_bad = static_cast<int64_t>(h[0]);
+  if (h[0]) {
+    r.first = static_cast<int64_t>(h[1] >> 3);
+    r.reason = static_cast<int>(h[1] & 7);
+  }
+  return r;
 }
 
 rp_chosen select(const rp_solution_set* s) {
@@ -1459,6 +1538,16 @@ rp_status rp_solve_reach_part(rp_ctx* ctx, const rp_arm* arm, const rp_quiver* q
                               int32_t part, int32_t parts, rp_solution_set** out) {
   return guarded([&] {
     *out = solve_reach(ctx, *arm, q, g, V3{target[0], target[1], target[2]}, *rp, part, parts);
+  });
+}
+
+rp_status rp_solution_set_revalidate(rp_solution_set* s, const rp_grid* grid, int64_t* n_bad,
+                                     int64_t* first_bad, int32_t* reason) {
+  return guarded([&] {
+    const RevalidateOut r = revalidate(s, grid);
+    if (n_bad) *n_bad = r.n_bad;
+    if (first_bad) *first_bad = r.first;
+    if (reason) *reason = r.reason;
   });
 }
 

@@ -233,6 +233,13 @@ HostPose solution_pose(rp_solution_set* s, int64_t ordinal);
 DevPose solution_dev_pose(rp_solution_set* s, int64_t ordinal);
 /// select_solution; returns kind and ordinal (throws no_solution on empty).
 rp_chosen select(const rp_solution_set* s);
+/// revalidate_solution (src/reach_solver.cpp:458-476) over every solution of
+/// the set, against `grid` (null: the solve's grid).
+struct RevalidateOut {
+  int64_t n_bad = 0, first = -1;
+  int reason = 0;  // of the first failure: 1 band, 2 limits, 3 self, 4 sample, 5 closure
+};
+RevalidateOut revalidate(rp_solution_set* s, const rp_grid* grid);
 /// The canonical ordinal of a solution key, counted on the device into
 /// *d_rank (stream order, no synchronisation).
 void launch_rank_of_key(const rp_solution_set* s, long long key, unsigned long long* d_rank);
