@@ -1520,6 +1520,28 @@ bool grid_seg2_cache(const rp_grid* g, const rp_quiver* q, const rp_arm& arm, in
   return true;
 }
 
+bool grid_seg2_base_cache(const rp_grid* g, const rp_quiver* q, const rp_arm& arm, int n,
+                          const uint32_t** bits, const uint8_t** ok, V3* lo, V3* hi) {
+  static const bool off = std::getenv("RP_NO_SEG2_CACHE") != nullptr;
+  const rp_grid* b = g->ov_base;
+  if (off || !b || g->exported || b->exported || g->ov_version != g->version ||
+      b->version != g->ov_base_version || q->n > 16384 || arm.n_offsets > 0 ||
+      arm.n_segments != 4)
+    return false;
+  const double key[5] = {arm.root[0], arm.root[1], arm.root[2], arm.lengths[0], arm.lengths[1]};
+  std::lock_guard<std::mutex> lock(*b->s2_mutex);
+  if (b->s2_version != b->version) return false;
+  for (const auto& e : b->s2)
+    if (e.q == q && e.n == n && std::memcmp(e.key, key, sizeof(key)) == 0) {
+      *bits = e.bits;
+      *ok = e.ok;
+      *lo = V3{g->ov_lo[0], g->ov_lo[1], g->ov_lo[2]};
+      *hi = V3{g->ov_hi[0], g->ov_hi[1], g->ov_hi[2]};
+      return true;
+    }
+  return false;
+}
+
 /// mark_obstacles + dilate(radius) for box / cloud obstacles (see file head).
 void grid_mark_dilate_boxes(rp_grid* g, const rp_obstacle* obs, int n, double radius,
                             bool or_into_existing) {
@@ -1863,6 +1885,31 @@ rp_status rp_grid_overlay(const rp_grid* base, const rp_obstacle* obs, rp_grid**
     ++g->version;
     *aug = g;
     check_boxes(obs, 1);
+    // what the overlay adds, for seeding this grid's walk cache from base's
+    g->ov_base = nullptr;
+    {
+      std::vector<Prim> hp;
+      const DilTable t = make_table(base->dilation_radius, base->voxel_size);
+      if (host_prims(g, obs, 1, &hp)) {
+        double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+        bool any = false;
+        for (const Prim& p : hp) {
+          if (p.a[0] > p.b[0] || p.a[1] > p.b[1] || p.a[2] > p.b[2]) continue;
+          any = true;
+          for (int a = 0; a < 3; ++a) {
+            lo[a] = std::min(lo[a], base->origin[a] + base->voxel_size * (p.a[a] - t.reach - 1));
+            hi[a] = std::max(hi[a], base->origin[a] + base->voxel_size * (p.b[a] + t.reach + 2));
+          }
+        }
+        g->ov_base = base;
+        g->ov_base_version = base->version;
+        g->ov_version = g->version;
+        for (int a = 0; a < 3; ++a) {
+          g->ov_lo[a] = any ? lo[a] : 1.0;
+          g->ov_hi[a] = any ? hi[a] : -1.0;  // empty: nothing added
+        }
+      }
+    }
     {
       // the common tick: a box (or a few cloud points) within reach 31 ->
       // one fused copy + raster launch, everything in the parameters

@@ -207,6 +207,13 @@ struct rp_grid {
     uint8_t* ok;     // [Q][ceil(Q/1024)]: row chunk computed
   };
   mutable std::vector<Seg2Cache> s2;
+  // Set by rp_grid_overlay: at version ov_version this grid is `ov_base` (at
+  // ov_base_version) plus occupancy only inside the world box [ov_lo, ov_hi]
+  // (the dynamic obstacle's dilated cells with a one-cell margin), so solves
+  // on it can read the base's walk cache (grid_seg2_base_cache).
+  const rp_grid* ov_base = nullptr;
+  uint64_t ov_base_version = 0, ov_version = ~0ull;
+  double ov_lo[3] = {0, 0, 0}, ov_hi[3] = {-1, -1, -1};
   // Segment-1 walk verdicts from the root (k_walk1_bits) for an arm (root,
   // L1, n) and quiver, shared by the planners on this grid version; `ready`
   // is recorded after the kernel on the computing stream (others wait on it).
@@ -412,6 +419,14 @@ ClearanceField grid_clearance_field(const rp_grid* g, rp_ctx* caller = nullptr);
 /// same first two segments reuses them. False when not cacheable.
 bool grid_seg2_cache(const rp_grid* g, const rp_quiver* q, const rp_arm& arm, int n,
                      uint32_t** bits, uint8_t** ok);
+/// An overlay grid (rp_grid_overlay) whose base grid has the walk cache for
+/// this arm and quiver: the base's verdicts, read-only, and the box holding
+/// every cell the overlay added. A base verdict "blocked" holds on the
+/// overlay too (cells are only added); a "clear" one holds unless the
+/// segment's bounding box meets the box, in which case the solve walks it
+/// again on the overlay grid (k_seg2_rows).
+bool grid_seg2_base_cache(const rp_grid* g, const rp_quiver* q, const rp_arm& arm, int n,
+                          const uint32_t** bits, const uint8_t** ok, V3* lo, V3* hi);
 
 /// side * sqrt(d2) of the coarse cell holding p projected onto the grid box
 /// (projection onto a convex set never increases distances to points in it),

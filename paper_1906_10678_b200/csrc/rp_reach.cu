@@ -375,7 +375,7 @@ __global__ void k_row_skip(SolveDev a, const SurvDev* __restrict__ sv, const int
   kskip[s] = static_cast<uint8_t>(k);
 }
 
-template <bool EIGHT>
+template <bool EIGHT, bool OV>
 __global__ void __launch_bounds__(256, 5) k_seg2_rows(SolveDev a, const SurvDev* __restrict__ sv,
                                                    const int* __restrict__ S1p, int part, int parts,
                                                    uint32_t* __restrict__ sol_bits,
@@ -383,7 +383,10 @@ __global__ void __launch_bounds__(256, 5) k_seg2_rows(SolveDev a, const SurvDev*
                                                    unsigned* sc_count, BestRec* __restrict__ block_best,
                                                    int* unit_ctr, const uint8_t* __restrict__ kskip,
                                                    const uint8_t* __restrict__ kend_b,
-                                                   uint32_t* __restrict__ c2bits, uint8_t* c2ok) {
+                                                   uint32_t* __restrict__ c2bits, uint8_t* c2ok,
+                                                   const uint32_t* __restrict__ c2bits_r,
+                                                   const uint8_t* __restrict__ c2ok_r, V3 ov_lo,
+                                                   V3 ov_hi) {
   unsigned c_lim = 0, c_clear = 0, c_gp = 0, c_jp = 0, c_v3 = 0, c_sol = 0;
   double best_len = 1e308;
   long long best_key = LLONG_MAX;
@@ -424,11 +427,27 @@ __global__ void __launch_bounds__(256, 5) k_seg2_rows(SolveDev a, const SurvDev*
     // the same grid (grid_seg2_cache), or computed here and recorded
     const size_t c2row = static_cast<size_t>(h.i) * ((a.Q + 31) >> 5);
     uint8_t* const c2flag = c2ok ? c2ok + static_cast<size_t>(h.i) * nchunk + chunk : nullptr;
-    const bool cached = c2flag && __ldcg(c2flag) != 0;
+    // an overlay grid reads its base grid's verdicts (c2*_r, never written
+    // here): blocked stays blocked, clear is walked again when the segment's
+    // box meets the box of the overlay's added cells
+    const bool from_base = OV;  // c2ok_r / c2bits_r set
+    const bool cached = from_base ? __ldg(c2ok_r + static_cast<size_t>(h.i) * nchunk + chunk) != 0
+                                  : (c2flag && __ldcg(c2flag) != 0);
     // a cached chunk's 32 words, one per lane (shuffled out per 32 j)
     const uint32_t c2mine =
-        cached && jbeg + 32 * lane < jend ? __ldcg(c2bits + c2row + (jbeg >> 5) + lane) : 0u;
+        cached && jbeg + 32 * lane < jend
+            ? (from_base ? __ldg(c2bits_r + c2row + (jbeg >> 5) + lane)
+                         : __ldcg(c2bits + c2row + (jbeg >> 5) + lane))
+            : 0u;
     const V3 p1 = h.p1;
+    bool row_meets = false;  // some segment of the row may reach the overlay box
+    if (OV) {
+      const double dx = fmax(fmax(ov_lo.x - p1.x, p1.x - ov_hi.x), 0.0);
+      const double dy = fmax(fmax(ov_lo.y - p1.y, p1.y - ov_hi.y), 0.0);
+      const double dz = fmax(fmax(ov_lo.z - p1.z, p1.z - ov_hi.z), 0.0);
+      row_meets = !(ov_lo.x > ov_hi.x) &&
+                  sqrt(dx * dx + dy * dy + dz * dz) <= L2 * (1.0 + 1e-9) + 1e-9;
+    }
     const V3 s1 = L1 * qvec(a, h.i);
     const int ks = kskip[s];  // leading samples of every segment-2 walk of this row that are free
     const bool row_near = rpd::sqnorm(a.target - p1) <= (L2 + rnear) * (L2 + rnear);
@@ -476,11 +495,16 @@ __global__ void __launch_bounds__(256, 5) k_seg2_rows(SolveDev a, const SurvDev*
         ++c_lim;
         const V3 dir2 = qvec(a, j);
         const V3 p2 = p1 + L2 * dir2;
-        const int fb =
+        int fb =
             cached ? static_cast<int>(((c2w >> lane) & 1u) ^ 1u)
             : ks >= a.n     ? 0
             : kSeg2ParWalk ? rpd::walk_first_blocked_fast_seg_from(a.g, p1, p2, a.n, ks)
                            : rpd::walk_first_blocked(a.g, p1, p2, a.n);
+        if (OV && cached && row_meets && fb == 0 &&
+            fmin(p1.x, p2.x) <= ov_hi.x + 1e-9 && fmax(p1.x, p2.x) >= ov_lo.x - 1e-9 &&
+            fmin(p1.y, p2.y) <= ov_hi.y + 1e-9 && fmax(p1.y, p2.y) >= ov_lo.y - 1e-9 &&
+            fmin(p1.z, p2.z) <= ov_hi.z + 1e-9 && fmax(p1.z, p2.z) >= ov_lo.z - 1e-9)
+          fb = rpd::walk_first_blocked(a.g, p1, p2, a.n);  // on the overlay grid
         if (c2flag && !cached) {
           const unsigned cm = __activemask();
           const unsigned clear = __ballot_sync(cm, fb == 0);
@@ -1213,15 +1237,24 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
         }
         uint32_t* c2bits = nullptr;
         uint8_t* c2ok = nullptr;
-        if (!grid_seg2_cache(g, q, arm, rp.n_samples, &c2bits, &c2ok)) c2bits = nullptr, c2ok = nullptr;
+        const uint32_t* c2bits_r = nullptr;
+        const uint8_t* c2ok_r = nullptr;
+        V3 ov_lo{1, 1, 1}, ov_hi{-1, -1, -1};
+        if (!grid_seg2_base_cache(g, q, arm, rp.n_samples, &c2bits_r, &c2ok_r, &ov_lo, &ov_hi) &&
+            !grid_seg2_cache(g, q, arm, rp.n_samples, &c2bits, &c2ok))
+          c2bits = nullptr, c2ok = nullptr;
         auto runr = [&](auto kern) {
           launch(ctx, "seg2", kern, dim3(rblocks), dim3(threads), 0, a,
                  static_cast<const SurvDev*>(s->surv.p), static_cast<const int*>(surv_cnt.p), part,
                  parts, s->sol_bits.p, ctr.p, sc_list.p,
                  sc_count.p, bb.p, unit_ctr.p, static_cast<const uint8_t*>(kskip.p),
-                 static_cast<const uint8_t*>(kend_b.p), c2bits, c2ok);
+                 static_cast<const uint8_t*>(kend_b.p), c2bits, c2ok, c2bits_r, c2ok_r, ov_lo,
+                 ov_hi);
         };
-        eight ? runr(k_seg2_rows<true>) : runr(k_seg2_rows<false>);
+        if (c2ok_r)
+          eight ? runr(k_seg2_rows<true, true>) : runr(k_seg2_rows<false, true>);
+        else
+          eight ? runr(k_seg2_rows<true, false>) : runr(k_seg2_rows<false, false>);
         blocks = rblocks;
       } else if (eight) {
         if (general) B1 ? run(k_seg2<true, true, true>) : run(k_seg2<true, true, false>);
