@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
 
 import numpy as np
 
@@ -178,7 +179,11 @@ class _Owned:
             self.h = None
 
     def __del__(self):
-        self.free()
+        # at interpreter shutdown the collector finalises objects in any
+        # order (a context may go before its children): the process is
+        # ending, so nothing is handed back to the library then
+        if not sys.is_finalizing():
+            self.free()
 
 
 class Context:
@@ -199,7 +204,8 @@ class Context:
             self.h = None
 
     def __del__(self):
-        self.close()
+        if not sys.is_finalizing():
+            self.close()
 
     def synchronize(self):
         _check(lib().rp_ctx_synchronize(self.h))
@@ -455,7 +461,7 @@ class Plan:
         self.n_samples = n_samples
 
     def __del__(self):
-        if getattr(self, "h", None) and _lib is not None:
+        if getattr(self, "h", None) and _lib is not None and not sys.is_finalizing():
             _lib.rp_plan_destroy(self.h)
             self.h = None
 

@@ -20,9 +20,11 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <unordered_map>
 
 namespace rp {
 namespace {
@@ -1520,14 +1522,27 @@ bool grid_seg2_cache(const rp_grid* g, const rp_quiver* q, const rp_arm& arm, in
   return true;
 }
 
+std::mutex& grid_registry_mutex() {
+  static std::mutex m;
+  return m;
+}
+std::unordered_map<uint64_t, const rp_grid*>& grid_registry() {
+  static std::unordered_map<uint64_t, const rp_grid*> r;
+  return r;
+}
+
 bool grid_seg2_base_cache(const rp_grid* g, const rp_quiver* q, const rp_arm& arm, int n,
                           const uint32_t** bits, const uint8_t** ok, V3* lo, V3* hi) {
   static const bool off = std::getenv("RP_NO_SEG2_CACHE") != nullptr;
-  const rp_grid* b = g->ov_base;
-  if (off || !b || g->exported || b->exported || g->ov_version != g->version ||
-      b->version != g->ov_base_version || q->n > 16384 || arm.n_offsets > 0 ||
-      arm.n_segments != 4)
+  if (off || !g->ov_base_id || g->exported || g->ov_version != g->version || q->n > 16384 ||
+      arm.n_offsets > 0 || arm.n_segments != 4)
     return false;
+  // the base grid, if it still exists (held while its cache is looked up)
+  std::lock_guard<std::mutex> reg(grid_registry_mutex());
+  const auto it = grid_registry().find(g->ov_base_id);
+  if (it == grid_registry().end()) return false;
+  const rp_grid* b = it->second;
+  if (b->exported || b->version != g->ov_base_version) return false;
   const double key[5] = {arm.root[0], arm.root[1], arm.root[2], arm.lengths[0], arm.lengths[1]};
   std::lock_guard<std::mutex> lock(*b->s2_mutex);
   if (b->s2_version != b->version) return false;
@@ -1582,6 +1597,18 @@ void grid_mark_dilate_boxes(rp_grid* g, const rp_obstacle* obs, int n, double ra
 }  // namespace rp
 
 using namespace rp;
+
+rp_grid::rp_grid() {
+  static std::atomic<uint64_t> next{1};
+  id = next.fetch_add(1);
+  std::lock_guard<std::mutex> lock(grid_registry_mutex());
+  grid_registry()[id] = this;
+}
+
+rp_grid::~rp_grid() {
+  std::lock_guard<std::mutex> lock(grid_registry_mutex());
+  grid_registry().erase(id);
+}
 
 extern "C" {
 
@@ -1886,7 +1913,7 @@ rp_status rp_grid_overlay(const rp_grid* base, const rp_obstacle* obs, rp_grid**
     *aug = g;
     check_boxes(obs, 1);
     // what the overlay adds, for seeding this grid's walk cache from base's
-    g->ov_base = nullptr;
+    g->ov_base_id = 0;
     {
       std::vector<Prim> hp;
       const DilTable t = make_table(base->dilation_radius, base->voxel_size);
@@ -1901,7 +1928,7 @@ rp_status rp_grid_overlay(const rp_grid* base, const rp_obstacle* obs, rp_grid**
             hi[a] = std::max(hi[a], base->origin[a] + base->voxel_size * (p.b[a] + t.reach + 2));
           }
         }
-        g->ov_base = base;
+        g->ov_base_id = base->id;
         g->ov_base_version = base->version;
         g->ov_version = g->version;
         for (int a = 0; a < 3; ++a) {

@@ -178,6 +178,13 @@ struct rp_quiver {
 };
 
 struct rp_grid {
+  // every live grid is registered by a serial number, so a grid can refer to
+  // another (ov_base_id) without a dangling pointer when that one is gone
+  rp_grid();
+  ~rp_grid();
+  rp_grid(const rp_grid&) = delete;
+  rp_grid& operator=(const rp_grid&) = delete;
+  uint64_t id = 0;
   rp_ctx* ctx = nullptr;
   int dims[3] = {0, 0, 0};
   int wx = 0;  // 64-bit words per x row
@@ -211,7 +218,7 @@ struct rp_grid {
   // ov_base_version) plus occupancy only inside the world box [ov_lo, ov_hi]
   // (the dynamic obstacle's dilated cells with a one-cell margin), so solves
   // on it can read the base's walk cache (grid_seg2_base_cache).
-  const rp_grid* ov_base = nullptr;
+  uint64_t ov_base_id = 0;  // 0: not an overlay
   uint64_t ov_base_version = 0, ov_version = ~0ull;
   double ov_lo[3] = {0, 0, 0}, ov_hi[3] = {-1, -1, -1};
   // Segment-1 walk verdicts from the root (k_walk1_bits) for an arm (root,

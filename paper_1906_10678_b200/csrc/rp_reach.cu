@@ -503,8 +503,23 @@ __global__ void __launch_bounds__(256, 5) k_seg2_rows(SolveDev a, const SurvDev*
         if (OV && cached && row_meets && fb == 0 &&
             fmin(p1.x, p2.x) <= ov_hi.x + 1e-9 && fmax(p1.x, p2.x) >= ov_lo.x - 1e-9 &&
             fmin(p1.y, p2.y) <= ov_hi.y + 1e-9 && fmax(p1.y, p2.y) >= ov_lo.y - 1e-9 &&
-            fmin(p1.z, p2.z) <= ov_hi.z + 1e-9 && fmax(p1.z, p2.z) >= ov_lo.z - 1e-9)
-          fb = rpd::walk_first_blocked(a.g, p1, p2, a.n);  // on the overlay grid
+            fmin(p1.z, p2.z) <= ov_hi.z + 1e-9 && fmax(p1.z, p2.z) >= ov_lo.z - 1e-9) {
+          // clear on the static grid: only samples inside the box of added
+          // cells (it holds every point that floors into one) can block now
+          const V3 diff = p2 - p1;
+          for (int k = 1; k <= a.n; ++k) {
+            const V3 sk = rpd::walk_sample(p1, diff, k, a.n);
+            if (sk.x < ov_lo.x - 1e-9 || sk.x > ov_hi.x + 1e-9 || sk.y < ov_lo.y - 1e-9 ||
+                sk.y > ov_hi.y + 1e-9 || sk.z < ov_lo.z - 1e-9 || sk.z > ov_hi.z + 1e-9)
+              continue;
+            int bit = 0;
+            const long long w = rpd::cell_word(a.g, sk, &bit);
+            if (w >= 0 && ((__ldg(a.g.bits + w) >> bit) & 1ull)) {
+              fb = k;
+              break;
+            }
+          }
+        }
         if (c2flag && !cached) {
           const unsigned cm = __activemask();
           const unsigned clear = __ballot_sync(cm, fb == 0);
