@@ -186,17 +186,29 @@ int main(int argc, char** argv) {
       j3 = attempt([&] { return plan_arbitrary(arm, q, grid, p1.poses.back(), second, rp, pp); }, &p3);
     const BackwardEndpoints be =
         backward_endpoints(scene.target, arm.lengths.back(), q, rp.approach_axis, 0.0, rp.mode);
+    // a reach pose to probe span_gap and the scan with: the chosen one, else
+    // (a shortcut was chosen) the first solution, else a straight chain
+    PoseChain probe_pose;
+    if (chosen.kind == ChosenPath::Kind::reach_pose) {
+      probe_pose = chosen.pose;
+    } else if (!set.solutions.empty()) {
+      probe_pose = set.solutions.front();
+    } else {
+      probe_pose.segments = {Vec3(arm.length(0), 0, 0), Vec3(arm.length(1), 0, 0)};
+      probe_pose.joints = {arm.root, arm.root + probe_pose.segments[0],
+                           arm.root + probe_pose.segments[0] + probe_pose.segments[1]};
+    }
     const std::vector<GapCandidate> gaps =
-        span_gap(chosen.pose.joints[2], be.points, arm.length(2), rp.resolved_epsilon(arm));
+        span_gap(probe_pose.joints[2], be.points, arm.length(2), rp.resolved_epsilon(arm));
     const SegmentProbe probe = segment_clear(grid, arm.root, scene.target, 8);
     // backward endpoints of a 0.25 rad approach cone, and span_gap over them
     const BackwardEndpoints cone =
         backward_endpoints(scene.target, arm.lengths.back(), q, rp.approach_axis, 0.25, rp.mode);
     const std::vector<GapCandidate> cone_gaps =
-        span_gap(chosen.pose.joints[2], cone.points, arm.length(2), rp.resolved_epsilon(arm));
+        span_gap(probe_pose.joints[2], cone.points, arm.length(2), rp.resolved_epsilon(arm));
     // prune_segment1 with the near-encounter scan (short_reach_scan) towards
     // a point 0.3 m out along the chosen segment-1 direction
-    const Vec3 scan_t = arm.root + 0.3 * chosen.pose.segments[0].normalized() + Vec3(0.004, -0.003, 0.002);
+    const Vec3 scan_t = arm.root + 0.3 * probe_pose.segments[0].normalized() + Vec3(0.004, -0.003, 0.002);
     std::vector<ShortcutPath> sink;
     SolveStats s1st;
     const std::vector<Seg1Hypothesis> surv =

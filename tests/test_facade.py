@@ -126,3 +126,25 @@ def test_facade_equals_reference_linked_caller(tmp_path, name, deg):
     for key in want:
         assert got[key] == want[key], key
     assert want["scan"]["shortcuts"], "the scan target should produce shortcuts"
+
+
+@pytest.mark.skipif(not os.path.exists(BIN_REF), reason="reference-linked check not built")
+@pytest.mark.parametrize("seed", list(range(12)))
+def test_facade_random_scenes(tmp_path, seed):
+    """The reference-style caller linked against the façade and against the
+    reference on random small scenes (tests/test_gpu_fuzz.py's, 6/8-DOF,
+    4-12 samples per segment): every printed result equal."""
+    import test_gpu_fuzz as F
+    sc = F._scene(seed)
+    if getattr(sc, "_rp_over", None):  # approach cones are not in the scene file format
+        pytest.skip("scene carries solver options")
+    scene = _scene_file(tmp_path, sc)
+    outs = []
+    for b in (BIN, BIN_REF):
+        r = subprocess.run([b, scene], capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stderr
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    got, want = outs
+    assert set(got) == set(want)
+    for key in want:
+        assert got[key] == want[key], (seed, key)
