@@ -951,47 +951,55 @@ __global__ void __launch_bounds__(256) k_dilate_general(const uint64_t* __restri
 // rows padded to whole 64-voxel words (16 groups per word): O(R) per voxel
 // instead of the O(R^2) row ORs of k_dilate_general.
 
-/// x pass: bits -> g1. Thread per 4 voxels: the nearest set bit on each
-/// side from the words around it (find-first-set / count-leading-zeros),
-/// capped at R. Padding voxels (x >= nx) are 255.
+/// x pass: bits -> g1. Thread per 64-voxel word (reach <= 63, so the word
+/// and its two neighbours hold every set bit within reach): per voxel the
+/// nearest set bit on each side by a funnel shift and find-first-set /
+/// count-leading-zeros, capped at R; the word's 16 groups leave as four
+/// 16-byte stores. Padding voxels (x >= nx) are 255.
 __global__ void __launch_bounds__(256) k_sdil_x(const uint64_t* __restrict__ bits, GridView g,
                                                uint32_t* __restrict__ g1, int reach) {
-  const int nqp = g.wx * 16;  // 4-voxel groups per padded row
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t total = static_cast<int64_t>(g.ny) * g.nz * nqp;
+  const int64_t total = static_cast<int64_t>(g.ny) * g.nz * g.wx;
   if (t >= total) return;
-  const int qx = static_cast<int>(t % nqp);
-  const int64_t row = t / nqp;
-  const uint64_t* r = bits + row * g.wx;
-  const int w = qx >> 4;
-  const uint64_t cur = __ldg(r + w);
-  uint32_t out = 0;
+  const int w = static_cast<int>(t % g.wx);
+  const uint64_t cur = __ldg(bits + t);
+  const uint64_t nxt = w + 1 < g.wx ? __ldg(bits + t + 1) : 0ull;
+  const uint64_t prv = w > 0 ? __ldg(bits + t - 1) : 0ull;
+  uint32_t o[16];
+  if ((cur | nxt | prv) == 0ull) {  // nothing within reach: all 255
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int x = 4 * qx + k;
-    int best = 255;
-    if (x < g.nx) {
-      const int b = x & 63;
-      // right: bits >= x in this word, else the next words within reach
-      uint64_t m = cur >> b;
-      int d = m ? __ffsll(static_cast<long long>(m)) - 1 : 1 << 20;
-      for (int ww = w + 1; d > reach && ww < g.wx && (ww << 6) - x <= reach; ++ww) {
-        const uint64_t v = __ldg(r + ww);
-        if (v) d = (ww << 6) + __ffsll(static_cast<long long>(v)) - 1 - x;
+    for (int k = 0; k < 16; ++k) o[k] = 0xFFFFFFFFu;
+  } else {
+#pragma unroll
+    for (int gq = 0; gq < 16; ++gq) {
+      uint32_t out = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int b = 4 * gq + k;
+        const int x = (w << 6) + b;
+        int best = 255;
+        if (x < g.nx) {
+          // right: bits >= b of cur, then nxt
+          const uint64_t r = b ? ((cur >> b) | (nxt << (64 - b))) : cur;
+          const uint64_t rh = b ? (nxt >> b) : nxt;
+          const int d = r ? __ffsll(static_cast<long long>(r)) - 1
+                          : (rh ? 64 + __ffsll(static_cast<long long>(rh)) - 1 : 1 << 20);
+          // left: bits <= b of cur, then prv
+          const uint64_t l = b < 63 ? ((cur << (63 - b)) | (prv >> (b + 1))) : cur;
+          const uint64_t lh = b < 63 ? (prv << (63 - b)) : prv;
+          const int e = l ? __clzll(static_cast<long long>(l))
+                          : (lh ? 64 + __clzll(static_cast<long long>(lh)) : 1 << 20);
+          const int dm = d < e ? d : e;
+          if (dm <= reach) best = dm * dm;
+        }
+        out |= static_cast<uint32_t>(best) << (8 * k);
       }
-      // left: bits <= x in this word, else the previous words
-      m = cur << (63 - b);
-      int e = m ? __clzll(static_cast<long long>(m)) : 1 << 20;
-      for (int ww = w - 1; e > reach && ww >= 0 && x - ((ww << 6) + 63) <= reach; --ww) {
-        const uint64_t v = __ldg(r + ww);
-        if (v) e = x - ((ww << 6) + 63 - __clzll(static_cast<long long>(v)));
-      }
-      const int dm = d < e ? d : e;
-      if (dm <= reach) best = dm * dm;
+      o[gq] = out;
     }
-    out |= static_cast<uint32_t>(best) << (8 * k);
   }
-  g1[t] = out;
+  uint4* dst = reinterpret_cast<uint4*>(g1 + t * 16);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) dst[k] = make_uint4(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]);
 }
 
 // The y and z passes compute in fp16x2 (native HADD2 / HMNMX2; the byte
@@ -1019,10 +1027,13 @@ template <int TY>
 __global__ void __launch_bounds__(256) k_sdil_y(const uint32_t* __restrict__ g1, GridView g,
                                                uint32_t* __restrict__ g2, int reach) {
   extern __shared__ uint2 sy[];  // [(TY + 2R) rows][64 groups]
+  __shared__ __half2 sadd[128];  // dy^2 for dy = -R..R (R <= 63)
   const int nqp = g.wx * 16;
   const int q0 = blockIdx.x * 64, y0 = blockIdx.y * TY, z = blockIdx.z;
   const int rows = TY + 2 * reach;
   const size_t plane = static_cast<size_t>(g.ny) * nqp;
+  for (int k = threadIdx.x; k <= 2 * reach; k += blockDim.x)
+    sadd[k] = __float2half2_rn(static_cast<float>((k - reach) * (k - reach)));
   for (int k = threadIdx.x; k < rows * 64; k += blockDim.x) {
     const int yy = y0 - reach + k / 64, qq = q0 + (k & 63);
     const uint32_t b = (yy >= 0 && yy < g.ny && qq < nqp)
@@ -1037,9 +1048,10 @@ __global__ void __launch_bounds__(256) k_sdil_y(const uint32_t* __restrict__ g1,
     const int y = y0 + ly;
     if (y >= g.ny || q0 + qq >= nqp) continue;
     __half2 lo = cap, hi = cap;
-    for (int dy = -reach; dy <= reach; ++dy) {
-      const __half2 add = __float2half2_rn(static_cast<float>(dy * dy));
-      const uint2 v = sy[(ly + reach + dy) * 64 + qq];
+    const uint2* col = sy + ly * 64 + qq;
+    for (int k = 0; k <= 2 * reach; ++k) {
+      const __half2 add = sadd[k];
+      const uint2 v = col[k * 64];
       lo = __hmin2(lo, __hadd2(as_h2(v.x), add));
       hi = __hmin2(hi, __hadd2(as_h2(v.y), add));
     }
@@ -1059,30 +1071,43 @@ __global__ void __launch_bounds__(256) k_sdil_z(const uint32_t* __restrict__ g2,
                                                uint64_t* __restrict__ out, int reach, int T,
                                                int z_lo, int z_hi) {
   extern __shared__ uint2 ring[];  // [2R + 1][256]
+  __shared__ __half2 ssub[128];   // -(1024 + T - dz^2) for dz = -R..R
   const int64_t gpl = static_cast<int64_t>(g.ny) * g.wx * 16;  // groups per plane
   const int64_t q = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
   const bool live = q < gpl;
   const int za = z_lo + blockIdx.y * ZC;
   const int zb = min(z_hi, za + ZC - 1);
   const int win = 2 * reach + 1;
-  for (int zz = za - reach; zz < za + reach; ++zz) {
-    const int slot = (zz - (za - reach)) % win;
-    ring[slot * 256 + threadIdx.x] =
-        bytes_to_h2((live && zz >= 0 && zz < g.nz) ? __ldg(g2 + zz * gpl + q) : 0xFFFFFFFFu);
+  for (int k = threadIdx.x; k < win; k += blockDim.x) {
+    const int dz = k - reach, lim = T - dz * dz;
+    // lim < 0: that plane cannot reach; a subtrahend of -1023 leaves every
+    // byte value (1024 + v, v >= 0) above zero
+    ssub[k] = __float2half2_rn(lim < 0 ? -1023.0f : -(1024.0f + static_cast<float>(lim)));
   }
+  for (int zz = za - reach; zz < za + reach; ++zz)
+    ring[((zz - (za - reach)) % win) * 256 + threadIdx.x] =
+        bytes_to_h2((live && zz >= 0 && zz < g.nz) ? __ldg(g2 + zz * gpl + q) : 0xFFFFFFFFu);
+  __syncthreads();  // ssub
   const int lane = threadIdx.x & 31;
   const __half2 zero = __float2half2_rn(0.0f);
+  const uint2* col = ring + threadIdx.x;
   for (int z = za; z <= zb; ++z) {
     const int zn = z + reach;  // newest plane of the window
     ring[((zn - (za - reach)) % win) * 256 + threadIdx.x] =
         bytes_to_h2((live && zn < g.nz) ? __ldg(g2 + zn * gpl + q) : 0xFFFFFFFFu);
     __half2 lo = __float2half2_rn(1.0f), hi = lo;
-    int slot = (z - reach - (za - reach)) % win;
-    for (int dz = -reach; dz <= reach; ++dz, slot = slot + 1 == win ? 0 : slot + 1) {
-      const int lim = T - dz * dz;
-      if (lim < 0) continue;
-      const __half2 sub = __float2half2_rn(-(1024.0f + static_cast<float>(lim)));
-      const uint2 v = ring[slot * 256 + threadIdx.x];
+    // the window starts at slot s0 and wraps once: slots s0..win-1 hold
+    // dz = -R.., slots 0..s0-1 the rest
+    const int s0 = (z - za) % win;
+    for (int k = 0; k < win - s0; ++k) {
+      const __half2 sub = ssub[k];
+      const uint2 v = col[(s0 + k) * 256];
+      lo = __hmin2(lo, __hadd2(as_h2(v.x), sub));
+      hi = __hmin2(hi, __hadd2(as_h2(v.y), sub));
+    }
+    for (int k = 0; k < s0; ++k) {
+      const __half2 sub = ssub[win - s0 + k];
+      const uint2 v = col[k * 256];
       lo = __hmin2(lo, __hadd2(as_h2(v.x), sub));
       hi = __hmin2(hi, __hadd2(as_h2(v.y), sub));
     }
@@ -1114,7 +1139,7 @@ bool dilate_separable(rp_grid* g, double radius, int z0, int z1) {
   const int64_t groups = static_cast<int64_t>(g->dims[2]) * g->dims[1] * g->wx * 16;
   DevBuf<uint32_t> g1(groups, st), g2(groups, st);
   const GridView v = g->view();
-  launch(ctx, "dilate", k_sdil_x, dim3(blocks_for(groups, 256)), dim3(256), 0,
+  launch(ctx, "dilate", k_sdil_x, dim3(blocks_for(groups / 16, 256)), dim3(256), 0,
          static_cast<const uint64_t*>(g->bits), v, g1.p, reach);
   constexpr int TY = 16;
   const size_t smy = static_cast<size_t>(TY + 2 * reach) * 64 * sizeof(uint2);
