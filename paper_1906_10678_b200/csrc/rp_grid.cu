@@ -1022,18 +1022,22 @@ __device__ __forceinline__ uint32_t as_u32(__half2 h) {
 
 /// y pass: g2 = min(255, min over |dy| <= R of g1(y + dy) + dy^2).
 /// Block = 64 groups x TY rows of one plane, staged (as fp16x2 pairs) with
-/// the R halo rows in shared memory.
+/// the R halo rows in shared memory; a thread computes 4 consecutive rows of
+/// one group column, so every staged row it loads serves all four.
 template <int TY>
 __global__ void __launch_bounds__(256) k_sdil_y(const uint32_t* __restrict__ g1, GridView g,
                                                uint32_t* __restrict__ g2, int reach) {
+  static_assert(TY % 16 == 0, "4 rows x 4 row groups per pass");
   extern __shared__ uint2 sy[];  // [(TY + 2R) rows][64 groups]
-  __shared__ __half2 sadd[128];  // dy^2 for dy = -R..R (R <= 63)
+  __shared__ __half2 sadd[130];  // dy^2 for dy = -R..R (R <= 63), then 3 pads
   const int nqp = g.wx * 16;
   const int q0 = blockIdx.x * 64, y0 = blockIdx.y * TY, z = blockIdx.z;
   const int rows = TY + 2 * reach;
   const size_t plane = static_cast<size_t>(g.ny) * nqp;
-  for (int k = threadIdx.x; k <= 2 * reach; k += blockDim.x)
-    sadd[k] = __float2half2_rn(static_cast<float>((k - reach) * (k - reach)));
+  // the pad 2048 lifts any sum above the cap 1024 + 255
+  const __half2 pad = __float2half2_rn(2048.0f);
+  for (int k = threadIdx.x; k <= 2 * reach + 3; k += blockDim.x)
+    sadd[k] = k <= 2 * reach ? __float2half2_rn(static_cast<float>((k - reach) * (k - reach))) : pad;
   for (int k = threadIdx.x; k < rows * 64; k += blockDim.x) {
     const int yy = y0 - reach + k / 64, qq = q0 + (k & 63);
     const uint32_t b = (yy >= 0 && yy < g.ny && qq < nqp)
@@ -1043,26 +1047,39 @@ __global__ void __launch_bounds__(256) k_sdil_y(const uint32_t* __restrict__ g1,
   }
   __syncthreads();
   const int qq = threadIdx.x & 63;
+  if (q0 + qq >= nqp) return;
   const __half2 cap = __float2half2_rn(1024.0f + 255.0f);
-  for (int ly = threadIdx.x >> 6; ly < TY; ly += blockDim.x >> 6) {
-    const int y = y0 + ly;
-    if (y >= g.ny || q0 + qq >= nqp) continue;
-    __half2 lo = cap, hi = cap;
-    const uint2* col = sy + ly * 64 + qq;
-    for (int k = 0; k <= 2 * reach; ++k) {
-      const __half2 add = sadd[k];
+  for (int ly0 = (threadIdx.x >> 6) * 4; ly0 < TY; ly0 += 16) {
+    if (y0 + ly0 >= g.ny) break;
+    __half2 lo[4], hi[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) lo[j] = hi[j] = cap;
+    // staged row ly0 + k meets output row ly0 + j with dy^2 entry k - j
+    __half2 a0 = sadd[0], a1 = pad, a2 = pad, a3 = pad;
+    const uint2* col = sy + ly0 * 64 + qq;
+    for (int k = 0; k <= 2 * reach + 3; ++k) {
       const uint2 v = col[k * 64];
-      lo = __hmin2(lo, __hadd2(as_h2(v.x), add));
-      hi = __hmin2(hi, __hadd2(as_h2(v.y), add));
+      const __half2 x = as_h2(v.x), y = as_h2(v.y);
+      lo[0] = __hmin2(lo[0], __hadd2(x, a0)); hi[0] = __hmin2(hi[0], __hadd2(y, a0));
+      lo[1] = __hmin2(lo[1], __hadd2(x, a1)); hi[1] = __hmin2(hi[1], __hadd2(y, a1));
+      lo[2] = __hmin2(lo[2], __hadd2(x, a2)); hi[2] = __hmin2(hi[2], __hadd2(y, a2));
+      lo[3] = __hmin2(lo[3], __hadd2(x, a3)); hi[3] = __hmin2(hi[3], __hadd2(y, a3));
+      a3 = a2; a2 = a1; a1 = a0;
+      a0 = sadd[min(k + 1, 2 * reach + 3)];
     }
-    g2[z * plane + static_cast<size_t>(y) * nqp + q0 + qq] =
-        __byte_perm(as_u32(lo), as_u32(hi), 0x6420);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int y = y0 + ly0 + j;
+      if (y < g.ny)
+        g2[z * plane + static_cast<size_t>(y) * nqp + q0 + qq] =
+            __byte_perm(as_u32(lo[j]), as_u32(hi[j]), 0x6420);
+    }
   }
 }
 
 /// z pass + threshold: thread per 4-voxel group of a plane, sliding along z
-/// over a chunk of ZC output planes with the 2R + 1 input planes around the
-/// current one in a shared-memory ring (fp16x2 pairs): bit = [min over
+/// over a chunk of ZC output planes, two at a time, with the 2R + 2 input
+/// planes around the pair in a shared-memory ring (fp16x2 pairs): bit = [min over
 /// |dz| <= R of g2(z + dz) - (T - dz^2) <= 0]. A half-warp holds the 16
 /// groups of one output word (rows are padded to whole words) and ORs their
 /// nibbles by shuffles.
@@ -1070,54 +1087,83 @@ template <int ZC>
 __global__ void __launch_bounds__(256) k_sdil_z(const uint32_t* __restrict__ g2, GridView g,
                                                uint64_t* __restrict__ out, int reach, int T,
                                                int z_lo, int z_hi) {
-  extern __shared__ uint2 ring[];  // [2R + 1][256]
-  __shared__ __half2 ssub[128];   // -(1024 + T - dz^2) for dz = -R..R
+  // two output planes per step: every window load serves both, the ring
+  // holds the 2R + 2 planes of the pair (z, z + 1)
+  extern __shared__ uint2 ring[];  // [2R + 2][256]
+  // ssub[1 + k] = -(1024 + T - dz^2) for dz = k - R; the pads ssub[0] and
+  // ssub[win + 1] (and planes with T < dz^2) hold -1023, which leaves every
+  // byte value 1024 + v (v >= 0) above zero
+  __shared__ __half2 ssub[130];
   const int64_t gpl = static_cast<int64_t>(g.ny) * g.wx * 16;  // groups per plane
   const int64_t q = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
   const bool live = q < gpl;
   const int za = z_lo + blockIdx.y * ZC;
   const int zb = min(z_hi, za + ZC - 1);
-  const int win = 2 * reach + 1;
-  for (int k = threadIdx.x; k < win; k += blockDim.x) {
-    const int dz = k - reach, lim = T - dz * dz;
-    // lim < 0: that plane cannot reach; a subtrahend of -1023 leaves every
-    // byte value (1024 + v, v >= 0) above zero
-    ssub[k] = __float2half2_rn(lim < 0 ? -1023.0f : -(1024.0f + static_cast<float>(lim)));
+  const int win = 2 * reach + 1, W = win + 1;
+  for (int k = threadIdx.x; k < win + 2; k += blockDim.x) {
+    const int dz = k - 1 - reach, lim = T - dz * dz;
+    const bool pad = k == 0 || k == win + 1 || lim < 0;
+    ssub[k] = __float2half2_rn(pad ? -1023.0f : -(1024.0f + static_cast<float>(lim)));
   }
   for (int zz = za - reach; zz < za + reach; ++zz)
-    ring[((zz - (za - reach)) % win) * 256 + threadIdx.x] =
+    ring[(zz - (za - reach)) * 256 + threadIdx.x] =
         bytes_to_h2((live && zz >= 0 && zz < g.nz) ? __ldg(g2 + zz * gpl + q) : 0xFFFFFFFFu);
   __syncthreads();  // ssub
   const int lane = threadIdx.x & 31;
   const __half2 zero = __float2half2_rn(0.0f);
+  const __half2 one = __float2half2_rn(1.0f);
   const uint2* col = ring + threadIdx.x;
-  for (int z = za; z <= zb; ++z) {
-    const int zn = z + reach;  // newest plane of the window
-    ring[((zn - (za - reach)) % win) * 256 + threadIdx.x] =
-        bytes_to_h2((live && zn < g.nz) ? __ldg(g2 + zn * gpl + q) : 0xFFFFFFFFu);
-    __half2 lo = __float2half2_rn(1.0f), hi = lo;
-    // the window starts at slot s0 and wraps once: slots s0..win-1 hold
-    // dz = -R.., slots 0..s0-1 the rest
-    const int s0 = (z - za) % win;
-    for (int k = 0; k < win - s0; ++k) {
-      const __half2 sub = ssub[k];
+  for (int z = za; z <= zb; z += 2) {
+    for (int d = 0; d < 2; ++d) {  // the pair's two newest planes
+      const int zn = z + reach + d;
+      ring[((zn - (za - reach)) % W) * 256 + threadIdx.x] =
+          bytes_to_h2((live && zn < g.nz) ? __ldg(g2 + zn * gpl + q) : 0xFFFFFFFFu);
+    }
+    __half2 alo = one, ahi = one, blo = one, bhi = one;
+    // plane z - R + k (k = 0..win) is at slot (s0 + k) % W; it meets plane z
+    // with ssub[k + 1] and plane z + 1 with ssub[k]
+    const int s0 = (z - za) % W;
+    __half2 sb = ssub[0];
+    for (int k = 0; k < W - s0; ++k) {
+      const __half2 sa = ssub[k + 1];
       const uint2 v = col[(s0 + k) * 256];
-      lo = __hmin2(lo, __hadd2(as_h2(v.x), sub));
-      hi = __hmin2(hi, __hadd2(as_h2(v.y), sub));
+      alo = __hmin2(alo, __hadd2(as_h2(v.x), sa));
+      ahi = __hmin2(ahi, __hadd2(as_h2(v.y), sa));
+      blo = __hmin2(blo, __hadd2(as_h2(v.x), sb));
+      bhi = __hmin2(bhi, __hadd2(as_h2(v.y), sb));
+      sb = sa;
     }
-    for (int k = 0; k < s0; ++k) {
-      const __half2 sub = ssub[win - s0 + k];
-      const uint2 v = col[k * 256];
-      lo = __hmin2(lo, __hadd2(as_h2(v.x), sub));
-      hi = __hmin2(hi, __hadd2(as_h2(v.y), sub));
+    for (int k = W - s0; k < W; ++k) {
+      const __half2 sa = ssub[k + 1];
+      const uint2 v = col[(k - (W - s0)) * 256];
+      alo = __hmin2(alo, __hadd2(as_h2(v.x), sa));
+      ahi = __hmin2(ahi, __hadd2(as_h2(v.y), sa));
+      blo = __hmin2(blo, __hadd2(as_h2(v.x), sb));
+      bhi = __hmin2(bhi, __hadd2(as_h2(v.y), sb));
+      sb = sa;
     }
-    const uint32_t ml = as_u32(__hle2(lo, zero)), mh = as_u32(__hle2(hi, zero));
-    const uint32_t nib = ((ml & 0xFFFFu) ? 1u : 0u) | ((ml >> 16) ? 2u : 0u) |
-                         ((mh & 0xFFFFu) ? 4u : 0u) | ((mh >> 16) ? 8u : 0u);
-    uint64_t v = static_cast<uint64_t>(nib) << (4 * (q & 15));
+    uint64_t va, vb;
+    {
+      const uint32_t ml = as_u32(__hle2(alo, zero)), mh = as_u32(__hle2(ahi, zero));
+      const uint32_t nib = ((ml & 0xFFFFu) ? 1u : 0u) | ((ml >> 16) ? 2u : 0u) |
+                           ((mh & 0xFFFFu) ? 4u : 0u) | ((mh >> 16) ? 8u : 0u);
+      va = static_cast<uint64_t>(nib) << (4 * (q & 15));
+    }
+    {
+      const uint32_t ml = as_u32(__hle2(blo, zero)), mh = as_u32(__hle2(bhi, zero));
+      const uint32_t nib = ((ml & 0xFFFFu) ? 1u : 0u) | ((ml >> 16) ? 2u : 0u) |
+                           ((mh & 0xFFFFu) ? 4u : 0u) | ((mh >> 16) ? 8u : 0u);
+      vb = static_cast<uint64_t>(nib) << (4 * (q & 15));
+    }
 #pragma unroll
-    for (int o = 1; o < 16; o <<= 1) v |= __shfl_xor_sync(0xFFFFFFFFu, v, o);
-    if (live && (lane & 15) == 0) out[(z * gpl + q) >> 4] = v;
+    for (int o = 1; o < 16; o <<= 1) {
+      va |= __shfl_xor_sync(0xFFFFFFFFu, va, o);
+      vb |= __shfl_xor_sync(0xFFFFFFFFu, vb, o);
+    }
+    if (live && (lane & 15) == 0) {
+      out[(z * gpl + q) >> 4] = va;
+      if (z + 1 <= zb) out[((z + 1) * gpl + q) >> 4] = vb;
+    }
   }
 }
 
@@ -1141,7 +1187,7 @@ bool dilate_separable(rp_grid* g, double radius, int z0, int z1) {
   const GridView v = g->view();
   launch(ctx, "dilate", k_sdil_x, dim3(blocks_for(groups / 16, 256)), dim3(256), 0,
          static_cast<const uint64_t*>(g->bits), v, g1.p, reach);
-  constexpr int TY = 16;
+  constexpr int TY = 32;
   const size_t smy = static_cast<size_t>(TY + 2 * reach) * 64 * sizeof(uint2);
   allow_smem(k_sdil_y<TY>, smy);
   launch(ctx, "dilate", k_sdil_y<TY>,
@@ -1155,7 +1201,7 @@ bool dilate_separable(rp_grid* g, double radius, int z0, int z1) {
     RP_CUDA(cudaMemcpyAsync(out, g->bits, g->n_words * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
   // ZC output planes per thread (the 2R halo planes are re-read per chunk)
   constexpr int ZC = 32;
-  const size_t smz = static_cast<size_t>(2 * reach + 1) * 256 * sizeof(uint2);
+  const size_t smz = static_cast<size_t>(2 * reach + 2) * 256 * sizeof(uint2);
   const int64_t gpl = static_cast<int64_t>(g->dims[1]) * g->wx * 16;
   const dim3 grid(static_cast<unsigned>((gpl + 255) / 256), static_cast<unsigned>((z1 - z0 + ZC) / ZC));
   allow_smem(k_sdil_z<ZC>, smz);
