@@ -16,7 +16,6 @@
 #include "rp_internal.hpp"
 
 #include <cuda.h>
-#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -1002,26 +1001,20 @@ __global__ void __launch_bounds__(256) k_sdil_x(const uint64_t* __restrict__ bit
   for (int k = 0; k < 4; ++k) dst[k] = make_uint4(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]);
 }
 
-// The y and z passes compute in fp16x2 (native HADD2 / HMNMX2; the byte
-// SIMD intrinsics are emulated): a byte k becomes the fp16 1024 + k (bits
-// 0x6400 | k, one PRMT for two voxels), every sum stays an integer below
-// 2048 (exact in fp16), and the low byte of the bits is k again.
-__device__ __forceinline__ uint2 bytes_to_h2(uint32_t b) {
-  return make_uint2(__byte_perm(b, 0x6464u, 0x4140), __byte_perm(b, 0x6464u, 0x4342));
+// The y and z passes compute in u16x2 lanes with the sm_90+ DPX
+// instruction VIADDMNMX.U16x2 (__viaddmin_u16x2: min(a + b, c) per 16-bit
+// half, one instruction per two voxels per tap; the byte SIMD intrinsics
+// are emulated on sm_100): a byte k becomes the half k (one PRMT for two
+// voxels) and every sum stays below 2^16.
+__device__ __forceinline__ uint2 bytes_to_u16(uint32_t b) {
+  return make_uint2(__byte_perm(b, 0u, 0x4140), __byte_perm(b, 0u, 0x4342));
 }
-__device__ __forceinline__ __half2 as_h2(uint32_t u) {
-  __half2 h;
-  memcpy(&h, &u, 4);
-  return h;
-}
-__device__ __forceinline__ uint32_t as_u32(__half2 h) {
-  uint32_t u;
-  memcpy(&u, &h, 4);
-  return u;
+__device__ __forceinline__ uint32_t splat16(int v) {
+  return static_cast<uint32_t>(v) * 0x00010001u;
 }
 
 /// y pass: g2 = min(255, min over |dy| <= R of g1(y + dy) + dy^2).
-/// Block = 64 groups x TY rows of one plane, staged (as fp16x2 pairs) with
+/// Block = 64 groups x TY rows of one plane, staged (as u16x2 pairs) with
 /// the R halo rows in shared memory; a thread computes 4 consecutive rows of
 /// one group column, so every staged row it loads serves all four.
 template <int TY>
@@ -1029,41 +1022,40 @@ __global__ void __launch_bounds__(256) k_sdil_y(const uint32_t* __restrict__ g1,
                                                uint32_t* __restrict__ g2, int reach) {
   static_assert(TY % 16 == 0, "4 rows x 4 row groups per pass");
   extern __shared__ uint2 sy[];  // [(TY + 2R) rows][64 groups]
-  __shared__ __half2 sadd[130];  // dy^2 for dy = -R..R (R <= 63), then 3 pads
+  __shared__ uint32_t sadd[130];  // dy^2 for dy = -R..R (R <= 63), then 3 pads
   const int nqp = g.wx * 16;
   const int q0 = blockIdx.x * 64, y0 = blockIdx.y * TY, z = blockIdx.z;
   const int rows = TY + 2 * reach;
   const size_t plane = static_cast<size_t>(g.ny) * nqp;
-  // the pad 2048 lifts any sum above the cap 1024 + 255
-  const __half2 pad = __float2half2_rn(2048.0f);
+  // the pad lifts any sum above the cap 255
+  const uint32_t pad = splat16(4096);
   for (int k = threadIdx.x; k <= 2 * reach + 3; k += blockDim.x)
-    sadd[k] = k <= 2 * reach ? __float2half2_rn(static_cast<float>((k - reach) * (k - reach))) : pad;
+    sadd[k] = k <= 2 * reach ? splat16((k - reach) * (k - reach)) : pad;
   for (int k = threadIdx.x; k < rows * 64; k += blockDim.x) {
     const int yy = y0 - reach + k / 64, qq = q0 + (k & 63);
     const uint32_t b = (yy >= 0 && yy < g.ny && qq < nqp)
                            ? __ldg(g1 + z * plane + static_cast<size_t>(yy) * nqp + qq)
                            : 0xFFFFFFFFu;
-    sy[k] = bytes_to_h2(b);
+    sy[k] = bytes_to_u16(b);
   }
   __syncthreads();
   const int qq = threadIdx.x & 63;
   if (q0 + qq >= nqp) return;
-  const __half2 cap = __float2half2_rn(1024.0f + 255.0f);
+  const uint32_t cap = splat16(255);
   for (int ly0 = (threadIdx.x >> 6) * 4; ly0 < TY; ly0 += 16) {
     if (y0 + ly0 >= g.ny) break;
-    __half2 lo[4], hi[4];
+    uint32_t lo[4], hi[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) lo[j] = hi[j] = cap;
     // staged row ly0 + k meets output row ly0 + j with dy^2 entry k - j
-    __half2 a0 = sadd[0], a1 = pad, a2 = pad, a3 = pad;
+    uint32_t a0 = sadd[0], a1 = pad, a2 = pad, a3 = pad;
     const uint2* col = sy + ly0 * 64 + qq;
     for (int k = 0; k <= 2 * reach + 3; ++k) {
       const uint2 v = col[k * 64];
-      const __half2 x = as_h2(v.x), y = as_h2(v.y);
-      lo[0] = __hmin2(lo[0], __hadd2(x, a0)); hi[0] = __hmin2(hi[0], __hadd2(y, a0));
-      lo[1] = __hmin2(lo[1], __hadd2(x, a1)); hi[1] = __hmin2(hi[1], __hadd2(y, a1));
-      lo[2] = __hmin2(lo[2], __hadd2(x, a2)); hi[2] = __hmin2(hi[2], __hadd2(y, a2));
-      lo[3] = __hmin2(lo[3], __hadd2(x, a3)); hi[3] = __hmin2(hi[3], __hadd2(y, a3));
+      lo[0] = __viaddmin_u16x2(v.x, a0, lo[0]); hi[0] = __viaddmin_u16x2(v.y, a0, hi[0]);
+      lo[1] = __viaddmin_u16x2(v.x, a1, lo[1]); hi[1] = __viaddmin_u16x2(v.y, a1, hi[1]);
+      lo[2] = __viaddmin_u16x2(v.x, a2, lo[2]); hi[2] = __viaddmin_u16x2(v.y, a2, hi[2]);
+      lo[3] = __viaddmin_u16x2(v.x, a3, lo[3]); hi[3] = __viaddmin_u16x2(v.y, a3, hi[3]);
       a3 = a2; a2 = a1; a1 = a0;
       a0 = sadd[min(k + 1, 2 * reach + 3)];
     }
@@ -1071,29 +1063,25 @@ __global__ void __launch_bounds__(256) k_sdil_y(const uint32_t* __restrict__ g1,
     for (int j = 0; j < 4; ++j) {
       const int y = y0 + ly0 + j;
       if (y < g.ny)
-        g2[z * plane + static_cast<size_t>(y) * nqp + q0 + qq] =
-            __byte_perm(as_u32(lo[j]), as_u32(hi[j]), 0x6420);
+        g2[z * plane + static_cast<size_t>(y) * nqp + q0 + qq] = __byte_perm(lo[j], hi[j], 0x6420);
     }
   }
 }
 
 /// z pass + threshold: thread per 4-voxel group of a plane, sliding along z
 /// over a chunk of ZC output planes, two at a time, with the 2R + 2 input
-/// planes around the pair in a shared-memory ring (fp16x2 pairs): bit = [min over
-/// |dz| <= R of g2(z + dz) - (T - dz^2) <= 0]. A half-warp holds the 16
-/// groups of one output word (rows are padded to whole words) and ORs their
-/// nibbles by shuffles.
+/// planes around the pair in a shared-memory ring (u16x2 pairs): bit =
+/// [min over |dz| <= R of g2(z + dz) + dz^2 <= T] (a plane with dz^2 > T
+/// cannot pass). A half-warp holds the 16 groups of one output word (rows
+/// are padded to whole words) and ORs their nibbles by shuffles.
 template <int ZC>
 __global__ void __launch_bounds__(256) k_sdil_z(const uint32_t* __restrict__ g2, GridView g,
                                                uint64_t* __restrict__ out, int reach, int T,
                                                int z_lo, int z_hi) {
-  // two output planes per step: every window load serves both, the ring
-  // holds the 2R + 2 planes of the pair (z, z + 1)
   extern __shared__ uint2 ring[];  // [2R + 2][256]
-  // ssub[1 + k] = -(1024 + T - dz^2) for dz = k - R; the pads ssub[0] and
-  // ssub[win + 1] (and planes with T < dz^2) hold -1023, which leaves every
-  // byte value 1024 + v (v >= 0) above zero
-  __shared__ __half2 ssub[130];
+  // sq[1 + k] = dz^2 for dz = k - R; the pads sq[0] and sq[win + 1] are
+  // above any threshold
+  __shared__ uint32_t sq[130];
   const int64_t gpl = static_cast<int64_t>(g.ny) * g.wx * 16;  // groups per plane
   const int64_t q = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
   const bool live = q < gpl;
@@ -1101,60 +1089,49 @@ __global__ void __launch_bounds__(256) k_sdil_z(const uint32_t* __restrict__ g2,
   const int zb = min(z_hi, za + ZC - 1);
   const int win = 2 * reach + 1, W = win + 1;
   for (int k = threadIdx.x; k < win + 2; k += blockDim.x) {
-    const int dz = k - 1 - reach, lim = T - dz * dz;
-    const bool pad = k == 0 || k == win + 1 || lim < 0;
-    ssub[k] = __float2half2_rn(pad ? -1023.0f : -(1024.0f + static_cast<float>(lim)));
+    const int dz = k - 1 - reach;
+    sq[k] = (k == 0 || k == win + 1) ? splat16(4096) : splat16(dz * dz);
   }
   for (int zz = za - reach; zz < za + reach; ++zz)
     ring[(zz - (za - reach)) * 256 + threadIdx.x] =
-        bytes_to_h2((live && zz >= 0 && zz < g.nz) ? __ldg(g2 + zz * gpl + q) : 0xFFFFFFFFu);
-  __syncthreads();  // ssub
+        bytes_to_u16((live && zz >= 0 && zz < g.nz) ? __ldg(g2 + zz * gpl + q) : 0xFFFFFFFFu);
+  __syncthreads();  // sq
   const int lane = threadIdx.x & 31;
-  const __half2 zero = __float2half2_rn(0.0f);
-  const __half2 one = __float2half2_rn(1.0f);
-  const uint2* col = ring + threadIdx.x;
+  const uint32_t init = splat16(0xFFFF);
+  const uint32_t* colx = reinterpret_cast<const uint32_t*>(ring) + 2 * threadIdx.x;
   for (int z = za; z <= zb; z += 2) {
     for (int d = 0; d < 2; ++d) {  // the pair's two newest planes
       const int zn = z + reach + d;
       ring[((zn - (za - reach)) % W) * 256 + threadIdx.x] =
-          bytes_to_h2((live && zn < g.nz) ? __ldg(g2 + zn * gpl + q) : 0xFFFFFFFFu);
+          bytes_to_u16((live && zn < g.nz) ? __ldg(g2 + zn * gpl + q) : 0xFFFFFFFFu);
     }
-    __half2 alo = one, ahi = one, blo = one, bhi = one;
+    uint32_t alo = init, ahi = init, blo = init, bhi = init;
     // plane z - R + k (k = 0..win) is at slot (s0 + k) % W; it meets plane z
-    // with ssub[k + 1] and plane z + 1 with ssub[k]
+    // with sq[k + 1] and plane z + 1 with sq[k]
     const int s0 = (z - za) % W;
-    __half2 sb = ssub[0];
+    uint32_t sb = sq[0];
     for (int k = 0; k < W - s0; ++k) {
-      const __half2 sa = ssub[k + 1];
-      const uint2 v = col[(s0 + k) * 256];
-      alo = __hmin2(alo, __hadd2(as_h2(v.x), sa));
-      ahi = __hmin2(ahi, __hadd2(as_h2(v.y), sa));
-      blo = __hmin2(blo, __hadd2(as_h2(v.x), sb));
-      bhi = __hmin2(bhi, __hadd2(as_h2(v.y), sb));
+      const uint32_t sa = sq[k + 1];
+      const uint2 v = *reinterpret_cast<const uint2*>(colx + (s0 + k) * 512);
+      alo = __viaddmin_u16x2(v.x, sa, alo); ahi = __viaddmin_u16x2(v.y, sa, ahi);
+      blo = __viaddmin_u16x2(v.x, sb, blo); bhi = __viaddmin_u16x2(v.y, sb, bhi);
       sb = sa;
     }
     for (int k = W - s0; k < W; ++k) {
-      const __half2 sa = ssub[k + 1];
-      const uint2 v = col[(k - (W - s0)) * 256];
-      alo = __hmin2(alo, __hadd2(as_h2(v.x), sa));
-      ahi = __hmin2(ahi, __hadd2(as_h2(v.y), sa));
-      blo = __hmin2(blo, __hadd2(as_h2(v.x), sb));
-      bhi = __hmin2(bhi, __hadd2(as_h2(v.y), sb));
+      const uint32_t sa = sq[k + 1];
+      const uint2 v = *reinterpret_cast<const uint2*>(colx + (k - (W - s0)) * 512);
+      alo = __viaddmin_u16x2(v.x, sa, alo); ahi = __viaddmin_u16x2(v.y, sa, ahi);
+      blo = __viaddmin_u16x2(v.x, sb, blo); bhi = __viaddmin_u16x2(v.y, sb, bhi);
       sb = sa;
     }
-    uint64_t va, vb;
-    {
-      const uint32_t ml = as_u32(__hle2(alo, zero)), mh = as_u32(__hle2(ahi, zero));
-      const uint32_t nib = ((ml & 0xFFFFu) ? 1u : 0u) | ((ml >> 16) ? 2u : 0u) |
-                           ((mh & 0xFFFFu) ? 4u : 0u) | ((mh >> 16) ? 8u : 0u);
-      va = static_cast<uint64_t>(nib) << (4 * (q & 15));
-    }
-    {
-      const uint32_t ml = as_u32(__hle2(blo, zero)), mh = as_u32(__hle2(bhi, zero));
-      const uint32_t nib = ((ml & 0xFFFFu) ? 1u : 0u) | ((ml >> 16) ? 2u : 0u) |
-                           ((mh & 0xFFFFu) ? 4u : 0u) | ((mh >> 16) ? 8u : 0u);
-      vb = static_cast<uint64_t>(nib) << (4 * (q & 15));
-    }
+    const auto nibble = [T](uint32_t lo, uint32_t hi) -> uint32_t {
+      return ((lo & 0xFFFFu) <= static_cast<uint32_t>(T) ? 1u : 0u) |
+             ((lo >> 16) <= static_cast<uint32_t>(T) ? 2u : 0u) |
+             ((hi & 0xFFFFu) <= static_cast<uint32_t>(T) ? 4u : 0u) |
+             ((hi >> 16) <= static_cast<uint32_t>(T) ? 8u : 0u);
+    };
+    uint64_t va = static_cast<uint64_t>(nibble(alo, ahi)) << (4 * (q & 15));
+    uint64_t vb = static_cast<uint64_t>(nibble(blo, bhi)) << (4 * (q & 15));
 #pragma unroll
     for (int o = 1; o < 16; o <<= 1) {
       va |= __shfl_xor_sync(0xFFFFFFFFu, va, o);
