@@ -1015,21 +1015,22 @@ __device__ __forceinline__ uint32_t splat16(int v) {
 
 /// y pass: g2 = min(255, min over |dy| <= R of g1(y + dy) + dy^2).
 /// Block = 64 groups x TY rows of one plane, staged (as u16x2 pairs) with
-/// the R halo rows in shared memory; a thread computes 4 consecutive rows of
-/// one group column, so every staged row it loads serves all four.
-template <int TY>
+/// the R halo rows in shared memory; a thread computes RY consecutive rows
+/// of one group column, so every staged row it loads serves all RY.
+template <int TY, int RY>
 __global__ void __launch_bounds__(256) k_sdil_y(const uint32_t* __restrict__ g1, GridView g,
                                                uint32_t* __restrict__ g2, int reach) {
-  static_assert(TY % 16 == 0, "4 rows x 4 row groups per pass");
+  static_assert(TY % (4 * RY) == 0, "RY rows x 4 row groups per pass");
   extern __shared__ uint2 sy[];  // [(TY + 2R) rows][64 groups]
-  __shared__ uint32_t sadd[130];  // dy^2 for dy = -R..R (R <= 63), then 3 pads
+  __shared__ uint32_t sadd[128 + RY];  // dy^2 for dy = -R..R (R <= 63), then RY - 1 pads
   const int nqp = g.wx * 16;
   const int q0 = blockIdx.x * 64, y0 = blockIdx.y * TY, z = blockIdx.z;
   const int rows = TY + 2 * reach;
+  const int last = 2 * reach + RY - 1;
   const size_t plane = static_cast<size_t>(g.ny) * nqp;
   // the pad lifts any sum above the cap 255
   const uint32_t pad = splat16(4096);
-  for (int k = threadIdx.x; k <= 2 * reach + 3; k += blockDim.x)
+  for (int k = threadIdx.x; k <= last; k += blockDim.x)
     sadd[k] = k <= 2 * reach ? splat16((k - reach) * (k - reach)) : pad;
   for (int k = threadIdx.x; k < rows * 64; k += blockDim.x) {
     const int yy = y0 - reach + k / 64, qq = q0 + (k & 63);
@@ -1042,25 +1043,30 @@ __global__ void __launch_bounds__(256) k_sdil_y(const uint32_t* __restrict__ g1,
   const int qq = threadIdx.x & 63;
   if (q0 + qq >= nqp) return;
   const uint32_t cap = splat16(255);
-  for (int ly0 = (threadIdx.x >> 6) * 4; ly0 < TY; ly0 += 16) {
+  for (int ly0 = (threadIdx.x >> 6) * RY; ly0 < TY; ly0 += 4 * RY) {
     if (y0 + ly0 >= g.ny) break;
-    uint32_t lo[4], hi[4];
+    uint32_t lo[RY], hi[RY], a[RY];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) lo[j] = hi[j] = cap;
+    for (int j = 0; j < RY; ++j) {
+      lo[j] = hi[j] = cap;
+      a[j] = pad;
+    }
     // staged row ly0 + k meets output row ly0 + j with dy^2 entry k - j
-    uint32_t a0 = sadd[0], a1 = pad, a2 = pad, a3 = pad;
+    a[0] = sadd[0];
     const uint2* col = sy + ly0 * 64 + qq;
-    for (int k = 0; k <= 2 * reach + 3; ++k) {
+    for (int k = 0; k <= last; ++k) {
       const uint2 v = col[k * 64];
-      lo[0] = __viaddmin_u16x2(v.x, a0, lo[0]); hi[0] = __viaddmin_u16x2(v.y, a0, hi[0]);
-      lo[1] = __viaddmin_u16x2(v.x, a1, lo[1]); hi[1] = __viaddmin_u16x2(v.y, a1, hi[1]);
-      lo[2] = __viaddmin_u16x2(v.x, a2, lo[2]); hi[2] = __viaddmin_u16x2(v.y, a2, hi[2]);
-      lo[3] = __viaddmin_u16x2(v.x, a3, lo[3]); hi[3] = __viaddmin_u16x2(v.y, a3, hi[3]);
-      a3 = a2; a2 = a1; a1 = a0;
-      a0 = sadd[min(k + 1, 2 * reach + 3)];
+#pragma unroll
+      for (int j = 0; j < RY; ++j) {
+        lo[j] = __viaddmin_u16x2(v.x, a[j], lo[j]);
+        hi[j] = __viaddmin_u16x2(v.y, a[j], hi[j]);
+      }
+#pragma unroll
+      for (int j = RY - 1; j > 0; --j) a[j] = a[j - 1];
+      a[0] = sadd[min(k + 1, last)];
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < RY; ++j) {
       const int y = y0 + ly0 + j;
       if (y < g.ny)
         g2[z * plane + static_cast<size_t>(y) * nqp + q0 + qq] = __byte_perm(lo[j], hi[j], 0x6420);
@@ -1069,28 +1075,30 @@ __global__ void __launch_bounds__(256) k_sdil_y(const uint32_t* __restrict__ g1,
 }
 
 /// z pass + threshold: thread per 4-voxel group of a plane, sliding along z
-/// over a chunk of ZC output planes, two at a time, with the 2R + 2 input
-/// planes around the pair in a shared-memory ring (u16x2 pairs): bit =
+/// over a chunk of ZC output planes, PZ at a time, with the 2R + PZ input
+/// planes around them in a shared-memory ring (u16x2 pairs): bit =
 /// [min over |dz| <= R of g2(z + dz) + dz^2 <= T] (a plane with dz^2 > T
 /// cannot pass). A half-warp holds the 16 groups of one output word (rows
 /// are padded to whole words) and ORs their nibbles by shuffles.
-template <int ZC>
+template <int ZC, int PZ>
 __global__ void __launch_bounds__(256) k_sdil_z(const uint32_t* __restrict__ g2, GridView g,
                                                uint64_t* __restrict__ out, int reach, int T,
                                                int z_lo, int z_hi) {
-  extern __shared__ uint2 ring[];  // [2R + 2][256]
-  // sq[1 + k] = dz^2 for dz = k - R; the pads sq[0] and sq[win + 1] are
-  // above any threshold
-  __shared__ uint32_t sq[130];
+  static_assert(ZC % PZ == 0, "whole steps per chunk");
+  extern __shared__ uint2 ring[];  // [2R + PZ][256]
+  // sq[PZ - 1 + k] = dz^2 for dz = k - R (k = 0..2R); the PZ - 1 pads on
+  // either side are above any threshold
+  __shared__ uint32_t sq[128 + 2 * PZ];
   const int64_t gpl = static_cast<int64_t>(g.ny) * g.wx * 16;  // groups per plane
   const int64_t q = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
   const bool live = q < gpl;
   const int za = z_lo + blockIdx.y * ZC;
   const int zb = min(z_hi, za + ZC - 1);
-  const int win = 2 * reach + 1, W = win + 1;
-  for (int k = threadIdx.x; k < win + 2; k += blockDim.x) {
-    const int dz = k - 1 - reach;
-    sq[k] = (k == 0 || k == win + 1) ? splat16(4096) : splat16(dz * dz);
+  const int win = 2 * reach + 1, W = win + PZ - 1;
+  const uint32_t pad = splat16(4096);
+  for (int k = threadIdx.x; k < win + 2 * PZ - 1; k += blockDim.x) {
+    const int dz = k - (PZ - 1) - reach;
+    sq[k] = (dz < -reach || dz > reach) ? pad : splat16(dz * dz);
   }
   for (int zz = za - reach; zz < za + reach; ++zz)
     ring[(zz - (za - reach)) * 256 + threadIdx.x] =
@@ -1099,47 +1107,44 @@ __global__ void __launch_bounds__(256) k_sdil_z(const uint32_t* __restrict__ g2,
   const int lane = threadIdx.x & 31;
   const uint32_t init = splat16(0xFFFF);
   const uint32_t* colx = reinterpret_cast<const uint32_t*>(ring) + 2 * threadIdx.x;
-  for (int z = za; z <= zb; z += 2) {
-    for (int d = 0; d < 2; ++d) {  // the pair's two newest planes
+  for (int z = za; z <= zb; z += PZ) {
+#pragma unroll
+    for (int d = 0; d < PZ; ++d) {  // the step's PZ newest planes
       const int zn = z + reach + d;
       ring[((zn - (za - reach)) % W) * 256 + threadIdx.x] =
           bytes_to_u16((live && zn < g.nz) ? __ldg(g2 + zn * gpl + q) : 0xFFFFFFFFu);
     }
-    uint32_t alo = init, ahi = init, blo = init, bhi = init;
-    // plane z - R + k (k = 0..win) is at slot (s0 + k) % W; it meets plane z
-    // with sq[k + 1] and plane z + 1 with sq[k]
-    const int s0 = (z - za) % W;
-    uint32_t sb = sq[0];
-    for (int k = 0; k < W - s0; ++k) {
-      const uint32_t sa = sq[k + 1];
-      const uint2 v = *reinterpret_cast<const uint2*>(colx + (s0 + k) * 512);
-      alo = __viaddmin_u16x2(v.x, sa, alo); ahi = __viaddmin_u16x2(v.y, sa, ahi);
-      blo = __viaddmin_u16x2(v.x, sb, blo); bhi = __viaddmin_u16x2(v.y, sb, bhi);
-      sb = sa;
-    }
-    for (int k = W - s0; k < W; ++k) {
-      const uint32_t sa = sq[k + 1];
-      const uint2 v = *reinterpret_cast<const uint2*>(colx + (k - (W - s0)) * 512);
-      alo = __viaddmin_u16x2(v.x, sa, alo); ahi = __viaddmin_u16x2(v.y, sa, ahi);
-      blo = __viaddmin_u16x2(v.x, sb, blo); bhi = __viaddmin_u16x2(v.y, sb, bhi);
-      sb = sa;
-    }
-    const auto nibble = [T](uint32_t lo, uint32_t hi) -> uint32_t {
-      return ((lo & 0xFFFFu) <= static_cast<uint32_t>(T) ? 1u : 0u) |
-             ((lo >> 16) <= static_cast<uint32_t>(T) ? 2u : 0u) |
-             ((hi & 0xFFFFu) <= static_cast<uint32_t>(T) ? 4u : 0u) |
-             ((hi >> 16) <= static_cast<uint32_t>(T) ? 8u : 0u);
-    };
-    uint64_t va = static_cast<uint64_t>(nibble(alo, ahi)) << (4 * (q & 15));
-    uint64_t vb = static_cast<uint64_t>(nibble(blo, bhi)) << (4 * (q & 15));
+    uint32_t lo[PZ], hi[PZ], a[PZ];
 #pragma unroll
-    for (int o = 1; o < 16; o <<= 1) {
-      va |= __shfl_xor_sync(0xFFFFFFFFu, va, o);
-      vb |= __shfl_xor_sync(0xFFFFFFFFu, vb, o);
+    for (int j = 0; j < PZ; ++j) {
+      lo[j] = hi[j] = init;
+      a[j] = pad;
     }
-    if (live && (lane & 15) == 0) {
-      out[(z * gpl + q) >> 4] = va;
-      if (z + 1 <= zb) out[((z + 1) * gpl + q) >> 4] = vb;
+    // plane z - R + k (k = 0..W-1) is at slot (s0 + k) % W; it meets plane
+    // z + j with sq[PZ - 1 + k - j]
+    a[0] = sq[PZ - 1];
+    const int s0 = (z - za) % W;
+    const auto tap = [&](const uint2 v, int k) {
+#pragma unroll
+      for (int j = 0; j < PZ; ++j) {
+        lo[j] = __viaddmin_u16x2(v.x, a[j], lo[j]);
+        hi[j] = __viaddmin_u16x2(v.y, a[j], hi[j]);
+      }
+#pragma unroll
+      for (int j = PZ - 1; j > 0; --j) a[j] = a[j - 1];
+      a[0] = sq[PZ + k];
+    };
+    for (int k = 0; k < W - s0; ++k) tap(*reinterpret_cast<const uint2*>(colx + (s0 + k) * 512), k);
+    for (int k = W - s0; k < W; ++k) tap(*reinterpret_cast<const uint2*>(colx + (k - (W - s0)) * 512), k);
+    const uint32_t tt = static_cast<uint32_t>(T);
+#pragma unroll
+    for (int j = 0; j < PZ; ++j) {
+      const uint32_t nib = ((lo[j] & 0xFFFFu) <= tt ? 1u : 0u) | ((lo[j] >> 16) <= tt ? 2u : 0u) |
+                           ((hi[j] & 0xFFFFu) <= tt ? 4u : 0u) | ((hi[j] >> 16) <= tt ? 8u : 0u);
+      uint64_t v = static_cast<uint64_t>(nib) << (4 * (q & 15));
+#pragma unroll
+      for (int o = 1; o < 16; o <<= 1) v |= __shfl_xor_sync(0xFFFFFFFFu, v, o);
+      if (live && (lane & 15) == 0 && z + j <= zb) out[((z + j) * gpl + q) >> 4] = v;
     }
   }
 }
@@ -1166,8 +1171,9 @@ bool dilate_separable(rp_grid* g, double radius, int z0, int z1) {
          static_cast<const uint64_t*>(g->bits), v, g1.p, reach);
   constexpr int TY = 32;
   const size_t smy = static_cast<size_t>(TY + 2 * reach) * 64 * sizeof(uint2);
-  allow_smem(k_sdil_y<TY>, smy);
-  launch(ctx, "dilate", k_sdil_y<TY>,
+  constexpr int RY = 4;
+  allow_smem(k_sdil_y<TY, RY>, smy);
+  launch(ctx, "dilate", k_sdil_y<TY, RY>,
          dim3(static_cast<unsigned>((g->wx * 16 + 63) / 64), static_cast<unsigned>((g->dims[1] + TY - 1) / TY),
               static_cast<unsigned>(g->dims[2])),
          dim3(256), smy, static_cast<const uint32_t*>(g1.p), v, g2.p, reach);
@@ -1178,11 +1184,12 @@ bool dilate_separable(rp_grid* g, double radius, int z0, int z1) {
     RP_CUDA(cudaMemcpyAsync(out, g->bits, g->n_words * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
   // ZC output planes per thread (the 2R halo planes are re-read per chunk)
   constexpr int ZC = 32;
-  const size_t smz = static_cast<size_t>(2 * reach + 2) * 256 * sizeof(uint2);
+  constexpr int PZ = 4;
+  const size_t smz = static_cast<size_t>(2 * reach + PZ) * 256 * sizeof(uint2);
   const int64_t gpl = static_cast<int64_t>(g->dims[1]) * g->wx * 16;
   const dim3 grid(static_cast<unsigned>((gpl + 255) / 256), static_cast<unsigned>((z1 - z0 + ZC) / ZC));
-  allow_smem(k_sdil_z<ZC>, smz);
-  launch(ctx, "dilate", k_sdil_z<ZC>, grid, dim3(256), smz, static_cast<const uint32_t*>(g2.p), v,
+  allow_smem(k_sdil_z<ZC, PZ>, smz);
+  launch(ctx, "dilate", k_sdil_z<ZC, PZ>, grid, dim3(256), smz, static_cast<const uint32_t*>(g2.p), v,
          out, reach, static_cast<int>(T), z0, z1);
   RP_CUDA(cudaFreeAsync(g->bits, st));
   g->bits = out;
