@@ -953,8 +953,9 @@ __global__ void __launch_bounds__(256) k_dilate_general(const uint64_t* __restri
 /// x pass: bits -> g1. Thread per 64-voxel word (reach <= 63, so the word
 /// and its two neighbours hold every set bit within reach): per voxel the
 /// nearest set bit on each side by a funnel shift and find-first-set /
-/// count-leading-zeros, capped at R; the word's 16 groups leave as four
-/// 16-byte stores. Padding voxels (x >= nx) are 255.
+/// count-leading-zeros over a 32-bit window each side, which sees every bit
+/// within reach (T <= 254 keeps R <= 15 < 32); the word's 16 groups leave as
+/// four 16-byte stores. Padding voxels (x >= nx) are 255.
 __global__ void __launch_bounds__(256) k_sdil_x(const uint64_t* __restrict__ bits, GridView g,
                                                uint32_t* __restrict__ g1, int reach) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -969,31 +970,32 @@ __global__ void __launch_bounds__(256) k_sdil_x(const uint64_t* __restrict__ bit
 #pragma unroll
     for (int k = 0; k < 16; ++k) o[k] = 0xFFFFFFFFu;
   } else {
+    const uint32_t c0 = static_cast<uint32_t>(cur), c1 = static_cast<uint32_t>(cur >> 32);
+    const uint32_t n0 = static_cast<uint32_t>(nxt), p1 = static_cast<uint32_t>(prv >> 32);
 #pragma unroll
     for (int gq = 0; gq < 16; ++gq) {
       uint32_t out = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int b = 4 * gq + k;
-        const int x = (w << 6) + b;
-        int best = 255;
-        if (x < g.nx) {
-          // right: bits >= b of cur, then nxt
-          const uint64_t r = b ? ((cur >> b) | (nxt << (64 - b))) : cur;
-          const uint64_t rh = b ? (nxt >> b) : nxt;
-          const int d = r ? __ffsll(static_cast<long long>(r)) - 1
-                          : (rh ? 64 + __ffsll(static_cast<long long>(rh)) - 1 : 1 << 20);
-          // left: bits <= b of cur, then prv
-          const uint64_t l = b < 63 ? ((cur << (63 - b)) | (prv >> (b + 1))) : cur;
-          const uint64_t lh = b < 63 ? (prv << (63 - b)) : prv;
-          const int e = l ? __clzll(static_cast<long long>(l))
-                          : (lh ? 64 + __clzll(static_cast<long long>(lh)) : 1 << 20);
-          const int dm = d < e ? d : e;
-          if (dm <= reach) best = dm * dm;
-        }
-        out |= static_cast<uint32_t>(best) << (8 * k);
+        // bits b .. b + 31 with bit b lowest; bits b - 31 .. b with bit b highest
+        const uint32_t rw = b < 32 ? __funnelshift_r(c0, c1, b) : __funnelshift_r(c1, n0, b - 32);
+        const uint32_t lw = b < 32 ? __funnelshift_l(p1, c0, 31 - b) : __funnelshift_l(c0, c1, 63 - b);
+        const int d = rw ? __ffs(static_cast<int>(rw)) - 1 : 64;
+        const int e = lw ? __clz(static_cast<int>(lw)) : 64;
+        const int dm = d < e ? d : e;
+        const uint32_t best = dm <= reach ? static_cast<uint32_t>(dm * dm) : 255u;
+        out |= best << (8 * k);
       }
       o[gq] = out;
+    }
+    const int valid = g.nx - (w << 6);  // voxels of this word inside the row
+    if (valid < 64) {
+#pragma unroll
+      for (int gq = 0; gq < 16; ++gq)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (4 * gq + k >= valid) o[gq] |= 0xFFu << (8 * k);
     }
   }
   uint4* dst = reinterpret_cast<uint4*>(g1 + t * 16);
@@ -1162,7 +1164,8 @@ bool dilate_separable(rp_grid* g, double radius, int z0, int z1) {
   while (static_cast<double>(T + 1) <= r2) ++T;
   while (T >= 0 && !(static_cast<double>(T) <= r2)) --T;
   static const bool off = std::getenv("RP_DILATE_NAIVE") != nullptr;
-  if (off || T > 254 || reach > 63 || reach < 1) return false;
+  // T <= 254 bounds R by 15 (the x pass's 32-bit windows need R <= 31)
+  if (off || T > 254 || reach > 31 || reach < 1) return false;
   cudaStream_t st = ctx->stream;
   const int64_t groups = static_cast<int64_t>(g->dims[2]) * g->dims[1] * g->wx * 16;
   DevBuf<uint32_t> g1(groups, st), g2(groups, st);
