@@ -191,6 +191,55 @@ __device__ __forceinline__ uint32_t walk_hits(const GridView& g, V3 from, V3 to,
   return mask;
 }
 
+/// walk_hits (non-INPLACE) with each sample's cell coordinate formed as one
+/// FMA, q = t * B + A with A = fl(from - o) * rvs and B = diff * rvs, instead
+/// of the sample point and its offset (4 fp64 ops per axis). q differs from
+/// the reference's fl(fl(fl(from + fl(t * diff)) - o) / vs) by at most
+/// ~9u M + u P cells (M bounds |A|, t |B| and |q|, P the sample's absolute
+/// coordinate in cells), which the caller's bracket half-width dqa covers
+/// (SolveDev::dq_aff); samples whose bracket holds an integer fail `exact`
+/// and the caller redoes the walk sequentially, so the verdict is the
+/// reference's.
+template <int N>
+__device__ __forceinline__ uint32_t walk_hits_affine(const GridView& g, V3 from, V3 to, int n,
+                                                     double dqa, bool* exact, int kstart = 0) {
+  const V3 diff = to - from;
+  const double Ax = (from.x - g.ox) * g.rvs, Ay = (from.y - g.oy) * g.rvs, Az = (from.z - g.oz) * g.rvs;
+  const double Bx = diff.x * g.rvs, By = diff.y * g.rvs, Bz = diff.z * g.rvs;
+  bool ok = true;
+  uint32_t mask = 0;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    if (k < kstart) continue;  // caller-proven free samples (warp-uniform)
+    const bool live = k < n;
+    const double t = c_tk.v[n][live ? k + 1 : n];
+    const double qx = fma(t, Bx, Ax), qy = fma(t, By, Ay), qz = fma(t, Bz, Az);
+    const double lx = floor(qx - dqa), ly = floor(qy - dqa), lz = floor(qz - dqa);
+    ok &= (qx + dqa < lx + 1.0) & (qy + dqa < ly + 1.0) & (qz + dqa < lz + 1.0);
+    const int ix = static_cast<int>(lx), iy = static_cast<int>(ly), iz = static_cast<int>(lz);
+    const bool inb = live & (static_cast<unsigned>(ix) < static_cast<unsigned>(g.nx)) &
+                     (static_cast<unsigned>(iy) < static_cast<unsigned>(g.ny)) &
+                     (static_cast<unsigned>(iz) < static_cast<unsigned>(g.nz));
+    const long long idx = inb ? (static_cast<long long>(iz) * g.ny + iy) * g.wx + (ix >> 6) : 0;
+    const uint64_t w = __ldg(g.bits + idx);
+    mask |= static_cast<uint32_t>((w >> (ix & 63)) & static_cast<uint64_t>(inb)) << k;
+  }
+  *exact = ok;
+  return mask;
+}
+
+/// walk_first_blocked_fast_seg_from over walk_hits_affine (bracket dqa).
+__device__ __forceinline__ int walk_first_blocked_affine_from(const GridView& g, V3 from, V3 to,
+                                                              int n, int kstart, double dqa) {
+  bool exact = true;
+  uint32_t m;
+  if (n == 8) m = walk_hits_affine<8>(g, from, to, 8, dqa, &exact, kstart);
+  else if (n <= kTkMax) m = walk_hits_affine<kTkMax>(g, from, to, n, dqa, &exact, kstart);
+  else return walk_first_blocked(g, from, to, n);
+  if (!exact) return walk_first_blocked(g, from, to, n);
+  return m ? __ffs(m) : 0;
+}
+
 /// walk_first_blocked with the gathers in flight together (n <= 16), the
 /// sequential walk otherwise. Identical result. INPLACE = resolve ambiguous
 /// floors by division inside the parallel walk (planner: walks from the root

@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(256, 5) k_seg2_rows(SolveDev a, const SurvDev*
         int fb =
             cached ? static_cast<int>(((c2w >> lane) & 1u) ^ 1u)
             : ks >= a.n     ? 0
-            : kSeg2ParWalk ? rpd::walk_first_blocked_fast_seg_from(a.g, p1, p2, a.n, ks)
+            : kSeg2ParWalk ? rpd::walk_first_blocked_affine_from(a.g, p1, p2, a.n, ks, a.dq_aff)
                            : rpd::walk_first_blocked(a.g, p1, p2, a.n);
         if (OV && cached && row_meets && fb == 0 &&
             fmin(p1.x, p2.x) <= ov_hi.x + 1e-9 && fmax(p1.x, p2.x) >= ov_lo.x - 1e-9 &&
@@ -1084,6 +1084,22 @@ static HostShortcut host_shortcut(const rp_solution_set* s, const ShortcutRec& r
   return h;
 }
 
+/// Bracket half-width (cells) of rpd::walk_hits_affine for walks between
+/// points the arm reaches: every such point lies within Rw = max |root - o|
+/// + sum(L) + sum(|off|) of the grid origin per axis, so M = 2 Rw / vs bounds
+/// |A|, t |B| and |q| and P = (max |o| + 2 Rw) / vs the absolute coordinate;
+/// the error bound ~9u M + u P is covered 8x, plus the grid's own dq.
+double affine_bracket(const rpd::GridView& g, const rp_arm& arm) {
+  double rw = std::max({std::fabs(arm.root[0] - g.ox), std::fabs(arm.root[1] - g.oy),
+                        std::fabs(arm.root[2] - g.oz)});
+  for (int k = 0; k < arm.n_segments && k < RP_MAX_SEGMENTS; ++k)
+    rw += std::fabs(arm.lengths[k]) + (k < arm.n_offsets ? std::fabs(arm.offsets[k]) : 0.0);
+  const double M = 2.0 * rw / g.vs;
+  const double P = (std::max({std::fabs(g.ox), std::fabs(g.oy), std::fabs(g.oz)}) + 2.0 * rw) / g.vs;
+  const double u = 1.1102230246251565e-16;
+  return 8.0 * u * (9.0 * M + P + 4.0) + g.dq;
+}
+
 rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q, const rp_grid* g,
                              V3 target, const rp_reach_params& rp, int part, int parts) {
   HostSpan span_("solve_reach");
@@ -1133,6 +1149,7 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
     a.eps = eps;
     a.coarse2 = (L3 + eps) * (L3 + eps) * (1.0 + 1e-12);
     a.band_lo2 = L3 - eps > 0.0 ? (L3 - eps) * (L3 - eps) * (1.0 - 1e-9) : 0.0;
+    a.dq_aff = affine_bracket(a.g, arm);
     double budget = arm.lengths[1] + arm.lengths[2] + eps;
     if (eight) budget += arm.lengths[3];
     budget += 1e-9;

@@ -34,6 +34,7 @@ struct SolveDev {
   int n_targets;
   double eps, coarse2, budget2, near_r, spacing, L4;
   double band_lo2;  // conservative lower bound of |v3|^2 for the gap band (prefilters)
+  double dq_aff;    // floor bracket of rpd::walk_hits_affine for segment-2 walks
   V3 target;
   const double* qx;
   const double* qy;
