@@ -181,6 +181,30 @@ constexpr size_t kUploadSlotBytes = 64 << 10;
 /// context's pinned ring and the DMA reads it from there. A pageable
 /// cudaMemcpyAsync would synchronise the stream before it starts; only
 /// uploads larger than a slot (a quiver or a uint8 grid, once) still do.
+namespace {
+/// Device copy out of a mapped pinned slot (UVA: the slot's host address is
+/// valid on the device), 16 bytes per thread.
+__global__ void k_copy_mapped(uint4* __restrict__ dst, const uint4* __restrict__ src, size_t n16) {
+  const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n16) dst[i] = src[i];
+}
+
+/// Slot -> device in stream order. Larger uploads go through a copy kernel
+/// reading the mapped slot: measured on B200 a 50 KB pinned cudaMemcpyAsync
+/// costs ~16 us of host time, a kernel launch ~4.
+void upload_from_slot(rp_ctx* ctx, void* dst, const void* slot, size_t bytes) {
+  static const bool dma = std::getenv("RP_UPLOAD_DMA") != nullptr;
+  const bool aligned = (reinterpret_cast<uintptr_t>(dst) & 15) == 0 && (bytes & 15) == 0;
+  if (dma || !aligned || bytes < 4096) {
+    RP_CUDA(cudaMemcpyAsync(dst, slot, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    return;
+  }
+  const size_t n16 = bytes / 16;
+  launch(ctx, "upload", k_copy_mapped, dim3(static_cast<unsigned>((n16 + 255) / 256)), dim3(256), 0,
+         static_cast<uint4*>(dst), static_cast<const uint4*>(slot), n16);
+}
+}  // namespace
+
 void copy_to_device(rp_ctx* ctx, void* dst, const void* src, size_t bytes) {
   if (!bytes) return;
   if (bytes > kUploadSlotBytes) {
@@ -203,7 +227,26 @@ void copy_to_device(rp_ctx* ctx, void* dst, const void* src, size_t bytes) {
   RP_CUDA(cudaEventSynchronize(ctx->upload_ev[k]));
   char* slot = ctx->upload_ring + static_cast<size_t>(k) * kUploadSlotBytes;
   std::memcpy(slot, src, bytes);
-  RP_CUDA(cudaMemcpyAsync(dst, slot, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  upload_from_slot(ctx, dst, slot, bytes);
+  RP_CUDA(cudaEventRecord(ctx->upload_ev[k], ctx->stream));
+}
+
+void copy_to_device_fill(rp_ctx* ctx, void* dst, size_t bytes,
+                         const std::function<void(unsigned char*)>& fill) {
+  if (!bytes) return;
+  if (bytes > kUploadSlotBytes || !ctx->upload_ring) {
+    std::vector<unsigned char> h(bytes);
+    fill(h.data());
+    copy_to_device(ctx, dst, h.data(), bytes);
+    return;
+  }
+  // fill the pinned slot in place (no staging copy)
+  const int k = ctx->upload_next;
+  ctx->upload_next = (k + 1) % kUploadSlots;
+  RP_CUDA(cudaEventSynchronize(ctx->upload_ev[k]));
+  unsigned char* slot = reinterpret_cast<unsigned char*>(ctx->upload_ring) + static_cast<size_t>(k) * kUploadSlotBytes;
+  fill(slot);
+  upload_from_slot(ctx, dst, slot, bytes);
   RP_CUDA(cudaEventRecord(ctx->upload_ev[k], ctx->stream));
 }
 

@@ -399,6 +399,10 @@ struct HostRead {
 };
 void copy_to_host_many(rp_ctx* ctx, std::initializer_list<HostRead> reads);
 void copy_to_device(rp_ctx* ctx, void* dst, const void* src, size_t bytes);
+/// copy_to_device of `bytes` written by `fill` straight into a pinned
+/// upload slot (no host staging copy).
+void copy_to_device_fill(rp_ctx* ctx, void* dst, size_t bytes,
+                         const std::function<void(unsigned char*)>& fill);
 
 // Derived reach parameters (src/reach_solver.cpp:28-43).
 double nominal_spacing(const rp_arm& a, const rp_reach_params& r);

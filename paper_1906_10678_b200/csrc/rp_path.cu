@@ -2861,18 +2861,17 @@ bool Planner::bp_launch(const std::vector<V3>& wps, const HostPose& anchor,
   const size_t o_win = o_kind + al(m * sizeof(int));
   const size_t io_bytes = o_win + al(m * sizeof(BpWin));
   if (bp_io.n < io_bytes) bp_io.alloc(io_bytes, st);
-  {
-    std::vector<unsigned char> h(io_bytes, 0);
-    std::memcpy(h.data() + o_wps, wps.data(), m * sizeof(V3));
+  copy_to_device_fill(ctx, bp_io.p, io_bytes, [&](unsigned char* h) {
+    std::memset(h, 0, io_bytes);
+    std::memcpy(h + o_wps, wps.data(), m * sizeof(V3));
     const DevPose da = to_dev(anchor);
-    std::memcpy(h.data() + o_poses + (m - 1) * sizeof(DevPose), &da, sizeof(DevPose));
+    std::memcpy(h + o_poses + (m - 1) * sizeof(DevPose), &da, sizeof(DevPose));
     for (int k = 0; k < m; ++k) {
       const double one = 1.0;
-      std::memcpy(h.data() + o_relax + k * sizeof(double), &one, sizeof(double));
+      std::memcpy(h + o_relax + k * sizeof(double), &one, sizeof(double));
     }
-    std::memset(h.data() + o_win, 0xFF, m * sizeof(BpWin));  // i = -1: not published
-    copy_to_device(ctx, bp_io.p, h.data(), io_bytes);
-  }
+    std::memset(h + o_win, 0xFF, m * sizeof(BpWin));  // i = -1: not published
+  });
   unsigned char* io = bp_io.p;
   if (!cluster) bp_bar.zero();
   A.wps = reinterpret_cast<V3*>(io + o_wps);

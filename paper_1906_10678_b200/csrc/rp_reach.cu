@@ -1304,11 +1304,11 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
     if (sync_free) {
       // the solve's one read-back: counters, shortcut count, best, S1 and
       // the survivor list
+      // (the survivor list stays on the device until rp_solution_set_keys)
       copy_to_host_many(ctx, {{hc, ctr.p, sizeof(hc)},
                               {&nsc, sc_count.p, sizeof(unsigned)},
                               {&hb, best.p, sizeof(BestRec)},
-                              {&S1, surv_cnt.p, sizeof(int)},
-                              {surv_all.data(), surv_idx.p, q->n * sizeof(int)}});
+                              {&S1, surv_cnt.p, sizeof(int)}});
       s_lo = static_cast<int>(static_cast<int64_t>(S1) * part / parts);
       s_hi = static_cast<int>(static_cast<int64_t>(S1) * (part + 1) / parts);
       s->n_pairs = static_cast<int64_t>(S1) * q->n;
@@ -1318,7 +1318,11 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
                               {&hb, best.p, p_hi > p_lo ? sizeof(BestRec) : 0}});
     }
     s->S1 = S1;
-    s->surv_i.assign(surv_all.begin(), surv_all.begin() + S1);
+    if (!sync_free) {
+      s->surv_i.assign(surv_all.begin(), surv_all.begin() + S1);
+      s->surv_i_ready = true;
+    }
+    s->surv_idx_d = std::move(surv_idx);
     require(nsc <= kShortcutCap, RP_E_CAPACITY_EXCEEDED, "too many near-encounter hypotheses");
 
     rp_solve_stats& S = s->stats;
@@ -1627,6 +1631,16 @@ rp_status rp_solution_set_sizes(const rp_solution_set* s, int64_t* ns, int64_t* 
   });
 }
 
+/// The segment-1 quiver index of every survivor row (read back on first use).
+static const std::vector<int>& surv_i_of(rp_solution_set* s) {
+  if (!s->surv_i_ready) {
+    s->surv_i.assign(s->S1, 0);
+    if (s->S1 > 0) copy_to_host(s->ctx, s->surv_i.data(), s->surv_idx_d.p, s->S1 * sizeof(int));
+    s->surv_i_ready = true;
+  }
+  return s->surv_i;
+}
+
 rp_status rp_solution_set_keys(const rp_solution_set* cs, int32_t* keys, int64_t cap) {
   return guarded([&] {
     auto* s = const_cast<rp_solution_set*>(cs);
@@ -1638,7 +1652,7 @@ rp_status rp_solution_set_keys(const rp_solution_set* cs, int32_t* keys, int64_t
       const long long p = k[t] / s->B;
       const int bi = static_cast<int>(k[t] - p * s->B);
       const int sidx = static_cast<int>(p / s->sd.Q);
-      keys[3 * t] = s->surv_i[sidx];
+      keys[3 * t] = surv_i_of(s)[sidx];
       keys[3 * t + 1] = static_cast<int>(p - static_cast<long long>(sidx) * s->sd.Q);
       keys[3 * t + 2] = s->sd.eight ? s->h_bcone[bi] : -1;
     }

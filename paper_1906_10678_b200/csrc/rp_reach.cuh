@@ -197,7 +197,9 @@ struct rp_solution_set {
   int S1 = 0;
   int part = 0, parts = 1;  // a part of a split solve (solve_reach)
   rp::DevBuf<rp::SurvDev> surv;
-  std::vector<int> surv_i;
+  std::vector<int> surv_i;     // segment-1 quiver index per survivor row (read lazily: surv_i_of)
+  rp::DevBuf<int> surv_idx_d;  // the same on the device (k_compact_small's list)
+  bool surv_i_ready = false;
   int B = 0;
   // backward points, directions, the target, cone indices and walk4 flags
   // (SolveDev bpts / bdirs / targets / bcone / walk4_ok point into it)
