@@ -508,7 +508,7 @@ def dominant_roofline(ctx, arm, q, sc, api, scenes):
            "ms": ms, "algorithmic_bytes_per_launch": sc.n ** 3 / 8 + pairs / 8,
            "algorithmic_bytes_def": "the bit grid once + one result bit per pair"}
     try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "r2b_c3_seg2_ncu.json")))
+        prof = json.load(open(os.path.join(ROOT, "profiles", "r2c_c3_seg2_ncu.json")))
         m = prof["launches"][0]["metrics"]
         out.update({
             "frac": float(m["smsp__issue_active.avg.pct_of_peak_sustained_active"][0]) / 100,
@@ -518,7 +518,7 @@ def dominant_roofline(ctx, arm, q, sc, api, scenes):
             "traffic": sum(float(m[k][0]) * {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6,
                                                "Gbyte": 1e9}.get(m[k][1], 1.0)
                            for k in ("dram__bytes_read.sum", "dram__bytes_write.sum")),
-            "traffic_source": "profiles/r2b_c3_seg2_ncu.json (ncu --set full, one launch)"})
+            "traffic_source": "profiles/r2c_c3_seg2_ncu.json (ncu --set full, one launch)"})
     except (OSError, KeyError, ValueError, IndexError):
         pass
     return out
