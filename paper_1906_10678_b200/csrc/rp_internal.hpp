@@ -120,6 +120,10 @@ struct rp_ctx {
   int* cancel_flag = nullptr;
   cudaStream_t aux = nullptr;
   cudaEvent_t aux_ev = nullptr;  // "cancel flags cleared" on aux
+  // solve_reach's temporaries (ctx_scratch): kept across solves, reused in
+  // the context stream's order
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
   // Pinned upload ring (copy_to_device): kUploadSlots slots of
   // kUploadSlotBytes; a slot is reused only after the event recorded behind
   // its last copy completed, so uploads never synchronise the stream.
@@ -346,6 +350,28 @@ inline void launch_pdl(rp_ctx* ctx, const char* name, void (*kernel)(KArgs...), 
   RP_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
   launch_end(ctx, name, ev);
 }
+
+/// The context's scratch block of at least `bytes` (grown stream-ordered;
+/// the contents are undefined). For temporaries of one call on the
+/// context's stream: the next call's kernels run after this call's.
+unsigned char* ctx_scratch(rp_ctx* ctx, size_t bytes);
+
+/// Lays typed arrays out in one block, 16-byte aligned: reserve() the
+/// sizes, bind() the block, then at() the arrays.
+struct ScratchCarver {
+  unsigned char* base = nullptr;
+  size_t off = 0;
+  template <typename T>
+  size_t reserve(size_t n) {
+    off = (off + 15) & ~size_t{15};
+    const size_t at = off;
+    off += n * sizeof(T);
+    return at;
+  }
+  void bind(unsigned char* b) { base = b; }
+  template <typename T>
+  T* at(size_t o) const { return reinterpret_cast<T*>(base + o); }
+};
 
 /// Stream-ordered device buffer.
 template <typename T>

@@ -1186,18 +1186,39 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
       launch(ctx, "walk4", k_walk4, dim3(nblk(s->B, 128)), dim3(128), 0, a,
              const_cast<uint8_t*>(a.walk4_ok));
 
-    DevBuf<unsigned long long> ctr(C_COUNT, st);
-    ctr.zero();
-    DevBuf<unsigned> sc_count(1, st);
-    sc_count.zero();
-    DevBuf<long long> sc_list(kShortcutCap, st);
+    // the solve's temporaries in the context's scratch block (one
+    // allocation kept across solves; stream order protects reuse): counters
+    // and flags first, zeroed by one memset
     const int qwords = (q->n + 31) / 32;
-    DevBuf<uint32_t> surv_bits(qwords, st);
-    launch(ctx, "seg1", k_seg1, dim3(nblk(q->n, 256)), dim3(256), 0, a, surv_bits.p, ctr.p,
-           sc_list.p, sc_count.p);
-    DevBuf<int> surv_idx(q->n + 1, st), surv_cnt(1, st);
+    ScratchCarver sk;
+    const size_t o_ctr = sk.reserve<unsigned long long>(C_COUNT);
+    const size_t o_scc = sk.reserve<unsigned>(1);
+    const size_t o_uc = sk.reserve<int>(1);
+    const size_t o_sv = sk.reserve<int>(1);
+    const size_t zero_bytes = sk.off;
+    const size_t o_scl = sk.reserve<long long>(kShortcutCap);
+    const size_t o_sb = sk.reserve<uint32_t>(qwords);
+    const size_t o_bb = sk.reserve<BestRec>(static_cast<size_t>(ctx->sm_count) * 8);
+    const size_t o_best = sk.reserve<BestRec>(1);
+    const size_t o_ks = sk.reserve<uint8_t>(std::max(1, q->n));
+    const size_t o_ke = sk.reserve<uint8_t>(1);
+    sk.bind(ctx_scratch(ctx, sk.off));
+    auto* ctr = sk.at<unsigned long long>(o_ctr);
+    auto* sc_count = sk.at<unsigned>(o_scc);
+    auto* unit_ctr = sk.at<int>(o_uc);
+    auto* surv_cnt = sk.at<int>(o_sv);
+    auto* sc_list = sk.at<long long>(o_scl);
+    auto* surv_bits = sk.at<uint32_t>(o_sb);
+    auto* bb = sk.at<BestRec>(o_bb);
+    auto* best = sk.at<BestRec>(o_best);
+    auto* kskip = sk.at<uint8_t>(o_ks);
+    auto* kend_b = sk.at<uint8_t>(o_ke);
+    RP_CUDA(cudaMemsetAsync(sk.base, 0, zero_bytes, st));
+    launch(ctx, "seg1", k_seg1, dim3(nblk(q->n, 256)), dim3(256), 0, a, surv_bits, ctr,
+           sc_list, sc_count);
+    DevBuf<int> surv_idx(q->n + 1, st);
     launch(ctx, "compact", k_compact_small, dim3(1), dim3(1024), 0,
-           static_cast<const uint32_t*>(surv_bits.p), q->n, surv_idx.p, surv_cnt.p);
+           static_cast<const uint32_t*>(surv_bits), q->n, surv_idx.p, surv_cnt);
     const bool B1 = s->B == 1;
     const bool general = a.arm.any_limit || a.arm.has_offsets || (rp.cone_precheck && eight);
     static const bool flat = std::getenv("RP_SEG2_FLAT") != nullptr;
@@ -1212,20 +1233,21 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
     int S1 = 0;
     std::vector<int> surv_all(q->n);
     if (!sync_free)
-      copy_to_host_many(ctx, {{&S1, surv_cnt.p, sizeof(int)},
+      copy_to_host_many(ctx, {{&S1, surv_cnt, sizeof(int)},
                               {surv_all.data(), surv_idx.p, q->n * sizeof(int)}});
     const int cap_rows = sync_free ? q->n : S1;
     s->surv.alloc(cap_rows + 1, st);
     if (cap_rows > 0)
       launch(ctx, "seg1", k_surv_data, dim3(nblk(cap_rows, 128)), dim3(128), 0, a,
-             static_cast<const int*>(surv_idx.p), static_cast<const int*>(surv_cnt.p), s->surv.p);
+             static_cast<const int*>(surv_idx.p), static_cast<const int*>(surv_cnt), s->surv.p);
     // this part's survivor rows (the whole set for parts == 1); the pair and
     // key indices stay global, so parts' keys concatenate in canonical order
     int s_lo = static_cast<int>(static_cast<int64_t>(S1) * part / parts);
     int s_hi = static_cast<int>(static_cast<int64_t>(S1) * (part + 1) / parts);
     s->part = part;
     s->parts = parts;
-    if (part != 0) sc_count.zero();  // segment-1 hypotheses belong to part 0
+    if (part != 0)  // segment-1 hypotheses belong to part 0
+      RP_CUDA(cudaMemsetAsync(sc_count, 0, sizeof(unsigned), st));
 
     s->n_pairs = static_cast<int64_t>(cap_rows) * q->n;  // exact once S1 is known
     const int64_t nbits = s->n_pairs * s->B;
@@ -1237,35 +1259,30 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
     const int64_t p_lo = static_cast<int64_t>(s_lo) * q->n, p_hi = static_cast<int64_t>(s_hi) * q->n;
     const int64_t need = (p_hi - p_lo + threads - 1) / threads;
     if (!rows_kernel && need < blocks) blocks = static_cast<int>(std::max<int64_t>(1, need));
-    DevBuf<BestRec> bb(blocks, st), best(1, st);
     if (sync_free || p_hi > p_lo) {
       auto run = [&](auto kern) {
         launch(ctx, "seg2", kern, dim3(blocks), dim3(threads), 0, a,
-               static_cast<const SurvDev*>(s->surv.p), p_lo, p_hi, s->sol_bits.p, ctr.p,
-               sc_list.p, sc_count.p, bb.p);
+               static_cast<const SurvDev*>(s->surv.p), p_lo, p_hi, s->sol_bits.p, ctr,
+               sc_list, sc_count, bb);
       };
       if (rows_kernel) {
         s->sol_bits.zero();
         const int64_t units = static_cast<int64_t>(cap_rows) * ((q->n + 1023) / 1024);
         const int rblocks = static_cast<int>(
             std::max<int64_t>(1, std::min<int64_t>(ctx->sm_count * 8, (units + 7) / 8)));
-        DevBuf<int> unit_ctr(1, st);
-        unit_ctr.zero();
         // free leading samples per row (k_row_skip) and trailing samples of
         // the v3 walks (k_tail_skip) from the grid's cached clearance field
-        DevBuf<uint8_t> kskip(std::max(1, cap_rows), st);
         static const bool no_skip = std::getenv("RP_NO_ROW_SKIP") != nullptr;
-        DevBuf<uint8_t> kend_b(1, st);
         if (no_skip) {
-          kskip.zero();
-          RP_CUDA(cudaMemsetAsync(kend_b.p, rp.n_samples, 1, st));
+          RP_CUDA(cudaMemsetAsync(kskip, 0, std::max(1, cap_rows), st));
+          RP_CUDA(cudaMemsetAsync(kend_b, rp.n_samples, 1, st));
         } else {
           const ClearanceField cf = grid_clearance_field(g, ctx);
           launch(ctx, "seg2", k_row_skip, dim3(nblk(std::max(1, cap_rows), 128)), dim3(128), 0, a,
-                 static_cast<const SurvDev*>(s->surv.p), static_cast<const int*>(surv_cnt.p), cf,
-                 kskip.p);
+                 static_cast<const SurvDev*>(s->surv.p), static_cast<const int*>(surv_cnt), cf,
+                 kskip);
           launch(ctx, "seg2", k_tail_skip, dim3(1), dim3(32), 0, a.g,
-                 static_cast<const V3*>(a.bpts), 1, L3 + eps, rp.n_samples, cf, kend_b.p);
+                 static_cast<const V3*>(a.bpts), 1, L3 + eps, rp.n_samples, cf, kend_b);
         }
         uint32_t* c2bits = nullptr;
         uint8_t* c2ok = nullptr;
@@ -1277,10 +1294,10 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
           c2bits = nullptr, c2ok = nullptr;
         auto runr = [&](auto kern) {
           launch(ctx, "seg2", kern, dim3(rblocks), dim3(threads), 0, a,
-                 static_cast<const SurvDev*>(s->surv.p), static_cast<const int*>(surv_cnt.p), part,
-                 parts, s->sol_bits.p, ctr.p, sc_list.p,
-                 sc_count.p, bb.p, unit_ctr.p, static_cast<const uint8_t*>(kskip.p),
-                 static_cast<const uint8_t*>(kend_b.p), c2bits, c2ok, c2bits_r, c2ok_r, ov_lo,
+                 static_cast<const SurvDev*>(s->surv.p), static_cast<const int*>(surv_cnt), part,
+                 parts, s->sol_bits.p, ctr, sc_list,
+                 sc_count, bb, unit_ctr, static_cast<const uint8_t*>(kskip),
+                 static_cast<const uint8_t*>(kend_b), c2bits, c2ok, c2bits_r, c2ok_r, ov_lo,
                  ov_hi);
         };
         if (c2ok_r)
@@ -1296,7 +1313,7 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
         else B1 ? run(k_seg2<false, false, true>) : run(k_seg2<false, false, false>);
       }
       launch(ctx, "select", k_best_final, dim3(1), dim3(256), 0,
-             static_cast<const BestRec*>(bb.p), blocks, best.p);
+             static_cast<const BestRec*>(bb), blocks, best);
     }
     unsigned long long hc[C_COUNT];
     unsigned nsc = 0;
@@ -1305,17 +1322,17 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
       // the solve's one read-back: counters, shortcut count, best, S1 and
       // the survivor list
       // (the survivor list stays on the device until rp_solution_set_keys)
-      copy_to_host_many(ctx, {{hc, ctr.p, sizeof(hc)},
-                              {&nsc, sc_count.p, sizeof(unsigned)},
-                              {&hb, best.p, sizeof(BestRec)},
-                              {&S1, surv_cnt.p, sizeof(int)}});
+      copy_to_host_many(ctx, {{hc, ctr, sizeof(hc)},
+                              {&nsc, sc_count, sizeof(unsigned)},
+                              {&hb, best, sizeof(BestRec)},
+                              {&S1, surv_cnt, sizeof(int)}});
       s_lo = static_cast<int>(static_cast<int64_t>(S1) * part / parts);
       s_hi = static_cast<int>(static_cast<int64_t>(S1) * (part + 1) / parts);
       s->n_pairs = static_cast<int64_t>(S1) * q->n;
     } else {
-      copy_to_host_many(ctx, {{hc, ctr.p, sizeof(hc)},
-                              {&nsc, sc_count.p, sizeof(unsigned)},
-                              {&hb, best.p, p_hi > p_lo ? sizeof(BestRec) : 0}});
+      copy_to_host_many(ctx, {{hc, ctr, sizeof(hc)},
+                              {&nsc, sc_count, sizeof(unsigned)},
+                              {&hb, best, p_hi > p_lo ? sizeof(BestRec) : 0}});
     }
     s->S1 = S1;
     if (!sync_free) {
@@ -1346,10 +1363,10 @@ rp_solution_set* solve_reach(rp_ctx* ctx, const rp_arm& arm, const rp_quiver* q,
     if (nsc > 0) {
       DevBuf<long long> sorted(nsc, st);
       size_t tmp_bytes = 0;
-      cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, sc_list.p, sorted.p, static_cast<int>(nsc),
+      cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, sc_list, sorted.p, static_cast<int>(nsc),
                                      0, 64, st);
       DevBuf<unsigned char> tmp(tmp_bytes, st);
-      RP_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, sc_list.p, sorted.p,
+      RP_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, sc_list, sorted.p,
                                              static_cast<int>(nsc), 0, 64, st));
       DevBuf<ShortcutRec> recs(nsc, st);
       launch(ctx, "shortcuts", k_shortcuts, dim3(nblk(nsc, 128)), dim3(128), 0, a,
