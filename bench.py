@@ -304,7 +304,7 @@ def plan_bytes(summary) -> int:
 KERNEL_GROUPS = ["voxelize", "mark_dilate", "dilate", "overlay", "seg1", "walk1", "compact",
                  "seg2", "tail", "clear2", "select", "shortcuts", "walk4", "backward_pass", "wik_filter",
                  "wik_compact", "wik_pairs", "score", "rank", "materialize", "unfold",
-                 "pose_check", "refine", "trail", "cone", "finish", "clearance", "upload"]
+                 "pose_check", "refine", "trail", "cone", "finish", "clearance", "upload", "readback"]
 
 
 def run_ours(args, sc):

@@ -148,6 +148,23 @@ void copy_to_host(rp_ctx* ctx, void* dst, const void* src, size_t bytes) {
   RP_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
+namespace {
+constexpr int kGatherMax = 8;
+constexpr size_t kGatherBytes = 4096;
+struct GatherArgs {
+  const unsigned char* src[kGatherMax];
+  unsigned bytes[kGatherMax];
+  unsigned off[kGatherMax];
+  int n;
+};
+/// Small reads gathered by one kernel straight into the mapped pinned
+/// read-back buffer (one launch instead of one DMA call per read).
+__global__ void k_gather_to_host(GatherArgs a, unsigned char* __restrict__ dst) {
+  for (int e = 0; e < a.n; ++e)
+    for (unsigned k = threadIdx.x; k < a.bytes[e]; k += blockDim.x) dst[a.off[e] + k] = a.src[e][k];
+}
+}  // namespace
+
 void copy_to_host_many(rp_ctx* ctx, std::initializer_list<HostRead> reads) {
   size_t total = 0;
   for (const HostRead& r : reads) total += (r.bytes + 15) & ~size_t{15};
@@ -156,6 +173,28 @@ void copy_to_host_many(rp_ctx* ctx, std::initializer_list<HostRead> reads) {
     return;
   }
   if (!ctx->readback) RP_CUDA(cudaMallocHost(&ctx->readback, kReadbackBytes));
+  static const bool dma = std::getenv("RP_READBACK_DMA") != nullptr;
+  if (!dma && reads.size() > 1 && reads.size() <= static_cast<size_t>(kGatherMax) &&
+      total <= kGatherBytes) {
+    GatherArgs ga{};
+    size_t o = 0;
+    for (const HostRead& r : reads) {
+      ga.src[ga.n] = static_cast<const unsigned char*>(r.src);
+      ga.bytes[ga.n] = static_cast<unsigned>(r.bytes);
+      ga.off[ga.n] = static_cast<unsigned>(o);
+      ++ga.n;
+      o += (r.bytes + 15) & ~size_t{15};
+    }
+    launch(ctx, "readback", k_gather_to_host, dim3(1), dim3(256), 0, ga,
+           static_cast<unsigned char*>(ctx->readback));
+    RP_CUDA(cudaStreamSynchronize(ctx->stream));
+    o = 0;
+    for (const HostRead& r : reads) {
+      if (r.bytes) std::memcpy(r.dst, static_cast<char*>(ctx->readback) + o, r.bytes);
+      o += (r.bytes + 15) & ~size_t{15};
+    }
+    return;
+  }
   size_t off = 0;
   for (const HostRead& r : reads) {
     if (r.bytes)

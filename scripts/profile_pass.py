@@ -45,7 +45,7 @@ rcs = step()
 dt = time.perf_counter() - t0
 names = ["voxelize", "mark_dilate", "seg1", "walk1", "compact", "seg2", "select", "shortcuts",
          "walk4", "backward_pass", "wik_filter", "wik_compact", "wik_pairs", "score", "rank",
-         "materialize", "unfold", "pose_check", "refine", "trail", "cone", "clearance", "upload"]
+         "materialize", "unfold", "pose_check", "refine", "trail", "cone", "clearance", "upload", "readback"]
 tot = 0.0
 for n in names:
     ms, cnt = ctx.kernel_time(n)
