@@ -131,23 +131,6 @@ namespace {
 constexpr size_t kReadbackBytes = 256 << 10;
 }  // namespace
 
-/// Device -> host copy that completes before returning. Reads up to 256 KiB
-/// go through the context's pinned staging buffer (a true async DMA plus one
-/// synchronisation, cheaper than a pageable copy's staging path); larger
-/// ones copy straight to the destination.
-void copy_to_host(rp_ctx* ctx, void* dst, const void* src, size_t bytes) {
-  if (!bytes) return;
-  if (bytes <= kReadbackBytes) {
-    if (!ctx->readback) RP_CUDA(cudaMallocHost(&ctx->readback, kReadbackBytes));
-    RP_CUDA(cudaMemcpyAsync(ctx->readback, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
-    RP_CUDA(cudaStreamSynchronize(ctx->stream));
-    std::memcpy(dst, ctx->readback, bytes);
-    return;
-  }
-  RP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
-  RP_CUDA(cudaStreamSynchronize(ctx->stream));
-}
-
 namespace {
 constexpr int kGatherMax = 8;
 constexpr size_t kGatherBytes = 4096;
@@ -163,7 +146,44 @@ __global__ void k_gather_to_host(GatherArgs a, unsigned char* __restrict__ dst) 
   for (int e = 0; e < a.n; ++e)
     for (unsigned k = threadIdx.x; k < a.bytes[e]; k += blockDim.x) dst[a.off[e] + k] = a.src[e][k];
 }
+/// Device -> mapped pinned host copy, 16 bytes per thread.
+__global__ void k_copy_to_mapped(uint4* __restrict__ dst, const uint4* __restrict__ src, size_t n16) {
+  const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n16) dst[i] = src[i];
+}
 }  // namespace
+
+/// Device -> host copy that completes before returning. Reads up to 256 KiB
+/// land in the context's pinned read-back buffer, written there by a copy
+/// kernel through its mapping (a DMA call costs ~5-16 us of host time, a
+/// launch ~4; RP_READBACK_DMA=1 restores the DMA).
+void copy_to_host(rp_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  if (bytes <= kReadbackBytes) {
+    if (!ctx->readback) RP_CUDA(cudaMallocHost(&ctx->readback, kReadbackBytes));
+    static const bool dma = std::getenv("RP_READBACK_DMA") != nullptr;
+    const bool aligned = (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (bytes & 15) == 0;
+    if (!dma && aligned) {
+      const size_t n16 = bytes / 16;
+      launch(ctx, "readback", k_copy_to_mapped, dim3(static_cast<unsigned>((n16 + 255) / 256)),
+             dim3(256), 0, static_cast<uint4*>(ctx->readback), static_cast<const uint4*>(src), n16);
+    } else if (!dma && bytes <= kGatherBytes) {
+      GatherArgs ga{};
+      ga.src[0] = static_cast<const unsigned char*>(src);
+      ga.bytes[0] = static_cast<unsigned>(bytes);
+      ga.n = 1;
+      launch(ctx, "readback", k_gather_to_host, dim3(1), dim3(256), 0, ga,
+             static_cast<unsigned char*>(ctx->readback));
+    } else {
+      RP_CUDA(cudaMemcpyAsync(ctx->readback, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    RP_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(dst, ctx->readback, bytes);
+    return;
+  }
+  RP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  RP_CUDA(cudaStreamSynchronize(ctx->stream));
+}
 
 void copy_to_host_many(rp_ctx* ctx, std::initializer_list<HostRead> reads) {
   size_t total = 0;
