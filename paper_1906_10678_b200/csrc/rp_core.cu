@@ -290,16 +290,18 @@ void copy_to_device(rp_ctx* ctx, void* dst, const void* src, size_t bytes) {
   RP_CUDA(cudaEventRecord(ctx->upload_ev[k], ctx->stream));
 }
 
-unsigned char* ctx_scratch(rp_ctx* ctx, size_t bytes) {
-  if (bytes > ctx->scratch_bytes) {
-    if (ctx->scratch) RP_CUDA(cudaFreeAsync(ctx->scratch, ctx->stream));
-    const size_t want = std::max(bytes, ctx->scratch_bytes + ctx->scratch_bytes / 2);
-    ctx->scratch = nullptr;
-    ctx->scratch_bytes = 0;
-    RP_CUDA(cudaMallocAsync(&ctx->scratch, want, ctx->stream));
-    ctx->scratch_bytes = want;
+unsigned char* ctx_scratch(rp_ctx* ctx, size_t bytes, int slot) {
+  void*& p = ctx->scratch[slot];
+  size_t& have = ctx->scratch_bytes[slot];
+  if (bytes > have) {
+    if (p) RP_CUDA(cudaFreeAsync(p, ctx->stream));
+    const size_t want = std::max(bytes, have + have / 2);
+    p = nullptr;
+    have = 0;
+    RP_CUDA(cudaMallocAsync(&p, want, ctx->stream));
+    have = want;
   }
-  return static_cast<unsigned char*>(ctx->scratch);
+  return static_cast<unsigned char*>(p);
 }
 
 void copy_to_device_fill(rp_ctx* ctx, void* dst, size_t bytes,
@@ -617,7 +619,8 @@ rp_status rp_ctx_destroy(rp_ctx* ctx) {
     if (ctx->cancel_flag) cudaFree(ctx->cancel_flag);
     if (ctx->aux) cudaStreamDestroy(ctx->aux);
     if (ctx->aux_ev) cudaEventDestroy(ctx->aux_ev);
-    if (ctx->scratch) cudaFree(ctx->scratch);
+    for (void* p : ctx->scratch)
+      if (p) cudaFree(p);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;
   });

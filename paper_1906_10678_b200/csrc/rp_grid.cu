@@ -1487,8 +1487,19 @@ ClearanceField grid_clearance_field(const rp_grid* g, rp_ctx* caller) {
   cudaStream_t st = ctx->stream;
   if (g->cf_ready) RP_CUDA(cudaStreamWaitEvent(st, g->cf_ready, 0));  // readers of the old field
   if (!g->cf) RP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&g->cf), cells * sizeof(uint16_t), st));
-  DevBuf<uint8_t> occ(cells, st);
-  DevBuf<unsigned> work(cells, st), work2(cells, st);
+  // temporaries in the caller context's second scratch block (slot 0 may
+  // be carved by a solve_reach in progress)
+  ScratchCarver sk;
+  const size_t o_occ = sk.reserve<uint8_t>(cells);
+  const size_t o_w1 = sk.reserve<unsigned>(cells);
+  const size_t o_w2 = sk.reserve<unsigned>(cells);
+  sk.bind(ctx_scratch(ctx, sk.off, 1));
+  struct {
+    uint8_t* p;
+  } occ{sk.at<uint8_t>(o_occ)};
+  struct {
+    unsigned* p;
+  } work{sk.at<unsigned>(o_w1)}, work2{sk.at<unsigned>(o_w2)};
   launch(ctx, "clearance", k_cf_occ, dim3(blocks_for(static_cast<int64_t>(cells), 256)), dim3(256),
          0, g->view(), bk, f.ncx, f.ncy, f.ncz, occ.p);
   // window: distances saturate at W coarse cells (>= 0.6 m: beyond the

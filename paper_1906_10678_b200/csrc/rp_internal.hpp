@@ -122,8 +122,8 @@ struct rp_ctx {
   cudaEvent_t aux_ev = nullptr;  // "cancel flags cleared" on aux
   // solve_reach's temporaries (ctx_scratch): kept across solves, reused in
   // the context stream's order
-  void* scratch = nullptr;
-  size_t scratch_bytes = 0;
+  void* scratch[2] = {nullptr, nullptr};  // 0: solve_reach, 1: grid_clearance_field
+  size_t scratch_bytes[2] = {0, 0};
   // Pinned upload ring (copy_to_device): kUploadSlots slots of
   // kUploadSlotBytes; a slot is reused only after the event recorded behind
   // its last copy completed, so uploads never synchronise the stream.
@@ -354,7 +354,7 @@ inline void launch_pdl(rp_ctx* ctx, const char* name, void (*kernel)(KArgs...), 
 /// The context's scratch block of at least `bytes` (grown stream-ordered;
 /// the contents are undefined). For temporaries of one call on the
 /// context's stream: the next call's kernels run after this call's.
-unsigned char* ctx_scratch(rp_ctx* ctx, size_t bytes);
+unsigned char* ctx_scratch(rp_ctx* ctx, size_t bytes, int slot = 0);
 
 /// Lays typed arrays out in one block, 16-byte aligned: reserve() the
 /// sizes, bind() the block, then at() the arrays.
