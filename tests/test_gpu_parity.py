@@ -71,6 +71,27 @@ def test_general_dilate_matches_reference(ctx):
         assert np.array_equal(g.to_u8(), want), r
 
 
+def test_general_dilate_reach_limits(ctx):
+    """The separable transform at the edge of its byte range: R = 15 with
+    T = 225, 253 and 254 (the largest it takes), T = 255 (the per-word
+    kernel) and a 20-cell radius, on a ragged grid (x padded inside its
+    third word) with isolated cells near every face."""
+    api = _api()
+    rng = np.random.default_rng(11)
+    dims = (130, 37, 41)
+    occ = np.zeros(dims[::-1], np.uint8)
+    for _ in range(14):
+        occ[rng.integers(0, dims[2]), rng.integers(0, dims[1]), rng.integers(0, dims[0])] = 1
+    occ[0, 0, 0] = occ[-1, -1, -1] = occ[20, 0, 129] = occ[0, 36, 64] = 1
+    occ = occ.reshape(-1)
+    origin, vs = (-0.3, 0.1, -0.2), 0.02
+    for rc in (15.0, 253 ** 0.5, 254 ** 0.5, 255 ** 0.5, 20.0):
+        g = api.Grid.from_u8(ctx, origin, vs, dims, occ)
+        g.dilate(rc * vs)
+        want = ref.dilate_bytes(origin, vs, dims, occ, rc * vs)
+        assert np.array_equal(g.to_u8(), want), rc
+
+
 def test_mark_and_cloud(ctx):
     api = _api()
     rng = np.random.default_rng(3)
