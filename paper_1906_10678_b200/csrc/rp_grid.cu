@@ -1034,19 +1034,37 @@ __global__ void __launch_bounds__(256) k_sdil_y(const uint32_t* __restrict__ g1,
   const uint32_t pad = splat16(4096);
   for (int k = threadIdx.x; k <= last; k += blockDim.x)
     sadd[k] = k <= 2 * reach ? splat16((k - reach) * (k - reach)) : pad;
+  // rowany[h] bit r: staged row r holds a finite value in column half h
+  // (the 32 columns one warp computes); TY + 2R <= 64 rows
+  __shared__ unsigned long long rowany[2];
+  if (threadIdx.x < 2) rowany[threadIdx.x] = 0ull;
+  __syncthreads();
+  // rows * 64 is a whole number of warps, so every lane runs every trip
   for (int k = threadIdx.x; k < rows * 64; k += blockDim.x) {
     const int yy = y0 - reach + k / 64, qq = q0 + (k & 63);
     const uint32_t b = (yy >= 0 && yy < g.ny && qq < nqp)
                            ? __ldg(g1 + z * plane + static_cast<size_t>(yy) * nqp + qq)
                            : 0xFFFFFFFFu;
     sy[k] = bytes_to_u16(b);
+    const unsigned any = __ballot_sync(0xFFFFFFFFu, b != 0xFFFFFFFFu);
+    if ((threadIdx.x & 31) == 0 && any) atomicOr(&rowany[(k & 63) >> 5], 1ull << (k / 64));
   }
   __syncthreads();
   const int qq = threadIdx.x & 63;
   if (q0 + qq >= nqp) return;
   const uint32_t cap = splat16(255);
+  const unsigned long long mine = rowany[qq >> 5];
+  const unsigned long long wmask = (last + 1 >= 64) ? ~0ull : ((1ull << (last + 1)) - 1ull);
   for (int ly0 = (threadIdx.x >> 6) * RY; ly0 < TY; ly0 += 4 * RY) {
     if (y0 + ly0 >= g.ny) break;
+    if (!(mine & (wmask << ly0))) {  // the warp's whole window is saturated: 255s
+#pragma unroll
+      for (int j = 0; j < RY; ++j) {
+        const int y = y0 + ly0 + j;
+        if (y < g.ny) g2[z * plane + static_cast<size_t>(y) * nqp + q0 + qq] = 0xFFFFFFFFu;
+      }
+      continue;
+    }
     uint32_t lo[RY], hi[RY], a[RY];
 #pragma unroll
     for (int j = 0; j < RY; ++j) {
@@ -1102,9 +1120,15 @@ __global__ void __launch_bounds__(256) k_sdil_z(const uint32_t* __restrict__ g2,
     const int dz = k - (PZ - 1) - reach;
     sq[k] = (dz < -reach || dz > reach) ? pad : splat16(dz * dz);
   }
-  for (int zz = za - reach; zz < za + reach; ++zz)
-    ring[(zz - (za - reach)) * 256 + threadIdx.x] =
-        bytes_to_u16((live && zz >= 0 && zz < g.nz) ? __ldg(g2 + zz * gpl + q) : 0xFFFFFFFFu);
+  // slotany bit s: ring slot s holds a finite value in one of the warp's 32
+  // columns (warp-uniform, from ballots; W <= 64 slots)
+  unsigned long long slotany = 0ull;
+  for (int zz = za - reach; zz < za + reach; ++zz) {
+    const uint32_t b = (live && zz >= 0 && zz < g.nz) ? __ldg(g2 + zz * gpl + q) : 0xFFFFFFFFu;
+    const int slot = zz - (za - reach);
+    ring[slot * 256 + threadIdx.x] = bytes_to_u16(b);
+    if (__ballot_sync(0xFFFFFFFFu, b != 0xFFFFFFFFu)) slotany |= 1ull << slot;
+  }
   __syncthreads();  // sq
   const int lane = threadIdx.x & 31;
   const uint32_t init = splat16(0xFFFF);
@@ -1113,8 +1137,11 @@ __global__ void __launch_bounds__(256) k_sdil_z(const uint32_t* __restrict__ g2,
 #pragma unroll
     for (int d = 0; d < PZ; ++d) {  // the step's PZ newest planes
       const int zn = z + reach + d;
-      ring[((zn - (za - reach)) % W) * 256 + threadIdx.x] =
-          bytes_to_u16((live && zn < g.nz) ? __ldg(g2 + zn * gpl + q) : 0xFFFFFFFFu);
+      const uint32_t b = (live && zn < g.nz) ? __ldg(g2 + zn * gpl + q) : 0xFFFFFFFFu;
+      const int slot = (zn - (za - reach)) % W;
+      ring[slot * 256 + threadIdx.x] = bytes_to_u16(b);
+      if (__ballot_sync(0xFFFFFFFFu, b != 0xFFFFFFFFu)) slotany |= 1ull << slot;
+      else slotany &= ~(1ull << slot);
     }
     uint32_t lo[PZ], hi[PZ], a[PZ];
 #pragma unroll
@@ -1136,8 +1163,11 @@ __global__ void __launch_bounds__(256) k_sdil_z(const uint32_t* __restrict__ g2,
       for (int j = PZ - 1; j > 0; --j) a[j] = a[j - 1];
       a[0] = sq[PZ + k];
     };
-    for (int k = 0; k < W - s0; ++k) tap(*reinterpret_cast<const uint2*>(colx + (s0 + k) * 512), k);
-    for (int k = W - s0; k < W; ++k) tap(*reinterpret_cast<const uint2*>(colx + (k - (W - s0)) * 512), k);
+    // the ring holds exactly this step's window: all saturated -> no bits
+    if (slotany) {
+      for (int k = 0; k < W - s0; ++k) tap(*reinterpret_cast<const uint2*>(colx + (s0 + k) * 512), k);
+      for (int k = W - s0; k < W; ++k) tap(*reinterpret_cast<const uint2*>(colx + (k - (W - s0)) * 512), k);
+    }
     const uint32_t tt = static_cast<uint32_t>(T);
 #pragma unroll
     for (int j = 0; j < PZ; ++j) {
@@ -1164,8 +1194,10 @@ bool dilate_separable(rp_grid* g, double radius, int z0, int z1) {
   while (static_cast<double>(T + 1) <= r2) ++T;
   while (T >= 0 && !(static_cast<double>(T) <= r2)) --T;
   static const bool off = std::getenv("RP_DILATE_NAIVE") != nullptr;
-  // T <= 254 bounds R by 15 (the x pass's 32-bit windows need R <= 31)
-  if (off || T > 254 || reach > 31 || reach < 1) return false;
+  // T <= 254 bounds R by 15 (the x pass's 32-bit windows need R <= 31, the
+  // y pass's 64-bit row masks TY + 2R <= 64, the z pass's slot masks
+  // 2R + PZ <= 64)
+  if (off || T > 254 || reach > 15 || reach < 1) return false;
   cudaStream_t st = ctx->stream;
   const int64_t groups = static_cast<int64_t>(g->dims[2]) * g->dims[1] * g->wx * 16;
   DevBuf<uint32_t> g1(groups, st), g2(groups, st);
