@@ -1096,7 +1096,8 @@ __global__ void __launch_bounds__(256) k_sdil_y(const uint32_t* __restrict__ g1,
 
 /// z pass + threshold: thread per 4-voxel group of a plane, sliding along z
 /// over a chunk of ZC output planes, PZ at a time, with the 2R + PZ input
-/// planes around them in a shared-memory ring (u16x2 pairs): bit =
+/// planes around them in a shared-memory ring (raw bytes, widened to u16x2
+/// pairs at each tap): bit =
 /// [min over |dz| <= R of g2(z + dz) + dz^2 <= T] (a plane with dz^2 > T
 /// cannot pass). A half-warp holds the 16 groups of one output word (rows
 /// are padded to whole words) and ORs their nibbles by shuffles.
@@ -1105,7 +1106,7 @@ __global__ void __launch_bounds__(256) k_sdil_z(const uint32_t* __restrict__ g2,
                                                uint64_t* __restrict__ out, int reach, int T,
                                                int z_lo, int z_hi) {
   static_assert(ZC % PZ == 0, "whole steps per chunk");
-  extern __shared__ uint2 ring[];  // [2R + PZ][256]
+  extern __shared__ uint32_t ring[];  // [2R + PZ][256] raw bytes (widened at use: occupancy)
   // sq[PZ - 1 + k] = dz^2 for dz = k - R (k = 0..2R); the PZ - 1 pads on
   // either side are above any threshold
   __shared__ uint32_t sq[128 + 2 * PZ];
@@ -1126,20 +1127,20 @@ __global__ void __launch_bounds__(256) k_sdil_z(const uint32_t* __restrict__ g2,
   for (int zz = za - reach; zz < za + reach; ++zz) {
     const uint32_t b = (live && zz >= 0 && zz < g.nz) ? __ldg(g2 + zz * gpl + q) : 0xFFFFFFFFu;
     const int slot = zz - (za - reach);
-    ring[slot * 256 + threadIdx.x] = bytes_to_u16(b);
+    ring[slot * 256 + threadIdx.x] = b;
     if (__ballot_sync(0xFFFFFFFFu, b != 0xFFFFFFFFu)) slotany |= 1ull << slot;
   }
   __syncthreads();  // sq
   const int lane = threadIdx.x & 31;
   const uint32_t init = splat16(0xFFFF);
-  const uint32_t* colx = reinterpret_cast<const uint32_t*>(ring) + 2 * threadIdx.x;
+  const uint32_t* colx = ring + threadIdx.x;
   for (int z = za; z <= zb; z += PZ) {
 #pragma unroll
     for (int d = 0; d < PZ; ++d) {  // the step's PZ newest planes
       const int zn = z + reach + d;
       const uint32_t b = (live && zn < g.nz) ? __ldg(g2 + zn * gpl + q) : 0xFFFFFFFFu;
       const int slot = (zn - (za - reach)) % W;
-      ring[slot * 256 + threadIdx.x] = bytes_to_u16(b);
+      ring[slot * 256 + threadIdx.x] = b;
       if (__ballot_sync(0xFFFFFFFFu, b != 0xFFFFFFFFu)) slotany |= 1ull << slot;
       else slotany &= ~(1ull << slot);
     }
@@ -1165,8 +1166,8 @@ __global__ void __launch_bounds__(256) k_sdil_z(const uint32_t* __restrict__ g2,
     };
     // the ring holds exactly this step's window: all saturated -> no bits
     if (slotany) {
-      for (int k = 0; k < W - s0; ++k) tap(*reinterpret_cast<const uint2*>(colx + (s0 + k) * 512), k);
-      for (int k = W - s0; k < W; ++k) tap(*reinterpret_cast<const uint2*>(colx + (k - (W - s0)) * 512), k);
+      for (int k = 0; k < W - s0; ++k) tap(bytes_to_u16(colx[(s0 + k) * 256]), k);
+      for (int k = W - s0; k < W; ++k) tap(bytes_to_u16(colx[(k - (W - s0)) * 256]), k);
     }
     const uint32_t tt = static_cast<uint32_t>(T);
 #pragma unroll
@@ -1220,7 +1221,7 @@ bool dilate_separable(rp_grid* g, double radius, int z0, int z1) {
   // ZC output planes per thread (the 2R halo planes are re-read per chunk)
   constexpr int ZC = 32;
   constexpr int PZ = 4;
-  const size_t smz = static_cast<size_t>(2 * reach + PZ) * 256 * sizeof(uint2);
+  const size_t smz = static_cast<size_t>(2 * reach + PZ) * 256 * sizeof(uint32_t);
   const int64_t gpl = static_cast<int64_t>(g->dims[1]) * g->wx * 16;
   const dim3 grid(static_cast<unsigned>((gpl + 255) / 256), static_cast<unsigned>((z1 - z0 + ZC) / ZC));
   allow_smem(k_sdil_z<ZC, PZ>, smz);
