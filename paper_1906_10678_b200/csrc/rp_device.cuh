@@ -202,7 +202,8 @@ __device__ __forceinline__ uint32_t walk_hits(const GridView& g, V3 from, V3 to,
 /// reference's.
 template <int N>
 __device__ __forceinline__ uint32_t walk_hits_affine(const GridView& g, V3 from, V3 to, int n,
-                                                     double dqa, bool* exact, int kstart = 0) {
+                                                     double dqa, bool* exact, int kstart = 0,
+                                                     int kend = N) {
   const V3 diff = to - from;
   const double Ax = (from.x - g.ox) * g.rvs, Ay = (from.y - g.oy) * g.rvs, Az = (from.z - g.oz) * g.rvs;
   const double Bx = diff.x * g.rvs, By = diff.y * g.rvs, Bz = diff.z * g.rvs;
@@ -210,7 +211,7 @@ __device__ __forceinline__ uint32_t walk_hits_affine(const GridView& g, V3 from,
   uint32_t mask = 0;
 #pragma unroll
   for (int k = 0; k < N; ++k) {
-    if (k < kstart) continue;  // caller-proven free samples (warp-uniform)
+    if (k < kstart || k >= kend) continue;  // caller-proven free samples (warp-uniform)
     const bool live = k < n;
     const double t = c_tk.v[n][live ? k + 1 : n];
     const double qx = fma(t, Bx, Ax), qy = fma(t, By, Ay), qz = fma(t, Bz, Az);
@@ -235,6 +236,18 @@ __device__ __forceinline__ int walk_first_blocked_affine_from(const GridView& g,
   uint32_t m;
   if (n == 8) m = walk_hits_affine<8>(g, from, to, 8, dqa, &exact, kstart);
   else if (n <= kTkMax) m = walk_hits_affine<kTkMax>(g, from, to, n, dqa, &exact, kstart);
+  else return walk_first_blocked(g, from, to, n);
+  if (!exact) return walk_first_blocked(g, from, to, n);
+  return m ? __ffs(m) : 0;
+}
+
+/// walk_any_blocked_upto over walk_hits_affine (bracket dqa).
+__device__ __forceinline__ int walk_any_blocked_upto_affine(const GridView& g, V3 from, V3 to, int n,
+                                                            int kend, double dqa) {
+  bool exact = true;
+  uint32_t m;
+  if (n == 8) m = walk_hits_affine<8>(g, from, to, 8, dqa, &exact, 0, kend);
+  else if (n <= kTkMax) m = walk_hits_affine<kTkMax>(g, from, to, n, dqa, &exact, 0, kend);
   else return walk_first_blocked(g, from, to, n);
   if (!exact) return walk_first_blocked(g, from, to, n);
   return m ? __ffs(m) : 0;

@@ -1910,7 +1910,8 @@ __global__ void __launch_bounds__(256, 4) k_clear2(SolveDev a, const uint32_t* _
     if (j < a.Q && ((walk1_bits[i >> 5] >> (i & 31)) & 1u)) {
       const V3 p1 = a.arm.root + a.arm.L[0] * qvec(a, i);
       const V3 p2 = p1 + a.arm.L[1] * qvec(a, j);
-      clear = (kSeg2ParWalk ? rpd::walk_first_blocked_fast_seg(a.g, p1, p2, a.n) : rpd::walk_first_blocked(a.g, p1, p2, a.n)) == 0;
+      clear = (kSeg2ParWalk ? rpd::walk_first_blocked_affine_from(a.g, p1, p2, a.n, 0, a.dq_aff)
+                            : rpd::walk_first_blocked(a.g, p1, p2, a.n)) == 0;
     }
     const unsigned m = __ballot_sync(FULL, clear);
     if (lane == 0) clear2[wd] = m;
@@ -2349,7 +2350,7 @@ __global__ void __launch_bounds__(kTailBlock, 5) k_bq_tail(BatchDev d) {
     const V3 dir2 = qvec(a, j);
     const V3 p2 = p1 + L2 * dir2;
     const V3 v3 = b - p2;
-    if (rpd::walk_any_blocked_upto(a.g, p2, b, a.n, d.kend_b[t]) == 0) {
+    if (rpd::walk_any_blocked_upto_affine(a.g, p2, b, a.n, d.kend_b[t], a.dq_aff) == 0) {
       ++c_v3;
       if (!EIGHT || d.walk4_ok[t]) {
         const V3 s2 = L2 * dir2;
@@ -2662,6 +2663,7 @@ extern "C" rp_status rp_solve_reach_batch(rp_ctx* ctx, const rp_arm* arm, const 
     a.eps = eps;
     a.coarse2 = (L3 + eps) * (L3 + eps) * (1.0 + 1e-12);
     a.band_lo2 = L3 - eps > 0.0 ? (L3 - eps) * (L3 - eps) * (1.0 - 1e-9) : 0.0;
+    a.dq_aff = affine_bracket(a.g, *arm);
     double budget = arm->lengths[1] + arm->lengths[2] + eps;
     if (eight) budget += arm->lengths[3];
     budget += 1e-9;
