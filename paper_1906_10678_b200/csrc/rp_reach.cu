@@ -464,7 +464,9 @@ __global__ void __launch_bounds__(256, 5) k_seg2_rows(SolveDev a, const SurvDev*
       ++c_gp;
       if (v3_len < 1e-12) return;
       ++c_jp;
-      if (rpd::walk_first_blocked(a.g, p2, b, a.n, kend_bv) != 0) return;
+      // |b - p2| passed the gap band, so both ends lie within the arm's reach
+      // (the affine bracket's bound); samples past kend_bv are proven free
+      if (rpd::walk_any_blocked_upto_affine(a.g, p2, b, a.n, kend_bv, a.dq_aff) != 0) return;
       ++c_v3;
       if (EIGHT && !walk4) return;
       const V3 s2 = L2 * dir2;
