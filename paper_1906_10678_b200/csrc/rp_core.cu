@@ -630,7 +630,11 @@ rp_status rp_ctx_set_stream(rp_ctx* ctx, void* stream) {
   return guarded([&] {
     require(ctx != nullptr, RP_E_INVALID_PARAMETER, "null ctx");
     drain_timing(ctx);
-    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+    cudaStream_t next = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+    // the context's scratch blocks and upload slots are reused in stream
+    // order: let the old stream's work on them finish first
+    if (ctx->stream && ctx->stream != next) RP_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->stream = next;
   });
 }
 
