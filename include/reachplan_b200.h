@@ -519,6 +519,10 @@ rp_status rp_plan_relax(const rp_plan* p, double* relax, int32_t cap);
 /* which: 0 = poses (one per waypoint), 1 = unfold prefix */
 rp_status rp_plan_pose(const rp_plan* p, int32_t which, int32_t k, rp_pose* pose,
                        double* waypoints, int32_t cap_waypoints);
+/* rp_plan_pose for poses [first, first + count) in one call: pose k's
+   waypoint samples at waypoints + 3 * wps_per_pose * (k - first) */
+rp_status rp_plan_poses(const rp_plan* p, int32_t which, int32_t first, int32_t count,
+                        rp_pose* poses, double* waypoints, int32_t wps_per_pose);
 rp_status rp_plan_note(const rp_plan* p, int32_t k, char* buf, int32_t cap);
 /* Build a plan handle from host data (e.g. a plan file) for rp_replan_dynamic. */
 rp_status rp_plan_create(const char* kind, const double* waypoints, const rp_pose* poses,

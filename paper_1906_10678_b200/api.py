@@ -123,6 +123,8 @@ def lib():
         "rp_plan_waypoints": ([vp, d3, C.c_int32], C.c_int32),
         "rp_plan_relax": ([vp, d3, C.c_int32], C.c_int32),
         "rp_plan_pose": ([vp, C.c_int32, C.c_int32, P(abi.Pose), vp, C.c_int32], C.c_int32),
+        "rp_plan_poses": ([vp, C.c_int32, C.c_int32, C.c_int32, P(abi.Pose), vp, C.c_int32],
+                          C.c_int32),
         "rp_plan_note": ([vp, C.c_int32, C.c_char_p, C.c_int32], C.c_int32),
         "rp_plan_create": ([C.c_char_p, d3, P(abi.Pose), d3, C.c_int32, P(abi.Pose), C.c_int32,
                             P(vp)], C.c_int32),
@@ -491,11 +493,14 @@ class Plan:
         poses, unfold = [], []
         cap = 64 * self.n_samples
         for which, dst, cnt in ((0, poses, i.n_poses), (1, unfold, i.n_unfold)):
+            if not cnt:
+                continue
+            # all of them in one call (rp_plan_poses)
+            arr = (abi.Pose * cnt)()
+            buf = np.zeros((cnt, cap, 3))
+            _check(lib().rp_plan_poses(self.h, which, 0, cnt, arr, buf.ctypes.data, cap))
             for k in range(cnt):
-                p = abi.Pose()
-                buf = np.zeros((cap, 3))
-                _check(lib().rp_plan_pose(self.h, which, k, C.byref(p), buf.ctypes.data, cap))
-                dst.append((p, buf[:p.n_waypoints].copy()))
+                dst.append((arr[k], buf[k, :arr[k].n_waypoints].copy()))
         notes = []
         for k in range(i.n_notes):
             b = C.create_string_buffer(256)

@@ -1441,6 +1441,18 @@ rp_status rp_plan_pose(const rp_plan* p, int32_t which, int32_t k, rp_pose* pose
   });
 }
 
+rp_status rp_plan_poses(const rp_plan* p, int32_t which, int32_t first, int32_t count,
+                        rp_pose* poses, double* wps, int32_t wps_per_pose) {
+  return guarded([&] {
+    const auto& v = which == 0 ? p->poses : p->unfold;
+    require(first >= 0 && count >= 0 && first + count <= static_cast<int>(v.size()),
+            RP_E_INVALID_PARAMETER, "pose range out of range");
+    for (int32_t k = 0; k < count; ++k)
+      to_abi(v[first + k], poses + k, wps ? wps + 3 * static_cast<size_t>(wps_per_pose) * k : nullptr,
+             wps_per_pose);
+  });
+}
+
 rp_status rp_plan_note(const rp_plan* p, int32_t k, char* buf, int32_t cap) {
   return guarded([&] {
     require(k >= 0 && k < static_cast<int>(p->notes.size()) && cap > 0, RP_E_INVALID_PARAMETER,
